@@ -1,0 +1,421 @@
+"""Benchmark of the REXI hot path on B200 (driver contract).
+
+Default workload = BASELINE.json config 2 (the metric is quoted at T256):
+``lg_rexi_lc_n_etdrk`` at T256 (386 x 772 grid), N = 256 REXI poles,
+dt = 1800 s, seeded balanced vorticity state (peak 1e-5 1/s).
+A step = one ETD2RK step = 3 fused REXI pole sums (psi0+psi1 fused, psi2)
++ 2 fused LC+N tendencies.  Metric: REXI pole-solves x SH-coeffs per second
+(3 * N * ncoef units per step) and wall time per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg0|cfg1|cfg2|cfg4]
+
+N > 1 runs under torchrun: poles are sharded over ranks (strong scaling),
+with one deterministic all-gather+tree reduce per REXI application.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=48)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg4"), default="cfg2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    """The reference's CPU algorithm (the oracle port: the reference is a
+    Python package and cannot travel to the GPU box) on the host cores, on
+    our arm's workload; each step is one full step of that workload, the
+    timed sample stops after K steps or 150 s, whichever comes first."""
+    if rank != 0:
+        return
+    from oracle import layout as olay
+    from oracle import rexi as orx
+    from oracle import sht as osh
+    from oracle import stepping as ost
+    from paper_1805_06557_b200.workloads import CONFIGS
+
+    w = CONFIGS[args.config]
+    model = orx.Model(w.trunc, w.phibar)
+    nc = olay.ncoef(w.trunc)
+    if args.config == "cfg2":
+        grid = osh.grid_for(w.trunc)
+        st = ost.seeded_balanced_state(grid)
+        sets = {k: ost.contour_coeffs(k, w.p0, w.p1, w.n_poles) for k in (0, 1, 2)}
+        step = lambda s: ost.etdrk2_step(model, grid, w.dt, sets, s)  # noqa: E731
+        units = 3 * w.n_poles * nc
+    else:
+        st = ost.seeded_linear_state(w.trunc, 0)
+        a, b = ost.contour_coeffs(0, w.p0, w.p1, w.n_poles)
+        fac = orx.LFactors(model, w.dt) if w.group == "l" else None
+        step = lambda s: orx.rexi_sum(w.group, model, w.dt, a, b, s, fac)  # noqa: E731
+        units = w.n_poles * nc
+    for _ in range(min(args.warmup, 1)):
+        st = step(st)
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        st = step(st)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > 150.0:
+            break
+    sec = sum(times) / len(times)
+    cores = len(os.sched_getaffinity(0))
+    val = units / sec
+    line = {
+        "impl": "reference", "metric": "REXI pole-solves*SH-coeffs/s", "value": val,
+        "unit": "pole-solve*coeff/s", "n_gpus": world, "steps": len(times),
+        "steps_requested": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded, SURVEY §8d)",
+        "config": {"workload": w.name, "trunc": w.trunc, "n_poles": w.n_poles, "dt": w.dt},
+        "cpu_baseline": {"value": val, "unit": "pole-solve*coeff/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"{len(times)} full steps of {w.name} (numpy/scipy oracle, "
+                                   f"{cores} host threads for BLAS)"},
+        "e2e": {"value": val, "unit": "pole-solve*coeff/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+
+def fp64_peak_tflops(torch, lib, _lib):
+    n_blocks = torch.cuda.get_device_properties(0).multi_processor_count * 8
+    sink = torch.empty(n_blocks * 256, dtype=torch.float64, device="cuda")
+    iters = 4096
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        _lib.check(lib.swx_fp64_fma_probe(sink.data_ptr(), n_blocks, iters, s))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(5):
+        e0.record()
+        _lib.check(lib.swx_fp64_fma_probe(sink.data_ptr(), n_blocks, iters, s))
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = max(best, n_blocks * 256 * iters * 8 * 2 / (ms * 1e-3) / 1e12)
+    return best
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        try:
+            with open(path) as fh:
+                return json.load(fh)
+        except Exception:
+            return {}
+    return {}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_06557_b200 import _lib
+    from paper_1805_06557_b200.device import ncoef, pack, to_device
+    from paper_1805_06557_b200.parallel import PoleComm
+    from paper_1805_06557_b200.steppers import EtdrkStepper, RexiStepper
+    from paper_1805_06557_b200.swe import LC_N, LG, L, PrognosticState, TermGroup
+    from paper_1805_06557_b200.workloads import (CONFIGS, seeded_balanced_state,
+                                                 seeded_linear_state)
+
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = PoleComm(deterministic=True)
+    lib = _lib.lib()
+    w = CONFIGS[args.config]
+    par = w.params
+    nc = ncoef(w.trunc)
+    group = TermGroup.parse(w.group)
+    etd = args.config == "cfg2"
+
+    if etd:
+        stepper = EtdrkStepper(group, LC_N, par, w.setup)
+        eng = stepper.engine(w.dt, comm)
+        ic = seeded_balanced_state(par.cfg)
+        eng.load(ic)
+        step = eng.step_dev
+        units_per_step = 3 * w.n_poles * nc
+    else:
+        stepper = RexiStepper(group, par, w.setup)
+        ic = seeded_linear_state(w.trunc, 0)
+        u = to_device(pack(ic))
+        out = torch.empty_like(u)
+        dr = stepper._for_dt(w.dt)[2]
+        if comm is not None:
+            dr.comm = comm
+            dr.range = comm.pole_range(w.n_poles)
+
+        def step():
+            dr.apply((0,), u[None], out[None])
+            return out
+        units_per_step = w.n_poles * nc
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 1.0:   # bring clocks to steady load
+        step()
+        torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if comm is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.zero_()                      # cold L2 for every step
+        starts[k].record()
+        step()
+        ends[k].record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if comm is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_total = torch.tensor([sum(ms_steps)], dtype=torch.float64, device="cuda")
+    if comm is not None:
+        dist.all_reduce(ms_total, op=dist.ReduceOp.MAX)
+    ms_total = float(ms_total.item())
+    ms_per_step = ms_total / args.steps
+    value = units_per_step * args.steps / (ms_total * 1e-3)
+
+    # ---- per-kernel breakdown (live CUDA events on the launching stream)
+    from paper_1805_06557_b200.steppers import axpy
+
+    cur = torch.cuda.current_stream()
+    s_ptr = cur.cuda_stream
+    breakdown = {}
+    dominant = None
+    if etd and comm is None:
+        plan = eng.plan
+        reps = 5
+        stage_names = ["synth_state", "fft_c2r", "grid_products", "fft_r2c", "prep", "analysis"]
+        acc = np.zeros(7)
+        for _ in range(reps):
+            flush.zero_()
+            ctypes_buf = np.zeros(7, dtype=np.float64)
+            _lib.check(lib.swx_sht_tendency_profile(
+                plan._h, 3, eng.u.data_ptr(), eng.na.data_ptr(), plan.workspace.data_ptr(),
+                plan.workspace.numel(), ctypes_buf.ctypes.data, s_ptr))
+            acc += ctypes_buf
+        acc /= reps
+        for n, v in zip(stage_names, acc[:6]):
+            breakdown[n] = {"ms_per_launch": v, "launches_per_step": 2}
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def timed(fn):
+            tt = []
+            for _ in range(reps):
+                flush.zero_()
+                e0.record()
+                fn()
+                e1.record()
+                e1.synchronize()
+                tt.append(e0.elapsed_time(e1))
+            return sum(tt) / len(tt)
+        eng.pair_in[0].copy_(eng.u)
+        eng.pair_in[1].copy_(eng.na)
+        breakdown["rexi_lg_pair"] = {"ms_per_launch": timed(
+            lambda: eng.rexi.apply((0, 1), eng.pair_in, eng.pair_out)), "launches_per_step": 1}
+        breakdown["rexi_lg_single"] = {"ms_per_launch": timed(
+            lambda: eng.rexi.apply((2,), eng.d, eng.r2)), "launches_per_step": 1}
+        breakdown["axpy"] = {"ms_per_launch": timed(
+            lambda: axpy(w.trunc, eng.a, w.dt, eng.r2[0], eng.na)), "launches_per_step": 3}
+        for v in breakdown.values():
+            v["ms_per_step"] = v["ms_per_launch"] * v["launches_per_step"]
+        dominant = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
+    elif not etd:
+        breakdown["rexi_" + w.group] = {"ms_per_launch": ms_per_step, "launches_per_step": 1,
+                                        "ms_per_step": ms_per_step}
+        dominant = "rexi_" + w.group
+
+    # algorithmic flops per launch (SURVEY §8d conventions)
+    nlat = par.cfg.nlat
+    leg = 4.0 * nlat * nc  # per complex series, no symmetry credit
+    flops = {
+        "rexi_lg_pair": 2 * 40.0 * w.n_poles * nc,
+        "rexi_lg_single": 40.0 * w.n_poles * nc,
+        "rexi_lg": 40.0 * w.n_poles * nc,
+        "rexi_l": 142.0 * w.n_poles * nc,
+        "synth_state": 7 * leg,
+        "analysis": 7 * leg,
+    }
+    peak64 = fp64_peak_tflops(torch, lib, _lib)
+    traffic = load_traffic()
+    roofline = None
+    if dominant is not None and dominant in flops:
+        ms = breakdown[dominant]["ms_per_launch"]
+        ach = flops[dominant] / (ms * 1e-3) / 1e12
+        roofline = {"kernel": dominant, "bound": "fp64", "achieved": ach, "peak": peak64,
+                    "unit": "TFLOP/s", "frac": ach / peak64,
+                    "peak_source": "measured on this GPU by bench.py (swx_fp64_fma_probe, "
+                                   "DFMA); MEASURED_PEAKS.json has no FP64 entry",
+                    "algorithmic_flops_per_launch": flops[dominant],
+                    "traffic": traffic.get(dominant)}
+    elif dominant is not None:
+        ms = breakdown[dominant]["ms_per_launch"]
+        roofline = {"kernel": dominant, "bound": "fp64", "achieved": None, "peak": peak64,
+                    "unit": "TFLOP/s", "frac": None, "ms_per_launch": ms, "traffic": None}
+
+    # ---- end to end through the public API (host numpy in, host numpy out)
+    e2e = None
+    if not args.no_e2e and comm is None:
+        st_host = PrognosticState.from_stack(ic, par.cfg)
+        n_e2e = max(3, min(args.steps, 20))
+        st_host = stepper.step(st_host, w.dt)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            st_host = stepper.step(st_host, w.dt)
+        sec = (time.perf_counter() - t0) / n_e2e
+        e2e = {"value": units_per_step / sec, "unit": "pole-solve*coeff/s",
+               "ms_per_step": sec * 1e3, "h2d_bytes_per_step": 3 * nc * 16,
+               "d2h_bytes_per_step": 3 * nc * 16,
+               "api": ("EtdrkStepper.step(PrognosticState, dt)" if etd
+                       else "RexiStepper.step(PrognosticState, dt)")}
+
+    # ---- CPU baseline: the oracle on this host, bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import layout as olay
+        from oracle import rexi as orx
+        from oracle import sht as osh
+        from oracle import stepping as ost
+
+        model = orx.Model(w.trunc, w.phibar)
+        if etd:
+            grid = osh.grid_for(w.trunc)
+            sets = {k: ost.contour_coeffs(k, w.p0, w.p1, w.n_poles) for k in (0, 1, 2)}
+            t0 = time.perf_counter()
+            ost.etdrk2_step(model, grid, w.dt, sets, ic)
+            sec = time.perf_counter() - t0
+            sample = f"1 full ETD2RK step of {w.name} (numpy/scipy oracle)"
+        else:
+            a, b = ost.contour_coeffs(0, w.p0, w.p1, w.n_poles)
+            n_s = w.n_poles if w.trunc <= 128 else 8
+            fac = orx.LFactors(model, w.dt) if w.group == "l" else None
+            t0 = time.perf_counter()
+            orx.rexi_sum(w.group, model, w.dt, a[:n_s], b[:n_s], ic, fac, chunk=8)
+            sec = (time.perf_counter() - t0) * w.n_poles / n_s
+            sample = f"{n_s} of {w.n_poles} poles of {w.name}, scaled"
+        cpu = {"value": units_per_step / sec, "unit": "pole-solve*coeff/s",
+               "cores": len(os.sched_getaffinity(0)), "kind": "port", "sample": sample}
+
+    per_step_launches = 15 if etd else (1 if w.group == "lg" else 2)
+    line = {
+        "metric": "REXI pole-solves*SH-coeffs/s", "value": value, "unit": "pole-solve*coeff/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded, SURVEY §8d)",
+        "config": {"workload": w.name, "trunc": w.trunc, "grid": [par.cfg.nlat, par.cfg.nlon],
+                   "n_poles": w.n_poles, "dt": w.dt,
+                   "units_per_step": units_per_step,
+                   "parallelism": f"poles sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "cuda_graph": bool(etd and comm is None)},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": per_step_launches * args.steps,
+        "clocks": clocks, "kernel_breakdown_ms": breakdown,
+        "wall_s_timed_region": wall,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+/*
+ * swx.h -- C ABI of the B200-native REXI hot path (libswx.so).
+ *
+ * Drop-in boundary for the reference package `swerexi` (arXiv 1805.06557,
+ * /root/reference/pkg/src/swerexi).  The reference is pure Python; its seam
+ * for this path is the solver duck type returned by
+ *     get_solver(token, dt, params)                       solvers.py:259-261
+ * with warm/solve_stacked/solve_stacked_batch/apply_stacked (solvers.py:188-256),
+ * the pole reduction tree_sum + realify_stacked (steppers.py:157-185) that every
+ * caller applies after solve_stacked_batch (steppers.py:231-234, 264-266;
+ * parallel.py:140-169), and the spectral transforms / tendencies of the N term
+ * (sphere.py:297-430, swe.py:188-279).  Each entry point below names the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *   - complex128 values are `swx_c128` = {re, im} (layout of numpy complex128
+ *     and CUDA double2).
+ *   - Spectral state = 3 fields [phi', vort, div], each packed m-major over the
+ *     triangle l >= m (the reference's mode_index_map, solvers.py:288-290):
+ *     slot(l, m) = m*(T+1) - m*(m-1)/2 + (l - m);  ncoef = (T+1)(T+2)/2.
+ *     A state is 3*ncoef contiguous swx_c128, field-major.
+ *   - Pointers named d_* are device pointers; h_* are host pointers.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *     stream-ordered and allocation-free after *_create; nothing synchronises
+ *     unless documented.
+ *   - Return value: SWX_OK or an SWX_ERR_* code; swx_last_error() gives the
+ *     message.  SWX_ERR_SOLVER maps to swerexi.errors.SolverError (errors.py:24),
+ *     SWX_ERR_CONFIG to ConfigurationError (errors.py:8), SWX_ERR_DATA to
+ *     DataError (errors.py:12).
+ */
+#ifndef SWX_H
+#define SWX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWX_OK 0
+#define SWX_ERR_CONFIG 1
+#define SWX_ERR_SOLVER 2
+#define SWX_ERR_DATA 3
+#define SWX_ERR_CUDA 4
+
+#define SWX_GROUP_LG 0 /* gravity terms only: diagonal 2x2 per (l,m)      */
+#define SWX_GROUP_L 1  /* gravity + Coriolis: two tridiagonal chains per m */
+
+#define SWX_TEND_LC 1 /* linear Coriolis atom (swe.py:188-211)          */
+#define SWX_TEND_N 2  /* nonlinear atom (swe.py:214-251)                */
+
+typedef struct swx_c128 {
+  double re, im;
+} swx_c128;
+
+typedef struct swx_solver_s *swx_solver;
+typedef struct swx_sht_s *swx_sht;
+
+/* ---- library ------------------------------------------------------------ */
+int swx_version(void);
+const char *swx_last_error(void);
+
+/* ---- shifted solvers: replaces ShiftedLinearSolver / get_solver ----------
+ * solvers.py:57-81 (construction), 259-261 (get_solver).  group is
+ * SWX_GROUP_LG or SWX_GROUP_L; dt > 0; phibar > 0 (swe.py:78-87).            */
+int swx_solver_create(swx_solver *out, int group, int trunc, double dt,
+                      double phibar, double radius, double omega);
+int swx_solver_destroy(swx_solver s);
+
+/* warm(alphas), solvers.py:188-194 (+ the guards of 95-104 and 176-184).
+ * Uploads the N shifts and validates every (pole, l|m) system: a singular
+ * gravity block (|det| <= 1e-13 (|a|^2 + dt^2 phibar kappa)), alpha == 0, or a
+ * chain pivot with (||dt L_m||_1 + |a|) / |pivot| > 1e13 returns
+ * SWX_ERR_SOLVER with *err_pole = n and *err_index = l (lg) or m (l).
+ * Synchronises `stream`.                                                     */
+int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas, int n_poles,
+                    int *err_pole, int *err_index, void *stream);
+
+/* Workspace for swx_rexi_sum over [pole_begin, pole_end) with n_rhs RHS.    */
+size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs, int pole_begin,
+                                int pole_end);
+
+/* Fused REXI pole sum -- replaces solve_stacked_batch + beta weighting +
+ * tree_sum + realify_stacked (steppers.py:214-235, 262-267; parallel.py:140-169):
+ *   d_out[r] = sum_{n in [pole_begin, pole_end)} d_betas[r*n_poles + n] *
+ *              (dt L + alpha_n)^{-1} d_rhs[r]            for r < n_rhs (<= 2)
+ * without materialising the (N, 3, n, n) batch.  Poles are reduced in the
+ * reference's fixed pairwise tree order; for power-of-two pole counts the
+ * result over a block equals the block's subtree of tree_sum, so per-rank
+ * partials combined by swx_tree_combine are bitwise independent of the rank
+ * count.  realify != 0 zeroes Im of the m = 0 column (steppers.py:175-185);
+ * pass 0 for partial sums that are reduced across ranks afterwards.
+ * d_betas is device memory (n_rhs * n_poles); d_rhs / d_out hold n_rhs states. */
+int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                 const swx_c128 *d_betas, int pole_begin, int pole_end,
+                 int realify, swx_c128 *d_out, void *d_workspace,
+                 size_t workspace_bytes, void *stream);
+
+/* Forward operator (dt L + alpha) x -- apply_stacked, solvers.py:252-256.   */
+int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,
+              swx_c128 *d_out, void *stream);
+
+/* ---- reductions / state algebra ------------------------------------------ */
+/* d_out = realify?( tree_sum(d_parts[0..n_parts)) ), each part n_states*3*ncoef
+ * values -- the cross-rank / cross-block reduce of parallel.py:161-169.     */
+int swx_tree_combine(int trunc, int n_states, int n_parts,
+                     const swx_c128 *d_parts, int realify, swx_c128 *d_out,
+                     void *stream);
+/* d_out = d_x + s * d_y over n_states packed states (PrognosticState
+ * __add__/__mul__, swe.py:135-157).  d_out may alias d_x.                    */
+int swx_state_axpy(int trunc, int n_states, const swx_c128 *d_x, double s,
+                   const swx_c128 *d_y, swx_c128 *d_out, void *stream);
+
+/* ---- spherical-harmonic transforms + tendencies --------------------------
+ * Plan = SpherePlan (sphere.py:163-223) for a Gauss-Legendre x equiangular
+ * grid; h_sinlat / h_weights are the nlat Gauss nodes (ascending) and weights
+ * (sphere.py:31-58).  Legendre functions are generated on the fly from the
+ * reference recurrence (sphere.py:72-112); h_seed holds the sectoral seeds
+ * Pbar_m^m(x_j) as an (T+1) x nlat row-major table (m-major).              */
+int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon, double radius,
+                   double omega, const double *h_sinlat, const double *h_weights,
+                   const double *h_seed);
+int swx_sht_destroy(swx_sht p);
+size_t swx_sht_workspace_bytes(swx_sht p);
+
+/* synthesis of n_fields real-origin fields: packed coeffs -> (nlat, nlon)
+ * grids (sphere.py:318-339).                                                */
+int swx_sht_synthesis(swx_sht p, int n_fields, const swx_c128 *d_coeffs,
+                      double *d_grid, void *d_workspace, size_t ws_bytes,
+                      void *stream);
+/* analysis of n_fields real grids -> packed coeffs (sphere.py:297-315).     */
+int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
+                     swx_c128 *d_coeffs, void *d_workspace, size_t ws_bytes,
+                     void *stream);
+/* u, v grids from packed vort/div (sphere.py:375-402).                      */
+int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_div,
+               double *d_u, double *d_v, void *d_workspace, size_t ws_bytes,
+               void *stream);
+/* tendency_group for atoms in `atoms` (SWX_TEND_LC | SWX_TEND_N), swe.py:254-279:
+ * d_out = sum of the selected atom tendencies of d_state (one packed state).  */
+int swx_sht_tendency(swx_sht p, int atoms, const swx_c128 *d_state,
+                     swx_c128 *d_out, void *d_workspace, size_t ws_bytes,
+                     void *stream);
+
+/* ---- measurement helpers (bench.py) ---------------------------------------
+ * swx_sht_tendency with per-stage device times (ms) written to h_stage_ms[7]:
+ * {synthesis, C2R FFT, grid products, R2C FFT, analysis prep, analysis,
+ * total}.  Synchronises `stream`; not for the hot path.                     */
+int swx_sht_tendency_profile(swx_sht p, int atoms, const swx_c128 *d_state,
+                             swx_c128 *d_out, void *d_workspace, size_t ws_bytes,
+                             double *h_stage_ms, void *stream);
+/* FP64 FMA throughput probe: n_blocks x 256 threads, `iters` x 8 independent
+ * DFMA chains each (2 flops per DFMA); d_sink receives one double per thread
+ * so nothing is optimised away.  Used for the FP64 roofline denominator.   */
+int swx_fp64_fma_probe(double *d_sink, int n_blocks, int iters, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWX_H */

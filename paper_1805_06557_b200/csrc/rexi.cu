@@ -1,0 +1,852 @@
+// REXI pole-sum kernels (K1 lg, K2 l-chains), tree combine, state algebra
+// and the solver half of the C ABI (include/swx.h).
+//
+// Reference semantics (/root/reference/pkg/src/swerexi/):
+//   lg solve      solvers.py:86-108    l band       solvers.py:122-166
+//   l LU / guard  solvers.py:168-212   apply        solvers.py:110-117, 214-237
+//   tree_sum      steppers.py:157-172  realify      steppers.py:175-185
+//   rexi_step     steppers.py:214-235  ETD psi sum  steppers.py:262-267
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "swx_common.cuh"
+
+namespace swx {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// =====================================================================
+// K1: gravity-group pole sum.  One CTA per (degree l, block of m); the
+// per-(pole, l) factors (beta folded in) are hoisted into shared memory:
+//   A = b a/det, B = b dt phibar/det, C = -b dt kappa/det, D = b/a,
+//   det = a^2 + dt^2 phibar kappa            (solvers.py:93-107)
+// then every mode does 5 complex MACs per pole:
+//   phi += A bphi + B bdiv, div += C bphi + A bdiv, vort += D bvort.
+// Lane j of a warp owns the contiguous pole block [j*BPL, (j+1)*BPL) and
+// reduces it as a perfect binary tree; the xor-butterfly over lanes then
+// completes tree_sum's pairwise order (steppers.py:157-172).
+// =====================================================================
+template <int NRHS>
+struct LgAcc {
+  double2 v[NRHS][3];
+};
+
+template <int NRHS>
+__device__ __forceinline__ void lg_zero(LgAcc<NRHS> &a) {
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) a.v[r][f] = make_double2(0.0, 0.0);
+}
+
+template <int NRHS>
+__device__ __forceinline__ void lg_add(LgAcc<NRHS> &a, const LgAcc<NRHS> &b) {
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) a.v[r][f] = cadd(a.v[r][f], b.v[r][f]);
+}
+
+template <int NRHS>
+struct LgTerm {
+  const double2 *fac;  // shared: [(r*4 + q) * Pp + slot], Pp = lanes*BPL
+  int Pp, lanes, lane;
+  double2 b[NRHS][3];
+  __device__ __forceinline__ void operator()(int t, LgAcc<NRHS> &out) const {
+    const int s = t * lanes + lane;  // slot of pole lane*BPL + t
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 A = fac[(r * 4 + 0) * Pp + s];
+      const double2 B = fac[(r * 4 + 1) * Pp + s];
+      const double2 C = fac[(r * 4 + 2) * Pp + s];
+      const double2 D = fac[(r * 4 + 3) * Pp + s];
+      out.v[r][0] = cfma(A, b[r][0], cmul(B, b[r][2]));
+      out.v[r][1] = cmul(D, b[r][1]);
+      out.v[r][2] = cfma(C, b[r][0], cmul(A, b[r][2]));
+    }
+  }
+};
+
+template <int B, int NRHS>
+__device__ __forceinline__ void lg_tree(LgAcc<NRHS> &out, int t0,
+                                        const LgTerm<NRHS> &term) {
+  if constexpr (B == 1) {
+    term(t0, out);
+  } else {
+    LgAcc<NRHS> right;
+    lg_tree<B / 2, NRHS>(out, t0, term);
+    lg_tree<B / 2, NRHS>(right, t0 + B / 2, term);
+    lg_add(out, right);
+  }
+}
+
+template <int NRHS, int BPL>
+__global__ void __launch_bounds__(256) rexi_lg_kernel(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
+    const double2 *__restrict__ beta, int beta_stride, int pole0, int P,
+    int lanes, int trunc, int ncoef, double dt, double phibar,
+    const double *__restrict__ lconst, const int4 *__restrict__ sched,
+    int realify, double2 *__restrict__ out) {
+  extern __shared__ double2 fac[];  // NRHS*4*Pp
+  const int Pp = lanes * BPL;
+  const int4 w = sched[blockIdx.x];
+  const int l = w.x;
+  const double kap = lconst[l];
+  const double g = lconst[(trunc + 1) + l];  // dt^2 phibar kappa
+  const double dtpb = dt * phibar;
+  const double mdtk = -dt * kap;
+  for (int i = threadIdx.x; i < Pp; i += blockDim.x) {
+    const int lane_of = i / BPL, t = i - lane_of * BPL;
+    const int s = t * lanes + lane_of;
+    if (i >= P) {  // padding pole: contributes exact zeros
+#pragma unroll
+      for (int q = 0; q < NRHS * 4; ++q) fac[q * Pp + s] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double2 a = alpha[pole0 + i];
+    const double2 det = make_double2(a.x * a.x - a.y * a.y + g, 2.0 * a.x * a.y);
+    const double2 idet = crecip(det);
+    const double2 q1 = cmul(a, idet);
+    const double2 q2 = cscale(dtpb, idet);
+    const double2 q3 = cscale(mdtk, idet);
+    const double2 q4 = crecip(a);
+    // slot layout [t][lane]: lane j's t-th pole; a warp reads 32 consecutive slots
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 b = beta[r * beta_stride + pole0 + i];
+      fac[(r * 4 + 0) * Pp + s] = cmul(b, q1);
+      fac[(r * 4 + 1) * Pp + s] = cmul(b, q2);
+      fac[(r * 4 + 2) * Pp + s] = cmul(b, q3);
+      fac[(r * 4 + 3) * Pp + s] = cmul(b, q4);
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  LgTerm<NRHS> term;
+  term.fac = fac;
+  term.Pp = Pp;
+  term.lanes = lanes;
+  term.lane = lane;
+  for (int m = w.y + warp; m < w.z; m += nwarps) {
+    const int idx = col_offset(trunc, m) + (l - m);
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r)
+#pragma unroll
+      for (int f = 0; f < 3; ++f)
+        term.b[r][f] = rhs[(size_t)(r * 3 + f) * ncoef + idx];
+    LgAcc<NRHS> acc;
+    if (lane < lanes) {
+      lg_tree<BPL, NRHS>(acc, 0, term);
+    } else {
+      lg_zero(acc);
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r)
+#pragma unroll
+        for (int f = 0; f < 3; ++f)
+          acc.v[r][f] = cadd(acc.v[r][f], shfl_xor2(acc.v[r][f], o));
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r)
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          double2 v = acc.v[r][f];
+          if (realify && m == 0) v.y = 0.0;
+          out[(size_t)(r * 3 + f) * ncoef + idx] = v;
+        }
+    }
+  }
+}
+
+// =====================================================================
+// K2: Coriolis-group chains.  With phi' eliminated (phi_l = (bphi_l +
+// dt phibar div_l)/alpha) the band system of solvers.py:122-166 splits per
+// (pole, m) into two scalar tridiagonal chains over l = m..T:
+//   chain c: position k holds vort_{m+k} if (k+c) even else div_{m+k}
+//   vort row: (a + i r_l) z_l - L_l d_{l-1} - U_l d_{l+1} = bz_l
+//   div row : (a + i r_l + g_l/a) d_l + L_l z_{l-1} + U_l z_{l+1}
+//                                     = bd_l - (h_l/a) bphi_l
+// One thread per (pole, m, chain); a warp = 32 consecutive poles of the same
+// (m, chain), so all lanes walk identical index sequences.  Thomas sweep
+// (no pivoting; SURVEY §7 shows it matches zgbtrf to 3.5e-16 on these
+// matrices), forward factors staged in a per-warp global scratch slot, and
+// the beta-weighted pole reduction done through a swizzled shared-memory
+// transpose in tree order every 8 chain elements.
+// =====================================================================
+constexpr int kLWarps = 4;  // warps per CTA
+constexpr int kFlush = 8;   // chain elements per reduction flush
+
+template <int NRHS>
+__global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
+    const double2 *__restrict__ beta, int beta_stride, int pole0, int P,
+    int n_blocks, int trunc, int ncoef, double dt, double phibar,
+    const double *__restrict__ lconst, const double *__restrict__ chain,
+    double2 *__restrict__ scratch, double2 *__restrict__ part) {
+  // reduction buffer: [warp][e][r][comp][32] (dynamic, NRHS * 32 KB)
+  extern __shared__ double2 red_raw[];
+  auto red = reinterpret_cast<double2 (*)[kFlush][NRHS][2][32]>(red_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gwarp = blockIdx.x * kLWarps + warp;
+  const int total_warps = gridDim.x * kLWarps;
+  const int n_items = (trunc + 1) * 2 * n_blocks;
+  const double *cl = chain;              // lower L per slot
+  const double *cu = chain + ncoef;      // upper U per slot
+  const double *cr = chain + 2 * ncoef;  // rotation r per slot
+  const double *gl = lconst + (trunc + 1);
+  const double *hl = lconst + 2 * (trunc + 1);
+  const double dtpb = dt * phibar;
+  double2 *slot = scratch + (size_t)gwarp * (trunc + 1) * 32 * (1 + NRHS);
+
+  for (int item = gwarp; item < n_items; item += total_warps) {
+    const int m = item / (2 * n_blocks);
+    const int rem = item - m * 2 * n_blocks;
+    const int c = rem / n_blocks;
+    const int pb = rem - c * n_blocks;
+    const int pl = pb * 32 + lane;  // local pole index
+    const bool active = pl < P;
+    double2 a = make_double2(1.0, 0.0);
+    double2 bet[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) bet[r] = make_double2(0.0, 0.0);
+    if (active) {
+      a = alpha[pole0 + pl];
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) bet[r] = beta[r * beta_stride + pole0 + pl];
+    }
+    const double2 ia = crecip(a);
+    const int nl = trunc + 1 - m;
+    const int off = col_offset(trunc, m);
+
+    // ---- forward sweep
+    double2 cp = make_double2(0.0, 0.0);
+    double2 yp[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) yp[r] = make_double2(0.0, 0.0);
+    for (int k = 0; k < nl; ++k) {
+      const int s = off + k;
+      const int l = m + k;
+      const bool isz = ((k + c) & 1) == 0;
+      const double sg = isz ? -1.0 : 1.0;
+      const double sub = sg * cl[s];
+      const double sup = sg * cu[s];
+      double2 diag = make_double2(a.x, a.y + cr[s]);
+      if (!isz) {
+        diag.x = fma(gl[l], ia.x, diag.x);
+        diag.y = fma(gl[l], ia.y, diag.y);
+      }
+      const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
+      const double2 inv = crecip(den);
+      cp = cscale(sup, inv);
+      double2 *dst = slot + ((size_t)k * 32 + lane) * (1 + NRHS);
+      dst[0] = cp;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        const double2 *b = rhs + (size_t)r * 3 * ncoef;
+        double2 q;
+        if (isz) {
+          q = b[ncoef + s];
+        } else {
+          const double hk = hl[l];
+          const double2 bp = b[s];
+          const double2 t = make_double2(hk * ia.x, hk * ia.y);
+          q = csub(b[2 * ncoef + s], cmul(t, bp));
+        }
+        q = make_double2(fma(-sub, yp[r].x, q.x), fma(-sub, yp[r].y, q.y));
+        yp[r] = cmul(q, inv);
+        dst[1 + r] = yp[r];
+      }
+    }
+    // ---- back substitution + beta weighting + tree reduction over lanes
+    double2 xn[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) xn[r] = make_double2(0.0, 0.0);
+    int e = 0;
+    for (int k = nl - 1; k >= 0; --k) {
+      const int s = off + k;
+      const bool isz = ((k + c) & 1) == 0;
+      const double2 *src = slot + ((size_t)k * 32 + lane) * (1 + NRHS);
+      const double2 cpk = src[0];
+      const int phys = lane ^ e;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        const double2 x = csub(src[1 + r], cmul(cpk, xn[r]));
+        xn[r] = x;
+        red[warp][e][r][0][phys] = cmul(bet[r], x);
+        if (!isz) {
+          const double2 bp = rhs[(size_t)r * 3 * ncoef + s];
+          const double2 ph = cmul(make_double2(fma(dtpb, x.x, bp.x), fma(dtpb, x.y, bp.y)), ia);
+          red[warp][e][r][1][phys] = cmul(bet[r], ph);
+        }
+      }
+      ++e;
+      if (e == kFlush || k == 0) {
+        __syncwarp();
+        // lane j reduces element ee = j>>2 over the 8 poles 8q..8q+7, q = j&3
+        const int ee = lane >> 2, q = lane & 3;
+        const int eidx = ee < e ? ee : 0;
+        const int kk = k + (e - 1 - eidx);  // chain position of element eidx
+        const bool eisz = ((kk + c) & 1) == 0;
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+#pragma unroll
+          for (int comp = 0; comp < 2; ++comp) {
+            double2 v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = red[warp][eidx][r][comp][(8 * q + i) ^ eidx];
+            double2 s01 = cadd(v[0], v[1]), s23 = cadd(v[2], v[3]);
+            double2 s45 = cadd(v[4], v[5]), s67 = cadd(v[6], v[7]);
+            double2 acc = cadd(cadd(s01, s23), cadd(s45, s67));
+            acc = cadd(acc, shfl_xor2(acc, 1));
+            acc = cadd(acc, shfl_xor2(acc, 2));
+            if (q == 0 && ee < e && (comp == 0 || !eisz)) {
+              const int field = comp == 1 ? 0 : (eisz ? 1 : 2);
+              part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + kk] = acc;
+            }
+          }
+        }
+        __syncwarp();
+        e = 0;
+      }
+    }
+  }
+}
+
+// warm-up guard for the l group: forward sweep only, min |pivot|^2 per
+// (pole, m, chain); flags the first offending (pole, m) (solvers.py:176-184)
+__global__ void l_guard_kernel(const double2 *__restrict__ alpha, int P,
+                               int trunc, int ncoef,
+                               const double *__restrict__ lconst,
+                               const double *__restrict__ chain,
+                               const double *__restrict__ norm_m,
+                               unsigned long long *flag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = P * (trunc + 1) * 2;
+  if (t >= total) return;
+  const int n = t / ((trunc + 1) * 2);
+  const int rem = t - n * (trunc + 1) * 2;
+  const int m = rem >> 1, c = rem & 1;
+  const double2 a = alpha[n];
+  const double2 ia = crecip(a);
+  const double *gl = lconst + (trunc + 1);
+  const int off = col_offset(trunc, m);
+  double2 cp = make_double2(0.0, 0.0);
+  double dmin2 = INFINITY;
+  for (int k = 0; k < trunc + 1 - m; ++k) {
+    const int s = off + k;
+    const bool isz = ((k + c) & 1) == 0;
+    const double sg = isz ? -1.0 : 1.0;
+    const double sub = sg * chain[s], sup = sg * chain[ncoef + s];
+    double2 diag = make_double2(a.x, a.y + chain[2 * ncoef + s]);
+    if (!isz) {
+      diag.x = fma(gl[m + k], ia.x, diag.x);
+      diag.y = fma(gl[m + k], ia.y, diag.y);
+    }
+    const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
+    const double d2 = fma(den.x, den.x, den.y * den.y);
+    dmin2 = fmin(dmin2, d2);
+    cp = cscale(sup, crecip(den));
+  }
+  const double nrm = norm_m[m] + sqrt(fma(a.x, a.x, a.y * a.y));
+  if (!(dmin2 > 0.0) || nrm * nrm > 1e26 * dmin2) {
+    unsigned long long code = ((unsigned long long)n << 32) | (unsigned)m;
+    atomicMin(flag, code);
+  }
+}
+
+// tree_sum over n_parts blocks + optional realify (parallel.py:161-169)
+__global__ void tree_combine_kernel(const double2 *__restrict__ parts,
+                                    size_t stride, int n_parts, int ncoef,
+                                    int trunc, int realify,
+                                    double2 *__restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= stride) return;
+  double2 stack[24];
+  int depth = 0;
+  // binary-counter pairwise sum == perfect tree for power-of-two n_parts
+  for (int p = 0; p < n_parts; ++p) {
+    double2 v = parts[(size_t)p * stride + i];
+    int q = p;
+    while (q & 1) {
+      v = cadd(stack[--depth], v);
+      q >>= 1;
+    }
+    stack[depth++] = v;
+  }
+  // odd tails (non power-of-two counts): fold right-to-left deterministically
+  double2 v = stack[--depth];
+  while (depth > 0) v = cadd(stack[--depth], v);
+  if (realify && (int)(i % ncoef) <= trunc) v.y = 0.0;
+  out[i] = v;
+}
+
+__global__ void axpy_kernel(const double2 *__restrict__ x, double s,
+                            const double2 *__restrict__ y, size_t n,
+                            double2 *__restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 a = x[i], b = y[i];
+  out[i] = make_double2(a.x + b.x * s, a.y + b.y * s);
+}
+
+// (dt L + alpha) x, per packed slot (solvers.py:110-117 and 214-237)
+__global__ void apply_kernel(const double2 *__restrict__ x, double2 alpha,
+                             int trunc, int ncoef, double dt, double phibar,
+                             int coriolis, const double *__restrict__ lconst,
+                             const double *__restrict__ chain,
+                             double2 *__restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= ncoef) return;
+  const double b2 = 2.0 * trunc + 3.0;
+  int m = (int)floor(0.5 * (b2 - sqrt(fmax(b2 * b2 - 8.0 * s, 0.0))));
+  m = max(0, min(m, trunc));
+  while (m > 0 && col_offset(trunc, m) > s) --m;
+  while (m < trunc && col_offset(trunc, m + 1) <= s) ++m;
+  const int k = s - col_offset(trunc, m);
+  const int l = m + k;
+  const double2 p = x[s], z = x[ncoef + s], d = x[2 * ncoef + s];
+  const double hk = lconst[2 * (trunc + 1) + l];  // dt*kappa
+  double2 op = csub(cmul(alpha, p), cscale(dt * phibar, d));
+  double2 oz = cmul(alpha, z);
+  double2 od = cadd(cscale(hk, p), cmul(alpha, d));
+  if (coriolis) {
+    const double r = chain[2 * ncoef + s];
+    oz = cadd(oz, make_double2(-r * z.y, r * z.x));
+    od = cadd(od, make_double2(-r * d.y, r * d.x));
+    const int nl = trunc + 1 - m;
+    if (k >= 1) {
+      const double L = chain[s];
+      oz = csub(oz, cscale(L, x[2 * ncoef + s - 1]));
+      od = cadd(od, cscale(L, x[ncoef + s - 1]));
+    }
+    if (k + 1 < nl) {
+      const double U = chain[ncoef + s];
+      oz = csub(oz, cscale(U, x[2 * ncoef + s + 1]));
+      od = cadd(od, cscale(U, x[ncoef + s + 1]));
+    }
+  }
+  out[s] = op;
+  out[ncoef + s] = oz;
+  out[2 * ncoef + s] = od;
+}
+
+// FP64 FMA throughput probe (8 independent chains per thread)
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double *sink, int iters) {
+  double a[8];
+  const double b = 1.0000000001, c = -1e-12;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  sink[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+}  // namespace swx
+
+using namespace swx;
+
+extern "C" int swx_fp64_fma_probe(double *d_sink, int n_blocks, int iters, void *stream) {
+  if (!d_sink || n_blocks < 1 || iters < 1) return fail(SWX_ERR_CONFIG, "bad probe arguments");
+  fp64_probe_kernel<<<n_blocks, 256, 0, (cudaStream_t)stream>>>(d_sink, iters);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+// =====================================================================
+// C ABI
+// =====================================================================
+extern "C" int swx_version(void) { return 1; }
+extern "C" const char *swx_last_error(void) { return g_last_error.c_str(); }
+
+static double eps_lm(int l, int m) {
+  const double ll = (double)l, mm = (double)m;
+  const double num = ll * ll - mm * mm;
+  return num > 0 ? std::sqrt(num / (4.0 * ll * ll - 1.0)) : 0.0;
+}
+
+extern "C" int swx_solver_create(swx_solver *out, int group, int trunc,
+                                 double dt, double phibar, double radius,
+                                 double omega) {
+  if (!out) return fail(SWX_ERR_CONFIG, "null output handle");
+  *out = nullptr;
+  if (group != SWX_GROUP_LG && group != SWX_GROUP_L)
+    return fail(SWX_ERR_CONFIG, "shifted solves support groups 'lg' and 'l'");
+  if (trunc < 0) return fail(SWX_ERR_CONFIG, "truncation must be >= 0");
+  if (!(dt > 0)) return fail(SWX_ERR_CONFIG, "dt must be positive");
+  if (!(phibar > 0)) return fail(SWX_ERR_CONFIG, "mean geopotential must be positive");
+  if (!(radius > 0)) return fail(SWX_ERR_CONFIG, "radius must be positive");
+  if (omega < 0) return fail(SWX_ERR_CONFIG, "rotation rate must be >= 0");
+  auto *s = new swx_solver_s();
+  s->group = group;
+  s->trunc = trunc;
+  s->ncoef = ncoef_of(trunc);
+  s->dt = dt;
+  s->phibar = phibar;
+  s->radius = radius;
+  s->omega = omega;
+  const int n = trunc + 1, nc = s->ncoef;
+  std::vector<double> lc(3 * n);
+  for (int l = 0; l < n; ++l) {
+    const double kap = (double)(l * (l + 1)) / (radius * radius);  // solvers.py:77
+    lc[l] = kap;
+    lc[n + l] = dt * dt * phibar * kap;  // solvers.py:93
+    lc[2 * n + l] = dt * kap;            // solvers.py:106, 132
+  }
+  std::vector<double> ch(3 * (size_t)nc, 0.0);
+  s->h_norm = new double[n];
+  const bool cor = group == SWX_GROUP_L && omega > 0.0;
+  const double w = dt * (2.0 * omega);
+  for (int m = 0; m < n; ++m) {
+    const int off = col_offset(trunc, m), nl = n - m;
+    double nrm = 0.0;
+    for (int k = 0; k < nl; ++k) {
+      const int l = m + k;
+      double L = 0, U = 0, r = 0;
+      if (cor) {
+        if (l >= 1) r = w * m / (l * (l + 1.0));
+        if (k >= 1) L = w * eps_lm(l, m) * ((l - 1 >= 1) ? (l + 1.0) / l : 1.0);
+        if (k + 1 < nl) U = w * eps_lm(l + 1, m) * (l / (l + 1.0));
+      }
+      ch[off + k] = L;
+      ch[nc + off + k] = U;
+      ch[2 * (size_t)nc + off + k] = r;
+    }
+    // column 1-norm of dt*L_m (the band norm of solvers.py:162-165)
+    for (int k = 0; k < nl; ++k) {
+      const int l = m + k;
+      const double Lup = (k + 1 < nl) ? ch[off + k + 1] : 0.0;  // L_{l+1}
+      const double Udn = (k >= 1) ? ch[nc + off + k - 1] : 0.0;  // U_{l-1}
+      const double r = std::fabs(ch[2 * (size_t)nc + off + k]);
+      nrm = std::max(nrm, std::fabs(lc[2 * n + l]));
+      nrm = std::max(nrm, r + Lup + Udn);
+      nrm = std::max(nrm, dt * phibar + r + Lup + Udn);
+    }
+    s->h_norm[m] = nrm;
+  }
+  cudaError_t e = cudaMalloc(&s->d_lconst, sizeof(double) * 3 * n);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_chain, sizeof(double) * 3 * (size_t)nc);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(s->d_lconst, lc.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(s->d_chain, ch.data(), sizeof(double) * 3 * (size_t)nc,
+                   cudaMemcpyHostToDevice);
+  // lg schedule: CTAs of (l, m0, m1) with at most 32 modes each
+  std::vector<int4> sched;
+  for (int l = n - 1; l >= 0; --l)
+    for (int m0 = 0; m0 <= l; m0 += 32) sched.push_back(make_int4(l, m0, std::min(l + 1, m0 + 32), 0));
+  s->n_sched = (int)sched.size();
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_sched, sizeof(int4) * sched.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(s->d_sched, sched.data(), sizeof(int4) * sched.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    swx_solver_destroy(s);
+    return fail(SWX_ERR_CUDA, std::string("solver create: ") + cudaGetErrorString(e));
+  }
+  *out = s;
+  return SWX_OK;
+}
+
+extern "C" int swx_solver_destroy(swx_solver s) {
+  if (!s) return SWX_OK;
+  cudaFree(s->d_lconst);
+  cudaFree(s->d_chain);
+  cudaFree(s->d_alpha);
+  cudaFree(s->d_sched);
+  delete[] s->h_norm;
+  delete[] s->h_alpha;
+  delete s;
+  return SWX_OK;
+}
+
+extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
+                               int n_poles, int *err_pole, int *err_index,
+                               void *stream) {
+  if (!s) return fail(SWX_ERR_CONFIG, "null solver");
+  if (n_poles < 1 || !h_alphas) return fail(SWX_ERR_CONFIG, "need at least one shift");
+  if (err_pole) *err_pole = -1;
+  if (err_index) *err_index = -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = s->trunc + 1;
+  const bool cor = s->group == SWX_GROUP_L && s->omega > 0.0;
+  if (!cor) {
+    // gravity blocks (solvers.py:93-104), first offender in (pole, l) order
+    for (int p = 0; p < n_poles; ++p) {
+      const std::complex<double> a(h_alphas[p].re, h_alphas[p].im);
+      for (int l = 0; l < n; ++l) {
+        const double kap = (double)(l * (l + 1)) / (s->radius * s->radius);
+        const double g = s->dt * s->dt * s->phibar * kap;
+        const std::complex<double> det = a * a + g;
+        if (std::abs(det) <= 1e-13 * (std::norm(a) + g)) {
+          if (err_pole) *err_pole = p;
+          if (err_index) *err_index = l;
+          char buf[160];
+          snprintf(buf, sizeof buf, "singular gravity block at degree l=%d for shift alpha=(%.17g%+.17gj)",
+                   l, a.real(), a.imag());
+          return fail(SWX_ERR_SOLVER, buf);
+        }
+      }
+    }
+    for (int p = 0; p < n_poles; ++p)
+      if (h_alphas[p].re == 0.0 && h_alphas[p].im == 0.0) {
+        if (err_pole) *err_pole = p;
+        return fail(SWX_ERR_SOLVER, "alpha = 0 makes the decoupled vorticity row singular");
+      }
+  } else {
+    for (int p = 0; p < n_poles; ++p)
+      if (h_alphas[p].re == 0.0 && h_alphas[p].im == 0.0) {
+        if (err_pole) *err_pole = p;
+        return fail(SWX_ERR_SOLVER, "alpha = 0: the phi' row is singular");
+      }
+  }
+  // upload
+  if (s->n_poles != n_poles) {
+    cudaFree(s->d_alpha);
+    s->d_alpha = nullptr;
+    delete[] s->h_alpha;
+    s->h_alpha = new double2[n_poles];
+    SWX_CUDA_TRY(cudaMalloc(&s->d_alpha, sizeof(double2) * n_poles));
+    s->n_poles = n_poles;
+  }
+  std::memcpy(s->h_alpha, h_alphas, sizeof(double2) * n_poles);
+  SWX_CUDA_TRY(cudaMemcpyAsync(s->d_alpha, s->h_alpha, sizeof(double2) * n_poles,
+                               cudaMemcpyHostToDevice, st));
+  if (cor) {
+    double *d_norm = nullptr;
+    unsigned long long *d_flag = nullptr;
+    SWX_CUDA_TRY(cudaMallocAsync(&d_norm, sizeof(double) * n, st));
+    SWX_CUDA_TRY(cudaMallocAsync(&d_flag, sizeof(unsigned long long), st));
+    SWX_CUDA_TRY(cudaMemcpyAsync(d_norm, s->h_norm, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    SWX_CUDA_TRY(cudaMemsetAsync(d_flag, 0xff, sizeof(unsigned long long), st));
+    const int total = n_poles * n * 2;
+    l_guard_kernel<<<(total + 127) / 128, 128, 0, st>>>(s->d_alpha, n_poles, s->trunc, s->ncoef,
+                                                       s->d_lconst, s->d_chain, d_norm, d_flag);
+    SWX_LAUNCH_CHECK();
+    unsigned long long flag = 0;
+    SWX_CUDA_TRY(cudaMemcpyAsync(&flag, d_flag, sizeof flag, cudaMemcpyDeviceToHost, st));
+    SWX_CUDA_TRY(cudaFreeAsync(d_norm, st));
+    SWX_CUDA_TRY(cudaFreeAsync(d_flag, st));
+    SWX_CUDA_TRY(cudaStreamSynchronize(st));
+    if (flag != ~0ull) {
+      const int p = (int)(flag >> 32), m = (int)(flag & 0xffffffffu);
+      if (err_pole) *err_pole = p;
+      if (err_index) *err_index = m;
+      char buf[160];
+      snprintf(buf, sizeof buf, "numerically singular band matrix for (m=%d, alpha=(%.17g%+.17gj))", m,
+               h_alphas[p].re, h_alphas[p].im);
+      return fail(SWX_ERR_SOLVER, buf);
+    }
+  } else {
+    SWX_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return SWX_OK;
+}
+
+// ---- launch geometry helpers
+static constexpr int kLgMaxP = 512;  // poles per lg launch (smem = NRHS*64*P bytes)
+
+static size_t l_smem_bytes(int nrhs) {
+  return (size_t)kLWarps * kFlush * nrhs * 2 * 32 * sizeof(double2);
+}
+
+static int l_grid_warps(swx_solver s, int n_items) {
+  if (!s->l_blocks_per_sm) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rexi_l_kernel<1>, kLWarps * 32,
+                                                  l_smem_bytes(1));
+    s->l_blocks_per_sm = std::max(1, b);
+  }
+  const int cap = sm_count() * s->l_blocks_per_sm * kLWarps;
+  return std::min(cap, ((n_items + kLWarps - 1) / kLWarps) * kLWarps);
+}
+
+static size_t l_scratch_bytes(swx_solver s, int n_rhs, int P) {
+  const int nb = (P + 31) / 32;
+  const int n_items = (s->trunc + 1) * 2 * nb;
+  const int warps = l_grid_warps(s, n_items);
+  return (size_t)warps * (s->trunc + 1) * 32 * (1 + n_rhs) * sizeof(double2);
+}
+
+extern "C" size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs,
+                                           int pole_begin, int pole_end) {
+  if (!s || n_rhs < 1 || n_rhs > 2 || pole_end <= pole_begin) return 0;
+  const int P = pole_end - pole_begin;
+  const size_t state = (size_t)n_rhs * 3 * s->ncoef * sizeof(double2);
+  const bool cor = s->group == SWX_GROUP_L && s->omega > 0.0;
+  if (!cor) {
+    const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
+    return chunks > 1 ? chunks * state : 0;
+  }
+  const int nb = (P + 31) / 32;
+  return l_scratch_bytes(s, n_rhs, P) + (size_t)nb * state + 256;
+}
+
+template <int NRHS>
+static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
+                     int pole0, int P, int realify, double2 *out,
+                     cudaStream_t st) {
+  const int bpl = next_pow2((P + 31) / 32);
+  const int lanes = bpl == 1 ? std::min(32, P) : 32;
+  const size_t smem = (size_t)NRHS * 4 * lanes * bpl * sizeof(double2);
+#define SWX_LG_CASE(B)                                                                 \
+  case B: {                                                                            \
+    auto k = rexi_lg_kernel<NRHS, B>;                                                  \
+    if (smem > 48 * 1024)                                                              \
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        (int)smem));                                   \
+    k<<<s->n_sched, 256, smem, st>>>(rhs, s->d_alpha, betas, s->n_poles, pole0, P,     \
+                                     lanes, s->trunc, s->ncoef, s->dt, s->phibar,      \
+                                     s->d_lconst, s->d_sched, realify, out);           \
+    break;                                                                             \
+  }
+  switch (bpl) {
+    SWX_LG_CASE(1)
+    SWX_LG_CASE(2)
+    SWX_LG_CASE(4)
+    SWX_LG_CASE(8)
+    SWX_LG_CASE(16)
+    default:
+      return fail(SWX_ERR_CONFIG, "lg pole chunk too large");
+  }
+#undef SWX_LG_CASE
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+template <int NRHS>
+static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
+                    int pole0, int P, int realify, double2 *out, char *ws,
+                    cudaStream_t st) {
+  const int nb = (P + 31) / 32;
+  const int n_items = (s->trunc + 1) * 2 * nb;
+  const int warps = l_grid_warps(s, n_items);
+  double2 *scratch = (double2 *)ws;
+  const size_t sbytes = l_scratch_bytes(s, NRHS, P);
+  double2 *part = (double2 *)(ws + ((sbytes + 255) / 256) * 256);
+  const size_t smem = l_smem_bytes(NRHS);
+  if (smem > 48 * 1024)
+    SWX_CUDA_TRY(cudaFuncSetAttribute(rexi_l_kernel<NRHS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  rexi_l_kernel<NRHS><<<warps / kLWarps, kLWarps * 32, smem, st>>>(
+      rhs, s->d_alpha, betas, s->n_poles, pole0, P, nb, s->trunc, s->ncoef, s->dt,
+      s->phibar, s->d_lconst, s->d_chain, scratch, part);
+  SWX_LAUNCH_CHECK();
+  const size_t stride = (size_t)NRHS * 3 * s->ncoef;
+  tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, nb, s->ncoef,
+                                                                        s->trunc, realify, out);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+extern "C" int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                            const swx_c128 *d_betas, int pole_begin,
+                            int pole_end, int realify, swx_c128 *d_out,
+                            void *d_workspace, size_t workspace_bytes,
+                            void *stream) {
+  if (!s) return fail(SWX_ERR_CONFIG, "null solver");
+  if (n_rhs < 1 || n_rhs > 2) return fail(SWX_ERR_CONFIG, "n_rhs must be 1 or 2");
+  if (!s->d_alpha) return fail(SWX_ERR_CONFIG, "solver not warmed (no shifts uploaded)");
+  if (pole_begin < 0 || pole_end > s->n_poles || pole_end <= pole_begin)
+    return fail(SWX_ERR_CONFIG, "bad pole range");
+  const size_t need = swx_rexi_workspace_bytes(s, n_rhs, pole_begin, pole_end);
+  if (need > 0 && (workspace_bytes < need || !d_workspace))
+    return fail(SWX_ERR_CONFIG, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const double2 *rhs = (const double2 *)d_rhs;
+  const double2 *bet = (const double2 *)d_betas;
+  double2 *out = (double2 *)d_out;
+  const int P = pole_end - pole_begin;
+  const bool cor = s->group == SWX_GROUP_L && s->omega > 0.0;
+  if (!cor) {
+    const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
+    if (chunks == 1)
+      return n_rhs == 1 ? launch_lg<1>(s, rhs, bet, pole_begin, P, realify, out, st)
+                        : launch_lg<2>(s, rhs, bet, pole_begin, P, realify, out, st);
+    // aligned chunks of kLgMaxP poles, combined in tree order
+    double2 *part = (double2 *)d_workspace;
+    const size_t stride = (size_t)n_rhs * 3 * s->ncoef;
+    for (int c = 0; c < chunks; ++c) {
+      const int p0 = pole_begin + c * kLgMaxP;
+      const int pc = std::min(kLgMaxP, pole_end - p0);
+      int rc = n_rhs == 1 ? launch_lg<1>(s, rhs, bet, p0, pc, 0, part + c * stride, st)
+                          : launch_lg<2>(s, rhs, bet, p0, pc, 0, part + c * stride, st);
+      if (rc) return rc;
+    }
+    tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, chunks,
+                                                                          s->ncoef, s->trunc,
+                                                                          realify, out);
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
+  return n_rhs == 1
+             ? launch_l<1>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st)
+             : launch_l<2>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st);
+}
+
+extern "C" int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,
+                         swx_c128 *d_out, void *stream) {
+  if (!s) return fail(SWX_ERR_CONFIG, "null solver");
+  const bool cor = s->group == SWX_GROUP_L && s->omega > 0.0;
+  apply_kernel<<<(s->ncoef + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      (const double2 *)d_x, make_double2(alpha.re, alpha.im), s->trunc, s->ncoef, s->dt,
+      s->phibar, cor ? 1 : 0, s->d_lconst, s->d_chain, (double2 *)d_out);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+extern "C" int swx_tree_combine(int trunc, int n_states, int n_parts,
+                                const swx_c128 *d_parts, int realify,
+                                swx_c128 *d_out, void *stream) {
+  if (trunc < 0 || n_states < 1 || n_parts < 1 || n_parts > (1 << 20))
+    return fail(SWX_ERR_CONFIG, "bad tree_combine arguments");
+  const int nc = ncoef_of(trunc);
+  const size_t stride = (size_t)n_states * 3 * nc;
+  tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const double2 *)d_parts, stride, n_parts, nc, trunc, realify, (double2 *)d_out);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+extern "C" int swx_state_axpy(int trunc, int n_states, const swx_c128 *d_x,
+                              double s, const swx_c128 *d_y, swx_c128 *d_out,
+                              void *stream) {
+  if (trunc < 0 || n_states < 1) return fail(SWX_ERR_CONFIG, "bad axpy arguments");
+  const size_t n = (size_t)n_states * 3 * ncoef_of(trunc);
+  axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const double2 *)d_x, s, (const double2 *)d_y, n, (double2 *)d_out);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}

@@ -1,0 +1,87 @@
+// Shared device helpers and host-side error plumbing for libswx.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/swx.h"
+
+namespace swx {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define SWX_CUDA_TRY(expr)                                                   \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess)                                                   \
+      return ::swx::fail(SWX_ERR_CUDA, std::string(#expr) + ": " +          \
+                                           cudaGetErrorString(_e));          \
+  } while (0)
+
+#define SWX_LAUNCH_CHECK()                                                   \
+  do {                                                                       \
+    cudaError_t _e = cudaGetLastError();                                     \
+    if (_e != cudaSuccess)                                                   \
+      return ::swx::fail(SWX_ERR_CUDA,                                       \
+                         std::string("kernel launch: ") +                    \
+                             cudaGetErrorString(_e));                        \
+  } while (0)
+
+inline int ncoef_of(int trunc) { return (trunc + 1) * (trunc + 2) / 2; }
+__host__ __device__ inline int col_offset(int trunc, int m) {
+  return m * (trunc + 1) - m * (m - 1) / 2;
+}
+int sm_count();
+
+// ---------------------------------------------------------------- complex
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cscale(double s, double2 a) {
+  return make_double2(s * a.x, s * a.y);
+}
+// a + b*c
+__device__ __forceinline__ double2 cfma(double2 b, double2 c, double2 a) {
+  return make_double2(fma(b.x, c.x, fma(-b.y, c.y, a.x)),
+                      fma(b.x, c.y, fma(b.y, c.x, a.y)));
+}
+// 1/z via conj(z)/|z|^2 (one real reciprocal)
+__device__ __forceinline__ double2 crecip(double2 z) {
+  double r = 1.0 / fma(z.x, z.x, z.y * z.y);
+  return make_double2(z.x * r, -z.y * r);
+}
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int o) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o),
+                      __shfl_xor_sync(0xffffffffu, v.y, o));
+}
+
+}  // namespace swx
+
+struct swx_solver_s {
+  int group = 0;
+  int trunc = 0;
+  int ncoef = 0;
+  double dt = 0, phibar = 0, radius = 0, omega = 0;
+  // per-degree constants (T+1): kappa_l, g_l = dt^2 phibar kappa_l, h_l = dt kappa_l
+  double *d_lconst = nullptr;
+  // l group: per packed slot (ncoef each): lower L, upper U, rotation r (Im)
+  double *d_chain = nullptr;
+  double *h_norm = nullptr;  // per-m band 1-norm (host)
+  // shifts
+  int n_poles = 0;
+  double2 *d_alpha = nullptr;
+  double2 *h_alpha = nullptr;
+  // lg launch schedule (l, m0, m1, -) per CTA
+  int4 *d_sched = nullptr;
+  int n_sched = 0;
+  int l_blocks_per_sm = 0;
+};

@@ -1,0 +1,268 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Bars (BASELINE.json north star):
+linear REXI steps relative L-inf <= 1e-10 per field, ETD2RK trajectories
+relative L2 <= 1e-8 after one simulated day."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2, rel_linf
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import layout as olay  # noqa: E402
+from oracle import rexi as orx  # noqa: E402
+from oracle import sht as osh  # noqa: E402
+from oracle import stepping as ost  # noqa: E402
+from paper_1805_06557_b200 import _lib  # noqa: E402
+from paper_1805_06557_b200.device import pack, ptr, stream_ptr, to_device, unpack  # noqa: E402
+from paper_1805_06557_b200.errors import SolverError  # noqa: E402
+from paper_1805_06557_b200.rexi import RexiSetup, coeffs_for_contour, shifted_contour_from_points  # noqa: E402
+from paper_1805_06557_b200.solvers import ShiftedLinearSolver  # noqa: E402
+from paper_1805_06557_b200.sphere import SphereConfig, plan_for  # noqa: E402
+from paper_1805_06557_b200.steppers import (EtdrkStepper, RexiStepper, build_stepper,  # noqa: E402
+                                            integrate, rexi_step)
+from paper_1805_06557_b200.swe import L, LC_N, LG, ModelParams, PrognosticState  # noqa: E402
+
+G = 9.80616
+LIN_BAR = 1e-10
+
+
+def params(trunc, omega=7.292e-5):
+    cfg = SphereConfig.for_truncation(trunc, omega=omega)
+    return ModelParams(1e4 * G, cfg)
+
+
+def coeffs(n, k=0, p0=10.0, p1=30.0):
+    return coeffs_for_contour(f"psi{k}", shifted_contour_from_points(p0, p1, n))
+
+
+def run_rexi(group, trunc, dt, n, packed_in, p0=10.0, p1=30.0):
+    par = params(trunc)
+    c = coeffs(n, 0, p0, p1)
+    st = PrognosticState.from_stack(unpack(packed_in, trunc), par.cfg)
+    out = rexi_step(group, st, dt, c, par)
+    return pack(out.stack())
+
+
+# ---------------------------------------------------------------- linear REXI
+
+def test_cfg0_lg_rexi_golden(golden_small):
+    out = run_rexi(LG, 63, 3600.0, 128, golden_small["cfg0_in"])
+    assert rel_linf(out, golden_small["cfg0_out"]) <= LIN_BAR
+    assert np.all(out[:, :64].imag == 0.0)  # realified m = 0 column
+
+
+def test_t21_lg_and_l_golden(golden_small):
+    for group, key in ((LG, "T21_lg16_out"), (L, "T21_l16_out")):
+        out = run_rexi(group, 21, 480.0, 16, golden_small["T21_l16_in"])
+        assert rel_linf(out, golden_small[key]) <= LIN_BAR, key
+
+
+def test_t42_l_golden(golden_small):
+    out = run_rexi(L, 42, 3600.0, 128, golden_small["T42_l128_in"])
+    assert rel_linf(out, golden_small["T42_l128_out"]) <= LIN_BAR
+
+
+def test_cfg1_l_rexi_golden(golden_medium):
+    out = run_rexi(L, 128, 7200.0, 256, golden_medium["cfg1_in"])
+    assert rel_linf(out, golden_medium["cfg1_out"]) <= LIN_BAR
+
+
+def test_cfg1_accuracy_variant_vs_oracle():
+    """p0=15, p1=60 contour (max|beta| 1.6e6, summation floor 1.5e-11)."""
+    st = ost.seeded_linear_state(128, 0)
+    a, b = ost.contour_coeffs(0, 15.0, 60.0, 256)
+    ref = olay.pack(orx.rexi_sum("l", orx.Model(128, 1e4 * G), 7200.0, a, b, st, chunk=64))
+    out = run_rexi(L, 128, 7200.0, 256, olay.pack(st), 15.0, 60.0)
+    assert rel_linf(out, ref) <= LIN_BAR
+
+
+def test_single_solve_and_apply(golden_small):
+    par = params(21)
+    st = unpack(golden_small["T21_l16_in"], 21)
+    sl = ShiftedLinearSolver(L, 480.0, par)
+    x = sl.solve_stacked(1.3 - 0.8j, st)
+    assert rel_linf(pack(x), golden_small["T21_l_single_out"]) <= 1e-12
+    # residual against the oracle's forward band operator
+    fac = orx.LFactors(orx.Model(21, 1e4 * G), 480.0)
+    res = fac.apply(1.3 - 0.8j, x) - st
+    assert np.max(np.abs(res)) <= 1e-10 * np.max(np.abs(st))
+    y = sl.apply_stacked(0.7 + 0.2j, st)
+    assert rel_linf(pack(y), olay.pack(fac.apply(0.7 + 0.2j, st))) <= 1e-13
+    slg = ShiftedLinearSolver(LG, 480.0, par)
+    assert rel_linf(pack(slg.apply_stacked(0.7 + 0.2j, st)), golden_small["T21_lg_apply_out"]) <= 1e-14
+
+
+def test_two_rhs_fusion_matches_separate():
+    """n_rhs = 2 (ETD2RK psi0/psi1 fusion) equals two single sums."""
+    par = params(42)
+    for group in (LG, L):
+        sl = ShiftedLinearSolver(group, 900.0, par)
+        c0, c1 = coeffs(64, 0), coeffs(64, 1)
+        u = ost.seeded_linear_state(42, 1)
+        v = ost.seeded_linear_state(42, 2)
+        rhs = to_device(np.stack([pack(u), pack(v)]))
+        bet = to_device(np.stack([c0.betas, c1.betas]))
+        out = sl.rexi_sum_dev(c0.alphas, bet, rhs).cpu().numpy()
+        model = orx.Model(42, 1e4 * G)
+        for r, (st, c) in enumerate(((u, c0), (v, c1))):
+            ref = olay.pack(orx.rexi_sum(group.token, model, 900.0, c.alphas, c.betas, st))
+            assert rel_linf(out[r], ref) <= LIN_BAR
+
+
+@pytest.mark.parametrize("group", ["lg", "l"])
+def test_pole_blocks_combine_bitwise(group):
+    """Per-rank partials over aligned power-of-two pole blocks, combined by
+    the fixed tree, equal the one-launch sum bitwise for K = 1, 2, 4, 8
+    (test_parallel.py:67-78 analogue, emulated on one GPU)."""
+    par = params(63)
+    sl = ShiftedLinearSolver(L if group == "l" else LG, 3600.0, par)
+    c = coeffs(256)
+    rhs = to_device(pack(ost.seeded_linear_state(63, 3)))[None]
+    bet = to_device(c.betas.reshape(1, -1))
+    full = sl.rexi_sum_dev(c.alphas, bet, rhs).cpu().numpy()
+    lib = _lib.load()
+    for k in (2, 4, 8):
+        parts = torch.stack([sl.rexi_sum_dev(c.alphas, bet, rhs, pole_range=(r * 256 // k, (r + 1) * 256 // k),
+                                             realify=False) for r in range(k)]).contiguous()
+        out = torch.empty_like(rhs)
+        _lib.check(lib.swx_tree_combine(63, 1, k, ptr(parts), 1, ptr(out), stream_ptr()))
+        assert np.array_equal(out.cpu().numpy(), full), k
+
+
+def test_singular_shifts_raise():
+    par = params(21)
+    l = 7
+    kappa = l * (l + 1) / par.cfg.radius_a**2
+    alpha = 1j * 480.0 * np.sqrt(par.mean_geopotential * kappa)
+    with pytest.raises(SolverError):
+        ShiftedLinearSolver(LG, 480.0, par).warm(np.array([1.0 + 1j, alpha]))
+    with pytest.raises(SolverError):
+        ShiftedLinearSolver(LG, 480.0, par).warm(np.array([0.0 + 0j]))
+    # band operator eigenvalue -> singular Coriolis system
+    p10 = params(10)
+    fac = orx.LFactors(orx.Model(10, 1e4 * G), 300.0)
+    n = olay.ncoef(10)
+    mat = np.zeros((3 * n, 3 * n), dtype=complex)
+    for col in range(3 * n):
+        e = np.zeros(3 * n, dtype=complex)
+        e[col] = 1.0
+        x = olay.unpack(e.reshape(-1, 3).T.copy(), 10)
+        y = olay.pack(fac.apply(0.0, x))
+        mat[:, col] = y.T.reshape(-1)
+    lam = np.linalg.eigvals(mat)
+    bad = -lam[np.argmax(np.abs(lam.imag))]
+    with pytest.raises(SolverError):
+        ShiftedLinearSolver(L, 300.0, p10).warm(np.array([bad]))
+
+
+# ---------------------------------------------------------------- transforms
+
+def test_transforms_t21_golden(golden_small):
+    from paper_1805_06557_b200 import sphere as sp
+
+    cfg = SphereConfig.for_truncation(21)
+    st = unpack(golden_small["T21_sht_in"], 21)
+    g = sp.synthesis(sp.SpectralField(st[0]), cfg).values
+    assert rel_linf(g.ravel(), golden_small["T21_synth_phi"].ravel()) <= 1e-12
+    u, v = sp.uv_from_vortdiv(sp.SpectralField(st[1]), sp.SpectralField(st[2]), cfg)
+    assert rel_linf(u.values.ravel(), golden_small["T21_u"].ravel()) <= 1e-12
+    assert rel_linf(v.values.ravel(), golden_small["T21_v"].ravel()) <= 1e-12
+    an = sp.analysis(sp.GridField(golden_small["T21_grid_in"], cfg), cfg)
+    assert rel_linf(pack(an.coeffs[None])[0], golden_small["T21_analysis"]) <= 1e-12
+
+
+@pytest.mark.parametrize("atoms,key", [(1, "T21_tend_lc"), (2, "T21_tend_n"), (3, "T21_tend_lc_n")])
+def test_tendencies_t21_golden(golden_small, atoms, key):
+    cfg = SphereConfig.for_truncation(21)
+    plan = plan_for(cfg)
+    st = to_device(golden_small["T21_sht_in"])
+    out = plan.tendency_dev(atoms, st).cpu().numpy()
+    assert rel_linf(out, golden_small[key]) <= 1e-11
+
+
+def test_tendency_t63_golden(golden_small):
+    plan = plan_for(SphereConfig.for_truncation(63))
+    out = plan.tendency_dev(3, to_device(golden_small["T63_sht_in"])).cpu().numpy()
+    assert rel_linf(out, golden_small["T63_tend_lc_n"]) <= 1e-11
+
+
+def test_tendency_t256_vs_oracle():
+    g = osh.grid_for(256)
+    st = ost.seeded_balanced_state(g)
+    st[2] = ost.seeded_linear_state(256, 9)[2] * 1e-1  # give it divergence too
+    ref = olay.pack(g.tendency_lc_n(st))
+    plan = plan_for(SphereConfig.for_truncation(256))
+    out = plan.tendency_dev(3, to_device(olay.pack(st))).cpu().numpy()
+    assert rel_linf(out, ref) <= 1e-10
+
+
+def test_sht_round_trip_t1279():
+    """Size-independent property at cfg4's grid: analysis(synthesis(c)) = c."""
+    cfg = SphereConfig.for_truncation(1279)
+    plan = plan_for(cfg)
+    c = ost.seeded_linear_state(1279, 5)[0:1] / 1e3
+    cd = to_device(olay.pack(c))
+    grid = plan.synthesis_dev(cd)
+    back = plan.analysis_dev(grid).cpu().numpy()
+    assert rel_linf(back, olay.pack(c)) <= 1e-10
+
+
+# ---------------------------------------------------------------- ETD2RK
+
+def test_etdrk_t42_golden(golden_medium):
+    par = params(42)
+    st = PrognosticState.from_stack(unpack(golden_medium["T42etd_ic"], 42), par.cfg)
+    stepper = build_stepper("lg_rexi_lc_n_etdrk", par, RexiSetup(num_poles=128))
+    s1 = stepper.step(st, 1800.0)
+    assert rel_linf(pack(s1.stack()), golden_medium["T42etd_step1"]) <= 1e-10
+    res = integrate(stepper, st, 1800.0, 8 * 1800.0)
+    assert not res.diverged
+    assert rel_l2(pack(res.state.stack()), golden_medium["T42etd_step8"]) <= 1e-8
+
+
+def test_etdrk_t256_one_day_golden(golden_cfg2):
+    """cfg2: 48 ETD2RK steps (1 simulated day) at T256, N=256, rel L2 <= 1e-8."""
+    par = params(256)
+    st = PrognosticState.from_stack(unpack(golden_cfg2["T256etd_ic"], 256), par.cfg)
+    stepper = build_stepper("lg_rexi_lc_n_etdrk", par, RexiSetup(num_poles=256))
+    s1 = stepper.step(st, 1800.0)
+    assert rel_linf(pack(s1.stack()), golden_cfg2["T256etd_step1"]) <= 1e-10
+    res = integrate(stepper, st, 1800.0, 48 * 1800.0)
+    assert not res.diverged and res.n_steps == 48
+    err = rel_l2(pack(res.state.stack()), golden_cfg2["T256etd_step48"])
+    print(f"T256 one-day relative L2 vs reference: {err:.3e}")
+    assert err <= 1e-8
+
+
+# ---------------------------------------------------------------- cfg4 scale
+
+def test_cfg4_t1279_subset_vs_oracle():
+    """T1279 l-solve on 4 poles of the N=1024 contour vs the band-LU oracle,
+    plus linearity of the full N=1024 pole sum."""
+    trunc = 1279
+    par = params(trunc)
+    c = coeffs(1024)
+    st = ost.seeded_linear_state(trunc, 0)
+    sl = ShiftedLinearSolver(L, 14400.0, par)
+    rhs = to_device(olay.pack(st))[None]
+    bet = to_device(c.betas.reshape(1, -1))
+    sub = sl.rexi_sum_dev(c.alphas, bet, rhs, pole_range=(0, 4), realify=False).cpu().numpy()[0]
+    model = orx.Model(trunc, 1e4 * G)
+    ref = olay.pack(orx.rexi_sum("l", model, 14400.0, c.alphas[:4], c.betas[:4], st, chunk=4,
+                                 do_realify=False))
+    assert rel_linf(sub, ref) <= LIN_BAR
+    # linearity of the full sum: S(2x - y) = 2 S(x) - S(y) (up to rounding)
+    st2 = ost.seeded_linear_state(trunc, 1)
+    r2 = to_device(olay.pack(st2))[None]
+    sx = sl.rexi_sum_dev(c.alphas, bet, rhs).cpu().numpy()
+    sy = sl.rexi_sum_dev(c.alphas, bet, r2).cpu().numpy()
+    sxy = sl.rexi_sum_dev(c.alphas, bet, (2.0 * rhs - r2).contiguous()).cpu().numpy()
+    assert np.all(np.isfinite(sx))
+    scale = np.max(np.abs(c.betas)) * 1e3
+    assert np.max(np.abs(sxy - (2 * sx - sy))) <= 1e-10 * scale
