@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg4"), default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="ncu mode: only warm-up + the K timed steps (no soak/e2e/cpu/breakdown)")
     return ap.parse_args()
 
 
@@ -244,7 +246,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < 1.0:   # bring clocks to steady load
+    while not args.profile and time.perf_counter() - t_soak < 1.0:   # steady clocks
         step()
         torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -270,6 +272,10 @@ def main():
     ms_total = float(ms_total.item())
     ms_per_step = ms_total / args.steps
     value = units_per_step * args.steps / (ms_total * 1e-3)
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"profile_mode": True, "ms_per_step": ms_per_step}), flush=True)
+        return
 
     # ---- per-kernel breakdown (live CUDA events on the launching stream)
     from paper_1805_06557_b200.steppers import axpy
