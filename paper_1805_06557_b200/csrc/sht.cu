@@ -13,13 +13,19 @@
 //    frexp/ldexp sectoral values, at the northern node of each equatorially
 //    symmetric latitude pair, and uses P(-x) = (-1)^(l+m) P(x),
 //    H(-x) = (-1)^(l+m+1) H(x) for the southern node.
-//  * synthesis: one thread per (latitude pair, m) walks l = m..T accumulating
-//    parity-split sums of all series at once (fully FP64-FMA, no smem traffic).
-//  * analysis: per m, (l x lat) tiles of P/H are generated into shared memory
-//    and contracted against the prepared Fourier data.
+//  * synthesis: one thread per (latitude pair, m) walks l = m..T with the
+//    column's coefficients and recurrence constants staged in shared memory,
+//    accumulating parity-split sums of all series at once (DFMA).
+//  * analysis: per m, (16 l x latitude) tiles of P and H are generated into
+//    shared memory and contracted with the prepared Fourier data on the FP64
+//    tensor cores (mma.sync m8n8k4 f64 = DMMA), K split over two warp groups.
 //  * The Coriolis atom is evaluated in Fourier space (f and df/dlat are
 //    latitude-only multipliers, so FFT(f*g) = f*FFT(g) exactly); only the 5
-//    nonlinear products go through the longitude FFT (cuFFT, batched).
+//    nonlinear products go through the longitude FFT (cuFFT, batched).  The
+//    products are quadratic in fields with m <= T, so any longitude count
+//    nlon_t >= 3T+1 gives the same m <= T coefficients; the tendency path uses
+//    the smallest 7-smooth such nlon_t (784 at T256 instead of the
+//    reference's 772 = 4*193, which cuFFT can only do by Bluestein).
 #include <cufft.h>
 
 #include <algorithm>
@@ -32,7 +38,10 @@
 // POD view passed to kernels by value
 struct ShtView {
   int trunc = 0, nlat = 0, nlon = 0, nh = 0, nm = 0, nfreq = 0, ncoef = 0;
-  double radius = 0, omega = 0, dlon = 0, fscale = 0;
+  int nhp = 0;       // latitude pairs padded to the analysis chunk granularity
+  int kc = 0;        // analysis latitude chunk (multiple of 16, <= 256)
+  int nlon_t = 0, nfreq_t = 0;  // FFT size of the tendency path
+  double radius = 0, omega = 0, dlon = 0, dlon_t = 0, fscale = 0;
   // per latitude pair (nh): north/south rows, x at the north node, 1/cos,
   // weights at both nodes
   int *d_jn = nullptr, *d_js = nullptr;
@@ -55,105 +64,122 @@ __host__ __device__ inline int rc_offset(int trunc, int m) {
 }
 
 // ---------------------------------------------------------------------
-// Legendre walker: P_l, H_l at one node for l = m, m+1, ...
-// ---------------------------------------------------------------------
-struct LegWalk {
-  double x, rcos;
-  double pm1, p0, p1;  // P_{l-1}, P_l, P_{l+1}
-  const double4 *rc;   // column m constants, index k = l - m
-  int k;
-  __device__ __forceinline__ void init(double xx, double rcs, double seed, int m,
-                                       const double4 *col) {
-    x = xx;
-    rcos = rcs;
-    rc = col;
-    k = 0;
-    pm1 = 0.0;
-    p0 = seed;
-    p1 = sqrt(2.0 * m + 3.0) * xx * seed;  // sphere.py:96-97
-  }
-  // H_l for the current l (uses P_{l-1}, P_{l+1}); sphere.py:102-111
-  __device__ __forceinline__ double h() const {
-    const double4 c = rc[k];
-    return (c.z * pm1 - c.w * p1) * rcos;
-  }
-  // advance l -> l+1 (computes P_{l+2} from the reference recurrence, 98-100)
-  __device__ __forceinline__ void step(int kmax) {
-    double p2 = 0.0;
-    if (k + 2 <= kmax) {
-      const double4 c = rc[k + 2];
-      p2 = fma(x, p1, -c.x * p0) * c.y;
-    }
-    pm1 = p0;
-    p0 = p1;
-    p1 = p2;
-    ++k;
-  }
-};
-
-// ---------------------------------------------------------------------
-// synthesis, state variant: from (phi', vort, div) produce the Fourier
-// coefficients of u, v, vort, phi' (C2R input rows) and the Fourier-space
-// Coriolis terms (tendency_lc before analysis).
+// synthesis.  CTA = (m, block of latitude pairs), one thread per pair.
+// MODE 0 (state): from (phi', vort, div) produce the Fourier coefficients of
+//   u, v, vort, phi' (C2R rows) and the Fourier-space Coriolis terms.
+// MODE 1 (plain): field blockIdx.z -> its Fourier coefficients.
 // ---------------------------------------------------------------------
 struct SynthArgs {
-  const double2 *state;  // packed (phi', vort, div)
-  double2 *c2r;          // [field][nlat][nfreq], fields u, v, vort, phi'
-  double2 *lc;           // [2][nlat][nm]: fft*dlon of -f div - f' v, f vort - f' u
+  const double2 *coef;  // packed state (MODE 0) or nf packed fields (MODE 1)
+  double2 *c2r;         // [field][nlat][nfreq]
+  double2 *lc;          // [2][nlat][nm]: fft*dlon of -f div - f' v, f vort - f' u
   int want_lc;
+  int nfreq;
 };
 
-__global__ void __launch_bounds__(128) synth_state_kernel(ShtView p, SynthArgs a) {
+constexpr int kSL = 128;  // l rows staged per chunk
+
+template <int MODE>
+__global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
+  constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
+  constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
+  __shared__ double2 cs[NS][kSL];
+  __shared__ double4 rcs[kSL + 2];
   const int m = blockIdx.x;
   const int i = blockIdx.y * blockDim.x + threadIdx.x;
-  if (i >= p.nh) return;
+  const int field = MODE == 1 ? blockIdx.z : 0;
   const int T = p.trunc, nc = p.ncoef;
   const int off = col_offset(T, m);
   const int kmax = T + 1 - m;
-  LegWalk w;
-  w.init(p.d_x[i], p.d_rcos[i], p.d_seed[(size_t)m * p.nh + i], m,
-         p.d_rc + rc_offset(T, m));
-  // parity-split accumulators [parity][series]; P series: vort, div, phi,
-  // psi, chi; H series: psi, chi
-  double2 sp[2][5], sh[2][2];
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  const bool has = i < p.nh;
+  double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
+  if (has) {
+    x = p.d_x[i];
+    rcos = p.d_rcos[i];
+    const double seed = p.d_seed[(size_t)m * p.nh + i];
+    p0 = seed;
+    p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
+  }
+  double2 sp[2][NS], sh[2][NH > 0 ? NH : 1];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
 #pragma unroll
-    for (int s = 0; s < 5; ++s) sp[q][s] = make_double2(0.0, 0.0);
-    sh[q][0] = sh[q][1] = make_double2(0.0, 0.0);
+    for (int s = 0; s < NS; ++s) sp[q][s] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int s = 0; s < (NH > 0 ? NH : 1); ++s) sh[q][s] = make_double2(0.0, 0.0);
   }
-  const double *invlap = p.d_lconst;
-  const double2 *cphi = a.state, *cvor = a.state + nc, *cdiv = a.state + 2 * nc;
-  for (int l = m; l <= T; ++l) {
-    const int q = (l - m) & 1;
-    const int s = off + (l - m);
-    const double P = w.p0, H = w.h();
-    const double2 z = __ldg(cvor + s), d = __ldg(cdiv + s), f = __ldg(cphi + s);
-    const double il = __ldg(invlap + l);
-    const double2 ps = make_double2(z.x * il, z.y * il);
-    const double2 ch = make_double2(d.x * il, d.y * il);
-    if (q == 0) {
-      sp[0][0].x = fma(P, z.x, sp[0][0].x); sp[0][0].y = fma(P, z.y, sp[0][0].y);
-      sp[0][1].x = fma(P, d.x, sp[0][1].x); sp[0][1].y = fma(P, d.y, sp[0][1].y);
-      sp[0][2].x = fma(P, f.x, sp[0][2].x); sp[0][2].y = fma(P, f.y, sp[0][2].y);
-      sp[0][3].x = fma(P, ps.x, sp[0][3].x); sp[0][3].y = fma(P, ps.y, sp[0][3].y);
-      sp[0][4].x = fma(P, ch.x, sp[0][4].x); sp[0][4].y = fma(P, ch.y, sp[0][4].y);
-      sh[0][0].x = fma(H, ps.x, sh[0][0].x); sh[0][0].y = fma(H, ps.y, sh[0][0].y);
-      sh[0][1].x = fma(H, ch.x, sh[0][1].x); sh[0][1].y = fma(H, ch.y, sh[0][1].y);
-    } else {
-      sp[1][0].x = fma(P, z.x, sp[1][0].x); sp[1][0].y = fma(P, z.y, sp[1][0].y);
-      sp[1][1].x = fma(P, d.x, sp[1][1].x); sp[1][1].y = fma(P, d.y, sp[1][1].y);
-      sp[1][2].x = fma(P, f.x, sp[1][2].x); sp[1][2].y = fma(P, f.y, sp[1][2].y);
-      sp[1][3].x = fma(P, ps.x, sp[1][3].x); sp[1][3].y = fma(P, ps.y, sp[1][3].y);
-      sp[1][4].x = fma(P, ch.x, sp[1][4].x); sp[1][4].y = fma(P, ch.y, sp[1][4].y);
-      sh[1][0].x = fma(H, ps.x, sh[1][0].x); sh[1][0].y = fma(H, ps.y, sh[1][0].y);
-      sh[1][1].x = fma(H, ch.x, sh[1][1].x); sh[1][1].y = fma(H, ch.y, sh[1][1].y);
+  for (int l0 = m; l0 <= T; l0 += kSL) {
+    const int n = min(kSL, T + 1 - l0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kSL + 2; t += blockDim.x) {
+      const int k = l0 - m + t;
+      if (k <= kmax) rcs[t] = rc[k];
     }
-    w.step(kmax);
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int s = off + (l0 - m) + t;
+      if (MODE == 0) {
+        const double il = p.d_lconst[l0 + t];
+        const double2 z = a.coef[nc + s], d = a.coef[2 * nc + s];
+        cs[0][t] = z;
+        cs[1][t] = d;
+        cs[NS > 2 ? 2 : 0][t] = a.coef[s];
+        cs[NS > 3 ? 3 : 0][t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
+        cs[NS > 4 ? 4 : 0][t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+      } else {
+        cs[0][t] = a.coef[(size_t)field * nc + s];
+      }
+    }
+    __syncthreads();
+    for (int t = 0; t < n; t += 2) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {  // static parity: l - m = (l0 - m) + t + q
+        if (q == 1 && t + 1 >= n) break;
+        const int tt = t + q;
+        const int k = l0 - m + tt;
+        const double P = p0;
+        double H = 0.0;
+        if (NH > 0) {
+          const double4 c = rcs[tt];
+          H = (c.z * pm1 - c.w * p1) * rcos;
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const double2 v = cs[s][tt];
+          sp[q][s].x = fma(P, v.x, sp[q][s].x);
+          sp[q][s].y = fma(P, v.y, sp[q][s].y);
+        }
+#pragma unroll
+        for (int s = 0; s < NH; ++s) {
+          const double2 v = cs[NS > 3 ? 3 + s : 0][tt];
+          sh[q][s].x = fma(H, v.x, sh[q][s].x);
+          sh[q][s].y = fma(H, v.y, sh[q][s].y);
+        }
+        double p2 = 0.0;
+        if (k + 2 <= kmax) {
+          const double4 c2 = rcs[tt + 2];
+          p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
+        }
+        pm1 = p0;
+        p0 = p1;
+        p1 = p2;
+      }
+    }
   }
-  const double rcos = p.d_rcos[i];
-  const double ra = 1.0 / p.radius;
+  if (!has) return;
   const int jn = p.d_jn[i], js = p.d_js[i];
+  const int nf = a.nfreq;
+  const size_t row = (size_t)p.nlat * nf;
+  // kSL is even and l0 - m advances by kSL, so sp[q] holds parity q of (l - m)
+  if (MODE == 1) {
+    double2 gn = make_double2(sp[0][0].x + sp[1][0].x, sp[0][0].y + sp[1][0].y);
+    double2 gs = make_double2(sp[0][0].x - sp[1][0].x, sp[0][0].y - sp[1][0].y);
+    if (m == 0) gn.y = gs.y = 0.0;  // irfft ignores Im of the DC bin
+    a.c2r[field * row + (size_t)jn * nf + m] = gn;
+    if (js != jn) a.c2r[field * row + (size_t)js * nf + m] = gs;
+    return;
+  }
+  const double ra = 1.0 / p.radius;
   const double fm = (double)m;
 #pragma unroll
   for (int hemi = 0; hemi < 2; ++hemi) {
@@ -162,23 +188,26 @@ __global__ void __launch_bounds__(128) synth_state_kernel(ShtView p, SynthArgs a
     const double sg = hemi ? -1.0 : 1.0;  // sign of the odd-parity part
     double2 G[5], GH[2];
 #pragma unroll
-    for (int s = 0; s < 5; ++s)
-      G[s] = make_double2(sp[0][s].x + sg * sp[1][s].x, sp[0][s].y + sg * sp[1][s].y);
+    for (int s = 0; s < 5; ++s) {
+      const int ss = s < NS ? s : 0;
+      G[s] = make_double2(sp[0][ss].x + sg * sp[1][ss].x, sp[0][ss].y + sg * sp[1][ss].y);
+    }
     // H has opposite parity: south = -even + odd
 #pragma unroll
-    for (int s = 0; s < 2; ++s)
-      GH[s] = make_double2(sg * sh[0][s].x + sh[1][s].x, sg * sh[0][s].y + sh[1][s].y);
-    // u = (dchi/dlon sec - dpsi/dlat)/a, v = (dpsi/dlon sec + dchi/dlat)/a
-    // with d/dlon = i m (sphere.py:393-402)
+    for (int s = 0; s < 2; ++s) {
+      const int ss = NH > 0 ? (s < NH ? s : 0) : 0;
+      GH[s] = make_double2(sg * sh[0][ss].x + sh[1][ss].x, sg * sh[0][ss].y + sh[1][ss].y);
+    }
+    // u = (dchi/dlon sec - dpsi/dlat)/a, v = (dpsi/dlon sec + dchi/dlat)/a,
+    // d/dlon = i m (sphere.py:393-402)
     double2 u = make_double2((-fm * G[4].y * rcos - GH[0].x) * ra, (fm * G[4].x * rcos - GH[0].y) * ra);
     double2 v = make_double2((-fm * G[3].y * rcos + GH[1].x) * ra, (fm * G[3].x * rcos + GH[1].y) * ra);
     double2 gz = G[0], gp = G[2], gd = G[1];
-    if (m == 0) u.y = v.y = gz.y = gp.y = gd.y = 0.0;  // irfft drops Im of the DC bin
-    const size_t row = (size_t)p.nlat * p.nfreq;
-    a.c2r[0 * row + (size_t)j * p.nfreq + m] = u;
-    a.c2r[1 * row + (size_t)j * p.nfreq + m] = v;
-    a.c2r[2 * row + (size_t)j * p.nfreq + m] = gz;
-    a.c2r[3 * row + (size_t)j * p.nfreq + m] = gp;
+    if (m == 0) u.y = v.y = gz.y = gp.y = gd.y = 0.0;
+    a.c2r[0 * row + (size_t)j * nf + m] = u;
+    a.c2r[1 * row + (size_t)j * nf + m] = v;
+    a.c2r[2 * row + (size_t)j * nf + m] = gz;
+    a.c2r[3 * row + (size_t)j * nf + m] = gp;
     if (a.want_lc) {
       const double f = p.d_frow[j], fp = p.d_frow[p.nlat + j];
       const double sc = p.fscale;  // nlon * dlon: fft(irfft(G) * nlon) * dlon
@@ -188,40 +217,6 @@ __global__ void __launch_bounds__(128) synth_state_kernel(ShtView p, SynthArgs a
       a.lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m] = l2;
     }
   }
-}
-
-// plain synthesis of nf packed fields -> C2R rows of fields 0..nf-1
-__global__ void __launch_bounds__(128) synth_plain_kernel(ShtView p, const double2 *coef,
-                                                          int nf, double2 *c2r) {
-  const int m = blockIdx.x;
-  const int i = blockIdx.y * blockDim.x + threadIdx.x;
-  const int f = blockIdx.z;
-  if (i >= p.nh || f >= nf) return;
-  const int T = p.trunc;
-  const int off = col_offset(T, m);
-  LegWalk w;
-  w.init(p.d_x[i], p.d_rcos[i], p.d_seed[(size_t)m * p.nh + i], m, p.d_rc + rc_offset(T, m));
-  double2 se = make_double2(0.0, 0.0), so = make_double2(0.0, 0.0);
-  const double2 *c = coef + (size_t)f * p.ncoef + off;
-  for (int l = m; l <= T; ++l) {
-    const double P = w.p0;
-    const double2 z = __ldg(c + (l - m));
-    if (((l - m) & 1) == 0) {
-      se.x = fma(P, z.x, se.x);
-      se.y = fma(P, z.y, se.y);
-    } else {
-      so.x = fma(P, z.x, so.x);
-      so.y = fma(P, z.y, so.y);
-    }
-    w.step(T + 1 - m);
-  }
-  const int jn = p.d_jn[i], js = p.d_js[i];
-  const size_t base = (size_t)f * p.nlat * p.nfreq;
-  double2 gn = make_double2(se.x + so.x, se.y + so.y);
-  double2 gs = make_double2(se.x - so.x, se.y - so.y);
-  if (m == 0) gn.y = gs.y = 0.0;
-  c2r[base + (size_t)jn * p.nfreq + m] = gn;
-  if (js != jn) c2r[base + (size_t)js * p.nfreq + m] = gs;
 }
 
 // zero the C2R rows above m = T (cuFFT may overwrite its input)
@@ -245,249 +240,321 @@ __global__ void products_kernel(double *g, size_t npts) {
 }
 
 // ---------------------------------------------------------------------
-// prepared analysis inputs A[m][parity][series][pair] (complex): the
-// quadrature weights, m-derivative factors and hemisphere folding applied.
-// Tendency series (P table): S1 dvort, S2 ddiv, S3 dphi, S4 KE;
-// (H table): S5 dvort, S6 ddiv, S7 dphi.   (vortdiv_from_uv, sphere.py:405-430)
+// prepared analysis inputs, DMMA layout A[m][part][parity][pair][kAS]:
+// quadrature weights, m-derivative factors and the hemisphere fold applied.
+// part 0 (P table) columns: S1 dvort, S2 ddiv, S3 dphi, S4 KE  (re, im)
+// part 1 (H table) columns: S5 dvort, S6 ddiv, S7 dphi, 0      (re, im)
+// (vortdiv_from_uv, sphere.py:405-430; tendency_lc/n, swe.py:188-251)
 // ---------------------------------------------------------------------
-constexpr int kSerTend = 7;
-constexpr int kSerTendP = 4;
+constexpr int kAS = 12;  // row stride (doubles) of prepared rows: conflict-free B fragments
+
+__device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double2 z = c < nv ? v[c] : make_double2(0.0, 0.0);
+    dst[2 * c] = z.x;
+    dst[2 * c + 1] = z.y;
+  }
+}
 
 __global__ void prep_tend_kernel(ShtView p, const double2 *Q, const double2 *lc,
-                                 int atoms, double2 *A) {
+                                 int atoms, double *A) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int m = blockIdx.y;
-  if (i >= p.nh) return;
-  const int jn = p.d_jn[i], js = p.d_js[i];
-  const double rcos = p.d_rcos[i];
-  const double ra = 1.0 / p.radius;
-  const double fm = (double)m;
-  double2 av[2][kSerTend];
+  if (i >= p.nhp) return;
+  double *base = A + (size_t)m * 4 * p.nhp * kAS;  // [part][par][pair][kAS]
+  double2 ev[7], od[7];
+  if (i >= p.nh) {
 #pragma unroll
-  for (int hemi = 0; hemi < 2; ++hemi) {
-    const int j = hemi ? js : jn;
-    const double wj = hemi ? p.d_ws[i] : p.d_wn[i];
-    const double woc = wj * rcos;
-    const size_t row = (size_t)p.nlat * p.nfreq;
-    const size_t at = (size_t)j * p.nfreq + m;
-    double2 F[5];
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-      const double2 q = Q[s * row + at];
-      F[s] = make_double2(q.x * p.dlon, q.y * p.dlon);  // fft * dlon
-    }
-    double2 l1 = make_double2(0.0, 0.0), l2 = l1;
-    if (atoms & SWX_TEND_LC) {
-      l1 = lc[(size_t)j * p.nm + m];
-      l2 = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
-    }
+    for (int s = 0; s < 7; ++s) ev[s] = od[s] = make_double2(0.0, 0.0);
+  } else {
+    const int jn = p.d_jn[i], js = p.d_js[i];
+    const double rcos = p.d_rcos[i];
+    const double ra = 1.0 / p.radius;
+    const double fm = (double)m;
     const bool nl = (atoms & SWX_TEND_N) != 0;
-    // (i m / a) * woc * F  ==  woc*m/a * (-F.y, F.x)
-    const double cm = woc * fm * ra;
-    const double2 imPu = make_double2(-cm * F[0].y, cm * F[0].x);  // phi'u
-    const double2 imZu = make_double2(-cm * F[2].y, cm * F[2].x);  // vort u
-    const double2 imZv = make_double2(-cm * F[3].y, cm * F[3].x);  // vort v
-    const double wa = wj * ra;
-    double2 *o = av[hemi];
-    o[0] = make_double2(wj * l1.x - (nl ? imZu.x : 0.0), wj * l1.y - (nl ? imZu.y : 0.0));
-    o[1] = make_double2(wj * l2.x + (nl ? imZv.x : 0.0), wj * l2.y + (nl ? imZv.y : 0.0));
-    o[2] = nl ? make_double2(-imPu.x, -imPu.y) : make_double2(0.0, 0.0);
-    o[3] = nl ? make_double2(wj * F[4].x, wj * F[4].y) : make_double2(0.0, 0.0);
-    o[4] = nl ? make_double2(wa * F[3].x, wa * F[3].y) : make_double2(0.0, 0.0);
-    o[5] = nl ? make_double2(wa * F[2].x, wa * F[2].y) : make_double2(0.0, 0.0);
-    o[6] = nl ? make_double2(wa * F[1].x, wa * F[1].y) : make_double2(0.0, 0.0);
-    if (js == jn) {
+    double2 av[2][7];
 #pragma unroll
-      for (int s = 0; s < kSerTend; ++s) av[1][s] = make_double2(0.0, 0.0);
-      break;
+    for (int hemi = 0; hemi < 2; ++hemi) {
+      const int j = hemi ? js : jn;
+      const double wj = hemi ? p.d_ws[i] : p.d_wn[i];
+      const double woc = wj * rcos;
+      const size_t row = (size_t)p.nlat * p.nfreq_t;
+      const size_t at = (size_t)j * p.nfreq_t + m;
+      double2 F[5];
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        const double2 q = nl ? Q[s * row + at] : make_double2(0.0, 0.0);
+        F[s] = make_double2(q.x * p.dlon_t, q.y * p.dlon_t);  // fft * dlon
+      }
+      double2 l1 = make_double2(0.0, 0.0), l2 = l1;
+      if (atoms & SWX_TEND_LC) {
+        l1 = lc[(size_t)j * p.nm + m];
+        l2 = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
+      }
+      // (i m / a) * woc * F  ==  woc*m/a * (-F.y, F.x)
+      const double cm = woc * fm * ra;
+      const double2 imPu = make_double2(-cm * F[0].y, cm * F[0].x);  // phi'u
+      const double2 imZu = make_double2(-cm * F[2].y, cm * F[2].x);  // vort u
+      const double2 imZv = make_double2(-cm * F[3].y, cm * F[3].x);  // vort v
+      const double wa = wj * ra;
+      double2 *o = av[hemi];
+      o[0] = make_double2(wj * l1.x - imZu.x, wj * l1.y - imZu.y);
+      o[1] = make_double2(wj * l2.x + imZv.x, wj * l2.y + imZv.y);
+      o[2] = make_double2(-imPu.x, -imPu.y);
+      o[3] = make_double2(wj * F[4].x, wj * F[4].y);
+      o[4] = make_double2(wa * F[3].x, wa * F[3].y);
+      o[5] = make_double2(wa * F[2].x, wa * F[2].y);
+      o[6] = make_double2(wa * F[1].x, wa * F[1].y);
+    }
+    if (js == jn) {  // equator node of an odd grid: counted once
+#pragma unroll
+      for (int s = 0; s < 7; ++s) ev[s] = od[s] = av[0][s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < 7; ++s) {
+        ev[s] = make_double2(av[0][s].x + av[1][s].x, av[0][s].y + av[1][s].y);
+        od[s] = make_double2(av[0][s].x - av[1][s].x, av[0][s].y - av[1][s].y);
+      }
     }
   }
-  // even part E = n + s, odd part O = n - s
-  double2 *base = A + (size_t)m * 2 * kSerTend * p.nh;
-#pragma unroll
-  for (int s = 0; s < kSerTend; ++s) {
-    const double2 e = make_double2(av[0][s].x + av[1][s].x, av[0][s].y + av[1][s].y);
-    const double2 od = (js == jn) ? av[0][s]
-                                  : make_double2(av[0][s].x - av[1][s].x, av[0][s].y - av[1][s].y);
-    base[(size_t)(0 * kSerTend + s) * p.nh + i] = e;
-    base[(size_t)(1 * kSerTend + s) * p.nh + i] = od;
-  }
+  const size_t ps = (size_t)p.nhp * kAS;
+  put_row(base + 0 * ps + (size_t)i * kAS, ev, 4);      // P, even
+  put_row(base + 1 * ps + (size_t)i * kAS, od, 4);      // P, odd
+  put_row(base + 2 * ps + (size_t)i * kAS, ev + 4, 3);  // H, even
+  put_row(base + 3 * ps + (size_t)i * kAS, od + 4, 3);  // H, odd
 }
 
-// plain analysis prep: nf grids already FFT'd into Q (fields 0..nf-1)
-__global__ void prep_plain_kernel(ShtView p, const double2 *Q, int nf, double2 *A) {
+// plain analysis prep: nf (<= 4) grids already FFT'd into Q (pitch nfreq)
+__global__ void prep_plain_kernel(ShtView p, const double2 *Q, int nf, double *A) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int m = blockIdx.y;
-  if (i >= p.nh) return;
-  const int jn = p.d_jn[i], js = p.d_js[i];
-  double2 *base = A + (size_t)m * 2 * nf * p.nh;
-  for (int f = 0; f < nf; ++f) {
-    const size_t row = (size_t)f * p.nlat * p.nfreq;
-    const double2 qn = Q[row + (size_t)jn * p.nfreq + m];
-    const double wn = p.d_wn[i] * p.dlon;
-    double2 an = make_double2(qn.x * wn, qn.y * wn), as = make_double2(0.0, 0.0);
-    if (js != jn) {
-      const double2 qs = Q[row + (size_t)js * p.nfreq + m];
-      const double ws = p.d_ws[i] * p.dlon;
-      as = make_double2(qs.x * ws, qs.y * ws);
+  if (i >= p.nhp) return;
+  double2 ev[4], od[4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) ev[f] = od[f] = make_double2(0.0, 0.0);
+  if (i < p.nh) {
+    const int jn = p.d_jn[i], js = p.d_js[i];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      if (f >= nf) break;
+      const size_t row = (size_t)f * p.nlat * p.nfreq;
+      const double2 qn = Q[row + (size_t)jn * p.nfreq + m];
+      const double wn = p.d_wn[i] * p.dlon;
+      const double2 an = make_double2(qn.x * wn, qn.y * wn);
+      double2 as = make_double2(0.0, 0.0);
+      if (js != jn) {
+        const double2 qs = Q[row + (size_t)js * p.nfreq + m];
+        const double ws = p.d_ws[i] * p.dlon;
+        as = make_double2(qs.x * ws, qs.y * ws);
+      }
+      ev[f] = make_double2(an.x + as.x, an.y + as.y);
+      od[f] = js == jn ? an : make_double2(an.x - as.x, an.y - as.y);
     }
-    base[(size_t)(0 * nf + f) * p.nh + i] = make_double2(an.x + as.x, an.y + as.y);
-    base[(size_t)(1 * nf + f) * p.nh + i] =
-        js == jn ? an : make_double2(an.x - as.x, an.y - as.y);
   }
+  double *base = A + (size_t)m * 2 * p.nhp * kAS;
+  put_row(base + (size_t)i * kAS, ev, 4);
+  put_row(base + (size_t)p.nhp * kAS + (size_t)i * kAS, od, 4);
 }
 
 // ---------------------------------------------------------------------
-// analysis contraction.  CTA per m; l processed in chunks of LC rows, the
-// latitude pairs in chunks of IC.  Generator threads (one per pair) walk the
-// recurrence LC steps and write P (and H) tiles to shared memory; consumer
-// threads (row r, series s) accumulate sum_i tile[r][i] * A[par][s][i].
+// analysis contraction on the FP64 tensor cores.
+// CTA per m, 256 threads.  Outer loop over latitude chunks of KC pairs,
+// inner loop over chunks of 16 degrees l.  Per l-chunk every thread walks
+// the recurrence 16 steps for its latitude and writes P (and H) into a
+// [pair][20] tile whose 16 row slots are parity-separated
+// (slot = (l-l0)%2 * 8 + (l-l0)/2), so an 8-row DMMA A-fragment holds 8
+// degrees of one parity.  Warps: tile = (table P|H) x (parity), K (the
+// latitudes) split over two warp groups; each warp runs two independent
+// accumulator chains of m8n8k4 DMMA; the K halves are summed in a fixed
+// order (deterministic).
 // ---------------------------------------------------------------------
-constexpr int kLC = 32;
-constexpr int kIC = 128;
+constexpr int kAT = 256;
+constexpr int kAL = 16;
+constexpr int kRS = 20;  // tile row stride (doubles): conflict-free A fragments
 
-template <int NSP, int NSH>
-struct AnaSmem {
-  double P[kLC][kIC + 1];
-  double H[NSH > 0 ? kLC : 1][kIC + 1];
-  double2 A[2][NSP + NSH][kIC];
-  double st[3][kIC];  // recurrence state for the chunk's pairs
-};
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
-// mode 0: tendency epilogue (3 fields from 7 series), mode 1: plain (NSP fields)
-template <int NSP, int NSH, int MODE>
-__global__ void __launch_bounds__(256) analysis_kernel(ShtView p, const double2 *A,
-                                                       double *state_ws, double2 *out) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  auto &sm = *reinterpret_cast<AnaSmem<NSP, NSH> *>(smraw);
-  constexpr int NS = NSP + NSH;
+template <int MODE>
+__global__ void __launch_bounds__(kAT) analysis_kernel(ShtView p, const double *A, double2 *out,
+                                                       int nf) {
+  constexpr int NPART = MODE == 0 ? 2 : 1;
+  extern __shared__ __align__(16) double sm[];
+  const int KC = p.kc;
+  double *Pt = sm;                                        // [KC][kRS]
+  double *Ht = Pt + (size_t)KC * kRS;                     // [KC][kRS]   (MODE 0)
+  double *As = Ht + (MODE == 0 ? (size_t)KC * kRS : 0);   // [part][par][KC][kAS]
+  double *red = As + (size_t)NPART * 2 * KC * kAS;        // [4][32][2]
+  double *res = red + 4 * 64;                             // [kAL][16]
+  double4 *rcs = reinterpret_cast<double4 *>(res + kAL * 16);  // [kAL + 2]
+
   const int m = blockIdx.x;
   const int T = p.trunc;
-  const int kmax = T + 1 - m;  // P needed up to l = T+1
+  const int kmax = T + 1 - m;
   const int off = col_offset(T, m);
   const double4 *rc = p.d_rc + rc_offset(T, m);
-  const int tid = threadIdx.x;
-  const int r = tid & 31, s = tid >> 5;  // consumer role (warp s = series)
-  // recurrence state lives in global workspace between l-chunks: [m][3][nh]
-  double *gst = state_ws + (size_t)m * 3 * p.nh;
-  const double2 *Am = A + (size_t)m * 2 * NS * p.nh;
-  __shared__ double2 res[kLC][NS];
+  const double *Am = A + (size_t)m * NPART * 2 * p.nhp * kAS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = warp & 3, part = tile >> 1, par = tile & 1, khalf = warp >> 2;
+  const int apar = part ? (par ^ 1) : par;  // H has the opposite fold parity
+  const bool mma_warp = MODE == 0 || part == 0;
+  const int lr = lane >> 2, lc4 = lane & 3;
 
-  for (int l0 = m; l0 <= T; l0 += kLC) {
-    const int nrow = min(kLC, T + 1 - l0);
-    double2 acc = make_double2(0.0, 0.0);
-    const int lrow = l0 + r;
-    const int par = (lrow - m) & 1;
-    // H series use the opposite parity of the fold
-    const int apar = (s < NSP) ? par : (par ^ 1);
-    for (int i0 = 0; i0 < p.nh; i0 += kIC) {
-      const int ni = min(kIC, p.nh - i0);
+  for (int i0 = 0; i0 < p.nh; i0 += KC) {
+    const int ni = min(KC, p.nh - i0);
+    const bool first = i0 == 0;
+    __syncthreads();
+    // prepared Fourier rows for this latitude chunk
+    for (int t = tid; t < NPART * 2 * KC; t += kAT) {
+      const int r = t % KC, pp = t / KC;
+      const double *src = Am + ((size_t)pp * p.nhp + i0 + r) * kAS;
+      double *dst = As + ((size_t)pp * KC + r) * kAS;
+      const bool ok = r < ni;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) dst[c] = ok ? src[c] : 0.0;
+    }
+    // recurrence state of this thread's latitude
+    const bool gen = tid < KC;
+    const bool has = tid < ni;
+    double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
+    if (has) {
+      const int i = i0 + tid;
+      x = p.d_x[i];
+      rcos = p.d_rcos[i];
+      const double seed = p.d_seed[(size_t)m * p.nh + i];
+      p0 = seed;
+      p1 = sqrt(2.0 * m + 3.0) * x * seed;
+    }
+    for (int l0 = m; l0 <= T; l0 += kAL) {
+      const int nrow = min(kAL, T + 1 - l0);
+      const int k0 = l0 - m;
+      __syncthreads();  // previous chunk's tiles / res fully consumed
+      if (tid < kAL + 2 && k0 + tid <= kmax) rcs[tid] = rc[k0 + tid];
       __syncthreads();
-      // load prepared inputs for this chunk
-      for (int t = tid; t < 2 * NS * kIC; t += blockDim.x) {
-        const int ii = t % kIC, ss = (t / kIC) % NS, pp = t / (kIC * NS);
-        sm.A[pp][ss][ii] = ii < ni ? Am[(size_t)(pp * NS + ss) * p.nh + i0 + ii]
-                                   : make_double2(0.0, 0.0);
-      }
-      // generate tiles
-      if (tid < kIC) {
-        const int i = i0 + tid;
-        double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
-        if (i < p.nh) {
-          x = p.d_x[i];
-          rcos = p.d_rcos[i];
-          if (l0 == m) {
-            const double seed = p.d_seed[(size_t)m * p.nh + i];
-            pm1 = 0.0;
-            p0 = seed;
-            p1 = sqrt(2.0 * m + 3.0) * x * seed;
-          } else {
-            pm1 = gst[i];
-            p0 = gst[p.nh + i];
-            p1 = gst[2 * p.nh + i];
-          }
-        }
-        for (int rr = 0; rr < kLC; ++rr) {
-          const int k = l0 - m + rr;
+      if (gen) {
+#pragma unroll 4
+        for (int rr = 0; rr < kAL; ++rr) {
           double pv = 0.0, hv = 0.0;
-          if (rr < nrow) {
+          if (rr < nrow && has) {
             pv = p0;
-            if (NSH > 0) {
-              const double4 c = rc[k];
+            if (MODE == 0) {
+              const double4 c = rcs[rr];
               hv = (c.z * pm1 - c.w * p1) * rcos;
             }
             double p2 = 0.0;
-            if (k + 2 <= kmax) {
-              const double4 c2 = rc[k + 2];
+            if (k0 + rr + 2 <= kmax) {
+              const double4 c2 = rcs[rr + 2];
               p2 = fma(x, p1, -c2.x * p0) * c2.y;
             }
             pm1 = p0;
             p0 = p1;
             p1 = p2;
           }
-          sm.P[rr][tid] = (tid < ni) ? pv : 0.0;
-          if (NSH > 0) sm.H[rr][tid] = (tid < ni) ? hv : 0.0;
-        }
-        if (i < p.nh && l0 + kLC <= T) {
-          gst[i] = pm1;
-          gst[p.nh + i] = p0;
-          gst[2 * p.nh + i] = p1;
+          const int slot = (rr & 1) * 8 + (rr >> 1);
+          Pt[tid * kRS + slot] = pv;
+          if (MODE == 0) Ht[tid * kRS + slot] = hv;
         }
       }
       __syncthreads();
-      if (s < NS && r < nrow) {
-        const double *row = (s < NSP) ? sm.P[r] : sm.H[NSH > 0 ? r : 0];
-        const double2 *av = sm.A[apar][s];
-#pragma unroll 4
-        for (int ii = 0; ii < kIC; ++ii) {
-          const double t = row[ii];
-          const double2 a = av[ii];
-          acc.x = fma(t, a.x, acc.x);
-          acc.y = fma(t, a.y, acc.y);
+      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+      if (mma_warp) {
+        const double *Tt = part ? Ht : Pt;
+        const double *Ab = As + (size_t)(part * 2 + apar) * KC * kAS;
+        const int kb = khalf * (KC >> 1), ke = kb + (KC >> 1);
+        const int arow = par * 8 + lr;
+        for (int k = kb; k < ke; k += 8) {
+          dmma(c0, c1, Tt[(k + lc4) * kRS + arow], Ab[(k + lc4) * kAS + lr]);
+          dmma(e0, e1, Tt[(k + 4 + lc4) * kRS + arow], Ab[(k + 4 + lc4) * kAS + lr]);
+        }
+        c0 += e0;
+        c1 += e1;
+        if (khalf == 1) {
+          red[(tile * 32 + lane) * 2] = c0;
+          red[(tile * 32 + lane) * 2 + 1] = c1;
+        }
+      }
+      __syncthreads();
+      if (mma_warp && khalf == 0) {
+        c0 += red[(tile * 32 + lane) * 2];
+        c1 += red[(tile * 32 + lane) * 2 + 1];
+        const int rr = 2 * lr + par;  // C row lr of this parity tile
+        res[rr * 16 + part * 8 + 2 * lc4] = c0;
+        res[rr * 16 + part * 8 + 2 * lc4 + 1] = c1;
+      }
+      __syncthreads();
+      if (tid < nrow) {
+        const int l = l0 + tid;
+        const int slot = off + (l - m);
+        const double *r = res + tid * 16;
+        if (MODE == 0) {
+          const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
+          double2 v0 = make_double2(r[4] + r[12], r[5] + r[13]);                            // dphi'
+          double2 v1 = make_double2(r[0] + r[8], r[1] + r[9]);                              // dvort
+          double2 v2 = make_double2(r[2] + r[10] + llk * r[6], r[3] + r[11] + llk * r[7]);  // ddiv
+          if (!first) {
+            const double2 a0 = out[slot], a1 = out[p.ncoef + slot], a2 = out[2 * p.ncoef + slot];
+            v0 = make_double2(a0.x + v0.x, a0.y + v0.y);
+            v1 = make_double2(a1.x + v1.x, a1.y + v1.y);
+            v2 = make_double2(a2.x + v2.x, a2.y + v2.y);
+          }
+          out[slot] = v0;
+          out[p.ncoef + slot] = v1;
+          out[2 * p.ncoef + slot] = v2;
+        } else {
+          for (int f = 0; f < nf; ++f) {
+            double2 v = make_double2(r[2 * f], r[2 * f + 1]);
+            if (!first) {
+              const double2 a0 = out[(size_t)f * p.ncoef + slot];
+              v = make_double2(a0.x + v.x, a0.y + v.y);
+            }
+            out[(size_t)f * p.ncoef + slot] = v;
+          }
         }
       }
     }
-    __syncthreads();
-    if (s < NS && r < nrow) res[r][s] = acc;
-    __syncthreads();
-    if (tid < nrow) {
-      const int l = l0 + tid;
-      const int slot = off + (l - m);
-      if (MODE == 0) {
-        const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
-        const double2 S1 = res[tid][0], S2 = res[tid][1], S3 = res[tid][2], S4 = res[tid][3];
-        const double2 S5 = res[tid][4], S6 = res[tid][5], S7 = res[tid][6];
-        out[slot] = make_double2(S3.x + S7.x, S3.y + S7.y);                    // dphi'
-        out[p.ncoef + slot] = make_double2(S1.x + S5.x, S1.y + S5.y);          // dvort
-        out[2 * p.ncoef + slot] = make_double2(S2.x + S6.x + llk * S4.x,       // ddiv
-                                               S2.y + S6.y + llk * S4.y);
-      } else {
-#pragma unroll
-        for (int f = 0; f < NSP; ++f) out[(size_t)f * p.ncoef + slot] = res[tid][f];
-      }
-    }
   }
+}
+
+// FFT size of the tendency path: smallest 7-smooth n >= 3T+1 (the user
+// grid's nlon when that is already 7-smooth and alias-free)
+static bool smooth7(int n) {
+  for (int f : {2, 3, 5, 7})
+    while (n % f == 0) n /= f;
+  return n == 1;
+}
+static int tendency_nlon(int trunc, int nlon) {
+  const int need = 3 * trunc + 1;
+  if (nlon >= need && smooth7(nlon)) return nlon;
+  int n = std::max(need, 2);
+  n += n & 1;
+  while (!smooth7(n)) n += 2;
+  return n;
 }
 
 }  // namespace swx
 
 using namespace swx;
 
-static int get_plan(swx_sht p, cufftType type, int batch, cufftHandle *out) {
-  const long long key = ((long long)type << 32) | (unsigned)batch;
+static int get_plan(swx_sht p, cufftType type, int nlon, int batch, cufftHandle *out) {
+  const long long key = ((long long)type << 48) | ((long long)nlon << 24) | (unsigned)batch;
   auto it = p->plans.find(key);
   if (it != p->plans.end()) {
     *out = it->second;
     return SWX_OK;
   }
   cufftHandle h;
-  int n[1] = {p->nlon};
-  int cn[1] = {p->nfreq};
+  const int nfreq = nlon / 2 + 1;
+  int n[1] = {nlon};
+  int cn[1] = {nfreq};
   cufftResult r;
   if (type == CUFFT_Z2D)
-    r = cufftPlanMany(&h, 1, n, cn, 1, p->nfreq, n, 1, p->nlon, CUFFT_Z2D, batch);
+    r = cufftPlanMany(&h, 1, n, cn, 1, nfreq, n, 1, nlon, CUFFT_Z2D, batch);
   else
-    r = cufftPlanMany(&h, 1, n, n, 1, p->nlon, cn, 1, p->nfreq, CUFFT_D2Z, batch);
+    r = cufftPlanMany(&h, 1, n, n, 1, nlon, cn, 1, nfreq, CUFFT_D2Z, batch);
   if (r != CUFFT_SUCCESS) return fail(SWX_ERR_CUDA, "cufftPlanMany failed: " + std::to_string(r));
   p->plans[key] = h;
   *out = h;
@@ -508,12 +575,17 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
   p->nlon = nlon;
   p->nm = trunc + 1;
   p->nh = (nlat + 1) / 2;
+  p->kc = p->nh <= 256 ? ((p->nh + 15) / 16) * 16 : 128;
+  p->nhp = ((p->nh + p->kc - 1) / p->kc) * p->kc;
   p->nfreq = nlon / 2 + 1;
+  p->nlon_t = tendency_nlon(trunc, nlon);
+  p->nfreq_t = p->nlon_t / 2 + 1;
   p->ncoef = ncoef_of(trunc);
   p->radius = radius;
   p->omega = omega;
   p->dlon = 2.0 * M_PI / nlon;  // sphere.py:201
-  p->fscale = nlon * p->dlon;
+  p->dlon_t = 2.0 * M_PI / p->nlon_t;
+  p->fscale = 2.0 * M_PI;       // nlon * dlon
   const int nh = p->nh, T = trunc;
   std::vector<int> jn(nh), js(nh);
   std::vector<double> x(nh), rcos(nh), wn(nh), ws(nh), seed((size_t)(T + 1) * nh);
@@ -554,7 +626,7 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
   std::vector<double> frow(2 * nlat);
   for (int j = 0; j < nlat; ++j) {
     const double s = h_sinlat[j];
-    frow[j] = 2.0 * omega * s;                                     // swe.py:203
+    frow[j] = 2.0 * omega * s;                                       // swe.py:203
     frow[nlat + j] = 2.0 * omega * std::sqrt(1.0 - s * s) / radius;  // swe.py:204
   }
   cudaError_t e = cudaSuccess;
@@ -578,8 +650,8 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     return fail(SWX_ERR_CUDA, std::string("sht create: ") + cudaGetErrorString(e));
   }
   cufftHandle h;
-  int rcd = get_plan(p, CUFFT_Z2D, 4 * nlat, &h);
-  if (!rcd) rcd = get_plan(p, CUFFT_D2Z, 5 * nlat, &h);
+  int rcd = get_plan(p, CUFFT_Z2D, p->nlon_t, 4 * nlat, &h);
+  if (!rcd) rcd = get_plan(p, CUFFT_D2Z, p->nlon_t, 5 * nlat, &h);
   if (rcd) {
     swx_sht_destroy(p);
     return rcd;
@@ -606,15 +678,14 @@ extern "C" int swx_sht_destroy(swx_sht p) {
 }
 
 // workspace layout (bytes, 256-aligned pieces):
-//   c2r  : 5 * nlat * nfreq complex
-//   grid : 5 * nlat * nlon  double
-//   Q    : 5 * nlat * nfreq complex
+//   c2r  : 5 * nlat * max(nfreq, nfreq_t) complex
+//   grid : 5 * nlat * max(nlon, nlon_t)   double
+//   Q    : 5 * nlat * max(nfreq, nfreq_t) complex
 //   lc   : 2 * nlat * nm    complex
-//   A    : nm * 2 * 7 * nh  complex
-//   st   : nm * 3 * nh      double
+//   A    : nm * 4 * nhp * kAS double
 struct ShtWs {
-  double2 *c2r, *Q, *lc, *A;
-  double *grid, *st;
+  double2 *c2r, *Q, *lc;
+  double *grid, *A;
   size_t bytes;
 };
 static size_t al(size_t b) { return (b + 255) / 256 * 256; }
@@ -622,13 +693,13 @@ static ShtWs carve(swx_sht p, void *base) {
   ShtWs w;
   char *c = (char *)base;
   size_t o = 0;
-  const size_t fr = (size_t)p->nlat * p->nfreq;
+  const size_t fr = (size_t)p->nlat * std::max(p->nfreq, p->nfreq_t);
+  const size_t gr = (size_t)p->nlat * std::max(p->nlon, p->nlon_t);
   w.c2r = (double2 *)(c + o); o += al(5 * fr * sizeof(double2));
-  w.grid = (double *)(c + o); o += al(5 * (size_t)p->nlat * p->nlon * sizeof(double));
+  w.grid = (double *)(c + o); o += al(5 * gr * sizeof(double));
   w.Q = (double2 *)(c + o); o += al(5 * fr * sizeof(double2));
   w.lc = (double2 *)(c + o); o += al(2 * (size_t)p->nlat * p->nm * sizeof(double2));
-  w.A = (double2 *)(c + o); o += al((size_t)p->nm * 2 * kSerTend * p->nh * sizeof(double2));
-  w.st = (double *)(c + o); o += al((size_t)p->nm * 3 * p->nh * sizeof(double));
+  w.A = (double *)(c + o); o += al((size_t)p->nm * 4 * p->nhp * kAS * sizeof(double));
   w.bytes = o;
   return w;
 }
@@ -638,21 +709,28 @@ extern "C" size_t swx_sht_workspace_bytes(swx_sht p) {
   return carve(p, nullptr).bytes;
 }
 
-template <int NSP, int NSH, int MODE>
-static int launch_analysis(swx_sht p, const double2 *A, double *st, double2 *out,
-                           cudaStream_t s) {
-  const size_t smem = sizeof(AnaSmem<NSP, NSH>);
-  auto k = analysis_kernel<NSP, NSH, MODE>;
+static size_t analysis_smem(swx_sht p, int mode) {
+  const size_t npart = mode == 0 ? 2 : 1;
+  const size_t kc = p->kc;
+  return sizeof(double) * (kc * kRS * (mode == 0 ? 2 : 1) + npart * 2 * kc * kAS + 4 * 64 +
+                           kAL * 16) +
+         sizeof(double4) * (kAL + 2);
+}
+
+template <int MODE>
+static int launch_analysis(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s) {
+  const size_t smem = analysis_smem(p, MODE);
+  auto k = analysis_kernel<MODE>;
   if (smem > 48 * 1024)
     SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<p->nm, 256, smem, s>>>(static_cast<const ShtView &>(*p), A, st, out);
+  k<<<p->nm, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
 
-static int c2r_exec(swx_sht p, int nf, double2 *in, double *out, cudaStream_t s) {
+static int c2r_exec(swx_sht p, int nlon, int nf, double2 *in, double *out, cudaStream_t s) {
   cufftHandle h;
-  int rc = get_plan(p, CUFFT_Z2D, nf * p->nlat, &h);
+  int rc = get_plan(p, CUFFT_Z2D, nlon, nf * p->nlat, &h);
   if (rc) return rc;
   cufftSetStream(h, s);
   if (cufftExecZ2D(h, (cufftDoubleComplex *)in, out) != CUFFT_SUCCESS)
@@ -660,9 +738,9 @@ static int c2r_exec(swx_sht p, int nf, double2 *in, double *out, cudaStream_t s)
   return SWX_OK;
 }
 
-static int r2c_exec(swx_sht p, int nf, double *in, double2 *out, cudaStream_t s) {
+static int r2c_exec(swx_sht p, int nlon, int nf, double *in, double2 *out, cudaStream_t s) {
   cufftHandle h;
-  int rc = get_plan(p, CUFFT_D2Z, nf * p->nlat, &h);
+  int rc = get_plan(p, CUFFT_D2Z, nlon, nf * p->nlat, &h);
   if (rc) return rc;
   cufftSetStream(h, s);
   if (cufftExecD2Z(h, in, (cufftDoubleComplex *)out) != CUFFT_SUCCESS)
@@ -670,11 +748,11 @@ static int r2c_exec(swx_sht p, int nf, double *in, double2 *out, cudaStream_t s)
   return SWX_OK;
 }
 
-static int zero_pad(swx_sht p, double2 *c2r, int nf, cudaStream_t s) {
-  const int w = p->nfreq - p->nm;
+static int zero_pad(swx_sht p, double2 *c2r, int nf, int nfreq, cudaStream_t s) {
+  const int w = nfreq - p->nm;
   if (w <= 0) return SWX_OK;
   dim3 g((w + 127) / 128, nf * p->nlat);
-  zero_pad_kernel<<<g, 128, 0, s>>>(c2r, nf * p->nlat, p->nfreq, p->nm);
+  zero_pad_kernel<<<g, 128, 0, s>>>(c2r, nf * p->nlat, nfreq, p->nm);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -685,6 +763,12 @@ static int check_ws(swx_sht p, void *ws, size_t bytes) {
   return SWX_OK;
 }
 
+static dim3 synth_grid(swx_sht p, int nz, int *threads) {
+  const int nt = std::min(256, ((p->nh + 31) / 32) * 32);
+  *threads = nt;
+  return dim3(p->nm, (p->nh + nt - 1) / nt, nz);
+}
+
 extern "C" int swx_sht_synthesis(swx_sht p, int n_fields, const swx_c128 *d_coeffs,
                                  double *d_grid, void *d_ws, size_t ws_bytes, void *stream) {
   int rc = check_ws(p, d_ws, ws_bytes);
@@ -692,11 +776,18 @@ extern "C" int swx_sht_synthesis(swx_sht p, int n_fields, const swx_c128 *d_coef
   if (n_fields < 1 || n_fields > 5) return fail(SWX_ERR_CONFIG, "1..5 fields per call");
   cudaStream_t s = (cudaStream_t)stream;
   ShtWs w = carve(p, d_ws);
-  if ((rc = zero_pad(p, w.c2r, n_fields, s))) return rc;
-  dim3 g(p->nm, (p->nh + 127) / 128, n_fields);
-  synth_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), (const double2 *)d_coeffs, n_fields, w.c2r);
+  if ((rc = zero_pad(p, w.c2r, n_fields, p->nfreq, s))) return rc;
+  SynthArgs a;
+  a.coef = (const double2 *)d_coeffs;
+  a.c2r = w.c2r;
+  a.lc = nullptr;
+  a.want_lc = 0;
+  a.nfreq = p->nfreq;
+  int nt;
+  dim3 g = synth_grid(p, n_fields, &nt);
+  synth_kernel<1><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
   SWX_LAUNCH_CHECK();
-  return c2r_exec(p, n_fields, w.c2r, d_grid, s);
+  return c2r_exec(p, p->nlon, n_fields, w.c2r, d_grid, s);
 }
 
 extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
@@ -706,34 +797,35 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
   if (n_fields < 1 || n_fields > 5) return fail(SWX_ERR_CONFIG, "1..5 fields per call");
   cudaStream_t s = (cudaStream_t)stream;
   ShtWs w = carve(p, d_ws);
-  // cuFFT D2Z does not modify its input for out-of-place 1-D real transforms,
-  // but copy anyway so the caller's grid is never touched
-  const size_t gbytes = (size_t)n_fields * p->nlat * p->nlon * sizeof(double);
-  SWX_CUDA_TRY(cudaMemcpyAsync(w.grid, d_grid, gbytes, cudaMemcpyDeviceToDevice, s));
-  if ((rc = r2c_exec(p, n_fields, w.grid, w.Q, s))) return rc;
-  dim3 g((p->nh + 127) / 128, p->nm);
-  prep_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, n_fields, w.A);
-  SWX_LAUNCH_CHECK();
   double2 *out = (double2 *)d_coeffs;
-  switch (n_fields) {
-    case 1: return launch_analysis<1, 0, 1>(p, w.A, w.st, out, s);
-    case 2: return launch_analysis<2, 0, 1>(p, w.A, w.st, out, s);
-    case 3: return launch_analysis<3, 0, 1>(p, w.A, w.st, out, s);
-    case 4: return launch_analysis<4, 0, 1>(p, w.A, w.st, out, s);
-    default: return launch_analysis<5, 0, 1>(p, w.A, w.st, out, s);
+  for (int f0 = 0; f0 < n_fields; f0 += 4) {
+    const int nf = std::min(4, n_fields - f0);
+    const size_t gbytes = (size_t)nf * p->nlat * p->nlon * sizeof(double);
+    // copy so the caller's grid is never touched by the transform
+    SWX_CUDA_TRY(cudaMemcpyAsync(w.grid, d_grid + (size_t)f0 * p->nlat * p->nlon, gbytes,
+                                 cudaMemcpyDeviceToDevice, s));
+    if ((rc = r2c_exec(p, p->nlon, nf, w.grid, w.Q, s))) return rc;
+    dim3 g((p->nhp + 127) / 128, p->nm);
+    prep_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, nf, w.A);
+    SWX_LAUNCH_CHECK();
+    if ((rc = launch_analysis<1>(p, w.A, out + (size_t)f0 * p->ncoef, nf, s))) return rc;
   }
+  return SWX_OK;
 }
 
-static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, cudaStream_t s) {
-  int rc = zero_pad(p, w.c2r, 4, s);
+static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, int nfreq,
+                       cudaStream_t s) {
+  int rc = zero_pad(p, w.c2r, 4, nfreq, s);
   if (rc) return rc;
   SynthArgs a;
-  a.state = state;
+  a.coef = state;
   a.c2r = w.c2r;
   a.lc = w.lc;
   a.want_lc = want_lc;
-  dim3 g(p->nm, (p->nh + 127) / 128);
-  synth_state_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), a);
+  a.nfreq = nfreq;
+  int nt;
+  dim3 g = synth_grid(p, 1, &nt);
+  synth_kernel<0><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -750,12 +842,44 @@ extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_d
   SWX_CUDA_TRY(cudaMemsetAsync(tmp, 0, nb, s));
   SWX_CUDA_TRY(cudaMemcpyAsync(tmp + p->ncoef, d_vort, nb, cudaMemcpyDeviceToDevice, s));
   SWX_CUDA_TRY(cudaMemcpyAsync(tmp + 2 * p->ncoef, d_div, nb, cudaMemcpyDeviceToDevice, s));
-  if ((rc = synth_state(p, tmp, w, 0, s))) return rc;
-  if ((rc = c2r_exec(p, 4, w.c2r, w.grid, s))) return rc;
+  if ((rc = synth_state(p, tmp, w, 0, p->nfreq, s))) return rc;
+  if ((rc = c2r_exec(p, p->nlon, 4, w.c2r, w.grid, s))) return rc;
   const size_t g = (size_t)p->nlat * p->nlon * sizeof(double);
   SWX_CUDA_TRY(cudaMemcpyAsync(d_u, w.grid, g, cudaMemcpyDeviceToDevice, s));
   SWX_CUDA_TRY(cudaMemcpyAsync(d_v, w.grid + (size_t)p->nlat * p->nlon, g,
                                cudaMemcpyDeviceToDevice, s));
+  return SWX_OK;
+}
+
+// the fused LC+N tendency; `ev` (7 events or null) brackets the stages
+static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *out, ShtWs &w,
+                         cudaStream_t s, cudaEvent_t *ev) {
+  int rc;
+  auto mark = [&](int k) {
+    if (ev) cudaEventRecord(ev[k], s);
+  };
+  mark(0);
+  if ((rc = synth_state(p, state, w, (atoms & SWX_TEND_LC) ? 1 : 0, p->nfreq_t, s))) return rc;
+  mark(1);
+  if (atoms & SWX_TEND_N) {
+    if ((rc = c2r_exec(p, p->nlon_t, 4, w.c2r, w.grid, s))) return rc;
+    mark(2);
+    const size_t npts = (size_t)p->nlat * p->nlon_t;
+    products_kernel<<<(unsigned)((npts + 255) / 256), 256, 0, s>>>(w.grid, npts);
+    SWX_LAUNCH_CHECK();
+    mark(3);
+    if ((rc = r2c_exec(p, p->nlon_t, 5, w.grid, w.Q, s))) return rc;
+  } else {
+    mark(2);
+    mark(3);
+  }
+  mark(4);
+  dim3 g((p->nhp + 127) / 128, p->nm);
+  prep_tend_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.lc, atoms, w.A);
+  SWX_LAUNCH_CHECK();
+  mark(5);
+  if ((rc = launch_analysis<0>(p, w.A, out, 3, s))) return rc;
+  mark(6);
   return SWX_OK;
 }
 
@@ -772,18 +896,7 @@ extern "C" int swx_sht_tendency(swx_sht p, int atoms, const swx_c128 *d_state,
     SWX_CUDA_TRY(cudaMemsetAsync(d_out, 0, 3 * (size_t)p->ncoef * sizeof(double2), s));
     return SWX_OK;
   }
-  if ((rc = synth_state(p, (const double2 *)d_state, w, (atoms & SWX_TEND_LC) ? 1 : 0, s))) return rc;
-  if (atoms & SWX_TEND_N) {
-    if ((rc = c2r_exec(p, 4, w.c2r, w.grid, s))) return rc;
-    const size_t npts = (size_t)p->nlat * p->nlon;
-    products_kernel<<<(unsigned)((npts + 255) / 256), 256, 0, s>>>(w.grid, npts);
-    SWX_LAUNCH_CHECK();
-    if ((rc = r2c_exec(p, 5, w.grid, w.Q, s))) return rc;
-  }
-  dim3 g((p->nh + 127) / 128, p->nm);
-  prep_tend_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.lc, atoms, w.A);
-  SWX_LAUNCH_CHECK();
-  return launch_analysis<kSerTendP, kSerTend - kSerTendP, 0>(p, w.A, w.st, (double2 *)d_out, s);
+  return tendency_impl(p, atoms, (const double2 *)d_state, (double2 *)d_out, w, s, nullptr);
 }
 
 extern "C" int swx_sht_tendency_profile(swx_sht p, int atoms, const swx_c128 *d_state,
@@ -798,29 +911,8 @@ extern "C" int swx_sht_tendency_profile(swx_sht p, int atoms, const swx_c128 *d_
   if (atoms <= 0) return fail(SWX_ERR_CONFIG, "profile needs a non-empty atom set");
   cudaEvent_t ev[7];
   for (int i = 0; i < 7; ++i) SWX_CUDA_TRY(cudaEventCreate(&ev[i]));
-  SWX_CUDA_TRY(cudaEventRecord(ev[0], s));
-  if ((rc = synth_state(p, (const double2 *)d_state, w, (atoms & SWX_TEND_LC) ? 1 : 0, s))) return rc;
-  SWX_CUDA_TRY(cudaEventRecord(ev[1], s));
-  const size_t npts = (size_t)p->nlat * p->nlon;
-  if (atoms & SWX_TEND_N) {
-    if ((rc = c2r_exec(p, 4, w.c2r, w.grid, s))) return rc;
-    SWX_CUDA_TRY(cudaEventRecord(ev[2], s));
-    products_kernel<<<(unsigned)((npts + 255) / 256), 256, 0, s>>>(w.grid, npts);
-    SWX_LAUNCH_CHECK();
-    SWX_CUDA_TRY(cudaEventRecord(ev[3], s));
-    if ((rc = r2c_exec(p, 5, w.grid, w.Q, s))) return rc;
-  } else {
-    SWX_CUDA_TRY(cudaEventRecord(ev[2], s));
-    SWX_CUDA_TRY(cudaEventRecord(ev[3], s));
-  }
-  SWX_CUDA_TRY(cudaEventRecord(ev[4], s));
-  dim3 g((p->nh + 127) / 128, p->nm);
-  prep_tend_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.lc, atoms, w.A);
-  SWX_LAUNCH_CHECK();
-  SWX_CUDA_TRY(cudaEventRecord(ev[5], s));
-  if ((rc = launch_analysis<kSerTendP, kSerTend - kSerTendP, 0>(p, w.A, w.st, (double2 *)d_out, s)))
-    return rc;
-  SWX_CUDA_TRY(cudaEventRecord(ev[6], s));
+  rc = tendency_impl(p, atoms, (const double2 *)d_state, (double2 *)d_out, w, s, ev);
+  if (rc) return rc;
   SWX_CUDA_TRY(cudaEventSynchronize(ev[6]));
   for (int i = 0; i < 6; ++i) {
     float ms = 0.f;

@@ -57,7 +57,7 @@ def to_device(packed: np.ndarray, device=None):
     import torch
 
     device = device or torch_device()
-    return torch.from_numpy(np.ascontiguousarray(packed, dtype=np.complex128)).to(device)
+    return torch.from_numpy(np.array(packed, dtype=np.complex128, copy=True)).to(device)
 
 
 def to_host(t) -> np.ndarray:
