@@ -51,59 +51,49 @@ static int next_pow2(int x) {
 // reduces it as a perfect binary tree; the xor-butterfly over lanes then
 // completes tree_sum's pairwise order (steppers.py:157-172).
 // =====================================================================
-template <int NRHS>
-struct LgAcc {
-  double2 v[NRHS][3];
+// Two modes of the same degree l per warp pass: every factor load from
+// shared memory feeds 2 x 5 complex MACs.
+struct Lg2 {
+  double2 a[3], b[3];  // [phi', vort, div] of mode a and mode b
 };
 
-template <int NRHS>
-__device__ __forceinline__ void lg_zero(LgAcc<NRHS> &a) {
+__device__ __forceinline__ void lg2_add(Lg2 &x, const Lg2 &y) {
 #pragma unroll
-  for (int r = 0; r < NRHS; ++r)
-#pragma unroll
-    for (int f = 0; f < 3; ++f) a.v[r][f] = make_double2(0.0, 0.0);
+  for (int f = 0; f < 3; ++f) {
+    x.a[f] = cadd(x.a[f], y.a[f]);
+    x.b[f] = cadd(x.b[f], y.b[f]);
+  }
 }
 
-template <int NRHS>
-__device__ __forceinline__ void lg_add(LgAcc<NRHS> &a, const LgAcc<NRHS> &b) {
-#pragma unroll
-  for (int r = 0; r < NRHS; ++r)
-#pragma unroll
-    for (int f = 0; f < 3; ++f) a.v[r][f] = cadd(a.v[r][f], b.v[r][f]);
-}
-
-template <int NRHS>
-struct LgTerm {
-  const double2 *fac;  // shared: [(r*4 + q) * Pp + slot], Pp = lanes*BPL
-  int Pp, lanes, lane;
-  double2 b[NRHS][3];
-  __device__ __forceinline__ void operator()(int t, LgAcc<NRHS> &out) const {
+struct LgTerm2 {
+  const double2 *A, *B, *C, *D;  // shared factor rows of one weight set, [t*lanes + lane]
+  int lanes, lane;
+  double2 ba[3], bb[3];          // right-hand sides of the two modes
+  __device__ __forceinline__ void operator()(int t, Lg2 &o) const {
     const int s = t * lanes + lane;  // slot of pole lane*BPL + t
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) {
-      const double2 A = fac[(r * 4 + 0) * Pp + s];
-      const double2 B = fac[(r * 4 + 1) * Pp + s];
-      const double2 C = fac[(r * 4 + 2) * Pp + s];
-      const double2 D = fac[(r * 4 + 3) * Pp + s];
-      out.v[r][0] = cfma(A, b[r][0], cmul(B, b[r][2]));
-      out.v[r][1] = cmul(D, b[r][1]);
-      out.v[r][2] = cfma(C, b[r][0], cmul(A, b[r][2]));
-    }
+    const double2 fa = A[s], fb = B[s], fc = C[s], fd = D[s];
+    o.a[0] = cfma(fa, ba[0], cmul(fb, ba[2]));
+    o.a[1] = cmul(fd, ba[1]);
+    o.a[2] = cfma(fc, ba[0], cmul(fa, ba[2]));
+    o.b[0] = cfma(fa, bb[0], cmul(fb, bb[2]));
+    o.b[1] = cmul(fd, bb[1]);
+    o.b[2] = cfma(fc, bb[0], cmul(fa, bb[2]));
   }
 };
 
-template <int B, int NRHS>
-__device__ __forceinline__ void lg_tree(LgAcc<NRHS> &out, int t0,
-                                        const LgTerm<NRHS> &term) {
+template <int B>
+__device__ __forceinline__ void lg_tree(Lg2 &out, int t0, const LgTerm2 &term) {
   if constexpr (B == 1) {
     term(t0, out);
   } else {
-    LgAcc<NRHS> right;
-    lg_tree<B / 2, NRHS>(out, t0, term);
-    lg_tree<B / 2, NRHS>(right, t0 + B / 2, term);
-    lg_add(out, right);
+    Lg2 right;
+    lg_tree<B / 2>(out, t0, term);
+    lg_tree<B / 2>(right, t0 + B / 2, term);
+    lg2_add(out, right);
   }
 }
+
+constexpr int kLgModes = 32;  // modes (one l, consecutive m) per CTA
 
 template <int NRHS, int BPL>
 __global__ void __launch_bounds__(256) rexi_lg_kernel(
@@ -112,14 +102,21 @@ __global__ void __launch_bounds__(256) rexi_lg_kernel(
     int lanes, int trunc, int ncoef, double dt, double phibar,
     const double *__restrict__ lconst, const int4 *__restrict__ sched,
     int realify, double2 *__restrict__ out) {
-  extern __shared__ double2 fac[];  // NRHS*4*Pp
+  extern __shared__ double2 fac[];  // [NRHS][4][Pp] then rhs stage [kLgModes][NRHS][3]
   const int Pp = lanes * BPL;
+  double2 *bs = fac + (size_t)NRHS * 4 * Pp;
   const int4 w = sched[blockIdx.x];
-  const int l = w.x;
+  const int l = w.x, m0 = w.y, nmodes = w.z - w.y;
   const double kap = lconst[l];
   const double g = lconst[(trunc + 1) + l];  // dt^2 phibar kappa
   const double dtpb = dt * phibar;
   const double mdtk = -dt * kap;
+  // stage the right-hand sides of this CTA's modes (one latency, not one per mode)
+  for (int t = threadIdx.x; t < nmodes * NRHS * 3; t += blockDim.x) {
+    const int mi = t / (NRHS * 3), rf = t - mi * NRHS * 3;
+    const int m = m0 + mi;
+    bs[t] = rhs[(size_t)rf * ncoef + col_offset(trunc, m) + (l - m)];
+  }
   for (int i = threadIdx.x; i < Pp; i += blockDim.x) {
     const int lane_of = i / BPL, t = i - lane_of * BPL;
     const int s = t * lanes + lane_of;
@@ -135,7 +132,6 @@ __global__ void __launch_bounds__(256) rexi_lg_kernel(
     const double2 q2 = cscale(dtpb, idet);
     const double2 q3 = cscale(mdtk, idet);
     const double2 q4 = crecip(a);
-    // slot layout [t][lane]: lane j's t-th pole; a warp reads 32 consecutive slots
 #pragma unroll
     for (int r = 0; r < NRHS; ++r) {
       const double2 b = beta[r * beta_stride + pole0 + i];
@@ -148,41 +144,50 @@ __global__ void __launch_bounds__(256) rexi_lg_kernel(
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  LgTerm<NRHS> term;
-  term.fac = fac;
-  term.Pp = Pp;
+  LgTerm2 term;
   term.lanes = lanes;
   term.lane = lane;
-  for (int m = w.y + warp; m < w.z; m += nwarps) {
-    const int idx = col_offset(trunc, m) + (l - m);
+  for (int ia = warp; ia < nmodes; ia += 2 * nwarps) {
+    const int ib = ia + nwarps;
+    const bool hb = ib < nmodes;
+#pragma unroll 1
+    for (int r = 0; r < NRHS; ++r) {
+      term.A = fac + (r * 4 + 0) * Pp;
+      term.B = fac + (r * 4 + 1) * Pp;
+      term.C = fac + (r * 4 + 2) * Pp;
+      term.D = fac + (r * 4 + 3) * Pp;
 #pragma unroll
-    for (int r = 0; r < NRHS; ++r)
+      for (int f = 0; f < 3; ++f) {
+        term.ba[f] = bs[(ia * NRHS + r) * 3 + f];
+        term.bb[f] = hb ? bs[(ib * NRHS + r) * 3 + f] : make_double2(0.0, 0.0);
+      }
+      Lg2 acc;
+      if (lane < lanes) {
+        lg_tree<BPL>(acc, 0, term);
+      } else {
 #pragma unroll
-      for (int f = 0; f < 3; ++f)
-        term.b[r][f] = rhs[(size_t)(r * 3 + f) * ncoef + idx];
-    LgAcc<NRHS> acc;
-    if (lane < lanes) {
-      lg_tree<BPL, NRHS>(acc, 0, term);
-    } else {
-      lg_zero(acc);
-    }
+        for (int f = 0; f < 3; ++f) acc.a[f] = acc.b[f] = make_double2(0.0, 0.0);
+      }
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r)
-#pragma unroll
-        for (int f = 0; f < 3; ++f)
-          acc.v[r][f] = cadd(acc.v[r][f], shfl_xor2(acc.v[r][f], o));
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r)
+      for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
-          double2 v = acc.v[r][f];
-          if (realify && m == 0) v.y = 0.0;
-          out[(size_t)(r * 3 + f) * ncoef + idx] = v;
+          acc.a[f] = cadd(acc.a[f], shfl_xor2(acc.a[f], o));
+          acc.b[f] = cadd(acc.b[f], shfl_xor2(acc.b[f], o));
         }
+      }
+      if (lane < 3) {  // lanes 0..2 write field f = lane of both modes
+        const int f = lane;
+        double2 va = f == 0 ? acc.a[0] : (f == 1 ? acc.a[1] : acc.a[2]);
+        double2 vb = f == 0 ? acc.b[0] : (f == 1 ? acc.b[1] : acc.b[2]);
+        const int ma = m0 + ia, mb = m0 + ib;
+        if (realify && ma == 0) va.y = 0.0;
+        out[(size_t)(r * 3 + f) * ncoef + col_offset(trunc, ma) + (l - ma)] = va;
+        if (hb) {
+          if (realify && mb == 0) vb.y = 0.0;
+          out[(size_t)(r * 3 + f) * ncoef + col_offset(trunc, mb) + (l - mb)] = vb;
+        }
+      }
     }
   }
 }
@@ -567,7 +572,8 @@ extern "C" int swx_solver_create(swx_solver *out, int group, int trunc,
   // lg schedule: CTAs of (l, m0, m1) with at most 32 modes each
   std::vector<int4> sched;
   for (int l = n - 1; l >= 0; --l)
-    for (int m0 = 0; m0 <= l; m0 += 32) sched.push_back(make_int4(l, m0, std::min(l + 1, m0 + 32), 0));
+    for (int m0 = 0; m0 <= l; m0 += kLgModes)
+      sched.push_back(make_int4(l, m0, std::min(l + 1, m0 + kLgModes), 0));
   s->n_sched = (int)sched.size();
   if (e == cudaSuccess) e = cudaMalloc(&s->d_sched, sizeof(int4) * sched.size());
   if (e == cudaSuccess)
@@ -720,7 +726,8 @@ static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
                      cudaStream_t st) {
   const int bpl = next_pow2((P + 31) / 32);
   const int lanes = bpl == 1 ? std::min(32, P) : 32;
-  const size_t smem = (size_t)NRHS * 4 * lanes * bpl * sizeof(double2);
+  const size_t smem = ((size_t)NRHS * 4 * lanes * bpl + (size_t)kLgModes * NRHS * 3) *
+                      sizeof(double2);
 #define SWX_LG_CASE(B)                                                                 \
   case B: {                                                                            \
     auto k = rexi_lg_kernel<NRHS, B>;                                                  \
