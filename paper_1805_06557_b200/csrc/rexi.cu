@@ -47,82 +47,117 @@ static int next_pow2(int x) {
 //   det = a^2 + dt^2 phibar kappa            (solvers.py:93-107)
 // then every mode does 5 complex MACs per pole:
 //   phi += A bphi + B bdiv, div += C bphi + A bdiv, vort += D bvort.
-// Lane j of a warp owns the contiguous pole block [j*BPL, (j+1)*BPL) and
-// reduces it as a perfect binary tree; the xor-butterfly over lanes then
-// completes tree_sum's pairwise order (steppers.py:157-172).
+// The pole sum is the perfect binary tree of tree_sum's pairwise order
+// (steppers.py:157-172) over the launch's pole block.
 // =====================================================================
-// Two modes of the same degree l per warp pass: every factor load from
-// shared memory feeds 2 x 5 complex MACs.
-struct Lg2 {
-  double2 a[3], b[3];  // [phi', vort, div] of mode a and mode b
+// Mapping: one lane per mode (l fixed per CTA, m = lane + 32*warp + m0), each
+// lane walks all NP poles of the launch as a perfect binary tree (fully
+// unrolled, depth-first: log2(NP) live partial sums), so the per-pole factor
+// reads are warp-wide shared-memory broadcasts and no shuffles are needed.
+// (phi', div) and vort are reduced in two passes to halve the live state.
+struct PhiDiv {
+  double2 p, d;
 };
 
-__device__ __forceinline__ void lg2_add(Lg2 &x, const Lg2 &y) {
-#pragma unroll
-  for (int f = 0; f < 3; ++f) {
-    x.a[f] = cadd(x.a[f], y.a[f]);
-    x.b[f] = cadd(x.b[f], y.b[f]);
-  }
-}
-
-struct LgTerm2 {
-  const double2 *A, *B, *C, *D;  // shared factor rows of one weight set, [t*lanes + lane]
-  int lanes, lane;
-  double2 ba[3], bb[3];          // right-hand sides of the two modes
-  __device__ __forceinline__ void operator()(int t, Lg2 &o) const {
-    const int s = t * lanes + lane;  // slot of pole lane*BPL + t
-    const double2 fa = A[s], fb = B[s], fc = C[s], fd = D[s];
-    o.a[0] = cfma(fa, ba[0], cmul(fb, ba[2]));
-    o.a[1] = cmul(fd, ba[1]);
-    o.a[2] = cfma(fc, ba[0], cmul(fa, ba[2]));
-    o.b[0] = cfma(fa, bb[0], cmul(fb, bb[2]));
-    o.b[1] = cmul(fd, bb[1]);
-    o.b[2] = cfma(fc, bb[0], cmul(fa, bb[2]));
-  }
-};
-
-template <int B>
-__device__ __forceinline__ void lg_tree(Lg2 &out, int t0, const LgTerm2 &term) {
-  if constexpr (B == 1) {
-    term(t0, out);
+template <int NP>
+__device__ __forceinline__ PhiDiv tree_pd(const double2 *__restrict__ A, const double2 *__restrict__ B,
+                                          const double2 *__restrict__ C, int t0, double2 bp,
+                                          double2 bd) {
+  if constexpr (NP == 1) {
+    const double2 fa = A[t0], fb = B[t0], fc = C[t0];
+    PhiDiv o;
+    o.p = cfma(fa, bp, cmul(fb, bd));  // (a phi + dt phibar div) / det, beta folded
+    o.d = cfma(fc, bp, cmul(fa, bd));  // (-dt kappa phi + a div) / det
+    return o;
   } else {
-    Lg2 right;
-    lg_tree<B / 2>(out, t0, term);
-    lg_tree<B / 2>(right, t0 + B / 2, term);
-    lg2_add(out, right);
+    PhiDiv x = tree_pd<NP / 2>(A, B, C, t0, bp, bd);
+    const PhiDiv y = tree_pd<NP / 2>(A, B, C, t0 + NP / 2, bp, bd);
+    x.p = cadd(x.p, y.p);
+    x.d = cadd(x.d, y.d);
+    return x;
   }
 }
 
-constexpr int kLgModes = 32;  // modes (one l, consecutive m) per CTA
+template <int NP>
+__device__ __forceinline__ double2 tree_z(const double2 *__restrict__ D, int t0, double2 bz) {
+  if constexpr (NP == 1) {
+    return cmul(D[t0], bz);  // vort / a, beta folded
+  } else {
+    const double2 x = tree_z<NP / 2>(D, t0, bz);
+    return cadd(x, tree_z<NP / 2>(D, t0 + NP / 2, bz));
+  }
+}
 
-template <int NRHS, int BPL>
-__global__ void __launch_bounds__(256) rexi_lg_kernel(
+constexpr int kLgModes = 64;   // modes (one l, consecutive m) per CTA = 2 warps
+constexpr int kLgLevels = 6;   // up to 64 leaf blocks (1024 poles) per launch
+
+// Perfect tree over NB (power of two) consecutive leaf subtrees of LEAF
+// poles: a binary counter whose partial sums live in a statically indexed
+// register stack (the first zero bit of the block index is where a subtree
+// waits for its right sibling).
+template <int LEAF>
+__device__ __forceinline__ PhiDiv pole_tree_pd(const double2 *A, const double2 *B,
+                                               const double2 *C, int nb, double2 bp, double2 bd) {
+  PhiDiv stk[kLgLevels];
+  PhiDiv v;
+  for (int blk = 0; blk < nb; ++blk) {
+    v = tree_pd<LEAF>(A, B, C, blk * LEAF, bp, bd);
+    bool done = false;
+#pragma unroll
+    for (int lv = 0; lv < kLgLevels; ++lv) {
+      if (!done) {
+        if ((blk >> lv) & 1) {
+          v.p = cadd(stk[lv].p, v.p);
+          v.d = cadd(stk[lv].d, v.d);
+        } else {
+          stk[lv] = v;
+          done = true;
+        }
+      }
+    }
+  }
+  return v;  // blk = nb-1 has all low bits set: v is the full tree
+}
+
+template <int LEAF>
+__device__ __forceinline__ double2 pole_tree_z(const double2 *D, int nb, double2 bz) {
+  double2 stk[kLgLevels];
+  double2 v;
+  for (int blk = 0; blk < nb; ++blk) {
+    v = tree_z<LEAF>(D, blk * LEAF, bz);
+    bool done = false;
+#pragma unroll
+    for (int lv = 0; lv < kLgLevels; ++lv) {
+      if (!done) {
+        if ((blk >> lv) & 1) {
+          v = cadd(stk[lv], v);
+        } else {
+          stk[lv] = v;
+          done = true;
+        }
+      }
+    }
+  }
+  return v;
+}
+
+template <int NRHS, int LEAF>
+__global__ void __launch_bounds__(kLgModes) rexi_lg_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
-    const double2 *__restrict__ beta, int beta_stride, int pole0, int P,
-    int lanes, int trunc, int ncoef, double dt, double phibar,
-    const double *__restrict__ lconst, const int4 *__restrict__ sched,
-    int realify, double2 *__restrict__ out) {
-  extern __shared__ double2 fac[];  // [NRHS][4][Pp] then rhs stage [kLgModes][NRHS][3]
-  const int Pp = lanes * BPL;
-  double2 *bs = fac + (size_t)NRHS * 4 * Pp;
+    const double2 *__restrict__ beta, int beta_stride, int pole0, int P, int np, int trunc,
+    int ncoef, double dt, double phibar, const double *__restrict__ lconst,
+    const int4 *__restrict__ sched, int realify, double2 *__restrict__ out) {
+  extern __shared__ double2 fac[];  // [NRHS][4][np]
   const int4 w = sched[blockIdx.x];
-  const int l = w.x, m0 = w.y, nmodes = w.z - w.y;
+  const int l = w.x, m0 = w.y, m1 = w.z;
   const double kap = lconst[l];
   const double g = lconst[(trunc + 1) + l];  // dt^2 phibar kappa
   const double dtpb = dt * phibar;
   const double mdtk = -dt * kap;
-  // stage the right-hand sides of this CTA's modes (one latency, not one per mode)
-  for (int t = threadIdx.x; t < nmodes * NRHS * 3; t += blockDim.x) {
-    const int mi = t / (NRHS * 3), rf = t - mi * NRHS * 3;
-    const int m = m0 + mi;
-    bs[t] = rhs[(size_t)rf * ncoef + col_offset(trunc, m) + (l - m)];
-  }
-  for (int i = threadIdx.x; i < Pp; i += blockDim.x) {
-    const int lane_of = i / BPL, t = i - lane_of * BPL;
-    const int s = t * lanes + lane_of;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
     if (i >= P) {  // padding pole: contributes exact zeros
 #pragma unroll
-      for (int q = 0; q < NRHS * 4; ++q) fac[q * Pp + s] = make_double2(0.0, 0.0);
+      for (int q = 0; q < NRHS * 4; ++q) fac[q * np + i] = make_double2(0.0, 0.0);
       continue;
     }
     const double2 a = alpha[pole0 + i];
@@ -135,60 +170,30 @@ __global__ void __launch_bounds__(256) rexi_lg_kernel(
 #pragma unroll
     for (int r = 0; r < NRHS; ++r) {
       const double2 b = beta[r * beta_stride + pole0 + i];
-      fac[(r * 4 + 0) * Pp + s] = cmul(b, q1);
-      fac[(r * 4 + 1) * Pp + s] = cmul(b, q2);
-      fac[(r * 4 + 2) * Pp + s] = cmul(b, q3);
-      fac[(r * 4 + 3) * Pp + s] = cmul(b, q4);
+      fac[(r * 4 + 0) * np + i] = cmul(b, q1);
+      fac[(r * 4 + 1) * np + i] = cmul(b, q2);
+      fac[(r * 4 + 2) * np + i] = cmul(b, q3);
+      fac[(r * 4 + 3) * np + i] = cmul(b, q4);
     }
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  LgTerm2 term;
-  term.lanes = lanes;
-  term.lane = lane;
-  for (int ia = warp; ia < nmodes; ia += 2 * nwarps) {
-    const int ib = ia + nwarps;
-    const bool hb = ib < nmodes;
+  const int m = m0 + threadIdx.x;
+  if (m >= m1) return;
+  const size_t idx = (size_t)col_offset(trunc, m) + (l - m);
+  const int nb = np / LEAF;
 #pragma unroll 1
-    for (int r = 0; r < NRHS; ++r) {
-      term.A = fac + (r * 4 + 0) * Pp;
-      term.B = fac + (r * 4 + 1) * Pp;
-      term.C = fac + (r * 4 + 2) * Pp;
-      term.D = fac + (r * 4 + 3) * Pp;
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        term.ba[f] = bs[(ia * NRHS + r) * 3 + f];
-        term.bb[f] = hb ? bs[(ib * NRHS + r) * 3 + f] : make_double2(0.0, 0.0);
-      }
-      Lg2 acc;
-      if (lane < lanes) {
-        lg_tree<BPL>(acc, 0, term);
-      } else {
-#pragma unroll
-        for (int f = 0; f < 3; ++f) acc.a[f] = acc.b[f] = make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-        for (int f = 0; f < 3; ++f) {
-          acc.a[f] = cadd(acc.a[f], shfl_xor2(acc.a[f], o));
-          acc.b[f] = cadd(acc.b[f], shfl_xor2(acc.b[f], o));
-        }
-      }
-      if (lane < 3) {  // lanes 0..2 write field f = lane of both modes
-        const int f = lane;
-        double2 va = f == 0 ? acc.a[0] : (f == 1 ? acc.a[1] : acc.a[2]);
-        double2 vb = f == 0 ? acc.b[0] : (f == 1 ? acc.b[1] : acc.b[2]);
-        const int ma = m0 + ia, mb = m0 + ib;
-        if (realify && ma == 0) va.y = 0.0;
-        out[(size_t)(r * 3 + f) * ncoef + col_offset(trunc, ma) + (l - ma)] = va;
-        if (hb) {
-          if (realify && mb == 0) vb.y = 0.0;
-          out[(size_t)(r * 3 + f) * ncoef + col_offset(trunc, mb) + (l - mb)] = vb;
-        }
-      }
-    }
+  for (int r = 0; r < NRHS; ++r) {
+    const double2 *F = fac + (size_t)r * 4 * np;
+    const double2 bp = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
+    const double2 bz = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
+    const double2 bd = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
+    const PhiDiv pd = pole_tree_pd<LEAF>(F, F + np, F + 2 * np, nb, bp, bd);
+    double2 z = pole_tree_z<LEAF>(F + 3 * np, nb, bz);
+    double2 vp = pd.p, vd = pd.d;
+    if (realify && m == 0) vp.y = z.y = vd.y = 0.0;
+    out[(size_t)(r * 3 + 0) * ncoef + idx] = vp;
+    out[(size_t)(r * 3 + 1) * ncoef + idx] = z;
+    out[(size_t)(r * 3 + 2) * ncoef + idx] = vd;
   }
 }
 
@@ -682,7 +687,7 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
 }
 
 // ---- launch geometry helpers
-static constexpr int kLgMaxP = 512;  // poles per lg launch (smem = NRHS*64*P bytes)
+static constexpr int kLgMaxP = 1024;  // poles per lg launch (smem = NRHS*64*P bytes)
 
 static size_t l_smem_bytes(int nrhs) {
   return (size_t)kLWarps * kFlush * nrhs * 2 * 32 * sizeof(double2);
@@ -724,29 +729,28 @@ template <int NRHS>
 static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
                      int pole0, int P, int realify, double2 *out,
                      cudaStream_t st) {
-  const int bpl = next_pow2((P + 31) / 32);
-  const int lanes = bpl == 1 ? std::min(32, P) : 32;
-  const size_t smem = ((size_t)NRHS * 4 * lanes * bpl + (size_t)kLgModes * NRHS * 3) *
-                      sizeof(double2);
-#define SWX_LG_CASE(B)                                                                 \
-  case B: {                                                                            \
-    auto k = rexi_lg_kernel<NRHS, B>;                                                  \
-    if (smem > 48 * 1024)                                                              \
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                        (int)smem));                                   \
-    k<<<s->n_sched, 256, smem, st>>>(rhs, s->d_alpha, betas, s->n_poles, pole0, P,     \
-                                     lanes, s->trunc, s->ncoef, s->dt, s->phibar,      \
-                                     s->d_lconst, s->d_sched, realify, out);           \
-    break;                                                                             \
+  const int np = next_pow2(P);
+  const int leaf = std::min(np, 16);
+  const size_t smem = (size_t)NRHS * 4 * np * sizeof(double2);
+#define SWX_LG_CASE(LV)                                                                     \
+  case LV: {                                                                                \
+    auto k = rexi_lg_kernel<NRHS, LV>;                                                      \
+    if (smem > 48 * 1024)                                                                   \
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                        (int)smem));                                        \
+    k<<<s->n_sched, kLgModes, smem, st>>>(rhs, s->d_alpha, betas, s->n_poles, pole0, P, np, \
+                                          s->trunc, s->ncoef, s->dt, s->phibar,             \
+                                          s->d_lconst, s->d_sched, realify, out);           \
+    break;                                                                                  \
   }
-  switch (bpl) {
+  switch (leaf) {
     SWX_LG_CASE(1)
     SWX_LG_CASE(2)
     SWX_LG_CASE(4)
     SWX_LG_CASE(8)
     SWX_LG_CASE(16)
     default:
-      return fail(SWX_ERR_CONFIG, "lg pole chunk too large");
+      return fail(SWX_ERR_CONFIG, "bad lg leaf size");
   }
 #undef SWX_LG_CASE
   SWX_LAUNCH_CHECK();
