@@ -291,6 +291,7 @@ def main():
         acc = np.zeros(7)
         for _ in range(reps):
             flush.zero_()
+            torch.cuda.synchronize()
             ctypes_buf = np.zeros(7, dtype=np.float64)
             _lib.check(lib.swx_sht_tendency_profile(
                 plan._h, 3, eng.u.data_ptr(), eng.na.data_ptr(), plan.workspace.data_ptr(),
@@ -301,10 +302,14 @@ def main():
             breakdown[n] = {"ms_per_launch": v, "launches_per_step": 2}
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
+        busy = torch.empty(1024 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
         def timed(fn):
+            # a 1 GiB memset ahead of e0 keeps the GPU busy while Python issues
+            # fn(), so the event interval is device time only (and L2 is cold)
             tt = []
             for _ in range(reps):
-                flush.zero_()
+                busy.zero_()
                 e0.record()
                 fn()
                 e1.record()

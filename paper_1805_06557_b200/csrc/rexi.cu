@@ -50,18 +50,17 @@ static int next_pow2(int x) {
 // The pole sum is the perfect binary tree of tree_sum's pairwise order
 // (steppers.py:157-172) over the launch's pole block.
 // =====================================================================
-// Mapping: one lane per mode (l fixed per CTA, m = lane + 32*warp + m0), each
-// lane walks all NP poles of the launch as a perfect binary tree (fully
-// unrolled, depth-first: log2(NP) live partial sums), so the per-pole factor
-// reads are warp-wide shared-memory broadcasts and no shuffles are needed.
-// (phi', div) and vort are reduced in two passes to halve the live state.
+// Mapping: a mode is owned by LPM lanes (l fixed per CTA), each walking its
+// pole block as a perfect binary tree; the per-pole factor reads are
+// shared-memory broadcasts within the lane group.  (phi', div) and vort are
+// reduced in two passes to halve the live state.
 struct PhiDiv {
   double2 p, d;
 };
 
 template <int NP>
 __device__ __forceinline__ PhiDiv tree_pd(const double2 *__restrict__ A, const double2 *__restrict__ B,
-                                          const double2 *__restrict__ C, int t0, double2 bp,
+                                          const double2 *__restrict__ C, int t0, int st, double2 bp,
                                           double2 bd) {
   if constexpr (NP == 1) {
     const double2 fa = A[t0], fb = B[t0], fc = C[t0];
@@ -70,8 +69,8 @@ __device__ __forceinline__ PhiDiv tree_pd(const double2 *__restrict__ A, const d
     o.d = cfma(fc, bp, cmul(fa, bd));  // (-dt kappa phi + a div) / det
     return o;
   } else {
-    PhiDiv x = tree_pd<NP / 2>(A, B, C, t0, bp, bd);
-    const PhiDiv y = tree_pd<NP / 2>(A, B, C, t0 + NP / 2, bp, bd);
+    PhiDiv x = tree_pd<NP / 2>(A, B, C, t0, st, bp, bd);
+    const PhiDiv y = tree_pd<NP / 2>(A, B, C, t0 + (NP / 2) * st, st, bp, bd);
     x.p = cadd(x.p, y.p);
     x.d = cadd(x.d, y.d);
     return x;
@@ -79,29 +78,31 @@ __device__ __forceinline__ PhiDiv tree_pd(const double2 *__restrict__ A, const d
 }
 
 template <int NP>
-__device__ __forceinline__ double2 tree_z(const double2 *__restrict__ D, int t0, double2 bz) {
+__device__ __forceinline__ double2 tree_z(const double2 *__restrict__ D, int t0, int st, double2 bz) {
   if constexpr (NP == 1) {
     return cmul(D[t0], bz);  // vort / a, beta folded
   } else {
-    const double2 x = tree_z<NP / 2>(D, t0, bz);
-    return cadd(x, tree_z<NP / 2>(D, t0 + NP / 2, bz));
+    const double2 x = tree_z<NP / 2>(D, t0, st, bz);
+    return cadd(x, tree_z<NP / 2>(D, t0 + (NP / 2) * st, st, bz));
   }
 }
 
-constexpr int kLgModes = 64;   // modes (one l, consecutive m) per CTA = 2 warps
-constexpr int kLgLevels = 6;   // up to 64 leaf blocks (1024 poles) per launch
+constexpr int kLgLevels = 3;  // up to 8 leaf blocks per lane (np <= 512, 8 lanes per mode, leaf 8)
 
 // Perfect tree over NB (power of two) consecutive leaf subtrees of LEAF
 // poles: a binary counter whose partial sums live in a statically indexed
 // register stack (the first zero bit of the block index is where a subtree
-// waits for its right sibling).
+// waits for its right sibling).  Pole t of this lane's block lives at
+// factor slot t*LPM + q (interleaved so the LPM lane groups of a warp read
+// distinct banks).
 template <int LEAF>
 __device__ __forceinline__ PhiDiv pole_tree_pd(const double2 *A, const double2 *B,
-                                               const double2 *C, int nb, double2 bp, double2 bd) {
+                                               const double2 *C, int nb, int lpm, double2 bp,
+                                               double2 bd) {
   PhiDiv stk[kLgLevels];
   PhiDiv v;
   for (int blk = 0; blk < nb; ++blk) {
-    v = tree_pd<LEAF>(A, B, C, blk * LEAF, bp, bd);
+    v = tree_pd<LEAF>(A, B, C, blk * LEAF * lpm, lpm, bp, bd);
     bool done = false;
 #pragma unroll
     for (int lv = 0; lv < kLgLevels; ++lv) {
@@ -120,11 +121,11 @@ __device__ __forceinline__ PhiDiv pole_tree_pd(const double2 *A, const double2 *
 }
 
 template <int LEAF>
-__device__ __forceinline__ double2 pole_tree_z(const double2 *D, int nb, double2 bz) {
+__device__ __forceinline__ double2 pole_tree_z(const double2 *D, int nb, int lpm, double2 bz) {
   double2 stk[kLgLevels];
   double2 v;
   for (int blk = 0; blk < nb; ++blk) {
-    v = tree_z<LEAF>(D, blk * LEAF, bz);
+    v = tree_z<LEAF>(D, blk * LEAF * lpm, lpm, bz);
     bool done = false;
 #pragma unroll
     for (int lv = 0; lv < kLgLevels; ++lv) {
@@ -141,59 +142,90 @@ __device__ __forceinline__ double2 pole_tree_z(const double2 *D, int nb, double2
   return v;
 }
 
-template <int NRHS, int LEAF>
-__global__ void __launch_bounds__(kLgModes) rexi_lg_kernel(
-    const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
-    const double2 *__restrict__ beta, int beta_stride, int pole0, int P, int np, int trunc,
-    int ncoef, double dt, double phibar, const double *__restrict__ lconst,
-    const int4 *__restrict__ sched, int realify, double2 *__restrict__ out) {
-  extern __shared__ double2 fac[];  // [NRHS][4][np]
-  const int4 w = sched[blockIdx.x];
-  const int l = w.x, m0 = w.y, m1 = w.z;
+// factor table fac[l][r][q][np] (q = A, B, C, D with beta folded in), poles
+// beyond P zero (solvers.py:93-107 with the reciprocals hoisted per (n, l))
+template <int NRHS>
+__global__ void lg_factor_kernel(const double2 *__restrict__ alpha, const double2 *__restrict__ beta,
+                                 int beta_stride, int pole0, int P, int np, int trunc, double dt,
+                                 double phibar, const double *__restrict__ lconst,
+                                 double2 *__restrict__ fac) {
+  const int l = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  double2 *F = fac + (size_t)l * NRHS * 4 * np;
+  if (i >= P) {
+#pragma unroll
+    for (int q = 0; q < NRHS * 4; ++q) F[(size_t)q * np + i] = make_double2(0.0, 0.0);
+    return;
+  }
   const double kap = lconst[l];
   const double g = lconst[(trunc + 1) + l];  // dt^2 phibar kappa
-  const double dtpb = dt * phibar;
-  const double mdtk = -dt * kap;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) {
-    if (i >= P) {  // padding pole: contributes exact zeros
+  const double2 a = alpha[pole0 + i];
+  const double2 det = make_double2(a.x * a.x - a.y * a.y + g, 2.0 * a.x * a.y);
+  const double2 idet = crecip(det);
+  const double2 q1 = cmul(a, idet);
+  const double2 q2 = cscale(dt * phibar, idet);
+  const double2 q3 = cscale(-dt * kap, idet);
+  const double2 q4 = crecip(a);
 #pragma unroll
-      for (int q = 0; q < NRHS * 4; ++q) fac[q * np + i] = make_double2(0.0, 0.0);
-      continue;
-    }
-    const double2 a = alpha[pole0 + i];
-    const double2 det = make_double2(a.x * a.x - a.y * a.y + g, 2.0 * a.x * a.y);
-    const double2 idet = crecip(det);
-    const double2 q1 = cmul(a, idet);
-    const double2 q2 = cscale(dtpb, idet);
-    const double2 q3 = cscale(mdtk, idet);
-    const double2 q4 = crecip(a);
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) {
-      const double2 b = beta[r * beta_stride + pole0 + i];
-      fac[(r * 4 + 0) * np + i] = cmul(b, q1);
-      fac[(r * 4 + 1) * np + i] = cmul(b, q2);
-      fac[(r * 4 + 2) * np + i] = cmul(b, q3);
-      fac[(r * 4 + 3) * np + i] = cmul(b, q4);
-    }
+  for (int r = 0; r < NRHS; ++r) {
+    const double2 b = beta[r * beta_stride + pole0 + i];
+    F[(size_t)(r * 4 + 0) * np + i] = cmul(b, q1);
+    F[(size_t)(r * 4 + 1) * np + i] = cmul(b, q2);
+    F[(size_t)(r * 4 + 2) * np + i] = cmul(b, q3);
+    F[(size_t)(r * 4 + 3) * np + i] = cmul(b, q4);
+  }
+}
+
+// One CTA = 4 warps = (one degree l, 4*32/LPM consecutive m).  A mode is
+// owned by LPM adjacent lanes, lane q of the group reducing the pole block
+// [q*np/LPM, (q+1)*np/LPM) as a perfect tree; an xor butterfly inside the
+// group completes tree_sum's order over the launch's np poles.
+template <int NRHS, int LEAF>
+__global__ void __launch_bounds__(128) rexi_lg_kernel(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int np, int lpm,
+    int trunc, int ncoef, const int4 *__restrict__ sched, int realify,
+    double2 *__restrict__ out) {
+  extern __shared__ double2 fac[];  // [NRHS][4][np] interleaved (t*LPM + q)
+  const int4 w = sched[blockIdx.x];
+  const int l = w.x, m0 = w.y, m1 = w.z;
+  const int ppl = np / lpm;  // poles per lane
+  const double2 *src = fac_g + (size_t)l * NRHS * 4 * np;
+  for (int i = threadIdx.x; i < NRHS * 4 * np; i += blockDim.x) {
+    const int row = i / np, pole = i - row * np;
+    const int q = pole / ppl, t = pole - q * ppl;
+    fac[row * np + t * lpm + q] = src[i];
   }
   __syncthreads();
-  const int m = m0 + threadIdx.x;
-  if (m >= m1) return;
-  const size_t idx = (size_t)col_offset(trunc, m) + (l - m);
-  const int nb = np / LEAF;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mpw = 32 / lpm;
+  const int q = lane % lpm;
+  const int m = m0 + warp * mpw + lane / lpm;
+  const bool has = m < m1;
+  const size_t idx = has ? (size_t)col_offset(trunc, m) + (l - m) : 0;
+  const int nb = ppl / LEAF;
 #pragma unroll 1
   for (int r = 0; r < NRHS; ++r) {
-    const double2 *F = fac + (size_t)r * 4 * np;
-    const double2 bp = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
-    const double2 bz = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
-    const double2 bd = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
-    const PhiDiv pd = pole_tree_pd<LEAF>(F, F + np, F + 2 * np, nb, bp, bd);
-    double2 z = pole_tree_z<LEAF>(F + 3 * np, nb, bz);
-    double2 vp = pd.p, vd = pd.d;
-    if (realify && m == 0) vp.y = z.y = vd.y = 0.0;
-    out[(size_t)(r * 3 + 0) * ncoef + idx] = vp;
-    out[(size_t)(r * 3 + 1) * ncoef + idx] = z;
-    out[(size_t)(r * 3 + 2) * ncoef + idx] = vd;
+    const double2 *F = fac + (size_t)r * 4 * np + q;
+    double2 bp = make_double2(0.0, 0.0), bz = bp, bd = bp;
+    if (has) {
+      bp = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
+      bz = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
+      bd = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
+    }
+    PhiDiv pd = pole_tree_pd<LEAF>(F, F + np, F + 2 * np, nb, lpm, bp, bd);
+    double2 z = pole_tree_z<LEAF>(F + 3 * np, nb, lpm, bz);
+    for (int o = 1; o < lpm; o <<= 1) {
+      pd.p = cadd(pd.p, shfl_xor2(pd.p, o));
+      pd.d = cadd(pd.d, shfl_xor2(pd.d, o));
+      z = cadd(z, shfl_xor2(z, o));
+    }
+    if (has && q == 0) {
+      if (realify && m == 0) pd.p.y = z.y = pd.d.y = 0.0;
+      out[(size_t)(r * 3 + 0) * ncoef + idx] = pd.p;
+      out[(size_t)(r * 3 + 1) * ncoef + idx] = z;
+      out[(size_t)(r * 3 + 2) * ncoef + idx] = pd.d;
+    }
   }
 }
 
@@ -574,15 +606,6 @@ extern "C" int swx_solver_create(swx_solver *out, int group, int trunc,
   if (e == cudaSuccess)
     e = cudaMemcpy(s->d_chain, ch.data(), sizeof(double) * 3 * (size_t)nc,
                    cudaMemcpyHostToDevice);
-  // lg schedule: CTAs of (l, m0, m1) with at most 32 modes each
-  std::vector<int4> sched;
-  for (int l = n - 1; l >= 0; --l)
-    for (int m0 = 0; m0 <= l; m0 += kLgModes)
-      sched.push_back(make_int4(l, m0, std::min(l + 1, m0 + kLgModes), 0));
-  s->n_sched = (int)sched.size();
-  if (e == cudaSuccess) e = cudaMalloc(&s->d_sched, sizeof(int4) * sched.size());
-  if (e == cudaSuccess)
-    e = cudaMemcpy(s->d_sched, sched.data(), sizeof(int4) * sched.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     swx_solver_destroy(s);
     return fail(SWX_ERR_CUDA, std::string("solver create: ") + cudaGetErrorString(e));
@@ -596,7 +619,7 @@ extern "C" int swx_solver_destroy(swx_solver s) {
   cudaFree(s->d_lconst);
   cudaFree(s->d_chain);
   cudaFree(s->d_alpha);
-  cudaFree(s->d_sched);
+  for (auto &kv : s->lg_sched) cudaFree(kv.second.first);
   delete[] s->h_norm;
   delete[] s->h_alpha;
   delete s;
@@ -687,7 +710,7 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
 }
 
 // ---- launch geometry helpers
-static constexpr int kLgMaxP = 1024;  // poles per lg launch (smem = NRHS*64*P bytes)
+static constexpr int kLgMaxP = 512;  // poles per lg launch (smem = NRHS*64*P bytes)
 
 static size_t l_smem_bytes(int nrhs) {
   return (size_t)kLWarps * kFlush * nrhs * 2 * 32 * sizeof(double2);
@@ -719,29 +742,56 @@ extern "C" size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs,
   const bool cor = s->group == SWX_GROUP_L && s->omega > 0.0;
   if (!cor) {
     const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
-    return chunks > 1 ? chunks * state : 0;
+    const int np = next_pow2(std::min(P, kLgMaxP));
+    const size_t fac = (size_t)(s->trunc + 1) * n_rhs * 4 * np * sizeof(double2);
+    return ((fac + 255) / 256) * 256 + (chunks > 1 ? chunks * state : 0);
   }
   const int nb = (P + 31) / 32;
   return l_scratch_bytes(s, n_rhs, P) + (size_t)nb * state + 256;
 }
 
+// modes per CTA for a given lanes-per-mode; schedules built lazily
+static const int4 *lg_schedule(swx_solver s, int mpc, int *n_cta) {
+  auto &e = s->lg_sched[mpc];
+  if (!e.first) {
+    std::vector<int4> sched;
+    for (int l = s->trunc; l >= 0; --l)
+      for (int m0 = 0; m0 <= l; m0 += mpc) sched.push_back(make_int4(l, m0, std::min(l + 1, m0 + mpc), 0));
+    int4 *d = nullptr;
+    if (cudaMalloc(&d, sizeof(int4) * sched.size()) != cudaSuccess) return nullptr;
+    cudaMemcpy(d, sched.data(), sizeof(int4) * sched.size(), cudaMemcpyHostToDevice);
+    e.first = d;
+    e.second = (int)sched.size();
+  }
+  *n_cta = e.second;
+  return e.first;
+}
+
 template <int NRHS>
 static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
-                     int pole0, int P, int realify, double2 *out,
+                     int pole0, int P, int realify, double2 *out, double2 *fac_ws,
                      cudaStream_t st) {
   const int np = next_pow2(P);
-  const int leaf = std::min(np, 16);
+  const int lpm = std::min(8, np);       // lanes per mode
+  const int ppl = np / lpm;              // poles per lane
+  const int leaf = std::min(ppl, 8);
+  dim3 fg((np + 127) / 128, s->trunc + 1);
+  lg_factor_kernel<NRHS><<<fg, 128, 0, st>>>(s->d_alpha, betas, s->n_poles, pole0, P, np,
+                                             s->trunc, s->dt, s->phibar, s->d_lconst, fac_ws);
+  SWX_LAUNCH_CHECK();
+  int n_cta = 0;
+  const int4 *sched = lg_schedule(s, 4 * 32 / lpm, &n_cta);
+  if (!sched) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
   const size_t smem = (size_t)NRHS * 4 * np * sizeof(double2);
-#define SWX_LG_CASE(LV)                                                                     \
-  case LV: {                                                                                \
-    auto k = rexi_lg_kernel<NRHS, LV>;                                                      \
-    if (smem > 48 * 1024)                                                                   \
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                        (int)smem));                                        \
-    k<<<s->n_sched, kLgModes, smem, st>>>(rhs, s->d_alpha, betas, s->n_poles, pole0, P, np, \
-                                          s->trunc, s->ncoef, s->dt, s->phibar,             \
-                                          s->d_lconst, s->d_sched, realify, out);           \
-    break;                                                                                  \
+#define SWX_LG_CASE(LV)                                                                  \
+  case LV: {                                                                             \
+    auto k = rexi_lg_kernel<NRHS, LV>;                                                   \
+    if (smem > 48 * 1024)                                                                \
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                        (int)smem));                                     \
+    k<<<n_cta, 128, smem, st>>>(rhs, fac_ws, np, lpm, s->trunc, s->ncoef, sched, realify, \
+                                out);                                                    \
+    break;                                                                               \
   }
   switch (leaf) {
     SWX_LG_CASE(1)
@@ -803,17 +853,21 @@ extern "C" int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
   const bool cor = s->group == SWX_GROUP_L && s->omega > 0.0;
   if (!cor) {
     const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
+    const int np = next_pow2(std::min(P, kLgMaxP));
+    const size_t fac = (size_t)(s->trunc + 1) * n_rhs * 4 * np * sizeof(double2);
+    double2 *fac_ws = (double2 *)d_workspace;
     if (chunks == 1)
-      return n_rhs == 1 ? launch_lg<1>(s, rhs, bet, pole_begin, P, realify, out, st)
-                        : launch_lg<2>(s, rhs, bet, pole_begin, P, realify, out, st);
+      return n_rhs == 1 ? launch_lg<1>(s, rhs, bet, pole_begin, P, realify, out, fac_ws, st)
+                        : launch_lg<2>(s, rhs, bet, pole_begin, P, realify, out, fac_ws, st);
     // aligned chunks of kLgMaxP poles, combined in tree order
-    double2 *part = (double2 *)d_workspace;
+    double2 *part = (double2 *)((char *)d_workspace + ((fac + 255) / 256) * 256);
     const size_t stride = (size_t)n_rhs * 3 * s->ncoef;
     for (int c = 0; c < chunks; ++c) {
       const int p0 = pole_begin + c * kLgMaxP;
       const int pc = std::min(kLgMaxP, pole_end - p0);
-      int rc = n_rhs == 1 ? launch_lg<1>(s, rhs, bet, p0, pc, 0, part + c * stride, st)
-                          : launch_lg<2>(s, rhs, bet, p0, pc, 0, part + c * stride, st);
+      int rc = n_rhs == 1
+                   ? launch_lg<1>(s, rhs, bet, p0, pc, 0, part + c * stride, fac_ws, st)
+                   : launch_lg<2>(s, rhs, bet, p0, pc, 0, part + c * stride, fac_ws, st);
       if (rc) return rc;
     }
     tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, chunks,

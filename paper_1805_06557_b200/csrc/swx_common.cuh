@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
+#include <utility>
 
 #include "../../include/swx.h"
 
@@ -80,8 +82,7 @@ struct swx_solver_s {
   int n_poles = 0;
   double2 *d_alpha = nullptr;
   double2 *h_alpha = nullptr;
-  // lg launch schedule (l, m0, m1, -) per CTA
-  int4 *d_sched = nullptr;
-  int n_sched = 0;
+  // lg launch schedules (l, m0, m1, -) per CTA, keyed by modes per CTA
+  std::map<int, std::pair<int4 *, int>> lg_sched;
   int l_blocks_per_sm = 0;
 };
