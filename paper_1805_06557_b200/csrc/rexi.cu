@@ -146,16 +146,20 @@ __device__ __forceinline__ double2 pole_tree_z(const double2 *D, int nb, int lpm
 // beyond P zero (solvers.py:93-107 with the reciprocals hoisted per (n, l))
 template <int NRHS>
 __global__ void lg_factor_kernel(const double2 *__restrict__ alpha, const double2 *__restrict__ beta,
-                                 int beta_stride, int pole0, int P, int np, int trunc, double dt,
-                                 double phibar, const double *__restrict__ lconst,
-                                 double2 *__restrict__ fac) {
+                                 int beta_stride, int pole0, int P, int np, int log2_ppl, int lpm,
+                                 int trunc, double dt, double phibar,
+                                 const double *__restrict__ lconst, double2 *__restrict__ fac) {
   const int l = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= np) return;
   double2 *F = fac + (size_t)l * NRHS * 4 * np;
+  // interleave: pole i = q*ppl + t is stored at t*lpm + q (lane group reads
+  // 128 contiguous bytes per pole step)
+  const int qq = i >> log2_ppl, tt = i - (qq << log2_ppl);
+  const int slot = tt * lpm + qq;
   if (i >= P) {
 #pragma unroll
-    for (int q = 0; q < NRHS * 4; ++q) F[(size_t)q * np + i] = make_double2(0.0, 0.0);
+    for (int q = 0; q < NRHS * 4; ++q) F[(size_t)q * np + slot] = make_double2(0.0, 0.0);
     return;
   }
   const double kap = lconst[l];
@@ -170,10 +174,10 @@ __global__ void lg_factor_kernel(const double2 *__restrict__ alpha, const double
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) {
     const double2 b = beta[r * beta_stride + pole0 + i];
-    F[(size_t)(r * 4 + 0) * np + i] = cmul(b, q1);
-    F[(size_t)(r * 4 + 1) * np + i] = cmul(b, q2);
-    F[(size_t)(r * 4 + 2) * np + i] = cmul(b, q3);
-    F[(size_t)(r * 4 + 3) * np + i] = cmul(b, q4);
+    F[(size_t)(r * 4 + 0) * np + slot] = cmul(b, q1);
+    F[(size_t)(r * 4 + 1) * np + slot] = cmul(b, q2);
+    F[(size_t)(r * 4 + 2) * np + slot] = cmul(b, q3);
+    F[(size_t)(r * 4 + 3) * np + slot] = cmul(b, q4);
   }
 }
 
@@ -184,29 +188,22 @@ __global__ void lg_factor_kernel(const double2 *__restrict__ alpha, const double
 template <int NRHS, int LEAF>
 __global__ void __launch_bounds__(128) rexi_lg_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int np, int lpm,
-    int trunc, int ncoef, const int4 *__restrict__ sched, int realify,
+    int log2_lpm, int trunc, int ncoef, const int4 *__restrict__ sched, int realify,
     double2 *__restrict__ out) {
-  extern __shared__ double2 fac[];  // [NRHS][4][np] interleaved (t*LPM + q)
+  // factors are read straight from the (L1/L2-resident) per-l table; no staging
   const int4 w = sched[blockIdx.x];
   const int l = w.x, m0 = w.y, m1 = w.z;
-  const int ppl = np / lpm;  // poles per lane
-  const double2 *src = fac_g + (size_t)l * NRHS * 4 * np;
-  for (int i = threadIdx.x; i < NRHS * 4 * np; i += blockDim.x) {
-    const int row = i / np, pole = i - row * np;
-    const int q = pole / ppl, t = pole - q * ppl;
-    fac[row * np + t * lpm + q] = src[i];
-  }
-  __syncthreads();
+  const int ppl = np >> log2_lpm;  // poles per lane
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int mpw = 32 / lpm;
-  const int q = lane % lpm;
-  const int m = m0 + warp * mpw + lane / lpm;
+  const int q = lane & (lpm - 1);
+  const int m = m0 + ((warp * 32 + lane) >> log2_lpm);
   const bool has = m < m1;
   const size_t idx = has ? (size_t)col_offset(trunc, m) + (l - m) : 0;
   const int nb = ppl / LEAF;
+  const double2 *Fl = fac_g + (size_t)l * NRHS * 4 * np + q;
 #pragma unroll 1
   for (int r = 0; r < NRHS; ++r) {
-    const double2 *F = fac + (size_t)r * 4 * np + q;
+    const double2 *F = Fl + (size_t)r * 4 * np;
     double2 bp = make_double2(0.0, 0.0), bz = bp, bd = bp;
     if (has) {
       bp = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
@@ -775,23 +772,22 @@ static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
   const int lpm = std::min(8, np);       // lanes per mode
   const int ppl = np / lpm;              // poles per lane
   const int leaf = std::min(ppl, 8);
+  int log2_ppl = 0, log2_lpm = 0;
+  while ((1 << log2_ppl) < ppl) ++log2_ppl;
+  while ((1 << log2_lpm) < lpm) ++log2_lpm;
   dim3 fg((np + 127) / 128, s->trunc + 1);
   lg_factor_kernel<NRHS><<<fg, 128, 0, st>>>(s->d_alpha, betas, s->n_poles, pole0, P, np,
-                                             s->trunc, s->dt, s->phibar, s->d_lconst, fac_ws);
+                                             log2_ppl, lpm, s->trunc, s->dt, s->phibar,
+                                             s->d_lconst, fac_ws);
   SWX_LAUNCH_CHECK();
   int n_cta = 0;
   const int4 *sched = lg_schedule(s, 4 * 32 / lpm, &n_cta);
   if (!sched) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
-  const size_t smem = (size_t)NRHS * 4 * np * sizeof(double2);
-#define SWX_LG_CASE(LV)                                                                  \
-  case LV: {                                                                             \
-    auto k = rexi_lg_kernel<NRHS, LV>;                                                   \
-    if (smem > 48 * 1024)                                                                \
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                        (int)smem));                                     \
-    k<<<n_cta, 128, smem, st>>>(rhs, fac_ws, np, lpm, s->trunc, s->ncoef, sched, realify, \
-                                out);                                                    \
-    break;                                                                               \
+#define SWX_LG_CASE(LV)                                                                   \
+  case LV: {                                                                              \
+    rexi_lg_kernel<NRHS, LV><<<n_cta, 128, 0, st>>>(rhs, fac_ws, np, lpm, log2_lpm, s->trunc, \
+                                                    s->ncoef, sched, realify, out);         \
+    break;                                                                                \
   }
   switch (leaf) {
     SWX_LG_CASE(1)
