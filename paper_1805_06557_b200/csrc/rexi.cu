@@ -185,43 +185,54 @@ __global__ void lg_factor_kernel(const double2 *__restrict__ alpha, const double
 // owned by LPM adjacent lanes, lane q of the group reducing the pole block
 // [q*np/LPM, (q+1)*np/LPM) as a perfect tree; an xor butterfly inside the
 // group completes tree_sum's order over the launch's np poles.
+constexpr int kLgPasses = 4;  // 16-mode passes per CTA (factor staging amortised 4x)
+
 template <int NRHS, int LEAF>
 __global__ void __launch_bounds__(128) rexi_lg_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int np, int lpm,
     int log2_lpm, int trunc, int ncoef, const int4 *__restrict__ sched, int realify,
     double2 *__restrict__ out) {
-  // factors are read straight from the (L1/L2-resident) per-l table; no staging
+  extern __shared__ double2 fac[];  // [NRHS][4][np], already interleaved (t*LPM + q)
   const int4 w = sched[blockIdx.x];
   const int l = w.x, m0 = w.y, m1 = w.z;
+  {
+    const double4 *src = reinterpret_cast<const double4 *>(fac_g + (size_t)l * NRHS * 4 * np);
+    double4 *dst = reinterpret_cast<double4 *>(fac);
+    const int n4 = NRHS * 2 * np;  // NRHS*4*np double2 = NRHS*2*np double4
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
   const int ppl = np >> log2_lpm;  // poles per lane
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & (lpm - 1);
-  const int m = m0 + ((warp * 32 + lane) >> log2_lpm);
-  const bool has = m < m1;
-  const size_t idx = has ? (size_t)col_offset(trunc, m) + (l - m) : 0;
+  const int per_pass = 128 >> log2_lpm;  // modes per pass
   const int nb = ppl / LEAF;
-  const double2 *Fl = fac_g + (size_t)l * NRHS * 4 * np + q;
+  for (int base = m0; base < m1; base += per_pass) {
+    const int m = base + ((warp * 32 + lane) >> log2_lpm);
+    const bool has = m < m1;
+    const size_t idx = has ? (size_t)col_offset(trunc, m) + (l - m) : 0;
 #pragma unroll 1
-  for (int r = 0; r < NRHS; ++r) {
-    const double2 *F = Fl + (size_t)r * 4 * np;
-    double2 bp = make_double2(0.0, 0.0), bz = bp, bd = bp;
-    if (has) {
-      bp = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
-      bz = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
-      bd = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
-    }
-    PhiDiv pd = pole_tree_pd<LEAF>(F, F + np, F + 2 * np, nb, lpm, bp, bd);
-    double2 z = pole_tree_z<LEAF>(F + 3 * np, nb, lpm, bz);
-    for (int o = 1; o < lpm; o <<= 1) {
-      pd.p = cadd(pd.p, shfl_xor2(pd.p, o));
-      pd.d = cadd(pd.d, shfl_xor2(pd.d, o));
-      z = cadd(z, shfl_xor2(z, o));
-    }
-    if (has && q == 0) {
-      if (realify && m == 0) pd.p.y = z.y = pd.d.y = 0.0;
-      out[(size_t)(r * 3 + 0) * ncoef + idx] = pd.p;
-      out[(size_t)(r * 3 + 1) * ncoef + idx] = z;
-      out[(size_t)(r * 3 + 2) * ncoef + idx] = pd.d;
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 *F = fac + (size_t)r * 4 * np + q;
+      double2 bp = make_double2(0.0, 0.0), bz = bp, bd = bp;
+      if (has) {
+        bp = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
+        bz = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
+        bd = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
+      }
+      PhiDiv pd = pole_tree_pd<LEAF>(F, F + np, F + 2 * np, nb, lpm, bp, bd);
+      double2 z = pole_tree_z<LEAF>(F + 3 * np, nb, lpm, bz);
+      for (int o = 1; o < lpm; o <<= 1) {
+        pd.p = cadd(pd.p, shfl_xor2(pd.p, o));
+        pd.d = cadd(pd.d, shfl_xor2(pd.d, o));
+        z = cadd(z, shfl_xor2(z, o));
+      }
+      if (has && q == 0) {
+        if (realify && m == 0) pd.p.y = z.y = pd.d.y = 0.0;
+        out[(size_t)(r * 3 + 0) * ncoef + idx] = pd.p;
+        out[(size_t)(r * 3 + 1) * ncoef + idx] = z;
+        out[(size_t)(r * 3 + 2) * ncoef + idx] = pd.d;
+      }
     }
   }
 }
@@ -781,13 +792,18 @@ static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
                                              s->d_lconst, fac_ws);
   SWX_LAUNCH_CHECK();
   int n_cta = 0;
-  const int4 *sched = lg_schedule(s, 4 * 32 / lpm, &n_cta);
+  const int4 *sched = lg_schedule(s, kLgPasses * 4 * 32 / lpm, &n_cta);
   if (!sched) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
-#define SWX_LG_CASE(LV)                                                                   \
-  case LV: {                                                                              \
-    rexi_lg_kernel<NRHS, LV><<<n_cta, 128, 0, st>>>(rhs, fac_ws, np, lpm, log2_lpm, s->trunc, \
-                                                    s->ncoef, sched, realify, out);         \
-    break;                                                                                \
+  const size_t smem = (size_t)NRHS * 4 * np * sizeof(double2);
+#define SWX_LG_CASE(LV)                                                                     \
+  case LV: {                                                                                \
+    auto k = rexi_lg_kernel<NRHS, LV>;                                                      \
+    if (smem > 48 * 1024)                                                                   \
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                        (int)smem));                                        \
+    k<<<n_cta, 128, smem, st>>>(rhs, fac_ws, np, lpm, log2_lpm, s->trunc, s->ncoef, sched,  \
+                                realify, out);                                              \
+    break;                                                                                  \
   }
   switch (leaf) {
     SWX_LG_CASE(1)

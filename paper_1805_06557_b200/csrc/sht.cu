@@ -13,12 +13,18 @@
 //    frexp/ldexp sectoral values, at the northern node of each equatorially
 //    symmetric latitude pair, and uses P(-x) = (-1)^(l+m) P(x),
 //    H(-x) = (-1)^(l+m+1) H(x) for the southern node.
-//  * synthesis: one thread per (latitude pair, m) walks l = m..T with the
-//    column's coefficients and recurrence constants staged in shared memory,
-//    accumulating parity-split sums of all series at once (DFMA).
-//  * analysis: per m, (16 l x latitude) tiles of P and H are generated into
-//    shared memory and contracted with the prepared Fourier data on the FP64
-//    tensor cores (mma.sync m8n8k4 f64 = DMMA), K split over two warp groups.
+//  * Work is cut into (m, 64-degree segment) items; each item starts its
+//    recurrence from plan-time checkpoints (P_{l0-1}, P_{l0}, P_{l0+1}), so no
+//    CTA walks a whole 257-degree column (critical path / load balance).
+//  * synthesis: one lane per (latitude pair), a warp per segment, the
+//    segment's coefficients and recurrence constants staged in shared memory,
+//    parity-split sums of all series at once (DFMA); segment partials are
+//    combined in a fixed order.
+//  * analysis: per (m, segment), (16 l x latitude) tiles of P and H are
+//    generated into shared memory and contracted with the prepared Fourier
+//    data on the FP64 tensor cores (mma.sync m8n8k4 f64 = DMMA), K split over
+//    two warp groups; the data preparation (weights, i*m, hemisphere fold) is
+//    fused into the same kernel.
 //  * The Coriolis atom is evaluated in Fourier space (f and df/dlat are
 //    latitude-only multipliers, so FFT(f*g) = f*FFT(g) exactly); only the 5
 //    nonlinear products go through the longitude FFT (cuFFT, batched).  The
@@ -50,6 +56,12 @@ struct ShtView {
   double4 *d_rc = nullptr;    // [m][k] k = 0..T+1-m: {e_{l-1}, 1/e_l, (l+1)e_l, l e_{l+1}}
   double *d_lconst = nullptr; // [T+1] inv_laplacian factor, [T+1] ll1/a^2
   double *d_frow = nullptr;   // [nlat] f = 2 Omega sin, [nlat] 2 Omega cos / a
+  // l-segments of kSeg degrees: CTA list (m, l0) and recurrence checkpoints
+  // (P_{l0-1}, P_{l0}, P_{l0+1}) at every segment start, [seg][3][nh]
+  int nseg = 0;
+  int2 *d_segs = nullptr;
+  int *d_segoff = nullptr;    // [m] index of the first segment of column m
+  double *d_ckpt = nullptr;
 };
 
 struct swx_sht_s : ShtView {
@@ -77,66 +89,69 @@ struct SynthArgs {
   int nfreq;
 };
 
-constexpr int kSL = 128;  // l rows staged per chunk
+constexpr int kSeg = 64;   // degrees per analysis/synthesis segment
+constexpr int kSynW = 8;   // warps per synthesis CTA (segments s = w, w+8, ...)
 
+// CTA = (m, block of 32 latitude pairs); warp w walks segments w, w+8, ... of
+// column m from the plan-time recurrence checkpoints, lane = latitude pair.
+// Segment partial sums are combined in a fixed order (per warp ascending,
+// then warps ascending): deterministic.
 template <int MODE>
-__global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
+__global__ void __launch_bounds__(kSynW * 32) synth_kernel(ShtView p, SynthArgs a) {
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
-  __shared__ double2 cs[NS][kSL];
-  __shared__ double4 rcs[kSL + 2];
+  constexpr int NACC = 4 * (NS + NH);    // doubles of parity-split partial sums
+  extern __shared__ __align__(16) double smem[];  // synth_smem_bytes(NS, NH)
   const int m = blockIdx.x;
-  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.y * 32 + lane;
   const int field = MODE == 1 ? blockIdx.z : 0;
   const int T = p.trunc, nc = p.ncoef;
   const int off = col_offset(T, m);
   const int kmax = T + 1 - m;
+  const int nsg = (kmax + kSeg - 1) / kSeg;
   const double4 *rc = p.d_rc + rc_offset(T, m);
   const bool has = i < p.nh;
-  double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
-  if (has) {
-    x = p.d_x[i];
-    rcos = p.d_rcos[i];
-    const double seed = p.d_seed[(size_t)m * p.nh + i];
-    p0 = seed;
-    p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
-  }
-  double2 sp[2][NS], sh[2][NH > 0 ? NH : 1];
+  double2 *cs = reinterpret_cast<double2 *>(smem) + (size_t)warp * kSeg * NS;  // [kSeg][NS]
+  double4 *rcs = reinterpret_cast<double4 *>(smem + kSynW * kSeg * NS * 2) + (size_t)warp * (kSeg + 2);
+  double acc[NACC];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) sp[q][s] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int s = 0; s < (NH > 0 ? NH : 1); ++s) sh[q][s] = make_double2(0.0, 0.0);
-  }
-  for (int l0 = m; l0 <= T; l0 += kSL) {
-    const int n = min(kSL, T + 1 - l0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < kSL + 2; t += blockDim.x) {
-      const int k = l0 - m + t;
-      if (k <= kmax) rcs[t] = rc[k];
-    }
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      const int s = off + (l0 - m) + t;
+  for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
+  const double x = has ? p.d_x[i] : 0.0;
+  const double rcos = has ? p.d_rcos[i] : 0.0;
+  for (int sg = warp; sg < nsg; sg += kSynW) {
+    const int k0 = sg * kSeg;
+    const int n = min(kSeg, kmax - k0);
+    // stage this segment's coefficients and recurrence constants (warp-private)
+    for (int t = lane; t < kSeg + 2; t += 32)
+      if (k0 + t <= kmax) rcs[t] = rc[k0 + t];
+    for (int t = lane; t < n; t += 32) {
+      const int s = off + k0 + t;
       if (MODE == 0) {
-        const double il = p.d_lconst[l0 + t];
+        const double il = p.d_lconst[m + k0 + t];
         const double2 z = a.coef[nc + s], d = a.coef[2 * nc + s];
-        cs[0][t] = z;
-        cs[1][t] = d;
-        cs[NS > 2 ? 2 : 0][t] = a.coef[s];
-        cs[NS > 3 ? 3 : 0][t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
-        cs[NS > 4 ? 4 : 0][t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+        cs[t * NS + 0] = z;
+        cs[t * NS + (NS > 1 ? 1 : 0)] = d;
+        cs[t * NS + (NS > 2 ? 2 : 0)] = a.coef[s];
+        cs[t * NS + (NS > 3 ? 3 : 0)] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
+        cs[t * NS + (NS > 4 ? 4 : 0)] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
       } else {
-        cs[0][t] = a.coef[(size_t)field * nc + s];
+        cs[t] = a.coef[(size_t)field * nc + s];
       }
     }
-    __syncthreads();
+    __syncwarp();
+    const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + sg) * 3 * p.nh;
+    double pm1 = 0.0, p0 = 0.0, p1 = 0.0;
+    if (has) {
+      pm1 = ck[i];
+      p0 = ck[p.nh + i];
+      p1 = ck[2 * p.nh + i];
+    }
     for (int t = 0; t < n; t += 2) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {  // static parity: l - m = (l0 - m) + t + q
+      for (int q = 0; q < 2; ++q) {  // static parity: l - m = k0 + t + q, k0 even
         if (q == 1 && t + 1 >= n) break;
         const int tt = t + q;
-        const int k = l0 - m + tt;
         const double P = p0;
         double H = 0.0;
         if (NH > 0) {
@@ -145,18 +160,19 @@ __global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
         }
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-          const double2 v = cs[s][tt];
-          sp[q][s].x = fma(P, v.x, sp[q][s].x);
-          sp[q][s].y = fma(P, v.y, sp[q][s].y);
+          const double2 v = cs[tt * NS + s];
+          acc[(q * NS + s) * 2] = fma(P, v.x, acc[(q * NS + s) * 2]);
+          acc[(q * NS + s) * 2 + 1] = fma(P, v.y, acc[(q * NS + s) * 2 + 1]);
         }
 #pragma unroll
         for (int s = 0; s < NH; ++s) {
-          const double2 v = cs[NS > 3 ? 3 + s : 0][tt];
-          sh[q][s].x = fma(H, v.x, sh[q][s].x);
-          sh[q][s].y = fma(H, v.y, sh[q][s].y);
+          const double2 v = cs[tt * NS + (NS > 3 ? 3 + s : 0)];
+          const int o = 4 * NS + (q * NH + s) * 2;
+          acc[o] = fma(H, v.x, acc[o]);
+          acc[o + 1] = fma(H, v.y, acc[o + 1]);
         }
         double p2 = 0.0;
-        if (k + 2 <= kmax) {
+        if (k0 + tt + 2 <= kmax) {
           const double4 c2 = rcs[tt + 2];
           p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
         }
@@ -165,12 +181,34 @@ __global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
         p1 = p2;
       }
     }
+    __syncwarp();
   }
-  if (!has) return;
+  // combine the warps' partial sums in ascending warp order
+  __syncthreads();
+  double *red = smem;  // [kSynW][32][NACC] (reuses the staging area)
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) red[((size_t)warp * 32 + lane) * NACC + q] = acc[q];
+  __syncthreads();
+  if (warp != 0 || !has) return;
+  for (int w = 1; w < kSynW && w < nsg; ++w) {
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) acc[q] += red[((size_t)w * 32 + lane) * NACC + q];
+  }
+  double2 sp[2][NS], sh[2][NH > 0 ? NH : 1];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      sp[q][s] = make_double2(acc[(q * NS + s) * 2], acc[(q * NS + s) * 2 + 1]);
+#pragma unroll
+    for (int s = 0; s < (NH > 0 ? NH : 1); ++s) {
+      const int o = 4 * NS + (q * NH + s) * 2;
+      sh[q][s] = NH > 0 ? make_double2(acc[o], acc[o + 1]) : make_double2(0.0, 0.0);
+    }
+  }
   const int jn = p.d_jn[i], js = p.d_js[i];
   const int nf = a.nfreq;
   const size_t row = (size_t)p.nlat * nf;
-  // kSL is even and l0 - m advances by kSL, so sp[q] holds parity q of (l - m)
   if (MODE == 1) {
     double2 gn = make_double2(sp[0][0].x + sp[1][0].x, sp[0][0].y + sp[1][0].y);
     double2 gs = make_double2(sp[0][0].x - sp[1][0].x, sp[0][0].y - sp[1][0].y);
@@ -257,72 +295,64 @@ __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
   }
 }
 
-__global__ void prep_tend_kernel(ShtView p, const double2 *Q, const double2 *lc,
-                                 int atoms, double *A) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int m = blockIdx.y;
-  if (i >= p.nhp) return;
-  double *base = A + (size_t)m * 4 * p.nhp * kAS;  // [part][par][pair][kAS]
-  double2 ev[7], od[7];
+// fold one latitude pair of the tendency inputs into even/odd parts of the
+// 7 analysis series (the prepared row of pair i, column m)
+__device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, const double2 *lc,
+                                         int atoms, int m, int i, double2 *ev, double2 *od) {
   if (i >= p.nh) {
 #pragma unroll
     for (int s = 0; s < 7; ++s) ev[s] = od[s] = make_double2(0.0, 0.0);
-  } else {
-    const int jn = p.d_jn[i], js = p.d_js[i];
-    const double rcos = p.d_rcos[i];
-    const double ra = 1.0 / p.radius;
-    const double fm = (double)m;
-    const bool nl = (atoms & SWX_TEND_N) != 0;
-    double2 av[2][7];
+    return;
+  }
+  const int jn = p.d_jn[i], js = p.d_js[i];
+  const double rcos = p.d_rcos[i];
+  const double ra = 1.0 / p.radius;
+  const double fm = (double)m;
+  const bool nl = (atoms & SWX_TEND_N) != 0;
+  double2 av[2][7];
 #pragma unroll
-    for (int hemi = 0; hemi < 2; ++hemi) {
-      const int j = hemi ? js : jn;
-      const double wj = hemi ? p.d_ws[i] : p.d_wn[i];
-      const double woc = wj * rcos;
-      const size_t row = (size_t)p.nlat * p.nfreq_t;
-      const size_t at = (size_t)j * p.nfreq_t + m;
-      double2 F[5];
+  for (int hemi = 0; hemi < 2; ++hemi) {
+    const int j = hemi ? js : jn;
+    const double wj = hemi ? p.d_ws[i] : p.d_wn[i];
+    const double woc = wj * rcos;
+    const size_t row = (size_t)p.nlat * p.nfreq_t;
+    const size_t at = (size_t)j * p.nfreq_t + m;
+    double2 F[5];
 #pragma unroll
-      for (int s = 0; s < 5; ++s) {
-        const double2 q = nl ? Q[s * row + at] : make_double2(0.0, 0.0);
-        F[s] = make_double2(q.x * p.dlon_t, q.y * p.dlon_t);  // fft * dlon
-      }
-      double2 l1 = make_double2(0.0, 0.0), l2 = l1;
-      if (atoms & SWX_TEND_LC) {
-        l1 = lc[(size_t)j * p.nm + m];
-        l2 = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
-      }
-      // (i m / a) * woc * F  ==  woc*m/a * (-F.y, F.x)
-      const double cm = woc * fm * ra;
-      const double2 imPu = make_double2(-cm * F[0].y, cm * F[0].x);  // phi'u
-      const double2 imZu = make_double2(-cm * F[2].y, cm * F[2].x);  // vort u
-      const double2 imZv = make_double2(-cm * F[3].y, cm * F[3].x);  // vort v
-      const double wa = wj * ra;
-      double2 *o = av[hemi];
-      o[0] = make_double2(wj * l1.x - imZu.x, wj * l1.y - imZu.y);
-      o[1] = make_double2(wj * l2.x + imZv.x, wj * l2.y + imZv.y);
-      o[2] = make_double2(-imPu.x, -imPu.y);
-      o[3] = make_double2(wj * F[4].x, wj * F[4].y);
-      o[4] = make_double2(wa * F[3].x, wa * F[3].y);
-      o[5] = make_double2(wa * F[2].x, wa * F[2].y);
-      o[6] = make_double2(wa * F[1].x, wa * F[1].y);
+    for (int s = 0; s < 5; ++s) {
+      const double2 q = nl ? Q[s * row + at] : make_double2(0.0, 0.0);
+      F[s] = make_double2(q.x * p.dlon_t, q.y * p.dlon_t);  // fft * dlon
     }
-    if (js == jn) {  // equator node of an odd grid: counted once
+    double2 l1 = make_double2(0.0, 0.0), l2 = l1;
+    if (atoms & SWX_TEND_LC) {
+      l1 = lc[(size_t)j * p.nm + m];
+      l2 = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
+    }
+    // (i m / a) * woc * F  ==  woc*m/a * (-F.y, F.x)
+    const double cm = woc * fm * ra;
+    const double2 imPu = make_double2(-cm * F[0].y, cm * F[0].x);  // phi'u
+    const double2 imZu = make_double2(-cm * F[2].y, cm * F[2].x);  // vort u
+    const double2 imZv = make_double2(-cm * F[3].y, cm * F[3].x);  // vort v
+    const double wa = wj * ra;
+    double2 *o = av[hemi];
+    o[0] = make_double2(wj * l1.x - imZu.x, wj * l1.y - imZu.y);
+    o[1] = make_double2(wj * l2.x + imZv.x, wj * l2.y + imZv.y);
+    o[2] = make_double2(-imPu.x, -imPu.y);
+    o[3] = make_double2(wj * F[4].x, wj * F[4].y);
+    o[4] = make_double2(wa * F[3].x, wa * F[3].y);
+    o[5] = make_double2(wa * F[2].x, wa * F[2].y);
+    o[6] = make_double2(wa * F[1].x, wa * F[1].y);
+  }
+  if (js == jn) {  // equator node of an odd grid: counted once
 #pragma unroll
-      for (int s = 0; s < 7; ++s) ev[s] = od[s] = av[0][s];
-    } else {
+    for (int s = 0; s < 7; ++s) ev[s] = od[s] = av[0][s];
+  } else {
 #pragma unroll
-      for (int s = 0; s < 7; ++s) {
-        ev[s] = make_double2(av[0][s].x + av[1][s].x, av[0][s].y + av[1][s].y);
-        od[s] = make_double2(av[0][s].x - av[1][s].x, av[0][s].y - av[1][s].y);
-      }
+    for (int s = 0; s < 7; ++s) {
+      ev[s] = make_double2(av[0][s].x + av[1][s].x, av[0][s].y + av[1][s].y);
+      od[s] = make_double2(av[0][s].x - av[1][s].x, av[0][s].y - av[1][s].y);
     }
   }
-  const size_t ps = (size_t)p.nhp * kAS;
-  put_row(base + 0 * ps + (size_t)i * kAS, ev, 4);      // P, even
-  put_row(base + 1 * ps + (size_t)i * kAS, od, 4);      // P, odd
-  put_row(base + 2 * ps + (size_t)i * kAS, ev + 4, 3);  // H, even
-  put_row(base + 3 * ps + (size_t)i * kAS, od + 4, 3);  // H, odd
 }
 
 // plain analysis prep: nf (<= 4) grids already FFT'd into Q (pitch nfreq)
@@ -379,9 +409,43 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// recurrence checkpoints at every segment start (plan time; data independent)
+__global__ void ckpt_kernel(ShtView p) {
+  const int m = blockIdx.x;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= p.nh) return;
+  const int T = p.trunc, kmax = T + 1 - m;
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  const double x = p.d_x[i];
+  const double seed = p.d_seed[(size_t)m * p.nh + i];
+  double pm1 = 0.0, p0 = seed, p1 = sqrt(2.0 * m + 3.0) * x * seed;
+  double *ck = p.d_ckpt + (size_t)p.d_segoff[m] * 3 * p.nh;
+  for (int k = 0; k < kmax; ++k) {
+    if (k % kSeg == 0) {
+      double *c = ck + (size_t)(k / kSeg) * 3 * p.nh;
+      c[i] = pm1;
+      c[p.nh + i] = p0;
+      c[2 * p.nh + i] = p1;
+    }
+    double p2 = 0.0;
+    if (k + 2 <= kmax) {
+      const double4 c2 = rc[k + 2];
+      p2 = fma(x, p1, -c2.x * p0) * c2.y;  // identical to the walkers below
+    }
+    pm1 = p0;
+    p0 = p1;
+    p1 = p2;
+  }
+}
+
+// CTA per (m, segment of <= kSeg degrees).  Outer loop over latitude
+// chunks of KC pairs, inner loop over chunks of 16 degrees.  MODE 0 builds
+// the prepared rows itself from the FFT'd products (fused prep); MODE 1 reads
+// them from A (prep_plain_kernel).
 template <int MODE>
-__global__ void __launch_bounds__(kAT) analysis_kernel(ShtView p, const double *A, double2 *out,
-                                                       int nf) {
+__global__ void __launch_bounds__(kAT) analysis_kernel(ShtView p, const double *A,
+                                                       const double2 *Q, const double2 *lcin,
+                                                       int atoms, double2 *out, int nf) {
   constexpr int NPART = MODE == 0 ? 2 : 1;
   extern __shared__ __align__(16) double sm[];
   const int KC = p.kc;
@@ -392,11 +456,14 @@ __global__ void __launch_bounds__(kAT) analysis_kernel(ShtView p, const double *
   double *res = red + 4 * 64;                             // [kAL][16]
   double4 *rcs = reinterpret_cast<double4 *>(res + kAL * 16);  // [kAL + 2]
 
-  const int m = blockIdx.x;
+  const int2 sg = p.d_segs[blockIdx.x];
+  const int m = sg.x, lseg = sg.y;
   const int T = p.trunc;
   const int kmax = T + 1 - m;
+  const int lend = min(T + 1, lseg + kSeg);
   const int off = col_offset(T, m);
   const double4 *rc = p.d_rc + rc_offset(T, m);
+  const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + (lseg - m) / kSeg) * 3 * p.nh;
   const double *Am = A + (size_t)m * NPART * 2 * p.nhp * kAS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = warp & 3, part = tile >> 1, par = tile & 1, khalf = warp >> 2;
@@ -409,15 +476,27 @@ __global__ void __launch_bounds__(kAT) analysis_kernel(ShtView p, const double *
     const bool first = i0 == 0;
     __syncthreads();
     // prepared Fourier rows for this latitude chunk
-    for (int t = tid; t < NPART * 2 * KC; t += kAT) {
-      const int r = t % KC, pp = t / KC;
-      const double *src = Am + ((size_t)pp * p.nhp + i0 + r) * kAS;
-      double *dst = As + ((size_t)pp * KC + r) * kAS;
-      const bool ok = r < ni;
+    if (MODE == 0) {
+      if (tid < KC) {
+        double2 ev[7], od[7];
+        tend_row(p, Q, lcin, atoms, m, i0 + tid, ev, od);
+        const size_t ps = (size_t)KC * kAS;
+        put_row(As + 0 * ps + (size_t)tid * kAS, ev, 4);
+        put_row(As + 1 * ps + (size_t)tid * kAS, od, 4);
+        put_row(As + 2 * ps + (size_t)tid * kAS, ev + 4, 3);
+        put_row(As + 3 * ps + (size_t)tid * kAS, od + 4, 3);
+      }
+    } else {
+      for (int t = tid; t < NPART * 2 * KC; t += kAT) {
+        const int r = t % KC, pp = t / KC;
+        const double *src = Am + ((size_t)pp * p.nhp + i0 + r) * kAS;
+        double *dst = As + ((size_t)pp * KC + r) * kAS;
+        const bool ok = r < ni;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) dst[c] = ok ? src[c] : 0.0;
+        for (int c = 0; c < 8; ++c) dst[c] = ok ? src[c] : 0.0;
+      }
     }
-    // recurrence state of this thread's latitude
+    // recurrence state of this thread's latitude at the segment start
     const bool gen = tid < KC;
     const bool has = tid < ni;
     double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
@@ -425,12 +504,12 @@ __global__ void __launch_bounds__(kAT) analysis_kernel(ShtView p, const double *
       const int i = i0 + tid;
       x = p.d_x[i];
       rcos = p.d_rcos[i];
-      const double seed = p.d_seed[(size_t)m * p.nh + i];
-      p0 = seed;
-      p1 = sqrt(2.0 * m + 3.0) * x * seed;
+      pm1 = ck[i];
+      p0 = ck[p.nh + i];
+      p1 = ck[2 * p.nh + i];
     }
-    for (int l0 = m; l0 <= T; l0 += kAL) {
-      const int nrow = min(kAL, T + 1 - l0);
+    for (int l0 = lseg; l0 < lend; l0 += kAL) {
+      const int nrow = min(kAL, lend - l0);
       const int k0 = l0 - m;
       __syncthreads();  // previous chunk's tiles / res fully consumed
       if (tid < kAL + 2 && k0 + tid <= kmax) rcs[tid] = rc[k0 + tid];
@@ -575,7 +654,7 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
   p->nlon = nlon;
   p->nm = trunc + 1;
   p->nh = (nlat + 1) / 2;
-  p->kc = p->nh <= 256 ? ((p->nh + 15) / 16) * 16 : 128;
+  p->kc = p->nh <= 128 ? ((p->nh + 15) / 16) * 16 : 128;
   p->nhp = ((p->nh + p->kc - 1) / p->kc) * p->kc;
   p->nfreq = nlon / 2 + 1;
   p->nlon_t = tendency_nlon(trunc, nlon);
@@ -649,6 +728,26 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     swx_sht_destroy(p);
     return fail(SWX_ERR_CUDA, std::string("sht create: ") + cudaGetErrorString(e));
   }
+  // l-segments and recurrence checkpoints (sphere.py:98-100 recurrence)
+  std::vector<int> segoff(T + 1);
+  std::vector<int2> segs;
+  for (int m = 0; m <= T; ++m) {
+    segoff[m] = (int)segs.size();
+    for (int l0 = m; l0 <= T; l0 += kSeg) segs.push_back(make_int2(m, l0));
+  }
+  p->nseg = (int)segs.size();
+  up((void **)&p->d_segoff, segoff.data(), sizeof(int) * segoff.size());
+  up((void **)&p->d_segs, segs.data(), sizeof(int2) * segs.size());
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_ckpt, sizeof(double) * 3 * (size_t)nh * segs.size());
+  if (e == cudaSuccess) {
+    ckpt_kernel<<<dim3(T + 1, (nh + 127) / 128), 128>>>(static_cast<const ShtView &>(*p));
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  if (e != cudaSuccess) {
+    swx_sht_destroy(p);
+    return fail(SWX_ERR_CUDA, std::string("sht checkpoints: ") + cudaGetErrorString(e));
+  }
   cufftHandle h;
   int rcd = get_plan(p, CUFFT_Z2D, p->nlon_t, 4 * nlat, &h);
   if (!rcd) rcd = get_plan(p, CUFFT_D2Z, p->nlon_t, 5 * nlat, &h);
@@ -673,6 +772,9 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_rc);
   cudaFree(p->d_lconst);
   cudaFree(p->d_frow);
+  cudaFree(p->d_segs);
+  cudaFree(p->d_segoff);
+  cudaFree(p->d_ckpt);
   delete p;
   return SWX_OK;
 }
@@ -718,12 +820,13 @@ static size_t analysis_smem(swx_sht p, int mode) {
 }
 
 template <int MODE>
-static int launch_analysis(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s) {
+static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const double2 *lc,
+                           int atoms, double2 *out, int nf, cudaStream_t s) {
   const size_t smem = analysis_smem(p, MODE);
   auto k = analysis_kernel<MODE>;
   if (smem > 48 * 1024)
     SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<p->nm, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
+  k<<<p->nseg, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, Q, lc, atoms, out, nf);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -763,10 +866,26 @@ static int check_ws(swx_sht p, void *ws, size_t bytes) {
   return SWX_OK;
 }
 
+static size_t synth_smem_bytes(int ns, int nh) {
+  const size_t stage = (size_t)kSynW * (kSeg * ns * 2 + (kSeg + 2) * 4) * sizeof(double);
+  const size_t red = (size_t)kSynW * 32 * 4 * (ns + nh) * sizeof(double);
+  return std::max(stage, red);
+}
+
+template <int MODE>
+static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
+  const size_t smem = MODE == 0 ? synth_smem_bytes(5, 2) : synth_smem_bytes(1, 0);
+  auto k = synth_kernel<MODE>;
+  if (smem > 48 * 1024)
+    SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<g, nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
 static dim3 synth_grid(swx_sht p, int nz, int *threads) {
-  const int nt = std::min(256, ((p->nh + 31) / 32) * 32);
-  *threads = nt;
-  return dim3(p->nm, (p->nh + nt - 1) / nt, nz);
+  *threads = kSynW * 32;
+  return dim3(p->nm, (p->nh + 31) / 32, nz);
 }
 
 extern "C" int swx_sht_synthesis(swx_sht p, int n_fields, const swx_c128 *d_coeffs,
@@ -785,8 +904,7 @@ extern "C" int swx_sht_synthesis(swx_sht p, int n_fields, const swx_c128 *d_coef
   a.nfreq = p->nfreq;
   int nt;
   dim3 g = synth_grid(p, n_fields, &nt);
-  synth_kernel<1><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
-  SWX_LAUNCH_CHECK();
+  if ((rc = launch_synth<1>(p, g, nt, a, s))) return rc;
   return c2r_exec(p, p->nlon, n_fields, w.c2r, d_grid, s);
 }
 
@@ -808,7 +926,8 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
     dim3 g((p->nhp + 127) / 128, p->nm);
     prep_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, nf, w.A);
     SWX_LAUNCH_CHECK();
-    if ((rc = launch_analysis<1>(p, w.A, out + (size_t)f0 * p->ncoef, nf, s))) return rc;
+    if ((rc = launch_analysis<1>(p, w.A, nullptr, nullptr, 0, out + (size_t)f0 * p->ncoef, nf, s)))
+      return rc;
   }
   return SWX_OK;
 }
@@ -825,9 +944,7 @@ static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, i
   a.nfreq = nfreq;
   int nt;
   dim3 g = synth_grid(p, 1, &nt);
-  synth_kernel<0><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
-  SWX_LAUNCH_CHECK();
-  return SWX_OK;
+  return launch_synth<0>(p, g, nt, a, s);
 }
 
 extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_div,
@@ -874,11 +991,8 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     mark(3);
   }
   mark(4);
-  dim3 g((p->nhp + 127) / 128, p->nm);
-  prep_tend_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.lc, atoms, w.A);
-  SWX_LAUNCH_CHECK();
-  mark(5);
-  if ((rc = launch_analysis<0>(p, w.A, out, 3, s))) return rc;
+  mark(5);  // prep is fused into the analysis kernel
+  if ((rc = launch_analysis<0>(p, w.A, w.Q, w.lc, atoms, out, 3, s))) return rc;
   mark(6);
   return SWX_OK;
 }
