@@ -13,13 +13,12 @@
 //    frexp/ldexp sectoral values, at the northern node of each equatorially
 //    symmetric latitude pair, and uses P(-x) = (-1)^(l+m) P(x),
 //    H(-x) = (-1)^(l+m+1) H(x) for the southern node.
-//  * Work is cut into (m, 64-degree segment) items; each item starts its
-//    recurrence from plan-time checkpoints (P_{l0-1}, P_{l0}, P_{l0+1}), so no
-//    CTA walks a whole 257-degree column (critical path / load balance).
-//  * synthesis: one lane per (latitude pair), a warp per segment, the
-//    segment's coefficients and recurrence constants staged in shared memory,
-//    parity-split sums of all series at once (DFMA); segment partials are
-//    combined in a fixed order.
+//  * Analysis work is cut into (m, 64-degree segment) items; each item starts
+//    its recurrence from plan-time checkpoints (P_{l0-1}, P_{l0}, P_{l0+1}),
+//    so no CTA walks a whole 257-degree column (critical path / balance).
+//  * synthesis: one thread per (latitude pair, m) walks l = m..T with the
+//    column's coefficients and recurrence constants staged in shared memory,
+//    accumulating parity-split sums of all series at once (DFMA).
 //  * analysis: per (m, segment), (16 l x latitude) tiles of P and H are
 //    generated into shared memory and contracted with the prepared Fourier
 //    data on the FP64 tensor cores (mma.sync m8n8k4 f64 = DMMA), K split over
@@ -89,69 +88,68 @@ struct SynthArgs {
   int nfreq;
 };
 
-constexpr int kSeg = 64;   // degrees per analysis/synthesis segment
-constexpr int kSynW = 8;   // warps per synthesis CTA (segments s = w, w+8, ...)
+constexpr int kSeg = 64;   // degrees per analysis segment
 
-// CTA = (m, block of 32 latitude pairs); warp w walks segments w, w+8, ... of
-// column m from the plan-time recurrence checkpoints, lane = latitude pair.
-// Segment partial sums are combined in a fixed order (per warp ascending,
-// then warps ascending): deterministic.
+constexpr int kSL = 128;  // l rows staged per chunk
+
 template <int MODE>
-__global__ void __launch_bounds__(kSynW * 32) synth_kernel(ShtView p, SynthArgs a) {
+__global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
-  constexpr int NACC = 4 * (NS + NH);    // doubles of parity-split partial sums
-  extern __shared__ __align__(16) double smem[];  // synth_smem_bytes(NS, NH)
+  __shared__ double2 cs[NS][kSL];
+  __shared__ double4 rcs[kSL + 2];
   const int m = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.y * 32 + lane;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
   const int field = MODE == 1 ? blockIdx.z : 0;
   const int T = p.trunc, nc = p.ncoef;
   const int off = col_offset(T, m);
   const int kmax = T + 1 - m;
-  const int nsg = (kmax + kSeg - 1) / kSeg;
   const double4 *rc = p.d_rc + rc_offset(T, m);
   const bool has = i < p.nh;
-  double2 *cs = reinterpret_cast<double2 *>(smem) + (size_t)warp * kSeg * NS;  // [kSeg][NS]
-  double4 *rcs = reinterpret_cast<double4 *>(smem + kSynW * kSeg * NS * 2) + (size_t)warp * (kSeg + 2);
-  double acc[NACC];
+  double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
+  if (has) {
+    x = p.d_x[i];
+    rcos = p.d_rcos[i];
+    const double seed = p.d_seed[(size_t)m * p.nh + i];
+    p0 = seed;
+    p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
+  }
+  double2 sp[2][NS], sh[2][NH > 0 ? NH : 1];
 #pragma unroll
-  for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
-  const double x = has ? p.d_x[i] : 0.0;
-  const double rcos = has ? p.d_rcos[i] : 0.0;
-  for (int sg = warp; sg < nsg; sg += kSynW) {
-    const int k0 = sg * kSeg;
-    const int n = min(kSeg, kmax - k0);
-    // stage this segment's coefficients and recurrence constants (warp-private)
-    for (int t = lane; t < kSeg + 2; t += 32)
-      if (k0 + t <= kmax) rcs[t] = rc[k0 + t];
-    for (int t = lane; t < n; t += 32) {
-      const int s = off + k0 + t;
+  for (int q = 0; q < 2; ++q) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) sp[q][s] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int s = 0; s < (NH > 0 ? NH : 1); ++s) sh[q][s] = make_double2(0.0, 0.0);
+  }
+  for (int l0 = m; l0 <= T; l0 += kSL) {
+    const int n = min(kSL, T + 1 - l0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kSL + 2; t += blockDim.x) {
+      const int k = l0 - m + t;
+      if (k <= kmax) rcs[t] = rc[k];
+    }
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int s = off + (l0 - m) + t;
       if (MODE == 0) {
-        const double il = p.d_lconst[m + k0 + t];
+        const double il = p.d_lconst[l0 + t];
         const double2 z = a.coef[nc + s], d = a.coef[2 * nc + s];
-        cs[t * NS + 0] = z;
-        cs[t * NS + (NS > 1 ? 1 : 0)] = d;
-        cs[t * NS + (NS > 2 ? 2 : 0)] = a.coef[s];
-        cs[t * NS + (NS > 3 ? 3 : 0)] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
-        cs[t * NS + (NS > 4 ? 4 : 0)] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+        cs[0][t] = z;
+        cs[1][t] = d;
+        cs[NS > 2 ? 2 : 0][t] = a.coef[s];
+        cs[NS > 3 ? 3 : 0][t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
+        cs[NS > 4 ? 4 : 0][t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
       } else {
-        cs[t] = a.coef[(size_t)field * nc + s];
+        cs[0][t] = a.coef[(size_t)field * nc + s];
       }
     }
-    __syncwarp();
-    const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + sg) * 3 * p.nh;
-    double pm1 = 0.0, p0 = 0.0, p1 = 0.0;
-    if (has) {
-      pm1 = ck[i];
-      p0 = ck[p.nh + i];
-      p1 = ck[2 * p.nh + i];
-    }
+    __syncthreads();
     for (int t = 0; t < n; t += 2) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {  // static parity: l - m = k0 + t + q, k0 even
+      for (int q = 0; q < 2; ++q) {  // static parity: l - m = (l0 - m) + t + q
         if (q == 1 && t + 1 >= n) break;
         const int tt = t + q;
+        const int k = l0 - m + tt;
         const double P = p0;
         double H = 0.0;
         if (NH > 0) {
@@ -160,19 +158,18 @@ __global__ void __launch_bounds__(kSynW * 32) synth_kernel(ShtView p, SynthArgs 
         }
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-          const double2 v = cs[tt * NS + s];
-          acc[(q * NS + s) * 2] = fma(P, v.x, acc[(q * NS + s) * 2]);
-          acc[(q * NS + s) * 2 + 1] = fma(P, v.y, acc[(q * NS + s) * 2 + 1]);
+          const double2 v = cs[s][tt];
+          sp[q][s].x = fma(P, v.x, sp[q][s].x);
+          sp[q][s].y = fma(P, v.y, sp[q][s].y);
         }
 #pragma unroll
         for (int s = 0; s < NH; ++s) {
-          const double2 v = cs[tt * NS + (NS > 3 ? 3 + s : 0)];
-          const int o = 4 * NS + (q * NH + s) * 2;
-          acc[o] = fma(H, v.x, acc[o]);
-          acc[o + 1] = fma(H, v.y, acc[o + 1]);
+          const double2 v = cs[NS > 3 ? 3 + s : 0][tt];
+          sh[q][s].x = fma(H, v.x, sh[q][s].x);
+          sh[q][s].y = fma(H, v.y, sh[q][s].y);
         }
         double p2 = 0.0;
-        if (k0 + tt + 2 <= kmax) {
+        if (k + 2 <= kmax) {
           const double4 c2 = rcs[tt + 2];
           p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
         }
@@ -181,34 +178,12 @@ __global__ void __launch_bounds__(kSynW * 32) synth_kernel(ShtView p, SynthArgs 
         p1 = p2;
       }
     }
-    __syncwarp();
   }
-  // combine the warps' partial sums in ascending warp order
-  __syncthreads();
-  double *red = smem;  // [kSynW][32][NACC] (reuses the staging area)
-#pragma unroll
-  for (int q = 0; q < NACC; ++q) red[((size_t)warp * 32 + lane) * NACC + q] = acc[q];
-  __syncthreads();
-  if (warp != 0 || !has) return;
-  for (int w = 1; w < kSynW && w < nsg; ++w) {
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) acc[q] += red[((size_t)w * 32 + lane) * NACC + q];
-  }
-  double2 sp[2][NS], sh[2][NH > 0 ? NH : 1];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-      sp[q][s] = make_double2(acc[(q * NS + s) * 2], acc[(q * NS + s) * 2 + 1]);
-#pragma unroll
-    for (int s = 0; s < (NH > 0 ? NH : 1); ++s) {
-      const int o = 4 * NS + (q * NH + s) * 2;
-      sh[q][s] = NH > 0 ? make_double2(acc[o], acc[o + 1]) : make_double2(0.0, 0.0);
-    }
-  }
+  if (!has) return;
   const int jn = p.d_jn[i], js = p.d_js[i];
   const int nf = a.nfreq;
   const size_t row = (size_t)p.nlat * nf;
+  // kSL is even and l0 - m advances by kSL, so sp[q] holds parity q of (l - m)
   if (MODE == 1) {
     double2 gn = make_double2(sp[0][0].x + sp[1][0].x, sp[0][0].y + sp[1][0].y);
     double2 gs = make_double2(sp[0][0].x - sp[1][0].x, sp[0][0].y - sp[1][0].y);
@@ -866,26 +841,17 @@ static int check_ws(swx_sht p, void *ws, size_t bytes) {
   return SWX_OK;
 }
 
-static size_t synth_smem_bytes(int ns, int nh) {
-  const size_t stage = (size_t)kSynW * (kSeg * ns * 2 + (kSeg + 2) * 4) * sizeof(double);
-  const size_t red = (size_t)kSynW * 32 * 4 * (ns + nh) * sizeof(double);
-  return std::max(stage, red);
-}
-
 template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
-  const size_t smem = MODE == 0 ? synth_smem_bytes(5, 2) : synth_smem_bytes(1, 0);
-  auto k = synth_kernel<MODE>;
-  if (smem > 48 * 1024)
-    SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<g, nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+  synth_kernel<MODE><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
 
 static dim3 synth_grid(swx_sht p, int nz, int *threads) {
-  *threads = kSynW * 32;
-  return dim3(p->nm, (p->nh + 31) / 32, nz);
+  const int nt = std::min(256, ((p->nh + 31) / 32) * 32);
+  *threads = nt;
+  return dim3(p->nm, (p->nh + nt - 1) / nt, nz);
 }
 
 extern "C" int swx_sht_synthesis(swx_sht p, int n_fields, const swx_c128 *d_coeffs,
