@@ -61,6 +61,8 @@ struct ShtView {
   int2 *d_segs = nullptr;
   int *d_segoff = nullptr;    // [m] index of the first segment of column m
   double *d_ckpt = nullptr;
+  int n_acta = 0;             // persistent analysis CTAs
+  int2 *d_arange = nullptr;   // [cta] contiguous range of work items
 };
 
 struct swx_sht_s : ShtView {
@@ -413,159 +415,197 @@ __global__ void ckpt_kernel(ShtView p) {
   }
 }
 
-// CTA per (m, segment of <= kSeg degrees).  Outer loop over latitude
-// chunks of KC pairs, inner loop over chunks of 16 degrees.  MODE 0 builds
-// the prepared rows itself from the FFT'd products (fused prep); MODE 1 reads
-// them from A (prep_plain_kernel).
+// Persistent, warp-specialised analysis.  One CTA per SM walks a contiguous,
+// cost-balanced range of (m, segment) work items (sorted by m, so the
+// prepared rows of a column are built once per CTA and column).  Per item,
+// warps 4..7 (producers) walk the recurrence from the plan-time checkpoint
+// and write 16-degree P/H tiles into a double buffer; warps 0..3 (consumers)
+// contract each tile with the prepared rows on the FP64 tensor cores
+// (one 8x8 output tile per warp: table P|H x parity) and write the result.
+// Producer/consumer hand-off uses named barriers (FULL/EMPTY per buffer).
+constexpr int kBarFull = 1, kBarEmpty = 3, kBarCons = 5;
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kAT) analysis_kernel(ShtView p, const double *A,
-                                                       const double2 *Q, const double2 *lcin,
-                                                       int atoms, double2 *out, int nf) {
+__global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const double *A,
+                                                          const double2 *Q, const double2 *lcin,
+                                                          int atoms, double2 *out, int nf) {
   constexpr int NPART = MODE == 0 ? 2 : 1;
   extern __shared__ __align__(16) double sm[];
   const int KC = p.kc;
-  double *Pt = sm;                                        // [KC][kRS]
-  double *Ht = Pt + (size_t)KC * kRS;                     // [KC][kRS]   (MODE 0)
-  double *As = Ht + (MODE == 0 ? (size_t)KC * kRS : 0);   // [part][par][KC][kAS]
-  double *red = As + (size_t)NPART * 2 * KC * kAS;        // [4][32][2]
-  double *res = red + 4 * 64;                             // [kAL][16]
-  double4 *rcs = reinterpret_cast<double4 *>(res + kAL * 16);  // [kAL + 2]
+  const size_t tile = (size_t)KC * kRS;
+  double *Tb = sm;                                   // [2 buf][NPART][KC][kRS]
+  double *As = Tb + 2 * NPART * tile;                // [part][par][KC][kAS]
+  double *res = As + (size_t)NPART * 2 * KC * kAS;   // [2 buf][kAL][16]
 
-  const int2 sg = p.d_segs[blockIdx.x];
-  const int m = sg.x, lseg = sg.y;
   const int T = p.trunc;
-  const int kmax = T + 1 - m;
-  const int lend = min(T + 1, lseg + kSeg);
-  const int off = col_offset(T, m);
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + (lseg - m) / kSeg) * 3 * p.nh;
-  const double *Am = A + (size_t)m * NPART * 2 * p.nhp * kAS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = warp & 3, part = tile >> 1, par = tile & 1, khalf = warp >> 2;
-  const int apar = part ? (par ^ 1) : par;  // H has the opposite fold parity
-  const bool mma_warp = MODE == 0 || part == 0;
+  const bool producer = warp >= 4;
+  const int ptid = tid - 128;                       // producer thread index
+  // consumer roles
+  const int ctile = warp & 3, part = ctile >> 1, par = ctile & 1;
+  const int apar = part ? (par ^ 1) : par;          // H has the opposite fold parity
+  const bool mma_warp = !producer && (MODE == 0 || part == 0);
   const int lr = lane >> 2, lc4 = lane & 3;
 
-  for (int i0 = 0; i0 < p.nh; i0 += KC) {
-    const int ni = min(KC, p.nh - i0);
-    const bool first = i0 == 0;
-    __syncthreads();
-    // prepared Fourier rows for this latitude chunk
-    if (MODE == 0) {
-      if (tid < KC) {
-        double2 ev[7], od[7];
-        tend_row(p, Q, lcin, atoms, m, i0 + tid, ev, od);
-        const size_t ps = (size_t)KC * kAS;
-        put_row(As + 0 * ps + (size_t)tid * kAS, ev, 4);
-        put_row(As + 1 * ps + (size_t)tid * kAS, od, 4);
-        put_row(As + 2 * ps + (size_t)tid * kAS, ev + 4, 3);
-        put_row(As + 3 * ps + (size_t)tid * kAS, od + 4, 3);
-      }
-    } else {
-      for (int t = tid; t < NPART * 2 * KC; t += kAT) {
-        const int r = t % KC, pp = t / KC;
-        const double *src = Am + ((size_t)pp * p.nhp + i0 + r) * kAS;
-        double *dst = As + ((size_t)pp * KC + r) * kAS;
-        const bool ok = r < ni;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) dst[c] = ok ? src[c] : 0.0;
-      }
-    }
-    // recurrence state of this thread's latitude at the segment start
-    const bool gen = tid < KC;
-    const bool has = tid < ni;
-    double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
-    if (has) {
-      const int i = i0 + tid;
-      x = p.d_x[i];
-      rcos = p.d_rcos[i];
-      pm1 = ck[i];
-      p0 = ck[p.nh + i];
-      p1 = ck[2 * p.nh + i];
-    }
-    for (int l0 = lseg; l0 < lend; l0 += kAL) {
-      const int nrow = min(kAL, lend - l0);
-      const int k0 = l0 - m;
-      __syncthreads();  // previous chunk's tiles / res fully consumed
-      if (tid < kAL + 2 && k0 + tid <= kmax) rcs[tid] = rc[k0 + tid];
-      __syncthreads();
-      if (gen) {
-#pragma unroll 4
-        for (int rr = 0; rr < kAL; ++rr) {
-          double pv = 0.0, hv = 0.0;
-          if (rr < nrow && has) {
-            pv = p0;
-            if (MODE == 0) {
-              const double4 c = rcs[rr];
-              hv = (c.z * pm1 - c.w * p1) * rcos;
-            }
-            double p2 = 0.0;
-            if (k0 + rr + 2 <= kmax) {
-              const double4 c2 = rcs[rr + 2];
-              p2 = fma(x, p1, -c2.x * p0) * c2.y;
-            }
-            pm1 = p0;
-            p0 = p1;
-            p1 = p2;
-          }
-          const int slot = (rr & 1) * 8 + (rr >> 1);
-          Pt[tid * kRS + slot] = pv;
-          if (MODE == 0) Ht[tid * kRS + slot] = hv;
-        }
-      }
-      __syncthreads();
-      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-      if (mma_warp) {
-        const double *Tt = part ? Ht : Pt;
-        const double *Ab = As + (size_t)(part * 2 + apar) * KC * kAS;
-        const int kb = khalf * (KC >> 1), ke = kb + (KC >> 1);
-        const int arow = par * 8 + lr;
-        for (int k = kb; k < ke; k += 8) {
-          dmma(c0, c1, Tt[(k + lc4) * kRS + arow], Ab[(k + lc4) * kAS + lr]);
-          dmma(e0, e1, Tt[(k + 4 + lc4) * kRS + arow], Ab[(k + 4 + lc4) * kAS + lr]);
-        }
-        c0 += e0;
-        c1 += e1;
-        if (khalf == 1) {
-          red[(tile * 32 + lane) * 2] = c0;
-          red[(tile * 32 + lane) * 2 + 1] = c1;
-        }
-      }
-      __syncthreads();
-      if (mma_warp && khalf == 0) {
-        c0 += red[(tile * 32 + lane) * 2];
-        c1 += red[(tile * 32 + lane) * 2 + 1];
-        const int rr = 2 * lr + par;  // C row lr of this parity tile
-        res[rr * 16 + part * 8 + 2 * lc4] = c0;
-        res[rr * 16 + part * 8 + 2 * lc4 + 1] = c1;
-      }
-      __syncthreads();
-      if (tid < nrow) {
-        const int l = l0 + tid;
-        const int slot = off + (l - m);
-        const double *r = res + tid * 16;
+  const int2 range = p.d_arange[blockIdx.x];
+  int cur_m = -1;
+  for (int it = range.x; it < range.y; ++it) {
+    const int2 sg = p.d_segs[it];
+    const int m = sg.x, lseg = sg.y;
+    const int kmax = T + 1 - m;
+    const int lend = min(T + 1, lseg + kSeg);
+    const int nc = (lend - lseg + kAL - 1) / kAL;
+    const int off = col_offset(T, m);
+    const double4 *rc = p.d_rc + rc_offset(T, m);
+    const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + (lseg - m) / kSeg) * 3 * p.nh;
+    for (int i0 = 0; i0 < p.nh; i0 += KC) {
+      const int ni = min(KC, p.nh - i0);
+      const bool first = i0 == 0;
+      __syncthreads();  // previous item fully done with As / buffers
+      if (m != cur_m || KC < p.nh) {
         if (MODE == 0) {
-          const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
-          double2 v0 = make_double2(r[4] + r[12], r[5] + r[13]);                            // dphi'
-          double2 v1 = make_double2(r[0] + r[8], r[1] + r[9]);                              // dvort
-          double2 v2 = make_double2(r[2] + r[10] + llk * r[6], r[3] + r[11] + llk * r[7]);  // ddiv
-          if (!first) {
-            const double2 a0 = out[slot], a1 = out[p.ncoef + slot], a2 = out[2 * p.ncoef + slot];
-            v0 = make_double2(a0.x + v0.x, a0.y + v0.y);
-            v1 = make_double2(a1.x + v1.x, a1.y + v1.y);
-            v2 = make_double2(a2.x + v2.x, a2.y + v2.y);
+          if (tid < KC) {
+            double2 ev[7], od[7];
+            tend_row(p, Q, lcin, atoms, m, i0 + tid, ev, od);
+            const size_t ps = (size_t)KC * kAS;
+            put_row(As + 0 * ps + (size_t)tid * kAS, ev, 4);
+            put_row(As + 1 * ps + (size_t)tid * kAS, od, 4);
+            put_row(As + 2 * ps + (size_t)tid * kAS, ev + 4, 3);
+            put_row(As + 3 * ps + (size_t)tid * kAS, od + 4, 3);
           }
-          out[slot] = v0;
-          out[p.ncoef + slot] = v1;
-          out[2 * p.ncoef + slot] = v2;
         } else {
-          for (int f = 0; f < nf; ++f) {
-            double2 v = make_double2(r[2 * f], r[2 * f + 1]);
-            if (!first) {
-              const double2 a0 = out[(size_t)f * p.ncoef + slot];
-              v = make_double2(a0.x + v.x, a0.y + v.y);
+          const double *Am = A + (size_t)m * NPART * 2 * p.nhp * kAS;
+          for (int t = tid; t < NPART * 2 * KC; t += kAT) {
+            const int r = t % KC, pp = t / KC;
+            const double *src = Am + ((size_t)pp * p.nhp + i0 + r) * kAS;
+            double *dst = As + ((size_t)pp * KC + r) * kAS;
+            const bool ok = r < ni;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dst[c] = ok ? src[c] : 0.0;
+          }
+        }
+        cur_m = m;
+      }
+      __syncthreads();
+      if (producer) {
+        // up to two latitudes per producer thread: ptid and ptid + 128
+        double x[2], rcos[2], pm1[2], p0[2], p1[2];
+        bool has[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int t = ptid + 128 * u;
+          has[u] = t < ni;
+          x[u] = rcos[u] = pm1[u] = p0[u] = p1[u] = 0.0;
+          if (has[u]) {
+            const int i = i0 + t;
+            x[u] = p.d_x[i];
+            rcos[u] = p.d_rcos[i];
+            pm1[u] = ck[i];
+            p0[u] = ck[p.nh + i];
+            p1[u] = ck[2 * p.nh + i];
+          }
+        }
+        for (int c = 0; c < nc; ++c) {
+          const int b = c & 1;
+          if (c >= 2) bar_sync(kBarEmpty + b, kAT);
+          const int l0 = lseg + c * kAL;
+          const int nrow = min(kAL, lend - l0);
+          const int k0 = l0 - m;
+          double *Pt = Tb + (size_t)b * NPART * tile;
+          double *Ht = Pt + tile;
+#pragma unroll 2
+          for (int rr = 0; rr < kAL; ++rr) {
+            const int slot = (rr & 1) * 8 + (rr >> 1);
+            const bool live = rr < nrow;
+            double4 ch = make_double4(0, 0, 0, 0), c2 = ch;
+            if (live) {
+              if (MODE == 0) ch = rc[k0 + rr];
+              if (k0 + rr + 2 <= kmax) c2 = rc[k0 + rr + 2];
             }
-            out[(size_t)f * p.ncoef + slot] = v;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int t = ptid + 128 * u;
+              if (t >= KC) continue;
+              double pv = 0.0, hv = 0.0;
+              if (live && has[u]) {
+                pv = p0[u];
+                if (MODE == 0) hv = (ch.z * pm1[u] - ch.w * p1[u]) * rcos[u];
+                const double p2 = (k0 + rr + 2 <= kmax) ? fma(x[u], p1[u], -c2.x * p0[u]) * c2.y : 0.0;
+                pm1[u] = p0[u];
+                p0[u] = p1[u];
+                p1[u] = p2;
+              }
+              Pt[t * kRS + slot] = pv;
+              if (MODE == 0) Ht[t * kRS + slot] = hv;
+            }
+          }
+          bar_arrive(kBarFull + b, kAT);
+        }
+      } else {
+        for (int c = 0; c < nc; ++c) {
+          const int b = c & 1;
+          bar_sync(kBarFull + b, kAT);
+          const int l0 = lseg + c * kAL;
+          const int nrow = min(kAL, lend - l0);
+          double *rs = res + (size_t)b * kAL * 16;
+          if (mma_warp) {
+            const double *Tt = Tb + (size_t)b * NPART * tile + (size_t)part * tile;
+            const double *Ab = As + (size_t)(part * 2 + apar) * KC * kAS;
+            const int arow = par * 8 + lr;
+            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;
+            int k = 0;
+            for (; k + 16 <= KC; k += 16) {
+              dmma(c0, c1, Tt[(k + lc4) * kRS + arow], Ab[(k + lc4) * kAS + lr]);
+              dmma(e0, e1, Tt[(k + 4 + lc4) * kRS + arow], Ab[(k + 4 + lc4) * kAS + lr]);
+              dmma(f0, f1, Tt[(k + 8 + lc4) * kRS + arow], Ab[(k + 8 + lc4) * kAS + lr]);
+              dmma(g0, g1, Tt[(k + 12 + lc4) * kRS + arow], Ab[(k + 12 + lc4) * kAS + lr]);
+            }
+            for (; k < KC; k += 4) dmma(c0, c1, Tt[(k + lc4) * kRS + arow], Ab[(k + lc4) * kAS + lr]);
+            if (c + 2 < nc) bar_arrive(kBarEmpty + b, kAT);
+            c0 = (c0 + e0) + (f0 + g0);
+            c1 = (c1 + e1) + (f1 + g1);
+            const int rr = 2 * lr + par;  // C row lr of this parity tile
+            rs[rr * 16 + part * 8 + 2 * lc4] = c0;
+            rs[rr * 16 + part * 8 + 2 * lc4 + 1] = c1;
+          } else if (c + 2 < nc) {
+            bar_arrive(kBarEmpty + b, kAT);
+          }
+          bar_sync(kBarCons, 128);
+          if (tid < nrow) {
+            const int l = l0 + tid;
+            const int slot = off + (l - m);
+            const double *r = rs + tid * 16;
+            if (MODE == 0) {
+              const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
+              double2 v0 = make_double2(r[4] + r[12], r[5] + r[13]);                            // dphi'
+              double2 v1 = make_double2(r[0] + r[8], r[1] + r[9]);                              // dvort
+              double2 v2 = make_double2(r[2] + r[10] + llk * r[6], r[3] + r[11] + llk * r[7]);  // ddiv
+              if (!first) {
+                const double2 a0 = out[slot], a1 = out[p.ncoef + slot], a2 = out[2 * p.ncoef + slot];
+                v0 = make_double2(a0.x + v0.x, a0.y + v0.y);
+                v1 = make_double2(a1.x + v1.x, a1.y + v1.y);
+                v2 = make_double2(a2.x + v2.x, a2.y + v2.y);
+              }
+              out[slot] = v0;
+              out[p.ncoef + slot] = v1;
+              out[2 * p.ncoef + slot] = v2;
+            } else {
+              for (int f = 0; f < nf; ++f) {
+                double2 v = make_double2(r[2 * f], r[2 * f + 1]);
+                if (!first) {
+                  const double2 a0 = out[(size_t)f * p.ncoef + slot];
+                  v = make_double2(a0.x + v.x, a0.y + v.y);
+                }
+                out[(size_t)f * p.ncoef + slot] = v;
+              }
+            }
           }
         }
       }
@@ -629,7 +669,7 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
   p->nlon = nlon;
   p->nm = trunc + 1;
   p->nh = (nlat + 1) / 2;
-  p->kc = p->nh <= 128 ? ((p->nh + 15) / 16) * 16 : 128;
+  p->kc = p->nh <= 256 ? ((p->nh + 15) / 16) * 16 : 128;
   p->nhp = ((p->nh + p->kc - 1) / p->kc) * p->kc;
   p->nfreq = nlon / 2 + 1;
   p->nlon_t = tendency_nlon(trunc, nlon);
@@ -711,6 +751,31 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     for (int l0 = m; l0 <= T; l0 += kSeg) segs.push_back(make_int2(m, l0));
   }
   p->nseg = (int)segs.size();
+  {
+    // cost-balanced contiguous ranges of work items, one per SM
+    const int g = std::max(1, std::min(sm_count(), p->nseg));
+    std::vector<double> cost(segs.size());
+    double total = 0;
+    for (size_t k = 0; k < segs.size(); ++k) {
+      const int rows = std::min(kSeg, T + 1 - segs[k].y);
+      cost[k] = 4.0 + (rows + kAL - 1) / kAL;  // chunk count + per-item overhead
+      total += cost[k];
+    }
+    std::vector<int2> ranges;
+    double acc = 0;
+    int begin = 0;
+    for (size_t k = 0; k < segs.size(); ++k) {
+      acc += cost[k];
+      const double target = total * (ranges.size() + 1) / g;
+      if (acc >= target - 1e-9 && (int)ranges.size() < g - 1) {
+        ranges.push_back(make_int2(begin, (int)k + 1));
+        begin = (int)k + 1;
+      }
+    }
+    ranges.push_back(make_int2(begin, (int)segs.size()));
+    p->n_acta = (int)ranges.size();
+    up((void **)&p->d_arange, ranges.data(), sizeof(int2) * ranges.size());
+  }
   up((void **)&p->d_segoff, segoff.data(), sizeof(int) * segoff.size());
   up((void **)&p->d_segs, segs.data(), sizeof(int2) * segs.size());
   if (e == cudaSuccess) e = cudaMalloc(&p->d_ckpt, sizeof(double) * 3 * (size_t)nh * segs.size());
@@ -750,6 +815,7 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_segs);
   cudaFree(p->d_segoff);
   cudaFree(p->d_ckpt);
+  cudaFree(p->d_arange);
   delete p;
   return SWX_OK;
 }
@@ -789,9 +855,7 @@ extern "C" size_t swx_sht_workspace_bytes(swx_sht p) {
 static size_t analysis_smem(swx_sht p, int mode) {
   const size_t npart = mode == 0 ? 2 : 1;
   const size_t kc = p->kc;
-  return sizeof(double) * (kc * kRS * (mode == 0 ? 2 : 1) + npart * 2 * kc * kAS + 4 * 64 +
-                           kAL * 16) +
-         sizeof(double4) * (kAL + 2);
+  return sizeof(double) * (2 * npart * kc * kRS + npart * 2 * kc * kAS + 2 * kAL * 16);
 }
 
 template <int MODE>
@@ -801,7 +865,7 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
   auto k = analysis_kernel<MODE>;
   if (smem > 48 * 1024)
     SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<p->nseg, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, Q, lc, atoms, out, nf);
+  k<<<p->n_acta, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, Q, lc, atoms, out, nf);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
