@@ -439,10 +439,12 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
   constexpr int NPART = MODE == 0 ? 2 : 1;
   extern __shared__ __align__(16) double sm[];
   const int KC = p.kc;
-  const size_t tile = (size_t)KC * kRS;
-  double *Tb = sm;                                   // [2 buf][NPART][KC][kRS]
+  const int KP = KC + 4;                             // tile row stride: KP % 16 == 4
+  const size_t tile = (size_t)kAL * KP;
+  double *Tb = sm;                                   // [2 buf][NPART][16 slots][KP]
   double *As = Tb + 2 * NPART * tile;                // [part][par][KC][kAS]
   double *res = As + (size_t)NPART * 2 * KC * kAS;   // [2 buf][kAL][16]
+  double4 *rcs = reinterpret_cast<double4 *>(res + 2 * kAL * 16);  // [kSeg + 2]
 
   const int T = p.trunc;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -469,6 +471,11 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
       const int ni = min(KC, p.nh - i0);
       const bool first = i0 == 0;
       __syncthreads();  // previous item fully done with As / buffers
+      // recurrence constants of this segment (k = lseg-m .. lseg-m+kSeg+1)
+      for (int t = tid; t < kSeg + 2; t += kAT) {
+        const int kk = lseg - m + t;
+        if (kk <= kmax) rcs[t] = rc[kk];
+      }
       if (m != cur_m || KC < p.nh) {
         if (MODE == 0) {
           if (tid < KC) {
@@ -518,6 +525,7 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
           const int l0 = lseg + c * kAL;
           const int nrow = min(kAL, lend - l0);
           const int k0 = l0 - m;
+          const int ks = c * kAL;  // index into rcs
           double *Pt = Tb + (size_t)b * NPART * tile;
           double *Ht = Pt + tile;
 #pragma unroll 2
@@ -526,8 +534,8 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
             const bool live = rr < nrow;
             double4 ch = make_double4(0, 0, 0, 0), c2 = ch;
             if (live) {
-              if (MODE == 0) ch = rc[k0 + rr];
-              if (k0 + rr + 2 <= kmax) c2 = rc[k0 + rr + 2];
+              if (MODE == 0) ch = rcs[ks + rr];
+              if (k0 + rr + 2 <= kmax) c2 = rcs[ks + rr + 2];
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
@@ -542,8 +550,8 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
                 p0[u] = p1[u];
                 p1[u] = p2;
               }
-              Pt[t * kRS + slot] = pv;
-              if (MODE == 0) Ht[t * kRS + slot] = hv;
+              Pt[slot * KP + t] = pv;
+              if (MODE == 0) Ht[slot * KP + t] = hv;
             }
           }
           bar_arrive(kBarFull + b, kAT);
@@ -558,16 +566,17 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
           if (mma_warp) {
             const double *Tt = Tb + (size_t)b * NPART * tile + (size_t)part * tile;
             const double *Ab = As + (size_t)(part * 2 + apar) * KC * kAS;
-            const int arow = par * 8 + lr;
+            const double *Ta = Tt + (size_t)(par * 8 + lr) * KP + lc4;  // A fragment row
+            const double *Bb = Ab + (size_t)lc4 * kAS + lr;              // B fragment column
             double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;
             int k = 0;
             for (; k + 16 <= KC; k += 16) {
-              dmma(c0, c1, Tt[(k + lc4) * kRS + arow], Ab[(k + lc4) * kAS + lr]);
-              dmma(e0, e1, Tt[(k + 4 + lc4) * kRS + arow], Ab[(k + 4 + lc4) * kAS + lr]);
-              dmma(f0, f1, Tt[(k + 8 + lc4) * kRS + arow], Ab[(k + 8 + lc4) * kAS + lr]);
-              dmma(g0, g1, Tt[(k + 12 + lc4) * kRS + arow], Ab[(k + 12 + lc4) * kAS + lr]);
+              dmma(c0, c1, Ta[k], Bb[k * kAS]);
+              dmma(e0, e1, Ta[k + 4], Bb[(k + 4) * kAS]);
+              dmma(f0, f1, Ta[k + 8], Bb[(k + 8) * kAS]);
+              dmma(g0, g1, Ta[k + 12], Bb[(k + 12) * kAS]);
             }
-            for (; k < KC; k += 4) dmma(c0, c1, Tt[(k + lc4) * kRS + arow], Ab[(k + lc4) * kAS + lr]);
+            for (; k < KC; k += 4) dmma(c0, c1, Ta[k], Bb[k * kAS]);
             if (c + 2 < nc) bar_arrive(kBarEmpty + b, kAT);
             c0 = (c0 + e0) + (f0 + g0);
             c1 = (c1 + e1) + (f1 + g1);
@@ -855,7 +864,8 @@ extern "C" size_t swx_sht_workspace_bytes(swx_sht p) {
 static size_t analysis_smem(swx_sht p, int mode) {
   const size_t npart = mode == 0 ? 2 : 1;
   const size_t kc = p->kc;
-  return sizeof(double) * (2 * npart * kc * kRS + npart * 2 * kc * kAS + 2 * kAL * 16);
+  return sizeof(double) * (2 * npart * kAL * (kc + 4) + npart * 2 * kc * kAS + 2 * kAL * 16) +
+         sizeof(double4) * (kSeg + 2);
 }
 
 template <int MODE>
