@@ -63,6 +63,16 @@ struct ShtView {
   double *d_ckpt = nullptr;
   int n_acta = 0;             // persistent analysis CTAs
   int2 *d_arange = nullptr;   // [cta] contiguous range of work items
+  // table path (T small enough): Pbar at the north node of each pair,
+  // parity-split planes per column: ptab[ptoff[m] + (par*half(m) + r)*nt16 + pair]
+  // with l - m = 2r + par, l = m..T+1, half(m) = (T+3-m)/2
+  int use_tab = 0;
+  int nt16 = 0;                // pairs padded to 16
+  long long *d_ptoff = nullptr;
+  double *d_ptab = nullptr;
+  double *d_rcos16 = nullptr;  // 1/cos per padded pair (0 on padding)
+  int n_titems = 0;            // analysis warp items (m, l0, par)
+  int4 *d_titems = nullptr;
 };
 
 struct swx_sht_s : ShtView {
@@ -94,7 +104,7 @@ constexpr int kSeg = 64;   // degrees per analysis segment
 
 constexpr int kSL = 128;  // l rows staged per chunk
 
-template <int MODE>
+template <int MODE, bool TAB>
 __global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
@@ -109,12 +119,24 @@ __global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
   const double4 *rc = p.d_rc + rc_offset(T, m);
   const bool has = i < p.nh;
   double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
+  // table path: plane pointers of column m (pair i)
+  const double *tp0 = nullptr, *tp1 = nullptr;
+  if (TAB) {
+    const int half = (T + 3 - m) >> 1;
+    tp0 = p.d_ptab + p.d_ptoff[m] + i;
+    tp1 = tp0 + (size_t)half * p.nt16;
+  }
   if (has) {
     x = p.d_x[i];
     rcos = p.d_rcos[i];
-    const double seed = p.d_seed[(size_t)m * p.nh + i];
-    p0 = seed;
-    p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
+    if (TAB) {
+      p0 = tp0[0];
+      p1 = tp1[0];
+    } else {
+      const double seed = p.d_seed[(size_t)m * p.nh + i];
+      p0 = seed;
+      p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
+    }
   }
   double2 sp[2][NS], sh[2][NH > 0 ? NH : 1];
 #pragma unroll
@@ -172,8 +194,12 @@ __global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
         }
         double p2 = 0.0;
         if (k + 2 <= kmax) {
-          const double4 c2 = rcs[tt + 2];
-          p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
+          if (TAB) {
+            if (has) p2 = ((k + 2) & 1 ? tp1 : tp0)[(size_t)((k + 2) >> 1) * p.nt16];
+          } else {
+            const double4 c2 = rcs[tt + 2];
+            p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
+          }
         }
         pm1 = p0;
         p0 = p1;
@@ -622,6 +648,173 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
   }
 }
 
+// ---------------------------------------------------------------------
+// Table path.  Pbar_l^m at the north node of every pair is precomputed at
+// plan time with the same recurrence (bit-identical to the walkers); the
+// transforms then stream it instead of re-running the recurrence, and
+// H = dP/dlat is formed from the P neighbours (sphere.py:102-111).
+// ---------------------------------------------------------------------
+__global__ void ptab_kernel(ShtView p) {
+  const int m = blockIdx.x;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= p.nt16) return;
+  const int T = p.trunc, kmax = T + 1 - m;
+  const int half = (T + 3 - m) >> 1;
+  double *t0 = p.d_ptab + p.d_ptoff[m] + i;
+  double *t1 = t0 + (size_t)half * p.nt16;
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  double x = 0.0, p0 = 0.0, p1 = 0.0;
+  if (i < p.nh) {
+    x = p.d_x[i];
+    const double seed = p.d_seed[(size_t)m * p.nh + i];
+    p0 = seed;
+    p1 = sqrt(2.0 * m + 3.0) * x * seed;
+  }
+  for (int k = 0; k <= kmax; ++k) {
+    ((k & 1) ? t1 : t0)[(size_t)(k >> 1) * p.nt16] = p0;
+    double p2 = 0.0;
+    if (k + 2 <= kmax) {
+      const double4 c2 = rc[k + 2];
+      p2 = fma(x, p1, -c2.x * p0) * c2.y;
+    }
+    p0 = p1;
+    p1 = p2;
+  }
+  if (((kmax + 1) & 1) == 1) t1[(size_t)(kmax >> 1) * p.nt16] = 0.0;  // unused tail row
+}
+
+// prepared rows for the table analysis: Ag[m][part][par][nt16][8]
+constexpr int kAG = 8;
+__global__ void prep_tab_tend_kernel(ShtView p, const double2 *Q, const double2 *lc, int atoms,
+                                     double *A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (i >= p.nt16) return;
+  double2 ev[7], od[7];
+  tend_row(p, Q, lc, atoms, m, i, ev, od);
+  const size_t ps = (size_t)p.nt16 * kAG;
+  double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+  put_row(base + 0 * ps, ev, 4);
+  put_row(base + 1 * ps, od, 4);
+  put_row(base + 2 * ps, ev + 4, 3);
+  put_row(base + 3 * ps, od + 4, 3);
+}
+
+__global__ void prep_tab_plain_kernel(ShtView p, const double2 *Q, int nf, double *A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (i >= p.nt16) return;
+  double2 ev[4], od[4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) ev[f] = od[f] = make_double2(0.0, 0.0);
+  if (i < p.nh) {
+    const int jn = p.d_jn[i], js = p.d_js[i];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      if (f >= nf) break;
+      const size_t row = (size_t)f * p.nlat * p.nfreq;
+      const double2 qn = Q[row + (size_t)jn * p.nfreq + m];
+      const double wn = p.d_wn[i] * p.dlon;
+      const double2 an = make_double2(qn.x * wn, qn.y * wn);
+      double2 as = make_double2(0.0, 0.0);
+      if (js != jn) {
+        const double2 qs = Q[row + (size_t)js * p.nfreq + m];
+        const double ws = p.d_ws[i] * p.dlon;
+        as = make_double2(qs.x * ws, qs.y * ws);
+      }
+      ev[f] = make_double2(an.x + as.x, an.y + as.y);
+      od[f] = js == jn ? an : make_double2(an.x - as.x, an.y - as.y);
+    }
+  }
+  const size_t ps = (size_t)p.nt16 * kAG;
+  double *base = A + (size_t)m * 2 * ps + (size_t)i * kAG;
+  put_row(base, ev, 4);
+  put_row(base + ps, od, 4);
+}
+
+// Table analysis: one warp = (m, 16 degrees l0..l0+15, parity).  The warp's
+// two 8x8 outputs (P table and H table columns) accumulate over all latitude
+// pairs with m8n8k4 DMMA; A fragments are loaded straight from the table
+// (8 rows x 32 B per load), H rows are formed from the other parity plane.
+template <int MODE>
+__global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const double *A,
+                                                           double2 *out, int nf) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= p.n_titems) return;
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc4 = lane & 3;
+  const int4 itm = p.d_titems[gw];
+  const int m = itm.x, l0 = itm.y, par = itm.z;
+  const int T = p.trunc, nt = p.nt16;
+  const int half = (T + 3 - m) >> 1;
+  const double *P0 = p.d_ptab + p.d_ptoff[m];
+  const double *Pp = P0 + (size_t)(par ? half : 0) * nt;  // own parity plane
+  const double *Po = P0 + (size_t)(par ? 0 : half) * nt;  // other parity plane
+  const int r = ((l0 - m) >> 1) + lr;
+  const int l = m + 2 * r + par;
+  const bool valid = l <= T;
+  const double *arow = Pp + (size_t)(valid ? r : 0) * nt + lc4;
+  double cz = 0.0, cw = 0.0;
+  const double *hm = Po + lc4, *hp = Po + lc4;
+  bool hasm = false;
+  if (MODE == 0 && valid) {
+    const double4 c = p.d_rc[rc_offset(T, m) + (l - m)];
+    cz = c.z;
+    cw = c.w;
+    // P_{l-1}, P_{l+1} live in the other plane: rows (r, r+1) for par = 1,
+    // (r-1, r) for par = 0
+    const int rm = par ? r : r - 1, rp = par ? r + 1 : r;
+    hasm = rm >= 0;
+    hm = Po + (size_t)(hasm ? rm : 0) * nt + lc4;
+    hp = Po + (size_t)rp * nt + lc4;
+  }
+  const size_t ps = (size_t)nt * kAG;
+  constexpr int NPART = MODE == 0 ? 2 : 1;
+  const double *Ab = A + (size_t)m * NPART * 2 * ps;
+  const double *Bp = Ab + (size_t)(0 * 2 + par) * ps + (size_t)lc4 * kAG + lr;
+  const double *Bh = Ab + (size_t)(1 * 2 + (par ^ 1)) * ps + (size_t)lc4 * kAG + lr;
+  const double *rcs = p.d_rcos16 + lc4;
+  double cp0 = 0.0, cp1 = 0.0, ch0 = 0.0, ch1 = 0.0;
+  double dp0 = 0.0, dp1 = 0.0, dh0 = 0.0, dh1 = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < nt; k += 8) {
+    const double a0 = valid ? arow[k] : 0.0;
+    const double a1 = valid ? arow[k + 4] : 0.0;
+    dmma(cp0, cp1, a0, Bp[(size_t)k * kAG]);
+    dmma(dp0, dp1, a1, Bp[(size_t)(k + 4) * kAG]);
+    if (MODE == 0) {
+      double h0 = 0.0, h1 = 0.0;
+      if (valid) {
+        h0 = (cz * (hasm ? hm[k] : 0.0) - cw * hp[k]) * rcs[k];
+        h1 = (cz * (hasm ? hm[k + 4] : 0.0) - cw * hp[k + 4]) * rcs[k + 4];
+      }
+      dmma(ch0, ch1, h0, Bh[(size_t)k * kAG]);
+      dmma(dh0, dh1, h1, Bh[(size_t)(k + 4) * kAG]);
+    }
+  }
+  cp0 += dp0;
+  cp1 += dp1;
+  ch0 += dh0;
+  ch1 += dh1;
+  const int slot = col_offset(T, m) + (l - m);
+  if (MODE == 0) {
+    // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ S4 from lane+2) (div); 2: S3,S7 (phi')
+    const double s4x = __shfl_down_sync(0xffffffffu, cp0, 2);
+    const double s4y = __shfl_down_sync(0xffffffffu, cp1, 2);
+    if (!valid || lc4 == 3) return;
+    double vx = cp0 + ch0, vy = cp1 + ch1;
+    if (lc4 == 1) {
+      const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
+      vx += llk * s4x;
+      vy += llk * s4y;
+    }
+    const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
+    out[(size_t)f * p.ncoef + slot] = make_double2(vx, vy);
+  } else {
+    if (!valid || lc4 >= nf) return;
+    out[(size_t)lc4 * p.ncoef + slot] = make_double2(cp0, cp1);
+  }
+}
+
 // FFT size of the tendency path: smallest 7-smooth n >= 3T+1 (the user
 // grid's nlon when that is already 7-smooth and alias-free)
 static bool smooth7(int n) {
@@ -797,6 +990,41 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     swx_sht_destroy(p);
     return fail(SWX_ERR_CUDA, std::string("sht checkpoints: ") + cudaGetErrorString(e));
   }
+  // Legendre table path when the table is small (T <= ~700 on this budget)
+  p->nt16 = ((nh + 15) / 16) * 16;
+  {
+    std::vector<long long> ptoff(T + 1);
+    long long tot = 0;
+    for (int m = 0; m <= T; ++m) {
+      ptoff[m] = tot;
+      tot += 2LL * ((T + 3 - m) / 2) * p->nt16;
+    }
+    const double tab_bytes = 8.0 * (double)tot;
+    p->use_tab = tab_bytes <= 4.0e9;
+    if (p->use_tab) {
+      std::vector<double> rc16(p->nt16, 0.0);
+      for (int i = 0; i < nh; ++i) rc16[i] = rcos[i];
+      std::vector<int4> items;
+      for (int m = 0; m <= T; ++m)
+        for (int l0 = m; l0 <= T; l0 += kAL)
+          for (int par = 0; par < 2; ++par)
+            if (l0 + par <= T) items.push_back(make_int4(m, l0, par, 0));
+      p->n_titems = (int)items.size();
+      up((void **)&p->d_ptoff, ptoff.data(), sizeof(long long) * ptoff.size());
+      up((void **)&p->d_rcos16, rc16.data(), sizeof(double) * rc16.size());
+      up((void **)&p->d_titems, items.data(), sizeof(int4) * items.size());
+      if (e == cudaSuccess) e = cudaMalloc(&p->d_ptab, sizeof(double) * (size_t)tot);
+      if (e == cudaSuccess) {
+        ptab_kernel<<<dim3(T + 1, (p->nt16 + 127) / 128), 128>>>(static_cast<const ShtView &>(*p));
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      }
+      if (e != cudaSuccess) {
+        swx_sht_destroy(p);
+        return fail(SWX_ERR_CUDA, std::string("sht table: ") + cudaGetErrorString(e));
+      }
+    }
+  }
   cufftHandle h;
   int rcd = get_plan(p, CUFFT_Z2D, p->nlon_t, 4 * nlat, &h);
   if (!rcd) rcd = get_plan(p, CUFFT_D2Z, p->nlon_t, 5 * nlat, &h);
@@ -825,6 +1053,10 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_segoff);
   cudaFree(p->d_ckpt);
   cudaFree(p->d_arange);
+  cudaFree(p->d_ptoff);
+  cudaFree(p->d_ptab);
+  cudaFree(p->d_rcos16);
+  cudaFree(p->d_titems);
   delete p;
   return SWX_OK;
 }
@@ -851,7 +1083,9 @@ static ShtWs carve(swx_sht p, void *base) {
   w.grid = (double *)(c + o); o += al(5 * gr * sizeof(double));
   w.Q = (double2 *)(c + o); o += al(5 * fr * sizeof(double2));
   w.lc = (double2 *)(c + o); o += al(2 * (size_t)p->nlat * p->nm * sizeof(double2));
-  w.A = (double *)(c + o); o += al((size_t)p->nm * 4 * p->nhp * kAS * sizeof(double));
+  w.A = (double *)(c + o);
+  o += al(std::max((size_t)p->nm * 4 * p->nhp * kAS, (size_t)p->nm * 4 * p->nt16 * kAG) *
+          sizeof(double));
   w.bytes = o;
   return w;
 }
@@ -876,6 +1110,14 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
   if (smem > 48 * 1024)
     SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<p->n_acta, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, Q, lc, atoms, out, nf);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+template <int MODE>
+static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s) {
+  const int blocks = (p->n_titems * 32 + 127) / 128;
+  analysis_tab_kernel<MODE><<<blocks, 128, 0, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -917,7 +1159,10 @@ static int check_ws(swx_sht p, void *ws, size_t bytes) {
 
 template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
-  synth_kernel<MODE><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
+  if (p->use_tab)
+    synth_kernel<MODE, true><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
+  else
+    synth_kernel<MODE, false><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -963,6 +1208,13 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
     SWX_CUDA_TRY(cudaMemcpyAsync(w.grid, d_grid + (size_t)f0 * p->nlat * p->nlon, gbytes,
                                  cudaMemcpyDeviceToDevice, s));
     if ((rc = r2c_exec(p, p->nlon, nf, w.grid, w.Q, s))) return rc;
+    if (p->use_tab) {
+      dim3 g((p->nt16 + 127) / 128, p->nm);
+      prep_tab_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, nf, w.A);
+      SWX_LAUNCH_CHECK();
+      if ((rc = launch_analysis_tab<1>(p, w.A, out + (size_t)f0 * p->ncoef, nf, s))) return rc;
+      continue;
+    }
     dim3 g((p->nhp + 127) / 128, p->nm);
     prep_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, nf, w.A);
     SWX_LAUNCH_CHECK();
@@ -1031,8 +1283,17 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     mark(3);
   }
   mark(4);
-  mark(5);  // prep is fused into the analysis kernel
-  if ((rc = launch_analysis<0>(p, w.A, w.Q, w.lc, atoms, out, 3, s))) return rc;
+  if (p->use_tab) {
+    dim3 g((p->nt16 + 127) / 128, p->nm);
+    prep_tab_tend_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.lc, atoms,
+                                           w.A);
+    SWX_LAUNCH_CHECK();
+    mark(5);
+    if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s))) return rc;
+  } else {
+    mark(5);  // prep is fused into the analysis kernel
+    if ((rc = launch_analysis<0>(p, w.A, w.Q, w.lc, atoms, out, 3, s))) return rc;
+  }
   mark(6);
   return SWX_OK;
 }
