@@ -815,6 +815,150 @@ __global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const doub
   }
 }
 
+// Table analysis, column version: CTA per m (longest columns first), 8 warps
+// = 4 output tiles (P|H x parity) x 2 K halves.  The prepared rows of the
+// column are staged once; for every 16-degree chunk the needed plane rows
+// (r0-1 .. r0+8 of both parity planes) are fetched with cp.async into a
+// double buffer while the previous chunk is contracted with DMMA.
+constexpr int kTR = 10;  // plane rows staged per chunk: r0-1 .. r0+8
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int MODE>
+__global__ void __launch_bounds__(kAT, 1) analysis_col_kernel(ShtView p, const double *A,
+                                                              double2 *out, int nf) {
+  constexpr int NPART = MODE == 0 ? 2 : 1;
+  extern __shared__ __align__(16) double sm[];
+  const int nt = p.nt16;
+  const int KP = nt + 4;                              // plane row stride, KP % 16 == 4
+  double *Bs = sm;                                    // [part][par][nt][kAS]
+  double *Pl = Bs + (size_t)NPART * 2 * nt * kAS;     // [2 buf][2 planes][kTR][KP]
+  double *rc16 = Pl + (size_t)2 * 2 * kTR * KP;       // [nt]
+  double *red = rc16 + nt;                            // [4][32][2]
+  double *res = red + 4 * 64;                         // [kAL][16]
+  const int m = p.trunc - blockIdx.x;                 // short columns last
+  const int T = p.trunc, kmax = T + 1 - m;
+  const int half = (T + 3 - m) >> 1;
+  const int off = col_offset(T, m);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = warp & 3, part = tile >> 1, par = tile & 1, khalf = warp >> 2;
+  const int apar = part ? (par ^ 1) : par;
+  const bool mma_warp = MODE == 0 || part == 0;
+  const int lr = lane >> 2, lc4 = lane & 3;
+  const double *P0 = p.d_ptab + p.d_ptoff[m];
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  // stage the prepared rows (kAG doubles each) into the kAS-strided layout
+  {
+    const size_t ps = (size_t)nt * kAG;
+    const double *Am = A + (size_t)m * NPART * 2 * ps;
+    for (int t = tid; t < NPART * 2 * nt; t += kAT) {
+      const double *src = Am + (size_t)t * kAG;
+      double *dst = Bs + (size_t)t * kAS;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) dst[c] = src[c];
+    }
+    for (int t = tid; t < nt; t += kAT) rc16[t] = p.d_rcos16[t];
+  }
+  const int nch = (kmax + kAL - 1) / kAL;
+  // async fetch of the plane rows of chunk c into buffer c&1
+  auto fetch = [&](int c) {
+    double *dst = Pl + (size_t)(c & 1) * 2 * kTR * KP;
+    const int r0 = c * (kAL / 2);
+    const int n16 = nt / 2;  // 16-byte pieces per row
+    for (int t = tid; t < 2 * kTR * n16; t += kAT) {
+      const int piece = t % n16, rowi = (t / n16) % kTR, pl = t / (n16 * kTR);
+      const int r = r0 - 1 + rowi;
+      double *d = dst + ((size_t)pl * kTR + rowi) * KP + 2 * piece;
+      if (r >= 0 && r < half) {
+        cp_async16(d, P0 + ((size_t)pl * half + r) * nt + 2 * piece);
+      } else {
+        d[0] = 0.0;
+        d[1] = 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+  fetch(0);
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait_all();
+    __syncthreads();  // buffer c&1 complete; previous chunk's res consumed
+    if (c + 1 < nch) fetch(c + 1);
+    const int l0 = m + c * kAL;
+    const int nrow = min(kAL, T + 1 - l0);
+    const double *pl = Pl + (size_t)(c & 1) * 2 * kTR * KP;
+    const double *own = pl + (size_t)par * kTR * KP;         // plane of this tile's parity
+    const double *oth = pl + (size_t)(par ^ 1) * kTR * KP;   // the other plane
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    if (mma_warp) {
+      // row of this lane in the fragment: l = l0 + 2*lr + par, plane row r0 + lr
+      const int l = l0 + 2 * lr + par;
+      const bool valid = l <= T;
+      const double *arow = own + (size_t)(1 + lr) * KP + lc4;   // staged row index 1 + lr
+      double cz = 0.0, cw = 0.0;
+      const double *hm = oth, *hp = oth;
+      if (MODE == 0 && part == 1 && valid) {
+        const double4 cc = rc[l - m];
+        cz = cc.z;
+        cw = cc.w;
+        // P_{l-1}, P_{l+1} in the other plane: staged rows (1+lr, 2+lr) for
+        // par = 1, (lr, 1+lr) for par = 0 (staged row 0 = r0 - 1)
+        hm = oth + (size_t)(par ? 1 + lr : lr) * KP + lc4;
+        hp = oth + (size_t)(par ? 2 + lr : 1 + lr) * KP + lc4;
+      }
+      const double *Bb = Bs + (size_t)(part * 2 + apar) * nt * kAS + (size_t)lc4 * kAS + lr;
+      const double *rcl = rc16 + lc4;
+      const int kb = khalf * (nt >> 1), ke = kb + (nt >> 1);
+      for (int k = kb; k < ke; k += 8) {
+        double a0, a1;
+        if (part == 0) {
+          a0 = valid ? arow[k] : 0.0;
+          a1 = valid ? arow[k + 4] : 0.0;
+        } else {
+          a0 = valid ? (cz * hm[k] - cw * hp[k]) * rcl[k] : 0.0;
+          a1 = valid ? (cz * hm[k + 4] - cw * hp[k + 4]) * rcl[k + 4] : 0.0;
+        }
+        dmma(c0, c1, a0, Bb[(size_t)k * kAS]);
+        dmma(e0, e1, a1, Bb[(size_t)(k + 4) * kAS]);
+      }
+      c0 += e0;
+      c1 += e1;
+      if (khalf == 1) {
+        red[(tile * 32 + lane) * 2] = c0;
+        red[(tile * 32 + lane) * 2 + 1] = c1;
+      }
+    }
+    __syncthreads();
+    if (mma_warp && khalf == 0) {
+      c0 += red[(tile * 32 + lane) * 2];
+      c1 += red[(tile * 32 + lane) * 2 + 1];
+      const int rr = 2 * lr + par;
+      res[rr * 16 + part * 8 + 2 * lc4] = c0;
+      res[rr * 16 + part * 8 + 2 * lc4 + 1] = c1;
+    }
+    __syncthreads();
+    if (tid < nrow) {
+      const int l = l0 + tid;
+      const int slot = off + (l - m);
+      const double *r = res + tid * 16;
+      if (MODE == 0) {
+        const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
+        out[slot] = make_double2(r[4] + r[12], r[5] + r[13]);                              // dphi'
+        out[p.ncoef + slot] = make_double2(r[0] + r[8], r[1] + r[9]);                      // dvort
+        out[2 * p.ncoef + slot] =
+            make_double2(r[2] + r[10] + llk * r[6], r[3] + r[11] + llk * r[7]);            // ddiv
+      } else {
+        for (int f = 0; f < nf; ++f)
+          out[(size_t)f * p.ncoef + slot] = make_double2(r[2 * f], r[2 * f + 1]);
+      }
+    }
+  }
+}
+
 // FFT size of the tendency path: smallest 7-smooth n >= 3T+1 (the user
 // grid's nlon when that is already 7-smooth and alias-free)
 static bool smooth7(int n) {
@@ -1116,8 +1260,19 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
 
 template <int MODE>
 static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s) {
-  const int blocks = (p->n_titems * 32 + 127) / 128;
-  analysis_tab_kernel<MODE><<<blocks, 128, 0, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
+  const int npart = MODE == 0 ? 2 : 1;
+  const size_t nt = p->nt16;
+  const size_t smem = sizeof(double) * (npart * 2 * nt * kAS + 2 * 2 * kTR * (nt + 4) + nt +
+                                        4 * 64 + kAL * 16);
+  if (smem <= 200 * 1024) {
+    auto k = analysis_col_kernel<MODE>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<p->nm, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
+  } else {
+    const int blocks = (p->n_titems * 32 + 127) / 128;
+    analysis_tab_kernel<MODE><<<blocks, 128, 0, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
+  }
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -1159,10 +1314,9 @@ static int check_ws(swx_sht p, void *ws, size_t bytes) {
 
 template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
-  if (p->use_tab)
-    synth_kernel<MODE, true><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
-  else
-    synth_kernel<MODE, false><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
+  // the recurrence walker beats streaming the table here (the table loads
+  // would sit on the critical path two steps ahead of their use)
+  synth_kernel<MODE, false><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
