@@ -732,10 +732,12 @@ __global__ void prep_tab_plain_kernel(ShtView p, const double2 *Q, int nf, doubl
   put_row(base + ps, od, 4);
 }
 
-// Table analysis: one warp = (m, 16 degrees l0..l0+15, parity).  The warp's
-// two 8x8 outputs (P table and H table columns) accumulate over all latitude
-// pairs with m8n8k4 DMMA; A fragments are loaded straight from the table
-// (8 rows x 32 B per load), H rows are formed from the other parity plane.
+// Table analysis: one warp = (m, 16 degrees l0..l0+15, both parities).
+// Four 8x8 outputs (P and H columns x parity) accumulate over all latitude
+// pairs with m8n8k4 DMMA.  A fragments come straight from the parity planes
+// (8 rows x 32 B per load); the P fragment of one parity is also the H
+// neighbour row of the other (row shifts by warp shuffles), so every plane
+// row of the chunk is read once.
 template <int MODE>
 __global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const double *A,
                                                            double2 *out, int nf) {
@@ -743,219 +745,85 @@ __global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const doub
   if (gw >= p.n_titems) return;
   const int lane = threadIdx.x & 31, lr = lane >> 2, lc4 = lane & 3;
   const int4 itm = p.d_titems[gw];
-  const int m = itm.x, l0 = itm.y, par = itm.z;
+  const int m = itm.x, l0 = itm.y;
   const int T = p.trunc, nt = p.nt16;
   const int half = (T + 3 - m) >> 1;
   const double *P0 = p.d_ptab + p.d_ptoff[m];
-  const double *Pp = P0 + (size_t)(par ? half : 0) * nt;  // own parity plane
-  const double *Po = P0 + (size_t)(par ? 0 : half) * nt;  // other parity plane
-  const int r = ((l0 - m) >> 1) + lr;
-  const int l = m + 2 * r + par;
-  const bool valid = l <= T;
-  const double *arow = Pp + (size_t)(valid ? r : 0) * nt + lc4;
-  double cz = 0.0, cw = 0.0;
-  const double *hm = Po + lc4, *hp = Po + lc4;
-  bool hasm = false;
-  if (MODE == 0 && valid) {
-    const double4 c = p.d_rc[rc_offset(T, m) + (l - m)];
-    cz = c.z;
-    cw = c.w;
-    // P_{l-1}, P_{l+1} live in the other plane: rows (r, r+1) for par = 1,
-    // (r-1, r) for par = 0
-    const int rm = par ? r : r - 1, rp = par ? r + 1 : r;
-    hasm = rm >= 0;
-    hm = Po + (size_t)(hasm ? rm : 0) * nt + lc4;
-    hp = Po + (size_t)rp * nt + lc4;
-  }
-  const size_t ps = (size_t)nt * kAG;
-  constexpr int NPART = MODE == 0 ? 2 : 1;
-  const double *Ab = A + (size_t)m * NPART * 2 * ps;
-  const double *Bp = Ab + (size_t)(0 * 2 + par) * ps + (size_t)lc4 * kAG + lr;
-  const double *Bh = Ab + (size_t)(1 * 2 + (par ^ 1)) * ps + (size_t)lc4 * kAG + lr;
-  const double *rcs = p.d_rcos16 + lc4;
-  double cp0 = 0.0, cp1 = 0.0, ch0 = 0.0, ch1 = 0.0;
-  double dp0 = 0.0, dp1 = 0.0, dh0 = 0.0, dh1 = 0.0;
-#pragma unroll 2
-  for (int k = 0; k < nt; k += 8) {
-    const double a0 = valid ? arow[k] : 0.0;
-    const double a1 = valid ? arow[k + 4] : 0.0;
-    dmma(cp0, cp1, a0, Bp[(size_t)k * kAG]);
-    dmma(dp0, dp1, a1, Bp[(size_t)(k + 4) * kAG]);
-    if (MODE == 0) {
-      double h0 = 0.0, h1 = 0.0;
-      if (valid) {
-        h0 = (cz * (hasm ? hm[k] : 0.0) - cw * hp[k]) * rcs[k];
-        h1 = (cz * (hasm ? hm[k + 4] : 0.0) - cw * hp[k + 4]) * rcs[k + 4];
-      }
-      dmma(ch0, ch1, h0, Bh[(size_t)k * kAG]);
-      dmma(dh0, dh1, h1, Bh[(size_t)(k + 4) * kAG]);
-    }
-  }
-  cp0 += dp0;
-  cp1 += dp1;
-  ch0 += dh0;
-  ch1 += dh1;
-  const int slot = col_offset(T, m) + (l - m);
+  const double *P1 = P0 + (size_t)half * nt;
+  const int r = ((l0 - m) >> 1) + lr;  // plane row of fragment row lr
+  // rows of this lane: l_even = m + 2r (parity 0), l_odd = m + 2r + 1 (parity 1)
+  const int le = m + 2 * r, lo = le + 1;
+  const bool ve = le <= T, vo = lo <= T;
+  // table rows exist for l - m <= T + 1 - m: plane 0 rows < half, plane 1 rows < (T+2-m)/2
+  const int kmax = T + 1 - m;
+  const bool e0ok = 2 * r <= kmax, e1ok = 2 * r + 1 <= kmax;
+  const double *a0p = P0 + (size_t)(e0ok ? r : 0) * nt + lc4;
+  const double *a1p = P1 + (size_t)(e1ok ? r : 0) * nt + lc4;
+  // edge rows: plane 1 row r-1 (needed by lr = 0), plane 0 row r+1 (needed by lr = 7)
+  const bool edge_lo = (lr == 0) && r >= 1;
+  const bool edge_hi = (lr == 7) && 2 * (r + 1) <= kmax;
+  const double *x1p = P1 + (size_t)(edge_lo ? r - 1 : 0) * nt + lc4;
+  const double *x0p = P0 + (size_t)(edge_hi ? r + 1 : 0) * nt + lc4;
+  double cz0 = 0.0, cw0 = 0.0, cz1 = 0.0, cw1 = 0.0;
   if (MODE == 0) {
-    // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ S4 from lane+2) (div); 2: S3,S7 (phi')
-    const double s4x = __shfl_down_sync(0xffffffffu, cp0, 2);
-    const double s4y = __shfl_down_sync(0xffffffffu, cp1, 2);
-    if (!valid || lc4 == 3) return;
-    double vx = cp0 + ch0, vy = cp1 + ch1;
-    if (lc4 == 1) {
-      const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
-      vx += llk * s4x;
-      vy += llk * s4y;
-    }
-    const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
-    out[(size_t)f * p.ncoef + slot] = make_double2(vx, vy);
-  } else {
-    if (!valid || lc4 >= nf) return;
-    out[(size_t)lc4 * p.ncoef + slot] = make_double2(cp0, cp1);
+    const double4 *rc = p.d_rc + rc_offset(T, m);
+    if (ve) { const double4 c = rc[le - m]; cz0 = c.z; cw0 = c.w; }
+    if (vo) { const double4 c = rc[lo - m]; cz1 = c.z; cw1 = c.w; }
   }
-}
-
-// Table analysis, column version: CTA per m (longest columns first), 8 warps
-// = 4 output tiles (P|H x parity) x 2 K halves.  The prepared rows of the
-// column are staged once; for every 16-degree chunk the needed plane rows
-// (r0-1 .. r0+8 of both parity planes) are fetched with cp.async into a
-// double buffer while the previous chunk is contracted with DMMA.
-constexpr int kTR = 10;  // plane rows staged per chunk: r0-1 .. r0+8
-
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
-template <int MODE>
-__global__ void __launch_bounds__(kAT, 1) analysis_col_kernel(ShtView p, const double *A,
-                                                              double2 *out, int nf) {
   constexpr int NPART = MODE == 0 ? 2 : 1;
-  extern __shared__ __align__(16) double sm[];
-  const int nt = p.nt16;
-  const int KP = nt + 4;                              // plane row stride, KP % 16 == 4
-  double *Bs = sm;                                    // [part][par][nt][kAS]
-  double *Pl = Bs + (size_t)NPART * 2 * nt * kAS;     // [2 buf][2 planes][kTR][KP]
-  double *rc16 = Pl + (size_t)2 * 2 * kTR * KP;       // [nt]
-  double *red = rc16 + nt;                            // [4][32][2]
-  double *res = red + 4 * 64;                         // [kAL][16]
-  const int m = p.trunc - blockIdx.x;                 // short columns last
-  const int T = p.trunc, kmax = T + 1 - m;
-  const int half = (T + 3 - m) >> 1;
-  const int off = col_offset(T, m);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = warp & 3, part = tile >> 1, par = tile & 1, khalf = warp >> 2;
-  const int apar = part ? (par ^ 1) : par;
-  const bool mma_warp = MODE == 0 || part == 0;
-  const int lr = lane >> 2, lc4 = lane & 3;
-  const double *P0 = p.d_ptab + p.d_ptoff[m];
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  // stage the prepared rows (kAG doubles each) into the kAS-strided layout
-  {
-    const size_t ps = (size_t)nt * kAG;
-    const double *Am = A + (size_t)m * NPART * 2 * ps;
-    for (int t = tid; t < NPART * 2 * nt; t += kAT) {
-      const double *src = Am + (size_t)t * kAG;
-      double *dst = Bs + (size_t)t * kAS;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) dst[c] = src[c];
+  const size_t ps = (size_t)nt * kAG;
+  const double *Ab = A + (size_t)m * NPART * 2 * ps + (size_t)lc4 * kAG + lr;
+  const double *Bpe = Ab, *Bpo = Ab + ps;                 // P table, fold even / odd
+  const double *Bhe = Ab + 2 * ps, *Bho = Ab + 3 * ps;    // H table, fold even / odd
+  const double *rcl = p.d_rcos16 + lc4;
+  double pe0 = 0, pe1 = 0, po0 = 0, po1 = 0, he0 = 0, he1 = 0, ho0 = 0, ho1 = 0;
+#pragma unroll 2
+  for (int k = 0; k < nt; k += 4) {
+    const double a0 = e0ok ? a0p[k] : 0.0;   // P_{le}
+    const double a1 = e1ok ? a1p[k] : 0.0;   // P_{lo}
+    dmma(pe0, pe1, ve ? a0 : 0.0, Bpe[(size_t)k * kAG]);
+    dmma(po0, po1, vo ? a1 : 0.0, Bpo[(size_t)k * kAG]);
+    if (MODE == 0) {
+      // P_{le-1} = plane 1 row r-1: lane-4's a1 (or the edge load for lr = 0)
+      double pm = __shfl_up_sync(0xffffffffu, a1, 4);
+      if (lr == 0) pm = edge_lo ? x1p[k] : 0.0;
+      // P_{lo+1} = plane 0 row r+1: lane+4's a0 (or the edge load for lr = 7)
+      double pp = __shfl_down_sync(0xffffffffu, a0, 4);
+      if (lr == 7) pp = edge_hi ? x0p[k] : 0.0;
+      const double rcs = rcl[k];
+      const double h0 = ve ? (cz0 * pm - cw0 * a1) * rcs : 0.0;  // H_{le}: P_{le-1}, P_{le+1}
+      const double h1 = vo ? (cz1 * a0 - cw1 * pp) * rcs : 0.0;  // H_{lo}: P_{lo-1}, P_{lo+1}
+      // H has the opposite fold parity: even l uses the odd fold and vice versa
+      dmma(he0, he1, h0, Bho[(size_t)k * kAG]);
+      dmma(ho0, ho1, h1, Bhe[(size_t)k * kAG]);
     }
-    for (int t = tid; t < nt; t += kAT) rc16[t] = p.d_rcos16[t];
   }
-  const int nch = (kmax + kAL - 1) / kAL;
-  // async fetch of the plane rows of chunk c into buffer c&1
-  auto fetch = [&](int c) {
-    double *dst = Pl + (size_t)(c & 1) * 2 * kTR * KP;
-    const int r0 = c * (kAL / 2);
-    const int n16 = nt / 2;  // 16-byte pieces per row
-    for (int t = tid; t < 2 * kTR * n16; t += kAT) {
-      const int piece = t % n16, rowi = (t / n16) % kTR, pl = t / (n16 * kTR);
-      const int r = r0 - 1 + rowi;
-      double *d = dst + ((size_t)pl * kTR + rowi) * KP + 2 * piece;
-      if (r >= 0 && r < half) {
-        cp_async16(d, P0 + ((size_t)pl * half + r) * nt + 2 * piece);
-      } else {
-        d[0] = 0.0;
-        d[1] = 0.0;
-      }
-    }
-    cp_async_commit();
-  };
-  fetch(0);
-  for (int c = 0; c < nch; ++c) {
-    cp_async_wait_all();
-    __syncthreads();  // buffer c&1 complete; previous chunk's res consumed
-    if (c + 1 < nch) fetch(c + 1);
-    const int l0 = m + c * kAL;
-    const int nrow = min(kAL, T + 1 - l0);
-    const double *pl = Pl + (size_t)(c & 1) * 2 * kTR * KP;
-    const double *own = pl + (size_t)par * kTR * KP;         // plane of this tile's parity
-    const double *oth = pl + (size_t)(par ^ 1) * kTR * KP;   // the other plane
-    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-    if (mma_warp) {
-      // row of this lane in the fragment: l = l0 + 2*lr + par, plane row r0 + lr
-      const int l = l0 + 2 * lr + par;
-      const bool valid = l <= T;
-      const double *arow = own + (size_t)(1 + lr) * KP + lc4;   // staged row index 1 + lr
-      double cz = 0.0, cw = 0.0;
-      const double *hm = oth, *hp = oth;
-      if (MODE == 0 && part == 1 && valid) {
-        const double4 cc = rc[l - m];
-        cz = cc.z;
-        cw = cc.w;
-        // P_{l-1}, P_{l+1} in the other plane: staged rows (1+lr, 2+lr) for
-        // par = 1, (lr, 1+lr) for par = 0 (staged row 0 = r0 - 1)
-        hm = oth + (size_t)(par ? 1 + lr : lr) * KP + lc4;
-        hp = oth + (size_t)(par ? 2 + lr : 1 + lr) * KP + lc4;
-      }
-      const double *Bb = Bs + (size_t)(part * 2 + apar) * nt * kAS + (size_t)lc4 * kAS + lr;
-      const double *rcl = rc16 + lc4;
-      const int kb = khalf * (nt >> 1), ke = kb + (nt >> 1);
-      for (int k = kb; k < ke; k += 8) {
-        double a0, a1;
-        if (part == 0) {
-          a0 = valid ? arow[k] : 0.0;
-          a1 = valid ? arow[k + 4] : 0.0;
-        } else {
-          a0 = valid ? (cz * hm[k] - cw * hp[k]) * rcl[k] : 0.0;
-          a1 = valid ? (cz * hm[k + 4] - cw * hp[k + 4]) * rcl[k + 4] : 0.0;
-        }
-        dmma(c0, c1, a0, Bb[(size_t)k * kAS]);
-        dmma(e0, e1, a1, Bb[(size_t)(k + 4) * kAS]);
-      }
-      c0 += e0;
-      c1 += e1;
-      if (khalf == 1) {
-        red[(tile * 32 + lane) * 2] = c0;
-        red[(tile * 32 + lane) * 2 + 1] = c1;
-      }
-    }
-    __syncthreads();
-    if (mma_warp && khalf == 0) {
-      c0 += red[(tile * 32 + lane) * 2];
-      c1 += red[(tile * 32 + lane) * 2 + 1];
-      const int rr = 2 * lr + par;
-      res[rr * 16 + part * 8 + 2 * lc4] = c0;
-      res[rr * 16 + part * 8 + 2 * lc4 + 1] = c1;
-    }
-    __syncthreads();
-    if (tid < nrow) {
-      const int l = l0 + tid;
-      const int slot = off + (l - m);
-      const double *r = res + tid * 16;
-      if (MODE == 0) {
+  const int off = col_offset(T, m);
+  if (MODE == 0) {
+    // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ llk*S4 from lane+2) (div); 2: S3,S7 (phi')
+    const double s4ex = __shfl_down_sync(0xffffffffu, pe0, 2);
+    const double s4ey = __shfl_down_sync(0xffffffffu, pe1, 2);
+    const double s4ox = __shfl_down_sync(0xffffffffu, po0, 2);
+    const double s4oy = __shfl_down_sync(0xffffffffu, po1, 2);
+    if (lc4 == 3) return;
+    const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int l = q ? lo : le;
+      if (l > T) continue;
+      double vx = q ? po0 + ho0 : pe0 + he0;
+      double vy = q ? po1 + ho1 : pe1 + he1;
+      if (lc4 == 1) {
         const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
-        out[slot] = make_double2(r[4] + r[12], r[5] + r[13]);                              // dphi'
-        out[p.ncoef + slot] = make_double2(r[0] + r[8], r[1] + r[9]);                      // dvort
-        out[2 * p.ncoef + slot] =
-            make_double2(r[2] + r[10] + llk * r[6], r[3] + r[11] + llk * r[7]);            // ddiv
-      } else {
-        for (int f = 0; f < nf; ++f)
-          out[(size_t)f * p.ncoef + slot] = make_double2(r[2 * f], r[2 * f + 1]);
+        vx += llk * (q ? s4ox : s4ex);
+        vy += llk * (q ? s4oy : s4ey);
       }
+      out[(size_t)f * p.ncoef + off + (l - m)] = make_double2(vx, vy);
     }
+  } else {
+    if (lc4 >= nf) return;
+    if (ve) out[(size_t)lc4 * p.ncoef + off + (le - m)] = make_double2(pe0, pe1);
+    if (vo) out[(size_t)lc4 * p.ncoef + off + (lo - m)] = make_double2(po0, po1);
   }
 }
 
@@ -1150,9 +1018,7 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
       for (int i = 0; i < nh; ++i) rc16[i] = rcos[i];
       std::vector<int4> items;
       for (int m = 0; m <= T; ++m)
-        for (int l0 = m; l0 <= T; l0 += kAL)
-          for (int par = 0; par < 2; ++par)
-            if (l0 + par <= T) items.push_back(make_int4(m, l0, par, 0));
+        for (int l0 = m; l0 <= T; l0 += kAL) items.push_back(make_int4(m, l0, 0, 0));
       p->n_titems = (int)items.size();
       up((void **)&p->d_ptoff, ptoff.data(), sizeof(long long) * ptoff.size());
       up((void **)&p->d_rcos16, rc16.data(), sizeof(double) * rc16.size());
@@ -1260,19 +1126,8 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
 
 template <int MODE>
 static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s) {
-  const int npart = MODE == 0 ? 2 : 1;
-  const size_t nt = p->nt16;
-  const size_t smem = sizeof(double) * (npart * 2 * nt * kAS + 2 * 2 * kTR * (nt + 4) + nt +
-                                        4 * 64 + kAL * 16);
-  if (smem <= 200 * 1024) {
-    auto k = analysis_col_kernel<MODE>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<p->nm, kAT, smem, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
-  } else {
-    const int blocks = (p->n_titems * 32 + 127) / 128;
-    analysis_tab_kernel<MODE><<<blocks, 128, 0, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
-  }
+  const int blocks = (p->n_titems * 32 + 127) / 128;
+  analysis_tab_kernel<MODE><<<blocks, 128, 0, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
