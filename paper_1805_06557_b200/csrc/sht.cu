@@ -732,12 +732,10 @@ __global__ void prep_tab_plain_kernel(ShtView p, const double2 *Q, int nf, doubl
   put_row(base + ps, od, 4);
 }
 
-// Table analysis: one warp = (m, 16 degrees l0..l0+15, both parities).
-// Four 8x8 outputs (P and H columns x parity) accumulate over all latitude
-// pairs with m8n8k4 DMMA.  A fragments come straight from the parity planes
-// (8 rows x 32 B per load); the P fragment of one parity is also the H
-// neighbour row of the other (row shifts by warp shuffles), so every plane
-// row of the chunk is read once.
+// Table analysis: one warp = (m, 16 degrees l0..l0+15, parity).  The warp's
+// two 8x8 outputs (P table and H table columns) accumulate over all latitude
+// pairs with m8n8k4 DMMA; A fragments are loaded straight from the table
+// (8 rows x 32 B per load), H rows are formed from the other parity plane.
 template <int MODE>
 __global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const double *A,
                                                            double2 *out, int nf) {
@@ -745,85 +743,75 @@ __global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const doub
   if (gw >= p.n_titems) return;
   const int lane = threadIdx.x & 31, lr = lane >> 2, lc4 = lane & 3;
   const int4 itm = p.d_titems[gw];
-  const int m = itm.x, l0 = itm.y;
+  const int m = itm.x, l0 = itm.y, par = itm.z;
   const int T = p.trunc, nt = p.nt16;
   const int half = (T + 3 - m) >> 1;
   const double *P0 = p.d_ptab + p.d_ptoff[m];
-  const double *P1 = P0 + (size_t)half * nt;
-  const int r = ((l0 - m) >> 1) + lr;  // plane row of fragment row lr
-  // rows of this lane: l_even = m + 2r (parity 0), l_odd = m + 2r + 1 (parity 1)
-  const int le = m + 2 * r, lo = le + 1;
-  const bool ve = le <= T, vo = lo <= T;
-  // table rows exist for l - m <= T + 1 - m: plane 0 rows < half, plane 1 rows < (T+2-m)/2
-  const int kmax = T + 1 - m;
-  const bool e0ok = 2 * r <= kmax, e1ok = 2 * r + 1 <= kmax;
-  const double *a0p = P0 + (size_t)(e0ok ? r : 0) * nt + lc4;
-  const double *a1p = P1 + (size_t)(e1ok ? r : 0) * nt + lc4;
-  // edge rows: plane 1 row r-1 (needed by lr = 0), plane 0 row r+1 (needed by lr = 7)
-  const bool edge_lo = (lr == 0) && r >= 1;
-  const bool edge_hi = (lr == 7) && 2 * (r + 1) <= kmax;
-  const double *x1p = P1 + (size_t)(edge_lo ? r - 1 : 0) * nt + lc4;
-  const double *x0p = P0 + (size_t)(edge_hi ? r + 1 : 0) * nt + lc4;
-  double cz0 = 0.0, cw0 = 0.0, cz1 = 0.0, cw1 = 0.0;
-  if (MODE == 0) {
-    const double4 *rc = p.d_rc + rc_offset(T, m);
-    if (ve) { const double4 c = rc[le - m]; cz0 = c.z; cw0 = c.w; }
-    if (vo) { const double4 c = rc[lo - m]; cz1 = c.z; cw1 = c.w; }
+  const double *Pp = P0 + (size_t)(par ? half : 0) * nt;  // own parity plane
+  const double *Po = P0 + (size_t)(par ? 0 : half) * nt;  // other parity plane
+  const int r = ((l0 - m) >> 1) + lr;
+  const int l = m + 2 * r + par;
+  const bool valid = l <= T;
+  const double *arow = Pp + (size_t)(valid ? r : 0) * nt + lc4;
+  double cz = 0.0, cw = 0.0;
+  const double *hm = Po + lc4, *hp = Po + lc4;
+  bool hasm = false;
+  if (MODE == 0 && valid) {
+    const double4 c = p.d_rc[rc_offset(T, m) + (l - m)];
+    cz = c.z;
+    cw = c.w;
+    // P_{l-1}, P_{l+1} live in the other plane: rows (r, r+1) for par = 1,
+    // (r-1, r) for par = 0
+    const int rm = par ? r : r - 1, rp = par ? r + 1 : r;
+    hasm = rm >= 0;
+    hm = Po + (size_t)(hasm ? rm : 0) * nt + lc4;
+    hp = Po + (size_t)rp * nt + lc4;
   }
-  constexpr int NPART = MODE == 0 ? 2 : 1;
   const size_t ps = (size_t)nt * kAG;
-  const double *Ab = A + (size_t)m * NPART * 2 * ps + (size_t)lc4 * kAG + lr;
-  const double *Bpe = Ab, *Bpo = Ab + ps;                 // P table, fold even / odd
-  const double *Bhe = Ab + 2 * ps, *Bho = Ab + 3 * ps;    // H table, fold even / odd
-  const double *rcl = p.d_rcos16 + lc4;
-  double pe0 = 0, pe1 = 0, po0 = 0, po1 = 0, he0 = 0, he1 = 0, ho0 = 0, ho1 = 0;
+  constexpr int NPART = MODE == 0 ? 2 : 1;
+  const double *Ab = A + (size_t)m * NPART * 2 * ps;
+  const double *Bp = Ab + (size_t)(0 * 2 + par) * ps + (size_t)lc4 * kAG + lr;
+  const double *Bh = Ab + (size_t)(1 * 2 + (par ^ 1)) * ps + (size_t)lc4 * kAG + lr;
+  const double *rcs = p.d_rcos16 + lc4;
+  double cp0 = 0.0, cp1 = 0.0, ch0 = 0.0, ch1 = 0.0;
+  double dp0 = 0.0, dp1 = 0.0, dh0 = 0.0, dh1 = 0.0;
 #pragma unroll 2
-  for (int k = 0; k < nt; k += 4) {
-    const double a0 = e0ok ? a0p[k] : 0.0;   // P_{le}
-    const double a1 = e1ok ? a1p[k] : 0.0;   // P_{lo}
-    dmma(pe0, pe1, ve ? a0 : 0.0, Bpe[(size_t)k * kAG]);
-    dmma(po0, po1, vo ? a1 : 0.0, Bpo[(size_t)k * kAG]);
+  for (int k = 0; k < nt; k += 8) {
+    const double a0 = valid ? arow[k] : 0.0;
+    const double a1 = valid ? arow[k + 4] : 0.0;
+    dmma(cp0, cp1, a0, Bp[(size_t)k * kAG]);
+    dmma(dp0, dp1, a1, Bp[(size_t)(k + 4) * kAG]);
     if (MODE == 0) {
-      // P_{le-1} = plane 1 row r-1: lane-4's a1 (or the edge load for lr = 0)
-      double pm = __shfl_up_sync(0xffffffffu, a1, 4);
-      if (lr == 0) pm = edge_lo ? x1p[k] : 0.0;
-      // P_{lo+1} = plane 0 row r+1: lane+4's a0 (or the edge load for lr = 7)
-      double pp = __shfl_down_sync(0xffffffffu, a0, 4);
-      if (lr == 7) pp = edge_hi ? x0p[k] : 0.0;
-      const double rcs = rcl[k];
-      const double h0 = ve ? (cz0 * pm - cw0 * a1) * rcs : 0.0;  // H_{le}: P_{le-1}, P_{le+1}
-      const double h1 = vo ? (cz1 * a0 - cw1 * pp) * rcs : 0.0;  // H_{lo}: P_{lo-1}, P_{lo+1}
-      // H has the opposite fold parity: even l uses the odd fold and vice versa
-      dmma(he0, he1, h0, Bho[(size_t)k * kAG]);
-      dmma(ho0, ho1, h1, Bhe[(size_t)k * kAG]);
+      double h0 = 0.0, h1 = 0.0;
+      if (valid) {
+        h0 = (cz * (hasm ? hm[k] : 0.0) - cw * hp[k]) * rcs[k];
+        h1 = (cz * (hasm ? hm[k + 4] : 0.0) - cw * hp[k + 4]) * rcs[k + 4];
+      }
+      dmma(ch0, ch1, h0, Bh[(size_t)k * kAG]);
+      dmma(dh0, dh1, h1, Bh[(size_t)(k + 4) * kAG]);
     }
   }
-  const int off = col_offset(T, m);
+  cp0 += dp0;
+  cp1 += dp1;
+  ch0 += dh0;
+  ch1 += dh1;
+  const int slot = col_offset(T, m) + (l - m);
   if (MODE == 0) {
-    // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ llk*S4 from lane+2) (div); 2: S3,S7 (phi')
-    const double s4ex = __shfl_down_sync(0xffffffffu, pe0, 2);
-    const double s4ey = __shfl_down_sync(0xffffffffu, pe1, 2);
-    const double s4ox = __shfl_down_sync(0xffffffffu, po0, 2);
-    const double s4oy = __shfl_down_sync(0xffffffffu, po1, 2);
-    if (lc4 == 3) return;
-    const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int l = q ? lo : le;
-      if (l > T) continue;
-      double vx = q ? po0 + ho0 : pe0 + he0;
-      double vy = q ? po1 + ho1 : pe1 + he1;
-      if (lc4 == 1) {
-        const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
-        vx += llk * (q ? s4ox : s4ex);
-        vy += llk * (q ? s4oy : s4ey);
-      }
-      out[(size_t)f * p.ncoef + off + (l - m)] = make_double2(vx, vy);
+    // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ S4 from lane+2) (div); 2: S3,S7 (phi')
+    const double s4x = __shfl_down_sync(0xffffffffu, cp0, 2);
+    const double s4y = __shfl_down_sync(0xffffffffu, cp1, 2);
+    if (!valid || lc4 == 3) return;
+    double vx = cp0 + ch0, vy = cp1 + ch1;
+    if (lc4 == 1) {
+      const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
+      vx += llk * s4x;
+      vy += llk * s4y;
     }
+    const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
+    out[(size_t)f * p.ncoef + slot] = make_double2(vx, vy);
   } else {
-    if (lc4 >= nf) return;
-    if (ve) out[(size_t)lc4 * p.ncoef + off + (le - m)] = make_double2(pe0, pe1);
-    if (vo) out[(size_t)lc4 * p.ncoef + off + (lo - m)] = make_double2(po0, po1);
+    if (!valid || lc4 >= nf) return;
+    out[(size_t)lc4 * p.ncoef + slot] = make_double2(cp0, cp1);
   }
 }
 
@@ -1018,7 +1006,9 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
       for (int i = 0; i < nh; ++i) rc16[i] = rcos[i];
       std::vector<int4> items;
       for (int m = 0; m <= T; ++m)
-        for (int l0 = m; l0 <= T; l0 += kAL) items.push_back(make_int4(m, l0, 0, 0));
+        for (int l0 = m; l0 <= T; l0 += kAL)
+          for (int par = 0; par < 2; ++par)
+            if (l0 + par <= T) items.push_back(make_int4(m, l0, par, 0));
       p->n_titems = (int)items.size();
       up((void **)&p->d_ptoff, ptoff.data(), sizeof(long long) * ptoff.size());
       up((void **)&p->d_rcos16, rc16.data(), sizeof(double) * rc16.size());
