@@ -206,9 +206,12 @@ def main():
 
     torch.cuda.set_device(local)
     comm = None
-    if world > 1:
+    # SWX_FORCE_COMM=1 routes a 1-rank run through the multi-rank reduce
+    # (NCCL all-gather + device tree combine), to exercise that path on 1 GPU
+    force = os.environ.get("SWX_FORCE_COMM") == "1"
+    if world > 1 or force:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        comm = PoleComm(deterministic=True)
+        comm = PoleComm(deterministic=os.environ.get("SWX_FAST_REDUCE") != "1")
     lib = _lib.lib()
     w = CONFIGS[args.config]
     par = w.params

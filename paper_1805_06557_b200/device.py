@@ -31,6 +31,67 @@ def packed_lm(trunc: int) -> tuple[np.ndarray, np.ndarray]:
     return l, m
 
 
+@functools.lru_cache(maxsize=16)
+def flat_index(trunc: int) -> np.ndarray:
+    """Index of every packed slot in a flattened dense (T+1, T+1) field."""
+    l, m = packed_lm(trunc)
+    idx = (l * (trunc + 1) + m).astype(np.intp)
+    idx.setflags(write=False)
+    return idx
+
+
+def pack_fields(fields, out: np.ndarray) -> np.ndarray:
+    """Pack dense (T+1, T+1) fields into the rows of ``out`` (F, ncoef)
+    without an intermediate stacked copy (the fast API edge)."""
+    trunc = fields[0].shape[-1] - 1
+    idx = flat_index(trunc)
+    for f, c in enumerate(fields):
+        c = np.asarray(c)
+        if c.dtype != np.complex128:
+            c = c.astype(np.complex128)
+        np.take(np.ascontiguousarray(c).reshape(-1), idx, out=out[f])
+    return out
+
+
+def unpack_fields(packed: np.ndarray, trunc: int) -> list:
+    """(F, ncoef) packed -> list of F fresh dense (T+1, T+1) arrays."""
+    idx = flat_index(trunc)
+    n = trunc + 1
+    res = []
+    for row in packed:
+        d = np.zeros(n * n, dtype=np.complex128)
+        d[idx] = row
+        res.append(d.reshape(n, n))
+    return res
+
+
+class HostStage:
+    """Pinned host staging buffers for one packed state shape (API edge)."""
+
+    def __init__(self, trunc: int, n_states: int = 1):
+        import torch
+
+        self.trunc = trunc
+        shape = (n_states, 3, ncoef(trunc)) if n_states > 1 else (3, ncoef(trunc))
+        self.h_in = torch.empty(shape, dtype=torch.complex128, pin_memory=True)
+        self.h_out = torch.empty(shape, dtype=torch.complex128, pin_memory=True)
+        self.np_in = self.h_in.numpy()
+        self.np_out = self.h_out.numpy()
+
+    def upload(self, state, dev_tensor):
+        """Pack a PrognosticState-like object straight into pinned memory and
+        copy it into ``dev_tensor`` (async on the current stream)."""
+        pack_fields((state.phi_pert.coeffs, state.vort.coeffs, state.div.coeffs), self.np_in)
+        dev_tensor.copy_(self.h_in, non_blocking=True)
+
+    def download(self, dev_tensor) -> list:
+        import torch
+
+        self.h_out.copy_(dev_tensor, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return unpack_fields(self.np_out, self.trunc)
+
+
 def pack(stack: np.ndarray) -> np.ndarray:
     """(..., n, n) dense -> (..., ncoef) packed (host)."""
     trunc = stack.shape[-1] - 1

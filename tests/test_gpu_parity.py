@@ -266,3 +266,40 @@ def test_cfg4_t1279_subset_vs_oracle():
     assert np.all(np.isfinite(sx))
     scale = np.max(np.abs(c.betas)) * 1e3
     assert np.max(np.abs(sxy - (2 * sx - sy))) <= 1e-10 * scale
+
+
+def test_polecomm_nccl_single_rank_matches_serial():
+    """The multi-rank reduce (NCCL all-gather + device tree combine, and the
+    fast all-reduce variant) on a 1-rank group equals the serial sum."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1805_06557_b200.parallel import PoleComm, distribute_terms, parallel_rexi_apply
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        par = params(42)
+        c = coeffs(128)
+        st = PrognosticState.from_stack(ost.seeded_linear_state(42, 7), par.cfg)
+        for group in (LG, L):
+            serial = rexi_step(group, st, 3600.0, c, par).stack()
+            plan = distribute_terms(c.num_terms, 1)
+            for det in (True, False):
+                out, bd = parallel_rexi_apply(group, st, 3600.0, c, plan, par, comm=PoleComm(),
+                                              deterministic=det)
+                if det:
+                    assert np.array_equal(out.stack(), serial)
+                else:
+                    assert rel_linf(pack(out.stack()), pack(serial)) <= 1e-13
+                bd.validate()
+    finally:
+        dist.destroy_process_group()
