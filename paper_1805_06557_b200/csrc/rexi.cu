@@ -255,6 +255,82 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
 constexpr int kLWarps = 4;  // warps per CTA
 constexpr int kFlush = 8;   // chain elements per reduction flush
 
+// Per chain element, forward Thomas step of chain c at k (l = m + k):
+//   den = diag_k - sub_k c'_{k-1};  c'_k = sup_k / den;
+//   y_k = (rhs_k - sub_k y_{k-1}) / den
+// The forward sweep is run twice: pass 1 over the whole chain keeps only the
+// state entering every kFlush-element segment (a checkpoint in global
+// scratch: 4 B per element instead of 32), pass 2 walks the segments
+// backwards, recomputes each segment's (c', y) in registers from its
+// checkpoint and back-substitutes it.  All loads of a segment are issued
+// before its dependent arithmetic (unrolled), so memory latency is paid once
+// per segment, not once per element.
+struct LElem {
+  double sub, sup, rot, g, h;  // signed couplings, rotation, dt^2 phibar kappa, dt kappa
+  int isz;
+};
+
+// one lane per element stages the (pole independent) chain coefficients and
+// right-hand sides of a segment into the warp's shared slots
+template <int NRHS>
+__device__ __forceinline__ void l_stage_seg(const double *__restrict__ chain,
+                                            const double *__restrict__ lconst,
+                                            const double2 *__restrict__ rhs, int ncoef, int trunc,
+                                            int m, int c, int k0, int n, int lane, LElem *ce,
+                                            double2 *bq, double2 *bp) {
+  if (lane < n) {
+    const int k = k0 + lane;
+    const int s = col_offset(trunc, m) + k, l = m + k;
+    const bool isz = ((k + c) & 1) == 0;
+    const double sg = isz ? -1.0 : 1.0;
+    LElem e;
+    e.sub = sg * chain[s];
+    e.sup = sg * chain[ncoef + s];
+    e.rot = chain[2 * ncoef + s];
+    e.g = isz ? 0.0 : lconst[(trunc + 1) + l];
+    e.h = lconst[2 * (trunc + 1) + l];
+    e.isz = isz;
+    ce[lane] = e;
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 *b = rhs + (size_t)r * 3 * ncoef;
+      const double2 vp = b[s];
+      bp[r * kFlush + lane] = vp;
+      if (isz) {
+        bq[r * kFlush + lane] = b[ncoef + s];
+      } else {
+        // div row right-hand side before the 1/alpha term: bd; the
+        // -(h/alpha) bphi part is pole dependent and added per lane
+        bq[r * kFlush + lane] = b[2 * ncoef + s];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int NRHS>
+__device__ __forceinline__ void l_fwd(const LElem &e, double2 a, double2 ia, const double2 *bq,
+                                      const double2 *bp, int idx, double2 &cp, double2 (&y)[NRHS]) {
+  double2 diag = make_double2(a.x, a.y + e.rot);
+  if (!e.isz) {
+    diag.x = fma(e.g, ia.x, diag.x);
+    diag.y = fma(e.g, ia.y, diag.y);
+  }
+  const double2 den = make_double2(fma(-e.sub, cp.x, diag.x), fma(-e.sub, cp.y, diag.y));
+  const double2 inv = crecip(den);
+  cp = cscale(e.sup, inv);
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) {
+    double2 q = bq[r * kFlush + idx];
+    if (!e.isz) {
+      const double2 t = make_double2(e.h * ia.x, e.h * ia.y);
+      q = csub(q, cmul(t, bp[r * kFlush + idx]));
+    }
+    q = make_double2(fma(-e.sub, y[r].x, q.x), fma(-e.sub, y[r].y, q.y));
+    y[r] = cmul(q, inv);
+  }
+}
+
 template <int NRHS>
 __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
@@ -265,17 +341,17 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
   // reduction buffer: [warp][e][r][comp][32] (dynamic, NRHS * 32 KB)
   extern __shared__ double2 red_raw[];
   auto red = reinterpret_cast<double2 (*)[kFlush][NRHS][2][32]>(red_raw);
+  __shared__ LElem ce_s[kLWarps][kFlush];
+  __shared__ double2 bq_s[kLWarps][NRHS * kFlush], bp_s[kLWarps][NRHS * kFlush];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gwarp = blockIdx.x * kLWarps + warp;
   const int total_warps = gridDim.x * kLWarps;
   const int n_items = (trunc + 1) * 2 * n_blocks;
-  const double *cl = chain;              // lower L per slot
-  const double *cu = chain + ncoef;      // upper U per slot
-  const double *cr = chain + 2 * ncoef;  // rotation r per slot
-  const double *gl = lconst + (trunc + 1);
-  const double *hl = lconst + 2 * (trunc + 1);
   const double dtpb = dt * phibar;
-  double2 *slot = scratch + (size_t)gwarp * (trunc + 1) * 32 * (1 + NRHS);
+  const int max_seg = (trunc + 1 + kFlush - 1) / kFlush;
+  double2 *slot = scratch + (size_t)gwarp * max_seg * 32 * (1 + NRHS);
+  LElem *ce = ce_s[warp];
+  double2 *bq = bq_s[warp], *bp = bp_s[warp];
 
   for (int item = gwarp; item < n_items; item += total_warps) {
     const int m = item / (2 * n_blocks);
@@ -296,97 +372,93 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     const double2 ia = crecip(a);
     const int nl = trunc + 1 - m;
     const int off = col_offset(trunc, m);
+    const int nseg = (nl + kFlush - 1) / kFlush;
 
-    // ---- forward sweep
+    // ---- pass 1: forward sweep, checkpoint the state entering each segment
     double2 cp = make_double2(0.0, 0.0);
-    double2 yp[NRHS];
+    double2 y[NRHS];
 #pragma unroll
-    for (int r = 0; r < NRHS; ++r) yp[r] = make_double2(0.0, 0.0);
-    for (int k = 0; k < nl; ++k) {
-      const int s = off + k;
-      const int l = m + k;
-      const bool isz = ((k + c) & 1) == 0;
-      const double sg = isz ? -1.0 : 1.0;
-      const double sub = sg * cl[s];
-      const double sup = sg * cu[s];
-      double2 diag = make_double2(a.x, a.y + cr[s]);
-      if (!isz) {
-        diag.x = fma(gl[l], ia.x, diag.x);
-        diag.y = fma(gl[l], ia.y, diag.y);
-      }
-      const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
-      const double2 inv = crecip(den);
-      cp = cscale(sup, inv);
-      double2 *dst = slot + ((size_t)k * 32 + lane) * (1 + NRHS);
+    for (int r = 0; r < NRHS; ++r) y[r] = make_double2(0.0, 0.0);
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      double2 *dst = slot + ((size_t)sgi * 32 + lane) * (1 + NRHS);
       dst[0] = cp;
 #pragma unroll
-      for (int r = 0; r < NRHS; ++r) {
-        const double2 *b = rhs + (size_t)r * 3 * ncoef;
-        double2 q;
-        if (isz) {
-          q = b[ncoef + s];
-        } else {
-          const double hk = hl[l];
-          const double2 bp = b[s];
-          const double2 t = make_double2(hk * ia.x, hk * ia.y);
-          q = csub(b[2 * ncoef + s], cmul(t, bp));
-        }
-        q = make_double2(fma(-sub, yp[r].x, q.x), fma(-sub, yp[r].y, q.y));
-        yp[r] = cmul(q, inv);
-        dst[1 + r] = yp[r];
-      }
+      for (int r = 0; r < NRHS; ++r) dst[1 + r] = y[r];
+      const int k0 = sgi * kFlush;
+      const int n = min(kFlush, nl - k0);
+      l_stage_seg<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0, n, lane, ce, bq, bp);
+#pragma unroll
+      for (int e = 0; e < kFlush; ++e)
+        if (e < n) l_fwd<NRHS>(ce[e], a, ia, bq, bp, e, cp, y);
+      __syncwarp();
     }
-    // ---- back substitution + beta weighting + tree reduction over lanes
+    // ---- pass 2: segments backwards: recompute (c', y) in registers, back-substitute
     double2 xn[NRHS];
 #pragma unroll
     for (int r = 0; r < NRHS; ++r) xn[r] = make_double2(0.0, 0.0);
-    int e = 0;
-    for (int k = nl - 1; k >= 0; --k) {
-      const int s = off + k;
-      const bool isz = ((k + c) & 1) == 0;
-      const double2 *src = slot + ((size_t)k * 32 + lane) * (1 + NRHS);
-      const double2 cpk = src[0];
-      const int phys = lane ^ e;
+    for (int sgi = nseg - 1; sgi >= 0; --sgi) {
+      const int k0 = sgi * kFlush;
+      const int n = min(kFlush, nl - k0);
+      const double2 *src = slot + ((size_t)sgi * 32 + lane) * (1 + NRHS);
+      cp = src[0];
 #pragma unroll
-      for (int r = 0; r < NRHS; ++r) {
-        const double2 x = csub(src[1 + r], cmul(cpk, xn[r]));
-        xn[r] = x;
-        red[warp][e][r][0][phys] = cmul(bet[r], x);
-        if (!isz) {
-          const double2 bp = rhs[(size_t)r * 3 * ncoef + s];
-          const double2 ph = cmul(make_double2(fma(dtpb, x.x, bp.x), fma(dtpb, x.y, bp.y)), ia);
-          red[warp][e][r][1][phys] = cmul(bet[r], ph);
+      for (int r = 0; r < NRHS; ++r) y[r] = src[1 + r];
+      l_stage_seg<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0, n, lane, ce, bq, bp);
+      double2 cps[kFlush], ys[NRHS][kFlush];
+#pragma unroll
+      for (int e = 0; e < kFlush; ++e) {
+        if (e < n) {
+          l_fwd<NRHS>(ce[e], a, ia, bq, bp, e, cp, y);
+          cps[e] = cp;
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) ys[r][e] = y[r];
         }
       }
-      ++e;
-      if (e == kFlush || k == 0) {
-        __syncwarp();
-        // lane j reduces element ee = j>>2 over the 8 poles 8q..8q+7, q = j&3
-        const int ee = lane >> 2, q = lane & 3;
-        const int eidx = ee < e ? ee : 0;
-        const int kk = k + (e - 1 - eidx);  // chain position of element eidx
-        const bool eisz = ((kk + c) & 1) == 0;
+      // back substitution; element e goes to reduction row (n-1-e)
 #pragma unroll
-        for (int r = 0; r < NRHS; ++r) {
+      for (int e = kFlush - 1; e >= 0; --e) {
+        if (e < n) {
+          const int er = n - 1 - e;
+          const bool isz = ce[e].isz;
+          const int phys = lane ^ er;
 #pragma unroll
-          for (int comp = 0; comp < 2; ++comp) {
-            double2 v[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = red[warp][eidx][r][comp][(8 * q + i) ^ eidx];
-            double2 s01 = cadd(v[0], v[1]), s23 = cadd(v[2], v[3]);
-            double2 s45 = cadd(v[4], v[5]), s67 = cadd(v[6], v[7]);
-            double2 acc = cadd(cadd(s01, s23), cadd(s45, s67));
-            acc = cadd(acc, shfl_xor2(acc, 1));
-            acc = cadd(acc, shfl_xor2(acc, 2));
-            if (q == 0 && ee < e && (comp == 0 || !eisz)) {
-              const int field = comp == 1 ? 0 : (eisz ? 1 : 2);
-              part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + kk] = acc;
+          for (int r = 0; r < NRHS; ++r) {
+            const double2 x = csub(ys[r][e], cmul(cps[e], xn[r]));
+            xn[r] = x;
+            red[warp][er][r][0][phys] = cmul(bet[r], x);
+            if (!isz) {
+              const double2 b = bp[r * kFlush + e];
+              const double2 ph = cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), ia);
+              red[warp][er][r][1][phys] = cmul(bet[r], ph);
             }
           }
         }
-        __syncwarp();
-        e = 0;
       }
+      __syncwarp();
+      // lane j reduces element ee = j>>2 over the 8 poles 8q..8q+7, q = j&3
+      const int ee = lane >> 2, q = lane & 3;
+      const int eidx = ee < n ? ee : 0;
+      const int kk = k0 + (n - 1 - eidx);  // chain position of reduction row eidx
+      const bool eisz = ((kk + c) & 1) == 0;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+#pragma unroll
+        for (int comp = 0; comp < 2; ++comp) {
+          double2 v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = red[warp][eidx][r][comp][(8 * q + i) ^ eidx];
+          const double2 s01 = cadd(v[0], v[1]), s23 = cadd(v[2], v[3]);
+          const double2 s45 = cadd(v[4], v[5]), s67 = cadd(v[6], v[7]);
+          double2 acc = cadd(cadd(s01, s23), cadd(s45, s67));
+          acc = cadd(acc, shfl_xor2(acc, 1));
+          acc = cadd(acc, shfl_xor2(acc, 2));
+          if (q == 0 && ee < n && (comp == 0 || !eisz)) {
+            const int field = comp == 1 ? 0 : (eisz ? 1 : 2);
+            part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + kk] = acc;
+          }
+        }
+      }
+      __syncwarp();
     }
   }
 }
@@ -739,7 +811,8 @@ static size_t l_scratch_bytes(swx_solver s, int n_rhs, int P) {
   const int nb = (P + 31) / 32;
   const int n_items = (s->trunc + 1) * 2 * nb;
   const int warps = l_grid_warps(s, n_items);
-  return (size_t)warps * (s->trunc + 1) * 32 * (1 + n_rhs) * sizeof(double2);
+  const int max_seg = (s->trunc + 1 + kFlush - 1) / kFlush;
+  return (size_t)warps * max_seg * 32 * (1 + n_rhs) * sizeof(double2);
 }
 
 extern "C" size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs,
