@@ -270,39 +270,51 @@ struct LElem {
   int isz;
 };
 
-// one lane per element stages the (pole independent) chain coefficients and
-// right-hand sides of a segment into the warp's shared slots
+// one lane per element fetches the (pole independent) chain coefficients and
+// right-hand sides of a segment (l_fetch, into registers, issued one segment
+// ahead) and later publishes them to the warp's shared slots (l_publish)
 template <int NRHS>
-__device__ __forceinline__ void l_stage_seg(const double *__restrict__ chain,
-                                            const double *__restrict__ lconst,
-                                            const double2 *__restrict__ rhs, int ncoef, int trunc,
-                                            int m, int c, int k0, int n, int lane, LElem *ce,
-                                            double2 *bq, double2 *bp) {
+struct LStage {
+  LElem e;
+  double2 q[NRHS], p[NRHS];
+};
+
+template <int NRHS>
+__device__ __forceinline__ void l_fetch(const double *__restrict__ chain,
+                                        const double *__restrict__ lconst,
+                                        const double2 *__restrict__ rhs, int ncoef, int trunc,
+                                        int m, int c, int k0, int n, int lane, LStage<NRHS> &st) {
   if (lane < n) {
     const int k = k0 + lane;
     const int s = col_offset(trunc, m) + k, l = m + k;
     const bool isz = ((k + c) & 1) == 0;
     const double sg = isz ? -1.0 : 1.0;
-    LElem e;
-    e.sub = sg * chain[s];
-    e.sup = sg * chain[ncoef + s];
-    e.rot = chain[2 * ncoef + s];
-    e.g = isz ? 0.0 : lconst[(trunc + 1) + l];
-    e.h = lconst[2 * (trunc + 1) + l];
-    e.isz = isz;
-    ce[lane] = e;
+    st.e.sub = sg * chain[s];
+    st.e.sup = sg * chain[ncoef + s];
+    st.e.rot = chain[2 * ncoef + s];
+    st.e.g = isz ? 0.0 : lconst[(trunc + 1) + l];
+    st.e.h = lconst[2 * (trunc + 1) + l];
+    st.e.isz = isz;
 #pragma unroll
     for (int r = 0; r < NRHS; ++r) {
       const double2 *b = rhs + (size_t)r * 3 * ncoef;
-      const double2 vp = b[s];
-      bp[r * kFlush + lane] = vp;
-      if (isz) {
-        bq[r * kFlush + lane] = b[ncoef + s];
-      } else {
-        // div row right-hand side before the 1/alpha term: bd; the
-        // -(h/alpha) bphi part is pole dependent and added per lane
-        bq[r * kFlush + lane] = b[2 * ncoef + s];
-      }
+      st.p[r] = b[s];
+      // vort rows: bz; div rows: bd (the -(h/alpha) bphi part is per pole)
+      st.q[r] = isz ? b[ncoef + s] : b[2 * ncoef + s];
+    }
+  }
+}
+
+template <int NRHS>
+__device__ __forceinline__ void l_publish(const LStage<NRHS> &st, int n, int lane, LElem *ce,
+                                          double2 *bq, double2 *bp) {
+  __syncwarp();  // previous segment's readers are done
+  if (lane < n) {
+    ce[lane] = st.e;
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      bq[r * kFlush + lane] = st.q[r];
+      bp[r * kFlush + lane] = st.p[r];
     }
   }
   __syncwarp();
@@ -379,6 +391,8 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     double2 y[NRHS];
 #pragma unroll
     for (int r = 0; r < NRHS; ++r) y[r] = make_double2(0.0, 0.0);
+    LStage<NRHS> nxt;
+    l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, 0, min(kFlush, nl), lane, nxt);
     for (int sgi = 0; sgi < nseg; ++sgi) {
       double2 *dst = slot + ((size_t)sgi * 32 + lane) * (1 + NRHS);
       dst[0] = cp;
@@ -386,24 +400,41 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       for (int r = 0; r < NRHS; ++r) dst[1 + r] = y[r];
       const int k0 = sgi * kFlush;
       const int n = min(kFlush, nl - k0);
-      l_stage_seg<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0, n, lane, ce, bq, bp);
+      l_publish<NRHS>(nxt, n, lane, ce, bq, bp);
+      if (sgi + 1 < nseg)  // next segment's loads fly during this segment's sweep
+        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0 + kFlush,
+                      min(kFlush, nl - k0 - kFlush), lane, nxt);
 #pragma unroll
       for (int e = 0; e < kFlush; ++e)
         if (e < n) l_fwd<NRHS>(ce[e], a, ia, bq, bp, e, cp, y);
-      __syncwarp();
     }
     // ---- pass 2: segments backwards: recompute (c', y) in registers, back-substitute
     double2 xn[NRHS];
 #pragma unroll
     for (int r = 0; r < NRHS; ++r) xn[r] = make_double2(0.0, 0.0);
+    double2 ck_cp, ck_y[NRHS];
+    {
+      const int k0 = (nseg - 1) * kFlush;
+      const double2 *src = slot + ((size_t)(nseg - 1) * 32 + lane) * (1 + NRHS);
+      ck_cp = src[0];
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) ck_y[r] = src[1 + r];
+      l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0, nl - k0, lane, nxt);
+    }
     for (int sgi = nseg - 1; sgi >= 0; --sgi) {
       const int k0 = sgi * kFlush;
       const int n = min(kFlush, nl - k0);
-      const double2 *src = slot + ((size_t)sgi * 32 + lane) * (1 + NRHS);
-      cp = src[0];
+      cp = ck_cp;
 #pragma unroll
-      for (int r = 0; r < NRHS; ++r) y[r] = src[1 + r];
-      l_stage_seg<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0, n, lane, ce, bq, bp);
+      for (int r = 0; r < NRHS; ++r) y[r] = ck_y[r];
+      l_publish<NRHS>(nxt, n, lane, ce, bq, bp);
+      if (sgi > 0) {  // previous segment's checkpoint and data fly during this one
+        const double2 *src = slot + ((size_t)(sgi - 1) * 32 + lane) * (1 + NRHS);
+        ck_cp = src[0];
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) ck_y[r] = src[1 + r];
+        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0 - kFlush, kFlush, lane, nxt);
+      }
       double2 cps[kFlush], ys[NRHS][kFlush];
 #pragma unroll
       for (int e = 0; e < kFlush; ++e) {
