@@ -265,80 +265,73 @@ constexpr int kFlush = 8;   // chain elements per reduction flush
 // checkpoint and back-substitutes it.  All loads of a segment are issued
 // before its dependent arithmetic (unrolled), so memory latency is paid once
 // per segment, not once per element.
-struct LElem {
-  double sub, sup, rot, g, h;  // signed couplings, rotation, dt^2 phibar kappa, dt kappa
-  int isz;
-};
+// Both chains of one (pole, m) run in the same thread, interleaved: at chain
+// position k (l = m + k) chain c holds vort_l if (k + c) is even, else div_l,
+// so the two chains share every coefficient and right-hand side of the
+// position, give two independent dependency chains (ILP), and together
+// produce (vort_l, div_l, phi'_l).
+constexpr int kLSeg = 4;  // positions per segment (x 2 chains = kFlush rows)
 
-// one lane per element fetches the (pole independent) chain coefficients and
-// right-hand sides of a segment (l_fetch, into registers, issued one segment
-// ahead) and later publishes them to the warp's shared slots (l_publish)
 template <int NRHS>
-struct LStage {
-  LElem e;
-  double2 q[NRHS], p[NRHS];
+struct LPos {
+  double L, U, rot, g, h;  // couplings, rotation, dt^2 phibar kappa, dt kappa
+  double2 bz[NRHS], bd[NRHS], bp[NRHS];
 };
 
 template <int NRHS>
 __device__ __forceinline__ void l_fetch(const double *__restrict__ chain,
                                         const double *__restrict__ lconst,
                                         const double2 *__restrict__ rhs, int ncoef, int trunc,
-                                        int m, int c, int k0, int n, int lane, LStage<NRHS> &st) {
+                                        int m, int k0, int n, int lane, LPos<NRHS> &st) {
   if (lane < n) {
     const int k = k0 + lane;
     const int s = col_offset(trunc, m) + k, l = m + k;
-    const bool isz = ((k + c) & 1) == 0;
-    const double sg = isz ? -1.0 : 1.0;
-    st.e.sub = sg * chain[s];
-    st.e.sup = sg * chain[ncoef + s];
-    st.e.rot = chain[2 * ncoef + s];
-    st.e.g = isz ? 0.0 : lconst[(trunc + 1) + l];
-    st.e.h = lconst[2 * (trunc + 1) + l];
-    st.e.isz = isz;
+    st.L = chain[s];
+    st.U = chain[ncoef + s];
+    st.rot = chain[2 * ncoef + s];
+    st.g = lconst[(trunc + 1) + l];
+    st.h = lconst[2 * (trunc + 1) + l];
 #pragma unroll
     for (int r = 0; r < NRHS; ++r) {
       const double2 *b = rhs + (size_t)r * 3 * ncoef;
-      st.p[r] = b[s];
-      // vort rows: bz; div rows: bd (the -(h/alpha) bphi part is per pole)
-      st.q[r] = isz ? b[ncoef + s] : b[2 * ncoef + s];
+      st.bp[r] = b[s];
+      st.bz[r] = b[ncoef + s];
+      st.bd[r] = b[2 * ncoef + s];
     }
   }
 }
 
 template <int NRHS>
-__device__ __forceinline__ void l_publish(const LStage<NRHS> &st, int n, int lane, LElem *ce,
-                                          double2 *bq, double2 *bp) {
+__device__ __forceinline__ void l_publish(const LPos<NRHS> &st, int n, int lane, LPos<NRHS> *sp) {
   __syncwarp();  // previous segment's readers are done
-  if (lane < n) {
-    ce[lane] = st.e;
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) {
-      bq[r * kFlush + lane] = st.q[r];
-      bp[r * kFlush + lane] = st.p[r];
-    }
-  }
+  if (lane < n) sp[lane] = st;
   __syncwarp();
 }
 
+// forward Thomas step of one chain at one position (isz: vorticity row)
 template <int NRHS>
-__device__ __forceinline__ void l_fwd(const LElem &e, double2 a, double2 ia, const double2 *bq,
-                                      const double2 *bp, int idx, double2 &cp, double2 (&y)[NRHS]) {
+__device__ __forceinline__ void l_fwd(const LPos<NRHS> &e, bool isz, double2 a, double2 ia,
+                                      double2 &cp, double2 (&y)[NRHS]) {
+  const double sg = isz ? -1.0 : 1.0;
+  const double sub = sg * e.L, sup = sg * e.U;
   double2 diag = make_double2(a.x, a.y + e.rot);
-  if (!e.isz) {
+  if (!isz) {
     diag.x = fma(e.g, ia.x, diag.x);
     diag.y = fma(e.g, ia.y, diag.y);
   }
-  const double2 den = make_double2(fma(-e.sub, cp.x, diag.x), fma(-e.sub, cp.y, diag.y));
+  const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
   const double2 inv = crecip(den);
-  cp = cscale(e.sup, inv);
+  cp = cscale(sup, inv);
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) {
-    double2 q = bq[r * kFlush + idx];
-    if (!e.isz) {
+    double2 q;
+    if (isz) {
+      q = e.bz[r];
+    } else {
       const double2 t = make_double2(e.h * ia.x, e.h * ia.y);
-      q = csub(q, cmul(t, bp[r * kFlush + idx]));
+      q = csub(e.bd[r], cmul(t, e.bp[r]));
     }
-    q = make_double2(fma(-e.sub, y[r].x, q.x), fma(-e.sub, y[r].y, q.y));
+    q = make_double2(fma(-sub, y[r].x, q.x), fma(-sub, y[r].y, q.y));
     y[r] = cmul(q, inv);
   }
 }
@@ -350,26 +343,23 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     int n_blocks, int trunc, int ncoef, double dt, double phibar,
     const double *__restrict__ lconst, const double *__restrict__ chain,
     double2 *__restrict__ scratch, double2 *__restrict__ part) {
-  // reduction buffer: [warp][e][r][comp][32] (dynamic, NRHS * 32 KB)
+  // reduction buffer: [warp][row][r][comp][32] (dynamic, NRHS * 32 KB)
   extern __shared__ double2 red_raw[];
   auto red = reinterpret_cast<double2 (*)[kFlush][NRHS][2][32]>(red_raw);
-  __shared__ LElem ce_s[kLWarps][kFlush];
-  __shared__ double2 bq_s[kLWarps][NRHS * kFlush], bp_s[kLWarps][NRHS * kFlush];
+  __shared__ LPos<NRHS> pos_s[kLWarps][kLSeg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gwarp = blockIdx.x * kLWarps + warp;
   const int total_warps = gridDim.x * kLWarps;
-  const int n_items = (trunc + 1) * 2 * n_blocks;
+  const int n_items = (trunc + 1) * n_blocks;
   const double dtpb = dt * phibar;
-  const int max_seg = (trunc + 1 + kFlush - 1) / kFlush;
-  double2 *slot = scratch + (size_t)gwarp * max_seg * 32 * (1 + NRHS);
-  LElem *ce = ce_s[warp];
-  double2 *bq = bq_s[warp], *bp = bp_s[warp];
+  const int max_seg = (trunc + 1 + kLSeg - 1) / kLSeg;
+  constexpr int CKW = 2 * (1 + NRHS);  // checkpoint words per lane: (cp, y) x 2 chains
+  double2 *slot = scratch + (size_t)gwarp * max_seg * 32 * CKW;
+  LPos<NRHS> *sp = pos_s[warp];
 
   for (int item = gwarp; item < n_items; item += total_warps) {
-    const int m = item / (2 * n_blocks);
-    const int rem = item - m * 2 * n_blocks;
-    const int c = rem / n_blocks;
-    const int pb = rem - c * n_blocks;
+    const int m = item / n_blocks;
+    const int pb = item - m * n_blocks;
     const int pl = pb * 32 + lane;  // local pole index
     const bool active = pl < P;
     double2 a = make_double2(1.0, 0.0);
@@ -384,93 +374,119 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     const double2 ia = crecip(a);
     const int nl = trunc + 1 - m;
     const int off = col_offset(trunc, m);
-    const int nseg = (nl + kFlush - 1) / kFlush;
+    const int nseg = (nl + kLSeg - 1) / kLSeg;
 
-    // ---- pass 1: forward sweep, checkpoint the state entering each segment
-    double2 cp = make_double2(0.0, 0.0);
-    double2 y[NRHS];
+    // ---- pass 1: forward sweep of both chains, checkpoint every segment
+    double2 cp[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    double2 y[2][NRHS];
 #pragma unroll
-    for (int r = 0; r < NRHS; ++r) y[r] = make_double2(0.0, 0.0);
-    LStage<NRHS> nxt;
-    l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, 0, min(kFlush, nl), lane, nxt);
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) y[c][r] = make_double2(0.0, 0.0);
+    LPos<NRHS> nxt;
+    l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, 0, min(kLSeg, nl), lane, nxt);
     for (int sgi = 0; sgi < nseg; ++sgi) {
-      double2 *dst = slot + ((size_t)sgi * 32 + lane) * (1 + NRHS);
-      dst[0] = cp;
+      double2 *dst = slot + ((size_t)sgi * 32 + lane) * CKW;
 #pragma unroll
-      for (int r = 0; r < NRHS; ++r) dst[1 + r] = y[r];
-      const int k0 = sgi * kFlush;
-      const int n = min(kFlush, nl - k0);
-      l_publish<NRHS>(nxt, n, lane, ce, bq, bp);
-      if (sgi + 1 < nseg)  // next segment's loads fly during this segment's sweep
-        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0 + kFlush,
-                      min(kFlush, nl - k0 - kFlush), lane, nxt);
+      for (int c = 0; c < 2; ++c) {
+        dst[c * (1 + NRHS)] = cp[c];
 #pragma unroll
-      for (int e = 0; e < kFlush; ++e)
-        if (e < n) l_fwd<NRHS>(ce[e], a, ia, bq, bp, e, cp, y);
-    }
-    // ---- pass 2: segments backwards: recompute (c', y) in registers, back-substitute
-    double2 xn[NRHS];
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) xn[r] = make_double2(0.0, 0.0);
-    double2 ck_cp, ck_y[NRHS];
-    {
-      const int k0 = (nseg - 1) * kFlush;
-      const double2 *src = slot + ((size_t)(nseg - 1) * 32 + lane) * (1 + NRHS);
-      ck_cp = src[0];
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) ck_y[r] = src[1 + r];
-      l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0, nl - k0, lane, nxt);
-    }
-    for (int sgi = nseg - 1; sgi >= 0; --sgi) {
-      const int k0 = sgi * kFlush;
-      const int n = min(kFlush, nl - k0);
-      cp = ck_cp;
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) y[r] = ck_y[r];
-      l_publish<NRHS>(nxt, n, lane, ce, bq, bp);
-      if (sgi > 0) {  // previous segment's checkpoint and data fly during this one
-        const double2 *src = slot + ((size_t)(sgi - 1) * 32 + lane) * (1 + NRHS);
-        ck_cp = src[0];
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) ck_y[r] = src[1 + r];
-        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, c, k0 - kFlush, kFlush, lane, nxt);
+        for (int r = 0; r < NRHS; ++r) dst[c * (1 + NRHS) + 1 + r] = y[c][r];
       }
-      double2 cps[kFlush], ys[NRHS][kFlush];
+      const int k0 = sgi * kLSeg;
+      const int n = min(kLSeg, nl - k0);
+      l_publish<NRHS>(nxt, n, lane, sp);
+      if (sgi + 1 < nseg)  // next segment's loads fly during this segment's sweep
+        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 + kLSeg,
+                      min(kLSeg, nl - k0 - kLSeg), lane, nxt);
 #pragma unroll
-      for (int e = 0; e < kFlush; ++e) {
+      for (int e = 0; e < kLSeg; ++e) {
         if (e < n) {
-          l_fwd<NRHS>(ce[e], a, ia, bq, bp, e, cp, y);
-          cps[e] = cp;
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) ys[r][e] = y[r];
+          const int k = k0 + e;
+          l_fwd<NRHS>(sp[e], (k & 1) == 0, a, ia, cp[0], y[0]);
+          l_fwd<NRHS>(sp[e], (k & 1) == 1, a, ia, cp[1], y[1]);
         }
       }
-      // back substitution; element e goes to reduction row (n-1-e)
+    }
+    // ---- pass 2: segments backwards: recompute (c', y) in registers, back-substitute
+    double2 xn[2][NRHS];
 #pragma unroll
-      for (int e = kFlush - 1; e >= 0; --e) {
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) xn[c][r] = make_double2(0.0, 0.0);
+    double2 ck_cp[2], ck_y[2][NRHS];
+    auto load_ck = [&](int sgi) {
+      const double2 *src = slot + ((size_t)sgi * 32 + lane) * CKW;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        ck_cp[c] = src[c * (1 + NRHS)];
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) ck_y[c][r] = src[c * (1 + NRHS) + 1 + r];
+      }
+    };
+    load_ck(nseg - 1);
+    l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, (nseg - 1) * kLSeg,
+                  nl - (nseg - 1) * kLSeg, lane, nxt);
+    for (int sgi = nseg - 1; sgi >= 0; --sgi) {
+      const int k0 = sgi * kLSeg;
+      const int n = min(kLSeg, nl - k0);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        cp[c] = ck_cp[c];
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) y[c][r] = ck_y[c][r];
+      }
+      l_publish<NRHS>(nxt, n, lane, sp);
+      if (sgi > 0) {  // previous segment's checkpoint and data fly during this one
+        load_ck(sgi - 1);
+        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 - kLSeg, kLSeg, lane, nxt);
+      }
+      double2 cps[2][kLSeg], ys[2][NRHS][kLSeg];
+#pragma unroll
+      for (int e = 0; e < kLSeg; ++e) {
         if (e < n) {
-          const int er = n - 1 - e;
-          const bool isz = ce[e].isz;
-          const int phys = lane ^ er;
+          const int k = k0 + e;
 #pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            const double2 x = csub(ys[r][e], cmul(cps[e], xn[r]));
-            xn[r] = x;
-            red[warp][er][r][0][phys] = cmul(bet[r], x);
-            if (!isz) {
-              const double2 b = bp[r * kFlush + e];
-              const double2 ph = cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), ia);
-              red[warp][er][r][1][phys] = cmul(bet[r], ph);
+          for (int c = 0; c < 2; ++c) {
+            l_fwd<NRHS>(sp[e], ((k + c) & 1) == 0, a, ia, cp[c], y[c]);
+            cps[c][e] = cp[c];
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) ys[c][r][e] = y[c][r];
+          }
+        }
+      }
+      // back substitution; (position e, chain c) -> reduction row (n-1-e)*2 + c
+#pragma unroll
+      for (int e = kLSeg - 1; e >= 0; --e) {
+        if (e < n) {
+          const int k = k0 + e;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const bool isz = ((k + c) & 1) == 0;
+            const int er = (n - 1 - e) * 2 + c;
+            const int phys = lane ^ er;
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) {
+              const double2 x = csub(ys[c][r][e], cmul(cps[c][e], xn[c][r]));
+              xn[c][r] = x;
+              red[warp][er][r][0][phys] = cmul(bet[r], x);
+              if (!isz) {
+                const double2 b = sp[e].bp[r];
+                const double2 ph = cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), ia);
+                red[warp][er][r][1][phys] = cmul(bet[r], ph);
+              }
             }
           }
         }
       }
       __syncwarp();
-      // lane j reduces element ee = j>>2 over the 8 poles 8q..8q+7, q = j&3
+      // lane j reduces row ee = j>>2 over the 8 poles 8q..8q+7, q = j&3
+      const int nrows = 2 * n;
       const int ee = lane >> 2, q = lane & 3;
-      const int eidx = ee < n ? ee : 0;
-      const int kk = k0 + (n - 1 - eidx);  // chain position of reduction row eidx
-      const bool eisz = ((kk + c) & 1) == 0;
+      const int eidx = ee < nrows ? ee : 0;
+      const int epos = n - 1 - (eidx >> 1), ec = eidx & 1;
+      const int kk = k0 + epos;
+      const bool eisz = ((kk + ec) & 1) == 0;
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) {
 #pragma unroll
@@ -483,7 +499,7 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
           double2 acc = cadd(cadd(s01, s23), cadd(s45, s67));
           acc = cadd(acc, shfl_xor2(acc, 1));
           acc = cadd(acc, shfl_xor2(acc, 2));
-          if (q == 0 && ee < n && (comp == 0 || !eisz)) {
+          if (q == 0 && ee < nrows && (comp == 0 || !eisz)) {
             const int field = comp == 1 ? 0 : (eisz ? 1 : 2);
             part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + kk] = acc;
           }
@@ -840,10 +856,10 @@ static int l_grid_warps(swx_solver s, int n_items) {
 
 static size_t l_scratch_bytes(swx_solver s, int n_rhs, int P) {
   const int nb = (P + 31) / 32;
-  const int n_items = (s->trunc + 1) * 2 * nb;
+  const int n_items = (s->trunc + 1) * nb;
   const int warps = l_grid_warps(s, n_items);
-  const int max_seg = (s->trunc + 1 + kFlush - 1) / kFlush;
-  return (size_t)warps * max_seg * 32 * (1 + n_rhs) * sizeof(double2);
+  const int max_seg = (s->trunc + 1 + kLSeg - 1) / kLSeg;
+  return (size_t)warps * max_seg * 32 * 2 * (1 + n_rhs) * sizeof(double2);
 }
 
 extern "C" size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs,
@@ -928,7 +944,7 @@ static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
                     int pole0, int P, int realify, double2 *out, char *ws,
                     cudaStream_t st) {
   const int nb = (P + 31) / 32;
-  const int n_items = (s->trunc + 1) * 2 * nb;
+  const int n_items = (s->trunc + 1) * nb;
   const int warps = l_grid_warps(s, n_items);
   double2 *scratch = (double2 *)ws;
   const size_t sbytes = l_scratch_bytes(s, NRHS, P);
