@@ -97,6 +97,21 @@ int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
                  int realify, swx_c128 *d_out, void *d_workspace,
                  size_t workspace_bytes, void *stream);
 
+/* Prepared pole sums.  For the gravity group the per-(pole, l) factors
+ * (beta folded, solvers.py:93-107 with the reciprocals hoisted) depend only
+ * on the shifts, the weights and l, so a caller that reuses one weight set
+ * (every ETD2RK step, rexi_step at fixed dt) builds them once with
+ * swx_rexi_prepare into a buffer of swx_rexi_prepared_bytes and then calls
+ * swx_rexi_sum_prepared (same result as swx_rexi_sum).  The Coriolis group
+ * needs no preparation (0 bytes; the prepared call forwards to swx_rexi_sum). */
+size_t swx_rexi_prepared_bytes(swx_solver s, int n_rhs, int pole_begin, int pole_end);
+int swx_rexi_prepare(swx_solver s, int n_rhs, const swx_c128 *d_betas, int pole_begin,
+                     int pole_end, void *d_prep, size_t prep_bytes, void *stream);
+int swx_rexi_sum_prepared(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                          const swx_c128 *d_betas, const void *d_prep, int pole_begin,
+                          int pole_end, int realify, swx_c128 *d_out, void *d_workspace,
+                          size_t workspace_bytes, void *stream);
+
 /* Forward operator (dt L + alpha) x -- apply_stacked, solvers.py:252-256.   */
 int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,
               swx_c128 *d_out, void *stream);

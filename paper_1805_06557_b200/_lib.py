@@ -40,6 +40,9 @@ SIGNATURES = {
     "swx_solver_warm": (_I, [_P, _P, _I, _IP, _IP, _P]),
     "swx_rexi_workspace_bytes": (_S, [_P, _I, _I, _I]),
     "swx_rexi_sum": (_I, [_P, _I, _P, _P, _I, _I, _I, _P, _P, _S, _P]),
+    "swx_rexi_prepared_bytes": (_S, [_P, _I, _I, _I]),
+    "swx_rexi_prepare": (_I, [_P, _I, _P, _I, _I, _P, _S, _P]),
+    "swx_rexi_sum_prepared": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _S, _P]),
     "swx_apply": (_I, [_P, C128, _P, _P, _P]),
     "swx_tree_combine": (_I, [_I, _I, _I, _P, _I, _P, _P]),
     "swx_state_axpy": (_I, [_I, _I, _P, _D, _P, _P, _P]),

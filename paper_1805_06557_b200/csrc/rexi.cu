@@ -8,6 +8,7 @@
 //   rexi_step     steppers.py:214-235  ETD psi sum  steppers.py:262-267
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstdio>
 #include <cstring>
@@ -87,7 +88,7 @@ __device__ __forceinline__ double2 tree_z(const double2 *__restrict__ D, int t0,
   }
 }
 
-constexpr int kLgLevels = 3;  // up to 8 leaf blocks per lane (np <= 512, 8 lanes per mode, leaf 8)
+constexpr int kLgLevels = 4;  // up to 16 leaf blocks per lane
 
 // Perfect tree over NB (power of two) consecutive leaf subtrees of LEAF
 // poles: a binary counter whose partial sums live in a statically indexed
@@ -895,37 +896,66 @@ static const int4 *lg_schedule(swx_solver s, int mpc, int *n_cta) {
   return e.first;
 }
 
+struct LgGeom {
+  int np, lpm, ppl, leaf, log2_ppl, log2_lpm;
+};
+
+static int lg_geom(int P, LgGeom &g) {
+  g.np = next_pow2(P);
+  // lanes per mode / leaf subtree (tuning overrides: SWX_LG_LPM, SWX_LG_LEAF)
+  static const int env_lpm = getenv("SWX_LG_LPM") ? atoi(getenv("SWX_LG_LPM")) : 8;
+  static const int env_leaf = getenv("SWX_LG_LEAF") ? atoi(getenv("SWX_LG_LEAF")) : 8;
+  g.lpm = std::min(env_lpm, g.np);
+  g.ppl = g.np / g.lpm;
+  g.leaf = std::min(g.ppl, env_leaf);
+  if (g.ppl / g.leaf > (1 << kLgLevels))
+    return fail(SWX_ERR_CONFIG, "lg tree deeper than the register stack");
+  g.log2_ppl = g.log2_lpm = 0;
+  while ((1 << g.log2_ppl) < g.ppl) ++g.log2_ppl;
+  while ((1 << g.log2_lpm) < g.lpm) ++g.log2_lpm;
+  return SWX_OK;
+}
+
+static size_t lg_table_bytes(swx_solver s, int n_rhs, int P) {
+  return (size_t)(s->trunc + 1) * n_rhs * 4 * next_pow2(P) * sizeof(double2);
+}
+
+// per-(pole, l) factor table of one pole chunk (beta folded in)
 template <int NRHS>
-static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
-                     int pole0, int P, int realify, double2 *out, double2 *fac_ws,
-                     cudaStream_t st) {
-  const int np = next_pow2(P);
-  const int lpm = std::min(8, np);       // lanes per mode
-  const int ppl = np / lpm;              // poles per lane
-  const int leaf = std::min(ppl, 8);
-  int log2_ppl = 0, log2_lpm = 0;
-  while ((1 << log2_ppl) < ppl) ++log2_ppl;
-  while ((1 << log2_lpm) < lpm) ++log2_lpm;
-  dim3 fg((np + 127) / 128, s->trunc + 1);
-  lg_factor_kernel<NRHS><<<fg, 128, 0, st>>>(s->d_alpha, betas, s->n_poles, pole0, P, np,
-                                             log2_ppl, lpm, s->trunc, s->dt, s->phibar,
-                                             s->d_lconst, fac_ws);
+static int build_lg_factors(swx_solver s, const double2 *betas, int pole0, int P, double2 *fac,
+                            cudaStream_t st) {
+  LgGeom g;
+  int rc = lg_geom(P, g);
+  if (rc) return rc;
+  dim3 fg((g.np + 127) / 128, s->trunc + 1);
+  lg_factor_kernel<NRHS><<<fg, 128, 0, st>>>(s->d_alpha, betas, s->n_poles, pole0, P, g.np,
+                                             g.log2_ppl, g.lpm, s->trunc, s->dt, s->phibar,
+                                             s->d_lconst, fac);
   SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+template <int NRHS>
+static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, int realify,
+                  double2 *out, cudaStream_t st) {
+  LgGeom g;
+  int rc = lg_geom(P, g);
+  if (rc) return rc;
   int n_cta = 0;
-  const int4 *sched = lg_schedule(s, kLgPasses * 4 * 32 / lpm, &n_cta);
+  const int4 *sched = lg_schedule(s, kLgPasses * 4 * 32 / g.lpm, &n_cta);
   if (!sched) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
-  const size_t smem = (size_t)NRHS * 4 * np * sizeof(double2);
-#define SWX_LG_CASE(LV)                                                                     \
-  case LV: {                                                                                \
-    auto k = rexi_lg_kernel<NRHS, LV>;                                                      \
-    if (smem > 48 * 1024)                                                                   \
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                        (int)smem));                                        \
-    k<<<n_cta, 128, smem, st>>>(rhs, fac_ws, np, lpm, log2_lpm, s->trunc, s->ncoef, sched,  \
-                                realify, out);                                              \
-    break;                                                                                  \
+  const size_t smem = (size_t)NRHS * 4 * g.np * sizeof(double2);
+#define SWX_LG_CASE(LV)                                                                        \
+  case LV: {                                                                                   \
+    auto k = rexi_lg_kernel<NRHS, LV>;                                                         \
+    if (smem > 48 * 1024)                                                                      \
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                        (int)smem));                                           \
+    k<<<n_cta, 128, smem, st>>>(rhs, fac, g.np, g.lpm, g.log2_lpm, s->trunc, s->ncoef, sched,  \
+                                realify, out);                                                 \
+    break;                                                                                     \
   }
-  switch (leaf) {
+  switch (g.leaf) {
     SWX_LG_CASE(1)
     SWX_LG_CASE(2)
     SWX_LG_CASE(4)
@@ -937,6 +967,15 @@ static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
 #undef SWX_LG_CASE
   SWX_LAUNCH_CHECK();
   return SWX_OK;
+}
+
+template <int NRHS>
+static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
+                     int pole0, int P, int realify, double2 *out, double2 *fac_ws,
+                     cudaStream_t st) {
+  int rc = build_lg_factors<NRHS>(s, betas, pole0, P, fac_ws, st);
+  if (rc) return rc;
+  return run_lg<NRHS>(s, rhs, fac_ws, P, realify, out, st);
 }
 
 template <int NRHS>
@@ -1011,6 +1050,83 @@ extern "C" int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
   return n_rhs == 1
              ? launch_l<1>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st)
              : launch_l<2>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st);
+}
+
+// ---- prepared pole sums: the lg factor tables depend only on (alpha, beta,
+// l), so callers that reuse one weight set (every ETD2RK step) build them once
+extern "C" size_t swx_rexi_prepared_bytes(swx_solver s, int n_rhs, int pole_begin,
+                                          int pole_end) {
+  if (!s || n_rhs < 1 || n_rhs > 2 || pole_end <= pole_begin) return 0;
+  const bool cor = s->group == SWX_GROUP_L && s->omega > 0.0;
+  if (cor) return 0;
+  const int P = pole_end - pole_begin;
+  const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
+  const size_t t = lg_table_bytes(s, n_rhs, std::min(P, kLgMaxP));
+  return chunks * ((t + 255) / 256) * 256;
+}
+
+extern "C" int swx_rexi_prepare(swx_solver s, int n_rhs, const swx_c128 *d_betas,
+                                int pole_begin, int pole_end, void *d_prep, size_t prep_bytes,
+                                void *stream) {
+  if (!s || !s->d_alpha) return fail(SWX_ERR_CONFIG, "solver not warmed");
+  if (n_rhs < 1 || n_rhs > 2) return fail(SWX_ERR_CONFIG, "n_rhs must be 1 or 2");
+  if (pole_begin < 0 || pole_end > s->n_poles || pole_end <= pole_begin)
+    return fail(SWX_ERR_CONFIG, "bad pole range");
+  const size_t need = swx_rexi_prepared_bytes(s, n_rhs, pole_begin, pole_end);
+  if (need == 0) return SWX_OK;
+  if (!d_prep || prep_bytes < need) return fail(SWX_ERR_CONFIG, "prepared buffer too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = pole_end - pole_begin;
+  const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
+  const size_t t = need / chunks;
+  for (int c = 0; c < chunks; ++c) {
+    const int p0 = pole_begin + c * kLgMaxP;
+    const int pc = std::min(kLgMaxP, pole_end - p0);
+    double2 *fac = (double2 *)((char *)d_prep + c * t);
+    const double2 *bet = (const double2 *)d_betas;
+    int rc = n_rhs == 1 ? build_lg_factors<1>(s, bet, p0, pc, fac, st)
+                        : build_lg_factors<2>(s, bet, p0, pc, fac, st);
+    if (rc) return rc;
+  }
+  return SWX_OK;
+}
+
+extern "C" int swx_rexi_sum_prepared(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                                     const swx_c128 *d_betas, const void *d_prep,
+                                     int pole_begin, int pole_end, int realify, swx_c128 *d_out,
+                                     void *d_workspace, size_t workspace_bytes, void *stream) {
+  const bool cor = s && s->group == SWX_GROUP_L && s->omega > 0.0;
+  if (!s || cor || !d_prep)  // nothing prepared for the chain solver
+    return swx_rexi_sum(s, n_rhs, d_rhs, d_betas, pole_begin, pole_end, realify, d_out,
+                        d_workspace, workspace_bytes, stream);
+  if (n_rhs < 1 || n_rhs > 2) return fail(SWX_ERR_CONFIG, "n_rhs must be 1 or 2");
+  if (pole_begin < 0 || pole_end > s->n_poles || pole_end <= pole_begin)
+    return fail(SWX_ERR_CONFIG, "bad pole range");
+  cudaStream_t st = (cudaStream_t)stream;
+  const double2 *rhs = (const double2 *)d_rhs;
+  double2 *out = (double2 *)d_out;
+  const int P = pole_end - pole_begin;
+  const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
+  const size_t t = swx_rexi_prepared_bytes(s, n_rhs, pole_begin, pole_end) / chunks;
+  if (chunks == 1)
+    return n_rhs == 1 ? run_lg<1>(s, rhs, (const double2 *)d_prep, P, realify, out, st)
+                      : run_lg<2>(s, rhs, (const double2 *)d_prep, P, realify, out, st);
+  const size_t stride = (size_t)n_rhs * 3 * s->ncoef;
+  if (!d_workspace || workspace_bytes < chunks * stride * sizeof(double2))
+    return fail(SWX_ERR_CONFIG, "workspace too small");
+  double2 *part = (double2 *)d_workspace;
+  for (int c = 0; c < chunks; ++c) {
+    const int pc = std::min(kLgMaxP, pole_end - (pole_begin + c * kLgMaxP));
+    const double2 *fac = (const double2 *)((const char *)d_prep + c * t);
+    int rc = n_rhs == 1 ? run_lg<1>(s, rhs, fac, pc, 0, part + c * stride, st)
+                        : run_lg<2>(s, rhs, fac, pc, 0, part + c * stride, st);
+    if (rc) return rc;
+  }
+  tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, chunks,
+                                                                        s->ncoef, s->trunc,
+                                                                        realify, out);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
 }
 
 extern "C" int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,

@@ -151,6 +151,35 @@ class ShiftedLinearSolver:
             ptr(out_dev), ptr(ws) if nbytes else 0, nbytes, stream_ptr(stream)))
         return out_dev
 
+    def prepare_dev(self, alphas, betas_dev, pole_range=None):
+        """Prepared factors for one weight set (None if the group needs none)."""
+        import torch
+
+        nat = self._native(alphas)
+        n_rhs = betas_dev.shape[0]
+        lo, hi = pole_range if pole_range is not None else (0, nat.alphas.size)
+        nbytes = int(self._lib.swx_rexi_prepared_bytes(nat.h, n_rhs, lo, hi))
+        if nbytes == 0:
+            return None
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=betas_dev.device)
+        _lib.check(self._lib.swx_rexi_prepare(nat.h, n_rhs, ptr(betas_dev), lo, hi, ptr(buf),
+                                              nbytes, stream_ptr()))
+        return buf
+
+    def rexi_sum_prepared_dev(self, alphas, betas_dev, prep, rhs_dev, out_dev, pole_range=None,
+                              realify: bool = True, stream=None):
+        if prep is None:
+            return self.rexi_sum_dev(alphas, betas_dev, rhs_dev, out_dev, pole_range, realify,
+                                     stream)
+        nat = self._native(alphas)
+        n_rhs = rhs_dev.shape[0]
+        lo, hi = pole_range if pole_range is not None else (0, nat.alphas.size)
+        ws, nbytes = self.workspace(nat, n_rhs, lo, hi)
+        _lib.check(self._lib.swx_rexi_sum_prepared(
+            nat.h, n_rhs, ptr(rhs_dev), ptr(betas_dev), ptr(prep), lo, hi, 1 if realify else 0,
+            ptr(out_dev), ptr(ws) if nbytes else 0, nbytes, stream_ptr(stream)))
+        return out_dev
+
     def apply_dev(self, alpha, x_dev, out_dev=None, stream=None):
         import torch
 

@@ -303,3 +303,19 @@ def test_polecomm_nccl_single_rank_matches_serial():
                 bd.validate()
     finally:
         dist.destroy_process_group()
+
+
+def test_prepared_sum_bitwise_equals_unprepared():
+    """swx_rexi_sum_prepared (cached lg factor tables) == swx_rexi_sum."""
+    par = params(63)
+    for group in (LG, L):
+        sl = ShiftedLinearSolver(group, 3600.0, par)
+        c0, c1 = coeffs(256, 0), coeffs(256, 1)
+        rhs = to_device(np.stack([pack(ost.seeded_linear_state(63, 1)),
+                                  pack(ost.seeded_linear_state(63, 2))]))
+        bet = to_device(np.stack([c0.betas, c1.betas]))
+        ref = sl.rexi_sum_dev(c0.alphas, bet, rhs).cpu().numpy()
+        prep = sl.prepare_dev(c0.alphas, bet)
+        out = torch.empty_like(rhs)
+        got = sl.rexi_sum_prepared_dev(c0.alphas, bet, prep, rhs, out).cpu().numpy()
+        assert np.array_equal(got, ref), group.token
