@@ -685,13 +685,11 @@ __global__ void ptab_kernel(ShtView p) {
 
 // prepared rows for the table analysis: Ag[m][part][par][nt16][8]
 constexpr int kAG = 8;
-// thread (m, pair) with m fastest: the FFT rows Q[field][j][m] are read
-// coalesced along m; each thread writes whole 64-byte prepared rows
 __global__ void prep_tab_tend_kernel(ShtView p, const double2 *Q, const double2 *lc, int atoms,
                                      double *A) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= p.nt16 || m >= p.nm) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (i >= p.nt16) return;
   double2 ev[7], od[7];
   tend_row(p, Q, lc, atoms, m, i, ev, od);
   const size_t ps = (size_t)p.nt16 * kAG;
@@ -1285,9 +1283,9 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
   }
   mark(4);
   if (p->use_tab) {
-    dim3 g((p->nm + 31) / 32, (p->nt16 + 3) / 4);
-    prep_tab_tend_kernel<<<g, dim3(32, 4), 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.lc,
-                                                   atoms, w.A);
+    dim3 g((p->nt16 + 127) / 128, p->nm);
+    prep_tab_tend_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.lc, atoms,
+                                           w.A);
     SWX_LAUNCH_CHECK();
     mark(5);
     if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s))) return rc;
