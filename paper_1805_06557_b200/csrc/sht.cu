@@ -104,38 +104,48 @@ constexpr int kSeg = 64;   // degrees per analysis segment
 
 constexpr int kSL = 128;  // l rows staged per chunk
 
-template <int MODE, bool TAB>
-__global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
+// SPLIT = 2: the CTA holds two half-blocks of NT = blockDim/2 threads (one
+// per latitude pair each); for columns longer than 96 degrees the second
+// half starts mid-column (a multiple of kSeg) from the plan-time recurrence
+// checkpoint, halving the per-thread walk of the long columns; the halves'
+// partial sums are added in a fixed order (first + second).
+template <int MODE, int SPLIT>
+__global__ void __launch_bounds__(512) synth_kernel(ShtView p, SynthArgs a) {
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
-  __shared__ double2 cs[NS][kSL];
-  __shared__ double4 rcs[kSL + 2];
+  constexpr int NACC = 4 * (NS + NH);
+  extern __shared__ __align__(16) double smem_syn[];
+  const int NT = blockDim.x / SPLIT;
+  const int half = threadIdx.x / NT, tt0 = threadIdx.x - half * NT;
+  double2 *cs = reinterpret_cast<double2 *>(smem_syn) + (size_t)half * NS * kSL;  // [NS][kSL]
+  double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)SPLIT * NS * kSL * 2) +
+                 (size_t)half * (kSL + 2);
   const int m = blockIdx.x;
-  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * NT + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
   const int T = p.trunc, nc = p.ncoef;
   const int off = col_offset(T, m);
   const int kmax = T + 1 - m;
   const double4 *rc = p.d_rc + rc_offset(T, m);
   const bool has = i < p.nh;
+  // this half's degree range [kb, ke) of the column
+  int split = kmax;
+  if (SPLIT == 2 && kmax > 96) split = ((kmax / 2 + kSeg - 1) / kSeg) * kSeg;
+  const int kb = half == 0 ? 0 : split;
+  const int ke = half == 0 ? split : kmax;
   double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
-  // table path: plane pointers of column m (pair i)
-  const double *tp0 = nullptr, *tp1 = nullptr;
-  if (TAB) {
-    const int half = (T + 3 - m) >> 1;
-    tp0 = p.d_ptab + p.d_ptoff[m] + i;
-    tp1 = tp0 + (size_t)half * p.nt16;
-  }
   if (has) {
     x = p.d_x[i];
     rcos = p.d_rcos[i];
-    if (TAB) {
-      p0 = tp0[0];
-      p1 = tp1[0];
-    } else {
+    if (kb == 0) {
       const double seed = p.d_seed[(size_t)m * p.nh + i];
       p0 = seed;
       p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
+    } else if (kb < kmax) {
+      const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + kb / kSeg) * 3 * p.nh;
+      pm1 = ck[i];
+      p0 = ck[p.nh + i];
+      p1 = ck[2 * p.nh + i];
     }
   }
   double2 sp[2][NS], sh[2][NH > 0 ? NH : 1];
@@ -146,34 +156,37 @@ __global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
 #pragma unroll
     for (int s = 0; s < (NH > 0 ? NH : 1); ++s) sh[q][s] = make_double2(0.0, 0.0);
   }
-  for (int l0 = m; l0 <= T; l0 += kSL) {
-    const int n = min(kSL, T + 1 - l0);
+  const int nchunk0 = (split + kSL - 1) / kSL, nchunk1 = (kmax - split + kSL - 1) / kSL;
+  const int nchunk = SPLIT == 2 ? max(nchunk0, nchunk1) : nchunk0;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int k0 = kb + ch * kSL;  // chunk start (even)
+    const int n = max(0, min(kSL, ke - k0));
     __syncthreads();
-    for (int t = threadIdx.x; t < kSL + 2; t += blockDim.x) {
-      const int k = l0 - m + t;
-      if (k <= kmax) rcs[t] = rc[k];
+    for (int t = tt0; t < kSL + 2; t += NT) {
+      const int k = k0 + t;
+      if (n > 0 && k <= kmax) rcs[t] = rc[k];
     }
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      const int s = off + (l0 - m) + t;
+    for (int t = tt0; t < n; t += NT) {
+      const int s = off + k0 + t;
       if (MODE == 0) {
-        const double il = p.d_lconst[l0 + t];
+        const double il = p.d_lconst[m + k0 + t];
         const double2 z = a.coef[nc + s], d = a.coef[2 * nc + s];
-        cs[0][t] = z;
-        cs[1][t] = d;
-        cs[NS > 2 ? 2 : 0][t] = a.coef[s];
-        cs[NS > 3 ? 3 : 0][t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
-        cs[NS > 4 ? 4 : 0][t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+        cs[0 * kSL + t] = z;
+        cs[(NS > 1 ? 1 : 0) * kSL + t] = d;
+        cs[(NS > 2 ? 2 : 0) * kSL + t] = a.coef[s];
+        cs[(NS > 3 ? 3 : 0) * kSL + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
+        cs[(NS > 4 ? 4 : 0) * kSL + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
       } else {
-        cs[0][t] = a.coef[(size_t)field * nc + s];
+        cs[t] = a.coef[(size_t)field * nc + s];
       }
     }
     __syncthreads();
     for (int t = 0; t < n; t += 2) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {  // static parity: l - m = (l0 - m) + t + q
+      for (int q = 0; q < 2; ++q) {  // static parity: l - m = k0 + t + q, k0 even
         if (q == 1 && t + 1 >= n) break;
         const int tt = t + q;
-        const int k = l0 - m + tt;
+        const int k = k0 + tt;
         const double P = p0;
         double H = 0.0;
         if (NH > 0) {
@@ -182,28 +195,59 @@ __global__ void __launch_bounds__(256) synth_kernel(ShtView p, SynthArgs a) {
         }
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-          const double2 v = cs[s][tt];
+          const double2 v = cs[s * kSL + tt];
           sp[q][s].x = fma(P, v.x, sp[q][s].x);
           sp[q][s].y = fma(P, v.y, sp[q][s].y);
         }
 #pragma unroll
         for (int s = 0; s < NH; ++s) {
-          const double2 v = cs[NS > 3 ? 3 + s : 0][tt];
+          const double2 v = cs[(NS > 3 ? 3 + s : 0) * kSL + tt];
           sh[q][s].x = fma(H, v.x, sh[q][s].x);
           sh[q][s].y = fma(H, v.y, sh[q][s].y);
         }
         double p2 = 0.0;
         if (k + 2 <= kmax) {
-          if (TAB) {
-            if (has) p2 = ((k + 2) & 1 ? tp1 : tp0)[(size_t)((k + 2) >> 1) * p.nt16];
-          } else {
-            const double4 c2 = rcs[tt + 2];
-            p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
-          }
+          const double4 c2 = rcs[tt + 2];
+          p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
         }
         pm1 = p0;
         p0 = p1;
         p1 = p2;
+      }
+    }
+  }
+  if (SPLIT == 2) {
+    // second half hands its partial sums to the first (fixed order)
+    __syncthreads();
+    double *red = smem_syn;  // [NT][NACC] (reuses the staging area)
+    if (half == 1) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+          red[(size_t)tt0 * NACC + (q * NS + s2) * 2] = sp[q][s2].x;
+          red[(size_t)tt0 * NACC + (q * NS + s2) * 2 + 1] = sp[q][s2].y;
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < NH; ++s2) {
+          red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2] = sh[q][s2].x;
+          red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2 + 1] = sh[q][s2].y;
+        }
+      }
+    }
+    __syncthreads();
+    if (half == 1) return;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) {
+        sp[q][s2].x += red[(size_t)tt0 * NACC + (q * NS + s2) * 2];
+        sp[q][s2].y += red[(size_t)tt0 * NACC + (q * NS + s2) * 2 + 1];
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < NH; ++s2) {
+        sh[q][s2].x += red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2];
+        sh[q][s2].y += red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2 + 1];
       }
     }
   }
@@ -1157,11 +1201,28 @@ static int check_ws(swx_sht p, void *ws, size_t bytes) {
   return SWX_OK;
 }
 
+static size_t synth_smem(int ns, int nh, int split, int nt) {
+  const size_t stage = (size_t)split * (ns * kSL * 2 + (kSL + 2) * 4) * sizeof(double);
+  const size_t red = split == 2 ? (size_t)nt * 4 * (ns + nh) * sizeof(double) : 0;
+  return std::max(stage, red);
+}
+
 template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
-  // the recurrence walker beats streaming the table here (the table loads
-  // would sit on the critical path two steps ahead of their use)
-  synth_kernel<MODE, false><<<g, nt, 0, s>>>(static_cast<const ShtView &>(*p), a);
+  const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
+  if (p->nh <= 256 && p->d_ckpt) {  // one pair-block per column: split long columns
+    const size_t smem = synth_smem(ns, nh, 2, nt);
+    auto k = synth_kernel<MODE, 2>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<g, 2 * nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+  } else {
+    const size_t smem = synth_smem(ns, nh, 1, nt);
+    auto k = synth_kernel<MODE, 1>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<g, nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+  }
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
