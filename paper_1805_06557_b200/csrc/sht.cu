@@ -1210,7 +1210,10 @@ static size_t synth_smem(int ns, int nh, int split, int nt) {
 template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
-  if (p->nh <= 256 && p->d_ckpt) {  // one pair-block per column: split long columns
+  // split long columns over two half-blocks (plain synthesis only: for the
+  // 7-series state variant the 448-thread CTAs fit one per SM and lose more
+  // to waves than they gain on the critical path)
+  if (MODE == 1 && p->nh <= 256 && p->d_ckpt) {
     const size_t smem = synth_smem(ns, nh, 2, nt);
     auto k = synth_kernel<MODE, 2>;
     if (smem > 48 * 1024)
