@@ -328,15 +328,23 @@ def main():
             b, prep = dr.betas_for(ks)
             dr.solver.rexi_sum_prepared_dev(dr.alphas, b, prep, rhs, out, dr.range,
                                             comm is None)
-        breakdown["rexi_lg_pair"] = {"ms_per_launch": timed(
-            lambda: local_sum((0, 1), eng.pair_in, eng.pair_out)), "launches_per_step": 1}
-        breakdown["rexi_lg_single"] = {"ms_per_launch": timed(
-            lambda: local_sum((2,), eng.d, eng.r2)), "launches_per_step": 1}
+        # the step runs three single-RHS prepared sums: psi0(u) (side stream,
+        # concurrent with N(u)), psi1(N(u)), psi2(N(a) - N(u)); warm caches first
+        for ks, rhs, o in (((0,), eng.pair_in[0:1], eng.pair_out[0:1]),
+                           ((1,), eng.pair_in[1:2], eng.pair_out[1:2]), ((2,), eng.d, eng.r2)):
+            local_sum(ks, rhs, o)
+        torch.cuda.synchronize()
+        breakdown["rexi_lg_psi0_overlapped"] = {"ms_per_launch": timed(
+            lambda: local_sum((0,), eng.pair_in[0:1], eng.pair_out[0:1])), "launches_per_step": 1}
+        breakdown["rexi_lg"] = {"ms_per_launch": timed(
+            lambda: local_sum((2,), eng.d, eng.r2)), "launches_per_step": 2}
         breakdown["axpy"] = {"ms_per_launch": timed(
             lambda: axpy(w.trunc, eng.a, w.dt, eng.r2[0], eng.na)), "launches_per_step": 3}
         for v in breakdown.values():
             v["ms_per_step"] = v["ms_per_launch"] * v["launches_per_step"]
-        dominant = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
+        # psi0(u) runs concurrently with N(u), off the critical path
+        dominant = max((k for k in breakdown if not k.endswith("_overlapped")),
+                       key=lambda k: breakdown[k]["ms_per_step"])
     elif not etd:
         breakdown["rexi_" + w.group] = {"ms_per_launch": ms_per_step, "launches_per_step": 1,
                                         "ms_per_step": ms_per_step}
@@ -346,8 +354,7 @@ def main():
     nlat = par.cfg.nlat
     leg = 4.0 * nlat * nc  # per complex series, no symmetry credit
     flops = {
-        "rexi_lg_pair": 2 * 40.0 * w.n_poles * nc,
-        "rexi_lg_single": 40.0 * w.n_poles * nc,
+        "rexi_lg_psi0_overlapped": 40.0 * w.n_poles * nc,
         "rexi_lg": 40.0 * w.n_poles * nc,
         "rexi_l": 142.0 * w.n_poles * nc,
         "synth_state": 7 * leg,
@@ -414,7 +421,7 @@ def main():
         cpu = {"value": units_per_step / sec, "unit": "pole-solve*coeff/s",
                "cores": len(os.sched_getaffinity(0)), "kind": "port", "sample": sample}
 
-    per_step_launches = 15 if etd else (1 if w.group == "lg" else 2)
+    per_step_launches = 16 if etd else (1 if w.group == "lg" else 2)
     line = {
         "metric": "REXI pole-solves*SH-coeffs/s", "value": value, "unit": "pole-solve*coeff/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
