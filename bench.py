@@ -290,7 +290,8 @@ def main():
     if etd:
         plan = eng.plan
         reps = 5
-        stage_names = ["synth_state", "fft_c2r", "grid_products", "fft_r2c", "prep", "analysis"]
+        # with the fused grid stage, C2R+products+R2C+prep all land in "grid_fused"
+        stage_names = ["synth_state", "fft_c2r", "grid_products", "grid_fused", "prep", "analysis"]
         acc = np.zeros(7)
         for _ in range(reps):
             flush.zero_()

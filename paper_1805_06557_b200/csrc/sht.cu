@@ -67,6 +67,10 @@ struct ShtView {
   // parity-split planes per column: ptab[ptoff[m] + (par*half(m) + r)*nt16 + pair]
   // with l - m = 2r + par, l = m..T+1, half(m) = (T+3-m)/2
   int use_tab = 0;
+  int fused_grid = 0;          // fused grid stage (nlon_t <= 1024, table path)
+  int fft_npass = 0;
+  int fft_radix[12] = {0};
+  double2 *d_tw = nullptr;     // W_N^t, t < nlon_t
   int nt16 = 0;                // pairs padded to 16
   long long *d_ptoff = nullptr;
   double *d_ptab = nullptr;
@@ -332,6 +336,7 @@ __global__ void products_kernel(double *g, size_t npts) {
 // (vortdiv_from_uv, sphere.py:405-430; tendency_lc/n, swe.py:188-251)
 // ---------------------------------------------------------------------
 constexpr int kAS = 12;  // row stride (doubles) of prepared rows: conflict-free B fragments
+constexpr int kAG = 8;   // row stride of the prepared rows of the table path (global)
 
 __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
 #pragma unroll
@@ -344,51 +349,38 @@ __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
 
 // fold one latitude pair of the tendency inputs into even/odd parts of the
 // 7 analysis series (the prepared row of pair i, column m)
-__device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, const double2 *lc,
-                                         int atoms, int m, int i, double2 *ev, double2 *od) {
-  if (i >= p.nh) {
-#pragma unroll
-    for (int s = 0; s < 7; ++s) ev[s] = od[s] = make_double2(0.0, 0.0);
-    return;
-  }
+// fold one latitude pair of the tendency inputs into even/odd parts of the
+// 7 analysis series (the prepared row of pair i, column m).  F[hemi][5] are
+// the products' Fourier coefficients times dlon (phi'u, phi'v, vort u,
+// vort v, KE), L1/L2[hemi] the Fourier-space Coriolis terms.
+__device__ __forceinline__ void tend_fold(const ShtView &p, const double2 (&F)[2][5],
+                                          const double2 (&L1)[2], const double2 (&L2)[2],
+                                          int m, int i, double2 *ev, double2 *od) {
   const int jn = p.d_jn[i], js = p.d_js[i];
   const double rcos = p.d_rcos[i];
   const double ra = 1.0 / p.radius;
   const double fm = (double)m;
-  const bool nl = (atoms & SWX_TEND_N) != 0;
   double2 av[2][7];
 #pragma unroll
   for (int hemi = 0; hemi < 2; ++hemi) {
-    const int j = hemi ? js : jn;
     const double wj = hemi ? p.d_ws[i] : p.d_wn[i];
     const double woc = wj * rcos;
-    const size_t row = (size_t)p.nlat * p.nfreq_t;
-    const size_t at = (size_t)j * p.nfreq_t + m;
-    double2 F[5];
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-      const double2 q = nl ? Q[s * row + at] : make_double2(0.0, 0.0);
-      F[s] = make_double2(q.x * p.dlon_t, q.y * p.dlon_t);  // fft * dlon
-    }
-    double2 l1 = make_double2(0.0, 0.0), l2 = l1;
-    if (atoms & SWX_TEND_LC) {
-      l1 = lc[(size_t)j * p.nm + m];
-      l2 = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
-    }
+    const double2 *Fh = F[hemi];
+    const double2 l1 = L1[hemi], l2 = L2[hemi];
     // (i m / a) * woc * F  ==  woc*m/a * (-F.y, F.x)
     const double cm = woc * fm * ra;
-    const double2 imPu = make_double2(-cm * F[0].y, cm * F[0].x);  // phi'u
-    const double2 imZu = make_double2(-cm * F[2].y, cm * F[2].x);  // vort u
-    const double2 imZv = make_double2(-cm * F[3].y, cm * F[3].x);  // vort v
+    const double2 imPu = make_double2(-cm * Fh[0].y, cm * Fh[0].x);  // phi'u
+    const double2 imZu = make_double2(-cm * Fh[2].y, cm * Fh[2].x);  // vort u
+    const double2 imZv = make_double2(-cm * Fh[3].y, cm * Fh[3].x);  // vort v
     const double wa = wj * ra;
     double2 *o = av[hemi];
     o[0] = make_double2(wj * l1.x - imZu.x, wj * l1.y - imZu.y);
     o[1] = make_double2(wj * l2.x + imZv.x, wj * l2.y + imZv.y);
     o[2] = make_double2(-imPu.x, -imPu.y);
-    o[3] = make_double2(wj * F[4].x, wj * F[4].y);
-    o[4] = make_double2(wa * F[3].x, wa * F[3].y);
-    o[5] = make_double2(wa * F[2].x, wa * F[2].y);
-    o[6] = make_double2(wa * F[1].x, wa * F[1].y);
+    o[3] = make_double2(wj * Fh[4].x, wj * Fh[4].y);
+    o[4] = make_double2(wa * Fh[3].x, wa * Fh[3].y);
+    o[5] = make_double2(wa * Fh[2].x, wa * Fh[2].y);
+    o[6] = make_double2(wa * Fh[1].x, wa * Fh[1].y);
   }
   if (js == jn) {  // equator node of an odd grid: counted once
 #pragma unroll
@@ -399,6 +391,201 @@ __device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, con
       ev[s] = make_double2(av[0][s].x + av[1][s].x, av[0][s].y + av[1][s].y);
       od[s] = make_double2(av[0][s].x - av[1][s].x, av[0][s].y - av[1][s].y);
     }
+  }
+}
+
+__device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, const double2 *lc,
+                                         int atoms, int m, int i, double2 *ev, double2 *od) {
+  if (i >= p.nh) {
+#pragma unroll
+    for (int s = 0; s < 7; ++s) ev[s] = od[s] = make_double2(0.0, 0.0);
+    return;
+  }
+  const int jn = p.d_jn[i], js = p.d_js[i];
+  const bool nl = (atoms & SWX_TEND_N) != 0;
+  double2 F[2][5], L1[2], L2[2];
+#pragma unroll
+  for (int hemi = 0; hemi < 2; ++hemi) {
+    const int j = hemi ? js : jn;
+    const size_t row = (size_t)p.nlat * p.nfreq_t;
+    const size_t at = (size_t)j * p.nfreq_t + m;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const double2 q = nl ? Q[s * row + at] : make_double2(0.0, 0.0);
+      F[hemi][s] = make_double2(q.x * p.dlon_t, q.y * p.dlon_t);  // fft * dlon
+    }
+    L1[hemi] = L2[hemi] = make_double2(0.0, 0.0);
+    if (atoms & SWX_TEND_LC) {
+      L1[hemi] = lc[(size_t)j * p.nm + m];
+      L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
+    }
+  }
+  tend_fold(p, F, L1, L2, m, i, ev, od);
+}
+
+// ---------------------------------------------------------------------
+// Fused grid stage of the tendency (replaces zero-pad + C2R FFT + products
+// + R2C FFT + prep): one CTA per latitude pair.  The north and south rows of
+// a real field share one complex FFT (z = north + i south).  Mixed-radix
+// Stockham FFT of length nlon_t (7-smooth) in shared memory, twiddles from a
+// plan-time table W_N^t = exp(-2 pi i t / N).
+// ---------------------------------------------------------------------
+constexpr int kMaxPass = 12;
+constexpr int kGridT = 256;
+
+__device__ __forceinline__ double2 tw_get(const double2 *tw, int t, int N, bool inv) {
+  const double2 w = tw[t % N];
+  return inv ? make_double2(w.x, -w.y) : w;
+}
+
+// in-place (ping-pong) Stockham FFT over the CTA; returns the buffer holding
+// the result (a or b).  inv: sign +1 (unnormalised inverse)
+__device__ double2 *cta_fft(double2 *a, double2 *b, int N, const int *radix, int npass,
+                            const double2 *tw, bool inv) {
+  int Ns = 1;
+  double2 *in = a, *out = b;
+  for (int ps = 0; ps < npass; ++ps) {
+    const int R = radix[ps];
+    const int nb = N / R;
+    const int tstep = N / (Ns * R);  // twiddle index unit
+    const int rstep = N / R;         // radix-R root index unit
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+      const int k = j % Ns;
+      double2 v[7];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        if (r < R) {
+          double2 x = in[j + r * nb];
+          if (r > 0) x = cmul(x, tw_get(tw, r * k * tstep, N, inv));
+          v[r] = x;
+        }
+      }
+      const int idxD = (j / Ns) * Ns * R + k;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        if (q < R) {
+          double2 acc = v[0];
+#pragma unroll
+          for (int r = 1; r < 7; ++r)
+            if (r < R) acc = cfma(v[r], tw_get(tw, ((r * q) % R) * rstep, N, inv), acc);
+          out[idxD + q * Ns] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    Ns *= R;
+    double2 *t = in;
+    in = out;
+    out = t;
+  }
+  return in;
+}
+
+__global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const double2 *c2r,
+                                                           const double2 *lc, int atoms,
+                                                           const double2 *tw_g, double *A) {
+  extern __shared__ __align__(16) double2 gsm[];
+  const int N = p.nlon_t, T = p.trunc;
+  const int i = blockIdx.x;  // latitude pair (padded to nt16)
+  const size_t ps = (size_t)p.nt16 * kAG;
+  if (i >= p.nh) {  // padding pairs: zero prepared rows
+    for (int m = threadIdx.x; m <= T; m += blockDim.x) {
+      double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < kAG; ++c) base[q * ps + c] = 0.0;
+    }
+    return;
+  }
+  double2 *tw = gsm;                    // [N]
+  double2 *buf[6];
+#pragma unroll
+  for (int b = 0; b < 6; ++b) buf[b] = gsm + (size_t)(1 + b) * N;
+  for (int t = threadIdx.x; t < N; t += blockDim.x) tw[t] = tw_g[t];
+  const int jn = p.d_jn[i], js = p.d_js[i];
+  const size_t row = (size_t)p.nlat * p.nfreq_t;
+  const bool nl = (atoms & SWX_TEND_N) != 0;
+  double2 *res[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (nl) {
+    // inverse: grids of u, v, vort, phi' (z = north + i south) into buf[0..3]
+    double2 *grid[4];
+    int freeb = 4;  // buf[4], buf[5] free
+    double2 *spare[2] = {buf[4], buf[5]};
+    for (int f = 0; f < 4; ++f) {
+      double2 *z = buf[f];
+      const double2 *Xn = c2r + f * row + (size_t)jn * p.nfreq_t;
+      const double2 *Xs = c2r + f * row + (size_t)js * p.nfreq_t;
+      for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        double2 X = make_double2(0.0, 0.0), Y = X;
+        if (k <= T) {
+          X = Xn[k];
+          Y = Xs[k];
+        } else if (N - k <= T) {
+          const double2 a = Xn[N - k], b = Xs[N - k];
+          X = make_double2(a.x, -a.y);
+          Y = make_double2(b.x, -b.y);
+        }
+        z[k] = make_double2(X.x - Y.y, X.y + Y.x);  // X + i Y
+      }
+      __syncthreads();
+      double2 *r = cta_fft(z, spare[0], N, p.fft_radix, p.fft_npass, tw, true);
+      if (r != z) {  // result landed in the spare: swap roles
+        spare[0] = z;
+      }
+      grid[f] = r;
+      (void)freeb;
+    }
+    // products on the grid, north in Re, south in Im:
+    // phi'u, phi'v, vort u, vort v, |V|^2/2  (swe.py:230-245)
+    double2 *out5[5] = {grid[0], grid[1], grid[2], grid[3], spare[0]};
+    double2 *spare_fwd = spare[1];
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const double2 u = grid[0][n], v = grid[1][n], z = grid[2][n], ph = grid[3][n];
+      out5[0][n] = make_double2(ph.x * u.x, ph.y * u.y);
+      out5[1][n] = make_double2(ph.x * v.x, ph.y * v.y);
+      out5[2][n] = make_double2(z.x * u.x, z.y * u.y);
+      out5[3][n] = make_double2(z.x * v.x, z.y * v.y);
+      out5[4][n] = make_double2(0.5 * (u.x * u.x + v.x * v.x), 0.5 * (u.y * u.y + v.y * v.y));
+    }
+    __syncthreads();
+    for (int f = 0; f < 5; ++f) {
+      double2 *r = cta_fft(out5[f], spare_fwd, N, p.fft_radix, p.fft_npass, tw, false);
+      if (r != out5[f]) spare_fwd = out5[f];
+      res[f] = r;
+    }
+  }
+  // fold + prepared rows for every m of this pair
+  for (int m = threadIdx.x; m <= T; m += blockDim.x) {
+    double2 F[2][5], L1[2], L2[2];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+      double2 X = make_double2(0.0, 0.0), Y = X;
+      if (nl) {
+        const double2 a = res[f][m], b = res[f][m == 0 ? 0 : N - m];
+        // X = (Z_m + conj Z_{N-m}) / 2, Y = (Z_m - conj Z_{N-m}) / (2i)
+        X = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+        Y = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
+      }
+      F[0][f] = make_double2(X.x * p.dlon_t, X.y * p.dlon_t);
+      F[1][f] = make_double2(Y.x * p.dlon_t, Y.y * p.dlon_t);
+    }
+#pragma unroll
+    for (int hemi = 0; hemi < 2; ++hemi) {
+      const int j = hemi ? js : jn;
+      L1[hemi] = L2[hemi] = make_double2(0.0, 0.0);
+      if (atoms & SWX_TEND_LC) {
+        L1[hemi] = lc[(size_t)j * p.nm + m];
+        L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
+      }
+    }
+    double2 ev[7], od[7];
+    tend_fold(p, F, L1, L2, m, i, ev, od);
+    double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+    put_row(base + 0 * ps, ev, 4);
+    put_row(base + 1 * ps, od, 4);
+    put_row(base + 2 * ps, ev + 4, 3);
+    put_row(base + 3 * ps, od + 4, 3);
   }
 }
 
@@ -728,7 +915,6 @@ __global__ void ptab_kernel(ShtView p) {
 }
 
 // prepared rows for the table analysis: Ag[m][part][par][nt16][8]
-constexpr int kAG = 8;
 __global__ void prep_tab_tend_kernel(ShtView p, const double2 *Q, const double2 *lc, int atoms,
                                      double *A) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1069,6 +1255,27 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
       }
     }
   }
+  // fused grid stage: radix plan + twiddle table of the tendency FFT length
+  if (p->use_tab && p->nlon_t <= 1024) {
+    int n = p->nlon_t, np = 0;
+    bool ok = true;
+    for (int r : {4, 2, 3, 5, 7})
+      while (n % r == 0 && np < kMaxPass) {
+        p->fft_radix[np++] = r;
+        n /= r;
+      }
+    ok = n == 1;
+    if (ok) {
+      p->fft_npass = np;
+      std::vector<double2> tw(p->nlon_t);
+      for (int t = 0; t < p->nlon_t; ++t) {
+        const double ang = -2.0 * M_PI * (double)t / p->nlon_t;
+        tw[t] = make_double2(std::cos(ang), std::sin(ang));
+      }
+      up((void **)&p->d_tw, tw.data(), sizeof(double2) * tw.size());
+      p->fused_grid = e == cudaSuccess;
+    }
+  }
   cufftHandle h;
   int rcd = get_plan(p, CUFFT_Z2D, p->nlon_t, 4 * nlat, &h);
   if (!rcd) rcd = get_plan(p, CUFFT_D2Z, p->nlon_t, 5 * nlat, &h);
@@ -1101,6 +1308,7 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_ptab);
   cudaFree(p->d_rcos16);
   cudaFree(p->d_titems);
+  cudaFree(p->d_tw);
   delete p;
   return SWX_OK;
 }
@@ -1331,6 +1539,33 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     if (ev) cudaEventRecord(ev[k], s);
   };
   mark(0);
+  if (p->fused_grid) {
+    // synthesis writes bins 0..T only; the fused grid kernel never reads above T
+    SynthArgs a;
+    a.coef = state;
+    a.c2r = w.c2r;
+    a.lc = w.lc;
+    a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
+    a.nfreq = p->nfreq_t;
+    int nt;
+    dim3 g = synth_grid(p, 1, &nt);
+    if ((rc = launch_synth<0>(p, g, nt, a, s))) return rc;
+    mark(1);
+    mark(2);
+    mark(3);
+    const size_t smem = (size_t)7 * p->nlon_t * sizeof(double2);
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(grid_tend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    grid_tend_kernel<<<p->nt16, kGridT, smem, s>>>(static_cast<const ShtView &>(*p), w.c2r, w.lc,
+                                                   atoms, p->d_tw, w.A);
+    SWX_LAUNCH_CHECK();
+    mark(4);
+    mark(5);
+    if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s))) return rc;
+    mark(6);
+    return SWX_OK;
+  }
   if ((rc = synth_state(p, state, w, (atoms & SWX_TEND_LC) ? 1 : 0, p->nfreq_t, s))) return rc;
   mark(1);
   if (atoms & SWX_TEND_N) {
