@@ -433,44 +433,52 @@ __device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, con
 constexpr int kMaxPass = 12;
 constexpr int kGridT = 256;
 
-__device__ __forceinline__ double2 tw_get(const double2 *tw, int t, int N, bool inv) {
-  const double2 w = tw[t % N];
-  return inv ? make_double2(w.x, -w.y) : w;
+// one Stockham pass of radix R over the CTA (twiddle index r*k*N/(Ns*R) < N)
+template <int R>
+__device__ __forceinline__ void fft_pass(const double2 *in, double2 *out, int N, int Ns,
+                                         const double2 *tw, bool inv) {
+  const int nb = N / R;
+  const int tstep = N / (Ns * R);
+  double2 wr[R];  // radix-R roots W_R^j
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const double2 w = tw[j * (N / R)];
+    wr[j] = inv ? make_double2(w.x, -w.y) : w;
+  }
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+    const int k = j % Ns;
+    double2 v[R];
+    v[0] = in[j];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double2 w0 = tw[r * k * tstep];
+      v[r] = cmul(in[j + r * nb], inv ? make_double2(w0.x, -w0.y) : w0);
+    }
+    const int idxD = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      double2 acc = v[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) acc = cfma(v[r], wr[(r * q) % R], acc);
+      out[idxD + q * Ns] = acc;
+    }
+  }
 }
 
-// in-place (ping-pong) Stockham FFT over the CTA; returns the buffer holding
-// the result (a or b).  inv: sign +1 (unnormalised inverse)
+// Stockham FFT over the CTA (ping-pong a/b); returns the buffer holding the
+// result.  inv: sign +1 (unnormalised inverse)
 __device__ double2 *cta_fft(double2 *a, double2 *b, int N, const int *radix, int npass,
                             const double2 *tw, bool inv) {
   int Ns = 1;
   double2 *in = a, *out = b;
   for (int ps = 0; ps < npass; ++ps) {
     const int R = radix[ps];
-    const int nb = N / R;
-    const int tstep = N / (Ns * R);  // twiddle index unit
-    const int rstep = N / R;         // radix-R root index unit
-    for (int j = threadIdx.x; j < nb; j += blockDim.x) {
-      const int k = j % Ns;
-      double2 v[7];
-#pragma unroll
-      for (int r = 0; r < 7; ++r) {
-        if (r < R) {
-          double2 x = in[j + r * nb];
-          if (r > 0) x = cmul(x, tw_get(tw, r * k * tstep, N, inv));
-          v[r] = x;
-        }
-      }
-      const int idxD = (j / Ns) * Ns * R + k;
-#pragma unroll
-      for (int q = 0; q < 7; ++q) {
-        if (q < R) {
-          double2 acc = v[0];
-#pragma unroll
-          for (int r = 1; r < 7; ++r)
-            if (r < R) acc = cfma(v[r], tw_get(tw, ((r * q) % R) * rstep, N, inv), acc);
-          out[idxD + q * Ns] = acc;
-        }
-      }
+    switch (R) {
+      case 2: fft_pass<2>(in, out, N, Ns, tw, inv); break;
+      case 3: fft_pass<3>(in, out, N, Ns, tw, inv); break;
+      case 4: fft_pass<4>(in, out, N, Ns, tw, inv); break;
+      case 5: fft_pass<5>(in, out, N, Ns, tw, inv); break;
+      default: fft_pass<7>(in, out, N, Ns, tw, inv); break;
     }
     __syncthreads();
     Ns *= R;
