@@ -434,9 +434,10 @@ constexpr int kMaxPass = 12;
 constexpr int kGridT = 256;
 
 // one Stockham pass of radix R over the CTA (twiddle index r*k*N/(Ns*R) < N)
+// nbat independent length-N arrays stored back to back (stride N)
 template <int R>
-__device__ __forceinline__ void fft_pass(const double2 *in, double2 *out, int N, int Ns,
-                                         const double2 *tw, bool inv) {
+__device__ __forceinline__ void fft_pass(const double2 *in0, double2 *out0, int N, int Ns,
+                                         int nbat, const double2 *tw, bool inv) {
   const int nb = N / R;
   const int tstep = N / (Ns * R);
   double2 wr[R];  // radix-R roots W_R^j
@@ -445,7 +446,10 @@ __device__ __forceinline__ void fft_pass(const double2 *in, double2 *out, int N,
     const double2 w = tw[j * (N / R)];
     wr[j] = inv ? make_double2(w.x, -w.y) : w;
   }
-  for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+  for (int jb = threadIdx.x; jb < nbat * nb; jb += blockDim.x) {
+    const int bt = jb / nb, j = jb - bt * nb;
+    const double2 *in = in0 + (size_t)bt * N;
+    double2 *out = out0 + (size_t)bt * N;
     const int k = j % Ns;
     double2 v[R];
     v[0] = in[j];
@@ -467,18 +471,18 @@ __device__ __forceinline__ void fft_pass(const double2 *in, double2 *out, int N,
 
 // Stockham FFT over the CTA (ping-pong a/b); returns the buffer holding the
 // result.  inv: sign +1 (unnormalised inverse)
-__device__ double2 *cta_fft(double2 *a, double2 *b, int N, const int *radix, int npass,
-                            const double2 *tw, bool inv) {
+__device__ double2 *cta_fft(double2 *a, double2 *b, int N, int nbat, const int *radix,
+                            int npass, const double2 *tw, bool inv) {
   int Ns = 1;
   double2 *in = a, *out = b;
   for (int ps = 0; ps < npass; ++ps) {
     const int R = radix[ps];
     switch (R) {
-      case 2: fft_pass<2>(in, out, N, Ns, tw, inv); break;
-      case 3: fft_pass<3>(in, out, N, Ns, tw, inv); break;
-      case 4: fft_pass<4>(in, out, N, Ns, tw, inv); break;
-      case 5: fft_pass<5>(in, out, N, Ns, tw, inv); break;
-      default: fft_pass<7>(in, out, N, Ns, tw, inv); break;
+      case 2: fft_pass<2>(in, out, N, Ns, nbat, tw, inv); break;
+      case 3: fft_pass<3>(in, out, N, Ns, nbat, tw, inv); break;
+      case 4: fft_pass<4>(in, out, N, Ns, nbat, tw, inv); break;
+      case 5: fft_pass<5>(in, out, N, Ns, nbat, tw, inv); break;
+      default: fft_pass<7>(in, out, N, Ns, nbat, tw, inv); break;
     }
     __syncthreads();
     Ns *= R;
@@ -506,62 +510,46 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     }
     return;
   }
-  double2 *tw = gsm;                    // [N]
-  double2 *buf[6];
-#pragma unroll
-  for (int b = 0; b < 6; ++b) buf[b] = gsm + (size_t)(1 + b) * N;
+  double2 *tw = gsm;                 // [N]
+  double2 *X = gsm + N;              // [5][N]
+  double2 *Y = X + (size_t)5 * N;    // [5][N]
   for (int t = threadIdx.x; t < N; t += blockDim.x) tw[t] = tw_g[t];
   const int jn = p.d_jn[i], js = p.d_js[i];
   const size_t row = (size_t)p.nlat * p.nfreq_t;
   const bool nl = (atoms & SWX_TEND_N) != 0;
-  double2 *res[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double2 *R = nullptr;  // forward results [5][N]
   if (nl) {
-    // inverse: grids of u, v, vort, phi' (z = north + i south) into buf[0..3]
-    double2 *grid[4];
-    int freeb = 4;  // buf[4], buf[5] free
-    double2 *spare[2] = {buf[4], buf[5]};
-    for (int f = 0; f < 4; ++f) {
-      double2 *z = buf[f];
+    // inverse: grids of u, v, vort, phi' (z = north + i south), batched
+    for (int t = threadIdx.x; t < 4 * N; t += blockDim.x) {
+      const int f = t / N, k = t - f * N;
       const double2 *Xn = c2r + f * row + (size_t)jn * p.nfreq_t;
       const double2 *Xs = c2r + f * row + (size_t)js * p.nfreq_t;
-      for (int k = threadIdx.x; k < N; k += blockDim.x) {
-        double2 X = make_double2(0.0, 0.0), Y = X;
-        if (k <= T) {
-          X = Xn[k];
-          Y = Xs[k];
-        } else if (N - k <= T) {
-          const double2 a = Xn[N - k], b = Xs[N - k];
-          X = make_double2(a.x, -a.y);
-          Y = make_double2(b.x, -b.y);
-        }
-        z[k] = make_double2(X.x - Y.y, X.y + Y.x);  // X + i Y
+      double2 a = make_double2(0.0, 0.0), b = a;
+      if (k <= T) {
+        a = Xn[k];
+        b = Xs[k];
+      } else if (N - k <= T) {
+        const double2 an = Xn[N - k], bs = Xs[N - k];
+        a = make_double2(an.x, -an.y);
+        b = make_double2(bs.x, -bs.y);
       }
-      __syncthreads();
-      double2 *r = cta_fft(z, spare[0], N, p.fft_radix, p.fft_npass, tw, true);
-      if (r != z) {  // result landed in the spare: swap roles
-        spare[0] = z;
-      }
-      grid[f] = r;
-      (void)freeb;
-    }
-    // products on the grid, north in Re, south in Im:
-    // phi'u, phi'v, vort u, vort v, |V|^2/2  (swe.py:230-245)
-    double2 *out5[5] = {grid[0], grid[1], grid[2], grid[3], spare[0]};
-    double2 *spare_fwd = spare[1];
-    for (int n = threadIdx.x; n < N; n += blockDim.x) {
-      const double2 u = grid[0][n], v = grid[1][n], z = grid[2][n], ph = grid[3][n];
-      out5[0][n] = make_double2(ph.x * u.x, ph.y * u.y);
-      out5[1][n] = make_double2(ph.x * v.x, ph.y * v.y);
-      out5[2][n] = make_double2(z.x * u.x, z.y * u.y);
-      out5[3][n] = make_double2(z.x * v.x, z.y * v.y);
-      out5[4][n] = make_double2(0.5 * (u.x * u.x + v.x * v.x), 0.5 * (u.y * u.y + v.y * v.y));
+      X[t] = make_double2(a.x - b.y, a.y + b.x);  // X + i Y
     }
     __syncthreads();
-    for (int f = 0; f < 5; ++f) {
-      double2 *r = cta_fft(out5[f], spare_fwd, N, p.fft_radix, p.fft_npass, tw, false);
-      if (r != out5[f]) spare_fwd = out5[f];
-      res[f] = r;
+    double2 *G = cta_fft(X, Y, N, 4, p.fft_radix, p.fft_npass, tw, true);
+    double2 *Pp = G == X ? Y : X;
+    // products on the grid, north in Re, south in Im:
+    // phi'u, phi'v, vort u, vort v, |V|^2/2  (swe.py:230-245)
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const double2 u = G[n], v = G[N + n], z = G[2 * N + n], ph = G[3 * N + n];
+      Pp[n] = make_double2(ph.x * u.x, ph.y * u.y);
+      Pp[N + n] = make_double2(ph.x * v.x, ph.y * v.y);
+      Pp[2 * N + n] = make_double2(z.x * u.x, z.y * u.y);
+      Pp[3 * N + n] = make_double2(z.x * v.x, z.y * v.y);
+      Pp[4 * N + n] = make_double2(0.5 * (u.x * u.x + v.x * v.x), 0.5 * (u.y * u.y + v.y * v.y));
     }
+    __syncthreads();
+    R = cta_fft(Pp, G, N, 5, p.fft_radix, p.fft_npass, tw, false);
   }
   // fold + prepared rows for every m of this pair
   for (int m = threadIdx.x; m <= T; m += blockDim.x) {
@@ -570,7 +558,7 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     for (int f = 0; f < 5; ++f) {
       double2 X = make_double2(0.0, 0.0), Y = X;
       if (nl) {
-        const double2 a = res[f][m], b = res[f][m == 0 ? 0 : N - m];
+        const double2 a = R[(size_t)f * N + m], b = R[(size_t)f * N + (m == 0 ? 0 : N - m)];
         // X = (Z_m + conj Z_{N-m}) / 2, Y = (Z_m - conj Z_{N-m}) / (2i)
         X = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
         Y = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
@@ -1561,7 +1549,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     mark(1);
     mark(2);
     mark(3);
-    const size_t smem = (size_t)7 * p->nlon_t * sizeof(double2);
+    const size_t smem = (size_t)11 * p->nlon_t * sizeof(double2);
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(grid_tend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
