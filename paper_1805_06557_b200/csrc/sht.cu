@@ -443,7 +443,7 @@ __device__ __forceinline__ void fft_pass(const double2 *in0, double2 *out0, int 
   double2 wr[R];  // radix-R roots W_R^j
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const double2 w = tw[j * (N / R)];
+    const double2 w = __ldg(tw + j * (N / R));
     wr[j] = inv ? make_double2(w.x, -w.y) : w;
   }
   for (int jb = threadIdx.x; jb < nbat * nb; jb += blockDim.x) {
@@ -455,7 +455,7 @@ __device__ __forceinline__ void fft_pass(const double2 *in0, double2 *out0, int 
     v[0] = in[j];
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      const double2 w0 = tw[r * k * tstep];
+      const double2 w0 = __ldg(tw + r * k * tstep);
       v[r] = cmul(in[j + r * nb], inv ? make_double2(w0.x, -w0.y) : w0);
     }
     const int idxD = (j / Ns) * Ns * R + k;
@@ -510,16 +510,15 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     }
     return;
   }
-  double2 *tw = gsm;                 // [N]
-  double2 *X = gsm + N;              // [5][N]
-  double2 *Y = X + (size_t)5 * N;    // [5][N]
-  for (int t = threadIdx.x; t < N; t += blockDim.x) tw[t] = tw_g[t];
+  // 9 buffers of N (twiddles stay in global/L1): 2 CTAs per SM at N = 784
+  double2 *B = gsm;
+  const double2 *tw = tw_g;
   const int jn = p.d_jn[i], js = p.d_js[i];
   const size_t row = (size_t)p.nlat * p.nfreq_t;
   const bool nl = (atoms & SWX_TEND_N) != 0;
-  double2 *R = nullptr;  // forward results [5][N]
+  const double2 *R4 = nullptr, *R1 = nullptr;  // forward results: 4 arrays + KE
   if (nl) {
-    // inverse: grids of u, v, vort, phi' (z = north + i south), batched
+    // inverse: grids of u, v, vort, phi' (z = north + i south), batched 4
     for (int t = threadIdx.x; t < 4 * N; t += blockDim.x) {
       const int f = t / N, k = t - f * N;
       const double2 *Xn = c2r + f * row + (size_t)jn * p.nfreq_t;
@@ -533,11 +532,12 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
         a = make_double2(an.x, -an.y);
         b = make_double2(bs.x, -bs.y);
       }
-      X[t] = make_double2(a.x - b.y, a.y + b.x);  // X + i Y
+      B[t] = make_double2(a.x - b.y, a.y + b.x);  // X + i Y
     }
     __syncthreads();
-    double2 *G = cta_fft(X, Y, N, 4, p.fft_radix, p.fft_npass, tw, true);
-    double2 *Pp = G == X ? Y : X;
+    double2 *G = cta_fft(B, B + 4 * (size_t)N, N, 4, p.fft_radix, p.fft_npass, tw, true);
+    double2 *Pp = G == B ? B + 4 * (size_t)N : B;  // 4 free arrays
+    double2 *Pk = B + 8 * (size_t)N;                // KE
     // products on the grid, north in Re, south in Im:
     // phi'u, phi'v, vort u, vort v, |V|^2/2  (swe.py:230-245)
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
@@ -546,10 +546,13 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
       Pp[N + n] = make_double2(ph.x * v.x, ph.y * v.y);
       Pp[2 * N + n] = make_double2(z.x * u.x, z.y * u.y);
       Pp[3 * N + n] = make_double2(z.x * v.x, z.y * v.y);
-      Pp[4 * N + n] = make_double2(0.5 * (u.x * u.x + v.x * v.x), 0.5 * (u.y * u.y + v.y * v.y));
+      Pk[n] = make_double2(0.5 * (u.x * u.x + v.x * v.x), 0.5 * (u.y * u.y + v.y * v.y));
     }
     __syncthreads();
-    R = cta_fft(Pp, G, N, 5, p.fft_radix, p.fft_npass, tw, false);
+    double2 *r4 = cta_fft(Pp, G, N, 4, p.fft_radix, p.fft_npass, tw, false);
+    double2 *spare = r4 == Pp ? G : Pp;  // 4 free arrays: one is the KE scratch
+    R1 = cta_fft(Pk, spare, N, 1, p.fft_radix, p.fft_npass, tw, false);
+    R4 = r4;
   }
   // fold + prepared rows for every m of this pair
   for (int m = threadIdx.x; m <= T; m += blockDim.x) {
@@ -558,7 +561,8 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     for (int f = 0; f < 5; ++f) {
       double2 X = make_double2(0.0, 0.0), Y = X;
       if (nl) {
-        const double2 a = R[(size_t)f * N + m], b = R[(size_t)f * N + (m == 0 ? 0 : N - m)];
+        const double2 *Rf = f < 4 ? R4 + (size_t)f * N : R1;
+        const double2 a = Rf[m], b = Rf[m == 0 ? 0 : N - m];
         // X = (Z_m + conj Z_{N-m}) / 2, Y = (Z_m - conj Z_{N-m}) / (2i)
         X = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
         Y = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
@@ -1549,7 +1553,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     mark(1);
     mark(2);
     mark(3);
-    const size_t smem = (size_t)11 * p->nlon_t * sizeof(double2);
+    const size_t smem = (size_t)9 * p->nlon_t * sizeof(double2);
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(grid_tend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
