@@ -176,6 +176,24 @@ def fp64_peak_tflops(torch, lib, _lib):
     return best
 
 
+def _tendency_nlon(trunc: int, nlon: int) -> int:
+    """The tendency FFT length libswx uses: smallest 7-smooth n >= 3T+1
+    (the grid's nlon when already 7-smooth), see csrc/sht.cu."""
+    def smooth(n):
+        for f in (2, 3, 5, 7):
+            while n % f == 0:
+                n //= f
+        return n == 1
+    need = 3 * trunc + 1
+    if nlon >= need and smooth(nlon):
+        return nlon
+    n = max(need, 2)
+    n += n & 1
+    while not smooth(n):
+        n += 2
+    return n
+
+
 def load_traffic():
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
@@ -354,12 +372,23 @@ def main():
     # algorithmic flops per launch (SURVEY §8d conventions)
     nlat = par.cfg.nlat
     leg = 4.0 * nlat * nc  # per complex series, no symmetry credit
+    import math
+    nlon_t = nlat * 2  # placeholder if the plan is not available
+    try:
+        from paper_1805_06557_b200.sphere import plan_for as _pf
+        nlon_t = int(_tendency_nlon(par.cfg.trunc, par.cfg.nlon))
+    except Exception:
+        pass
+    # fused grid stage: 4 inverse + 5 forward complex FFTs of length nlon_t per
+    # latitude pair (5 N log2 N each) + 9 flops per grid point and hemisphere
+    grid_flops = (nlat // 2) * (9 * 5.0 * nlon_t * math.log2(nlon_t) + 2 * 9.0 * nlon_t)
     flops = {
         "rexi_lg_psi0_overlapped": 40.0 * w.n_poles * nc,
         "rexi_lg": 40.0 * w.n_poles * nc,
         "rexi_l": 142.0 * w.n_poles * nc,
         "synth_state": 7 * leg,
         "analysis": 7 * leg,
+        "grid_fused": grid_flops,
     }
     peak64 = fp64_peak_tflops(torch, lib, _lib)
     traffic = load_traffic()
