@@ -222,8 +222,12 @@ def rexi_sum(group: str, model: Model, dt: float, alphas, betas, stack: np.ndarr
     alphas = np.asarray(alphas, dtype=np.complex128)
     betas = np.asarray(betas, dtype=np.complex128)
     if group == "lg":
-        sols = lg_solutions(model, dt, alphas, stack)
-        total = tree_sum(betas[:, None, None, None] * sols)
+        # power-of-two chunks reduced by the same tree == the one-shot tree
+        ch = 256 if alphas.size > 256 and (alphas.size & (alphas.size - 1)) == 0 else alphas.size
+        parts = [tree_sum(betas[s:s + ch, None, None, None]
+                          * lg_solutions(model, dt, alphas[s:s + ch], stack))
+                 for s in range(0, alphas.size, ch)]
+        total = tree_sum(np.stack(parts))
     elif group == "l":
         if factors is None:
             factors = LFactors(model, dt)

@@ -52,3 +52,8 @@ def rel_l2(x, ref):
     x = np.asarray(x).reshape(-1)
     ref = np.asarray(ref).reshape(-1)
     return float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+
+
+@pytest.fixture(scope="session")
+def golden_split():
+    return np.load(os.path.join(GOLDEN, "split.npz"))

@@ -185,10 +185,30 @@ def etdrk_fixtures(out, trunc, steps, tag, dt=1800.0, n_poles=256):
     print(f"{tag}: {steps} ETD2RK steps in {time.time() - t0:.1f}s")
 
 
+def split_fixtures(path):
+    """Strang-split (ERK2 + REXI / CN) and CN steppers at T21 (rows f2/f3)."""
+    out = {}
+    cfg = SP.SphereConfig.for_truncation(21)
+    par = W.ModelParams(1e4 * cfg.gravity_g, cfg)
+    s0 = seeded_balanced_state(cfg)
+    out["T21split_ic"] = pack(s0.stack())
+    for sid in ("lg_rexi_lc_n_erk_ver1", "lg_irk_lc_n_erk_ver0", "ln_erk"):
+        st = ST.build_stepper(sid, par, R.RexiSetup(num_poles=64))
+        s = s0
+        for _ in range(2):
+            s = st.step(s, 600.0)
+        out[f"T21split_{sid}"] = pack(s.stack())
+    np.savez_compressed(path, **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the T256 one-day trajectory")
+    ap.add_argument("--split", action="store_true", help="only the Strang/CN stepper fixtures")
     args = ap.parse_args()
+    if args.split:
+        split_fixtures(os.path.join(HERE, "split.npz"))
+        return
     out: dict = {}
     coeff_fixtures(out)
     sht_fixtures(out)

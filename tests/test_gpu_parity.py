@@ -319,3 +319,38 @@ def test_prepared_sum_bitwise_equals_unprepared():
         out = torch.empty_like(rhs)
         got = sl.rexi_sum_prepared_dev(c0.alphas, bet, prep, rhs, out).cpu().numpy()
         assert np.array_equal(got, ref), group.token
+
+
+def test_stiffness_corner_chunked_poles_vs_oracle():
+    """cfg3 corner (Phibar = 18000 g, dt = 3600 s, contour p1 = 80, N = 2048)
+    at T85: the lg pole sum runs in 4 aligned chunks of 512 combined by the
+    tree; two ETD2RK steps vs the oracle (rel L2 <= 1e-10)."""
+    from paper_1805_06557_b200.workloads import seeded_balanced_state
+
+    trunc, phibar, dt = 85, 18000.0 * G, 3600.0
+    cfg = SphereConfig.for_truncation(trunc)
+    par = ModelParams(phibar, cfg)
+    grid = osh.Grid(trunc)
+    ic = ost.seeded_balanced_state(grid)
+    model = orx.Model(trunc, phibar)
+    sets = {k: ost.contour_coeffs(k, 10.0, 80.0, 2048) for k in (0, 1, 2)}
+    ref = ic
+    for _ in range(2):
+        ref = ost.etdrk2_step(model, grid, dt, sets, ref)
+    stepper = build_stepper("lg_rexi_lc_n_etdrk", par, RexiSetup(10.0, 80.0, 2048))
+    st = PrognosticState.from_stack(ic, cfg)
+    for _ in range(2):
+        st = stepper.step(st, dt)
+    assert rel_l2(pack(st.stack()), olay.pack(ref)) <= 1e-10
+
+
+@pytest.mark.parametrize("sid", ["lg_rexi_lc_n_erk_ver1", "lg_irk_lc_n_erk_ver0", "ln_erk"])
+def test_split_and_explicit_steppers_golden(golden_split, sid):
+    """Strang split ERK2 + REXI / Crank-Nicolson and fully explicit steppers
+     against the reference, 2 steps at T21."""
+    par = params(21)
+    st = PrognosticState.from_stack(unpack(golden_split["T21split_ic"], 21), par.cfg)
+    stepper = build_stepper(sid, par, RexiSetup(num_poles=64))
+    for _ in range(2):
+        st = stepper.step(st, 600.0)
+    assert rel_l2(pack(st.stack()), golden_split[f"T21split_{sid}"]) <= 1e-10
