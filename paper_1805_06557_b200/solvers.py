@@ -121,14 +121,17 @@ class ShiftedLinearSolver:
         self._native(alphas)
         return self
 
-    def workspace(self, nat: _Native, n_rhs: int, lo: int, hi: int):
+    def workspace(self, nat: _Native, n_rhs: int, lo: int, hi: int, stream=None):
+        """Scratch for one pole sum; one buffer per stream, so sums issued
+        concurrently on different streams never share partials."""
         import torch
 
         nbytes = int(self._lib.swx_rexi_workspace_bytes(nat.h, n_rhs, lo, hi))
-        buf = self._ws.get("buf")
+        key = stream_ptr(stream)
+        buf = self._ws.get(key)
         if nbytes and (buf is None or buf.numel() < nbytes):
             buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-            self._ws["buf"] = buf
+            self._ws[key] = buf
         return buf, nbytes
 
     # -- device entry points ------------------------------------------------
@@ -145,7 +148,7 @@ class ShiftedLinearSolver:
         lo, hi = pole_range if pole_range is not None else (0, nat.alphas.size)
         if out_dev is None:
             out_dev = torch.empty_like(rhs_dev)
-        ws, nbytes = self.workspace(nat, n_rhs, lo, hi)
+        ws, nbytes = self.workspace(nat, n_rhs, lo, hi, stream)
         _lib.check(self._lib.swx_rexi_sum(
             nat.h, n_rhs, ptr(rhs_dev), ptr(betas_dev), lo, hi, 1 if realify else 0,
             ptr(out_dev), ptr(ws) if nbytes else 0, nbytes, stream_ptr(stream)))
@@ -174,7 +177,7 @@ class ShiftedLinearSolver:
         nat = self._native(alphas)
         n_rhs = rhs_dev.shape[0]
         lo, hi = pole_range if pole_range is not None else (0, nat.alphas.size)
-        ws, nbytes = self.workspace(nat, n_rhs, lo, hi)
+        ws, nbytes = self.workspace(nat, n_rhs, lo, hi, stream)
         _lib.check(self._lib.swx_rexi_sum_prepared(
             nat.h, n_rhs, ptr(rhs_dev), ptr(betas_dev), ptr(prep), lo, hi, 1 if realify else 0,
             ptr(out_dev), ptr(ws) if nbytes else 0, nbytes, stream_ptr(stream)))
