@@ -338,13 +338,11 @@ __global__ void products_kernel(double *g, size_t npts) {
 constexpr int kAS = 12;  // row stride (doubles) of prepared rows: conflict-free B fragments
 constexpr int kAG = 8;   // row stride of the prepared rows of the table path (global)
 
+// one prepared row (4 complex = 64 B, 16-byte aligned): 4 vector stores
 __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
+  double2 *d2 = reinterpret_cast<double2 *>(dst);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const double2 z = c < nv ? v[c] : make_double2(0.0, 0.0);
-    dst[2 * c] = z.x;
-    dst[2 * c + 1] = z.y;
-  }
+  for (int c = 0; c < 4; ++c) d2[c] = c < nv ? v[c] : make_double2(0.0, 0.0);
 }
 
 // fold one latitude pair of the tendency inputs into even/odd parts of the
