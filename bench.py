@@ -451,7 +451,10 @@ def main():
         cpu = {"value": units_per_step / sec, "unit": "pole-solve*coeff/s",
                "cores": len(os.sched_getaffinity(0)), "kind": "port", "sample": sample}
 
-    per_step_launches = 16 if etd else (1 if w.group == "lg" else 2)
+    # kernels per step: counted from the captured step graph (ETD2RK); the linear
+    # configs launch one fused pole-sum kernel (lg) or kernel + tree combine (l)
+    per_step_launches = (eng.kernel_launches if etd else None) or \
+        (12 if etd else (1 if w.group == "lg" else 2))
     line = {
         "metric": "REXI pole-solves*SH-coeffs/s", "value": value, "unit": "pole-solve*coeff/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -351,6 +351,9 @@ __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
 // 7 analysis series (the prepared row of pair i, column m).  F[hemi][5] are
 // the products' Fourier coefficients times dlon (phi'u, phi'v, vort u,
 // vort v, KE), L1/L2[hemi] the Fourier-space Coriolis terms.
+// hcos: fold 1/cos of the pair into the H-table rows (table analysis forms H
+// without the 1/cos factor)
+template <bool HCOS>
 __device__ __forceinline__ void tend_fold(const ShtView &p, const double2 (&F)[2][5],
                                           const double2 (&L1)[2], const double2 (&L2)[2],
                                           int m, int i, double2 *ev, double2 *od) {
@@ -370,7 +373,7 @@ __device__ __forceinline__ void tend_fold(const ShtView &p, const double2 (&F)[2
     const double2 imPu = make_double2(-cm * Fh[0].y, cm * Fh[0].x);  // phi'u
     const double2 imZu = make_double2(-cm * Fh[2].y, cm * Fh[2].x);  // vort u
     const double2 imZv = make_double2(-cm * Fh[3].y, cm * Fh[3].x);  // vort v
-    const double wa = wj * ra;
+    const double wa = HCOS ? wj * ra * rcos : wj * ra;
     double2 *o = av[hemi];
     o[0] = make_double2(wj * l1.x - imZu.x, wj * l1.y - imZu.y);
     o[1] = make_double2(wj * l2.x + imZv.x, wj * l2.y + imZv.y);
@@ -392,6 +395,7 @@ __device__ __forceinline__ void tend_fold(const ShtView &p, const double2 (&F)[2
   }
 }
 
+template <bool HCOS>
 __device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, const double2 *lc,
                                          int atoms, int m, int i, double2 *ev, double2 *od) {
   if (i >= p.nh) {
@@ -418,7 +422,7 @@ __device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, con
       L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
     }
   }
-  tend_fold(p, F, L1, L2, m, i, ev, od);
+  tend_fold<HCOS>(p, F, L1, L2, m, i, ev, od);
 }
 
 // ---------------------------------------------------------------------
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
       }
     }
     double2 ev[7], od[7];
-    tend_fold(p, F, L1, L2, m, i, ev, od);
+    tend_fold<true>(p, F, L1, L2, m, i, ev, od);
     double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
     put_row(base + 0 * ps, ev, 4);
     put_row(base + 1 * ps, od, 4);
@@ -735,7 +739,7 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
         if (MODE == 0) {
           if (tid < KC) {
             double2 ev[7], od[7];
-            tend_row(p, Q, lcin, atoms, m, i0 + tid, ev, od);
+            tend_row<false>(p, Q, lcin, atoms, m, i0 + tid, ev, od);
             const size_t ps = (size_t)KC * kAS;
             put_row(As + 0 * ps + (size_t)tid * kAS, ev, 4);
             put_row(As + 1 * ps + (size_t)tid * kAS, od, 4);
@@ -919,7 +923,7 @@ __global__ void prep_tab_tend_kernel(ShtView p, const double2 *Q, const double2 
   const int m = blockIdx.y;
   if (i >= p.nt16) return;
   double2 ev[7], od[7];
-  tend_row(p, Q, lc, atoms, m, i, ev, od);
+  tend_row<true>(p, Q, lc, atoms, m, i, ev, od);
   const size_t ps = (size_t)p.nt16 * kAG;
   double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
   put_row(base + 0 * ps, ev, 4);
@@ -980,19 +984,20 @@ __global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const doub
   const int r = ((l0 - m) >> 1) + lr;
   const int l = m + 2 * r + par;
   const bool valid = l <= T;
+  // branch-free streaming: rows past T (and the missing P_{l-1} of l = m) read
+  // a valid row and are masked by their coefficients; an invalid A row only
+  // affects its own (unwritten) output row
   const double *arow = Pp + (size_t)(valid ? r : 0) * nt + lc4;
   double cz = 0.0, cw = 0.0;
   const double *hm = Po + lc4, *hp = Po + lc4;
-  bool hasm = false;
   if (MODE == 0 && valid) {
     const double4 c = p.d_rc[rc_offset(T, m) + (l - m)];
-    cz = c.z;
     cw = c.w;
     // P_{l-1}, P_{l+1} live in the other plane: rows (r, r+1) for par = 1,
     // (r-1, r) for par = 0
     const int rm = par ? r : r - 1, rp = par ? r + 1 : r;
-    hasm = rm >= 0;
-    hm = Po + (size_t)(hasm ? rm : 0) * nt + lc4;
+    cz = rm >= 0 ? c.z : 0.0;
+    hm = Po + (size_t)(rm >= 0 ? rm : 0) * nt + lc4;
     hp = Po + (size_t)rp * nt + lc4;
   }
   const size_t ps = (size_t)nt * kAG;
@@ -1000,23 +1005,49 @@ __global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const doub
   const double *Ab = A + (size_t)m * NPART * 2 * ps;
   const double *Bp = Ab + (size_t)(0 * 2 + par) * ps + (size_t)lc4 * kAG + lr;
   const double *Bh = Ab + (size_t)(1 * 2 + (par ^ 1)) * ps + (size_t)lc4 * kAG + lr;
-  const double *rcs = p.d_rcos16 + lc4;
   double cp0 = 0.0, cp1 = 0.0, ch0 = 0.0, ch1 = 0.0;
   double dp0 = 0.0, dp1 = 0.0, dh0 = 0.0, dh1 = 0.0;
-#pragma unroll 2
-  for (int k = 0; k < nt; k += 8) {
-    const double a0 = valid ? arow[k] : 0.0;
-    const double a1 = valid ? arow[k + 4] : 0.0;
-    dmma(cp0, cp1, a0, Bp[(size_t)k * kAG]);
-    dmma(dp0, dp1, a1, Bp[(size_t)(k + 4) * kAG]);
-    if (MODE == 0) {
-      double h0 = 0.0, h1 = 0.0;
-      if (valid) {
-        h0 = (cz * (hasm ? hm[k] : 0.0) - cw * hp[k]) * rcs[k];
-        h1 = (cz * (hasm ? hm[k + 4] : 0.0) - cw * hp[k + 4]) * rcs[k + 4];
+  // batches of 16 pairs (nt is a multiple of 16), loads of batch b+1 issued
+  // before the DMMAs of batch b.  Even k-steps accumulate in (c*), odd in (d*).
+  constexpr int U = 4;
+  double a[U], hmv[U], hpv[U], bp[U], bh[U];
+  double na[U], nhm[U], nhp[U], nbp[U], nbh[U];
+  auto load = [&](int k, double *xa, double *xm, double *xp, double *xb, double *xh) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xa[u] = arow[k + 4 * u];
+      xb[u] = Bp[(size_t)(k + 4 * u) * kAG];
+      if (MODE == 0) {
+        xm[u] = hm[k + 4 * u];
+        xp[u] = hp[k + 4 * u];
+        xh[u] = Bh[(size_t)(k + 4 * u) * kAG];
       }
-      dmma(ch0, ch1, h0, Bh[(size_t)k * kAG]);
-      dmma(dh0, dh1, h1, Bh[(size_t)(k + 4) * kAG]);
+    }
+  };
+  load(0, a, hmv, hpv, bp, bh);
+  for (int k = 0; k < nt; k += 4 * U) {
+    if (k + 4 * U < nt) load(k + 4 * U, na, nhm, nhp, nbp, nbh);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u & 1)
+        dmma(dp0, dp1, a[u], bp[u]);
+      else
+        dmma(cp0, cp1, a[u], bp[u]);
+      if (MODE == 0) {
+        const double h = fma(cz, hmv[u], -cw * hpv[u]);
+        if (u & 1)
+          dmma(dh0, dh1, h, bh[u]);
+        else
+          dmma(ch0, ch1, h, bh[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = na[u];
+      hmv[u] = nhm[u];
+      hpv[u] = nhp[u];
+      bp[u] = nbp[u];
+      bh[u] = nbh[u];
     }
   }
   cp0 += dp0;
