@@ -964,114 +964,197 @@ __global__ void prep_tab_plain_kernel(ShtView p, const double2 *Q, int nf, doubl
   put_row(base + ps, od, 4);
 }
 
-// Table analysis: one warp = (m, 16 degrees l0..l0+15, parity).  The warp's
-// two 8x8 outputs (P table and H table columns) accumulate over all latitude
-// pairs with m8n8k4 DMMA; A fragments are loaded straight from the table
-// (8 rows x 32 B per load), H rows are formed from the other parity plane.
+// Table analysis: one warp item = (m, 16 degrees l0..l0+15, one parity): two
+// 8x8 outputs (P-table and H-table columns) accumulated over all latitude
+// pairs with m8n8k4 DMMA.  Warps are persistent and stream their sequence of
+// (item, 16-pair stage) through a private kTS-deep cp.async ring in shared
+// memory: the table rows of the item (8 own-parity rows, 9 rows of the other
+// parity plane for H = dP/dlat, sphere.py:102-111) and the prepared rows of
+// the pair block (P part and H part).  No register staging, no CTA barriers.
+constexpr int kTK = 16;                 // latitude pairs per stage
+constexpr int kTS = 4;                  // ring depth (stages in flight)
+constexpr int kTWarps = 4;              // warps per CTA
+constexpr int kPR = 20;                 // smem row pitch of table rows (doubles)
+constexpr int kBR = 12;                 // smem row pitch of prepared rows (doubles)
+constexpr int kSA = 0, kSH = 8 * kPR, kSBp = kSH + 9 * kPR, kSBh = kSBp + kTK * kBR;
+constexpr int kStage = kSBh + kTK * kBR;  // doubles per stage
+constexpr size_t kTabSmem = (size_t)kTWarps * kTS * kStage * sizeof(double);
+
+__device__ __forceinline__ void cp16(double *dst, const double *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// issue-side view of one item: per-lane source pointers at stage 0
+struct TabSrc {
+  const double *a0, *a1, *h0, *h1, *h2, *bp, *bh;
+};
+
 template <int MODE>
-__global__ void __launch_bounds__(128) analysis_tab_kernel(ShtView p, const double *A,
-                                                           double2 *out, int nf) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= p.n_titems) return;
-  const int lane = threadIdx.x & 31, lr = lane >> 2, lc4 = lane & 3;
-  const int4 itm = p.d_titems[gw];
+__device__ __forceinline__ TabSrc tab_src(const ShtView &p, const double *A, int4 itm, int lane) {
   const int m = itm.x, l0 = itm.y, par = itm.z;
   const int T = p.trunc, nt = p.nt16;
   const int half = (T + 3 - m) >> 1;
   const double *P0 = p.d_ptab + p.d_ptoff[m];
-  const double *Pp = P0 + (size_t)(par ? half : 0) * nt;  // own parity plane
-  const double *Po = P0 + (size_t)(par ? 0 : half) * nt;  // other parity plane
-  const int r = ((l0 - m) >> 1) + lr;
-  const int l = m + 2 * r + par;
-  const bool valid = l <= T;
-  // branch-free streaming: rows past T (and the missing P_{l-1} of l = m) read
-  // a valid row and are masked by their coefficients; an invalid A row only
-  // affects its own (unwritten) output row
-  const double *arow = Pp + (size_t)(valid ? r : 0) * nt + lc4;
-  double cz = 0.0, cw = 0.0;
-  const double *hm = Po + lc4, *hp = Po + lc4;
-  if (MODE == 0 && valid) {
-    const double4 c = p.d_rc[rc_offset(T, m) + (l - m)];
-    cw = c.w;
-    // P_{l-1}, P_{l+1} live in the other plane: rows (r, r+1) for par = 1,
-    // (r-1, r) for par = 0
-    const int rm = par ? r : r - 1, rp = par ? r + 1 : r;
-    cz = rm >= 0 ? c.z : 0.0;
-    hm = Po + (size_t)(rm >= 0 ? rm : 0) * nt + lc4;
-    hp = Po + (size_t)rp * nt + lc4;
-  }
+  const double *Pp = P0 + (size_t)(par ? half : 0) * nt;
+  const double *Po = P0 + (size_t)(par ? 0 : half) * nt;
+  const int r = (l0 - m) >> 1;
+  const int ch = lane & 7, rw = lane >> 3;  // 16-byte chunk of a row, row group
+  // own rows r + j (rows past T read row 0: their output rows are discarded)
+  auto own = [&](int j) {
+    const int l = m + 2 * (r + j) + par;
+    return Pp + (size_t)(l <= T ? r + j : 0) * nt + 2 * ch;
+  };
+  // other-plane rows rb + j, rb = r - 1 (par 0) or r (par 1); out of range -> row 0
+  const int rb = par ? r : r - 1;
+  auto oth = [&](int j) {
+    const int q = rb + j;
+    return Po + (size_t)(q >= 0 && q < half ? q : 0) * nt + 2 * ch;
+  };
+  TabSrc t;
+  t.a0 = own(rw);
+  t.a1 = own(rw + 4);
+  t.h0 = oth(rw);
+  t.h1 = oth(rw + 4);
+  t.h2 = oth(8);
   const size_t ps = (size_t)nt * kAG;
   constexpr int NPART = MODE == 0 ? 2 : 1;
   const double *Ab = A + (size_t)m * NPART * 2 * ps;
-  const double *Bp = Ab + (size_t)(0 * 2 + par) * ps + (size_t)lc4 * kAG + lr;
-  const double *Bh = Ab + (size_t)(1 * 2 + (par ^ 1)) * ps + (size_t)lc4 * kAG + lr;
-  double cp0 = 0.0, cp1 = 0.0, ch0 = 0.0, ch1 = 0.0;
-  double dp0 = 0.0, dp1 = 0.0, dh0 = 0.0, dh1 = 0.0;
-  // batches of 16 pairs (nt is a multiple of 16), loads of batch b+1 issued
-  // before the DMMAs of batch b.  Even k-steps accumulate in (c*), odd in (d*).
-  constexpr int U = 4;
-  double a[U], hmv[U], hpv[U], bp[U], bh[U];
-  double na[U], nhm[U], nhp[U], nbp[U], nbh[U];
-  auto load = [&](int k, double *xa, double *xm, double *xp, double *xb, double *xh) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      xa[u] = arow[k + 4 * u];
-      xb[u] = Bp[(size_t)(k + 4 * u) * kAG];
-      if (MODE == 0) {
-        xm[u] = hm[k + 4 * u];
-        xp[u] = hp[k + 4 * u];
-        xh[u] = Bh[(size_t)(k + 4 * u) * kAG];
-      }
-    }
-  };
-  load(0, a, hmv, hpv, bp, bh);
-  for (int k = 0; k < nt; k += 4 * U) {
-    if (k + 4 * U < nt) load(k + 4 * U, na, nhm, nhp, nbp, nbh);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (u & 1)
-        dmma(dp0, dp1, a[u], bp[u]);
-      else
-        dmma(cp0, cp1, a[u], bp[u]);
-      if (MODE == 0) {
-        const double h = fma(cz, hmv[u], -cw * hpv[u]);
-        if (u & 1)
-          dmma(dh0, dh1, h, bh[u]);
-        else
-          dmma(ch0, ch1, h, bh[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      a[u] = na[u];
-      hmv[u] = nhm[u];
-      hpv[u] = nhp[u];
-      bp[u] = nbp[u];
-      bh[u] = nbh[u];
-    }
-  }
-  cp0 += dp0;
-  cp1 += dp1;
-  ch0 += dh0;
-  ch1 += dh1;
-  const int slot = col_offset(T, m) + (l - m);
+  // prepared rows: 16 pairs x 64 B, lane -> (pair lane>>2 (+8), chunk lane&3)
+  t.bp = Ab + (size_t)(0 * 2 + par) * ps + (size_t)(lane >> 2) * kAG + 2 * (lane & 3);
+  t.bh = Ab + (size_t)(1 * 2 + (par ^ 1)) * ps + (size_t)(lane >> 2) * kAG + 2 * (lane & 3);
+  return t;
+}
+
+template <int MODE>
+__device__ __forceinline__ void tab_issue(const TabSrc &t, int st, double *sb, int lane) {
+  const int k0 = st * kTK;
+  const int ch = lane & 7, rw = lane >> 3;
+  cp16(sb + kSA + rw * kPR + 2 * ch, t.a0 + k0);
+  cp16(sb + kSA + (rw + 4) * kPR + 2 * ch, t.a1 + k0);
+  const int pr = lane >> 2, bc = 2 * (lane & 3);
+  cp16(sb + kSBp + pr * kBR + bc, t.bp + (size_t)k0 * kAG);
+  cp16(sb + kSBp + (pr + 8) * kBR + bc, t.bp + (size_t)(k0 + 8) * kAG);
   if (MODE == 0) {
-    // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ S4 from lane+2) (div); 2: S3,S7 (phi')
-    const double s4x = __shfl_down_sync(0xffffffffu, cp0, 2);
-    const double s4y = __shfl_down_sync(0xffffffffu, cp1, 2);
-    if (!valid || lc4 == 3) return;
-    double vx = cp0 + ch0, vy = cp1 + ch1;
-    if (lc4 == 1) {
-      const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
-      vx += llk * s4x;
-      vy += llk * s4y;
-    }
-    const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
-    out[(size_t)f * p.ncoef + slot] = make_double2(vx, vy);
-  } else {
-    if (!valid || lc4 >= nf) return;
-    out[(size_t)lc4 * p.ncoef + slot] = make_double2(cp0, cp1);
+    cp16(sb + kSH + rw * kPR + 2 * ch, t.h0 + k0);
+    cp16(sb + kSH + (rw + 4) * kPR + 2 * ch, t.h1 + k0);
+    if (lane < 8) cp16(sb + kSH + 8 * kPR + 2 * ch, t.h2 + k0);
+    cp16(sb + kSBh + pr * kBR + bc, t.bh + (size_t)k0 * kAG);
+    cp16(sb + kSBh + (pr + 8) * kBR + bc, t.bh + (size_t)(k0 + 8) * kAG);
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTWarps * 32) analysis_tab_kernel(ShtView p, const double *A,
+                                                                    double2 *out, int nf) {
+  extern __shared__ __align__(16) double tsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lr = lane >> 2, lc4 = lane & 3;
+  double *ring = tsm + (size_t)wid * kTS * kStage;
+  const int nwarps = gridDim.x * kTWarps;
+  const int T = p.trunc;
+  const int nst = p.nt16 / kTK;  // stages per item
+  int it_i = blockIdx.x * kTWarps + wid;  // item being issued
+  int st_i = 0;
+  TabSrc src;
+  if (it_i < p.n_titems) src = tab_src<MODE>(p, A, p.d_titems[it_i], lane);
+  // prologue: kTS - 1 stages in flight
+#pragma unroll
+  for (int q = 0; q < kTS - 1; ++q) {
+    if (it_i < p.n_titems) {
+      tab_issue<MODE>(src, st_i, ring + (size_t)q * kStage, lane);
+      if (++st_i == nst) {
+        st_i = 0;
+        it_i += nwarps;
+        if (it_i < p.n_titems) src = tab_src<MODE>(p, A, p.d_titems[it_i], lane);
+      }
+    }
+    cp_commit();
+  }
+  int slot = 0;
+  for (int it = blockIdx.x * kTWarps + wid; it < p.n_titems; it += nwarps) {
+    const int4 itm = p.d_titems[it];
+    const int m = itm.x, l0 = itm.y, par = itm.z;
+    const int r = ((l0 - m) >> 1) + lr;
+    const int l = m + 2 * r + par;
+    const bool valid = l <= T;
+    double cz = 0.0, cw = 0.0;
+    if (MODE == 0 && valid) {
+      const double4 c = p.d_rc[rc_offset(T, m) + (l - m)];
+      cw = c.w;
+      cz = (par || r > 0) ? c.z : 0.0;  // l = m has no P_{l-1}
+    }
+    double cp0 = 0.0, cp1 = 0.0, ch0 = 0.0, ch1 = 0.0;
+    double dp0 = 0.0, dp1 = 0.0, dh0 = 0.0, dh1 = 0.0;
+    for (int st = 0; st < nst; ++st) {
+      // keep kTS - 1 stages in flight: issue the stage kTS - 1 ahead
+      {
+        double *dst = ring + (size_t)((slot + kTS - 1) % kTS) * kStage;
+        if (it_i < p.n_titems) {
+          tab_issue<MODE>(src, st_i, dst, lane);
+          if (++st_i == nst) {
+            st_i = 0;
+            it_i += nwarps;
+            if (it_i < p.n_titems) src = tab_src<MODE>(p, A, p.d_titems[it_i], lane);
+          }
+        }
+        cp_commit();
+      }
+      cp_wait<kTS - 1>();
+      __syncwarp();
+      const double *sb = ring + (size_t)slot * kStage;
+#pragma unroll
+      for (int u = 0; u < kTK / 4; ++u) {
+        const int kk = 4 * u;
+        const double a = sb[kSA + lr * kPR + kk + lc4];
+        const double b = sb[kSBp + (kk + lc4) * kBR + lr];
+        if (u & 1)
+          dmma(dp0, dp1, a, b);
+        else
+          dmma(cp0, cp1, a, b);
+        if (MODE == 0) {
+          const double hm = sb[kSH + lr * kPR + kk + lc4];
+          const double hp = sb[kSH + (lr + 1) * kPR + kk + lc4];
+          const double h = fma(cz, hm, -cw * hp);
+          const double bh = sb[kSBh + (kk + lc4) * kBR + lr];
+          if (u & 1)
+            dmma(dh0, dh1, h, bh);
+          else
+            dmma(ch0, ch1, h, bh);
+        }
+      }
+      __syncwarp();  // slot free for the next issue
+      slot = (slot + 1) % kTS;
+    }
+    cp0 += dp0;
+    cp1 += dp1;
+    ch0 += dh0;
+    ch1 += dh1;
+    const int slotc = col_offset(T, m) + (l - m);
+    if (MODE == 0) {
+      // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ S4 from lane+2) (div); 2: S3,S7 (phi')
+      const double s4x = __shfl_down_sync(0xffffffffu, cp0, 2);
+      const double s4y = __shfl_down_sync(0xffffffffu, cp1, 2);
+      if (valid && lc4 != 3) {
+        double vx = cp0 + ch0, vy = cp1 + ch1;
+        if (lc4 == 1) {
+          const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
+          vx += llk * s4x;
+          vy += llk * s4y;
+        }
+        const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
+        out[(size_t)f * p.ncoef + slotc] = make_double2(vx, vy);
+      }
+    } else {
+      if (valid && lc4 < nf) out[(size_t)lc4 * p.ncoef + slotc] = make_double2(cp0, cp1);
+    }
+  }
+  cp_wait<0>();
 }
 
 // FFT size of the tendency path: smallest 7-smooth n >= 3T+1 (the user
@@ -1397,8 +1480,23 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
 
 template <int MODE>
 static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s) {
-  const int blocks = (p->n_titems * 32 + 127) / 128;
-  analysis_tab_kernel<MODE><<<blocks, 128, 0, s>>>(static_cast<const ShtView &>(*p), A, out, nf);
+  // resident CTAs per SM and SM count, queried once per mode
+  static int nsm[2] = {0, 0}, per_sm[2] = {0, 0};
+  if (!nsm[MODE]) {
+    SWX_CUDA_TRY(cudaFuncSetAttribute(analysis_tab_kernel<MODE>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabSmem));
+    int dev = 0, n = 0, k = 0;
+    SWX_CUDA_TRY(cudaGetDevice(&dev));
+    SWX_CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, analysis_tab_kernel<MODE>,
+                                                               kTWarps * 32, kTabSmem));
+    per_sm[MODE] = std::max(k, 1);
+    nsm[MODE] = n;
+  }
+  const int need = (p->n_titems + kTWarps - 1) / kTWarps;
+  const int blocks = std::max(1, std::min(need, nsm[MODE] * per_sm[MODE]));
+  analysis_tab_kernel<MODE><<<blocks, kTWarps * 32, kTabSmem, s>>>(static_cast<const ShtView &>(*p),
+                                                                   A, out, nf);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
