@@ -32,6 +32,7 @@
 //    the smallest 7-smooth such nlon_t (784 at T256 instead of the
 //    reference's 772 = 4*193, which cuFFT can only do by Bluestein).
 #include <cufft.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -81,6 +82,7 @@ struct ShtView {
 
 struct swx_sht_s : ShtView {
   std::map<long long, cufftHandle> plans;
+  CUtensorMap ptab_map;  // 2D view [rows][nt16] of the P table, box kTBox x 17
 };
 
 namespace swx {
@@ -345,8 +347,16 @@ __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
   for (int c = 0; c < 4; ++c) d2[c] = c < nv ? v[c] : make_double2(0.0, 0.0);
 }
 
-// fold one latitude pair of the tendency inputs into even/odd parts of the
-// 7 analysis series (the prepared row of pair i, column m)
+// the same row in the table-analysis layout: rows of pairs with bit 1 set are
+// stored rotated by two complex slots (column c -> c ^ 4 in doubles), which
+// makes the analysis' B-fragment reads from shared memory conflict-free
+__device__ __forceinline__ void put_row_t(double *dst, const double2 *v, int nv, int i) {
+  double2 *d2 = reinterpret_cast<double2 *>(dst);
+  const int rot = (i & 2) ? 2 : 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) d2[(c + rot) & 3] = c < nv ? v[c] : make_double2(0.0, 0.0);
+}
+
 // fold one latitude pair of the tendency inputs into even/odd parts of the
 // 7 analysis series (the prepared row of pair i, column m).  F[hemi][5] are
 // the products' Fourier coefficients times dlon (phi'u, phi'v, vort u,
@@ -584,10 +594,10 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     double2 ev[7], od[7];
     tend_fold<true>(p, F, L1, L2, m, i, ev, od);
     double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
-    put_row(base + 0 * ps, ev, 4);
-    put_row(base + 1 * ps, od, 4);
-    put_row(base + 2 * ps, ev + 4, 3);
-    put_row(base + 3 * ps, od + 4, 3);
+    put_row_t(base + 0 * ps, ev, 4, i);
+    put_row_t(base + 1 * ps, od, 4, i);
+    put_row_t(base + 2 * ps, ev + 4, 3, i);
+    put_row_t(base + 3 * ps, od + 4, 3, i);
   }
 }
 
@@ -926,10 +936,10 @@ __global__ void prep_tab_tend_kernel(ShtView p, const double2 *Q, const double2 
   tend_row<true>(p, Q, lc, atoms, m, i, ev, od);
   const size_t ps = (size_t)p.nt16 * kAG;
   double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
-  put_row(base + 0 * ps, ev, 4);
-  put_row(base + 1 * ps, od, 4);
-  put_row(base + 2 * ps, ev + 4, 3);
-  put_row(base + 3 * ps, od + 4, 3);
+  put_row_t(base + 0 * ps, ev, 4, i);
+  put_row_t(base + 1 * ps, od, 4, i);
+  put_row_t(base + 2 * ps, ev + 4, 3, i);
+  put_row_t(base + 3 * ps, od + 4, 3, i);
 }
 
 __global__ void prep_tab_plain_kernel(ShtView p, const double2 *Q, int nf, double *A) {
@@ -960,127 +970,145 @@ __global__ void prep_tab_plain_kernel(ShtView p, const double2 *Q, int nf, doubl
   }
   const size_t ps = (size_t)p.nt16 * kAG;
   double *base = A + (size_t)m * 2 * ps + (size_t)i * kAG;
-  put_row(base, ev, 4);
-  put_row(base + ps, od, 4);
+  put_row_t(base, ev, 4, i);
+  put_row_t(base + ps, od, 4, i);
 }
 
-// Table analysis: one warp item = (m, 16 degrees l0..l0+15, one parity): two
-// 8x8 outputs (P-table and H-table columns) accumulated over all latitude
-// pairs with m8n8k4 DMMA.  Warps are persistent and stream their sequence of
-// (item, 16-pair stage) through a private kTS-deep cp.async ring in shared
-// memory: the table rows of the item (8 own-parity rows, 9 rows of the other
-// parity plane for H = dP/dlat, sphere.py:102-111) and the prepared rows of
-// the pair block (P part and H part).  No register staging, no CTA barriers.
+// Table analysis.  CTA item = (m, 32 degrees l0..l0+31): four consumer warps
+// (parity x 16-degree half), each accumulating two 8x8 outputs (P-table and
+// H-table columns) over all latitude pairs with m8n8k4 DMMA, and one producer
+// warp that streams the item's table rows and prepared rows, 16 latitude pairs
+// per stage, into a kTS-deep shared-memory ring with bulk async copies
+// completing on mbarriers.  The four warps share every staged byte: 17 rows
+// of each parity plane cover the own rows of both parities and the P_{l-1},
+// P_{l+1} neighbours that form H = dP/dlat (sphere.py:102-111).  CTAs are
+// persistent and the ring runs across item boundaries.
+constexpr int kTL = 32;                 // degrees per item
 constexpr int kTK = 16;                 // latitude pairs per stage
-constexpr int kTS = 4;                  // ring depth (stages in flight)
-constexpr int kTWarps = 4;              // warps per CTA
-constexpr int kPR = 20;                 // smem row pitch of table rows (doubles)
-constexpr int kBR = 12;                 // smem row pitch of prepared rows (doubles)
-constexpr int kSA = 0, kSH = 8 * kPR, kSBp = kSH + 9 * kPR, kSBh = kSBp + kTK * kBR;
-constexpr int kStage = kSBh + kTK * kBR;  // doubles per stage
-constexpr size_t kTabSmem = (size_t)kTWarps * kTS * kStage * sizeof(double);
+constexpr int kTS = 4;                  // ring depth
+constexpr int kPR = 20;                 // smem pitch of a staged table row (doubles) = TMA box width
+constexpr int kTBoxRows = 17;           // rows per parity plane per stage
+constexpr int kP1 = 352;                // plane-1 box offset (doubles, 128 B aligned)
+constexpr int kSB = 704;                // prepared-row blocks offset (doubles, 128 B aligned)
+constexpr int kStage = kSB + 4 * kTK * kAG;  // doubles per stage (multiple of 16)
+constexpr int kTabThreads = 5 * 32;
+constexpr size_t kTabSmem = (size_t)kTS * kStage * sizeof(double) + 2 * kTS * sizeof(uint64_t);
+static_assert(kP1 >= kTBoxRows * kPR && kSB >= kP1 + kTBoxRows * kPR, "stage layout");
+static_assert((kStage * 8) % 128 == 0 && (kP1 * 8) % 128 == 0 && (kSB * 8) % 128 == 0, "TMA alignment");
 
-__device__ __forceinline__ void cp16(double *dst, const double *src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+__device__ __forceinline__ unsigned smem_u32(const void *ptr) {
+  return (unsigned)__cvta_generic_to_shared(ptr);
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SWX_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra SWX_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double *dst, const double *src, unsigned bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// issue-side view of one item: per-lane source pointers at stage 0
-struct TabSrc {
-  const double *a0, *a1, *h0, *h1, *h2, *bp, *bh;
-};
-
-template <int MODE>
-__device__ __forceinline__ TabSrc tab_src(const ShtView &p, const double *A, int4 itm, int lane) {
-  const int m = itm.x, l0 = itm.y, par = itm.z;
-  const int T = p.trunc, nt = p.nt16;
-  const int half = (T + 3 - m) >> 1;
-  const double *P0 = p.d_ptab + p.d_ptoff[m];
-  const double *Pp = P0 + (size_t)(par ? half : 0) * nt;
-  const double *Po = P0 + (size_t)(par ? 0 : half) * nt;
-  const int r = (l0 - m) >> 1;
-  const int ch = lane & 7, rw = lane >> 3;  // 16-byte chunk of a row, row group
-  // own rows r + j (rows past T read row 0: their output rows are discarded)
-  auto own = [&](int j) {
-    const int l = m + 2 * (r + j) + par;
-    return Pp + (size_t)(l <= T ? r + j : 0) * nt + 2 * ch;
-  };
-  // other-plane rows rb + j, rb = r - 1 (par 0) or r (par 1); out of range -> row 0
-  const int rb = par ? r : r - 1;
-  auto oth = [&](int j) {
-    const int q = rb + j;
-    return Po + (size_t)(q >= 0 && q < half ? q : 0) * nt + 2 * ch;
-  };
-  TabSrc t;
-  t.a0 = own(rw);
-  t.a1 = own(rw + 4);
-  t.h0 = oth(rw);
-  t.h1 = oth(rw + 4);
-  t.h2 = oth(8);
-  const size_t ps = (size_t)nt * kAG;
-  constexpr int NPART = MODE == 0 ? 2 : 1;
-  const double *Ab = A + (size_t)m * NPART * 2 * ps;
-  // prepared rows: 16 pairs x 64 B, lane -> (pair lane>>2 (+8), chunk lane&3)
-  t.bp = Ab + (size_t)(0 * 2 + par) * ps + (size_t)(lane >> 2) * kAG + 2 * (lane & 3);
-  t.bh = Ab + (size_t)(1 * 2 + (par ^ 1)) * ps + (size_t)(lane >> 2) * kAG + 2 * (lane & 3);
-  return t;
+__device__ __forceinline__ void tma_2d(double *dst, const CUtensorMap *map, int c0, int c1,
+                                       uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
 template <int MODE>
-__device__ __forceinline__ void tab_issue(const TabSrc &t, int st, double *sb, int lane) {
-  const int k0 = st * kTK;
-  const int ch = lane & 7, rw = lane >> 3;
-  cp16(sb + kSA + rw * kPR + 2 * ch, t.a0 + k0);
-  cp16(sb + kSA + (rw + 4) * kPR + 2 * ch, t.a1 + k0);
-  const int pr = lane >> 2, bc = 2 * (lane & 3);
-  cp16(sb + kSBp + pr * kBR + bc, t.bp + (size_t)k0 * kAG);
-  cp16(sb + kSBp + (pr + 8) * kBR + bc, t.bp + (size_t)(k0 + 8) * kAG);
-  if (MODE == 0) {
-    cp16(sb + kSH + rw * kPR + 2 * ch, t.h0 + k0);
-    cp16(sb + kSH + (rw + 4) * kPR + 2 * ch, t.h1 + k0);
-    if (lane < 8) cp16(sb + kSH + 8 * kPR + 2 * ch, t.h2 + k0);
-    cp16(sb + kSBh + pr * kBR + bc, t.bh + (size_t)k0 * kAG);
-    cp16(sb + kSBh + (pr + 8) * kBR + bc, t.bh + (size_t)(k0 + 8) * kAG);
-  }
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kTWarps * 32) analysis_tab_kernel(ShtView p, const double *A,
-                                                                    double2 *out, int nf) {
-  extern __shared__ __align__(16) double tsm[];
+__global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
+                                                                   const __grid_constant__ CUtensorMap tmap,
+                                                                   const double *A, double2 *out,
+                                                                   int nf) {
+  extern __shared__ __align__(128) double tsm[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(tsm + (size_t)kTS * kStage);
+  uint64_t *empty = full + kTS;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int lr = lane >> 2, lc4 = lane & 3;
-  double *ring = tsm + (size_t)wid * kTS * kStage;
-  const int nwarps = gridDim.x * kTWarps;
-  const int T = p.trunc;
-  const int nst = p.nt16 / kTK;  // stages per item
-  int it_i = blockIdx.x * kTWarps + wid;  // item being issued
-  int st_i = 0;
-  TabSrc src;
-  if (it_i < p.n_titems) src = tab_src<MODE>(p, A, p.d_titems[it_i], lane);
-  // prologue: kTS - 1 stages in flight
+  const int T = p.trunc, nt = p.nt16;
+  const int nst = nt / kTK;  // stages per item
+  constexpr int NPART = MODE == 0 ? 2 : 1;
+  const size_t ps = (size_t)nt * kAG;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kTS; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (wid == 4) {
+    // ---------------- producer warp (one lane) ----------------
+    // per stage: one 2D box (kPR pairs x 17 rows) from each parity plane --
+    // plane 0 rows r0..r0+16, plane 1 rows r0-1..r0+15 (rows outside the
+    // column read neighbouring finite rows or zeros; they only feed masked or
+    // discarded outputs) -- and the 4 (2) prepared-row blocks of the stage
+    if (lane != 0) return;
+    const unsigned bytes =
+        (unsigned)((2 * kTBoxRows * kPR + NPART * 2 * kTK * kAG) * sizeof(double));
+    int q = 0;  // sequence number of the stage being filled
+    for (int it = blockIdx.x; it < p.n_titems; it += gridDim.x) {
+      const int4 itm = p.d_titems[it];
+      const int m = itm.x, l0 = itm.y;
+      const int half = (T + 3 - m) >> 1;
+      const int r0 = (l0 - m) >> 1;
+      const int row0 = itm.z + r0, row1 = itm.z + half + r0 - 1;
+      const double *Ab = A + (size_t)m * NPART * 2 * ps;
+      for (int st = 0; st < nst; ++st, ++q) {
+        const int slot = q % kTS;
+        const int pass = q / kTS;
+        if (pass > 0) mbar_wait(empty + slot, (pass - 1) & 1);
+        mbar_expect_tx(full + slot, bytes);
+        double *sb = tsm + (size_t)slot * kStage;
+        const int k0 = st * kTK;
+        tma_2d(sb, &tmap, k0, row0, full + slot);
+        tma_2d(sb + kP1, &tmap, k0, row1, full + slot);
 #pragma unroll
-  for (int q = 0; q < kTS - 1; ++q) {
-    if (it_i < p.n_titems) {
-      tab_issue<MODE>(src, st_i, ring + (size_t)q * kStage, lane);
-      if (++st_i == nst) {
-        st_i = 0;
-        it_i += nwarps;
-        if (it_i < p.n_titems) src = tab_src<MODE>(p, A, p.d_titems[it_i], lane);
+        for (int b = 0; b < NPART * 2; ++b)  // part * 2 + parity
+          bulk_g2s(sb + kSB + b * kTK * kAG, Ab + (size_t)b * ps + (size_t)k0 * kAG,
+                   kTK * kAG * sizeof(double), full + slot);
       }
     }
-    cp_commit();
+    return;
   }
-  int slot = 0;
-  for (int it = blockIdx.x * kTWarps + wid; it < p.n_titems; it += nwarps) {
+
+  // ---------------- consumer warps ----------------
+  const int lr = lane >> 2, lc4 = lane & 3;
+  const int par = wid & 1, hb = wid >> 1;
+  const int sl = 8 * hb + lr;                 // row slot within the staged planes
+  // staged rows (offsets in doubles): plane 0 row j at j*kPR, plane 1 row j at kP1 + j*kPR
+  const int own = par ? kP1 + (sl + 1) * kPR : sl * kPR;    // own row
+  const int hb0 = par ? sl * kPR : kP1 + sl * kPR;          // H rows hb0, hb0 + kPR
+
+  const int bsw = (lc4 & 2) << 1;             // column rotation of pairs with bit 1 set
+  int q = 0;
+  for (int it = blockIdx.x; it < p.n_titems; it += gridDim.x) {
     const int4 itm = p.d_titems[it];
-    const int m = itm.x, l0 = itm.y, par = itm.z;
-    const int r = ((l0 - m) >> 1) + lr;
+    const int m = itm.x, l0 = itm.y;
+    const int r = ((l0 - m) >> 1) + sl;
     const int l = m + 2 * r + par;
     const bool valid = l <= T;
     double cz = 0.0, cw = 0.0;
@@ -1089,52 +1117,37 @@ __global__ void __launch_bounds__(kTWarps * 32) analysis_tab_kernel(ShtView p, c
       cw = c.w;
       cz = (par || r > 0) ? c.z : 0.0;  // l = m has no P_{l-1}
     }
-    double cp0 = 0.0, cp1 = 0.0, ch0 = 0.0, ch1 = 0.0;
-    double dp0 = 0.0, dp1 = 0.0, dh0 = 0.0, dh1 = 0.0;
-    for (int st = 0; st < nst; ++st) {
-      // keep kTS - 1 stages in flight: issue the stage kTS - 1 ahead
-      {
-        double *dst = ring + (size_t)((slot + kTS - 1) % kTS) * kStage;
-        if (it_i < p.n_titems) {
-          tab_issue<MODE>(src, st_i, dst, lane);
-          if (++st_i == nst) {
-            st_i = 0;
-            it_i += nwarps;
-            if (it_i < p.n_titems) src = tab_src<MODE>(p, A, p.d_titems[it_i], lane);
-          }
-        }
-        cp_commit();
-      }
-      cp_wait<kTS - 1>();
-      __syncwarp();
-      const double *sb = ring + (size_t)slot * kStage;
+    // one accumulator pair per k-step of a stage: independent DMMA chains
+    double cp[kTK / 4][2], ch[kTK / 4][2];
+#pragma unroll
+    for (int u = 0; u < kTK / 4; ++u) cp[u][0] = cp[u][1] = ch[u][0] = ch[u][1] = 0.0;
+    const int bp = (0 * 2 + par) * kTK * kAG, bh = (1 * 2 + (par ^ 1)) * kTK * kAG;
+    for (int st = 0; st < nst; ++st, ++q) {
+      const int slot = q % kTS;
+      mbar_wait(full + slot, (q / kTS) & 1);
+      const double *sb = tsm + (size_t)slot * kStage;
 #pragma unroll
       for (int u = 0; u < kTK / 4; ++u) {
         const int kk = 4 * u;
-        const double a = sb[kSA + lr * kPR + kk + lc4];
-        const double b = sb[kSBp + (kk + lc4) * kBR + lr];
-        if (u & 1)
-          dmma(dp0, dp1, a, b);
-        else
-          dmma(cp0, cp1, a, b);
+        const double a = sb[own + kk + lc4];
+        const double b = sb[kSB + bp + (kk + lc4) * kAG + (lr ^ bsw)];
+        dmma(cp[u][0], cp[u][1], a, b);
         if (MODE == 0) {
-          const double hm = sb[kSH + lr * kPR + kk + lc4];
-          const double hp = sb[kSH + (lr + 1) * kPR + kk + lc4];
-          const double h = fma(cz, hm, -cw * hp);
-          const double bh = sb[kSBh + (kk + lc4) * kBR + lr];
-          if (u & 1)
-            dmma(dh0, dh1, h, bh);
-          else
-            dmma(ch0, ch1, h, bh);
+          const double hm = sb[hb0 + kk + lc4];
+          const double hq = sb[hb0 + kPR + kk + lc4];
+          const double h = fma(cz, hm, -cw * hq);
+          const double bb = sb[kSB + bh + (kk + lc4) * kAG + (lr ^ bsw)];
+          dmma(ch[u][0], ch[u][1], h, bb);
         }
       }
-      __syncwarp();  // slot free for the next issue
-      slot = (slot + 1) % kTS;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
     }
-    cp0 += dp0;
-    cp1 += dp1;
-    ch0 += dh0;
-    ch1 += dh1;
+    // pairwise combine of the k-step partial sums
+    const double cp0 = (cp[0][0] + cp[1][0]) + (cp[2][0] + cp[3][0]);
+    const double cp1 = (cp[0][1] + cp[1][1]) + (cp[2][1] + cp[3][1]);
+    const double ch0 = (ch[0][0] + ch[1][0]) + (ch[2][0] + ch[3][0]);
+    const double ch1 = (ch[0][1] + ch[1][1]) + (ch[2][1] + ch[3][1]);
     const int slotc = col_offset(T, m) + (l - m);
     if (MODE == 0) {
       // lane lc4 = 0: S1,S5 (vort); 1: S2,S6 (+ S4 from lane+2) (div); 2: S3,S7 (phi')
@@ -1154,7 +1167,6 @@ __global__ void __launch_bounds__(kTWarps * 32) analysis_tab_kernel(ShtView p, c
       if (valid && lc4 < nf) out[(size_t)lc4 * p.ncoef + slotc] = make_double2(cp0, cp1);
     }
   }
-  cp_wait<0>();
 }
 
 // FFT size of the tendency path: smallest 7-smooth n >= 3T+1 (the user
@@ -1348,14 +1360,30 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
       for (int i = 0; i < nh; ++i) rc16[i] = rcos[i];
       std::vector<int4> items;
       for (int m = 0; m <= T; ++m)
-        for (int l0 = m; l0 <= T; l0 += kAL)
-          for (int par = 0; par < 2; ++par)
-            if (l0 + par <= T) items.push_back(make_int4(m, l0, par, 0));
+        for (int l0 = m; l0 <= T; l0 += kTL)
+          items.push_back(make_int4(m, l0, (int)(ptoff[m] / p->nt16), 0));
       p->n_titems = (int)items.size();
       up((void **)&p->d_ptoff, ptoff.data(), sizeof(long long) * ptoff.size());
       up((void **)&p->d_rcos16, rc16.data(), sizeof(double) * rc16.size());
       up((void **)&p->d_titems, items.data(), sizeof(int4) * items.size());
       if (e == cudaSuccess) e = cudaMalloc(&p->d_ptab, sizeof(double) * (size_t)tot);
+      if (e == cudaSuccess) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr);
+        if (e == cudaSuccess && (qr != cudaDriverEntryPointSuccess || !fn)) e = cudaErrorNotSupported;
+        if (e == cudaSuccess) {
+          const cuuint64_t dims[2] = {(cuuint64_t)p->nt16, (cuuint64_t)(tot / p->nt16)};
+          const cuuint64_t strides[1] = {(cuuint64_t)p->nt16 * sizeof(double)};
+          const cuuint32_t box[2] = {(cuuint32_t)kPR, (cuuint32_t)kTBoxRows};
+          const cuuint32_t es[2] = {1, 1};
+          CUresult cr = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(
+              &p->ptab_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, p->d_ptab, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (cr != CUDA_SUCCESS) e = cudaErrorInvalidValue;
+        }
+      }
       if (e == cudaSuccess) {
         ptab_kernel<<<dim3(T + 1, (p->nt16 + 127) / 128), 128>>>(static_cast<const ShtView &>(*p));
         e = cudaGetLastError();
@@ -1489,14 +1517,16 @@ static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf,
     SWX_CUDA_TRY(cudaGetDevice(&dev));
     SWX_CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
     SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, analysis_tab_kernel<MODE>,
-                                                               kTWarps * 32, kTabSmem));
+                                                               kTabThreads, kTabSmem));
     per_sm[MODE] = std::max(k, 1);
     nsm[MODE] = n;
   }
-  const int need = (p->n_titems + kTWarps - 1) / kTWarps;
-  const int blocks = std::max(1, std::min(need, nsm[MODE] * per_sm[MODE]));
-  analysis_tab_kernel<MODE><<<blocks, kTWarps * 32, kTabSmem, s>>>(static_cast<const ShtView &>(*p),
-                                                                   A, out, nf);
+  // equal-cost items: give every CTA the same number of items
+  const int slots = nsm[MODE] * per_sm[MODE];
+  const int per_cta = (p->n_titems + slots - 1) / slots;
+  const int blocks = std::max(1, (p->n_titems + per_cta - 1) / per_cta);
+  analysis_tab_kernel<MODE><<<blocks, kTabThreads, kTabSmem, s>>>(static_cast<const ShtView &>(*p),
+                                                                  p->ptab_map, A, out, nf);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
