@@ -111,6 +111,16 @@ int swx_rexi_sum_prepared(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
                           const swx_c128 *d_betas, const void *d_prep, int pole_begin,
                           int pole_end, int realify, swx_c128 *d_out, void *d_workspace,
                           size_t workspace_bytes, void *stream);
+/* The same sum with the ETD2RK combination fused into its epilogue:
+ * d_out = d_base + scale * (realified) sum, per state -- the
+ * `psi0 u + dt psi1 N(u)` and `a + dt psi2 (N(a) - N(u))` updates of
+ * etdrk2_step (steppers.py:259-269), bitwise equal to swx_rexi_sum_prepared
+ * followed by swx_state_axpy.  d_base has the layout of d_out.              */
+int swx_rexi_sum_prepared_axpy(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                               const swx_c128 *d_betas, const void *d_prep, int pole_begin,
+                               int pole_end, int realify, const swx_c128 *d_base,
+                               double scale, swx_c128 *d_out, void *d_workspace,
+                               size_t workspace_bytes, void *stream);
 
 /* Forward operator (dt L + alpha) x -- apply_stacked, solvers.py:252-256.   */
 int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,
@@ -157,6 +167,12 @@ int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_div,
 int swx_sht_tendency(swx_sht p, int atoms, const swx_c128 *d_state,
                      swx_c128 *d_out, void *d_workspace, size_t ws_bytes,
                      void *stream);
+/* d_out = tendency(d_state) - d_sub, the difference N(a) - N(u) of the
+ * ETD2RK stage (steppers.py:262-266) fused into the analysis epilogue;
+ * bitwise equal to swx_sht_tendency followed by swx_state_axpy(-1).        */
+int swx_sht_tendency_sub(swx_sht p, int atoms, const swx_c128 *d_state,
+                         const swx_c128 *d_sub, swx_c128 *d_out, void *d_workspace,
+                         size_t ws_bytes, void *stream);
 
 /* ---- measurement helpers (bench.py) ---------------------------------------
  * swx_sht_tendency with per-stage device times (ms) written to h_stage_ms[7]:

@@ -43,6 +43,7 @@ SIGNATURES = {
     "swx_rexi_prepared_bytes": (_S, [_P, _I, _I, _I]),
     "swx_rexi_prepare": (_I, [_P, _I, _P, _I, _I, _P, _S, _P]),
     "swx_rexi_sum_prepared": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _S, _P]),
+    "swx_rexi_sum_prepared_axpy": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P, _D, _P, _P, _S, _P]),
     "swx_apply": (_I, [_P, C128, _P, _P, _P]),
     "swx_tree_combine": (_I, [_I, _I, _I, _P, _I, _P, _P]),
     "swx_state_axpy": (_I, [_I, _I, _P, _D, _P, _P, _P]),
@@ -53,6 +54,7 @@ SIGNATURES = {
     "swx_sht_analysis": (_I, [_P, _I, _P, _P, _P, _S, _P]),
     "swx_sht_uv": (_I, [_P, _P, _P, _P, _P, _P, _S, _P]),
     "swx_sht_tendency": (_I, [_P, _I, _P, _P, _P, _S, _P]),
+    "swx_sht_tendency_sub": (_I, [_P, _I, _P, _P, _P, _P, _S, _P]),
     "swx_sht_tendency_profile": (_I, [_P, _I, _P, _P, _P, _S, _P, _P]),
     "swx_fp64_fma_probe": (_I, [_P, _I, _I, _P]),
 }

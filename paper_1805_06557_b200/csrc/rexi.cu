@@ -186,12 +186,25 @@ __global__ void lg_factor_kernel(const double2 *__restrict__ alpha, const double
 // owned by LPM adjacent lanes, lane q of the group reducing the pole block
 // [q*np/LPM, (q+1)*np/LPM) as a perfect tree; an xor butterfly inside the
 // group completes tree_sum's order over the launch's np poles.
+// optional fused update of a pole sum's output: out = base + scale * sum
+// (the ETD2RK combinations, steppers.py:238-269); base == nullptr: out = sum
+struct Axpy {
+  const double2 *base;
+  double scale;
+};
+
+__device__ __forceinline__ double2 axpy_out(const Axpy &ep, size_t i, double2 v) {
+  if (!ep.base) return v;
+  const double2 b = ep.base[i];
+  return make_double2(b.x + v.x * ep.scale, b.y + v.y * ep.scale);
+}
+
 constexpr int kLgPasses = 4;  // 16-mode passes per CTA (factor staging amortised 4x)
 
 template <int NRHS, int LEAF>
 __global__ void __launch_bounds__(128) rexi_lg_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int np, int lpm,
-    int log2_lpm, int trunc, int ncoef, const int4 *__restrict__ sched, int realify,
+    int log2_lpm, int trunc, int ncoef, const int4 *__restrict__ sched, int realify, Axpy ep,
     double2 *__restrict__ out) {
   extern __shared__ double2 fac[];  // [NRHS][4][np], already interleaved (t*LPM + q)
   const int4 w = sched[blockIdx.x];
@@ -230,9 +243,10 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
       }
       if (has && q == 0) {
         if (realify && m == 0) pd.p.y = z.y = pd.d.y = 0.0;
-        out[(size_t)(r * 3 + 0) * ncoef + idx] = pd.p;
-        out[(size_t)(r * 3 + 1) * ncoef + idx] = z;
-        out[(size_t)(r * 3 + 2) * ncoef + idx] = pd.d;
+        const size_t o = (size_t)r * 3 * ncoef + idx;
+        out[o] = axpy_out(ep, o, pd.p);
+        out[o + ncoef] = axpy_out(ep, o + ncoef, z);
+        out[o + 2 * (size_t)ncoef] = axpy_out(ep, o + 2 * (size_t)ncoef, pd.d);
       }
     }
   }
@@ -556,7 +570,7 @@ __global__ void l_guard_kernel(const double2 *__restrict__ alpha, int P,
 // tree_sum over n_parts blocks + optional realify (parallel.py:161-169)
 __global__ void tree_combine_kernel(const double2 *__restrict__ parts,
                                     size_t stride, int n_parts, int ncoef,
-                                    int trunc, int realify,
+                                    int trunc, int realify, Axpy ep,
                                     double2 *__restrict__ out) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= stride) return;
@@ -576,7 +590,7 @@ __global__ void tree_combine_kernel(const double2 *__restrict__ parts,
   double2 v = stack[--depth];
   while (depth > 0) v = cadd(stack[--depth], v);
   if (realify && (int)(i % ncoef) <= trunc) v.y = 0.0;
-  out[i] = v;
+  out[i] = axpy_out(ep, i, v);
 }
 
 __global__ void axpy_kernel(const double2 *__restrict__ x, double s,
@@ -937,7 +951,7 @@ static int build_lg_factors(swx_solver s, const double2 *betas, int pole0, int P
 
 template <int NRHS>
 static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, int realify,
-                  double2 *out, cudaStream_t st) {
+                  double2 *out, cudaStream_t st, Axpy ep = Axpy{nullptr, 0.0}) {
   LgGeom g;
   int rc = lg_geom(P, g);
   if (rc) return rc;
@@ -952,7 +966,7 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                         (int)smem));                                           \
     k<<<n_cta, 128, smem, st>>>(rhs, fac, g.np, g.lpm, g.log2_lpm, s->trunc, s->ncoef, sched,  \
-                                realify, out);                                                 \
+                                realify, ep, out);                                             \
     break;                                                                                     \
   }
   switch (g.leaf) {
@@ -972,16 +986,16 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
 template <int NRHS>
 static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
                      int pole0, int P, int realify, double2 *out, double2 *fac_ws,
-                     cudaStream_t st) {
+                     cudaStream_t st, Axpy ep = Axpy{nullptr, 0.0}) {
   int rc = build_lg_factors<NRHS>(s, betas, pole0, P, fac_ws, st);
   if (rc) return rc;
-  return run_lg<NRHS>(s, rhs, fac_ws, P, realify, out, st);
+  return run_lg<NRHS>(s, rhs, fac_ws, P, realify, out, st, ep);
 }
 
 template <int NRHS>
 static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
                     int pole0, int P, int realify, double2 *out, char *ws,
-                    cudaStream_t st) {
+                    cudaStream_t st, Axpy ep = Axpy{nullptr, 0.0}) {
   const int nb = (P + 31) / 32;
   const int n_items = (s->trunc + 1) * nb;
   const int warps = l_grid_warps(s, n_items);
@@ -998,16 +1012,15 @@ static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
   SWX_LAUNCH_CHECK();
   const size_t stride = (size_t)NRHS * 3 * s->ncoef;
   tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, nb, s->ncoef,
-                                                                        s->trunc, realify, out);
+                                                                        s->trunc, realify, ep, out);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
 
-extern "C" int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
-                            const swx_c128 *d_betas, int pole_begin,
-                            int pole_end, int realify, swx_c128 *d_out,
-                            void *d_workspace, size_t workspace_bytes,
-                            void *stream) {
+static int rexi_sum_impl(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                         const swx_c128 *d_betas, int pole_begin, int pole_end, int realify,
+                         Axpy ep, swx_c128 *d_out, void *d_workspace, size_t workspace_bytes,
+                         void *stream) {
   if (!s) return fail(SWX_ERR_CONFIG, "null solver");
   if (n_rhs < 1 || n_rhs > 2) return fail(SWX_ERR_CONFIG, "n_rhs must be 1 or 2");
   if (!s->d_alpha) return fail(SWX_ERR_CONFIG, "solver not warmed (no shifts uploaded)");
@@ -1028,8 +1041,8 @@ extern "C" int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
     const size_t fac = (size_t)(s->trunc + 1) * n_rhs * 4 * np * sizeof(double2);
     double2 *fac_ws = (double2 *)d_workspace;
     if (chunks == 1)
-      return n_rhs == 1 ? launch_lg<1>(s, rhs, bet, pole_begin, P, realify, out, fac_ws, st)
-                        : launch_lg<2>(s, rhs, bet, pole_begin, P, realify, out, fac_ws, st);
+      return n_rhs == 1 ? launch_lg<1>(s, rhs, bet, pole_begin, P, realify, out, fac_ws, st, ep)
+                        : launch_lg<2>(s, rhs, bet, pole_begin, P, realify, out, fac_ws, st, ep);
     // aligned chunks of kLgMaxP poles, combined in tree order
     double2 *part = (double2 *)((char *)d_workspace + ((fac + 255) / 256) * 256);
     const size_t stride = (size_t)n_rhs * 3 * s->ncoef;
@@ -1043,13 +1056,22 @@ extern "C" int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
     }
     tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, chunks,
                                                                           s->ncoef, s->trunc,
-                                                                          realify, out);
+                                                                          realify, ep, out);
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
   return n_rhs == 1
-             ? launch_l<1>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st)
-             : launch_l<2>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st);
+             ? launch_l<1>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st, ep)
+             : launch_l<2>(s, rhs, bet, pole_begin, P, realify, out, (char *)d_workspace, st, ep);
+}
+
+extern "C" int swx_rexi_sum(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                            const swx_c128 *d_betas, int pole_begin,
+                            int pole_end, int realify, swx_c128 *d_out,
+                            void *d_workspace, size_t workspace_bytes,
+                            void *stream) {
+  return rexi_sum_impl(s, n_rhs, d_rhs, d_betas, pole_begin, pole_end, realify,
+                       Axpy{nullptr, 0.0}, d_out, d_workspace, workspace_bytes, stream);
 }
 
 // ---- prepared pole sums: the lg factor tables depend only on (alpha, beta,
@@ -1091,14 +1113,14 @@ extern "C" int swx_rexi_prepare(swx_solver s, int n_rhs, const swx_c128 *d_betas
   return SWX_OK;
 }
 
-extern "C" int swx_rexi_sum_prepared(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
-                                     const swx_c128 *d_betas, const void *d_prep,
-                                     int pole_begin, int pole_end, int realify, swx_c128 *d_out,
-                                     void *d_workspace, size_t workspace_bytes, void *stream) {
+static int rexi_sum_prepared_impl(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                                  const swx_c128 *d_betas, const void *d_prep, int pole_begin,
+                                  int pole_end, int realify, Axpy ep, swx_c128 *d_out,
+                                  void *d_workspace, size_t workspace_bytes, void *stream) {
   const bool cor = s && s->group == SWX_GROUP_L && s->omega > 0.0;
   if (!s || cor || !d_prep)  // nothing prepared for the chain solver
-    return swx_rexi_sum(s, n_rhs, d_rhs, d_betas, pole_begin, pole_end, realify, d_out,
-                        d_workspace, workspace_bytes, stream);
+    return rexi_sum_impl(s, n_rhs, d_rhs, d_betas, pole_begin, pole_end, realify, ep, d_out,
+                         d_workspace, workspace_bytes, stream);
   if (n_rhs < 1 || n_rhs > 2) return fail(SWX_ERR_CONFIG, "n_rhs must be 1 or 2");
   if (pole_begin < 0 || pole_end > s->n_poles || pole_end <= pole_begin)
     return fail(SWX_ERR_CONFIG, "bad pole range");
@@ -1109,8 +1131,8 @@ extern "C" int swx_rexi_sum_prepared(swx_solver s, int n_rhs, const swx_c128 *d_
   const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
   const size_t t = swx_rexi_prepared_bytes(s, n_rhs, pole_begin, pole_end) / chunks;
   if (chunks == 1)
-    return n_rhs == 1 ? run_lg<1>(s, rhs, (const double2 *)d_prep, P, realify, out, st)
-                      : run_lg<2>(s, rhs, (const double2 *)d_prep, P, realify, out, st);
+    return n_rhs == 1 ? run_lg<1>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep)
+                      : run_lg<2>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep);
   const size_t stride = (size_t)n_rhs * 3 * s->ncoef;
   if (!d_workspace || workspace_bytes < chunks * stride * sizeof(double2))
     return fail(SWX_ERR_CONFIG, "workspace too small");
@@ -1124,9 +1146,29 @@ extern "C" int swx_rexi_sum_prepared(swx_solver s, int n_rhs, const swx_c128 *d_
   }
   tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, chunks,
                                                                         s->ncoef, s->trunc,
-                                                                        realify, out);
+                                                                        realify, ep, out);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
+}
+
+extern "C" int swx_rexi_sum_prepared(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                                     const swx_c128 *d_betas, const void *d_prep,
+                                     int pole_begin, int pole_end, int realify, swx_c128 *d_out,
+                                     void *d_workspace, size_t workspace_bytes, void *stream) {
+  return rexi_sum_prepared_impl(s, n_rhs, d_rhs, d_betas, d_prep, pole_begin, pole_end, realify,
+                                Axpy{nullptr, 0.0}, d_out, d_workspace, workspace_bytes, stream);
+}
+
+extern "C" int swx_rexi_sum_prepared_axpy(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                                          const swx_c128 *d_betas, const void *d_prep,
+                                          int pole_begin, int pole_end, int realify,
+                                          const swx_c128 *d_base, double scale, swx_c128 *d_out,
+                                          void *d_workspace, size_t workspace_bytes,
+                                          void *stream) {
+  if (!d_base) return fail(SWX_ERR_CONFIG, "null base state");
+  return rexi_sum_prepared_impl(s, n_rhs, d_rhs, d_betas, d_prep, pole_begin, pole_end, realify,
+                                Axpy{(const double2 *)d_base, scale}, d_out, d_workspace,
+                                workspace_bytes, stream);
 }
 
 extern "C" int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,
@@ -1148,7 +1190,8 @@ extern "C" int swx_tree_combine(int trunc, int n_states, int n_parts,
   const int nc = ncoef_of(trunc);
   const size_t stride = (size_t)n_states * 3 * nc;
   tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      (const double2 *)d_parts, stride, n_parts, nc, trunc, realify, (double2 *)d_out);
+      (const double2 *)d_parts, stride, n_parts, nc, trunc, realify, Axpy{nullptr, 0.0},
+      (double2 *)d_out);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }

@@ -1042,7 +1042,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
                                                                    const __grid_constant__ CUtensorMap tmap,
                                                                    const double *A, double2 *out,
-                                                                   int nf) {
+                                                                   int nf, const double2 *sub) {
   extern __shared__ __align__(128) double tsm[];
   uint64_t *full = reinterpret_cast<uint64_t *>(tsm + (size_t)kTS * kStage);
   uint64_t *empty = full + kTS;
@@ -1161,7 +1161,13 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
           vy += llk * s4y;
         }
         const int f = lc4 == 0 ? 1 : (lc4 == 1 ? 2 : 0);
-        out[(size_t)f * p.ncoef + slotc] = make_double2(vx, vy);
+        const size_t o = (size_t)f * p.ncoef + slotc;
+        if (sub) {  // fused difference N(a) - N(u) of the ETD2RK step
+          const double2 b = sub[o];
+          vx = vx + b.x * -1.0;
+          vy = vy + b.y * -1.0;
+        }
+        out[o] = make_double2(vx, vy);
       }
     } else {
       if (valid && lc4 < nf) out[(size_t)lc4 * p.ncoef + slotc] = make_double2(cp0, cp1);
@@ -1507,7 +1513,8 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
 }
 
 template <int MODE>
-static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s) {
+static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
+                               const double2 *sub = nullptr) {
   // resident CTAs per SM and SM count, queried once per mode
   static int nsm[2] = {0, 0}, per_sm[2] = {0, 0};
   if (!nsm[MODE]) {
@@ -1526,7 +1533,7 @@ static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf,
   const int per_cta = (p->n_titems + slots - 1) / slots;
   const int blocks = std::max(1, (p->n_titems + per_cta - 1) / per_cta);
   analysis_tab_kernel<MODE><<<blocks, kTabThreads, kTabSmem, s>>>(static_cast<const ShtView &>(*p),
-                                                                  p->ptab_map, A, out, nf);
+                                                                  p->ptab_map, A, out, nf, sub);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -1689,8 +1696,16 @@ extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_d
 }
 
 // the fused LC+N tendency; `ev` (7 events or null) brackets the stages
+// out = tendency(state) - sub (sub may be null)
+__global__ void sub_kernel(double2 *out, const double2 *sub, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 a = out[i], b = sub[i];
+  out[i] = make_double2(a.x + b.x * -1.0, a.y + b.y * -1.0);
+}
+
 static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *out, ShtWs &w,
-                         cudaStream_t s, cudaEvent_t *ev) {
+                         cudaStream_t s, cudaEvent_t *ev, const double2 *sub = nullptr) {
   int rc;
   auto mark = [&](int k) {
     if (ev) cudaEventRecord(ev[k], s);
@@ -1719,7 +1734,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     SWX_LAUNCH_CHECK();
     mark(4);
     mark(5);
-    if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s))) return rc;
+    if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s, sub))) return rc;
     mark(6);
     return SWX_OK;
   }
@@ -1744,10 +1759,16 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
                                            w.A);
     SWX_LAUNCH_CHECK();
     mark(5);
-    if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s))) return rc;
+    if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s, sub))) return rc;
+    sub = nullptr;
   } else {
     mark(5);  // prep is fused into the analysis kernel
     if ((rc = launch_analysis<0>(p, w.A, w.Q, w.lc, atoms, out, 3, s))) return rc;
+  }
+  if (sub) {
+    const size_t n = 3 * (size_t)p->ncoef;
+    sub_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, sub, n);
+    SWX_LAUNCH_CHECK();
   }
   mark(6);
   return SWX_OK;
@@ -1767,6 +1788,28 @@ extern "C" int swx_sht_tendency(swx_sht p, int atoms, const swx_c128 *d_state,
     return SWX_OK;
   }
   return tendency_impl(p, atoms, (const double2 *)d_state, (double2 *)d_out, w, s, nullptr);
+}
+
+extern "C" int swx_sht_tendency_sub(swx_sht p, int atoms, const swx_c128 *d_state,
+                                    const swx_c128 *d_sub, swx_c128 *d_out, void *d_ws,
+                                    size_t ws_bytes, void *stream) {
+  int rc = check_ws(p, d_ws, ws_bytes);
+  if (rc) return rc;
+  if (!d_sub) return fail(SWX_ERR_CONFIG, "null subtrahend");
+  if (atoms <= 0 || (atoms & ~(SWX_TEND_LC | SWX_TEND_N)))
+    return fail(SWX_ERR_CONFIG, "atoms must be a non-empty subset of {lc, n}");
+  cudaStream_t s = (cudaStream_t)stream;
+  ShtWs w = carve(p, d_ws);
+  const double2 *sub = (const double2 *)d_sub;
+  if (p->omega == 0.0) atoms &= ~SWX_TEND_LC;  // swe.py:200-201
+  if (atoms == 0) {
+    SWX_CUDA_TRY(cudaMemsetAsync(d_out, 0, 3 * (size_t)p->ncoef * sizeof(double2), s));
+    const size_t n = 3 * (size_t)p->ncoef;
+    sub_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((double2 *)d_out, sub, n);
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
+  return tendency_impl(p, atoms, (const double2 *)d_state, (double2 *)d_out, w, s, nullptr, sub);
 }
 
 extern "C" int swx_sht_tendency_profile(swx_sht p, int atoms, const swx_c128 *d_state,
@@ -1789,6 +1832,8 @@ extern "C" int swx_sht_tendency_profile(swx_sht p, int atoms, const swx_c128 *d_
     cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
     h_stage_ms[i] = ms;
   }
+  if (p->fused_grid)  // C2R, products and prep live inside the fused grid stage
+    h_stage_ms[1] = h_stage_ms[2] = h_stage_ms[4] = 0.0;
   float tot = 0.f;
   cudaEventElapsedTime(&tot, ev[0], ev[6]);
   h_stage_ms[6] = tot;

@@ -170,17 +170,25 @@ class ShiftedLinearSolver:
         return buf
 
     def rexi_sum_prepared_dev(self, alphas, betas_dev, prep, rhs_dev, out_dev, pole_range=None,
-                              realify: bool = True, stream=None):
-        if prep is None:
-            return self.rexi_sum_dev(alphas, betas_dev, rhs_dev, out_dev, pole_range, realify,
-                                     stream)
+                              realify: bool = True, stream=None, base=None, scale: float = 0.0):
+        """Prepared pole sum; with ``base``: out = base + scale * sum (fused)."""
         nat = self._native(alphas)
         n_rhs = rhs_dev.shape[0]
         lo, hi = pole_range if pole_range is not None else (0, nat.alphas.size)
+        if prep is None and base is None:
+            return self.rexi_sum_dev(alphas, betas_dev, rhs_dev, out_dev, pole_range, realify,
+                                     stream)
         ws, nbytes = self.workspace(nat, n_rhs, lo, hi, stream)
-        _lib.check(self._lib.swx_rexi_sum_prepared(
-            nat.h, n_rhs, ptr(rhs_dev), ptr(betas_dev), ptr(prep), lo, hi, 1 if realify else 0,
-            ptr(out_dev), ptr(ws) if nbytes else 0, nbytes, stream_ptr(stream)))
+        if base is None:
+            _lib.check(self._lib.swx_rexi_sum_prepared(
+                nat.h, n_rhs, ptr(rhs_dev), ptr(betas_dev), ptr(prep), lo, hi,
+                1 if realify else 0, ptr(out_dev), ptr(ws) if nbytes else 0, nbytes,
+                stream_ptr(stream)))
+        else:
+            _lib.check(self._lib.swx_rexi_sum_prepared_axpy(
+                nat.h, n_rhs, ptr(rhs_dev), ptr(betas_dev), ptr(prep) if prep is not None else 0,
+                lo, hi, 1 if realify else 0, ptr(base), float(scale), ptr(out_dev),
+                ptr(ws) if nbytes else 0, nbytes, stream_ptr(stream)))
         return out_dev
 
     def apply_dev(self, alpha, x_dev, out_dev=None, stream=None):

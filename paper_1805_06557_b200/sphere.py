@@ -215,14 +215,20 @@ class ShtPlan:
             self.workspace.numel(), stream_ptr(stream)))
         return u, v
 
-    def tendency_dev(self, atoms: int, state, out=None, stream=None):
+    def tendency_dev(self, atoms: int, state, out=None, stream=None, sub=None):
+        """out = tendency(state) (minus ``sub`` when given, fused on the device)."""
         import torch
 
         if out is None:
             out = torch.empty_like(state)
-        _lib.check(self._lib.swx_sht_tendency(
-            self._h, atoms, ptr(state), ptr(out), ptr(self.workspace),
-            self.workspace.numel(), stream_ptr(stream)))
+        if sub is None:
+            _lib.check(self._lib.swx_sht_tendency(
+                self._h, atoms, ptr(state), ptr(out), ptr(self.workspace),
+                self.workspace.numel(), stream_ptr(stream)))
+        else:
+            _lib.check(self._lib.swx_sht_tendency_sub(
+                self._h, atoms, ptr(state), ptr(sub), ptr(out), ptr(self.workspace),
+                self.workspace.numel(), stream_ptr(stream)))
         return out
 
 

@@ -321,6 +321,41 @@ def test_prepared_sum_bitwise_equals_unprepared():
         assert np.array_equal(got, ref), group.token
 
 
+@pytest.mark.parametrize("n_poles", [256, 1024])
+def test_fused_axpy_sum_bitwise(n_poles):
+    """swx_rexi_sum_prepared_axpy == prepared sum followed by swx_state_axpy,
+    bitwise, for the single-chunk and the chunked (tree-combined) lg path and
+    the Coriolis chain path."""
+    from paper_1805_06557_b200.steppers import axpy
+    par = params(63)
+    for group in (LG, L):
+        sl = ShiftedLinearSolver(group, 3600.0, par)
+        c0 = coeffs(n_poles, 1)
+        rhs = to_device(pack(ost.seeded_linear_state(63, 4))[None])
+        base = to_device(pack(ost.seeded_linear_state(63, 5))[None])
+        bet = to_device(c0.betas[None])
+        prep = sl.prepare_dev(c0.alphas, bet)
+        plain = sl.rexi_sum_prepared_dev(c0.alphas, bet, prep, rhs, torch.empty_like(rhs))
+        ref = axpy(63, base, 1800.0, plain, torch.empty_like(rhs)).cpu().numpy()
+        got = sl.rexi_sum_prepared_dev(c0.alphas, bet, prep, rhs, torch.empty_like(rhs),
+                                       base=base, scale=1800.0).cpu().numpy()
+        assert np.array_equal(got, ref), (group.token, n_poles)
+
+
+def test_tendency_sub_bitwise():
+    """swx_sht_tendency_sub == tendency followed by axpy(-1), bitwise (T63:
+    fused table path; the plain difference is exercised by the T256 day)."""
+    from paper_1805_06557_b200.steppers import axpy
+    plan = plan_for(SphereConfig.for_truncation(63))
+    g = osh.grid_for(63)
+    st = to_device(olay.pack(ost.seeded_balanced_state(g)))
+    sub = to_device(pack(ost.seeded_linear_state(63, 6)))
+    t = plan.tendency_dev(3, st)
+    ref = axpy(63, t, -1.0, sub, torch.empty_like(t)).cpu().numpy()
+    got = plan.tendency_dev(3, st, sub=sub).cpu().numpy()
+    assert np.array_equal(got, ref)
+
+
 def test_stiffness_corner_chunked_poles_vs_oracle():
     """cfg3 corner (Phibar = 18000 g, dt = 3600 s, contour p1 = 80, N = 2048)
     at T85: the lg pole sum runs in 4 aligned chunks of 512 combined by the
