@@ -36,10 +36,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <vector>
 
 #include "swx_common.cuh"
+#include "fft_reg.cuh"
 
 // POD view passed to kernels by value
 struct ShtView {
@@ -505,21 +507,68 @@ __device__ double2 *cta_fft(double2 *a, double2 *b, int N, int nbat, const int *
   return in;
 }
 
+// fold of one latitude pair's forward transforms into the prepared analysis
+// rows of every m (quadrature weights, i m, 1/a, hemisphere even/odd);
+// X(f, k) returns bin k of forward transform f (phi'u, phi'v, vort u, vort v, KE)
+template <typename XF>
+__device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bool nl,
+                                          const double2 *lc, double *A, XF X) {
+  const int T = p.trunc, N = p.nlon_t;
+  const int jn = p.d_jn[i], js = p.d_js[i];
+  const size_t ps = (size_t)p.nt16 * kAG;
+  for (int m = threadIdx.x; m <= T; m += blockDim.x) {
+    double2 F[2][5], L1[2], L2[2];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+      double2 Xv = make_double2(0.0, 0.0), Yv = Xv;
+      if (nl) {
+        const double2 a = X(f, m), b = X(f, m == 0 ? 0 : N - m);
+        // X = (Z_m + conj Z_{N-m}) / 2, Y = (Z_m - conj Z_{N-m}) / (2i)
+        Xv = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+        Yv = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
+      }
+      F[0][f] = make_double2(Xv.x * p.dlon_t, Xv.y * p.dlon_t);
+      F[1][f] = make_double2(Yv.x * p.dlon_t, Yv.y * p.dlon_t);
+    }
+#pragma unroll
+    for (int hemi = 0; hemi < 2; ++hemi) {
+      const int j = hemi ? js : jn;
+      L1[hemi] = L2[hemi] = make_double2(0.0, 0.0);
+      if (atoms & SWX_TEND_LC) {
+        L1[hemi] = lc[(size_t)j * p.nm + m];
+        L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
+      }
+    }
+    double2 ev[7], od[7];
+    tend_fold<true>(p, F, L1, L2, m, i, ev, od);
+    double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+    put_row_t(base + 0 * ps, ev, 4, i);
+    put_row_t(base + 1 * ps, od, 4, i);
+    put_row_t(base + 2 * ps, ev + 4, 3, i);
+    put_row_t(base + 3 * ps, od + 4, 3, i);
+  }
+}
+
+// zero prepared rows of the padding pairs i >= nh
+__device__ __forceinline__ void grid_zero_rows(const ShtView &p, int i, double *A) {
+  const size_t ps = (size_t)p.nt16 * kAG;
+  for (int m = threadIdx.x; m <= p.trunc; m += blockDim.x) {
+    double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < kAG; ++c) base[q * ps + c] = 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const double2 *c2r,
                                                            const double2 *lc, int atoms,
                                                            const double2 *tw_g, double *A) {
   extern __shared__ __align__(16) double2 gsm[];
   const int N = p.nlon_t, T = p.trunc;
   const int i = blockIdx.x;  // latitude pair (padded to nt16)
-  const size_t ps = (size_t)p.nt16 * kAG;
   if (i >= p.nh) {  // padding pairs: zero prepared rows
-    for (int m = threadIdx.x; m <= T; m += blockDim.x) {
-      double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int c = 0; c < kAG; ++c) base[q * ps + c] = 0.0;
-    }
+    grid_zero_rows(p, i, A);
     return;
   }
   // 9 buffers of N (twiddles stay in global/L1): 2 CTAs per SM at N = 784
@@ -566,39 +615,141 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     R1 = cta_fft(Pk, spare, N, 1, p.fft_radix, p.fft_npass, tw, false);
     R4 = r4;
   }
-  // fold + prepared rows for every m of this pair
-  for (int m = threadIdx.x; m <= T; m += blockDim.x) {
-    double2 F[2][5], L1[2], L2[2];
-#pragma unroll
-    for (int f = 0; f < 5; ++f) {
-      double2 X = make_double2(0.0, 0.0), Y = X;
-      if (nl) {
-        const double2 *Rf = f < 4 ? R4 + (size_t)f * N : R1;
-        const double2 a = Rf[m], b = Rf[m == 0 ? 0 : N - m];
-        // X = (Z_m + conj Z_{N-m}) / 2, Y = (Z_m - conj Z_{N-m}) / (2i)
-        X = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-        Y = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
-      }
-      F[0][f] = make_double2(X.x * p.dlon_t, X.y * p.dlon_t);
-      F[1][f] = make_double2(Y.x * p.dlon_t, Y.y * p.dlon_t);
-    }
-#pragma unroll
-    for (int hemi = 0; hemi < 2; ++hemi) {
-      const int j = hemi ? js : jn;
-      L1[hemi] = L2[hemi] = make_double2(0.0, 0.0);
-      if (atoms & SWX_TEND_LC) {
-        L1[hemi] = lc[(size_t)j * p.nm + m];
-        L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
-      }
-    }
-    double2 ev[7], od[7];
-    tend_fold<true>(p, F, L1, L2, m, i, ev, od);
-    double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
-    put_row_t(base + 0 * ps, ev, 4, i);
-    put_row_t(base + 1 * ps, od, 4, i);
-    put_row_t(base + 2 * ps, ev + 4, 3, i);
-    put_row_t(base + 3 * ps, od + 4, 3, i);
+  grid_fold(p, i, atoms, nl, lc, A, [&](int f, int k) {
+    return f < 4 ? R4[(size_t)f * N + k] : R1[k];
+  });
+}
+
+// Fused grid stage with register FFTs, for nlon_t = R1 * R2 (one CTA per
+// latitude pair, north + i south packed as one complex row).  Four-step
+// transforms in place in shared memory (row pitch R1 + 1, odd: conflict-free
+// for both the row and the column walks):
+//   inverse:  column DFTs (length R2, read straight from the Fourier rows),
+//             twiddle W_N^{-n1 k2}, row DFTs (length R1) -> grid point
+//             g = k2 + R2 k1 at position k1 + (R1+1) k2 (transposed)
+//   products: pointwise in that order (swe.py:230-245)
+//   forward:  row DFTs (length R1), twiddle W_N^{a c}, column DFTs (length
+//             R2) -> bin k = c + R1 d at position c + (R1+1) d (natural)
+// Two barriers per transform instead of one per radix pass, no index
+// divisions, every DFT in registers.
+template <int R1, int R2>
+struct SqCfg {
+  static constexpr int N = R1 * R2, RP = R1 + 1, FS = RP * R2;
+  static constexpr int MT = (R1 > R2 ? R1 : R2);
+  static constexpr int NT = ((5 * MT + 31) / 32) * 32;
+  static constexpr size_t SMEM = (size_t)5 * FS * sizeof(double2);
+};
+
+template <int R1, int R2>
+__global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p, const double2 *c2r,
+                                                                    const double2 *lc, int atoms,
+                                                                    const double2 *tw_g,
+                                                                    double *A) {
+  using C = SqCfg<R1, R2>;
+  constexpr int N = C::N, RP = C::RP, FS = C::FS;
+  extern __shared__ __align__(16) double2 gsm[];
+  double2 *F = gsm;  // [5][FS]
+  const int i = blockIdx.x;
+  if (i >= p.nh) {
+    grid_zero_rows(p, i, A);
+    return;
   }
+  const int T = p.trunc;
+  const bool nl = (atoms & SWX_TEND_N) != 0;
+  if (nl) {
+    const int jn = p.d_jn[i], js = p.d_js[i];
+    const size_t row = (size_t)p.nlat * p.nfreq_t;
+    // inverse, column DFTs: input bin k = n1 + R1 n2 of u, v, vort, phi'
+    for (int t = threadIdx.x; t < 4 * R1; t += blockDim.x) {
+      const int f = t / R1, n1 = t - f * R1;
+      const double2 *Xn = c2r + f * row + (size_t)jn * p.nfreq_t;
+      const double2 *Xs = c2r + f * row + (size_t)js * p.nfreq_t;
+      double2 v[R2];
+#pragma unroll
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const int k = n1 + R1 * n2;
+        double2 a = make_double2(0.0, 0.0), b = a;
+        if (k <= T) {
+          a = Xn[k];
+          b = Xs[k];
+        } else if (N - k <= T) {
+          const double2 an = Xn[N - k], bs = Xs[N - k];
+          a = make_double2(an.x, -an.y);
+          b = make_double2(bs.x, -bs.y);
+        }
+        v[n2] = make_double2(a.x - b.y, a.y + b.x);  // X + i Y
+      }
+      regfft::Dft<R2, true>::run(v);
+      double2 *o = F + (size_t)f * FS + n1;
+#pragma unroll
+      for (int k2 = 0; k2 < R2; ++k2) {
+        double2 x = v[k2];
+        if (k2 > 0) {
+          const double2 w = __ldg(tw_g + (n1 * k2) % N);  // conj for the inverse
+          x = make_double2(x.x * w.x + x.y * w.y, x.y * w.x - x.x * w.y);
+        }
+        o[RP * k2] = x;
+      }
+    }
+    __syncthreads();
+    // inverse, row DFTs
+    for (int t = threadIdx.x; t < 4 * R2; t += blockDim.x) {
+      const int f = t / R2, k2 = t - f * R2;
+      double2 *o = F + (size_t)f * FS + RP * k2;
+      double2 v[R1];
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) v[n1] = o[n1];
+      regfft::Dft<R1, true>::run(v);
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) o[k1] = v[k1];
+    }
+    __syncthreads();
+    // products on the grid, north in Re, south in Im:
+    // phi'u, phi'v, vort u, vort v, |V|^2/2  (swe.py:230-245)
+    for (int n = threadIdx.x; n < FS; n += blockDim.x) {
+      const double2 u = F[n], v = F[FS + n], z = F[2 * FS + n], ph = F[3 * FS + n];
+      F[n] = make_double2(ph.x * u.x, ph.y * u.y);
+      F[FS + n] = make_double2(ph.x * v.x, ph.y * v.y);
+      F[2 * FS + n] = make_double2(z.x * u.x, z.y * u.y);
+      F[3 * FS + n] = make_double2(z.x * v.x, z.y * v.y);
+      F[4 * FS + n] = make_double2(0.5 * (u.x * u.x + v.x * v.x), 0.5 * (u.y * u.y + v.y * v.y));
+    }
+    __syncthreads();
+    // forward, row DFTs (grid point g = a + R2 b at b + RP a) and twiddles
+    for (int t = threadIdx.x; t < 5 * R2; t += blockDim.x) {
+      const int f = t / R2, a = t - f * R2;
+      double2 *o = F + (size_t)f * FS + RP * a;
+      double2 v[R1];
+#pragma unroll
+      for (int b = 0; b < R1; ++b) v[b] = o[b];
+      regfft::Dft<R1, false>::run(v);
+#pragma unroll
+      for (int c = 0; c < R1; ++c) {
+        double2 x = v[c];
+        if (c > 0 && a > 0) {
+          const double2 w = __ldg(tw_g + (a * c) % N);
+          x = make_double2(x.x * w.x - x.y * w.y, x.x * w.y + x.y * w.x);
+        }
+        o[c] = x;
+      }
+    }
+    __syncthreads();
+    // forward, column DFTs -> bin k = c + R1 d at c + RP d
+    for (int t = threadIdx.x; t < 5 * R1; t += blockDim.x) {
+      const int f = t / R1, c = t - f * R1;
+      double2 *o = F + (size_t)f * FS + c;
+      double2 v[R2];
+#pragma unroll
+      for (int a = 0; a < R2; ++a) v[a] = o[RP * a];
+      regfft::Dft<R2, false>::run(v);
+#pragma unroll
+      for (int d = 0; d < R2; ++d) o[RP * d] = v[d];
+    }
+    __syncthreads();
+  }
+  grid_fold(p, i, atoms, nl, lc, A, [&](int f, int k) {
+    return F[(size_t)f * FS + (k % R1) + RP * (k / R1)];
+  });
 }
 
 // plain analysis prep: nf (<= 4) grids already FFT'd into Q (pitch nfreq)
@@ -1695,6 +1846,46 @@ extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_d
   return SWX_OK;
 }
 
+template <int R1, int R2>
+static int launch_grid_sq(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
+  using C = SqCfg<R1, R2>;
+  static bool attr = false;
+  if (!attr) {
+    SWX_CUDA_TRY(cudaFuncSetAttribute(grid_sq_kernel<R1, R2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  grid_sq_kernel<R1, R2><<<p->nt16, C::NT, C::SMEM, s>>>(static_cast<const ShtView &>(*p), w.c2r,
+                                                         w.lc, atoms, p->d_tw, w.A);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+// fused grid stage: register four-step FFTs where nlon_t has a compiled
+// split (SWX_GRID_STOCKHAM=1 forces the generic shared-memory Stockham path)
+static int launch_grid(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
+  static const bool stockham = [] {
+    const char *e = getenv("SWX_GRID_STOCKHAM");
+    return e && atoi(e) != 0;
+  }();
+  if (!stockham) {
+    switch (p->nlon_t) {
+      case 784: return launch_grid_sq<28, 28>(p, atoms, w, s);   // T256
+      case 256: return launch_grid_sq<16, 16>(p, atoms, w, s);   // T85
+      case 192: return launch_grid_sq<12, 16>(p, atoms, w, s);   // T63
+      default: break;
+    }
+  }
+  const size_t smem = (size_t)9 * p->nlon_t * sizeof(double2);
+  if (smem > 48 * 1024)
+    SWX_CUDA_TRY(cudaFuncSetAttribute(grid_tend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  grid_tend_kernel<<<p->nt16, kGridT, smem, s>>>(static_cast<const ShtView &>(*p), w.c2r, w.lc,
+                                                 atoms, p->d_tw, w.A);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
 // the fused LC+N tendency; `ev` (7 events or null) brackets the stages
 // out = tendency(state) - sub (sub may be null)
 __global__ void sub_kernel(double2 *out, const double2 *sub, size_t n) {
@@ -1725,13 +1916,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     mark(1);
     mark(2);
     mark(3);
-    const size_t smem = (size_t)9 * p->nlon_t * sizeof(double2);
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(grid_tend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-    grid_tend_kernel<<<p->nt16, kGridT, smem, s>>>(static_cast<const ShtView &>(*p), w.c2r, w.lc,
-                                                   atoms, p->d_tw, w.A);
-    SWX_LAUNCH_CHECK();
+    if ((rc = launch_grid(p, atoms, w, s))) return rc;
     mark(4);
     mark(5);
     if ((rc = launch_analysis_tab<0>(p, w.A, out, 3, s, sub))) return rc;
