@@ -507,14 +507,22 @@ __device__ double2 *cta_fft(double2 *a, double2 *b, int N, int nbat, const int *
   return in;
 }
 
+// 16-byte asynchronous global -> shared copies (LDGSTS)
+__device__ __forceinline__ void cp16(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // fold of one latitude pair's forward transforms into the prepared analysis
 // rows of every m (quadrature weights, i m, 1/a, hemisphere even/odd);
-// X(f, k) returns bin k of forward transform f (phi'u, phi'v, vort u, vort v, KE)
-template <typename XF>
-__device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bool nl,
-                                          const double2 *lc, double *A, XF X) {
+// X(f, k) returns bin k of forward transform f (phi'u, phi'v, vort u, vort v, KE),
+// LC(term, hemisphere, m) the Fourier-space Coriolis terms of the pair
+template <typename XF, typename LF>
+__device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bool nl, double *A,
+                                          XF X, LF LC) {
   const int T = p.trunc, N = p.nlon_t;
-  const int jn = p.d_jn[i], js = p.d_js[i];
   const size_t ps = (size_t)p.nt16 * kAG;
   for (int m = threadIdx.x; m <= T; m += blockDim.x) {
     double2 F[2][5], L1[2], L2[2];
@@ -532,11 +540,10 @@ __device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bo
     }
 #pragma unroll
     for (int hemi = 0; hemi < 2; ++hemi) {
-      const int j = hemi ? js : jn;
       L1[hemi] = L2[hemi] = make_double2(0.0, 0.0);
       if (atoms & SWX_TEND_LC) {
-        L1[hemi] = lc[(size_t)j * p.nm + m];
-        L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
+        L1[hemi] = LC(0, hemi, m);
+        L2[hemi] = LC(1, hemi, m);
       }
     }
     double2 ev[7], od[7];
@@ -615,9 +622,12 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     R1 = cta_fft(Pk, spare, N, 1, p.fft_radix, p.fft_npass, tw, false);
     R4 = r4;
   }
-  grid_fold(p, i, atoms, nl, lc, A, [&](int f, int k) {
-    return f < 4 ? R4[(size_t)f * N + k] : R1[k];
-  });
+  const int jn0 = p.d_jn[i], js0 = p.d_js[i];
+  grid_fold(
+      p, i, atoms, nl, A, [&](int f, int k) { return f < 4 ? R4[(size_t)f * N + k] : R1[k]; },
+      [&](int term, int hemi, int m) {
+        return lc[(size_t)term * p.nlat * p.nm + (size_t)(hemi ? js0 : jn0) * p.nm + m];
+      });
 }
 
 // Fused grid stage with register FFTs, for nlon_t = R1 * R2 (one CTA per
@@ -637,7 +647,9 @@ struct SqCfg {
   static constexpr int N = R1 * R2, RP = R1 + 1, FS = RP * R2;
   static constexpr int MT = (R1 > R2 ? R1 : R2);
   static constexpr int NT = ((5 * MT + 31) / 32) * 32;
-  static constexpr size_t SMEM = (size_t)5 * FS * sizeof(double2);
+  static constexpr int LCM = N / 3 + 1;  // >= T + 1 (N >= 3T + 1)
+  // 5 transform rows, the twiddle table W_N^t, the pair's Coriolis terms [2][2][LCM]
+  static constexpr size_t SMEM = (size_t)(5 * FS + N + 4 * LCM) * sizeof(double2);
 };
 
 template <int R1, int R2>
@@ -656,15 +668,31 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
   }
   const int T = p.trunc;
   const bool nl = (atoms & SWX_TEND_N) != 0;
+  const int jn = p.d_jn[i], js = p.d_js[i];
+  double2 *TW = F + 5 * FS;  // W_N^t
+  double2 *LCs = TW + N;     // [term][hemi][LCM]
+  // stage the twiddles and this pair's Coriolis terms asynchronously; they
+  // land while the first transform stage loads and computes
+  if (nl)
+    for (int t = threadIdx.x; t < N; t += blockDim.x) cp16(TW + t, tw_g + t);
+  if (atoms & SWX_TEND_LC)
+    for (int t = threadIdx.x; t < 4 * (T + 1); t += blockDim.x) {
+      const int q = t / (T + 1), m = t - q * (T + 1);  // q = term * 2 + hemi
+      const int j = (q & 1) ? js : jn;
+      cp16(LCs + q * C::LCM + m, lc + (size_t)(q >> 1) * p.nlat * p.nm + (size_t)j * p.nm + m);
+    }
+  cp_commit();
   if (nl) {
-    const int jn = p.d_jn[i], js = p.d_js[i];
     const size_t row = (size_t)p.nlat * p.nfreq_t;
     // inverse, column DFTs: input bin k = n1 + R1 n2 of u, v, vort, phi'
-    for (int t = threadIdx.x; t < 4 * R1; t += blockDim.x) {
-      const int f = t / R1, n1 = t - f * R1;
+    // (one task per thread: 4 R1 <= blockDim)
+    const int t = threadIdx.x;
+    const bool act = t < 4 * R1;
+    const int f = act ? t / R1 : 0, n1 = t - f * R1;
+    double2 v[R2];
+    if (act) {
       const double2 *Xn = c2r + f * row + (size_t)jn * p.nfreq_t;
       const double2 *Xs = c2r + f * row + (size_t)js * p.nfreq_t;
-      double2 v[R2];
 #pragma unroll
       for (int n2 = 0; n2 < R2; ++n2) {
         const int k = n1 + R1 * n2;
@@ -680,12 +708,16 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
         v[n2] = make_double2(a.x - b.y, a.y + b.x);  // X + i Y
       }
       regfft::Dft<R2, true>::run(v);
+    }
+    cp_wait_all();
+    __syncthreads();  // twiddles staged
+    if (act) {
       double2 *o = F + (size_t)f * FS + n1;
 #pragma unroll
       for (int k2 = 0; k2 < R2; ++k2) {
         double2 x = v[k2];
         if (k2 > 0) {
-          const double2 w = __ldg(tw_g + (n1 * k2) % N);  // conj for the inverse
+          const double2 w = TW[(n1 * k2) % N];  // conj for the inverse
           x = make_double2(x.x * w.x + x.y * w.y, x.y * w.x - x.x * w.y);
         }
         o[RP * k2] = x;
@@ -727,7 +759,7 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
       for (int c = 0; c < R1; ++c) {
         double2 x = v[c];
         if (c > 0 && a > 0) {
-          const double2 w = __ldg(tw_g + (a * c) % N);
+          const double2 w = TW[(a * c) % N];
           x = make_double2(x.x * w.x - x.y * w.y, x.x * w.y + x.y * w.x);
         }
         o[c] = x;
@@ -747,9 +779,11 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
     }
     __syncthreads();
   }
-  grid_fold(p, i, atoms, nl, lc, A, [&](int f, int k) {
-    return F[(size_t)f * FS + (k % R1) + RP * (k / R1)];
-  });
+  cp_wait_all();
+  __syncthreads();  // Coriolis terms staged (when no transform ran)
+  grid_fold(
+      p, i, atoms, nl, A, [&](int f, int k) { return F[(size_t)f * FS + (k % R1) + RP * (k / R1)]; },
+      [&](int term, int hemi, int m) { return LCs[(term * 2 + hemi) * C::LCM + m]; });
 }
 
 // plain analysis prep: nf (<= 4) grids already FFT'd into Q (pitch nfreq)
