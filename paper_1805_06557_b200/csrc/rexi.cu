@@ -201,11 +201,18 @@ __device__ __forceinline__ double2 axpy_out(const Axpy &ep, size_t i, double2 v)
 
 constexpr int kLgPasses = 4;  // 16-mode passes per CTA (factor staging amortised 4x)
 
-template <int NRHS, int LEAF>
+// SLPM > 0 (with SNB > 0): static geometry -- LPM lanes per mode, SNB leaf
+// blocks per lane -- so every pole's tree is fully unrolled (same pairwise
+// order as the binary counter) and the factor offsets are immediates.
+template <int NRHS, int LEAF, int SNB = 0, int SLPM = 0>
 __global__ void __launch_bounds__(128) rexi_lg_kernel(
-    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int np, int lpm,
-    int log2_lpm, int trunc, int ncoef, const int4 *__restrict__ sched, int realify, Axpy ep,
+    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int np_rt, int lpm_rt,
+    int log2_lpm_rt, int trunc, int ncoef, const int4 *__restrict__ sched, int realify, Axpy ep,
     double2 *__restrict__ out) {
+  constexpr bool kStatic = SNB > 0 && SLPM > 0;
+  const int lpm = kStatic ? SLPM : lpm_rt;
+  const int np = kStatic ? SLPM * LEAF * SNB : np_rt;
+  const int log2_lpm = kStatic ? (SLPM == 4 ? 2 : SLPM == 8 ? 3 : SLPM == 16 ? 4 : 5) : log2_lpm_rt;
   extern __shared__ double2 fac[];  // [NRHS][4][np], already interleaved (t*LPM + q)
   const int4 w = sched[blockIdx.x];
   const int l = w.x, m0 = w.y, m1 = w.z;
@@ -234,8 +241,15 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
         bz = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
         bd = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
       }
-      PhiDiv pd = pole_tree_pd<LEAF>(F, F + np, F + 2 * np, nb, lpm, bp, bd);
-      double2 z = pole_tree_z<LEAF>(F + 3 * np, nb, lpm, bz);
+      PhiDiv pd;
+      double2 z;
+      if constexpr (kStatic) {
+        pd = tree_pd<LEAF * SNB>(F, F + np, F + 2 * np, 0, SLPM, bp, bd);
+        z = tree_z<LEAF * SNB>(F + 3 * np, 0, SLPM, bz);
+      } else {
+        pd = pole_tree_pd<LEAF>(F, F + np, F + 2 * np, nb, lpm, bp, bd);
+        z = pole_tree_z<LEAF>(F + 3 * np, nb, lpm, bz);
+      }
       for (int o = 1; o < lpm; o <<= 1) {
         pd.p = cadd(pd.p, shfl_xor2(pd.p, o));
         pd.d = cadd(pd.d, shfl_xor2(pd.d, o));
@@ -968,6 +982,18 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
     k<<<n_cta, 128, smem, st>>>(rhs, fac, g.np, g.lpm, g.log2_lpm, s->trunc, s->ncoef, sched,  \
                                 realify, ep, out);                                             \
     break;                                                                                     \
+  }
+  // static geometries of the common pole counts (128 / 256 / 512 poles, 8 lanes per mode)
+  if (g.lpm == 8 && g.leaf == 8 && (g.ppl == 16 || g.ppl == 32 || g.ppl == 64)) {
+    auto k = g.ppl == 16   ? rexi_lg_kernel<NRHS, 8, 2, 8>
+             : g.ppl == 32 ? rexi_lg_kernel<NRHS, 8, 4, 8>
+                           : rexi_lg_kernel<NRHS, 8, 8, 8>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<n_cta, 128, smem, st>>>(rhs, fac, g.np, g.lpm, g.log2_lpm, s->trunc, s->ncoef, sched,
+                                realify, ep, out);
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
   }
   switch (g.leaf) {
     SWX_LG_CASE(1)
