@@ -88,6 +88,49 @@ __device__ __forceinline__ double2 tree_z(const double2 *__restrict__ D, int t0,
   }
 }
 
+// the same trees for MPL modes of one degree at once: every factor load is
+// shared by the MPL modes (per-mode pairwise order unchanged)
+template <int NP, int MPL>
+__device__ __forceinline__ void tree_pd_m(const double2 *__restrict__ A,
+                                          const double2 *__restrict__ B,
+                                          const double2 *__restrict__ C, int t0, int st,
+                                          const double2 (&bp)[MPL], const double2 (&bd)[MPL],
+                                          PhiDiv (&o)[MPL]) {
+  if constexpr (NP == 1) {
+    const double2 fa = A[t0], fb = B[t0], fc = C[t0];
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) {
+      o[j].p = cfma(fa, bp[j], cmul(fb, bd[j]));
+      o[j].d = cfma(fc, bp[j], cmul(fa, bd[j]));
+    }
+  } else {
+    PhiDiv y[MPL];
+    tree_pd_m<NP / 2, MPL>(A, B, C, t0, st, bp, bd, o);
+    tree_pd_m<NP / 2, MPL>(A, B, C, t0 + (NP / 2) * st, st, bp, bd, y);
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) {
+      o[j].p = cadd(o[j].p, y[j].p);
+      o[j].d = cadd(o[j].d, y[j].d);
+    }
+  }
+}
+
+template <int NP, int MPL>
+__device__ __forceinline__ void tree_z_m(const double2 *__restrict__ D, int t0, int st,
+                                         const double2 (&bz)[MPL], double2 (&o)[MPL]) {
+  if constexpr (NP == 1) {
+    const double2 fd = D[t0];
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) o[j] = cmul(fd, bz[j]);
+  } else {
+    double2 y[MPL];
+    tree_z_m<NP / 2, MPL>(D, t0, st, bz, o);
+    tree_z_m<NP / 2, MPL>(D, t0 + (NP / 2) * st, st, bz, y);
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) o[j] = cadd(o[j], y[j]);
+  }
+}
+
 constexpr int kLgLevels = 4;  // up to 16 leaf blocks per lane
 
 // Perfect tree over NB (power of two) consecutive leaf subtrees of LEAF
@@ -262,6 +305,82 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
         out[o + ncoef] = axpy_out(ep, o + ncoef, z);
         out[o + 2 * (size_t)ncoef] = axpy_out(ep, o + 2 * (size_t)ncoef, pd.d);
       }
+    }
+  }
+}
+
+// Static-geometry variant with MPL modes per lane group: LPM lanes own MPL
+// modes of the same degree (m = base + g, base + g + 128/LPM, ...), so each
+// factor load from shared memory feeds MPL modes.
+template <int NRHS, int NP, int LPM, int MPL>
+__global__ void __launch_bounds__(128) rexi_lg_mm_kernel(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
+    const int4 *__restrict__ sched, int realify, Axpy ep, double2 *__restrict__ out) {
+  constexpr int PPL = NP / LPM;          // poles per lane
+  constexpr int GROUPS = 128 / LPM;      // lane groups per CTA
+  extern __shared__ double2 fac[];       // [NRHS][4][NP], interleaved (t*LPM + q)
+  const int4 w = sched[blockIdx.x];
+  const int l = w.x, m0 = w.y, m1 = w.z;
+  {
+    const double4 *src = reinterpret_cast<const double4 *>(fac_g + (size_t)l * NRHS * 4 * NP);
+    double4 *dst = reinterpret_cast<double4 *>(fac);
+    for (int i = threadIdx.x; i < NRHS * 2 * NP; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int q = threadIdx.x & (LPM - 1);
+  const int g = threadIdx.x / LPM;
+  for (int base = m0; base < m1; base += GROUPS * MPL) {
+    int m[MPL];
+    bool has[MPL];
+    size_t idx[MPL];
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) {
+      m[j] = base + g + j * GROUPS;
+      has[j] = m[j] < m1;
+      idx[j] = has[j] ? (size_t)col_offset(trunc, m[j]) + (l - m[j]) : 0;
+    }
+#pragma unroll 1
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 *F = fac + (size_t)r * 4 * NP + q;
+      double2 bp[MPL], bz[MPL], bd[MPL], e[MPL][3];
+#pragma unroll
+      for (int j = 0; j < MPL; ++j) {
+        bp[j] = bz[j] = bd[j] = make_double2(0.0, 0.0);
+        if (has[j]) {
+          bp[j] = rhs[(size_t)(r * 3 + 0) * ncoef + idx[j]];
+          bz[j] = rhs[(size_t)(r * 3 + 1) * ncoef + idx[j]];
+          bd[j] = rhs[(size_t)(r * 3 + 2) * ncoef + idx[j]];
+        }
+        // the fused update's base values, fetched under the pole sums
+        if (ep.base && has[j] && q == 0)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) e[j][c] = ep.base[(size_t)(r * 3 + c) * ncoef + idx[j]];
+      }
+      PhiDiv pd[MPL];
+      double2 z[MPL];
+      tree_pd_m<PPL, MPL>(F, F + NP, F + 2 * NP, 0, LPM, bp, bd, pd);
+      tree_z_m<PPL, MPL>(F + 3 * NP, 0, LPM, bz, z);
+#pragma unroll
+      for (int o = 1; o < LPM; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < MPL; ++j) {
+          pd[j].p = cadd(pd[j].p, shfl_xor2(pd[j].p, o));
+          pd[j].d = cadd(pd[j].d, shfl_xor2(pd[j].d, o));
+          z[j] = cadd(z[j], shfl_xor2(z[j], o));
+        }
+#pragma unroll
+      for (int j = 0; j < MPL; ++j)
+        if (has[j] && q == 0) {
+          if (realify && m[j] == 0) pd[j].p.y = z[j].y = pd[j].d.y = 0.0;
+          const size_t o = (size_t)r * 3 * ncoef + idx[j];
+          double2 v[3] = {pd[j].p, z[j], pd[j].d};
+          if (ep.base)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              v[c] = make_double2(e[j][c].x + v[c].x * ep.scale, e[j][c].y + v[c].y * ep.scale);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) out[o + (size_t)c * ncoef] = v[c];
+        }
     }
   }
 }
@@ -984,6 +1103,15 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
     break;                                                                                     \
   }
   // static geometries of the common pole counts (128 / 256 / 512 poles, 8 lanes per mode)
+  static const int env_mpl = getenv("SWX_LG_MPL") ? atoi(getenv("SWX_LG_MPL")) : 2;
+  if (g.lpm == 8 && g.ppl == 32 && env_mpl == 2) {
+    auto k = rexi_lg_mm_kernel<NRHS, 256, 8, 2>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<n_cta, 128, smem, st>>>(rhs, fac, s->trunc, s->ncoef, sched, realify, ep, out);
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
   if (g.lpm == 8 && g.leaf == 8 && (g.ppl == 16 || g.ppl == 32 || g.ppl == 64)) {
     auto k = g.ppl == 16   ? rexi_lg_kernel<NRHS, 8, 2, 8>
              : g.ppl == 32 ? rexi_lg_kernel<NRHS, 8, 4, 8>

@@ -45,8 +45,10 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
 __device__ __forceinline__ double2 csub(double2 a, double2 b) {
   return make_double2(a.x - b.x, a.y - b.y);
 }
+// explicit rounding (no compiler-chosen contraction): every kernel that
+// multiplies the same operands gets the same bits
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return make_double2(fma(a.x, b.x, -__dmul_rn(a.y, b.y)), fma(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 __device__ __forceinline__ double2 cscale(double s, double2 a) {
   return make_double2(s * a.x, s * a.y);
