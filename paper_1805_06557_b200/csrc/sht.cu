@@ -1764,9 +1764,29 @@ static size_t synth_smem(int ns, int nh, int split, int nt) {
   return std::max(stage, red);
 }
 
+// state-synthesis geometry (tuning overrides SWX_SYNTH_NT / SWX_SYNTH_SPLIT):
+// pairs per CTA half and whether long columns are split over two halves
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
+  static const int st_nt = env_int("SWX_SYNTH_NT", 0), st_split = env_int("SWX_SYNTH_SPLIT", 0);
+  if (MODE == 0 && p->d_ckpt && st_nt > 0) {
+    nt = st_nt;
+    g.y = (p->nh + nt - 1) / nt;
+    const int sp = st_split ? 2 : 1;
+    const size_t smem = synth_smem(ns, nh, sp, nt);
+    auto k = sp == 2 ? synth_kernel<MODE, 2> : synth_kernel<MODE, 1>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<g, sp * nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
   // split long columns over two half-blocks (plain synthesis only: for the
   // 7-series state variant the 448-thread CTAs fit one per SM and lose more
   // to waves than they gain on the critical path)
