@@ -118,7 +118,8 @@ constexpr int kSL = 128;  // l rows staged per chunk
 // checkpoint, halving the per-thread walk of the long columns; the halves'
 // partial sums are added in a fixed order (first + second).
 template <int MODE, int SPLIT>
-__global__ void __launch_bounds__(512) synth_kernel(ShtView p, SynthArgs a) {
+__global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_kernel(ShtView p,
+                                                                                  SynthArgs a) {
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
   constexpr int NACC = 4 * (NS + NH);
@@ -166,62 +167,75 @@ __global__ void __launch_bounds__(512) synth_kernel(ShtView p, SynthArgs a) {
   }
   const int nchunk0 = (split + kSL - 1) / kSL, nchunk1 = (kmax - split + kSL - 1) / kSL;
   const int nchunk = SPLIT == 2 ? max(nchunk0, nchunk1) : nchunk0;
+  // recurrence constants split for two 16-byte loads per degree:
+  // rcA[t] = {e_{l-1}, 1/e_l} (recurrence), rcB[t] = {(l+1)e_l, l e_{l+1}} (H)
+  double2 *rcA = reinterpret_cast<double2 *>(rcs), *rcB = rcA + (kSL + 2);
   for (int ch = 0; ch < nchunk; ++ch) {
     const int k0 = kb + ch * kSL;  // chunk start (even)
     const int n = max(0, min(kSL, ke - k0));
     __syncthreads();
+    // past the column end the constants and coefficients are zero, so the
+    // walk needs no bounds checks (the recurrence then produces zeros)
     for (int t = tt0; t < kSL + 2; t += NT) {
       const int k = k0 + t;
-      if (n > 0 && k <= kmax) rcs[t] = rc[k];
+      double4 c = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (n > 0 && k <= kmax) c = rc[k];
+      rcA[t] = make_double2(c.x, c.y);
+      rcB[t] = make_double2(c.z, c.w);
     }
-    for (int t = tt0; t < n; t += NT) {
+    for (int t = tt0; t < ((n + 1) & ~1); t += NT) {
       const int s = off + k0 + t;
+      const bool in = t < n;
       if (MODE == 0) {
-        const double il = p.d_lconst[m + k0 + t];
-        const double2 z = a.coef[nc + s], d = a.coef[2 * nc + s];
+        const double il = in ? p.d_lconst[m + k0 + t] : 0.0;
+        const double2 z = in ? a.coef[nc + s] : make_double2(0.0, 0.0);
+        const double2 d = in ? a.coef[2 * nc + s] : make_double2(0.0, 0.0);
         cs[0 * kSL + t] = z;
         cs[(NS > 1 ? 1 : 0) * kSL + t] = d;
-        cs[(NS > 2 ? 2 : 0) * kSL + t] = a.coef[s];
+        cs[(NS > 2 ? 2 : 0) * kSL + t] = in ? a.coef[s] : make_double2(0.0, 0.0);
         cs[(NS > 3 ? 3 : 0) * kSL + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
         cs[(NS > 4 ? 4 : 0) * kSL + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
       } else {
-        cs[t] = a.coef[(size_t)field * nc + s];
+        cs[t] = in ? a.coef[(size_t)field * nc + s] : make_double2(0.0, 0.0);
       }
     }
     __syncthreads();
+    // two degrees per iteration (static parity q = 0, 1: l - m = k0 + tt)
+    // entering: pm1 = P_{k-1}, p0 = P_k, p1 = P_{k+1}
     for (int t = 0; t < n; t += 2) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {  // static parity: l - m = k0 + t + q, k0 even
-        if (q == 1 && t + 1 >= n) break;
-        const int tt = t + q;
-        const int k = k0 + tt;
-        const double P = p0;
-        double H = 0.0;
-        if (NH > 0) {
-          const double4 c = rcs[tt];
-          H = (c.z * pm1 - c.w * p1) * rcos;
-        }
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          const double2 v = cs[s * kSL + tt];
-          sp[q][s].x = fma(P, v.x, sp[q][s].x);
-          sp[q][s].y = fma(P, v.y, sp[q][s].y);
-        }
-#pragma unroll
-        for (int s = 0; s < NH; ++s) {
-          const double2 v = cs[(NS > 3 ? 3 + s : 0) * kSL + tt];
-          sh[q][s].x = fma(H, v.x, sh[q][s].x);
-          sh[q][s].y = fma(H, v.y, sh[q][s].y);
-        }
-        double p2 = 0.0;
-        if (k + 2 <= kmax) {
-          const double4 c2 = rcs[tt + 2];
-          p2 = fma(x, p1, -c2.x * p0) * c2.y;  // sphere.py:98-100
-        }
-        pm1 = p0;
-        p0 = p1;
-        p1 = p2;
+      double H0 = 0.0, H1 = 0.0;
+      if (NH > 0) {
+        const double2 c0 = rcB[t];
+        H0 = (c0.x * pm1 - c0.y * p1) * rcos;
       }
+      const double2 r2 = rcA[t + 2];
+      const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
+      if (NH > 0) {
+        const double2 c1 = rcB[t + 1];
+        H1 = (c1.x * p0 - c1.y * p2) * rcos;
+      }
+      const double2 r3 = rcA[t + 3];
+      const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) {
+        const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
+        sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
+        sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
+        sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
+        sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < NH; ++s2) {
+        const double2 v0 = cs[(NS > 3 ? 3 + s2 : 0) * kSL + t];
+        const double2 v1 = cs[(NS > 3 ? 3 + s2 : 0) * kSL + t + 1];
+        sh[0][s2].x = fma(H0, v0.x, sh[0][s2].x);
+        sh[0][s2].y = fma(H0, v0.y, sh[0][s2].y);
+        sh[1][s2].x = fma(H1, v1.x, sh[1][s2].x);
+        sh[1][s2].y = fma(H1, v1.y, sh[1][s2].y);
+      }
+      pm1 = p1;
+      p0 = p2;
+      p1 = p3;
     }
   }
   if (SPLIT == 2) {
@@ -1778,7 +1792,8 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
   if (MODE == 0 && p->d_ckpt && st_nt > 0) {
     nt = st_nt;
     g.y = (p->nh + nt - 1) / nt;
-    const int sp = st_split ? 2 : 1;
+    const int sp = st_split && 2 * nt <= 512 ? 2 : 1;
+    if (sp == 1 && nt > 256) return fail(SWX_ERR_CONFIG, "SWX_SYNTH_NT > 256");
     const size_t smem = synth_smem(ns, nh, sp, nt);
     auto k = sp == 2 ? synth_kernel<MODE, 2> : synth_kernel<MODE, 1>;
     if (smem > 48 * 1024)
