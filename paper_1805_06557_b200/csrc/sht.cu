@@ -112,6 +112,56 @@ constexpr int kSeg = 64;   // degrees per analysis segment
 
 constexpr int kSL = 128;  // l rows staged per chunk
 
+// Fourier rows of the state synthesis for column m, latitude pair (jn, js),
+// from the even/odd partial sums: sp[q] = (vort, div, phi', psi, chi),
+// sh[q] = (dpsi/dlat, dchi/dlat) with q the parity of l - m
+// fr[hemi] = (f, df/dlat) of the pair's two latitudes
+__device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a, int m, int jn,
+                                           int js, double rcos, const double2 (&sp)[2][5],
+                                           const double2 (&sh)[2][2], const double2 (&fr)[2]) {
+  constexpr int NS = 5, NH = 2;
+  const int nf = a.nfreq;
+  const size_t row = (size_t)p.nlat * nf;
+  const double ra = 1.0 / p.radius;
+  const double fm = (double)m;
+#pragma unroll
+  for (int hemi = 0; hemi < 2; ++hemi) {
+    if (hemi == 1 && js == jn) break;
+    const int j = hemi ? js : jn;
+    const double sg = hemi ? -1.0 : 1.0;  // sign of the odd-parity part
+    double2 G[5], GH[2];
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int ss = s < NS ? s : 0;
+      G[s] = make_double2(sp[0][ss].x + sg * sp[1][ss].x, sp[0][ss].y + sg * sp[1][ss].y);
+    }
+    // H has opposite parity: south = -even + odd
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int ss = NH > 0 ? (s < NH ? s : 0) : 0;
+      GH[s] = make_double2(sg * sh[0][ss].x + sh[1][ss].x, sg * sh[0][ss].y + sh[1][ss].y);
+    }
+    // u = (dchi/dlon sec - dpsi/dlat)/a, v = (dpsi/dlon sec + dchi/dlat)/a,
+    // d/dlon = i m (sphere.py:393-402)
+    double2 u = make_double2((-fm * G[4].y * rcos - GH[0].x) * ra, (fm * G[4].x * rcos - GH[0].y) * ra);
+    double2 v = make_double2((-fm * G[3].y * rcos + GH[1].x) * ra, (fm * G[3].x * rcos + GH[1].y) * ra);
+    double2 gz = G[0], gp = G[2], gd = G[1];
+    if (m == 0) u.y = v.y = gz.y = gp.y = gd.y = 0.0;
+    a.c2r[0 * row + (size_t)j * nf + m] = u;
+    a.c2r[1 * row + (size_t)j * nf + m] = v;
+    a.c2r[2 * row + (size_t)j * nf + m] = gz;
+    a.c2r[3 * row + (size_t)j * nf + m] = gp;
+    if (a.want_lc) {
+      const double f = fr[hemi].x, fp = fr[hemi].y;
+      const double sc = p.fscale;  // nlon * dlon: fft(irfft(G) * nlon) * dlon
+      const double2 l1 = make_double2(sc * (-f * gd.x - fp * v.x), sc * (-f * gd.y - fp * v.y));
+      const double2 l2 = make_double2(sc * (f * gz.x - fp * u.x), sc * (f * gz.y - fp * u.y));
+      a.lc[(size_t)j * p.nm + m] = l1;
+      a.lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m] = l2;
+    }
+  }
+}
+
 // SPLIT = 2: the CTA holds two half-blocks of NT = blockDim/2 threads (one
 // per latitude pair each); for columns longer than 96 degrees the second
 // half starts mid-column (a multiple of kSeg) from the plan-time recurrence
@@ -286,44 +336,137 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
     if (js != jn) a.c2r[field * row + (size_t)js * nf + m] = gs;
     return;
   }
-  const double ra = 1.0 / p.radius;
-  const double fm = (double)m;
-#pragma unroll
-  for (int hemi = 0; hemi < 2; ++hemi) {
-    if (hemi == 1 && js == jn) break;
-    const int j = hemi ? js : jn;
-    const double sg = hemi ? -1.0 : 1.0;  // sign of the odd-parity part
-    double2 G[5], GH[2];
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-      const int ss = s < NS ? s : 0;
-      G[s] = make_double2(sp[0][ss].x + sg * sp[1][ss].x, sp[0][ss].y + sg * sp[1][ss].y);
-    }
-    // H has opposite parity: south = -even + odd
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int ss = NH > 0 ? (s < NH ? s : 0) : 0;
-      GH[s] = make_double2(sg * sh[0][ss].x + sh[1][ss].x, sg * sh[0][ss].y + sh[1][ss].y);
-    }
-    // u = (dchi/dlon sec - dpsi/dlat)/a, v = (dpsi/dlon sec + dchi/dlat)/a,
-    // d/dlon = i m (sphere.py:393-402)
-    double2 u = make_double2((-fm * G[4].y * rcos - GH[0].x) * ra, (fm * G[4].x * rcos - GH[0].y) * ra);
-    double2 v = make_double2((-fm * G[3].y * rcos + GH[1].x) * ra, (fm * G[3].x * rcos + GH[1].y) * ra);
-    double2 gz = G[0], gp = G[2], gd = G[1];
-    if (m == 0) u.y = v.y = gz.y = gp.y = gd.y = 0.0;
-    a.c2r[0 * row + (size_t)j * nf + m] = u;
-    a.c2r[1 * row + (size_t)j * nf + m] = v;
-    a.c2r[2 * row + (size_t)j * nf + m] = gz;
-    a.c2r[3 * row + (size_t)j * nf + m] = gp;
+  if constexpr (MODE == 0) {
+    const double2 fr[2] = {make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]),
+                           make_double2(p.d_frow[js], p.d_frow[p.nlat + js])};
+    state_rows(p, a, m, jn, js, rcos, sp, sh, fr);
+  }
+}
+
+// State synthesis with the whole column staged once (T small enough):
+// CTA = (m, block of latitude pairs), one thread per pair walking l = m..T+1.
+// The dP/dlat series are summed by parts,
+//   sum_k H_k v_k = rcos sum_j P_j (c_{j+1}.z v_{j+1} - c_{j-1}.w v_{j-1}),
+// (H_k = (c_k.z P_{k-1} - c_k.w P_{k+1}) rcos, sphere.py:102-111), so the
+// psi/chi derivative series become two more P series with per-column
+// coefficients w_j staged with the others: 7 complex series of P and the
+// recurrence per degree, no per-pair H arithmetic.  P_j of parity q feeds the
+// H parity 1 - q.
+constexpr int kSCS = 7;  // staged series: vort, div, phi', psi, chi, w_psi, w_chi
+
+__host__ __device__ inline int synth_col_kp(int trunc, int m) {
+  return ((trunc + 3 - m) + 1) & ~1;  // degrees j = 0..kmax (kmax = T+1-m), padded even
+}
+
+// paired = 1: CTA j runs columns j and T - j (equal work per CTA)
+__global__ void __launch_bounds__(256) synth_col_kernel(ShtView p, SynthArgs a, int paired) {
+  extern __shared__ __align__(16) double2 scs[];
+  const int ncol = paired && blockIdx.x != p.trunc - blockIdx.x ? 2 : 1;
+  for (int cc = 0; cc < ncol; ++cc) {
+  const int m = cc == 0 ? blockIdx.x : p.trunc - blockIdx.x;
+  if (cc > 0) __syncthreads();  // staging area reuse
+  const int T = p.trunc, nc = p.ncoef;
+  const int kmax = T + 1 - m;
+  const int KP = synth_col_kp(T, m);           // staged degrees (>= kmax + 1, even)
+  const int KS = synth_col_kp(T, 0) + 2;       // series stride (all columns)
+  double2 *cs = scs;                            // [kSCS][KS]
+  double2 *rcA = scs + kSCS * KS;               // [KS] {e_{l-1}, 1/e_l}
+  double2 *rzw = rcA + KS;                      // [KS] {(l+1)e_l, l e_{l+1}}
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  const bool has = i < p.nh;
+  // per-pair values first: their latency overlaps the staging
+  double x = 0.0, rcos = 0.0, seed = 0.0;
+  int jn = 0, js = 0;
+  double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  if (has) {
+    x = p.d_x[i];
+    rcos = p.d_rcos[i];
+    seed = p.d_seed[(size_t)m * p.nh + i];
+    jn = p.d_jn[i];
+    js = p.d_js[i];
     if (a.want_lc) {
-      const double f = p.d_frow[j], fp = p.d_frow[p.nlat + j];
-      const double sc = p.fscale;  // nlon * dlon: fft(irfft(G) * nlon) * dlon
-      const double2 l1 = make_double2(sc * (-f * gd.x - fp * v.x), sc * (-f * gd.y - fp * v.y));
-      const double2 l2 = make_double2(sc * (f * gz.x - fp * u.x), sc * (f * gz.y - fp * u.y));
-      a.lc[(size_t)j * p.nm + m] = l1;
-      a.lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m] = l2;
+      fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
+      fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
     }
   }
+  const int off = col_offset(T, m);
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  for (int t = threadIdx.x; t < KP + 2; t += blockDim.x) {
+    double4 c = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (t <= kmax) c = rc[t];
+    rcA[t] = make_double2(c.x, c.y);
+    rzw[t] = make_double2(c.z, c.w);
+    if (t < KP) {
+      const bool in = t < kmax;
+      const int s = off + t;
+      const double il = in ? p.d_lconst[m + t] : 0.0;
+      const double2 z = in ? a.coef[nc + s] : make_double2(0.0, 0.0);
+      const double2 d = in ? a.coef[2 * nc + s] : make_double2(0.0, 0.0);
+      cs[0 * KS + t] = z;
+      cs[1 * KS + t] = d;
+      cs[2 * KS + t] = in ? a.coef[s] : make_double2(0.0, 0.0);
+      cs[3 * KS + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
+      cs[4 * KS + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < KP; t += blockDim.x) {
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const double2 *v = cs + (3 + s2) * KS;
+      const double2 up = t + 1 < KP ? v[t + 1] : make_double2(0.0, 0.0);
+      const double2 dn = t > 0 ? v[t - 1] : make_double2(0.0, 0.0);
+      const double cz = t + 1 < KP + 2 ? rzw[t + 1].x : 0.0;
+      const double cw = t > 0 ? rzw[t - 1].y : 0.0;
+      cs[(5 + s2) * KS + t] = make_double2(cz * up.x - cw * dn.x, cz * up.y - cw * dn.y);
+    }
+  }
+  __syncthreads();
+  if (has) {
+  double p0 = seed, p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
+  double2 sp[2][5], sw[2][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) sp[q][s2] = make_double2(0.0, 0.0);
+    sw[q][0] = sw[q][1] = make_double2(0.0, 0.0);
+  }
+  for (int t = 0; t < KP; t += 2) {
+    const double2 r2 = rcA[t + 2], r3 = rcA[t + 3];
+    const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
+    const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) {
+      const double2 v0 = cs[s2 * KS + t], v1 = cs[s2 * KS + t + 1];
+      sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
+      sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
+      sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
+      sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const double2 w0 = cs[(5 + s2) * KS + t], w1 = cs[(5 + s2) * KS + t + 1];
+      sw[1][s2].x = fma(p0, w0.x, sw[1][s2].x);
+      sw[1][s2].y = fma(p0, w0.y, sw[1][s2].y);
+      sw[0][s2].x = fma(p1, w1.x, sw[0][s2].x);
+      sw[0][s2].y = fma(p1, w1.y, sw[0][s2].y);
+    }
+    p0 = p2;
+    p1 = p3;
+  }
+  double2 sh[2][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) sh[q][s2] = make_double2(sw[q][s2].x * rcos, sw[q][s2].y * rcos);
+  state_rows(p, a, m, jn, js, rcos, sp, sh, fr);
+  }
+  }
+}
+
+static size_t synth_col_smem(int trunc) {
+  const int KS = synth_col_kp(trunc, 0) + 2;
+  return (size_t)(kSCS + 2) * KS * sizeof(double2);
 }
 
 // zero the C2R rows above m = T (cuFFT may overwrite its input)
@@ -1789,6 +1932,20 @@ template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
   static const int st_nt = env_int("SWX_SYNTH_NT", 0), st_split = env_int("SWX_SYNTH_SPLIT", 0);
+  static const int st_col = env_int("SWX_SYNTH_COL", 0);
+  if (MODE == 0 && st_col && synth_col_smem(p->trunc) <= 64 * 1024) {
+    const int ntc = st_nt > 0 ? st_nt : nt;
+    g.y = (p->nh + ntc - 1) / ntc;
+    const size_t smem = synth_col_smem(p->trunc);
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(synth_col_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int paired = st_col == 2 ? 1 : 0;
+    if (paired) g.x = p->trunc / 2 + 1;
+    synth_col_kernel<<<g, ntc, smem, s>>>(static_cast<const ShtView &>(*p), a, paired);
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
   if (MODE == 0 && p->d_ckpt && st_nt > 0) {
     nt = st_nt;
     g.y = (p->nh + nt - 1) / nt;
