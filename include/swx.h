@@ -185,6 +185,10 @@ int swx_sht_tendency_profile(swx_sht p, int atoms, const swx_c128 *d_state,
  * DFMA chains each (2 flops per DFMA); d_sink receives one double per thread
  * so nothing is optimised away.  Used for the FP64 roofline denominator.   */
 int swx_fp64_fma_probe(double *d_sink, int n_blocks, int iters, void *stream);
+/* Per-CTA phase trace of the instrumented transform kernels (state synthesis,
+ * square fused grid stage): enable 1/0 (-1: unchanged); when h_out is
+ * non-null, copies n_ctas records of 8 u64 {smid, globaltimer marks (ns)}.  */
+int swx_trace(int enable, unsigned long long *h_out, int n_ctas);
 
 #ifdef __cplusplus
 }

@@ -106,7 +106,21 @@ struct SynthArgs {
   double2 *lc;          // [2][nlat][nm]: fft*dlon of -f div - f' v, f vort - f' u
   int want_lc;
   int nfreq;
+  // zpack: the fused grid stage's input format instead of C2R rows: per
+  // latitude pair i, field f (u, v, vort, phi'), bins m = 0..T:
+  //   c2r[((i * 4 + f) * 2 + 0) * (T+1) + m] = X_n(m) + i X_s(m)
+  //   c2r[((i * 4 + f) * 2 + 1) * (T+1) + m] = conj(X_n(m)) + i conj(X_s(m))
+  // (X_s = X_n on the equator node), i.e. the packed row z = north + i south
+  // at bin m and at bin N - m.
+  int zpack = 0;
 };
+
+// bin k of the packed complex row z = north + i south of field f (zero above T)
+__device__ __forceinline__ double2 zrow_bin(const double2 *zf, int k, int T, int N) {
+  const bool lo = k <= T, hi = !lo && N - k <= T;
+  const double2 v = zf[(hi ? (T + 1) : 0) + (lo ? k : (hi ? N - k : 0))];
+  return (lo || hi) ? v : make_double2(0.0, 0.0);
+}
 
 constexpr int kSeg = 64;   // degrees per analysis segment
 
@@ -116,9 +130,11 @@ constexpr int kSL = 128;  // l rows staged per chunk
 // from the even/odd partial sums: sp[q] = (vort, div, phi', psi, chi),
 // sh[q] = (dpsi/dlat, dchi/dlat) with q the parity of l - m
 // fr[hemi] = (f, df/dlat) of the pair's two latitudes
-__device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a, int m, int jn,
-                                           int js, double rcos, const double2 (&sp)[2][5],
+__device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a, int m, int i,
+                                           int jn, int js, double rcos, const double2 (&sp)[2][5],
                                            const double2 (&sh)[2][2], const double2 (&fr)[2]) {
+  double2 X[2][4];  // zpack: per hemisphere u, v, vort, phi'
+
   constexpr int NS = 5, NH = 2;
   const int nf = a.nfreq;
   const size_t row = (size_t)p.nlat * nf;
@@ -147,10 +163,21 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
     double2 v = make_double2((-fm * G[3].y * rcos + GH[1].x) * ra, (fm * G[3].x * rcos + GH[1].y) * ra);
     double2 gz = G[0], gp = G[2], gd = G[1];
     if (m == 0) u.y = v.y = gz.y = gp.y = gd.y = 0.0;
-    a.c2r[0 * row + (size_t)j * nf + m] = u;
-    a.c2r[1 * row + (size_t)j * nf + m] = v;
-    a.c2r[2 * row + (size_t)j * nf + m] = gz;
-    a.c2r[3 * row + (size_t)j * nf + m] = gp;
+    if (a.zpack) {
+      X[hemi][0] = u;
+      X[hemi][1] = v;
+      X[hemi][2] = gz;
+      X[hemi][3] = gp;
+      if (js == jn) {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) X[1][f] = X[0][f];
+      }
+    } else {
+      a.c2r[0 * row + (size_t)j * nf + m] = u;
+      a.c2r[1 * row + (size_t)j * nf + m] = v;
+      a.c2r[2 * row + (size_t)j * nf + m] = gz;
+      a.c2r[3 * row + (size_t)j * nf + m] = gp;
+    }
     if (a.want_lc) {
       const double f = fr[hemi].x, fp = fr[hemi].y;
       const double sc = p.fscale;  // nlon * dlon: fft(irfft(G) * nlon) * dlon
@@ -158,6 +185,16 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
       const double2 l2 = make_double2(sc * (f * gz.x - fp * u.x), sc * (f * gz.y - fp * u.y));
       a.lc[(size_t)j * p.nm + m] = l1;
       a.lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m] = l2;
+    }
+  }
+  if (a.zpack) {
+    const int T1 = p.trunc + 1;
+    double2 *z = a.c2r + (size_t)i * 8 * T1 + m;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double2 n = X[0][f], s = X[1][f];
+      z[(f * 2 + 0) * T1] = make_double2(n.x - s.y, n.y + s.x);   // X_n + i X_s
+      z[(f * 2 + 1) * T1] = make_double2(n.x + s.y, -n.y + s.x);  // conj(X_n) + i conj(X_s)
     }
   }
 }
@@ -182,6 +219,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
   const int m = blockIdx.x;
   const int i = blockIdx.y * NT + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
+  if (MODE == 0) trace_mark(0);
   const int T = p.trunc, nc = p.ncoef;
   const int off = col_offset(T, m);
   const int kmax = T + 1 - m;
@@ -337,9 +375,11 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
     return;
   }
   if constexpr (MODE == 0) {
+    trace_mark(1);
     const double2 fr[2] = {make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]),
                            make_double2(p.d_frow[js], p.d_frow[p.nlat + js])};
-    state_rows(p, a, m, jn, js, rcos, sp, sh, fr);
+    state_rows(p, a, m, i, jn, js, rcos, sp, sh, fr);
+    trace_mark(2);
   }
 }
 
@@ -459,7 +499,7 @@ __global__ void __launch_bounds__(256) synth_col_kernel(ShtView p, SynthArgs a, 
   for (int q = 0; q < 2; ++q)
 #pragma unroll
     for (int s2 = 0; s2 < 2; ++s2) sh[q][s2] = make_double2(sw[q][s2].x * rcos, sw[q][s2].y * rcos);
-  state_rows(p, a, m, jn, js, rcos, sp, sh, fr);
+  state_rows(p, a, m, i, jn, js, rcos, sp, sh, fr);
   }
   }
 }
@@ -522,18 +562,32 @@ __device__ __forceinline__ void put_row_t(double *dst, const double2 *v, int nv,
 // vort v, KE), L1/L2[hemi] the Fourier-space Coriolis terms.
 // hcos: fold 1/cos of the pair into the H-table rows (table analysis forms H
 // without the 1/cos factor)
+// constants of one latitude pair used by the fold (loaded once per pair)
+struct PairK {
+  bool eq;       // equator node of an odd grid (js == jn)
+  double rcos;   // 1 / cos(lat)
+  double w[2];   // quadrature weights, north / south
+};
+__device__ __forceinline__ PairK pair_k(const ShtView &p, int i) {
+  PairK k;
+  k.eq = p.d_js[i] == p.d_jn[i];
+  k.rcos = p.d_rcos[i];
+  k.w[0] = p.d_wn[i];
+  k.w[1] = p.d_ws[i];
+  return k;
+}
+
 template <bool HCOS>
 __device__ __forceinline__ void tend_fold(const ShtView &p, const double2 (&F)[2][5],
                                           const double2 (&L1)[2], const double2 (&L2)[2],
-                                          int m, int i, double2 *ev, double2 *od) {
-  const int jn = p.d_jn[i], js = p.d_js[i];
-  const double rcos = p.d_rcos[i];
+                                          int m, const PairK &pk, double2 *ev, double2 *od) {
+  const double rcos = pk.rcos;
   const double ra = 1.0 / p.radius;
   const double fm = (double)m;
   double2 av[2][7];
 #pragma unroll
   for (int hemi = 0; hemi < 2; ++hemi) {
-    const double wj = hemi ? p.d_ws[i] : p.d_wn[i];
+    const double wj = pk.w[hemi];
     const double woc = wj * rcos;
     const double2 *Fh = F[hemi];
     const double2 l1 = L1[hemi], l2 = L2[hemi];
@@ -552,7 +606,7 @@ __device__ __forceinline__ void tend_fold(const ShtView &p, const double2 (&F)[2
     o[5] = make_double2(wa * Fh[2].x, wa * Fh[2].y);
     o[6] = make_double2(wa * Fh[1].x, wa * Fh[1].y);
   }
-  if (js == jn) {  // equator node of an odd grid: counted once
+  if (pk.eq) {  // equator node of an odd grid: counted once
 #pragma unroll
     for (int s = 0; s < 7; ++s) ev[s] = od[s] = av[0][s];
   } else {
@@ -591,7 +645,7 @@ __device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, con
       L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
     }
   }
-  tend_fold<HCOS>(p, F, L1, L2, m, i, ev, od);
+  tend_fold<HCOS>(p, F, L1, L2, m, pair_k(p, i), ev, od);
 }
 
 // ---------------------------------------------------------------------
@@ -678,7 +732,7 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;
 // LC(term, hemisphere, m) the Fourier-space Coriolis terms of the pair
 template <typename XF, typename LF>
 __device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bool nl, double *A,
-                                          XF X, LF LC) {
+                                          const PairK &pk, XF X, LF LC) {
   const int T = p.trunc, N = p.nlon_t;
   const size_t ps = (size_t)p.nt16 * kAG;
   for (int m = threadIdx.x; m <= T; m += blockDim.x) {
@@ -704,7 +758,7 @@ __device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bo
       }
     }
     double2 ev[7], od[7];
-    tend_fold<true>(p, F, L1, L2, m, i, ev, od);
+    tend_fold<true>(p, F, L1, L2, m, pk, ev, od);
     double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
     put_row_t(base + 0 * ps, ev, 4, i);
     put_row_t(base + 1 * ps, od, 4, i);
@@ -738,26 +792,13 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
   // 9 buffers of N (twiddles stay in global/L1): 2 CTAs per SM at N = 784
   double2 *B = gsm;
   const double2 *tw = tw_g;
-  const int jn = p.d_jn[i], js = p.d_js[i];
-  const size_t row = (size_t)p.nlat * p.nfreq_t;
   const bool nl = (atoms & SWX_TEND_N) != 0;
   const double2 *R4 = nullptr, *R1 = nullptr;  // forward results: 4 arrays + KE
   if (nl) {
     // inverse: grids of u, v, vort, phi' (z = north + i south), batched 4
     for (int t = threadIdx.x; t < 4 * N; t += blockDim.x) {
       const int f = t / N, k = t - f * N;
-      const double2 *Xn = c2r + f * row + (size_t)jn * p.nfreq_t;
-      const double2 *Xs = c2r + f * row + (size_t)js * p.nfreq_t;
-      double2 a = make_double2(0.0, 0.0), b = a;
-      if (k <= T) {
-        a = Xn[k];
-        b = Xs[k];
-      } else if (N - k <= T) {
-        const double2 an = Xn[N - k], bs = Xs[N - k];
-        a = make_double2(an.x, -an.y);
-        b = make_double2(bs.x, -bs.y);
-      }
-      B[t] = make_double2(a.x - b.y, a.y + b.x);  // X + i Y
+      B[t] = zrow_bin(c2r + ((size_t)i * 4 + f) * 2 * (T + 1), k, T, N);  // zpack rows
     }
     __syncthreads();
     double2 *G = cta_fft(B, B + 4 * (size_t)N, N, 4, p.fft_radix, p.fft_npass, tw, true);
@@ -780,8 +821,9 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
     R4 = r4;
   }
   const int jn0 = p.d_jn[i], js0 = p.d_js[i];
+  const PairK pk = pair_k(p, i);
   grid_fold(
-      p, i, atoms, nl, A, [&](int f, int k) { return f < 4 ? R4[(size_t)f * N + k] : R1[k]; },
+      p, i, atoms, nl, A, pk, [&](int f, int k) { return f < 4 ? R4[(size_t)f * N + k] : R1[k]; },
       [&](int term, int hemi, int m) {
         return lc[(size_t)term * p.nlat * p.nm + (size_t)(hemi ? js0 : jn0) * p.nm + m];
       });
@@ -826,6 +868,7 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
   const int T = p.trunc;
   const bool nl = (atoms & SWX_TEND_N) != 0;
   const int jn = p.d_jn[i], js = p.d_js[i];
+  const PairK pk = pair_k(p, i);
   double2 *TW = F + 5 * FS;  // W_N^t
   double2 *LCs = TW + N;     // [term][hemi][LCM]
   // stage the twiddles and this pair's Coriolis terms asynchronously; they
@@ -840,7 +883,6 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
     }
   cp_commit();
   if (nl) {
-    const size_t row = (size_t)p.nlat * p.nfreq_t;
     // inverse, column DFTs: input bin k = n1 + R1 n2 of u, v, vort, phi'
     // (one task per thread: 4 R1 <= blockDim)
     const int t = threadIdx.x;
@@ -848,22 +890,9 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
     const int f = act ? t / R1 : 0, n1 = t - f * R1;
     double2 v[R2];
     if (act) {
-      const double2 *Xn = c2r + f * row + (size_t)jn * p.nfreq_t;
-      const double2 *Xs = c2r + f * row + (size_t)js * p.nfreq_t;
+      const double2 *zf = c2r + ((size_t)i * 4 + f) * 2 * (T + 1);  // zpack rows
 #pragma unroll
-      for (int n2 = 0; n2 < R2; ++n2) {
-        const int k = n1 + R1 * n2;
-        double2 a = make_double2(0.0, 0.0), b = a;
-        if (k <= T) {
-          a = Xn[k];
-          b = Xs[k];
-        } else if (N - k <= T) {
-          const double2 an = Xn[N - k], bs = Xs[N - k];
-          a = make_double2(an.x, -an.y);
-          b = make_double2(bs.x, -bs.y);
-        }
-        v[n2] = make_double2(a.x - b.y, a.y + b.x);  // X + i Y
-      }
+      for (int n2 = 0; n2 < R2; ++n2) v[n2] = zrow_bin(zf, n1 + R1 * n2, T, N);
       regfft::Dft<R2, true>::run(v);
     }
     cp_wait_all();
@@ -939,8 +968,116 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
   cp_wait_all();
   __syncthreads();  // Coriolis terms staged (when no transform ran)
   grid_fold(
-      p, i, atoms, nl, A, [&](int f, int k) { return F[(size_t)f * FS + (k % R1) + RP * (k / R1)]; },
+      p, i, atoms, nl, A, pk, [&](int f, int k) { return F[(size_t)f * FS + (k % R1) + RP * (k / R1)]; },
       [&](int term, int hemi, int m) { return LCs[(term * 2 + hemi) * C::LCM + m]; });
+}
+
+// Square nlon_t = R * R: the four transform stages (inverse columns, inverse
+// rows, forward rows, forward columns) run as iterations of one loop over a
+// single run-time-direction R-point DFT body, so the kernel's code is one DFT
+// plus glue (the per-stage inlined variant overflows the instruction cache).
+template <int R>
+__global__ void __launch_bounds__(SqCfg<R, R>::NT, 2) grid_sq1_kernel(ShtView p, const double2 *c2r,
+                                                                      const double2 *lc, int atoms,
+                                                                      const double2 *tw_g,
+                                                                      double *A) {
+  using C = SqCfg<R, R>;
+  constexpr int N = C::N, RP = C::RP, FS = C::FS;
+  extern __shared__ __align__(16) double2 gsm[];
+  double2 *F = gsm;  // [5][FS]
+  const int i = blockIdx.x;
+  if (i >= p.nh) {
+    grid_zero_rows(p, i, A);
+    return;
+  }
+  trace_mark(0, 2048);
+  const int T = p.trunc;
+  const bool nl = (atoms & SWX_TEND_N) != 0;
+  const int jn = p.d_jn[i], js = p.d_js[i];
+  const PairK pk = pair_k(p, i);
+  double2 *TW = F + 5 * FS;  // W_N^t
+  double2 *LCs = TW + N;     // [term][hemi][LCM]
+  if (nl)
+    for (int t = threadIdx.x; t < N; t += blockDim.x) cp16(TW + t, tw_g + t);
+  if (atoms & SWX_TEND_LC)
+    for (int t = threadIdx.x; t < 4 * (T + 1); t += blockDim.x) {
+      const int q = t / (T + 1), m = t - q * (T + 1);  // q = term * 2 + hemi
+      const int j = (q & 1) ? js : jn;
+      cp16(LCs + q * C::LCM + m, lc + (size_t)(q >> 1) * p.nlat * p.nm + (size_t)j * p.nm + m);
+    }
+  cp_commit();
+  if (nl) {
+    const int t = threadIdx.x;
+#pragma unroll 1
+    for (int ph = 0; ph < 4; ++ph) {
+      // 0: inverse columns (from the Fourier rows), 1: inverse rows,
+      // 2: forward rows (+ twiddles), 3: forward columns
+      const int nf = ph < 2 ? 4 : 5;
+      const unsigned neg = ph < 2 ? 0x80000000u : 0u;
+      const bool colw = ph == 0 || ph == 3;  // column walk (stride RP)
+      const bool act = t < nf * R;
+      const int f = act ? t / R : 0, idx = t - f * R;
+      double2 *base = F + (size_t)f * FS + (colw ? idx : RP * idx);
+      const int stride = colw ? RP : 1;
+      double2 v[R];
+      if (act) {
+        if (ph == 0) {
+          const double2 *zf = c2r + ((size_t)i * 4 + f) * 2 * (T + 1);  // zpack rows
+#pragma unroll
+          for (int n2 = 0; n2 < R; ++n2) v[n2] = zrow_bin(zf, idx + R * n2, T, N);
+        } else {
+#pragma unroll
+          for (int j = 0; j < R; ++j) v[j] = base[j * stride];
+        }
+        regfft::DftD<R>::run(v, neg);
+      }
+      if (ph == 0) {
+        if (act) {  // trace: thread 0 after its loads + DFT (v consumed)
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < R; ++j) acc += v[j].x;
+          if (acc == 12345.678) v[0].y = acc;
+        }
+        trace_mark(6, 2048);
+        cp_wait_all();
+        __syncthreads();  // twiddles staged
+      }
+      if (act) {
+        if (ph == 0 || ph == 2) {  // W_N^{idx j} (conjugated for the inverse)
+#pragma unroll
+          for (int j = 1; j < R; ++j) {
+            if (idx == 0) break;
+            const double2 w = TW[(idx * j) % N];
+            const double wy = regfft::flip(w.y, neg);
+            const double2 x = v[j];
+            v[j] = make_double2(x.x * w.x - x.y * wy, x.x * wy + x.y * w.x);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) base[j * stride] = v[j];
+      }
+      __syncthreads();
+      trace_mark(1 + ph, 2048);
+      if (ph == 1) {
+        // products on the grid, north in Re, south in Im (swe.py:230-245)
+        for (int n = threadIdx.x; n < FS; n += blockDim.x) {
+          const double2 u = F[n], vv = F[FS + n], z = F[2 * FS + n], ph_ = F[3 * FS + n];
+          F[n] = make_double2(ph_.x * u.x, ph_.y * u.y);
+          F[FS + n] = make_double2(ph_.x * vv.x, ph_.y * vv.y);
+          F[2 * FS + n] = make_double2(z.x * u.x, z.y * u.y);
+          F[3 * FS + n] = make_double2(z.x * vv.x, z.y * vv.y);
+          F[4 * FS + n] = make_double2(0.5 * (u.x * u.x + vv.x * vv.x), 0.5 * (u.y * u.y + vv.y * vv.y));
+        }
+        __syncthreads();
+      }
+    }
+  }
+  cp_wait_all();
+  __syncthreads();  // Coriolis terms staged (when no transform ran)
+  grid_fold(
+      p, i, atoms, nl, A, pk, [&](int f, int k) { return F[(size_t)f * FS + (k % R) + RP * (k / R)]; },
+      [&](int term, int hemi, int m) { return LCs[(term * 2 + hemi) * C::LCM + m]; });
+  trace_mark(5, 2048);
 }
 
 // plain analysis prep: nf (<= 4) grids already FFT'd into Q (pitch nfreq)
@@ -2072,6 +2209,21 @@ extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_d
   return SWX_OK;
 }
 
+template <int R>
+static int launch_grid_sq1(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
+  using C = SqCfg<R, R>;
+  static bool attr = false;
+  if (!attr) {
+    SWX_CUDA_TRY(cudaFuncSetAttribute(grid_sq1_kernel<R>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  grid_sq1_kernel<R><<<p->nt16, C::NT, C::SMEM, s>>>(static_cast<const ShtView &>(*p), w.c2r, w.lc,
+                                                    atoms, p->d_tw, w.A);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
 template <int R1, int R2>
 static int launch_grid_sq(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
   using C = SqCfg<R1, R2>;
@@ -2094,10 +2246,16 @@ static int launch_grid(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
     const char *e = getenv("SWX_GRID_STOCKHAM");
     return e && atoi(e) != 0;
   }();
+  static const bool sq1 = [] {  // SWX_GRID_SQ1=0: per-stage inlined square kernels
+    const char *e = getenv("SWX_GRID_SQ1");
+    return !e || atoi(e) != 0;
+  }();
   if (!stockham) {
     switch (p->nlon_t) {
-      case 784: return launch_grid_sq<28, 28>(p, atoms, w, s);   // T256
-      case 256: return launch_grid_sq<16, 16>(p, atoms, w, s);   // T85
+      case 784:   // T256
+        return sq1 ? launch_grid_sq1<28>(p, atoms, w, s) : launch_grid_sq<28, 28>(p, atoms, w, s);
+      case 256:   // T85
+        return sq1 ? launch_grid_sq1<16>(p, atoms, w, s) : launch_grid_sq<16, 16>(p, atoms, w, s);
       case 192: return launch_grid_sq<12, 16>(p, atoms, w, s);   // T63
       default: break;
     }
@@ -2136,6 +2294,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     a.lc = w.lc;
     a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
     a.nfreq = p->nfreq_t;
+    a.zpack = 1;  // packed north/south rows for the fused grid stage
     int nt;
     dim3 g = synth_grid(p, 1, &nt);
     if ((rc = launch_synth<0>(p, g, nt, a, s))) return rc;
@@ -2249,5 +2408,25 @@ extern "C" int swx_sht_tendency_profile(swx_sht p, int atoms, const swx_c128 *d_
   cudaEventElapsedTime(&tot, ev[0], ev[6]);
   h_stage_ms[6] = tot;
   for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
+  return SWX_OK;
+}
+
+// ---- measurement helper: per-CTA phase trace of the instrumented kernels
+// (synth_kernel<0,1>, grid_sq1_kernel).  enable: 1 on, 0 off, -1 leave;
+// copies n_ctas x 8 u64 {smid, t0..t6 (ns)} to h_out when non-null.
+extern "C" int swx_trace(int enable, unsigned long long *h_out, int n_ctas) {
+  if (enable >= 0) {
+    SWX_CUDA_TRY(cudaMemcpyToSymbol(swx::g_trace_on, &enable, sizeof(int)));
+    if (enable) {
+      static unsigned long long z[swx::kTraceCtas * swx::kTraceSlots];
+      SWX_CUDA_TRY(cudaMemcpyToSymbol(swx::g_trace, z, sizeof(z)));
+    }
+  }
+  if (h_out && n_ctas > 0) {
+    const int n = std::min(n_ctas, swx::kTraceCtas);
+    SWX_CUDA_TRY(cudaDeviceSynchronize());
+    SWX_CUDA_TRY(cudaMemcpyFromSymbol(h_out, swx::g_trace,
+                                      sizeof(unsigned long long) * swx::kTraceSlots * n));
+  }
   return SWX_OK;
 }

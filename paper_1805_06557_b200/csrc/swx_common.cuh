@@ -88,3 +88,31 @@ struct swx_solver_s {
   std::map<int, std::pair<int4 *, int>> lg_sched;
   int l_blocks_per_sm = 0;
 };
+
+// ---- per-CTA phase tracer (measurement helper, swx_trace_*) ---------------
+// When enabled, thread 0 of every CTA of an instrumented kernel records
+// (%smid, globaltimer at up to 7 phase marks) in a fixed device buffer.
+namespace swx {
+constexpr int kTraceSlots = 8;
+constexpr int kTraceCtas = 4096;
+// translation-unit local (no relocatable device code): swx_trace reads sht.cu's copy
+static __device__ int g_trace_on;
+static __device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// records of one kernel start at CTA slot `base`
+__device__ __forceinline__ void trace_mark(int k, int base = 0) {
+  if (g_trace_on && threadIdx.x == 0 && base + blockIdx.x < kTraceCtas && blockIdx.y == 0) {
+    unsigned long long *t = g_trace + (size_t)(base + blockIdx.x) * kTraceSlots;
+    if (k == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      t[0] = sm;
+    }
+    t[1 + k] = gtimer();
+  }
+}
+}  // namespace swx
