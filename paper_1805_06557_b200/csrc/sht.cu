@@ -1471,7 +1471,9 @@ constexpr int kP1 = 352;                // plane-1 box offset (doubles, 128 B al
 constexpr int kSB = 704;                // prepared-row blocks offset (doubles, 128 B aligned)
 constexpr int kStage = kSB + 4 * kTK * kAG;  // doubles per stage (multiple of 16)
 constexpr int kTabThreads = 5 * 32;
-constexpr size_t kTabSmem = (size_t)kTS * kStage * sizeof(double) + 2 * kTS * sizeof(uint64_t);
+constexpr size_t tab_smem(int kts) {
+  return (size_t)kts * kStage * sizeof(double) + 2 * kts * sizeof(uint64_t);
+}
 static_assert(kP1 >= kTBoxRows * kPR && kSB >= kP1 + kTBoxRows * kPR, "stage layout");
 static_assert((kStage * 8) % 128 == 0 && (kP1 * 8) % 128 == 0 && (kSB * 8) % 128 == 0, "TMA alignment");
 
@@ -1517,7 +1519,7 @@ __device__ __forceinline__ void tma_2d(double *dst, const CUtensorMap *map, int 
       : "memory");
 }
 
-template <int MODE>
+template <int MODE, int kTS = 4>
 __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
                                                                    const __grid_constant__ CUtensorMap tmap,
                                                                    const double *A, double2 *out,
@@ -1991,30 +1993,47 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
   return SWX_OK;
 }
 
+// state-synthesis geometry (tuning overrides SWX_SYNTH_NT / SWX_SYNTH_SPLIT):
+// pairs per CTA half and whether long columns are split over two halves
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int MODE, int KTS>
+static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
+                                 const double2 *sub) {
+  // resident CTAs per SM and SM count, queried once per instantiation
+  static int nsm = 0, per_sm = 0;
+  auto k = analysis_tab_kernel<MODE, KTS>;
+  const size_t smem = tab_smem(KTS);
+  if (!nsm) {
+    SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, n = 0, b = 0;
+    SWX_CUDA_TRY(cudaGetDevice(&dev));
+    SWX_CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kTabThreads, smem));
+    per_sm = std::max(b, 1);
+    static const int cap = env_int("SWX_TAB_CTAS", 0);  // tuning: cap CTAs per SM
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+    nsm = n;
+  }
+  // equal-cost items: give every CTA the same number of items
+  const int slots = nsm * per_sm;
+  const int per_cta = (p->n_titems + slots - 1) / slots;
+  const int blocks = std::max(1, (p->n_titems + per_cta - 1) / per_cta);
+  k<<<blocks, kTabThreads, smem, s>>>(static_cast<const ShtView &>(*p), p->ptab_map, A, out, nf,
+                                      sub);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
 template <int MODE>
 static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
                                const double2 *sub = nullptr) {
-  // resident CTAs per SM and SM count, queried once per mode
-  static int nsm[2] = {0, 0}, per_sm[2] = {0, 0};
-  if (!nsm[MODE]) {
-    SWX_CUDA_TRY(cudaFuncSetAttribute(analysis_tab_kernel<MODE>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabSmem));
-    int dev = 0, n = 0, k = 0;
-    SWX_CUDA_TRY(cudaGetDevice(&dev));
-    SWX_CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, analysis_tab_kernel<MODE>,
-                                                               kTabThreads, kTabSmem));
-    per_sm[MODE] = std::max(k, 1);
-    nsm[MODE] = n;
-  }
-  // equal-cost items: give every CTA the same number of items
-  const int slots = nsm[MODE] * per_sm[MODE];
-  const int per_cta = (p->n_titems + slots - 1) / slots;
-  const int blocks = std::max(1, (p->n_titems + per_cta - 1) / per_cta);
-  analysis_tab_kernel<MODE><<<blocks, kTabThreads, kTabSmem, s>>>(static_cast<const ShtView &>(*p),
-                                                                  p->ptab_map, A, out, nf, sub);
-  SWX_LAUNCH_CHECK();
-  return SWX_OK;
+  static const int stages = env_int("SWX_TAB_STAGES", 4);  // tuning: ring depth 4 or 8
+  return stages == 8 ? launch_analysis_tab_k<MODE, 8>(p, A, out, nf, s, sub)
+                     : launch_analysis_tab_k<MODE, 4>(p, A, out, nf, s, sub);
 }
 
 static int c2r_exec(swx_sht p, int nlon, int nf, double2 *in, double *out, cudaStream_t s) {
@@ -2056,13 +2075,6 @@ static size_t synth_smem(int ns, int nh, int split, int nt) {
   const size_t stage = (size_t)split * (ns * kSL * 2 + (kSL + 2) * 4) * sizeof(double);
   const size_t red = split == 2 ? (size_t)nt * 4 * (ns + nh) * sizeof(double) : 0;
   return std::max(stage, red);
-}
-
-// state-synthesis geometry (tuning overrides SWX_SYNTH_NT / SWX_SYNTH_SPLIT):
-// pairs per CTA half and whether long columns are split over two halves
-static int env_int(const char *name, int dflt) {
-  const char *e = getenv(name);
-  return e ? atoi(e) : dflt;
 }
 
 template <int MODE>

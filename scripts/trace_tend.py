@@ -38,6 +38,8 @@ for name, lo, hi, nm in (("synth", 0, 257, 3), ("grid", 2048, 2048 + 208, 6)):
     sm = r[:, 0]
     per_sm = np.bincount(sm.astype(int))
     out[name]["ctas_per_sm_hist"] = np.bincount(per_sm).tolist()
+    out[name]["late_starts"] = sorted([(int(lo + k), round(float(rel[k, 0]), 2), int(sm[k]))
+                                       for k in range(len(r)) if rel[k, 0] > 2.0], key=lambda x: x[1])[:12]
     if name == "synth":
         order = np.argsort(-dur)[:8]
         out[name]["slowest"] = [(int(lo + k), float(dur[k]), int(sm[k])) for k in order]
