@@ -174,6 +174,17 @@ int swx_sht_tendency_sub(swx_sht p, int atoms, const swx_c128 *d_state,
                          const swx_c128 *d_sub, swx_c128 *d_out, void *d_workspace,
                          size_t ws_bytes, void *stream);
 
+/* ---- host layout conversion (API edge) ------------------------------------
+ * Dense (T+1)x(T+1) complex128 fields, C order (row l, column m) -- the
+ * reference's SpectralField.coeffs (sphere.py) -- to and from packed m-major
+ * states (n_fields x ncoef).  Host memory only, multithreaded; unpack writes
+ * every dense entry (zeros for m > l).  Used by the swerexi-shaped stepper API
+ * around each step (solvers.py:288-307 index map).                          */
+int swx_host_pack(int trunc, int n_fields, const swx_c128 *const *h_dense,
+                  swx_c128 *h_packed);
+int swx_host_unpack(int trunc, int n_fields, const swx_c128 *h_packed,
+                    swx_c128 *const *h_dense);
+
 /* ---- measurement helpers (bench.py) ---------------------------------------
  * swx_sht_tendency with per-stage device times (ms) written to h_stage_ms[7]:
  * {synthesis, C2R FFT, grid products, R2C FFT, analysis prep, analysis,

@@ -57,6 +57,8 @@ SIGNATURES = {
     "swx_sht_tendency_sub": (_I, [_P, _I, _P, _P, _P, _P, _S, _P]),
     "swx_sht_tendency_profile": (_I, [_P, _I, _P, _P, _P, _S, _P, _P]),
     "swx_fp64_fma_probe": (_I, [_P, _I, _I, _P]),
+    "swx_host_pack": (_I, [_I, _I, _P, _P]),
+    "swx_host_unpack": (_I, [_I, _I, _P, _P]),
     "swx_trace": (_I, [_I, _P, _I]),
 }
 

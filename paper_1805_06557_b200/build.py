@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libswx.so")
-SOURCES = ["rexi.cu", "sht.cu"]
+SOURCES = ["rexi.cu", "sht.cu", "host.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -41,10 +41,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cuda = os.path.dirname(os.path.dirname(nvcc()))
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared",
-           "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
+           "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-Xptxas", "-warn-spills",
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-o", LIB + ".tmp",
-           f"-L{cuda}/lib64", "-lcufft", f"-Xlinker", f"-rpath={cuda}/lib64"]
+           f"-L{cuda}/lib64", "-lcufft", "-lgomp", f"-Xlinker", f"-rpath={cuda}/lib64"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

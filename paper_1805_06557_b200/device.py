@@ -12,6 +12,8 @@ from __future__ import annotations
 
 import functools
 
+import ctypes
+
 import numpy as np
 
 from .errors import ConfigurationError
@@ -40,28 +42,46 @@ def flat_index(trunc: int) -> np.ndarray:
     return idx
 
 
+def _host_lib():
+    """libswx.so's host layout helpers (None if the library is not built)."""
+    try:
+        from . import _lib
+        return _lib.load()
+    except Exception:  # pragma: no cover - host utility only
+        return None
+
+
 def pack_fields(fields, out: np.ndarray) -> np.ndarray:
     """Pack dense (T+1, T+1) fields into the rows of ``out`` (F, ncoef)
-    without an intermediate stacked copy (the fast API edge)."""
+    without an intermediate stacked copy (the fast API edge): the library's
+    multithreaded blocked transpose (swx_host_pack), numpy otherwise."""
     trunc = fields[0].shape[-1] - 1
+    arrs = [np.ascontiguousarray(c, dtype=np.complex128) for c in fields]
+    lib = _host_lib()
+    if lib is not None and out.flags.c_contiguous and out.dtype == np.complex128:
+        ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        if lib.swx_host_pack(trunc, len(arrs), ptrs, out.ctypes.data) == 0:
+            return out
     idx = flat_index(trunc)
-    for f, c in enumerate(fields):
-        c = np.asarray(c)
-        if c.dtype != np.complex128:
-            c = c.astype(np.complex128)
-        np.take(np.ascontiguousarray(c).reshape(-1), idx, out=out[f])
+    for f, c in enumerate(arrs):
+        np.take(c.reshape(-1), idx, out=out[f])
     return out
 
 
 def unpack_fields(packed: np.ndarray, trunc: int) -> list:
     """(F, ncoef) packed -> list of F fresh dense (T+1, T+1) arrays."""
-    idx = flat_index(trunc)
     n = trunc + 1
-    res = []
-    for row in packed:
-        d = np.zeros(n * n, dtype=np.complex128)
-        d[idx] = row
-        res.append(d.reshape(n, n))
+    res = [np.empty((n, n), dtype=np.complex128) for _ in range(packed.shape[0])]
+    lib = _host_lib()
+    src = np.ascontiguousarray(packed, dtype=np.complex128)
+    if lib is not None:
+        ptrs = (ctypes.c_void_p * len(res))(*[a.ctypes.data for a in res])
+        if lib.swx_host_unpack(trunc, len(res), src.ctypes.data, ptrs) == 0:
+            return res
+    idx = flat_index(trunc)
+    for d, row in zip(res, src):
+        d.fill(0)
+        d.reshape(-1)[idx] = row
     return res
 
 
