@@ -253,6 +253,8 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
     int log2_lpm_rt, int trunc, int ncoef, const int4 *__restrict__ sched, int realify, Axpy ep,
     double2 *__restrict__ out) {
   constexpr bool kStatic = SNB > 0 && SLPM > 0;
+  pdl_trigger();
+  pdl_wait();
   const int lpm = kStatic ? SLPM : lpm_rt;
   const int np = kStatic ? SLPM * LEAF * SNB : np_rt;
   const int log2_lpm = kStatic ? (SLPM == 4 ? 2 : SLPM == 8 ? 3 : SLPM == 16 ? 4 : 5) : log2_lpm_rt;
@@ -315,10 +317,15 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
 template <int NRHS, int NP, int LPM, int MPL>
 __global__ void __launch_bounds__(128) rexi_lg_mm_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
-    const int4 *__restrict__ sched, int realify, Axpy ep, double2 *__restrict__ out) {
+    const int4 *__restrict__ sched, int realify, Axpy ep, int fac_ready,
+    double2 *__restrict__ out) {
   constexpr int PPL = NP / LPM;          // poles per lane
   constexpr int GROUPS = 128 / LPM;      // lane groups per CTA
   extern __shared__ double2 fac[];       // [NRHS][4][NP], interleaved (t*LPM + q)
+  pdl_trigger();
+  // prepared factor tables do not depend on the preceding kernel: stage them
+  // before waiting for it (PDL overlap)
+  if (!fac_ready) pdl_wait();
   const int4 w = sched[blockIdx.x];
   const int l = w.x, m0 = w.y, m1 = w.z;
   {
@@ -327,6 +334,7 @@ __global__ void __launch_bounds__(128) rexi_lg_mm_kernel(
     for (int i = threadIdx.x; i < NRHS * 2 * NP; i += blockDim.x) dst[i] = src[i];
   }
   __syncthreads();
+  pdl_wait();
   const int q = threadIdx.x & (LPM - 1);
   const int g = threadIdx.x / LPM;
   for (int base = m0; base < m1; base += GROUPS * MPL) {
@@ -1084,7 +1092,8 @@ static int build_lg_factors(swx_solver s, const double2 *betas, int pole0, int P
 
 template <int NRHS>
 static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, int realify,
-                  double2 *out, cudaStream_t st, Axpy ep = Axpy{nullptr, 0.0}) {
+                  double2 *out, cudaStream_t st, Axpy ep = Axpy{nullptr, 0.0},
+                  int fac_ready = 0) {
   LgGeom g;
   int rc = lg_geom(P, g);
   if (rc) return rc;
@@ -1108,7 +1117,8 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
     auto k = rexi_lg_mm_kernel<NRHS, 256, 8, 2>;
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<n_cta, 128, smem, st>>>(rhs, fac, s->trunc, s->ncoef, sched, realify, ep, out);
+    SWX_CUDA_TRY(launch_pdl(k, dim3(n_cta), dim3(128), smem, st, rhs, fac, s->trunc, s->ncoef,
+                            sched, realify, ep, fac_ready, out));
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
@@ -1285,8 +1295,8 @@ static int rexi_sum_prepared_impl(swx_solver s, int n_rhs, const swx_c128 *d_rhs
   const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
   const size_t t = swx_rexi_prepared_bytes(s, n_rhs, pole_begin, pole_end) / chunks;
   if (chunks == 1)
-    return n_rhs == 1 ? run_lg<1>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep)
-                      : run_lg<2>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep);
+    return n_rhs == 1 ? run_lg<1>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep, 1)
+                      : run_lg<2>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep, 1);
   const size_t stride = (size_t)n_rhs * 3 * s->ncoef;
   if (!d_workspace || workspace_bytes < chunks * stride * sizeof(double2))
     return fail(SWX_ERR_CONFIG, "workspace too small");
@@ -1294,8 +1304,8 @@ static int rexi_sum_prepared_impl(swx_solver s, int n_rhs, const swx_c128 *d_rhs
   for (int c = 0; c < chunks; ++c) {
     const int pc = std::min(kLgMaxP, pole_end - (pole_begin + c * kLgMaxP));
     const double2 *fac = (const double2 *)((const char *)d_prep + c * t);
-    int rc = n_rhs == 1 ? run_lg<1>(s, rhs, fac, pc, 0, part + c * stride, st)
-                        : run_lg<2>(s, rhs, fac, pc, 0, part + c * stride, st);
+    int rc = n_rhs == 1 ? run_lg<1>(s, rhs, fac, pc, 0, part + c * stride, st, Axpy{nullptr, 0.0}, 1)
+                        : run_lg<2>(s, rhs, fac, pc, 0, part + c * stride, st, Axpy{nullptr, 0.0}, 1);
     if (rc) return rc;
   }
   tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, chunks,

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
   const int m = blockIdx.x;
   const int i = blockIdx.y * NT + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
+  pdl_trigger();
   if (MODE == 0) trace_mark(0);
   const int T = p.trunc, nc = p.ncoef;
   const int off = col_offset(T, m);
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
 #pragma unroll
     for (int s = 0; s < (NH > 0 ? NH : 1); ++s) sh[q][s] = make_double2(0.0, 0.0);
   }
+  pdl_wait();  // the coefficients come from the preceding kernel
   const int nchunk0 = (split + kSL - 1) / kSL, nchunk1 = (kmax - split + kSL - 1) / kSL;
   const int nchunk = SPLIT == 2 ? max(nchunk0, nchunk1) : nchunk0;
   // recurrence constants split for two 16-byte loads per degree:
@@ -783,6 +785,8 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
                                                            const double2 *lc, int atoms,
                                                            const double2 *tw_g, double *A) {
   extern __shared__ __align__(16) double2 gsm[];
+  pdl_trigger();
+  pdl_wait();
   const int N = p.nlon_t, T = p.trunc;
   const int i = blockIdx.x;  // latitude pair (padded to nt16)
   if (i >= p.nh) {  // padding pairs: zero prepared rows
@@ -860,6 +864,8 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
   constexpr int N = C::N, RP = C::RP, FS = C::FS;
   extern __shared__ __align__(16) double2 gsm[];
   double2 *F = gsm;  // [5][FS]
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   if (i >= p.nh) {
     grid_zero_rows(p, i, A);
@@ -990,6 +996,7 @@ __global__ void __launch_bounds__(SqCfg<R, R>::NT, 2) grid_sq1_kernel(ShtView p,
     grid_zero_rows(p, i, A);
     return;
   }
+  pdl_trigger();
   trace_mark(0, 2048);
   const int T = p.trunc;
   const bool nl = (atoms & SWX_TEND_N) != 0;
@@ -999,6 +1006,7 @@ __global__ void __launch_bounds__(SqCfg<R, R>::NT, 2) grid_sq1_kernel(ShtView p,
   double2 *LCs = TW + N;     // [term][hemi][LCM]
   if (nl)
     for (int t = threadIdx.x; t < N; t += blockDim.x) cp16(TW + t, tw_g + t);
+  pdl_wait();  // zpack rows and Coriolis terms come from the synthesis
   if (atoms & SWX_TEND_LC)
     for (int t = threadIdx.x; t < 4 * (T + 1); t += blockDim.x) {
       const int q = t / (T + 1), m = t - q * (T + 1);  // q = term * 2 + hemi
@@ -1532,6 +1540,7 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
   const int nst = nt / kTK;  // stages per item
   constexpr int NPART = MODE == 0 ? 2 : 1;
   const size_t ps = (size_t)nt * kAG;
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int q = 0; q < kTS; ++q) {
       mbar_init(full + q, 1);
@@ -1540,6 +1549,7 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // the prepared rows come from the preceding kernel
 
   if (wid == 4) {
     // ---------------- producer warp (one lane) ----------------
@@ -2022,8 +2032,8 @@ static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int n
   const int slots = nsm * per_sm;
   const int per_cta = (p->n_titems + slots - 1) / slots;
   const int blocks = std::max(1, (p->n_titems + per_cta - 1) / per_cta);
-  k<<<blocks, kTabThreads, smem, s>>>(static_cast<const ShtView &>(*p), p->ptab_map, A, out, nf,
-                                      sub);
+  SWX_CUDA_TRY(launch_pdl(k, dim3(blocks), dim3(kTabThreads), smem, s,
+                          static_cast<const ShtView &>(*p), p->ptab_map, A, out, nf, sub));
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -2104,7 +2114,7 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
     auto k = sp == 2 ? synth_kernel<MODE, 2> : synth_kernel<MODE, 1>;
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<g, sp * nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(sp * nt), smem, s, static_cast<const ShtView &>(*p), a));
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
@@ -2116,13 +2126,13 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
     auto k = synth_kernel<MODE, 2>;
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<g, 2 * nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(2 * nt), smem, s, static_cast<const ShtView &>(*p), a));
   } else {
     const size_t smem = synth_smem(ns, nh, 1, nt);
     auto k = synth_kernel<MODE, 1>;
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<g, nt, smem, s>>>(static_cast<const ShtView &>(*p), a);
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
   }
   SWX_LAUNCH_CHECK();
   return SWX_OK;
@@ -2230,8 +2240,9 @@ static int launch_grid_sq1(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  grid_sq1_kernel<R><<<p->nt16, C::NT, C::SMEM, s>>>(static_cast<const ShtView &>(*p), w.c2r, w.lc,
-                                                    atoms, p->d_tw, w.A);
+  SWX_CUDA_TRY(launch_pdl(grid_sq1_kernel<R>, dim3(p->nt16), dim3(C::NT), C::SMEM, s,
+                          static_cast<const ShtView &>(*p), (const double2 *)w.c2r,
+                          (const double2 *)w.lc, atoms, (const double2 *)p->d_tw, w.A));
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <utility>
@@ -114,5 +115,42 @@ __device__ __forceinline__ void trace_mark(int k, int base = 0) {
     }
     t[1 + k] = gtimer();
   }
+}
+}  // namespace swx
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Hot-path kernels trigger their dependents at entry and wait for their
+// predecessor (griddepcontrol.wait) only before the first read of its output,
+// so a kernel's constant-data prologue (twiddles, factor tables, Legendre
+// table tiles) overlaps the previous kernel's tail.  Without the launch
+// attribute both instructions are no-ops.  SWX_PDL=0 disables.
+namespace swx {
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("SWX_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 }  // namespace swx
