@@ -78,6 +78,10 @@ struct ShtView {
   long long *d_ptoff = nullptr;
   double *d_ptab = nullptr;
   double *d_rcos16 = nullptr;  // 1/cos per padded pair (0 on padding)
+  int n_sitems = 0;            // state-synthesis items (m, kb, ke, seg), longest first
+  int4 *d_sitems = nullptr;
+  int *d_scnt = nullptr;       // [m] arrival counters of split columns
+  double2 *d_spart = nullptr;  // [m][2][nh][14] partial sums of split columns
   int n_titems = 0;            // analysis warp items (m, l0, par)
   int4 *d_titems = nullptr;
 };
@@ -113,6 +117,13 @@ struct SynthArgs {
   // (X_s = X_n on the equator node), i.e. the packed row z = north + i south
   // at bin m and at bin N - m.
   int zpack = 0;
+  // cross-CTA column split (state synthesis): CTA b runs items[b] =
+  // (m, kb, ke, seg); seg >= 0 marks one of the two segments of a long
+  // column, whose partial sums meet in `part` and are combined in fixed
+  // order (segment 0 + segment 1) by whichever CTA arrives second (`cnt`)
+  const int4 *items = nullptr;
+  int *cnt = nullptr;
+  double2 *part = nullptr;
 };
 
 // bin k of the packed complex row z = north + i south of field f (zero above T)
@@ -216,7 +227,9 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
   double2 *cs = reinterpret_cast<double2 *>(smem_syn) + (size_t)half * NS * kSL;  // [NS][kSL]
   double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)SPLIT * NS * kSL * 2) +
                  (size_t)half * (kSL + 2);
-  const int m = blockIdx.x;
+  int4 itm = make_int4(blockIdx.x, 0, 0, -1);
+  if (MODE == 0 && SPLIT == 1 && a.items) itm = a.items[blockIdx.x];
+  const int m = itm.x;
   const int i = blockIdx.y * NT + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
   pdl_trigger();
@@ -229,8 +242,12 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
   // this half's degree range [kb, ke) of the column
   int split = kmax;
   if (SPLIT == 2 && kmax > 96) split = ((kmax / 2 + kSeg - 1) / kSeg) * kSeg;
-  const int kb = half == 0 ? 0 : split;
-  const int ke = half == 0 ? split : kmax;
+  int kb = half == 0 ? 0 : split;
+  int ke = half == 0 ? split : kmax;
+  if (itm.w >= 0) {  // one segment of a split column
+    kb = itm.y;
+    ke = itm.z;
+  }
   double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
   if (has) {
     x = p.d_x[i];
@@ -360,6 +377,48 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
       for (int s2 = 0; s2 < NH; ++s2) {
         sh[q][s2].x += red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2];
         sh[q][s2].y += red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2 + 1];
+      }
+    }
+  }
+  if constexpr (MODE == 0 && SPLIT == 1) {
+    if (itm.w >= 0) {
+      constexpr int NP = 2 * (NS + NH);  // partial sums per pair (complex)
+      if (has) {
+        double2 *mine = a.part + (((size_t)m * 2 + itm.w) * p.nh + i) * NP;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+#pragma unroll
+          for (int s2 = 0; s2 < NS; ++s2) mine[q * NS + s2] = sp[q][s2];
+#pragma unroll
+          for (int s2 = 0; s2 < NH; ++s2) mine[2 * NS + q * NH + s2] = sh[q][s2];
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      __shared__ int s_last;
+      if (threadIdx.x == 0) {
+        s_last = atomicAdd(a.cnt + m, 1) == 1;
+        if (s_last) a.cnt[m] = 0;  // ready for the next launch
+      }
+      __syncthreads();
+      if (!s_last) return;
+      __threadfence();
+      if (has) {
+        const double2 *oth = a.part + (((size_t)m * 2 + (1 - itm.w)) * p.nh + i) * NP;
+        const bool first = itm.w == 0;  // fixed order: segment 0 + segment 1
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+#pragma unroll
+          for (int s2 = 0; s2 < NS; ++s2) {
+            const double2 o = __ldcg(oth + q * NS + s2);
+            sp[q][s2] = first ? cadd(sp[q][s2], o) : cadd(o, sp[q][s2]);
+          }
+#pragma unroll
+          for (int s2 = 0; s2 < NH; ++s2) {
+            const double2 o = __ldcg(oth + 2 * NS + q * NH + s2);
+            sh[q][s2] = first ? cadd(sh[q][s2], o) : cadd(o, sh[q][s2]);
+          }
+        }
       }
     }
   }
@@ -1837,6 +1896,32 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
+  // state-synthesis items: columns longer than 128 degrees split in two at a
+  // checkpoint (multiple of kSeg), the rest whole; longest first (LPT order)
+  if (e == cudaSuccess) {
+    std::vector<int4> it;
+    int nsplit = 0;
+    for (int m = 0; m <= T; ++m) {
+      const int kmax = T + 1 - m;
+      if (kmax > 2 * kSeg) {
+        int sp = (int)std::lround(kmax / (2.0 * kSeg)) * kSeg;
+        sp = std::max(kSeg, std::min(sp, kmax - 1));
+        it.push_back(make_int4(m, 0, sp, 0));
+        it.push_back(make_int4(m, sp, kmax, 1));
+        ++nsplit;
+      } else {
+        it.push_back(make_int4(m, 0, kmax, -1));
+      }
+    }
+    std::stable_sort(it.begin(), it.end(),
+                     [](const int4 &a, const int4 &b) { return a.z - a.y > b.z - b.y; });
+    p->n_sitems = (int)it.size();
+    up((void **)&p->d_sitems, it.data(), sizeof(int4) * it.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_scnt, sizeof(int) * (T + 1));
+    if (e == cudaSuccess) e = cudaMemset(p->d_scnt, 0, sizeof(int) * (T + 1));
+    if (e == cudaSuccess && nsplit)
+      e = cudaMalloc(&p->d_spart, sizeof(double2) * (size_t)(T + 1) * 2 * nh * 14);
+  }
   if (e != cudaSuccess) {
     swx_sht_destroy(p);
     return fail(SWX_ERR_CUDA, std::string("sht checkpoints: ") + cudaGetErrorString(e));
@@ -1945,6 +2030,9 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_ptab);
   cudaFree(p->d_rcos16);
   cudaFree(p->d_titems);
+  cudaFree(p->d_sitems);
+  cudaFree(p->d_scnt);
+  cudaFree(p->d_spart);
   cudaFree(p->d_tw);
   delete p;
   return SWX_OK;
@@ -2130,9 +2218,19 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
   } else {
     const size_t smem = synth_smem(ns, nh, 1, nt);
     auto k = synth_kernel<MODE, 1>;
+    // cross-CTA split of the long columns: balanced, but at one 7-warp CTA per
+    // SM (142 registers) the extra items run as a second wave -- off by default
+    static const int st_items = env_int("SWX_SYNTH_ITEMS", 0);
+    SynthArgs ai = a;
+    if (MODE == 0 && st_items && p->d_sitems && p->d_spart && g.y == 1) {
+      ai.items = p->d_sitems;
+      ai.cnt = p->d_scnt;
+      ai.part = p->d_spart;
+      g.x = p->n_sitems;
+    }
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), ai));
   }
   SWX_LAUNCH_CHECK();
   return SWX_OK;
