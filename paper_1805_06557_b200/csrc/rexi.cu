@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
 template <int NRHS, int NP, int LPM, int MPL>
 __global__ void __launch_bounds__(128) rexi_lg_mm_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
-    const int4 *__restrict__ sched, int realify, Axpy ep, int fac_ready,
+    const int4 *__restrict__ sched, int n_items, int realify, Axpy ep, int fac_ready,
     double2 *__restrict__ out) {
   constexpr int PPL = NP / LPM;          // poles per lane
   constexpr int GROUPS = 128 / LPM;      // lane groups per CTA
@@ -326,7 +326,10 @@ __global__ void __launch_bounds__(128) rexi_lg_mm_kernel(
   // prepared factor tables do not depend on the preceding kernel: stage them
   // before waiting for it (PDL overlap)
   if (!fac_ready) pdl_wait();
-  const int4 w = sched[blockIdx.x];
+  // persistent CTAs over (l, mode block) items, largest first
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  if (it != blockIdx.x) __syncthreads();  // previous item's factor reads done
+  const int4 w = sched[it];
   const int l = w.x, m0 = w.y, m1 = w.z;
   {
     const double4 *src = reinterpret_cast<const double4 *>(fac_g + (size_t)l * NRHS * 4 * NP);
@@ -391,6 +394,7 @@ __global__ void __launch_bounds__(128) rexi_lg_mm_kernel(
         }
     }
   }
+}
 }
 
 // =====================================================================
@@ -1035,12 +1039,18 @@ extern "C" size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs,
 }
 
 // modes per CTA for a given lanes-per-mode; schedules built lazily
-static const int4 *lg_schedule(swx_solver s, int mpc, int *n_cta) {
-  auto &e = s->lg_sched[mpc];
+// (l, m0, m1) blocks of mpc modes, l descending; mpc < 0: blocks of -mpc
+// modes ordered by size, largest first (persistent kernels)
+static const int4 *lg_schedule(swx_solver s, int mpc_in, int *n_cta) {
+  auto &e = s->lg_sched[mpc_in];
   if (!e.first) {
+    const int mpc = mpc_in < 0 ? -mpc_in : mpc_in;
     std::vector<int4> sched;
     for (int l = s->trunc; l >= 0; --l)
       for (int m0 = 0; m0 <= l; m0 += mpc) sched.push_back(make_int4(l, m0, std::min(l + 1, m0 + mpc), 0));
+    if (mpc_in < 0)
+      std::stable_sort(sched.begin(), sched.end(),
+                       [](const int4 &a, const int4 &b) { return a.z - a.y > b.z - b.y; });
     int4 *d = nullptr;
     if (cudaMalloc(&d, sizeof(int4) * sched.size()) != cudaSuccess) return nullptr;
     cudaMemcpy(d, sched.data(), sizeof(int4) * sched.size(), cudaMemcpyHostToDevice);
@@ -1115,10 +1125,26 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
   static const int env_mpl = getenv("SWX_LG_MPL") ? atoi(getenv("SWX_LG_MPL")) : 2;
   if (g.lpm == 8 && g.ppl == 32 && env_mpl == 2) {
     auto k = rexi_lg_mm_kernel<NRHS, 256, 8, 2>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SWX_CUDA_TRY(launch_pdl(k, dim3(n_cta), dim3(128), smem, st, rhs, fac, s->trunc, s->ncoef,
-                            sched, realify, ep, fac_ready, out));
+    static int per_sm[3] = {0, 0, 0};
+    if (!per_sm[NRHS]) {
+      if (smem > 48 * 1024)
+        SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int b = 0;
+      SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, 128, smem));
+      per_sm[NRHS] = std::max(b, 1);
+    }
+    // one pass (32 modes) per item, items largest first, persistent CTAs
+    static const int env_pers = getenv("SWX_LG_PERSIST") ? atoi(getenv("SWX_LG_PERSIST")) : 0;
+    int n_items = n_cta;
+    const int4 *items = sched;
+    int grid = n_cta;
+    if (env_pers) {
+      items = lg_schedule(s, -32, &n_items);
+      if (!items) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
+      grid = std::min(n_items, sm_count() * per_sm[NRHS]);
+    }
+    SWX_CUDA_TRY(launch_pdl(k, dim3(grid), dim3(128), smem, st, rhs, fac, s->trunc, s->ncoef,
+                            items, n_items, realify, ep, fac_ready, out));
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
