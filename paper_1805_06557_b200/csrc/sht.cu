@@ -82,13 +82,18 @@ struct ShtView {
   int4 *d_sitems = nullptr;
   int *d_scnt = nullptr;       // [m] arrival counters of split columns
   double2 *d_spart = nullptr;  // [m][2][nh][14] partial sums of split columns
+  int tab_rows = 0;            // rows of the P table (both planes of every column)
+  int n_sblk = 0;              // table synthesis: CTAs and their item ranges
+  int2 *d_sblk = nullptr;      // [cta] [begin, end) into d_slist
+  int2 *d_slist = nullptr;     // (m, 16-pair block), LPT order per CTA
   int n_titems = 0;            // analysis warp items (m, l0, par)
   int4 *d_titems = nullptr;
 };
 
 struct swx_sht_s : ShtView {
   std::map<long long, cufftHandle> plans;
-  CUtensorMap ptab_map;  // 2D view [rows][nt16] of the P table, box kTBox x 17
+  CUtensorMap ptab_map;    // 2D view [rows][nt16] of the P table, box kTBox x 17
+  CUtensorMap ptab_map16;  // the same view, box kPR x 16 (table synthesis)
 };
 
 namespace swx {
@@ -1725,6 +1730,225 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
   }
 }
 
+// ---------------------------------------------------------------------
+// Table synthesis of the state (T small enough for the P table).  The
+// recurrence is replaced by the plan-time table and the column sums become
+// DMMA GEMMs: for column m and parity plane q,
+//   out[pair][c] = sum_r Pq[r][pair] * Cq[r][c],   c = 16 coefficient columns
+// with Cq rows (degree l = m + 2r + q) = {vort, div, phi', psi, chi, w_psi,
+// w_chi, 0} (re, im): the psi/chi series and, summed by parts, their d/dlat
+// series (w_j = c_{j+1}.z v_{j+1} - c_{j-1}.w v_{j-1}, rc as in sphere.py:
+// 102-111), so all 7 series are P-series.  Plane q's w columns feed the
+// H parity 1 - q.  synth_coef_kernel builds C (row layout of the table,
+// columns rotated by (r & 3) * 4 for conflict-free B fragments);
+// synth_tab_kernel streams table tiles (2D TMA) and C rows (bulk copies)
+// through an mbarrier ring, 4 consumer warps = (parity, 8-pair tile), and
+// writes the packed grid-stage rows and Coriolis terms (state_rows).
+// ---------------------------------------------------------------------
+constexpr int kSK = 16;                       // table rows per plane per stage
+constexpr int kSTS = 4;                       // ring depth
+constexpr int kSTab = 2 * kSK * kPR;          // table doubles per stage
+constexpr int kSStage = kSTab + 2 * kSK * 16; // + coefficient rows
+constexpr size_t kSTabSmem = (size_t)kSTS * kSStage * sizeof(double) +
+                             (size_t)2 * 2 * 16 * 16 * sizeof(double) +
+                             (2 * kSTS + 4) * sizeof(uint64_t);
+static_assert((kSStage * 8) % 128 == 0 && (kSTab * 8) % 128 == 0, "TMA alignment");
+
+__global__ void synth_coef_kernel(ShtView p, const double2 *state, double *Cs) {
+  const int m = blockIdx.x;
+  const int k = blockIdx.y * blockDim.x + threadIdx.x;
+  const int T = p.trunc, nc = p.ncoef;
+  const int half = (T + 3 - m) >> 1;
+  if (k >= 2 * half) return;
+  pdl_trigger();
+  pdl_wait();  // the state comes from the preceding kernel
+  const int kmax = T + 1 - m;  // degrees k = 0..kmax (kmax: l = T + 1)
+  const int off = col_offset(T, m);
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  auto coef = [&](int kk, int f) -> double2 {  // f: 0 vort, 1 div, 2 phi
+    if (kk < 0 || kk >= kmax) return make_double2(0.0, 0.0);
+    return state[(size_t)(f == 2 ? 0 : f + 1) * nc + off + kk];
+  };
+  auto inv_lap = [&](int kk) { return kk >= 0 && kk < kmax ? p.d_lconst[m + kk] : 0.0; };
+  double c[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) c[j] = 0.0;
+  if (k <= kmax) {
+    const double2 z = coef(k, 0), d = coef(k, 1), ph = coef(k, 2);
+    const double il = inv_lap(k);
+    c[0] = z.x;
+    c[1] = z.y;
+    c[2] = d.x;
+    c[3] = d.y;
+    c[4] = ph.x;
+    c[5] = ph.y;
+    c[6] = z.x * il;
+    c[7] = z.y * il;
+    c[8] = d.x * il;
+    c[9] = d.y * il;
+    // w_k = c_{k+1}.z v_{k+1} - c_{k-1}.w v_{k-1}, v = psi, chi
+    const double czp = k + 1 <= kmax ? rc[k + 1].z : 0.0;
+    const double cwm = k >= 1 ? rc[k - 1].w : 0.0;
+    const double ilp = inv_lap(k + 1), ilm = inv_lap(k - 1);
+    const double2 zp = coef(k + 1, 0), zm = coef(k - 1, 0), dp = coef(k + 1, 1), dm = coef(k - 1, 1);
+    c[10] = czp * (zp.x * ilp) - cwm * (zm.x * ilm);
+    c[11] = czp * (zp.y * ilp) - cwm * (zm.y * ilm);
+    c[12] = czp * (dp.x * ilp) - cwm * (dm.x * ilm);
+    c[13] = czp * (dp.y * ilp) - cwm * (dm.y * ilm);
+  }
+  const int q = k & 1, r = k >> 1;
+  const size_t row = (size_t)(p.d_ptoff[m] / p.nt16) + (size_t)q * half + r;
+  double *o = Cs + row * 16;
+  const int rot = (r & 3) << 2;
+#pragma unroll
+  for (int j = 0; j < 16; j += 2)
+    *reinterpret_cast<double2 *>(o + (j ^ rot)) = make_double2(c[j], c[j + 1]);
+}
+
+constexpr int kSynThreads = 6 * 32;  // 4 consumer warps, TMA producer, epilogue warp
+
+__global__ void __launch_bounds__(kSynThreads) synth_tab_kernel(ShtView p,
+                                                                const __grid_constant__ CUtensorMap tmap,
+                                                                const double *Cs, SynthArgs a) {
+  extern __shared__ __align__(128) double ssm[];
+  double *Out = ssm + (size_t)kSTS * kSStage;  // [2 buffers][2 planes][16 pairs][16]
+  uint64_t *full = reinterpret_cast<uint64_t *>(Out + 2 * 2 * 16 * 16);
+  uint64_t *empty = full + kSTS;
+  uint64_t *ofull = empty + kSTS;   // [2] item sums ready (128 consumer threads)
+  uint64_t *oempty = ofull + 2;     // [2] item rows written (epilogue warp)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int T = p.trunc;
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kSTS; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, 4);
+    }
+    for (int b2 = 0; b2 < 2; ++b2) {
+      mbar_init(ofull + b2, 128);  // every consumer thread releases its own writes
+      mbar_init(oempty + b2, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();  // coefficient rows come from synth_coef_kernel
+  const int2 rng = p.d_sblk[blockIdx.x];
+  if (wid == 4) {
+    // ---------------- producer (one lane) ----------------
+    if (lane != 0) return;
+    const unsigned bytes = (unsigned)((kSTab + 2 * kSK * 16) * sizeof(double));
+    int qn = 0;
+    for (int it = rng.x; it < rng.y; ++it) {
+      const int2 itm = p.d_slist[it];
+      const int m = itm.x, pb = itm.y;
+      const int half = (T + 3 - m) >> 1;
+      const int nst = (half + kSK - 1) / kSK;
+      const int row0 = (int)(p.d_ptoff[m] / p.nt16);
+      for (int st = 0; st < nst; ++st, ++qn) {
+        const int slot = qn % kSTS, pass = qn / kSTS;
+        if (pass > 0) mbar_wait(empty + slot, (pass - 1) & 1);
+        mbar_expect_tx(full + slot, bytes);
+        double *sb = ssm + (size_t)slot * kSStage;
+        const int r0 = st * kSK;
+        tma_2d(sb, &tmap, pb * 16, row0 + r0, full + slot);
+        tma_2d(sb + kSK * kPR, &tmap, pb * 16, row0 + half + r0, full + slot);
+        bulk_g2s(sb + kSTab, Cs + (size_t)(row0 + r0) * 16, kSK * 16 * sizeof(double), full + slot);
+        bulk_g2s(sb + kSTab + kSK * 16, Cs + (size_t)(row0 + half + r0) * 16,
+                 kSK * 16 * sizeof(double), full + slot);
+      }
+    }
+    return;
+  }
+  if (wid == 5) {
+    // ---------------- epilogue warp: Fourier rows of the finished items ----
+    int n = 0;
+    for (int it = rng.x; it < rng.y; ++it, ++n) {
+      const int2 itm = p.d_slist[it];
+      const int m = itm.x, pb = itm.y;
+      const int ip = pb * 16 + lane;
+      const bool ep = lane < 16 && ip < p.nh;
+      double rcos = 0.0;
+      int jn = 0, js = 0;
+      double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+      if (ep) {
+        rcos = p.d_rcos[ip];
+        jn = p.d_jn[ip];
+        js = p.d_js[ip];
+        if (a.want_lc) {
+          fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
+          fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
+        }
+      }
+      const int buf = n & 1;
+      mbar_wait(ofull + buf, (n >> 1) & 1);
+      const double *ob = Out + (size_t)buf * 2 * 16 * 16;
+      double2 sp[2][5], sh[2][2];
+      if (ep) {
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const double *o = ob + ((size_t)qq * 16 + lane) * 16;
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2) sp[qq][s2] = make_double2(o[2 * s2], o[2 * s2 + 1]);
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2)  // plane qq's w columns: H parity 1 - qq
+            sh[1 - qq][s2] = make_double2(o[10 + 2 * s2] * rcos, o[11 + 2 * s2] * rcos);
+        }
+      }
+      if (ep) state_rows(p, a, m, ip, jn, js, rcos, sp, sh, fr);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(oempty + buf);  // buffer reads long complete
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int lr = lane >> 2, lc4 = lane & 3;
+  const int q = wid & 1, t = wid >> 1;  // parity plane, 8-pair tile
+  int qn = 0, n = 0;
+  for (int it = rng.x; it < rng.y; ++it, ++n) {
+    const int2 itm = p.d_slist[it];
+    const int m = itm.x;
+    const int half = (T + 3 - m) >> 1;
+    const int nst = (half + kSK - 1) / kSK;
+    double acc[4][2][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int nn = 0; nn < 2; ++nn) acc[u][nn][0] = acc[u][nn][1] = 0.0;
+    for (int st = 0; st < nst; ++st, ++qn) {
+      const int slot = qn % kSTS;
+      mbar_wait(full + slot, (qn / kSTS) & 1);
+      const double *sb = ssm + (size_t)slot * kSStage;
+      const double *sT = sb + q * kSK * kPR;
+      const double *sC = sb + kSTab + q * kSK * 16;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = 4 * u + lc4;  // row within the stage
+        const bool valid = st * kSK + rr < half;
+        const double av = sT[rr * kPR + t * 8 + lr];
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn) {
+          const double bv = valid ? sC[rr * 16 + ((nn * 8 + lr) ^ (lc4 << 2))] : 0.0;
+          dmma(acc[u][nn][0], acc[u][nn][1], av, bv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+    }
+    // hand the item's sums to the epilogue warp (double-buffered)
+    const int buf = n & 1;
+    if (n >= 2) mbar_wait(oempty + buf, ((n >> 1) - 1) & 1);
+    double *ob = Out + (size_t)buf * 2 * 16 * 16;
+    // C fragment: pair t*8 + lr, columns nn*8 + 2*lc4 + {0, 1}
+#pragma unroll
+    for (int nn = 0; nn < 2; ++nn) {
+      double *o = ob + ((size_t)q * 16 + t * 8 + lr) * 16 + nn * 8 + 2 * lc4;
+      o[0] = (acc[0][nn][0] + acc[1][nn][0]) + (acc[2][nn][0] + acc[3][nn][0]);
+      o[1] = (acc[0][nn][1] + acc[1][nn][1]) + (acc[2][nn][1] + acc[3][nn][1]);
+    }
+    mbar_arrive(ofull + buf);
+  }
+}
+
 // FFT size of the tendency path: smallest 7-smooth n >= 3T+1 (the user
 // grid's nlon when that is already 7-smooth and alias-free)
 static bool smooth7(int n) {
@@ -1963,7 +2187,14 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
               &p->ptab_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, p->d_ptab, dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          const cuuint32_t box16[2] = {(cuuint32_t)kPR, (cuuint32_t)kSK};
+          if (cr == CUDA_SUCCESS)
+            cr = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(
+                &p->ptab_map16, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, p->d_ptab, dims, strides, box16,
+                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
           if (cr != CUDA_SUCCESS) e = cudaErrorInvalidValue;
+          p->tab_rows = (int)(tot / p->nt16);
         }
       }
       if (e == cudaSuccess) {
@@ -2031,6 +2262,8 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_rcos16);
   cudaFree(p->d_titems);
   cudaFree(p->d_sitems);
+  cudaFree(p->d_sblk);
+  cudaFree(p->d_slist);
   cudaFree(p->d_scnt);
   cudaFree(p->d_spart);
   cudaFree(p->d_tw);
@@ -2046,7 +2279,7 @@ extern "C" int swx_sht_destroy(swx_sht p) {
 //   A    : nm * 4 * nhp * kAS double
 struct ShtWs {
   double2 *c2r, *Q, *lc;
-  double *grid, *A;
+  double *grid, *A, *Cs;
   size_t bytes;
 };
 static size_t al(size_t b) { return (b + 255) / 256 * 256; }
@@ -2063,6 +2296,9 @@ static ShtWs carve(swx_sht p, void *base) {
   w.A = (double *)(c + o);
   o += al(std::max((size_t)p->nm * 4 * p->nhp * kAS, (size_t)p->nm * 4 * p->nt16 * kAG) *
           sizeof(double));
+  // table-synthesis coefficient rows (+ one stage of slack for the last column)
+  w.Cs = (double *)(c + o);
+  o += al(p->use_tab ? (size_t)(p->tab_rows + 2 * kSK) * 16 * sizeof(double) : 0);
   w.bytes = o;
   return w;
 }
@@ -2329,6 +2565,61 @@ extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_d
   return SWX_OK;
 }
 
+// table synthesis of the state: coefficient rows, then the streamed DMMA sums.
+// Items (m, 16-pair block) are assigned to persistent CTAs longest-first to
+// the least-loaded CTA (cost = stages + 1), once per plan.
+static int launch_synth_tab(swx_sht p, const SynthArgs &a, ShtWs &w, cudaStream_t s) {
+  const int T = p->trunc;
+  if (!p->d_sblk) {
+    SWX_CUDA_TRY(cudaFuncSetAttribute(synth_tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSTabSmem));
+    int b = 0;
+    SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, synth_tab_kernel, kSynThreads,
+                                                               kSTabSmem));
+    int dev = 0, nsm = 0;
+    SWX_CUDA_TRY(cudaGetDevice(&dev));
+    SWX_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    std::vector<std::pair<int, int2>> items;  // (cost, (m, pb))
+    const int npb = p->nt16 / 16;
+    for (int m = 0; m <= T; ++m) {
+      const int half = (T + 3 - m) / 2;
+      const int cost = (half + kSK - 1) / kSK + 1;
+      for (int pb = 0; pb < npb; ++pb) items.push_back({cost, make_int2(m, pb)});
+    }
+    std::stable_sort(items.begin(), items.end(),
+                     [](const std::pair<int, int2> &x, const std::pair<int, int2> &y) {
+                       return x.first > y.first;
+                     });
+    const int nc = std::max(1, std::min((int)items.size(), nsm * std::max(b, 1)));
+    std::vector<std::vector<int2>> lists(nc);
+    std::vector<long long> load(nc, 0);
+    for (auto &it : items) {  // LPT: least-loaded CTA first
+      int k = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      lists[k].push_back(it.second);
+      load[k] += it.first;
+    }
+    std::vector<int2> blk(nc), flat;
+    for (int k = 0; k < nc; ++k) {
+      blk[k] = make_int2((int)flat.size(), (int)(flat.size() + lists[k].size()));
+      flat.insert(flat.end(), lists[k].begin(), lists[k].end());
+    }
+    int2 *d_blk = nullptr, *d_list = nullptr;
+    SWX_CUDA_TRY(cudaMalloc(&d_blk, sizeof(int2) * blk.size()));
+    SWX_CUDA_TRY(cudaMalloc(&d_list, sizeof(int2) * flat.size()));
+    SWX_CUDA_TRY(cudaMemcpy(d_blk, blk.data(), sizeof(int2) * blk.size(), cudaMemcpyHostToDevice));
+    SWX_CUDA_TRY(cudaMemcpy(d_list, flat.data(), sizeof(int2) * flat.size(), cudaMemcpyHostToDevice));
+    p->d_sblk = d_blk;
+    p->d_slist = d_list;
+    p->n_sblk = nc;
+  }
+  SWX_CUDA_TRY(launch_pdl(synth_coef_kernel, dim3(T + 1, (T + 3 + 127) / 128), dim3(128), 0, s,
+                          static_cast<const ShtView &>(*p), a.coef, w.Cs));
+  SWX_CUDA_TRY(launch_pdl(synth_tab_kernel, dim3(p->n_sblk), dim3(kSynThreads), kSTabSmem, s,
+                          static_cast<const ShtView &>(*p), p->ptab_map16, (const double *)w.Cs,
+                          a));
+  return SWX_OK;
+}
+
 template <int R>
 static int launch_grid_sq1(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
   using C = SqCfg<R, R>;
@@ -2416,9 +2707,14 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
     a.nfreq = p->nfreq_t;
     a.zpack = 1;  // packed north/south rows for the fused grid stage
-    int nt;
-    dim3 g = synth_grid(p, 1, &nt);
-    if ((rc = launch_synth<0>(p, g, nt, a, s))) return rc;
+    static const int st_tab = env_int("SWX_SYNTH_TAB", 1);
+    if (st_tab) {
+      if ((rc = launch_synth_tab(p, a, w, s))) return rc;
+    } else {
+      int nt;
+      dim3 g = synth_grid(p, 1, &nt);
+      if ((rc = launch_synth<0>(p, g, nt, a, s))) return rc;
+    }
     mark(1);
     mark(2);
     mark(3);
