@@ -2707,7 +2707,9 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
     a.nfreq = p->nfreq_t;
     a.zpack = 1;  // packed north/south rows for the fused grid stage
-    static const int st_tab = env_int("SWX_SYNTH_TAB", 1);
+    // table synthesis (DMMA): correct but slower than the recurrence kernel at
+    // T256 (2 CTAs/SM at 144 registers) -- opt-in
+    static const int st_tab = env_int("SWX_SYNTH_TAB", 0);
     if (st_tab) {
       if ((rc = launch_synth_tab(p, a, w, s))) return rc;
     } else {
