@@ -215,13 +215,18 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
   }
 }
 
+#ifndef SWX_SYNTH_MINB
+#define SWX_SYNTH_MINB 1  // resident state-synthesis CTAs per SM the register budget targets
+#endif
+
 // SPLIT = 2: the CTA holds two half-blocks of NT = blockDim/2 threads (one
 // per latitude pair each); for columns longer than 96 degrees the second
 // half starts mid-column (a multiple of kSeg) from the plan-time recurrence
 // checkpoint, halving the per-thread walk of the long columns; the halves'
 // partial sums are added in a fixed order (first + second).
 template <int MODE, int SPLIT>
-__global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_kernel(ShtView p,
+__global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
+                                  MODE == 0 && SPLIT == 1 ? SWX_SYNTH_MINB : 1) synth_kernel(ShtView p,
                                                                                   SynthArgs a) {
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
@@ -229,8 +234,12 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
   extern __shared__ __align__(16) double smem_syn[];
   const int NT = blockDim.x / SPLIT;
   const int half = threadIdx.x / NT, tt0 = threadIdx.x - half * NT;
-  double2 *cs = reinterpret_cast<double2 *>(smem_syn) + (size_t)half * NS * kSL;  // [NS][kSL]
-  double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)SPLIT * NS * kSL * 2) +
+  // staged series: NS P-series; MODE 0 adds the two d/dlat series summed by
+  // parts (w_k = c_{k+1}.z v_{k+1} - c_{k-1}.w v_{k-1}, v = psi, chi), so
+  // sum_k H_k v_k = rcos sum_k P_k w_k and no per-pair H arithmetic is needed
+  constexpr int NC = NS + NH;
+  double2 *cs = reinterpret_cast<double2 *>(smem_syn) + (size_t)half * NC * kSL;  // [NC][kSL]
+  double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)SPLIT * NC * kSL * 2) +
                  (size_t)half * (kSL + 2);
   int4 itm = make_int4(blockIdx.x, 0, 0, -1);
   if (MODE == 0 && SPLIT == 1 && a.items) itm = a.items[blockIdx.x];
@@ -282,9 +291,13 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
   // recurrence constants split for two 16-byte loads per degree:
   // rcA[t] = {e_{l-1}, 1/e_l} (recurrence), rcB[t] = {(l+1)e_l, l e_{l+1}} (H)
   double2 *rcA = reinterpret_cast<double2 *>(rcs), *rcB = rcA + (kSL + 2);
-  for (int ch = 0; ch < nchunk; ++ch) {
+  // MODE 0: the w-series also pair P_{T+1} (k = kmax) with w_kmax, so the
+  // column's last segment runs one degree further (P-series coefficients 0)
+  const int kw = (NH > 0 && ke == kmax) ? kmax + 1 : ke;
+  const int nchunk_w = SPLIT == 2 ? nchunk : max(nchunk, (kw - kb + kSL - 1) / kSL);
+  for (int ch = 0; ch < nchunk_w; ++ch) {
     const int k0 = kb + ch * kSL;  // chunk start (even)
-    const int n = max(0, min(kSL, ke - k0));
+    const int n = max(0, min(kSL, kw - k0));
     __syncthreads();
     // past the column end the constants and coefficients are zero, so the
     // walk needs no bounds checks (the recurrence then produces zeros)
@@ -297,16 +310,35 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
     }
     for (int t = tt0; t < ((n + 1) & ~1); t += NT) {
       const int s = off + k0 + t;
-      const bool in = t < n;
+      const int k = k0 + t;
+      const bool in = t < n && k < kmax;
       if (MODE == 0) {
-        const double il = in ? p.d_lconst[m + k0 + t] : 0.0;
+        const double il = in ? p.d_lconst[m + k] : 0.0;
         const double2 z = in ? a.coef[nc + s] : make_double2(0.0, 0.0);
         const double2 d = in ? a.coef[2 * nc + s] : make_double2(0.0, 0.0);
         cs[0 * kSL + t] = z;
-        cs[(NS > 1 ? 1 : 0) * kSL + t] = d;
-        cs[(NS > 2 ? 2 : 0) * kSL + t] = in ? a.coef[s] : make_double2(0.0, 0.0);
-        cs[(NS > 3 ? 3 : 0) * kSL + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
-        cs[(NS > 4 ? 4 : 0) * kSL + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+        cs[(NC > 1 ? 1 : 0) * kSL + t] = d;
+        cs[(NC > 2 ? 2 : 0) * kSL + t] = in ? a.coef[s] : make_double2(0.0, 0.0);
+        cs[(NC > 3 ? 3 : 0) * kSL + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
+        cs[(NC > 4 ? 4 : 0) * kSL + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+        // w-series of psi, chi at degree k (zero past the column)
+        double2 wz = make_double2(0.0, 0.0), wd = wz;
+        if (t < n && k <= kmax) {
+          if (k + 1 < kmax) {
+            const double cz = rc[k + 1].z * p.d_lconst[m + k + 1];
+            const double2 zp = a.coef[nc + s + 1], dp = a.coef[2 * nc + s + 1];
+            wz = make_double2(cz * zp.x, cz * zp.y);
+            wd = make_double2(cz * dp.x, cz * dp.y);
+          }
+          if (k >= 1 && k - 1 < kmax) {
+            const double cw = rc[k - 1].w * p.d_lconst[m + k - 1];
+            const double2 zm = a.coef[nc + s - 1], dm = a.coef[2 * nc + s - 1];
+            wz = make_double2(wz.x - cw * zm.x, wz.y - cw * zm.y);
+            wd = make_double2(wd.x - cw * dm.x, wd.y - cw * dm.y);
+          }
+        }
+        cs[(NC > 5 ? 5 : 0) * kSL + t] = wz;
+        cs[(NC > 6 ? 6 : 0) * kSL + t] = wd;
       } else {
         cs[t] = in ? a.coef[(size_t)field * nc + s] : make_double2(0.0, 0.0);
       }
@@ -315,17 +347,8 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
     // two degrees per iteration (static parity q = 0, 1: l - m = k0 + tt)
     // entering: pm1 = P_{k-1}, p0 = P_k, p1 = P_{k+1}
     for (int t = 0; t < n; t += 2) {
-      double H0 = 0.0, H1 = 0.0;
-      if (NH > 0) {
-        const double2 c0 = rcB[t];
-        H0 = (c0.x * pm1 - c0.y * p1) * rcos;
-      }
       const double2 r2 = rcA[t + 2];
       const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
-      if (NH > 0) {
-        const double2 c1 = rcB[t + 1];
-        H1 = (c1.x * p0 - c1.y * p2) * rcos;
-      }
       const double2 r3 = rcA[t + 3];
       const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
 #pragma unroll
@@ -337,13 +360,12 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
         sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
       }
 #pragma unroll
-      for (int s2 = 0; s2 < NH; ++s2) {
-        const double2 v0 = cs[(NS > 3 ? 3 + s2 : 0) * kSL + t];
-        const double2 v1 = cs[(NS > 3 ? 3 + s2 : 0) * kSL + t + 1];
-        sh[0][s2].x = fma(H0, v0.x, sh[0][s2].x);
-        sh[0][s2].y = fma(H0, v0.y, sh[0][s2].y);
-        sh[1][s2].x = fma(H1, v1.x, sh[1][s2].x);
-        sh[1][s2].y = fma(H1, v1.y, sh[1][s2].y);
+      for (int s2 = 0; s2 < NH; ++s2) {  // P of parity q feeds the H parity 1 - q
+        const double2 w0 = cs[(NS + s2) * kSL + t], w1 = cs[(NS + s2) * kSL + t + 1];
+        sh[1][s2].x = fma(p0, w0.x, sh[1][s2].x);
+        sh[1][s2].y = fma(p0, w0.y, sh[1][s2].y);
+        sh[0][s2].x = fma(p1, w1.x, sh[0][s2].x);
+        sh[0][s2].y = fma(p1, w1.y, sh[0][s2].y);
       }
       pm1 = p1;
       p0 = p2;
@@ -441,6 +463,10 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512) synth_ker
     return;
   }
   if constexpr (MODE == 0) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int s2 = 0; s2 < NH; ++s2) sh[q][s2] = make_double2(sh[q][s2].x * rcos, sh[q][s2].y * rcos);
     trace_mark(1);
     const double2 fr[2] = {make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]),
                            make_double2(p.d_frow[js], p.d_frow[p.nlat + js])};
@@ -2406,7 +2432,7 @@ static int check_ws(swx_sht p, void *ws, size_t bytes) {
 }
 
 static size_t synth_smem(int ns, int nh, int split, int nt) {
-  const size_t stage = (size_t)split * (ns * kSL * 2 + (kSL + 2) * 4) * sizeof(double);
+  const size_t stage = (size_t)split * ((ns + nh) * kSL * 2 + (kSL + 2) * 4) * sizeof(double);
   const size_t red = split == 2 ? (size_t)nt * 4 * (ns + nh) * sizeof(double) : 0;
   return std::max(stage, red);
 }
