@@ -224,22 +224,31 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
 // half starts mid-column (a multiple of kSeg) from the plan-time recurrence
 // checkpoint, halving the per-thread walk of the long columns; the halves'
 // partial sums are added in a fixed order (first + second).
+// SPLIT = 3 (state synthesis): two thread groups per latitude pair share the
+// staged column and each run the recurrence; group 0 sums (vort, div, phi'),
+// group 1 (psi, chi) and the two d/dlat series -- twice the warps on the long
+// columns' critical path, half the accumulators per thread; group 1 hands
+// its sums to group 0 through shared memory.
 template <int MODE, int SPLIT>
 __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
                                   MODE == 0 && SPLIT == 1 ? SWX_SYNTH_MINB : 1) synth_kernel(ShtView p,
                                                                                   SynthArgs a) {
+  constexpr bool GRP = SPLIT == 3;
+  constexpr int NSPL = GRP ? 2 : SPLIT;  // thread sets per CTA
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
   constexpr int NACC = 4 * (NS + NH);
   extern __shared__ __align__(16) double smem_syn[];
-  const int NT = blockDim.x / SPLIT;
-  const int half = threadIdx.x / NT, tt0 = threadIdx.x - half * NT;
+  const int NT = blockDim.x / NSPL;
+  const int grp = threadIdx.x / NT, tt0 = threadIdx.x - grp * NT;
+  const int half = GRP ? 0 : grp;  // staging set (groups share one)
   // staged series: NS P-series; MODE 0 adds the two d/dlat series summed by
   // parts (w_k = c_{k+1}.z v_{k+1} - c_{k-1}.w v_{k-1}, v = psi, chi), so
   // sum_k H_k v_k = rcos sum_k P_k w_k and no per-pair H arithmetic is needed
   constexpr int NC = NS + NH;
   double2 *cs = reinterpret_cast<double2 *>(smem_syn) + (size_t)half * NC * kSL;  // [NC][kSL]
-  double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)SPLIT * NC * kSL * 2) +
+  constexpr int NSTG = GRP ? 1 : NSPL;  // staging sets
+  double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)NSTG * NC * kSL * 2) +
                  (size_t)half * (kSL + 2);
   int4 itm = make_int4(blockIdx.x, 0, 0, -1);
   if (MODE == 0 && SPLIT == 1 && a.items) itm = a.items[blockIdx.x];
@@ -286,7 +295,9 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
     for (int s = 0; s < (NH > 0 ? NH : 1); ++s) sh[q][s] = make_double2(0.0, 0.0);
   }
   pdl_wait();  // the coefficients come from the preceding kernel
-  const int nchunk0 = (split + kSL - 1) / kSL, nchunk1 = (kmax - split + kSL - 1) / kSL;
+  const int kext = NH > 0 ? 1 : 0;  // MODE 0: one more degree (P_{T+1}) for the w-series
+  const int nchunk0 = (split + (split == kmax ? kext : 0) + kSL - 1) / kSL;
+  const int nchunk1 = (kmax + kext - split + kSL - 1) / kSL;
   const int nchunk = SPLIT == 2 ? max(nchunk0, nchunk1) : nchunk0;
   // recurrence constants split for two 16-byte loads per degree:
   // rcA[t] = {e_{l-1}, 1/e_l} (recurrence), rcB[t] = {(l+1)e_l, l e_{l+1}} (H)
@@ -295,20 +306,21 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
   // column's last segment runs one degree further (P-series coefficients 0)
   const int kw = (NH > 0 && ke == kmax) ? kmax + 1 : ke;
   const int nchunk_w = SPLIT == 2 ? nchunk : max(nchunk, (kw - kb + kSL - 1) / kSL);
+  const int tst = GRP ? (int)threadIdx.x : tt0, nst = GRP ? (int)blockDim.x : NT;  // stagers
   for (int ch = 0; ch < nchunk_w; ++ch) {
     const int k0 = kb + ch * kSL;  // chunk start (even)
     const int n = max(0, min(kSL, kw - k0));
     __syncthreads();
     // past the column end the constants and coefficients are zero, so the
     // walk needs no bounds checks (the recurrence then produces zeros)
-    for (int t = tt0; t < kSL + 2; t += NT) {
+    for (int t = tst; t < kSL + 2; t += nst) {
       const int k = k0 + t;
       double4 c = make_double4(0.0, 0.0, 0.0, 0.0);
       if (n > 0 && k <= kmax) c = rc[k];
       rcA[t] = make_double2(c.x, c.y);
       rcB[t] = make_double2(c.z, c.w);
     }
-    for (int t = tt0; t < ((n + 1) & ~1); t += NT) {
+    for (int t = tst; t < ((n + 1) & ~1); t += nst) {
       const int s = off + k0 + t;
       const int k = k0 + t;
       const bool in = t < n && k < kmax;
@@ -351,16 +363,28 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
       const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
       const double2 r3 = rcA[t + 3];
       const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
+      if (!GRP || grp == 0) {
 #pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2) {
-        const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
-        sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
-        sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
-        sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
-        sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
+        for (int s2 = 0; s2 < (GRP ? 3 : NS); ++s2) {
+          const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
+          sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
+          sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
+          sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
+          sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
+        }
+      }
+      if (GRP && grp == 1) {
+#pragma unroll
+        for (int s2 = 3; s2 < NS; ++s2) {
+          const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
+          sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
+          sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
+          sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
+          sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
+        }
       }
 #pragma unroll
-      for (int s2 = 0; s2 < NH; ++s2) {  // P of parity q feeds the H parity 1 - q
+      for (int s2 = 0; s2 < ((GRP && grp == 0) ? 0 : NH); ++s2) {  // P of parity q feeds H parity 1 - q
         const double2 w0 = cs[(NS + s2) * kSL + t], w1 = cs[(NS + s2) * kSL + t + 1];
         sh[1][s2].x = fma(p0, w0.x, sh[1][s2].x);
         sh[1][s2].y = fma(p0, w0.y, sh[1][s2].y);
@@ -405,6 +429,29 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
         sh[q][s2].x += red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2];
         sh[q][s2].y += red[(size_t)tt0 * NACC + 4 * NS + (q * NH + s2) * 2 + 1];
       }
+    }
+  }
+  if constexpr (GRP) {
+    // group 1 hands (psi, chi) and the d/dlat sums to group 0
+    __syncthreads();
+    double2 *red = reinterpret_cast<double2 *>(smem_syn);  // [NT][8] (staging reused)
+    if (grp == 1) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        red[(size_t)tt0 * 8 + q * 4 + 0] = sp[q][3];
+        red[(size_t)tt0 * 8 + q * 4 + 1] = sp[q][4];
+        red[(size_t)tt0 * 8 + q * 4 + 2] = sh[q][0];
+        red[(size_t)tt0 * 8 + q * 4 + 3] = sh[q][1];
+      }
+    }
+    __syncthreads();
+    if (grp == 1) return;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      sp[q][3] = red[(size_t)tt0 * 8 + q * 4 + 0];
+      sp[q][4] = red[(size_t)tt0 * 8 + q * 4 + 1];
+      sh[q][0] = red[(size_t)tt0 * 8 + q * 4 + 2];
+      sh[q][1] = red[(size_t)tt0 * 8 + q * 4 + 3];
     }
   }
   if constexpr (MODE == 0 && SPLIT == 1) {
@@ -2441,6 +2488,16 @@ template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
   static const int st_nt = env_int("SWX_SYNTH_NT", 0), st_split = env_int("SWX_SYNTH_SPLIT", 0);
+  static const int st_grp = env_int("SWX_SYNTH_GRP", 1);
+  if (MODE == 0 && st_grp && nt <= 256) {
+    // two series groups per latitude pair (SPLIT = 3)
+    const size_t smem = std::max(synth_smem(ns, nh, 1, nt), (size_t)nt * 8 * sizeof(double2));
+    auto k = synth_kernel<MODE, 3>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(2 * nt), smem, s, static_cast<const ShtView &>(*p), a));
+    return SWX_OK;
+  }
   static const int st_col = env_int("SWX_SYNTH_COL", 0);
   if (MODE == 0 && st_col && synth_col_smem(p->trunc) <= 64 * 1024) {
     const int ntc = st_nt > 0 ? st_nt : nt;
