@@ -129,6 +129,9 @@ struct SynthArgs {
   const int4 *items = nullptr;
   int *cnt = nullptr;
   double2 *part = nullptr;
+  // nyb > 0: 1D grid, block b = column b / nyb, pair block b % nyb (all pair
+  // blocks of the long columns dispatch first)
+  int nyb = 0;
 };
 
 // bin k of the packed complex row z = north + i south of field f (zero above T)
@@ -250,10 +253,10 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
   constexpr int NSTG = GRP ? 1 : NSPL;  // staging sets
   double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)NSTG * NC * kSL * 2) +
                  (size_t)half * (kSL + 2);
-  int4 itm = make_int4(blockIdx.x, 0, 0, -1);
+  int4 itm = make_int4(a.nyb > 0 ? blockIdx.x / a.nyb : blockIdx.x, 0, 0, -1);
   if (MODE == 0 && SPLIT == 1 && a.items) itm = a.items[blockIdx.x];
   const int m = itm.x;
-  const int i = blockIdx.y * NT + tt0;
+  const int i = (a.nyb > 0 ? blockIdx.x % a.nyb : blockIdx.y) * NT + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
   pdl_trigger();
   if (MODE == 0) trace_mark(0);
@@ -646,6 +649,205 @@ __global__ void __launch_bounds__(256) synth_col_kernel(ShtView p, SynthArgs a, 
 static size_t synth_col_smem(int trunc) {
   const int KS = synth_col_kp(trunc, 0) + 2;
   return (size_t)(kSCS + 2) * KS * sizeof(double2);
+}
+
+// State synthesis, PPT latitude pairs per thread.  The column sums are bound
+// by shared-memory broadcast loads (every coefficient load returns 512 B to
+// a warp for 2 FMAs per pair), so each loaded coefficient now feeds PPT
+// pairs: CTA = column m, thread t owns pairs t, t + NT, ...; same staging,
+// recurrence, d/dlat series summed by parts and epilogue as synth_kernel<0>.
+template <int PPT>
+__global__ void __launch_bounds__(256) synth_pp_kernel(ShtView p, SynthArgs a) {
+  constexpr int NS = 5, NH = 2, NC = NS + NH;
+  extern __shared__ __align__(16) double smem_syn[];
+  const int NT = blockDim.x;
+  double2 *cs = reinterpret_cast<double2 *>(smem_syn);  // [NC][kSL]
+  double2 *rcA = reinterpret_cast<double2 *>(smem_syn + (size_t)NC * kSL * 2);  // [kSL + 4]
+  // item: (m, kb, ke, seg) -- a whole column (seg < 0) or one of the two
+  // checkpoint-aligned segments of a long column (a.items)
+  const int4 itm = a.items ? a.items[blockIdx.x] : make_int4(blockIdx.x, 0, 0, -1);
+  const int m = itm.x;
+  pdl_trigger();
+  trace_mark(0);
+  const int T = p.trunc, nc = p.ncoef;
+  const int off = col_offset(T, m);
+  const int kmax = T + 1 - m;
+  const int kb = itm.w >= 0 ? itm.y : 0, ke = itm.w >= 0 ? itm.z : kmax;
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  double x[PPT], p0[PPT], p1[PPT];
+  double2 sp[PPT][2][NS], sh[PPT][2][NH];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int i = threadIdx.x + j * NT;
+    x[j] = p0[j] = p1[j] = 0.0;
+    if (i < p.nh) {
+      x[j] = p.d_x[i];
+      if (kb == 0) {
+        const double seed = p.d_seed[(size_t)m * p.nh + i];
+        p0[j] = seed;
+        p1[j] = sqrt(2.0 * m + 3.0) * x[j] * seed;  // sphere.py:96-97
+      } else {  // plan-time recurrence checkpoint at degree kb (multiple of kSeg)
+        const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + kb / kSeg) * 3 * p.nh;
+        p0[j] = ck[p.nh + i];
+        p1[j] = ck[2 * p.nh + i];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) sp[j][q][s2] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s2 = 0; s2 < NH; ++s2) sh[j][q][s2] = make_double2(0.0, 0.0);
+    }
+  }
+  pdl_wait();  // the coefficients come from the preceding kernel
+  const int kw = ke == kmax ? kmax + 1 : ke;  // the w-series pair P_{T+1} with w_kmax
+  const int nchunk = (kw - kb + kSL - 1) / kSL;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int k0 = kb + ch * kSL;
+    const int n = min(kSL, kw - k0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kSL + 4; t += NT) {
+      const int k = k0 + t;
+      const double4 c = k <= kmax ? rc[k] : make_double4(0.0, 0.0, 0.0, 0.0);
+      rcA[t] = make_double2(c.x, c.y);
+    }
+    for (int t = threadIdx.x; t < ((n + 1) & ~1); t += NT) {
+      const int s = off + k0 + t;
+      const int k = k0 + t;
+      const bool in = t < n && k < kmax;
+      const double il = in ? p.d_lconst[m + k] : 0.0;
+      const double2 z = in ? a.coef[nc + s] : make_double2(0.0, 0.0);
+      const double2 d = in ? a.coef[2 * nc + s] : make_double2(0.0, 0.0);
+      cs[0 * kSL + t] = z;
+      cs[1 * kSL + t] = d;
+      cs[2 * kSL + t] = in ? a.coef[s] : make_double2(0.0, 0.0);
+      cs[3 * kSL + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
+      cs[4 * kSL + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
+      double2 wz = make_double2(0.0, 0.0), wd = wz;
+      if (t < n && k <= kmax) {
+        if (k + 1 < kmax) {
+          const double cz = rc[k + 1].z * p.d_lconst[m + k + 1];
+          const double2 zp = a.coef[nc + s + 1], dp = a.coef[2 * nc + s + 1];
+          wz = make_double2(cz * zp.x, cz * zp.y);
+          wd = make_double2(cz * dp.x, cz * dp.y);
+        }
+        if (k >= 1 && k - 1 < kmax) {
+          const double cw = rc[k - 1].w * p.d_lconst[m + k - 1];
+          const double2 zm = a.coef[nc + s - 1], dm = a.coef[2 * nc + s - 1];
+          wz = make_double2(wz.x - cw * zm.x, wz.y - cw * zm.y);
+          wd = make_double2(wd.x - cw * dm.x, wd.y - cw * dm.y);
+        }
+      }
+      cs[5 * kSL + t] = wz;
+      cs[6 * kSL + t] = wd;
+    }
+    __syncthreads();
+    for (int t = 0; t < n; t += 2) {
+      const double2 r2 = rcA[t + 2], r3 = rcA[t + 3];
+      double q0[PPT], q1[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const double p2 = fma(x[j], p1[j], -r2.x * p0[j]) * r2.y;  // sphere.py:98-100
+        const double p3 = fma(x[j], p2, -r3.x * p1[j]) * r3.y;
+        q0[j] = p0[j];
+        q1[j] = p1[j];
+        p0[j] = p2;
+        p1[j] = p3;
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) {
+        const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          sp[j][0][s2].x = fma(q0[j], v0.x, sp[j][0][s2].x);
+          sp[j][0][s2].y = fma(q0[j], v0.y, sp[j][0][s2].y);
+          sp[j][1][s2].x = fma(q1[j], v1.x, sp[j][1][s2].x);
+          sp[j][1][s2].y = fma(q1[j], v1.y, sp[j][1][s2].y);
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < NH; ++s2) {  // P of parity q feeds the H parity 1 - q
+        const double2 w0 = cs[(NS + s2) * kSL + t], w1 = cs[(NS + s2) * kSL + t + 1];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          sh[j][1][s2].x = fma(q0[j], w0.x, sh[j][1][s2].x);
+          sh[j][1][s2].y = fma(q0[j], w0.y, sh[j][1][s2].y);
+          sh[j][0][s2].x = fma(q1[j], w1.x, sh[j][0][s2].x);
+          sh[j][0][s2].y = fma(q1[j], w1.y, sh[j][0][s2].y);
+        }
+      }
+    }
+  }
+  if (itm.w >= 0) {
+    // split column: partial sums meet in a.part; the second CTA to arrive
+    // adds them in fixed order (segment 0 + segment 1) and writes the rows
+    constexpr int NP = 2 * (NS + NH);
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int i = threadIdx.x + j * NT;
+      if (i >= p.nh) continue;
+      double2 *mine = a.part + (((size_t)m * 2 + itm.w) * p.nh + i) * NP;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) mine[q * NS + s2] = sp[j][q][s2];
+#pragma unroll
+        for (int s2 = 0; s2 < NH; ++s2) mine[2 * NS + q * NH + s2] = sh[j][q][s2];
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      s_last = atomicAdd(a.cnt + m, 1) == 1;
+      if (s_last) a.cnt[m] = 0;  // ready for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const bool first = itm.w == 0;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int i = threadIdx.x + j * NT;
+      if (i >= p.nh) continue;
+      const double2 *oth = a.part + (((size_t)m * 2 + (1 - itm.w)) * p.nh + i) * NP;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+          const double2 o = __ldcg(oth + q * NS + s2);
+          sp[j][q][s2] = first ? cadd(sp[j][q][s2], o) : cadd(o, sp[j][q][s2]);
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < NH; ++s2) {
+          const double2 o = __ldcg(oth + 2 * NS + q * NH + s2);
+          sh[j][q][s2] = first ? cadd(sh[j][q][s2], o) : cadd(o, sh[j][q][s2]);
+        }
+      }
+    }
+  }
+  trace_mark(1);
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int i = threadIdx.x + j * NT;
+    if (i >= p.nh) continue;
+    const double rcos = p.d_rcos[i];
+    const int jn = p.d_jn[i], js = p.d_js[i];
+    double2 shr[2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int s2 = 0; s2 < NH; ++s2)
+        shr[q][s2] = make_double2(sh[j][q][s2].x * rcos, sh[j][q][s2].y * rcos);
+    double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    if (a.want_lc) {
+      fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
+      fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
+    }
+    state_rows(p, a, m, i, jn, js, rcos, sp[j], shr, fr);
+  }
+  trace_mark(2);
 }
 
 // zero the C2R rows above m = T (cuFFT may overwrite its input)
@@ -2488,7 +2690,27 @@ template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
   static const int st_nt = env_int("SWX_SYNTH_NT", 0), st_split = env_int("SWX_SYNTH_SPLIT", 0);
-  static const int st_grp = env_int("SWX_SYNTH_GRP", 1);
+  static const int st_grp = env_int("SWX_SYNTH_GRP", 0);
+  static const int st_ppt = env_int("SWX_SYNTH_PPT", 2);
+  if (MODE == 0 && (st_ppt == 2 || st_ppt == 3) && p->nh <= 256 * st_ppt && p->d_ckpt) {
+    // PPT latitude pairs per thread: one CTA per column, NT = pairs / PPT
+    const int ntp = std::max(32, ((p->nh + st_ppt - 1) / st_ppt + 31) / 32 * 32);
+    dim3 gp(p->nm, 1, 1);
+    const size_t smem = ((size_t)(ns + nh) * kSL * 2 + (kSL + 4) * 2) * sizeof(double);
+    auto k = st_ppt == 2 ? synth_pp_kernel<2> : synth_pp_kernel<3>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static const int st_items = env_int("SWX_SYNTH_ITEMS", 1);
+    SynthArgs ai = a;
+    if (st_items && p->d_sitems && p->d_spart) {
+      ai.items = p->d_sitems;
+      ai.cnt = p->d_scnt;
+      ai.part = p->d_spart;
+      gp.x = p->n_sitems;
+    }
+    SWX_CUDA_TRY(launch_pdl(k, gp, dim3(ntp), smem, s, static_cast<const ShtView &>(*p), ai));
+    return SWX_OK;
+  }
   if (MODE == 0 && st_grp && nt <= 256) {
     // two series groups per latitude pair (SPLIT = 3)
     const size_t smem = std::max(synth_smem(ns, nh, 1, nt), (size_t)nt * 8 * sizeof(double2));
@@ -2515,13 +2737,17 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
   if (MODE == 0 && p->d_ckpt && st_nt > 0) {
     nt = st_nt;
     g.y = (p->nh + nt - 1) / nt;
+    SynthArgs am = a;
+    am.nyb = g.y;  // column-major dispatch: long columns' blocks first
+    g.x *= g.y;
+    g.y = 1;
     const int sp = st_split && 2 * nt <= 512 ? 2 : 1;
     if (sp == 1 && nt > 256) return fail(SWX_ERR_CONFIG, "SWX_SYNTH_NT > 256");
     const size_t smem = synth_smem(ns, nh, sp, nt);
     auto k = sp == 2 ? synth_kernel<MODE, 2> : synth_kernel<MODE, 1>;
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SWX_CUDA_TRY(launch_pdl(k, g, dim3(sp * nt), smem, s, static_cast<const ShtView &>(*p), a));
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(sp * nt), smem, s, static_cast<const ShtView &>(*p), am));
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
