@@ -167,6 +167,11 @@ int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_div,
 int swx_sht_tendency(swx_sht p, int atoms, const swx_c128 *d_state,
                      swx_c128 *d_out, void *d_workspace, size_t ws_bytes,
                      void *stream);
+/* Record `event` (cudaEvent_t; null clears) on the tendency's stream right
+ * after the synthesis stage of every following swx_sht_tendency[_sub] call,
+ * so independent work on another stream can overlap the lighter grid and
+ * analysis stages instead of the FP64-bound synthesis.                      */
+int swx_sht_set_synth_event(swx_sht p, void *event);
 /* d_out = tendency(d_state) - d_sub, the difference N(a) - N(u) of the
  * ETD2RK stage (steppers.py:262-266) fused into the analysis epilogue;
  * bitwise equal to swx_sht_tendency followed by swx_state_axpy(-1).        */

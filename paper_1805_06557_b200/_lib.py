@@ -55,6 +55,7 @@ SIGNATURES = {
     "swx_sht_uv": (_I, [_P, _P, _P, _P, _P, _P, _S, _P]),
     "swx_sht_tendency": (_I, [_P, _I, _P, _P, _P, _S, _P]),
     "swx_sht_tendency_sub": (_I, [_P, _I, _P, _P, _P, _P, _S, _P]),
+    "swx_sht_set_synth_event": (_I, [_P, _P]),
     "swx_sht_tendency_profile": (_I, [_P, _I, _P, _P, _P, _S, _P, _P]),
     "swx_fp64_fma_probe": (_I, [_P, _I, _I, _P]),
     "swx_host_pack": (_I, [_I, _I, _P, _P]),

@@ -92,6 +92,7 @@ struct ShtView {
 
 struct swx_sht_s : ShtView {
   std::map<long long, cufftHandle> plans;
+  cudaEvent_t synth_done = nullptr;  // recorded after each tendency's synthesis (optional)
   CUtensorMap ptab_map;    // 2D view [rows][nt16] of the P table, box kTBox x 17
   CUtensorMap ptab_map16;  // the same view, box kPR x 16 (table synthesis)
 };
@@ -2691,7 +2692,7 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
   static const int st_nt = env_int("SWX_SYNTH_NT", 0), st_split = env_int("SWX_SYNTH_SPLIT", 0);
   static const int st_grp = env_int("SWX_SYNTH_GRP", 0);
-  static const int st_ppt = env_int("SWX_SYNTH_PPT", 2);
+  static const int st_ppt = env_int("SWX_SYNTH_PPT", 0);
   if (MODE == 0 && (st_ppt == 2 || st_ppt == 3) && p->nh <= 256 * st_ppt && p->d_ckpt) {
     // PPT latitude pairs per thread: one CTA per column, NT = pairs / PPT
     const int ntp = std::max(32, ((p->nh + st_ppt - 1) / st_ppt + 31) / 32 * 32);
@@ -3026,6 +3027,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
       dim3 g = synth_grid(p, 1, &nt);
       if ((rc = launch_synth<0>(p, g, nt, a, s))) return rc;
     }
+    if (p->synth_done) SWX_CUDA_TRY(cudaEventRecord(p->synth_done, s));
     mark(1);
     mark(2);
     mark(3);
@@ -3156,5 +3158,15 @@ extern "C" int swx_trace(int enable, unsigned long long *h_out, int n_ctas) {
     SWX_CUDA_TRY(cudaMemcpyFromSymbol(h_out, swx::g_trace,
                                       sizeof(unsigned long long) * swx::kTraceSlots * n));
   }
+  return SWX_OK;
+}
+
+// Optional overlap hook: record `event` (a cudaEvent_t, or null to clear)
+// after the synthesis of every subsequent tendency of this plan, so a caller
+// can start independent work on another stream once the synthesis -- the
+// FP64-heaviest stage -- has finished (the ETD2RK engine starts psi0(u) there).
+extern "C" int swx_sht_set_synth_event(swx_sht p, void *event) {
+  if (!p) return fail(SWX_ERR_CONFIG, "null plan");
+  p->synth_done = (cudaEvent_t)event;
   return SWX_OK;
 }

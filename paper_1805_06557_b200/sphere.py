@@ -215,6 +215,12 @@ class ShtPlan:
             self.workspace.numel(), stream_ptr(stream)))
         return u, v
 
+    def set_synth_event(self, event=None):
+        """Record ``event`` (torch.cuda.Event) after the synthesis of each
+        following tendency call (None clears)."""
+        _lib.check(self._lib.swx_sht_set_synth_event(
+            self._h, event.cuda_event if event is not None else 0))
+
     def tendency_dev(self, atoms: int, state, out=None, stream=None, sub=None):
         """out = tendency(state) (minus ``sub`` when given, fused on the device)."""
         import torch
