@@ -36,13 +36,15 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True compiles the per-CTA phase marks read by swx_trace."""
     if not force and not stale():
         return LIB
     cuda = os.path.dirname(os.path.dirname(nvcc()))
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared",
            "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-Xptxas", "-warn-spills",
            *[os.path.join(CSRC, s) for s in SOURCES],
+           *(["-DSWX_TRACE"] if trace else []),
            "-o", LIB + ".tmp",
            f"-L{cuda}/lib64", "-lcufft", "-lgomp", f"-Xlinker", f"-rpath={cuda}/lib64"]
     if verbose:
@@ -53,5 +55,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv or "--trace" in sys.argv, verbose=True,
+          trace="--trace" in sys.argv)
     print(LIB)

@@ -104,9 +104,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// records of one kernel start at CTA slot `base`
+// records of one kernel start at CTA slot `base`.  Compiled in only with
+// -DSWX_TRACE (python -m paper_1805_06557_b200.build --trace): the flag load
+// would otherwise sit on every instrumented kernel's critical path.
 __device__ __forceinline__ void trace_mark(int k, int base = 0) {
-  if (g_trace_on && threadIdx.x == 0 && base + blockIdx.x < kTraceCtas && blockIdx.y == 0) {
+#ifdef SWX_TRACE
+  if (threadIdx.x == 0 && g_trace_on && base + blockIdx.x < kTraceCtas && blockIdx.y == 0) {
     unsigned long long *t = g_trace + (size_t)(base + blockIdx.x) * kTraceSlots;
     if (k == 0) {
       unsigned sm;
@@ -115,6 +118,10 @@ __device__ __forceinline__ void trace_mark(int k, int base = 0) {
     }
     t[1 + k] = gtimer();
   }
+#else
+  (void)k;
+  (void)base;
+#endif
 }
 }  // namespace swx
 
