@@ -311,11 +311,15 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
   }
 }
 
+#ifndef SWX_LG_MINB
+#define SWX_LG_MINB 3  // resident CTAs per SM the two-mode kernel's register budget targets
+#endif
+
 // Static-geometry variant with MPL modes per lane group: LPM lanes own MPL
 // modes of the same degree (m = base + g, base + g + 128/LPM, ...), so each
 // factor load from shared memory feeds MPL modes.
 template <int NRHS, int NP, int LPM, int MPL>
-__global__ void __launch_bounds__(128) rexi_lg_mm_kernel(
+__global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
     const int4 *__restrict__ sched, int n_items, int realify, Axpy ep, int fac_ready,
     double2 *__restrict__ out) {
