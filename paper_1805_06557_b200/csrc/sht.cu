@@ -233,12 +233,20 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
 // group 1 (psi, chi) and the two d/dlat series -- twice the warps on the long
 // columns' critical path, half the accumulators per thread; group 1 hands
 // its sums to group 0 through shared memory.
+// SPLIT = 4 (state synthesis): every staged chunk is walked twice from the
+// same recurrence state -- (vort, div, phi') first, then (psi, chi) and the
+// d/dlat series -- so fewer loaded coefficients are live at once and the
+// kernel fits two 7-warp CTAs per SM (<= 128 registers); the recurrence is
+// recomputed (3 of 17 FP64 per degree).
 template <int MODE, int SPLIT>
-__global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
-                                  MODE == 0 && SPLIT == 1 ? SWX_SYNTH_MINB : 1) synth_kernel(ShtView p,
-                                                                                  SynthArgs a) {
+__global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 : 512,
+                                  MODE == 0 && SPLIT == 1   ? SWX_SYNTH_MINB
+                                  : MODE == 0 && SPLIT == 4 ? 2
+                                                            : 1) synth_kernel(ShtView p,
+                                                                              SynthArgs a) {
   constexpr bool GRP = SPLIT == 3;
-  constexpr int NSPL = GRP ? 2 : SPLIT;  // thread sets per CTA
+  constexpr bool TWO = SPLIT == 4;
+  constexpr int NSPL = GRP ? 2 : (TWO ? 1 : SPLIT);  // thread sets per CTA
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
   constexpr int NACC = 4 * (NS + NH);
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
   double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)NSTG * NC * kSL * 2) +
                  (size_t)half * (kSL + 2);
   int4 itm = make_int4(a.nyb > 0 ? blockIdx.x / a.nyb : blockIdx.x, 0, 0, -1);
-  if (MODE == 0 && SPLIT == 1 && a.items) itm = a.items[blockIdx.x];
+  if (MODE == 0 && (SPLIT == 1 || SPLIT == 4) && a.items) itm = a.items[blockIdx.x];
   const int m = itm.x;
   const int i = (a.nyb > 0 ? blockIdx.x % a.nyb : blockIdx.y) * NT + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
@@ -362,14 +370,21 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
     __syncthreads();
     // two degrees per iteration (static parity q = 0, 1: l - m = k0 + tt)
     // entering: pm1 = P_{k-1}, p0 = P_k, p1 = P_{k+1}
+    const double c0 = p0, c1 = p1;  // chunk-entry recurrence state (TWO)
+#pragma unroll 1
+    for (int pass = 0; pass < (TWO ? 2 : 1); ++pass) {
+    if (TWO && pass == 1) {
+      p0 = c0;
+      p1 = c1;
+    }
     for (int t = 0; t < n; t += 2) {
       const double2 r2 = rcA[t + 2];
       const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
       const double2 r3 = rcA[t + 3];
       const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
-      if (!GRP || grp == 0) {
+      if ((!GRP || grp == 0) && (!TWO || pass == 0)) {
 #pragma unroll
-        for (int s2 = 0; s2 < (GRP ? 3 : NS); ++s2) {
+        for (int s2 = 0; s2 < ((GRP || TWO) ? 3 : NS); ++s2) {
           const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
           sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
           sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
@@ -377,7 +392,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
           sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
         }
       }
-      if (GRP && grp == 1) {
+      if ((GRP && grp == 1) || (TWO && pass == 1)) {
 #pragma unroll
         for (int s2 = 3; s2 < NS; ++s2) {
           const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
@@ -388,7 +403,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
         }
       }
 #pragma unroll
-      for (int s2 = 0; s2 < ((GRP && grp == 0) ? 0 : NH); ++s2) {  // P of parity q feeds H parity 1 - q
+      for (int s2 = 0; s2 < (((GRP && grp == 0) || (TWO && pass == 0)) ? 0 : NH); ++s2) {  // H parity 1 - q
         const double2 w0 = cs[(NS + s2) * kSL + t], w1 = cs[(NS + s2) * kSL + t + 1];
         sh[1][s2].x = fma(p0, w0.x, sh[1][s2].x);
         sh[1][s2].y = fma(p0, w0.y, sh[1][s2].y);
@@ -398,6 +413,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
       pm1 = p1;
       p0 = p2;
       p1 = p3;
+    }
     }
   }
   if (SPLIT == 2) {
@@ -458,7 +474,7 @@ __global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
       sh[q][1] = red[(size_t)tt0 * 8 + q * 4 + 3];
     }
   }
-  if constexpr (MODE == 0 && SPLIT == 1) {
+  if constexpr (MODE == 0 && (SPLIT == 1 || SPLIT == 4)) {
     if (itm.w >= 0) {
       constexpr int NP = 2 * (NS + NH);  // partial sums per pair (complex)
       if (has) {
@@ -2692,6 +2708,24 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
   static const int st_nt = env_int("SWX_SYNTH_NT", 0), st_split = env_int("SWX_SYNTH_SPLIT", 0);
   static const int st_grp = env_int("SWX_SYNTH_GRP", 0);
+  static const int st_two = env_int("SWX_SYNTH_TWO", 0);
+  if (MODE == 0 && st_two && nt <= 256) {
+    // two passes per staged chunk (SPLIT = 4), optionally with split items
+    const size_t smem = synth_smem(ns, nh, 1, nt);
+    auto k = synth_kernel<MODE, 4>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static const int st_items2 = env_int("SWX_SYNTH_ITEMS", 0);
+    SynthArgs ai = a;
+    if (st_items2 && p->d_sitems && p->d_spart && g.y == 1) {
+      ai.items = p->d_sitems;
+      ai.cnt = p->d_scnt;
+      ai.part = p->d_spart;
+      g.x = p->n_sitems;
+    }
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), ai));
+    return SWX_OK;
+  }
   static const int st_ppt = env_int("SWX_SYNTH_PPT", 0);
   if (MODE == 0 && (st_ppt == 2 || st_ppt == 3) && p->nh <= 256 * st_ppt && p->d_ckpt) {
     // PPT latitude pairs per thread: one CTA per column, NT = pairs / PPT
