@@ -162,3 +162,29 @@ def test_compute_refuses_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(ConfigurationError):
         _lib.lib()
+
+
+@pytest.mark.parametrize("trunc", [0, 1, 21, 63, 256])
+def test_host_pack_unpack_match_layout(trunc):
+    """swx_host_pack / swx_host_unpack (multithreaded blocked transpose) ==
+    the index-map packing of solvers.py:288-307 (device.pack / unpack)."""
+    import ctypes
+
+    from paper_1805_06557_b200.device import pack, pack_fields, unpack, unpack_fields
+
+    rng = np.random.default_rng(trunc)
+    n = trunc + 1
+    dense = rng.standard_normal((3, n, n)) + 1j * rng.standard_normal((3, n, n))
+    dense = np.tril(dense)  # (l, m) with m <= l
+    ref = pack(dense)
+    out = np.empty_like(ref)
+    pack_fields(tuple(dense), out)
+    assert np.array_equal(out, ref)
+    back = unpack_fields(ref, trunc)
+    assert all(np.array_equal(b, d) for b, d in zip(back, unpack(ref, trunc)))
+    # unpack writes every entry (zeros above the diagonal), no stale memory
+    lib = _lib.load()
+    dst = [np.full((n, n), np.nan + 1j * np.nan) for _ in range(3)]
+    ptrs = (ctypes.c_void_p * 3)(*[d.ctypes.data for d in dst])
+    assert lib.swx_host_unpack(trunc, 3, np.ascontiguousarray(ref).ctypes.data, ptrs) == 0
+    assert all(np.array_equal(a, b) for a, b in zip(dst, dense))
