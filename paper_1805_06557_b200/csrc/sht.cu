@@ -78,6 +78,8 @@ struct ShtView {
   long long *d_ptoff = nullptr;
   double *d_ptab = nullptr;
   double *d_rcos16 = nullptr;  // 1/cos per padded pair (0 on padding)
+  int n_pitems = 0;            // state-synthesis items (m, first pair, pairs)
+  int4 *d_pitems = nullptr;
   int n_sitems = 0;            // state-synthesis items (m, kb, ke, seg), longest first
   int4 *d_sitems = nullptr;
   int *d_scnt = nullptr;       // [m] arrival counters of split columns
@@ -133,6 +135,9 @@ struct SynthArgs {
   // nyb > 0: 1D grid, block b = column b / nyb, pair block b % nyb (all pair
   // blocks of the long columns dispatch first)
   int nyb = 0;
+  // pitems: CTA b runs column pitems[b].x for pairs [y, y + z) -- the long
+  // columns split over two SMs by latitude pairs, one CTA per SM
+  const int4 *pitems = nullptr;
 };
 
 // bin k of the packed complex row z = north + i south of field f (zero above T)
@@ -264,8 +269,15 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
                  (size_t)half * (kSL + 2);
   int4 itm = make_int4(a.nyb > 0 ? blockIdx.x / a.nyb : blockIdx.x, 0, 0, -1);
   if (MODE == 0 && (SPLIT == 1 || SPLIT == 4) && a.items) itm = a.items[blockIdx.x];
+  int pstart = (a.nyb > 0 ? blockIdx.x % a.nyb : blockIdx.y) * NT, pcount = NT;
+  if (MODE == 0 && SPLIT == 1 && a.pitems) {
+    const int4 pi = a.pitems[blockIdx.x];
+    itm = make_int4(pi.x, 0, 0, -1);
+    pstart = pi.y;
+    pcount = pi.z;
+  }
   const int m = itm.x;
-  const int i = (a.nyb > 0 ? blockIdx.x % a.nyb : blockIdx.y) * NT + tt0;
+  const int i = pstart + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
   pdl_trigger();
   if (MODE == 0) trace_mark(0);
@@ -273,7 +285,9 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
   const int off = col_offset(T, m);
   const int kmax = T + 1 - m;
   const double4 *rc = p.d_rc + rc_offset(T, m);
-  const bool has = i < p.nh;
+  const bool has = i < p.nh && tt0 < pcount;
+  // warps without pairs skip the walk (they still stage and synchronise)
+  const bool warp_busy = __any_sync(0xffffffffu, has);
   // this half's degree range [kb, ke) of the column
   int split = kmax;
   if (SPLIT == 2 && kmax > 96) split = ((kmax / 2 + kSeg - 1) / kSeg) * kSeg;
@@ -372,7 +386,7 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
     // entering: pm1 = P_{k-1}, p0 = P_k, p1 = P_{k+1}
     const double c0 = p0, c1 = p1;  // chunk-entry recurrence state (TWO)
 #pragma unroll 1
-    for (int pass = 0; pass < (TWO ? 2 : 1); ++pass) {
+    for (int pass = 0; pass < (TWO ? 2 : 1) && warp_busy; ++pass) {
     if (TWO && pass == 1) {
       p0 = c0;
       p1 = c1;
@@ -2554,6 +2568,7 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_rcos16);
   cudaFree(p->d_titems);
   cudaFree(p->d_sitems);
+  cudaFree(p->d_pitems);
   cudaFree(p->d_sblk);
   cudaFree(p->d_slist);
   cudaFree(p->d_scnt);
@@ -2801,7 +2816,48 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
     // cross-CTA split of the long columns: balanced, but at one 7-warp CTA per
     // SM (142 registers) the extra items run as a second wave -- off by default
     static const int st_items = env_int("SWX_SYNTH_ITEMS", 0);
+    // SWX_SYNTH_PSPLIT=n: columns m < n split by latitude pairs over two CTAs
+    // (measured: no gain; with 128-thread CTAs every column must be split)
+    static const int st_psplit = env_int("SWX_SYNTH_PSPLIT", 0);
     SynthArgs ai = a;
+    if (MODE == 0 && st_psplit > 0 && g.y == 1 && p->nh >= 64 && !st_items) {
+      if (!p->d_pitems) {
+        std::vector<int4> it;
+        const int h0 = ((p->nh + 1) / 2 + 31) / 32 * 32;  // first half, whole warps
+        for (int m = 0; m <= p->trunc; ++m) {
+          if (m < st_psplit) {
+            it.push_back(make_int4(m, 0, h0, 0));
+            it.push_back(make_int4(m, h0, p->nh - h0, 0));
+          } else {
+            it.push_back(make_int4(m, 0, p->nh, 0));
+          }
+        }
+        int4 *d = nullptr;
+        SWX_CUDA_TRY(cudaMalloc(&d, sizeof(int4) * it.size()));
+        SWX_CUDA_TRY(cudaMemcpy(d, it.data(), sizeof(int4) * it.size(), cudaMemcpyHostToDevice));
+        p->d_pitems = d;
+        p->n_pitems = (int)it.size();
+      }
+      ai.pitems = p->d_pitems;
+      g.x = p->n_pitems;
+      // SWX_SYNTH_PBIG=1: one CTA per SM (the split halves get whole SMs);
+      // otherwise 128-thread CTAs (the first half's width) co-reside
+      static const int st_big = env_int("SWX_SYNTH_PBIG", 0);
+      const int h0 = ((p->nh + 1) / 2 + 31) / 32 * 32;
+      if (!st_big && st_psplit <= p->trunc)
+        return fail(SWX_ERR_CONFIG, "SWX_SYNTH_PSPLIT without PBIG must split every column");
+      const int bt = st_big ? nt : std::max(h0, p->nh - h0);
+      const size_t sm2 = synth_smem(ns, nh, 1, bt);
+      const size_t big = st_big ? std::max(sm2, (size_t)120 * 1024) : sm2;
+      static bool attr = false;
+      if (!attr && big > 48 * 1024) {
+        SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big));
+        attr = true;
+      }
+      SWX_CUDA_TRY(launch_pdl(k, g, dim3(bt), big, s, static_cast<const ShtView &>(*p), ai));
+      SWX_LAUNCH_CHECK();
+      return SWX_OK;
+    }
     if (MODE == 0 && st_items && p->d_sitems && p->d_spart && g.y == 1) {
       ai.items = p->d_sitems;
       ai.cnt = p->d_scnt;
