@@ -162,6 +162,11 @@ int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
 int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_div,
                double *d_u, double *d_v, void *d_workspace, size_t ws_bytes,
                void *stream);
+/* Vorticity and divergence coefficients from grid winds, vortdiv_from_uv
+ * (sphere.py:405-430): d_u, d_v are (nlat, nlon) float64 grids; needs the
+ * plan's Legendre table (SWX_ERR_CONFIG above T ~700).                     */
+int swx_sht_vortdiv(swx_sht p, const double *d_u, const double *d_v, swx_c128 *d_vort,
+                    swx_c128 *d_div, void *d_workspace, size_t ws_bytes, void *stream);
 /* tendency_group for atoms in `atoms` (SWX_TEND_LC | SWX_TEND_N), swe.py:254-279:
  * d_out = sum of the selected atom tendencies of d_state (one packed state).  */
 int swx_sht_tendency(swx_sht p, int atoms, const swx_c128 *d_state,

@@ -53,6 +53,7 @@ SIGNATURES = {
     "swx_sht_synthesis": (_I, [_P, _I, _P, _P, _P, _S, _P]),
     "swx_sht_analysis": (_I, [_P, _I, _P, _P, _P, _S, _P]),
     "swx_sht_uv": (_I, [_P, _P, _P, _P, _P, _P, _S, _P]),
+    "swx_sht_vortdiv": (_I, [_P, _P, _P, _P, _P, _P, _S, _P]),
     "swx_sht_tendency": (_I, [_P, _I, _P, _P, _P, _S, _P]),
     "swx_sht_tendency_sub": (_I, [_P, _I, _P, _P, _P, _P, _S, _P]),
     "swx_sht_set_synth_event": (_I, [_P, _P]),

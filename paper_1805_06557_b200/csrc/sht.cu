@@ -1831,6 +1831,42 @@ __global__ void prep_tab_plain_kernel(ShtView p, const double2 *Q, int nf, doubl
   put_row_t(base + ps, od, 4, i);
 }
 
+// prepared rows of vortdiv_from_uv (sphere.py:405-430) for the table analysis:
+// with F = (0, 0, -fv, fu, 0) and no Coriolis terms the tendency fold gives
+// S1 = i m w fv /(a cos), S5 = w fu / a (H part), S2 = i m w fu /(a cos),
+// S6 = -w fv / a, so the analysis' vort = S1 + S5 = (i m iq_v + ih_u)/a and
+// div = S2 + S6 = (i m iq_u - ih_v)/a, exactly the reference's contraction.
+__global__ void prep_tab_vortdiv_kernel(ShtView p, const double2 *Q, double *A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (i >= p.nt16) return;
+  double2 ev[7], od[7];
+  if (i < p.nh) {
+    const int jn = p.d_jn[i], js = p.d_js[i];
+    const size_t row = (size_t)p.nlat * p.nfreq;
+    double2 F[2][5], L[2];
+#pragma unroll
+    for (int hemi = 0; hemi < 2; ++hemi) {
+      const size_t at = (size_t)(hemi ? js : jn) * p.nfreq + m;
+      const double2 fu = Q[at], fv = Q[row + at];
+      F[hemi][0] = F[hemi][1] = F[hemi][4] = make_double2(0.0, 0.0);
+      F[hemi][2] = make_double2(-fv.x * p.dlon, -fv.y * p.dlon);
+      F[hemi][3] = make_double2(fu.x * p.dlon, fu.y * p.dlon);
+      L[hemi] = make_double2(0.0, 0.0);
+    }
+    tend_fold<true>(p, F, L, L, m, pair_k(p, i), ev, od);
+  } else {
+#pragma unroll
+    for (int s2 = 0; s2 < 7; ++s2) ev[s2] = od[s2] = make_double2(0.0, 0.0);
+  }
+  const size_t ps = (size_t)p.nt16 * kAG;
+  double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+  put_row_t(base + 0 * ps, ev, 4, i);
+  put_row_t(base + 1 * ps, od, 4, i);
+  put_row_t(base + 2 * ps, ev + 4, 3, i);
+  put_row_t(base + 3 * ps, od + 4, 3, i);
+}
+
 // Table analysis.  CTA item = (m, 32 degrees l0..l0+31): four consumer warps
 // (parity x 16-degree half), each accumulating two 8x8 outputs (P-table and
 // H-table columns) over all latitude pairs with m8n8k4 DMMA, and one producer
@@ -2962,6 +2998,32 @@ extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_d
   SWX_CUDA_TRY(cudaMemcpyAsync(d_u, w.grid, g, cudaMemcpyDeviceToDevice, s));
   SWX_CUDA_TRY(cudaMemcpyAsync(d_v, w.grid + (size_t)p->nlat * p->nlon, g,
                                cudaMemcpyDeviceToDevice, s));
+  return SWX_OK;
+}
+
+// vorticity and divergence from grid winds (sphere.py:405-430): R2C of u, v,
+// the vortdiv fold into the prepared rows, then the table analysis
+extern "C" int swx_sht_vortdiv(swx_sht p, const double *d_u, const double *d_v,
+                               swx_c128 *d_vort, swx_c128 *d_div, void *d_ws, size_t ws_bytes,
+                               void *stream) {
+  int rc = check_ws(p, d_ws, ws_bytes);
+  if (rc) return rc;
+  if (!p->use_tab)
+    return fail(SWX_ERR_CONFIG, "vortdiv_from_uv needs the Legendre table (T <= ~700)");
+  cudaStream_t s = (cudaStream_t)stream;
+  ShtWs w = carve(p, d_ws);
+  const size_t g = (size_t)p->nlat * p->nlon;
+  SWX_CUDA_TRY(cudaMemcpyAsync(w.grid, d_u, g * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  SWX_CUDA_TRY(cudaMemcpyAsync(w.grid + g, d_v, g * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if ((rc = r2c_exec(p, p->nlon, 2, w.grid, w.Q, s))) return rc;
+  dim3 gp((p->nt16 + 127) / 128, p->nm);
+  prep_tab_vortdiv_kernel<<<gp, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, w.A);
+  SWX_LAUNCH_CHECK();
+  double2 *out3 = w.c2r;  // (phi' = 0, vort, div)
+  if ((rc = launch_analysis_tab<0>(p, w.A, out3, 3, s))) return rc;
+  const size_t nb = (size_t)p->ncoef * sizeof(double2);
+  SWX_CUDA_TRY(cudaMemcpyAsync(d_vort, out3 + p->ncoef, nb, cudaMemcpyDeviceToDevice, s));
+  SWX_CUDA_TRY(cudaMemcpyAsync(d_div, out3 + 2 * (size_t)p->ncoef, nb, cudaMemcpyDeviceToDevice, s));
   return SWX_OK;
 }
 

@@ -215,6 +215,16 @@ class ShtPlan:
             self.workspace.numel(), stream_ptr(stream)))
         return u, v
 
+    def vortdiv_dev(self, u, v, stream=None):
+        import torch
+
+        vort = torch.empty(ncoef(self.cfg.trunc), dtype=torch.complex128, device=self.device)
+        div = torch.empty_like(vort)
+        _lib.check(self._lib.swx_sht_vortdiv(
+            self._h, ptr(u), ptr(v), ptr(vort), ptr(div), ptr(self.workspace),
+            self.workspace.numel(), stream_ptr(stream)))
+        return vort, div
+
     def set_synth_event(self, event=None):
         """Record ``event`` (torch.cuda.Event) after the synthesis of each
         following tendency call (None clears)."""
@@ -328,3 +338,18 @@ def uv_from_vortdiv(zeta: SpectralField, delta: SpectralField, cfg: SphereConfig
     d = to_device(pack(_pad_coeffs(delta.coeffs, cfg.trunc)), plan.device)
     u, v = plan.uv_dev(z, d)
     return GridField(u.cpu().numpy(), cfg), GridField(v.cpu().numpy(), cfg)
+
+
+def vortdiv_from_uv(u: GridField, v: GridField, cfg: SphereConfig):
+    """Vorticity and divergence coefficients from grid velocities
+    (sphere.py:405-430): one device FFT + table analysis (swx_sht_vortdiv)."""
+    _check_grid(u, cfg)
+    _check_grid(v, cfg)
+    plan = plan_for(cfg)
+    import torch
+
+    ug = torch.from_numpy(np.ascontiguousarray(np.real(u.values), dtype=np.float64)).to(plan.device)
+    vg = torch.from_numpy(np.ascontiguousarray(np.real(v.values), dtype=np.float64)).to(plan.device)
+    z, d = plan.vortdiv_dev(ug, vg)
+    return (SpectralField(unpack(z.cpu().numpy(), cfg.trunc)),
+            SpectralField(unpack(d.cpu().numpy(), cfg.trunc)))

@@ -57,3 +57,8 @@ def rel_l2(x, ref):
 @pytest.fixture(scope="session")
 def golden_split():
     return np.load(os.path.join(GOLDEN, "split.npz"))
+
+
+@pytest.fixture(scope="session")
+def golden_io():
+    return np.load(os.path.join(GOLDEN, "io.npz"))

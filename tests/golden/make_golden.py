@@ -201,11 +201,54 @@ def split_fixtures(path):
     np.savez_compressed(path, **out)
 
 
+def io_fixtures(path):
+    """f4: vorticity/divergence from grid winds, the Galewsky jet initial
+    state, the L-inf error metric and the byte format of field dumps."""
+    import io as _io
+
+    from swerexi import benchmarks as B
+    from swerexi import fieldio as FIO
+
+    out = {}
+    for trunc in (21, 42):
+        cfg = SP.SphereConfig.for_truncation(trunc)
+        src = seeded_linear_state(trunc, 7)
+        u, v = SP.uv_from_vortdiv(SP.SpectralField(src[1]), SP.SpectralField(src[2]), cfg)
+        z, d = SP.vortdiv_from_uv(u, v, cfg)
+        out[f"T{trunc}_u"] = u.values
+        out[f"T{trunc}_v"] = v.values
+        out[f"T{trunc}_vort"] = pack(z.coeffs)
+        out[f"T{trunc}_div"] = pack(d.coeffs)
+    cfg = SP.SphereConfig.for_truncation(42)
+    st = B.init_barotropic_instability(cfg, with_bump=True)
+    out["T42_galewsky"] = pack(st.stack())
+    st0 = B.init_barotropic_instability(cfg, with_bump=False)
+    out["T42_galewsky_nobump"] = pack(st0.stack())
+    out["T42_linf_h"] = np.array(B.linf_error(st, st0, "h"))
+    out["T42_linf_vort"] = np.array(B.linf_error(st, st0, "vort"))
+    # byte format of a two-block spectral dump and one grid block (T5 state)
+    cfg5 = SP.SphereConfig.for_truncation(5)
+    s5 = seeded_linear_state(5, 3)
+    buf = _io.BytesIO()
+    for f in range(3):
+        FIO.write_spectral_block(buf, SP.SpectralField(s5[f]), cfg5)
+    g = SP.synthesis(SP.SpectralField(s5[0]), cfg5)
+    FIO.write_grid_block(buf, g, cfg5)
+    out["T5_dump_bytes"] = np.frombuffer(buf.getvalue(), dtype=np.uint8)
+    out["T5_state"] = pack(s5)
+    out["T5_grid"] = g.values
+    np.savez_compressed(path, **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the T256 one-day trajectory")
     ap.add_argument("--split", action="store_true", help="only the Strang/CN stepper fixtures")
+    ap.add_argument("--io", action="store_true", help="only the f4 (IC / error / dump) fixtures")
     args = ap.parse_args()
+    if args.io:
+        io_fixtures(os.path.join(HERE, "io.npz"))
+        return
     if args.split:
         split_fixtures(os.path.join(HERE, "split.npz"))
         return

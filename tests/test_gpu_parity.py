@@ -389,3 +389,37 @@ def test_split_and_explicit_steppers_golden(golden_split, sid):
     for _ in range(2):
         st = stepper.step(st, 600.0)
     assert rel_l2(pack(st.stack()), golden_split[f"T21split_{sid}"]) <= 1e-10
+
+
+# ---------------------------------------------------------------- f4: IC, error, winds
+
+@pytest.mark.parametrize("trunc", [21, 42])
+def test_vortdiv_from_uv_golden(golden_io, trunc):
+    """swx_sht_vortdiv vs the reference's vortdiv_from_uv (sphere.py:405-430)."""
+    from paper_1805_06557_b200.sphere import GridField, vortdiv_from_uv
+
+    cfg = SphereConfig.for_truncation(trunc)
+    z, d = vortdiv_from_uv(GridField(golden_io[f"T{trunc}_u"], cfg),
+                           GridField(golden_io[f"T{trunc}_v"], cfg), cfg)
+    assert rel_linf(pack(z.coeffs), golden_io[f"T{trunc}_vort"]) <= 1e-11
+    assert rel_linf(pack(d.coeffs), golden_io[f"T{trunc}_div"]) <= 1e-11
+
+
+def test_galewsky_initial_state_and_error_golden(golden_io):
+    """Balanced jet + bump at T42 (benchmarks.py:147-215) and the L-inf metric
+    (benchmarks.py:290-306) vs the reference."""
+    from paper_1805_06557_b200.benchmarks import init_barotropic_instability, linf_error
+
+    cfg = SphereConfig.for_truncation(42)
+    st = init_barotropic_instability(cfg, with_bump=True)
+    st0 = init_barotropic_instability(cfg, with_bump=False)
+    ref = golden_io["T42_galewsky"]
+    for f in range(3):
+        if np.abs(ref[f]).max() == 0:
+            assert np.abs(pack(st.stack())[f]).max() == 0
+        else:
+            assert rel_linf(pack(st.stack())[f], ref[f]) <= 1e-10, f
+    assert rel_linf(pack(st0.stack())[0], golden_io["T42_galewsky_nobump"][0]) <= 1e-10
+    h = linf_error(st, st0, "h")
+    assert abs(h - float(golden_io["T42_linf_h"])) <= 1e-9 * float(golden_io["T42_linf_h"])
+    assert linf_error(st, st0, "vort") == 0.0
