@@ -184,6 +184,50 @@ int swx_sht_tendency_sub(swx_sht p, int atoms, const swx_c128 *d_state,
                          const swx_c128 *d_sub, swx_c128 *d_out, void *d_workspace,
                          size_t ws_bytes, void *stream);
 
+/* ---- column-sharded N term over ranks -----------------
+ * The reference evaluates the non-linear tendency on every worker (the
+ * paper's replicated "no communication" non-linearities, parallel.py:185-214,
+ * PAPER.md:849-853).  Here rank r of K owns the zonal columns
+ * [m_bounds[r], m_bounds[r+1]) -- balanced by column length, so the Legendre
+ * synthesis/analysis and the lg pole sums split evenly -- and the latitude
+ * pairs [p_bounds[r], p_bounds[r+1]) of the padded pair range [0, nt16) for
+ * the longitude transforms and grid products.  One tendency is three stages
+ * separated by two all-to-all exchanges the caller performs (NCCL
+ * all_to_all_single with the byte counts of swx_sht_shard_counts):
+ *   stage 0: synthesis of the own columns for all pairs; packs exchange 0
+ *            (Fourier rows of every peer's pairs, own columns) into d_send;
+ *   stage 1: unpacks exchange 0 from d_recv; fused grid stage of the own
+ *            pairs; packs exchange 1 (prepared analysis rows of every peer's
+ *            columns, own pairs) into d_send;
+ *   stage 2: unpacks exchange 1; analysis of the own columns into the own
+ *            columns' slots of d_out (d_out - d_sub with d_sub).
+ * Slabs are ordered by peer rank; the self slab is empty (it stays in the
+ * workspace).  With K = 1 the stages run exactly the kernels of
+ * swx_sht_tendency; for any K every coefficient is computed by the same
+ * kernel arithmetic, so the sharded result is bitwise equal to it.
+ * Needs the fused grid path (Legendre table, nlon_t <= 1024).               */
+#define SWX_MAX_RANKS 64
+typedef struct swx_shard {
+  int nranks, rank;
+  int m_bounds[SWX_MAX_RANKS + 1]; /* columns of rank r: [m_bounds[r], m_bounds[r+1])   */
+  int p_bounds[SWX_MAX_RANKS + 1]; /* padded latitude pairs of rank r (last ends at nt16) */
+} swx_shard;
+/* Balanced bounds (host only, no device needed).                            */
+int swx_shard_init(swx_shard *sh, int trunc, int nlat, int nranks, int rank);
+/* Per-peer byte counts of `exchange` (0 or 1) for atoms; h_send/h_recv hold
+ * nranks entries.  Returns max(total send, total recv) bytes (0 on error).  */
+size_t swx_sht_shard_counts(swx_sht p, const swx_shard *sh, int exchange, int atoms,
+                            size_t *h_send, size_t *h_recv);
+int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx_shard *sh,
+                           const swx_c128 *d_state, const swx_c128 *d_sub, swx_c128 *d_out,
+                           const void *d_recv, void *d_send, void *d_workspace,
+                           size_t ws_bytes, void *stream);
+/* Restrict the pole sums of an lg solver to columns [m_begin, m_end) (the
+ * column shard of the caller's rank; m_end < 0: all).  Slots of other
+ * columns in d_out are left unspecified.  SWX_ERR_CONFIG for the Coriolis
+ * group, whose ranks shard the poles instead (parallel.py:100-182).        */
+int swx_solver_set_columns(swx_solver s, int m_begin, int m_end);
+
 /* ---- host layout conversion (API edge) ------------------------------------
  * Dense (T+1)x(T+1) complex128 fields, C order (row l, column m) -- the
  * reference's SpectralField.coeffs (sphere.py) -- to and from packed m-major

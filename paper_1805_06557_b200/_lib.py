@@ -62,7 +62,20 @@ SIGNATURES = {
     "swx_host_pack": (_I, [_I, _I, _P, _P]),
     "swx_host_unpack": (_I, [_I, _I, _P, _P]),
     "swx_trace": (_I, [_I, _P, _I]),
+    "swx_shard_init": (_I, [_P, _I, _I, _I, _I]),
+    "swx_sht_shard_counts": (_S, [_P, _P, _I, _I, _P, _P]),
+    "swx_sht_tendency_shard": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
+    "swx_solver_set_columns": (_I, [_P, _I, _I]),
 }
+
+SWX_MAX_RANKS = 64
+
+
+class Shard(ctypes.Structure):
+    """swx_shard (include/swx.h): column and latitude-pair bounds of K ranks."""
+    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int),
+                ("m_bounds", ctypes.c_int * (SWX_MAX_RANKS + 1)),
+                ("p_bounds", ctypes.c_int * (SWX_MAX_RANKS + 1))]
 
 _lib = None
 _lock = threading.Lock()

@@ -1046,12 +1046,15 @@ extern "C" size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs,
 // (l, m0, m1) blocks of mpc modes, l descending; mpc < 0: blocks of -mpc
 // modes ordered by size, largest first (persistent kernels)
 static const int4 *lg_schedule(swx_solver s, int mpc_in, int *n_cta) {
-  auto &e = s->lg_sched[mpc_in];
+  const int lo = s->col_lo, hi = s->col_hi < 0 ? s->trunc + 1 : s->col_hi;
+  auto &e = s->lg_sched[std::make_tuple(mpc_in, lo, hi)];
   if (!e.first) {
     const int mpc = mpc_in < 0 ? -mpc_in : mpc_in;
     std::vector<int4> sched;
-    for (int l = s->trunc; l >= 0; --l)
-      for (int m0 = 0; m0 <= l; m0 += mpc) sched.push_back(make_int4(l, m0, std::min(l + 1, m0 + mpc), 0));
+    for (int l = s->trunc; l >= lo; --l)
+      for (int m0 = lo; m0 <= l && m0 < hi; m0 += mpc)
+        sched.push_back(make_int4(l, m0, std::min(std::min(l + 1, hi), m0 + mpc), 0));
+    if (sched.empty()) sched.push_back(make_int4(0, 0, 0, 0));  // empty shard: one idle CTA
     if (mpc_in < 0)
       std::stable_sort(sched.begin(), sched.end(),
                        [](const int4 &a, const int4 &b) { return a.z - a.y > b.z - b.y; });
@@ -1398,5 +1401,17 @@ extern "C" int swx_state_axpy(int trunc, int n_states, const swx_c128 *d_x,
   axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       (const double2 *)d_x, s, (const double2 *)d_y, n, (double2 *)d_out);
   SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
+extern "C" int swx_solver_set_columns(swx_solver s, int m_begin, int m_end) {
+  if (!s) return fail(SWX_ERR_CONFIG, "null solver");
+  if (s->group == SWX_GROUP_L && s->omega > 0.0)
+    return fail(SWX_ERR_CONFIG, "column shards are for the lg group; the Coriolis group shards poles");
+  if (m_end < 0) m_end = s->trunc + 1;
+  if (m_begin < 0 || m_begin > m_end || m_end > s->trunc + 1)
+    return fail(SWX_ERR_CONFIG, "bad column range");
+  s->col_lo = m_begin;
+  s->col_hi = m_end;
   return SWX_OK;
 }

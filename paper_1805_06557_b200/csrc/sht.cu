@@ -138,6 +138,9 @@ struct SynthArgs {
   // pitems: CTA b runs column pitems[b].x for pairs [y, y + z) -- the long
   // columns split over two SMs by latitude pairs, one CTA per SM
   const int4 *pitems = nullptr;
+  // first column of the launch (column-sharded tendency: CTA x runs column
+  // m0 + x of the default and nyb dispatches)
+  int m0 = 0;
 };
 
 // bin k of the packed complex row z = north + i south of field f (zero above T)
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
   constexpr int NSTG = GRP ? 1 : NSPL;  // staging sets
   double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)NSTG * NC * kSL * 2) +
                  (size_t)half * (kSL + 2);
-  int4 itm = make_int4(a.nyb > 0 ? blockIdx.x / a.nyb : blockIdx.x, 0, 0, -1);
+  int4 itm = make_int4((a.nyb > 0 ? blockIdx.x / a.nyb : blockIdx.x) + a.m0, 0, 0, -1);
   if (MODE == 0 && (SPLIT == 1 || SPLIT == 4) && a.items) itm = a.items[blockIdx.x];
   int pstart = (a.nyb > 0 ? blockIdx.x % a.nyb : blockIdx.y) * NT, pcount = NT;
   if (MODE == 0 && SPLIT == 1 && a.pitems) {
@@ -1153,12 +1156,13 @@ __device__ __forceinline__ void grid_zero_rows(const ShtView &p, int i, double *
 
 __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const double2 *c2r,
                                                            const double2 *lc, int atoms,
-                                                           const double2 *tw_g, double *A) {
+                                                           const double2 *tw_g, double *A,
+                                                           int i0) {
   extern __shared__ __align__(16) double2 gsm[];
   pdl_trigger();
   pdl_wait();
   const int N = p.nlon_t, T = p.trunc;
-  const int i = blockIdx.x;  // latitude pair (padded to nt16)
+  const int i = blockIdx.x + i0;  // latitude pair (padded to nt16)
   if (i >= p.nh) {  // padding pairs: zero prepared rows
     grid_zero_rows(p, i, A);
     return;
@@ -1229,14 +1233,14 @@ template <int R1, int R2>
 __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p, const double2 *c2r,
                                                                     const double2 *lc, int atoms,
                                                                     const double2 *tw_g,
-                                                                    double *A) {
+                                                                    double *A, int i0) {
   using C = SqCfg<R1, R2>;
   constexpr int N = C::N, RP = C::RP, FS = C::FS;
   extern __shared__ __align__(16) double2 gsm[];
   double2 *F = gsm;  // [5][FS]
   pdl_trigger();
   pdl_wait();
-  const int i = blockIdx.x;
+  const int i = blockIdx.x + i0;
   if (i >= p.nh) {
     grid_zero_rows(p, i, A);
     return;
@@ -1356,12 +1360,12 @@ template <int R>
 __global__ void __launch_bounds__(SqCfg<R, R>::NT, 2) grid_sq1_kernel(ShtView p, const double2 *c2r,
                                                                       const double2 *lc, int atoms,
                                                                       const double2 *tw_g,
-                                                                      double *A) {
+                                                                      double *A, int i0) {
   using C = SqCfg<R, R>;
   constexpr int N = C::N, RP = C::RP, FS = C::FS;
   extern __shared__ __align__(16) double2 gsm[];
   double2 *F = gsm;  // [5][FS]
-  const int i = blockIdx.x;
+  const int i = blockIdx.x + i0;  // latitude pair (padded to nt16)
   if (i >= p.nh) {
     grid_zero_rows(p, i, A);
     return;
@@ -2679,7 +2683,7 @@ static int env_int(const char *name, int dflt) {
 
 template <int MODE, int KTS>
 static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
-                                 const double2 *sub) {
+                                 const double2 *sub, int it0, int it1) {
   // resident CTAs per SM and SM count, queried once per instantiation
   static int nsm = 0, per_sm = 0;
   auto k = analysis_tab_kernel<MODE, KTS>;
@@ -2696,21 +2700,27 @@ static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int n
     nsm = n;
   }
   // equal-cost items: give every CTA the same number of items
+  // items [it0, it1) (m-major: a column range is an item range)
+  ShtView v = static_cast<const ShtView &>(*p);
+  if (it1 < 0) it1 = p->n_titems;
+  v.d_titems += it0;
+  v.n_titems = it1 - it0;
+  if (v.n_titems <= 0) return SWX_OK;
   const int slots = nsm * per_sm;
-  const int per_cta = (p->n_titems + slots - 1) / slots;
-  const int blocks = std::max(1, (p->n_titems + per_cta - 1) / per_cta);
-  SWX_CUDA_TRY(launch_pdl(k, dim3(blocks), dim3(kTabThreads), smem, s,
-                          static_cast<const ShtView &>(*p), p->ptab_map, A, out, nf, sub));
+  const int per_cta = (v.n_titems + slots - 1) / slots;
+  const int blocks = std::max(1, (v.n_titems + per_cta - 1) / per_cta);
+  SWX_CUDA_TRY(launch_pdl(k, dim3(blocks), dim3(kTabThreads), smem, s, v, p->ptab_map, A, out, nf,
+                          sub));
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
 
 template <int MODE>
 static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
-                               const double2 *sub = nullptr) {
+                               const double2 *sub = nullptr, int it0 = 0, int it1 = -1) {
   static const int stages = env_int("SWX_TAB_STAGES", 4);  // tuning: ring depth 4 or 8
-  return stages == 8 ? launch_analysis_tab_k<MODE, 8>(p, A, out, nf, s, sub)
-                     : launch_analysis_tab_k<MODE, 4>(p, A, out, nf, s, sub);
+  return stages == 8 ? launch_analysis_tab_k<MODE, 8>(p, A, out, nf, s, sub, it0, it1)
+                     : launch_analysis_tab_k<MODE, 4>(p, A, out, nf, s, sub, it0, it1);
 }
 
 static int c2r_exec(swx_sht p, int nlon, int nf, double2 *in, double *out, cudaStream_t s) {
@@ -3083,7 +3093,7 @@ static int launch_synth_tab(swx_sht p, const SynthArgs &a, ShtWs &w, cudaStream_
 }
 
 template <int R>
-static int launch_grid_sq1(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
+static int launch_grid_sq1(swx_sht p, int atoms, ShtWs &w, cudaStream_t s, int i0, int npairs) {
   using C = SqCfg<R, R>;
   static bool attr = false;
   if (!attr) {
@@ -3091,15 +3101,15 @@ static int launch_grid_sq1(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  SWX_CUDA_TRY(launch_pdl(grid_sq1_kernel<R>, dim3(p->nt16), dim3(C::NT), C::SMEM, s,
+  SWX_CUDA_TRY(launch_pdl(grid_sq1_kernel<R>, dim3(npairs), dim3(C::NT), C::SMEM, s,
                           static_cast<const ShtView &>(*p), (const double2 *)w.c2r,
-                          (const double2 *)w.lc, atoms, (const double2 *)p->d_tw, w.A));
+                          (const double2 *)w.lc, atoms, (const double2 *)p->d_tw, w.A, i0));
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
 
 template <int R1, int R2>
-static int launch_grid_sq(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
+static int launch_grid_sq(swx_sht p, int atoms, ShtWs &w, cudaStream_t s, int i0, int npairs) {
   using C = SqCfg<R1, R2>;
   static bool attr = false;
   if (!attr) {
@@ -3107,15 +3117,19 @@ static int launch_grid_sq(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  grid_sq_kernel<R1, R2><<<p->nt16, C::NT, C::SMEM, s>>>(static_cast<const ShtView &>(*p), w.c2r,
-                                                         w.lc, atoms, p->d_tw, w.A);
+  grid_sq_kernel<R1, R2><<<npairs, C::NT, C::SMEM, s>>>(static_cast<const ShtView &>(*p), w.c2r,
+                                                        w.lc, atoms, p->d_tw, w.A, i0);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
 
 // fused grid stage: register four-step FFTs where nlon_t has a compiled
-// split (SWX_GRID_STOCKHAM=1 forces the generic shared-memory Stockham path)
-static int launch_grid(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
+// split (SWX_GRID_STOCKHAM=1 forces the generic shared-memory Stockham path);
+// latitude pairs [i0, i0 + npairs) of the padded range [0, nt16)
+static int launch_grid(swx_sht p, int atoms, ShtWs &w, cudaStream_t s, int i0 = 0,
+                       int npairs = -1) {
+  if (npairs < 0) npairs = p->nt16 - i0;
+  if (npairs <= 0) return SWX_OK;
   static const bool stockham = [] {
     const char *e = getenv("SWX_GRID_STOCKHAM");
     return e && atoi(e) != 0;
@@ -3127,10 +3141,12 @@ static int launch_grid(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
   if (!stockham) {
     switch (p->nlon_t) {
       case 784:   // T256
-        return sq1 ? launch_grid_sq1<28>(p, atoms, w, s) : launch_grid_sq<28, 28>(p, atoms, w, s);
+        return sq1 ? launch_grid_sq1<28>(p, atoms, w, s, i0, npairs)
+                   : launch_grid_sq<28, 28>(p, atoms, w, s, i0, npairs);
       case 256:   // T85
-        return sq1 ? launch_grid_sq1<16>(p, atoms, w, s) : launch_grid_sq<16, 16>(p, atoms, w, s);
-      case 192: return launch_grid_sq<12, 16>(p, atoms, w, s);   // T63
+        return sq1 ? launch_grid_sq1<16>(p, atoms, w, s, i0, npairs)
+                   : launch_grid_sq<16, 16>(p, atoms, w, s, i0, npairs);
+      case 192: return launch_grid_sq<12, 16>(p, atoms, w, s, i0, npairs);   // T63
       default: break;
     }
   }
@@ -3138,8 +3154,8 @@ static int launch_grid(swx_sht p, int atoms, ShtWs &w, cudaStream_t s) {
   if (smem > 48 * 1024)
     SWX_CUDA_TRY(cudaFuncSetAttribute(grid_tend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-  grid_tend_kernel<<<p->nt16, kGridT, smem, s>>>(static_cast<const ShtView &>(*p), w.c2r, w.lc,
-                                                 atoms, p->d_tw, w.A);
+  grid_tend_kernel<<<npairs, kGridT, smem, s>>>(static_cast<const ShtView &>(*p), w.c2r, w.lc,
+                                                atoms, p->d_tw, w.A, i0);
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -3321,4 +3337,218 @@ extern "C" int swx_sht_set_synth_event(swx_sht p, void *event) {
   if (!p) return fail(SWX_ERR_CONFIG, "null plan");
   p->synth_done = (cudaEvent_t)event;
   return SWX_OK;
+}
+
+// ---------------------------------------------------------------------
+// Column-sharded tendency (see swx.h).  Rank r owns columns
+// [m_bounds[r], m_bounds[r+1]) and padded latitude pairs [p_bounds[r],
+// p_bounds[r+1]); the workspace keeps the single-rank layout, so every stage
+// runs the single-rank kernels on a sub-range and the exchanges move
+// rectangular blocks of it (strided device copies into / out of contiguous
+// per-peer slabs).
+// ---------------------------------------------------------------------
+extern "C" int swx_shard_init(swx_shard *sh, int trunc, int nlat, int nranks, int rank) {
+  if (!sh) return fail(SWX_ERR_CONFIG, "null shard");
+  if (trunc < 0 || nlat < 1 || nranks < 1 || nranks > SWX_MAX_RANKS || rank < 0 || rank >= nranks)
+    return fail(SWX_ERR_CONFIG, "bad shard geometry");
+  *sh = swx_shard{};
+  sh->nranks = nranks;
+  sh->rank = rank;
+  // columns: contiguous, balanced by column length T + 1 - m (the work of
+  // the Legendre sums and of the lg pole sums of column m)
+  const long long total = (long long)(trunc + 1) * (trunc + 2) / 2;
+  long long acc = 0;
+  int m = 0;
+  sh->m_bounds[0] = 0;
+  for (int r = 1; r < nranks; ++r) {
+    const long long target = (total * r + nranks / 2) / nranks;
+    while (m <= trunc && acc + (trunc + 1 - m) / 2 < target) acc += trunc + 1 - m++;
+    sh->m_bounds[r] = m;
+  }
+  sh->m_bounds[nranks] = trunc + 1;
+  // latitude pairs: equal counts of real pairs; the padding up to nt16 goes to
+  // the last rank (its zero prepared rows travel with its slab)
+  const int nh = (nlat + 1) / 2, nt16 = ((nh + 15) / 16) * 16;
+  for (int r = 0; r < nranks; ++r) sh->p_bounds[r] = (int)((long long)nh * r / nranks);
+  sh->p_bounds[nranks] = nt16;
+  return SWX_OK;
+}
+
+namespace {
+
+struct Blk {  // one rectangular block of the workspace: rows x width bytes at pitch
+  size_t off, pitch, width, rows;
+};
+
+// blocks of exchange `ex` sent by rank `from` to rank `to` (byte offsets into
+// the workspace; the receiver writes the same blocks of its own workspace)
+static void shard_blocks(swx_sht p, const ShtWs &w, const swx_shard *sh, int ex, int atoms,
+                         int from, int to, std::vector<Blk> &out) {
+  out.clear();
+  const int T1 = p->trunc + 1;
+  const char *base = (const char *)w.c2r;
+  if (ex == 0) {  // Fourier rows: pairs of `to`, columns of `from`
+    const int m0 = sh->m_bounds[from], nm = sh->m_bounds[from + 1] - m0;
+    const int a = std::min(sh->p_bounds[to], p->nh), b = std::min(sh->p_bounds[to + 1], p->nh);
+    if (nm <= 0 || b <= a) return;
+    if (atoms & SWX_TEND_N)
+      out.push_back({(size_t)((const char *)(w.c2r + (size_t)a * 8 * T1 + m0) - base),
+                     (size_t)T1 * sizeof(double2), (size_t)nm * sizeof(double2),
+                     (size_t)(b - a) * 8});
+    if (atoms & SWX_TEND_LC)
+      for (int term = 0; term < 2; ++term) {
+        const double2 *lt = w.lc + (size_t)term * p->nlat * p->nm;
+        // south rows js = i, north rows jn = nlat - 1 - i (both contiguous)
+        const int j0[2] = {a, p->nlat - b};
+        for (int h = 0; h < 2; ++h)
+          out.push_back({(size_t)((const char *)(lt + (size_t)j0[h] * p->nm + m0) - base),
+                         (size_t)p->nm * sizeof(double2), (size_t)nm * sizeof(double2),
+                         (size_t)(b - a)});
+      }
+  } else {  // prepared rows: columns of `to`, pairs of `from`
+    const int m0 = sh->m_bounds[to], nm = sh->m_bounds[to + 1] - m0;
+    const int a = sh->p_bounds[from], b = sh->p_bounds[from + 1];
+    if (nm <= 0 || b <= a) return;
+    const size_t ps = (size_t)p->nt16 * kAG;
+    out.push_back({(size_t)((const char *)(w.A + (size_t)m0 * 4 * ps + (size_t)a * kAG) - base),
+                   ps * sizeof(double), (size_t)(b - a) * kAG * sizeof(double), (size_t)nm * 4});
+  }
+}
+
+static size_t blocks_bytes(const std::vector<Blk> &v) {
+  size_t n = 0;
+  for (const Blk &b : v) n += b.width * b.rows;
+  return n;
+}
+
+static int check_shard(swx_sht p, const swx_shard *sh) {
+  if (!p) return fail(SWX_ERR_CONFIG, "null SHT plan");
+  if (!sh || sh->nranks < 1 || sh->nranks > SWX_MAX_RANKS || sh->rank < 0 ||
+      sh->rank >= sh->nranks)
+    return fail(SWX_ERR_CONFIG, "bad shard");
+  const int K = sh->nranks;
+  if (sh->m_bounds[0] != 0 || sh->m_bounds[K] != p->trunc + 1 || sh->p_bounds[0] != 0 ||
+      sh->p_bounds[K] != p->nt16)
+    return fail(SWX_ERR_CONFIG, "shard bounds do not cover the plan");
+  for (int r = 0; r < K; ++r)
+    if (sh->m_bounds[r + 1] < sh->m_bounds[r] || sh->p_bounds[r + 1] < sh->p_bounds[r])
+      return fail(SWX_ERR_CONFIG, "shard bounds not monotone");
+  if (!p->fused_grid || !p->use_tab)
+    return fail(SWX_ERR_CONFIG, "column-sharded tendency needs the fused grid stage (Legendre table)");
+  return SWX_OK;
+}
+
+// pack (dir 0: workspace -> slabs) or unpack (dir 1: slabs -> workspace)
+static int shard_move(swx_sht p, const ShtWs &w, const swx_shard *sh, int ex, int atoms, int dir,
+                      char *slab, cudaStream_t s) {
+  std::vector<Blk> blks;
+  size_t o = 0;
+  char *base = (char *)w.c2r;
+  for (int peer = 0; peer < sh->nranks; ++peer) {
+    if (peer == sh->rank) continue;
+    if (dir == 0)
+      shard_blocks(p, w, sh, ex, atoms, sh->rank, peer, blks);
+    else
+      shard_blocks(p, w, sh, ex, atoms, peer, sh->rank, blks);
+    for (const Blk &b : blks) {
+      if (dir == 0)
+        SWX_CUDA_TRY(cudaMemcpy2DAsync(slab + o, b.width, base + b.off, b.pitch, b.width, b.rows,
+                                       cudaMemcpyDeviceToDevice, s));
+      else
+        SWX_CUDA_TRY(cudaMemcpy2DAsync(base + b.off, b.pitch, slab + o, b.width, b.width, b.rows,
+                                       cudaMemcpyDeviceToDevice, s));
+      o += b.width * b.rows;
+    }
+  }
+  return SWX_OK;
+}
+
+// first analysis item of column m (items are m-major, kTL degrees each)
+static int first_item(int trunc, int m) {
+  int n = 0;
+  for (int c = 0; c < m; ++c) n += (trunc + 1 - c + kTL - 1) / kTL;
+  return n;
+}
+
+}  // namespace
+
+extern "C" size_t swx_sht_shard_counts(swx_sht p, const swx_shard *sh, int exchange, int atoms,
+                                       size_t *h_send, size_t *h_recv) {
+  if (check_shard(p, sh) || (exchange != 0 && exchange != 1) || !h_send || !h_recv) return 0;
+  ShtWs w = carve(p, nullptr);
+  std::vector<Blk> blks;
+  size_t ts = 0, tr = 0;
+  for (int peer = 0; peer < sh->nranks; ++peer) {
+    h_send[peer] = h_recv[peer] = 0;
+    if (peer == sh->rank) continue;
+    shard_blocks(p, w, sh, exchange, atoms, sh->rank, peer, blks);
+    h_send[peer] = blocks_bytes(blks);
+    shard_blocks(p, w, sh, exchange, atoms, peer, sh->rank, blks);
+    h_recv[peer] = blocks_bytes(blks);
+    ts += h_send[peer];
+    tr += h_recv[peer];
+  }
+  return std::max<size_t>(std::max(ts, tr), 1);
+}
+
+extern "C" int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx_shard *sh,
+                                      const swx_c128 *d_state, const swx_c128 *d_sub,
+                                      swx_c128 *d_out, const void *d_recv, void *d_send,
+                                      void *d_ws, size_t ws_bytes, void *stream) {
+  int rc = check_ws(p, d_ws, ws_bytes);
+  if (rc) return rc;
+  if ((rc = check_shard(p, sh))) return rc;
+  if (atoms <= 0 || (atoms & ~(SWX_TEND_LC | SWX_TEND_N)))
+    return fail(SWX_ERR_CONFIG, "atoms must be a non-empty subset of {lc, n}");
+  if (p->omega == 0.0) atoms &= ~SWX_TEND_LC;  // swe.py:200-201
+  if (atoms == 0) return fail(SWX_ERR_CONFIG, "sharded tendency with no active atom");
+  const bool multi = sh->nranks > 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  ShtWs w = carve(p, d_ws);
+  const int r = sh->rank;
+  const int m0 = sh->m_bounds[r], m1 = sh->m_bounds[r + 1];
+  switch (stage) {
+    case 0: {
+      if (!d_state) return fail(SWX_ERR_CONFIG, "null state");
+      if (multi && !d_send) return fail(SWX_ERR_CONFIG, "null send slab");
+      if (m1 > m0) {
+        SynthArgs a;
+        a.coef = (const double2 *)d_state;
+        a.c2r = w.c2r;
+        a.lc = w.lc;
+        a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
+        a.nfreq = p->nfreq_t;
+        a.zpack = 1;
+        a.m0 = m0;
+        int nt;
+        dim3 g = synth_grid(p, 1, &nt);
+        g.x = m1 - m0;
+        const size_t smem = synth_smem(5, 2, 1, nt);
+        auto k = synth_kernel<0, 1>;
+        if (smem > 48 * 1024)
+          SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
+        SWX_LAUNCH_CHECK();
+      }
+      if (p->synth_done) SWX_CUDA_TRY(cudaEventRecord(p->synth_done, s));
+      return multi ? shard_move(p, w, sh, 0, atoms, 0, (char *)d_send, s) : SWX_OK;
+    }
+    case 1: {
+      if (multi && (!d_send || !d_recv)) return fail(SWX_ERR_CONFIG, "null exchange slab");
+      if (multi && (rc = shard_move(p, w, sh, 0, atoms, 1, (char *)d_recv, s))) return rc;
+      const int i0 = sh->p_bounds[r], i1 = sh->p_bounds[r + 1];
+      if ((rc = launch_grid(p, atoms, w, s, i0, i1 - i0))) return rc;
+      return multi ? shard_move(p, w, sh, 1, atoms, 0, (char *)d_send, s) : SWX_OK;
+    }
+    case 2: {
+      if (!d_out) return fail(SWX_ERR_CONFIG, "null output");
+      if (multi && !d_recv) return fail(SWX_ERR_CONFIG, "null receive slab");
+      if (multi && (rc = shard_move(p, w, sh, 1, atoms, 1, (char *)d_recv, s))) return rc;
+      if (m1 <= m0) return SWX_OK;
+      return launch_analysis_tab<0>(p, w.A, (double2 *)d_out, 3, s, (const double2 *)d_sub,
+                                    first_item(p->trunc, m0), first_item(p->trunc, m1));
+    }
+    default:
+      return fail(SWX_ERR_CONFIG, "shard stage must be 0, 1 or 2");
+  }
 }

@@ -5,6 +5,7 @@
 
 #include <cstdlib>
 #include <map>
+#include <tuple>
 #include <string>
 #include <utility>
 
@@ -85,8 +86,11 @@ struct swx_solver_s {
   int n_poles = 0;
   double2 *d_alpha = nullptr;
   double2 *h_alpha = nullptr;
-  // lg launch schedules (l, m0, m1, -) per CTA, keyed by modes per CTA
-  std::map<int, std::pair<int4 *, int>> lg_sched;
+  // lg launch schedules (l, m0, m1, -) per CTA, keyed by (modes per CTA,
+  // column range)
+  std::map<std::tuple<int, int, int>, std::pair<int4 *, int>> lg_sched;
+  // column shard of the lg pole sums (swx_solver_set_columns): [col_lo, col_hi)
+  int col_lo = 0, col_hi = -1;
   int l_blocks_per_sm = 0;
 };
 

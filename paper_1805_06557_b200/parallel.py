@@ -235,3 +235,261 @@ def amdahl_report(breakdowns: dict) -> list[dict]:
             "max_speedup": 1.0 / ser if ser > 0 else float("inf"),
         })
     return rows
+
+
+# ----------------------------------------------------------------------
+# Column-sharded N term and ETD2RK over ranks
+#
+# The reference replicates the non-linear tendency on every worker
+# (parallel.py:185-214: the Amdahl serial part).  Here rank r owns the zonal
+# columns [m_bounds[r], m_bounds[r+1]) of the packed state (a contiguous slot
+# range: the layout is m-major) and the latitude pairs [p_bounds[r],
+# p_bounds[r+1]).  A tendency is three device stages with two all-to-all
+# exchanges in between (swx_sht_tendency_shard); the lg pole sums are
+# diagonal in (l, m), so they run on the own columns with no exchange at all.
+# An ETD2RK step therefore needs four all-to-alls and no all-reduce, and the
+# state stays column-sharded between steps.
+
+def shard_bounds(trunc: int, nlat: int, nranks: int) -> tuple[tuple, tuple]:
+    """Host mirror of swx_shard_init: columns balanced by length T+1-m,
+    latitude pairs split evenly, padding pairs (up to a multiple of 16) on
+    the last rank."""
+    if nranks < 1 or nranks > _lib.SWX_MAX_RANKS:
+        raise ConfigurationError("bad number of ranks")
+    total = (trunc + 1) * (trunc + 2) // 2
+    mb, acc, m = [0], 0, 0
+    for r in range(1, nranks):
+        target = (total * r + nranks // 2) // nranks
+        while m <= trunc and acc + (trunc + 1 - m) // 2 < target:
+            acc += trunc + 1 - m
+            m += 1
+        mb.append(m)
+    mb.append(trunc + 1)
+    nh = (nlat + 1) // 2
+    nt16 = (nh + 15) // 16 * 16
+    pb = [nh * r // nranks for r in range(nranks)] + [nt16]
+    return tuple(mb), tuple(pb)
+
+
+def column_slots(trunc: int, m0: int, m1: int) -> tuple[int, int]:
+    """Packed slot range [s0, s1) of columns [m0, m1) (slot(l, m) m-major)."""
+    off = lambda m: m * (trunc + 1) - m * (m - 1) // 2  # noqa: E731
+    return off(m0), off(m1)
+
+
+class ColumnShard:
+    """One rank's share of a column-sharded plan (the swx_shard struct)."""
+
+    def __init__(self, cfg, rank: int, nranks: int):
+        import ctypes
+
+        self.cfg = cfg
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.c = _lib.Shard()
+        _lib.check(_lib.load().swx_shard_init(ctypes.byref(self.c), cfg.trunc, cfg.nlat,
+                                              self.nranks, self.rank))
+        self.m_bounds = tuple(self.c.m_bounds[: self.nranks + 1])
+        self.p_bounds = tuple(self.c.p_bounds[: self.nranks + 1])
+
+    @property
+    def columns(self) -> tuple[int, int]:
+        return self.m_bounds[self.rank], self.m_bounds[self.rank + 1]
+
+    def slots(self, rank: int | None = None) -> tuple[int, int]:
+        r = self.rank if rank is None else rank
+        return column_slots(self.cfg.trunc, self.m_bounds[r], self.m_bounds[r + 1])
+
+
+class ColumnComm:
+    """torch.distributed plumbing of the column shards (NCCL on GPUs)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise ConfigurationError("ColumnComm needs an initialised torch.distributed group")
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_to_all(self, send, send_counts, recv, recv_counts):
+        """Byte slabs ordered by peer (swx_sht_shard_counts order)."""
+        self.dist.all_to_all_single(recv[: sum(recv_counts)], send[: sum(send_counts)],
+                                    list(recv_counts), list(send_counts), group=self.group)
+
+    def gather_columns(self, state, shard: ColumnShard):
+        """Full packed state(s) on every rank from the ranks' own columns.
+        ``state``: (..., 3, ncoef); returns a new tensor of the same shape."""
+        import torch
+
+        lead = state.shape[:-1]
+        spans = [shard.slots(r) for r in range(self.world)]
+        width = max(b - a for a, b in spans)
+        a, b = spans[self.rank]
+        mine = torch.zeros(lead + (width,), dtype=state.dtype, device=state.device)
+        mine[..., : b - a] = state[..., a:b]
+        flat = torch.view_as_real(mine).reshape(-1) if mine.is_complex() else mine.reshape(-1)
+        allp = torch.empty((self.world * flat.numel(),), dtype=flat.dtype, device=state.device)
+        self.dist.all_gather_into_tensor(allp, flat, group=self.group)
+        if mine.is_complex():
+            allp = torch.view_as_complex(allp.view(-1, 2))
+        allp = allp.view((self.world,) + tuple(mine.shape))
+        out = torch.empty_like(state)
+        for r, (a, b) in enumerate(spans):
+            out[..., a:b] = allp[r][..., : b - a]
+        return out
+
+
+class ShardedTendency:
+    """tendency_group of one rank's columns (swx_sht_tendency_shard).
+
+    Owns its workspace and exchange slabs.  ``stage(k, ...)`` runs device
+    stage k; ``slabs(ex)`` gives (send, send_counts, recv, recv_counts) of
+    exchange ``ex`` for the caller's all-to-all.
+    """
+
+    def __init__(self, plan, shard: ColumnShard, atoms: int):
+        import ctypes
+
+        import torch
+
+        self.plan, self.shard, self.atoms = plan, shard, int(atoms)
+        lib = self._lib = _lib.lib()
+        dev = plan.device
+        self.workspace = torch.empty(plan.workspace.numel(), dtype=torch.uint8, device=dev)
+        K = shard.nranks
+        self.counts = []
+        size = 1
+        for ex in (0, 1):
+            snd, rcv = (ctypes.c_size_t * K)(), (ctypes.c_size_t * K)()
+            n = lib.swx_sht_shard_counts(plan._h, ctypes.byref(shard.c), ex, self.atoms, snd, rcv)
+            if n == 0:
+                _lib.check(_lib.SWX_ERR_CONFIG)
+            self.counts.append((tuple(snd), tuple(rcv)))
+            size = max(size, int(n))
+        self.send = torch.empty(size, dtype=torch.uint8, device=dev)
+        self.recv = torch.empty(size, dtype=torch.uint8, device=dev)
+
+    def slabs(self, ex: int):
+        s, r = self.counts[ex]
+        return self.send, s, self.recv, r
+
+    def stage(self, k: int, state=None, out=None, sub=None, stream=None):
+        import ctypes
+
+        _lib.check(self._lib.swx_sht_tendency_shard(
+            self.plan._h, int(k), self.atoms, ctypes.byref(self.shard.c),
+            ptr(state) if state is not None else 0, ptr(sub) if sub is not None else 0,
+            ptr(out) if out is not None else 0, ptr(self.recv), ptr(self.send),
+            ptr(self.workspace), self.workspace.numel(), stream_ptr(stream)))
+
+    def phases(self, state, out, sub=None, stream=None):
+        """Generator: runs the stages, yielding (self, ex) where exchange
+        ``ex`` must happen before the next stage."""
+        self.stage(0, state, None, None, stream)
+        yield self, 0
+        self.stage(1, None, None, None, stream)
+        yield self, 1
+        self.stage(2, None, out, sub, stream)
+
+    def run(self, comm: ColumnComm, state, out, sub=None, stream=None):
+        for t, ex in self.phases(state, out, sub, stream):
+            comm.all_to_all(*t.slabs(ex))
+        return out
+
+
+def virtual_exchange(ranks, ex: int):
+    """All-to-all between co-resident shards of ONE device (tests and the
+    single-GPU check of the multi-rank path): rank r's slab for peer s is
+    copied into peer s's receive slab at r's position.  Stream-ordered on
+    the current stream after every rank's preceding stage."""
+    K = len(ranks)
+    for s in range(K):
+        _, _, recv_s, rcounts_s = ranks[s].slabs(ex)
+        for r in range(K):
+            if r == s:
+                continue
+            send_r, scounts_r, _, _ = ranks[r].slabs(ex)
+            so = sum(scounts_r[:s])
+            ro = sum(rcounts_s[:r])
+            n = scounts_r[s]
+            assert n == rcounts_s[r], (r, s, n, rcounts_s[r])
+            if n:
+                recv_s[ro:ro + n].copy_(send_r[so:so + n])
+
+
+def run_lockstep(gens, exchange):
+    """Advance one phase generator per rank in lockstep; ``exchange(items)``
+    gets the (tendency, ex) of every rank at each exchange point."""
+    gens = list(gens)
+    while True:
+        items = []
+        done = 0
+        for g in gens:
+            try:
+                items.append(next(g))
+            except StopIteration:
+                done += 1
+        if done == len(gens):
+            return
+        if done:
+            raise ConfigurationError("ranks disagree on the number of exchanges")
+        exchange(items)
+
+
+class ColumnEtdrkEngine:
+    """ETD2RK (steppers.py:238-269) of one column shard: lg by REXI on the own
+    columns (swx_solver_set_columns), the remainder by ShardedTendency.
+
+    ``phases()`` is the step as a generator over exchange points, so the same
+    body runs under a real communicator (``step_dev(comm)``) or in lockstep
+    with co-resident virtual ranks on one device (``run_lockstep``).  The
+    state ``u`` is a full-size packed buffer of which only the own columns'
+    slots are maintained.
+    """
+
+    def __init__(self, linear_group: TermGroup, remainder_group: TermGroup,
+                 params: ModelParams, dt: float, coeff_set: dict, shard: ColumnShard):
+        import torch
+
+        from .sphere import plan_for
+        from .steppers import DeviceRexi
+        from .swe import atoms_mask
+
+        if linear_group.token != "lg":
+            raise ConfigurationError("column shards need the lg linear group "
+                                     "(the Coriolis chains couple degrees: shard poles)")
+        self.params, self.trunc, self.dt = params, params.cfg.trunc, float(dt)
+        self.shard = shard
+        self.plan = plan_for(params.cfg)
+        atoms = atoms_mask(remainder_group)
+        self.tend = ShardedTendency(self.plan, shard, atoms)
+        solver = ShiftedLinearSolver(linear_group, dt, params, columns=shard.columns)
+        self.rexi = DeviceRexi(solver, coeff_set[0].alphas,
+                               {k: coeff_set[k].betas for k in (0, 1, 2)})
+        nc = ncoef(self.trunc)
+        z = lambda *s: torch.zeros(s, dtype=torch.complex128, device=self.plan.device)  # noqa
+        self.u, self.a = z(3, nc), z(3, nc)
+        self.nu, self.d, self.psi0 = z(1, 3, nc), z(1, 3, nc), z(1, 3, nc)
+
+    def phases(self, stream=None):
+        dt = self.dt
+        self.rexi.apply((0,), self.u[None], self.psi0, stream)                       # psi0 u
+        yield from self.tend.phases(self.u, self.nu[0], None, stream)                 # N(u)
+        self.rexi.apply((1,), self.nu, self.a[None], stream, base=self.psi0, scale=dt)
+        yield from self.tend.phases(self.a, self.d[0], self.nu[0], stream)            # N(a)-N(u)
+        self.rexi.apply((2,), self.d, self.u[None], stream, base=self.a[None], scale=dt)
+
+    def step_dev(self, comm: ColumnComm, stream=None):
+        for t, ex in self.phases(stream):
+            comm.all_to_all(*t.slabs(ex))
+        return self.u
+
+    def load(self, stack: np.ndarray):
+        self.u.copy_(to_device(pack(stack), self.u.device))
+
+    def own(self, x=None):
+        """View of the own columns' slots of ``x`` (default: the state)."""
+        a, b = self.shard.slots()
+        return (self.u if x is None else x)[..., a:b]

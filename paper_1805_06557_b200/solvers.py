@@ -50,12 +50,18 @@ class ShiftedSolveSpec:
 class _Native:
     """One libswx solver handle warmed with one shift set."""
 
-    def __init__(self, lib, group_code, cfg, dt, phibar, alphas, stream):
+    def __init__(self, lib, group_code, cfg, dt, phibar, alphas, stream, columns=None):
         self.lib = lib
         h = ctypes.c_void_p()
         _lib.check(lib.swx_solver_create(ctypes.byref(h), group_code, cfg.trunc, float(dt),
                                          float(phibar), cfg.radius_a, cfg.omega))
         self.h = h
+        if columns is not None:
+            rc = lib.swx_solver_set_columns(h, int(columns[0]), int(columns[1]))
+            if rc:
+                lib.swx_solver_destroy(h)
+                self.h = None
+                _lib.check(rc)
         self.alphas = np.ascontiguousarray(alphas, dtype=np.complex128)
         ep, ei = ctypes.c_int(-1), ctypes.c_int(-1)
         rc = lib.swx_solver_warm(h, self.alphas.ctypes.data, self.alphas.size,
@@ -85,7 +91,10 @@ class ShiftedLinearSolver:
 
     _MAX_SETS = 4
 
-    def __init__(self, group: TermGroup, dt: float, params: ModelParams):
+    def __init__(self, group: TermGroup, dt: float, params: ModelParams, columns=None):
+        """``columns=(m0, m1)`` restricts the lg pole sums to one column
+        shard (parallel.ColumnShard); such a solver is private to its engine,
+        never the shared ``get_solver`` instance."""
         if group.atoms not in (LG.atoms, L.atoms):
             raise ConfigurationError(
                 f"shifted solves support groups 'lg' and 'l', got {group.token!r}")
@@ -101,6 +110,7 @@ class ShiftedLinearSolver:
         self._lib = _lib.lib()
         self._sets: collections.OrderedDict = collections.OrderedDict()
         self._ws = {}
+        self.columns = None if columns is None else (int(columns[0]), int(columns[1]))
 
     # -- shift sets ---------------------------------------------------------
     def _native(self, alphas) -> _Native:
@@ -111,7 +121,7 @@ class ShiftedLinearSolver:
             self._sets.move_to_end(key)
             return hit
         nat = _Native(self._lib, self._code, self.params.cfg, self.dt,
-                      self.params.mean_geopotential, a, stream_ptr())
+                      self.params.mean_geopotential, a, stream_ptr(), self.columns)
         self._sets[key] = nat
         while len(self._sets) > self._MAX_SETS:
             self._sets.popitem(last=False)

@@ -423,3 +423,87 @@ def test_galewsky_initial_state_and_error_golden(golden_io):
     h = linf_error(st, st0, "h")
     assert abs(h - float(golden_io["T42_linf_h"])) <= 1e-9 * float(golden_io["T42_linf_h"])
     assert linf_error(st, st0, "vort") == 0.0
+
+
+# ------------------------------------------------- column shards (§8f f1)
+
+def _virtual_tendency(trunc, K, st, sub=None):
+    """K co-resident column shards of one device run the sharded tendency in
+    lockstep (virtual all-to-all); returns the assembled packed result."""
+    from paper_1805_06557_b200.parallel import (ColumnShard, ShardedTendency, run_lockstep,
+                                                virtual_exchange)
+    cfg = SphereConfig.for_truncation(trunc)
+    plan = plan_for(cfg)
+    shards = [ColumnShard(cfg, r, K) for r in range(K)]
+    tends = [ShardedTendency(plan, sh, 3) for sh in shards]
+    outs = [torch.full_like(st, float("nan")) for _ in range(K)]
+    run_lockstep((t.phases(st, o, sub) for t, o in zip(tends, outs)),
+                 lambda items: virtual_exchange([t for t, _ in items], items[0][1]))
+    full = torch.full_like(st, float("nan"))
+    for sh, o in zip(shards, outs):
+        a, b = sh.slots()
+        full[:, a:b] = o[:, a:b]
+    return full.cpu().numpy()
+
+
+@pytest.mark.parametrize("trunc,ks", [(63, (1, 2, 3, 8)), (256, (2, 4, 8))])
+def test_column_sharded_tendency_bitwise(trunc, ks):
+    """m-sharded synthesis / latitude-sharded grid stage / m-sharded analysis
+    with two all-to-alls == the single-rank fused tendency, bitwise."""
+    g = osh.grid_for(trunc)
+    st = ost.seeded_balanced_state(g)
+    st[2] = ost.seeded_linear_state(trunc, 9)[2] * 1e-1
+    st = to_device(olay.pack(st))
+    sub = to_device(pack(ost.seeded_linear_state(trunc, 6)))
+    plan = plan_for(SphereConfig.for_truncation(trunc))
+    ref = plan.tendency_dev(3, st).cpu().numpy()
+    ref_sub = plan.tendency_dev(3, st, sub=sub).cpu().numpy()
+    for K in ks:
+        assert np.array_equal(_virtual_tendency(trunc, K, st), ref), K
+        assert np.array_equal(_virtual_tendency(trunc, K, st, sub), ref_sub), K
+
+
+def test_column_sharded_etdrk_bitwise():
+    """cfg2-shaped ETD2RK (T85, N=128) on 3 column shards: lg pole sums on the
+    own columns, sharded tendencies; 2 steps == the single-rank engine."""
+    from paper_1805_06557_b200.parallel import (ColumnEtdrkEngine, ColumnShard, run_lockstep,
+                                                virtual_exchange)
+    from paper_1805_06557_b200.steppers import EtdrkStepper
+    trunc, K, dt = 85, 3, 1800.0
+    par = params(trunc)
+    ic = ost.seeded_balanced_state(osh.grid_for(trunc))
+    stepper = EtdrkStepper(LG, LC_N, par, RexiSetup(num_poles=128))
+    sets = stepper.coeff_set(dt)
+    ref = stepper.engine(dt)
+    ref.load(ic)
+    engines = [ColumnEtdrkEngine(LG, LC_N, par, dt, sets, ColumnShard(par.cfg, r, K))
+               for r in range(K)]
+    for e in engines:
+        e.load(ic)
+    for _ in range(2):
+        ref.step_dev()
+        run_lockstep((e.phases() for e in engines),
+                     lambda items: virtual_exchange([t for t, _ in items], items[0][1]))
+    want = ref.u.cpu().numpy()
+    for e in engines:
+        a, b = e.shard.slots()
+        assert np.array_equal(e.own().cpu().numpy(), want[:, a:b]), e.shard.rank
+
+
+def test_lg_column_restricted_sum_bitwise():
+    """swx_solver_set_columns: the own columns of a restricted lg pole sum
+    equal the full sum bitwise; the Coriolis group refuses column shards."""
+    from paper_1805_06557_b200.errors import ConfigurationError
+    par = params(63)
+    c = coeffs(128)
+    st = to_device(pack(ost.seeded_linear_state(63, 2)))[None]
+    b = to_device(np.asarray(c.betas).reshape(1, -1))
+    full = ShiftedLinearSolver(LG, 900.0, par).rexi_sum_dev(c.alphas, b, st).cpu().numpy()
+    from paper_1805_06557_b200.parallel import column_slots
+    for m0, m1 in ((0, 9), (9, 40), (40, 64), (63, 64)):
+        s = ShiftedLinearSolver(LG, 900.0, par, columns=(m0, m1))
+        got = s.rexi_sum_dev(c.alphas, b, st).cpu().numpy()
+        a, z = column_slots(63, m0, m1)
+        assert np.array_equal(got[..., a:z], full[..., a:z]), (m0, m1)
+    with pytest.raises(ConfigurationError):
+        ShiftedLinearSolver(L, 900.0, par, columns=(0, 9)).warm(c.alphas)

@@ -188,3 +188,27 @@ def test_host_pack_unpack_match_layout(trunc):
     ptrs = (ctypes.c_void_p * 3)(*[d.ctypes.data for d in dst])
     assert lib.swx_host_unpack(trunc, 3, np.ascontiguousarray(ref).ctypes.data, ptrs) == 0
     assert all(np.array_equal(a, b) for a, b in zip(dst, dense))
+
+
+@pytest.mark.parametrize("trunc", [21, 63, 85, 256, 1279])
+def test_column_shard_bounds_c_matches_host_mirror(trunc):
+    """swx_shard_init (host code in the library, no device) == the Python
+    mirror; columns cover [0, T] contiguously with balanced column work."""
+    from paper_1805_06557_b200.parallel import ColumnShard, column_slots, shard_bounds
+    cfg = SphereConfig.for_truncation(trunc)
+    for K in (1, 2, 3, 4, 8):
+        mb, pb = shard_bounds(trunc, cfg.nlat, K)
+        for r in range(K):
+            sh = ColumnShard(cfg, r, K)
+            assert sh.m_bounds == mb and sh.p_bounds == pb
+        assert mb[0] == 0 and mb[-1] == trunc + 1 and list(mb) == sorted(mb)
+        nh = (cfg.nlat + 1) // 2
+        assert pb[-1] == (nh + 15) // 16 * 16 and pb[-2] <= nh
+        work = [column_slots(trunc, mb[r], mb[r + 1]) for r in range(K)]
+        sizes = [b - a for a, b in work]
+        assert sum(sizes) == (trunc + 1) * (trunc + 2) // 2
+        # balanced: every share within one (longest) column of the ideal
+        ideal = sum(sizes) / K
+        assert max(abs(n - ideal) for n in sizes) <= trunc + 1
+    with pytest.raises(ConfigurationError):
+        ColumnShard(cfg, 2, 2)

@@ -57,3 +57,122 @@ def test_two_rank_tree_reduce_bitwise(tmp_path):
     for group in ("lg", "l"):
         combined, serial = np.load(path + f"_{group}.npy")
         assert np.array_equal(combined, serial), group
+
+
+# ------------------------------------------------------------------ column shards
+# The exchange protocol of the column-sharded tendency on
+# real ranks: the device stages are replaced by numpy restatements of the
+# same three stages (Legendre synthesis of the own columns -> latitude rows
+# of every peer; grid products of the own latitude pairs -> columns of every
+# peer; Legendre analysis of the own columns), moved by ColumnComm.all_to_all
+# over gloo with the ColumnShard bounds of the library, then assembled by
+# ColumnComm.gather_columns.  The result must equal the oracle's unsharded
+# tendency_n.
+
+def _pair_rows(nlat, a, b):
+    """Latitude rows of pairs [a, b): south rows a..b-1, north rows nlat-b..nlat-a-1."""
+    nh = (nlat + 1) // 2
+    a, b = min(a, nh), min(b, nh)
+    return np.unique(np.r_[np.arange(a, b), np.arange(nlat - b, nlat - a)]).astype(int)
+
+
+def _col_worker(rank, world, port, result_path):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import layout as olay
+    from oracle import sht as osh
+    from oracle import stepping as ost
+    from paper_1805_06557_b200.parallel import ColumnComm, ColumnShard
+    from paper_1805_06557_b200.sphere import SphereConfig
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        trunc = 21
+        g = osh.grid_for(trunc)
+        cfg = SphereConfig.for_truncation(trunc)
+        assert (cfg.nlat, cfg.nlon) == (g.nlat, g.nlon)
+        shard = ColumnShard(cfg, rank, world)
+        comm = ColumnComm()
+        mb, pb = shard.m_bounds, shard.p_bounds
+        st = ost.seeded_balanced_state(g)
+        st[2] = ost.seeded_linear_state(trunc, 9)[2] * 1e-1
+        T1, nlat, a_r = trunc + 1, g.nlat, g.radius
+        im = 1j * g.ms[None, :]
+        sec = 1.0 / g.cosl[:, None]
+        rows = [_pair_rows(nlat, pb[r], pb[r + 1]) for r in range(world)]
+        cols = [np.arange(mb[r], mb[r + 1]) for r in range(world)]
+
+        def exchange(blocks):  # blocks[peer] -> numpy array for that peer
+            send = [np.ascontiguousarray(blocks[s]).view(np.uint8).ravel()
+                    if s != rank else np.zeros(0, np.uint8) for s in range(world)]
+            sc = [x.size for x in send]
+            rc = torch.tensor(sc)
+            allc = [torch.zeros_like(rc) for _ in range(world)]
+            dist.all_gather(allc, rc)
+            rcv = [int(allc[r][rank]) for r in range(world)]
+            sbuf = torch.from_numpy(np.concatenate(send) if sum(sc) else np.zeros(1, np.uint8))
+            rbuf = torch.zeros(max(sum(rcv), 1), dtype=torch.uint8)
+            comm.all_to_all(sbuf, sc, rbuf, rcv)
+            out, o = {}, 0
+            for r in range(world):
+                out[r] = rbuf[o:o + rcv[r]].numpy()
+                o += rcv[r]
+            return out
+
+        # stage 0: own columns, all latitudes (u, v, vort, phi' Fourier rows)
+        own = np.zeros(T1)
+        own[cols[rank]] = 1.0
+        vort, div, phi = st[1] * own, st[2] * own, st[0] * own
+        psi, chi = g.inv_laplacian(vort), g.inv_laplacian(div)
+        ls = g.legendre_synthesis
+        F = np.stack([(ls(chi * im, "p") * sec - ls(psi, "h")) / a_r,
+                      (ls(psi * im, "p") * sec + ls(chi, "h")) / a_r,
+                      ls(vort, "p"), ls(phi, "p")])
+        got = exchange({s: F[:, rows[s]][:, :, cols[rank]] for s in range(world)})
+        Fr = np.zeros((4, rows[rank].size, T1), complex)
+        for r in range(world):
+            blk = F[:, rows[rank]][:, :, cols[r]] if r == rank else \
+                got[r].view(complex).reshape(4, rows[rank].size, cols[r].size)
+            Fr[:, :, cols[r]] = blk
+        # stage 1: own latitude rows -> grids -> products -> Fourier rows
+        half = np.zeros((4, rows[rank].size, g.nlon // 2 + 1), complex)
+        half[..., :T1] = Fr
+        u, v, z, p = np.fft.irfft(half, n=g.nlon, axis=2) * g.nlon
+        prods = np.stack([p * u, p * v, z * u, z * v, 0.5 * (u * u + v * v)])
+        Gr = np.fft.fft(prods, axis=2)[..., :T1] * g.dlon
+        got = exchange({r: Gr[:, :, cols[r]] for r in range(world)})
+        Gc = np.zeros((5, nlat, T1), complex)
+        for s in range(world):
+            blk = Gr[:, :, cols[rank]] if s == rank else \
+                got[s].view(complex).reshape(5, rows[s].size, cols[rank].size)
+            Gc[:, rows[s][:, None], cols[rank][None, :]] = blk
+        # stage 2: own columns, Legendre analysis (vortdiv_from_uv, sphere.py:405-430)
+        la = g.legendre_analysis
+        woc = g.w / g.cosl
+
+        def vortdiv(fu, fv):
+            return ((im * la(fv, "p", woc) + la(fu, "h", g.w)) / a_r,
+                    (im * la(fu, "p", woc) - la(fv, "h", g.w)) / a_r)
+
+        _, div_pf = vortdiv(Gc[0], Gc[1])
+        curl_zf, div_zf = vortdiv(Gc[2], Gc[3])
+        ke = la(Gc[4], "p", g.w)
+        res = np.stack([-div_pf, -div_zf, curl_zf - g.laplacian(ke)]) * own
+        full = comm.gather_columns(torch.from_numpy(olay.pack(res)), shard).numpy()
+        if rank == 0:
+            np.save(result_path, np.stack([full, olay.pack(g.tendency_n(st))]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_column_sharded_tendency_exchange(tmp_path, world):
+    port = _free_port()
+    path = str(tmp_path / "col.npy")
+    mp.spawn(_col_worker, args=(world, port, path), nprocs=world, join=True)
+    got, ref = np.load(path)
+    err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
+    assert err <= 1e-12, err
