@@ -37,6 +37,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg4"), default="cfg2")
+    ap.add_argument("--shard", choices=("auto", "poles", "cols"), default="auto",
+                    help="N>1: shard REXI poles (+ all-reduce) or zonal columns (ETD2RK: "
+                         "sharded N term, 4 all-to-alls per step); auto = cols for cfg2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -205,6 +208,48 @@ def load_traffic():
     return {}
 
 
+def column_breakdown(torch, eng, ccomm, flush, reps=5):
+    """Rank-local device times of the column-sharded step's pieces: the
+    three tendency stages (each with its slab pack/unpack copies) and one
+    column-restricted pole sum; the all-to-alls are in the step time only."""
+    t = eng.tend
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    acc = np.zeros(4)
+    for _ in range(reps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev[0].record()
+        t.stage(0, eng.u, None, None)
+        ev[1].record()
+        ccomm.all_to_all(*t.slabs(0))
+        ev[2].record()
+        t.stage(1)
+        ev[3].record()
+        ccomm.all_to_all(*t.slabs(1))
+        ev[4].record()
+        t.stage(2, None, eng.nu[0], None)
+        ev[5].record()
+        torch.cuda.synchronize()
+        acc[0] += ev[0].elapsed_time(ev[1])
+        acc[1] += ev[2].elapsed_time(ev[3])
+        acc[2] += ev[4].elapsed_time(ev[5])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        e0.record()
+        eng.rexi.apply((2,), eng.d, eng.psi0, None, base=eng.a[None], scale=eng.dt)
+        e1.record()
+        e1.synchronize()
+        acc[3] += e0.elapsed_time(e1)
+    acc /= reps
+    bd = {"synth_state": {"ms_per_launch": acc[0], "launches_per_step": 2},
+          "grid_fused": {"ms_per_launch": acc[1], "launches_per_step": 2},
+          "analysis": {"ms_per_launch": acc[2], "launches_per_step": 2},
+          "rexi_lg": {"ms_per_launch": acc[3], "launches_per_step": 3}}
+    for v in bd.values():
+        v["ms_per_step"] = v["ms_per_launch"] * v["launches_per_step"]
+    return bd, max(bd, key=lambda k: bd[k]["ms_per_step"])
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -216,28 +261,45 @@ def main():
 
     from paper_1805_06557_b200 import _lib
     from paper_1805_06557_b200.device import ncoef, pack, to_device
-    from paper_1805_06557_b200.parallel import PoleComm
+    from paper_1805_06557_b200.parallel import (ColumnComm, ColumnEtdrkEngine, ColumnShard,
+                                                PoleComm)
     from paper_1805_06557_b200.steppers import EtdrkStepper, RexiStepper
     from paper_1805_06557_b200.swe import LC_N, LG, L, PrognosticState, TermGroup
     from paper_1805_06557_b200.workloads import (CONFIGS, seeded_balanced_state,
                                                  seeded_linear_state)
 
     torch.cuda.set_device(local)
-    comm = None
-    # SWX_FORCE_COMM=1 routes a 1-rank run through the multi-rank reduce
-    # (NCCL all-gather + device tree combine), to exercise that path on 1 GPU
+    comm = ccomm = None
+    etd = args.config == "cfg2"
+    mode = args.shard if args.shard != "auto" else ("cols" if etd else "poles")
+    if mode == "cols" and not etd:
+        raise SystemExit("--shard cols is the ETD2RK (cfg2) decomposition")
+    # SWX_FORCE_COMM=1 routes a 1-rank run through the multi-rank path (NCCL
+    # process group, pole reduce or column exchanges), to exercise it on 1 GPU
     force = os.environ.get("SWX_FORCE_COMM") == "1"
     if world > 1 or force:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        comm = PoleComm(deterministic=os.environ.get("SWX_FAST_REDUCE") != "1")
+        if mode == "cols":
+            ccomm = ColumnComm()
+        else:
+            comm = PoleComm(deterministic=os.environ.get("SWX_FAST_REDUCE") != "1")
     lib = _lib.lib()
     w = CONFIGS[args.config]
     par = w.params
     nc = ncoef(w.trunc)
     group = TermGroup.parse(w.group)
-    etd = args.config == "cfg2"
 
-    if etd:
+    if ccomm is not None:
+        stepper = EtdrkStepper(group, LC_N, par, w.setup)
+        shard = ColumnShard(par.cfg, rank, world)
+        eng = ColumnEtdrkEngine(group, LC_N, par, w.dt, stepper.coeff_set(w.dt), shard)
+        ic = seeded_balanced_state(par.cfg)
+        eng.load(ic)
+
+        def step():
+            return eng.step_dev(ccomm)
+        units_per_step = 3 * w.n_poles * nc
+    elif etd:
         stepper = EtdrkStepper(group, LC_N, par, w.setup)
         eng = stepper.engine(w.dt, comm)
         ic = seeded_balanced_state(par.cfg)
@@ -272,7 +334,8 @@ def main():
         torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if comm is not None:
+    multi = comm is not None or ccomm is not None
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
@@ -283,12 +346,12 @@ def main():
         ends[k].record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
-    if comm is not None:
+    if multi:
         dist.barrier()
     clocks = sampler.stop()
     ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_total = torch.tensor([sum(ms_steps)], dtype=torch.float64, device="cuda")
-    if comm is not None:
+    if multi:
         dist.all_reduce(ms_total, op=dist.ReduceOp.MAX)
     ms_total = float(ms_total.item())
     ms_per_step = ms_total / args.steps
@@ -305,7 +368,9 @@ def main():
     s_ptr = cur.cuda_stream
     breakdown = {}
     dominant = None
-    if etd:
+    if ccomm is not None:
+        breakdown, dominant = column_breakdown(torch, eng, ccomm, flush)
+    elif etd:
         plan = eng.plan
         reps = 5
         # with the fused grid stage, C2R+products+R2C+prep all land in "grid_fused"
@@ -396,6 +461,13 @@ def main():
         "analysis": 7 * leg,
         "grid_fused": grid_flops,
     }
+    if ccomm is not None:  # rank-local shares: own columns / own latitude pairs
+        a, b = eng.shard.slots()
+        fc = (b - a) / nc
+        pb = eng.shard.p_bounds
+        fp = (min(pb[rank + 1], nlat // 2) - min(pb[rank], nlat // 2)) / (nlat // 2)
+        flops = {"rexi_lg": flops["rexi_lg"] * fc, "synth_state": flops["synth_state"] * fc,
+                 "analysis": flops["analysis"] * fc, "grid_fused": grid_flops * fp}
     peak64 = fp64_peak_tflops(torch, lib, _lib)
     traffic = load_traffic()
     roofline = None
@@ -415,7 +487,31 @@ def main():
 
     # ---- end to end through the public API (host numpy in, host numpy out)
     e2e = None
-    if not args.no_e2e and comm is None:
+    if not args.no_e2e and ccomm is not None:
+        # every rank: host pack + H2D of the full state, the sharded step, the
+        # column all-gather and D2H + unpack of the full state
+        from paper_1805_06557_b200.device import HostStage
+        stage = HostStage(w.trunc)
+        st_host = PrognosticState.from_stack(ic, par.cfg)
+        n_e2e = max(3, min(args.steps, 20))
+        tt = []
+        for k in range(n_e2e + 1):
+            dist.barrier()
+            t0 = time.perf_counter()
+            stage.upload(st_host, eng.u)
+            eng.step_dev(ccomm)
+            full = ccomm.gather_columns(eng.u, eng.shard)
+            f = stage.download(full)
+            tt.append(time.perf_counter() - t0)
+            st_host = PrognosticState.from_stack(np.stack(f), par.cfg)
+        sec = torch.tensor([sum(tt[1:]) / n_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(sec, op=dist.ReduceOp.MAX)
+        sec = float(sec.item())
+        e2e = {"value": units_per_step / sec, "unit": "pole-solve*coeff/s",
+               "ms_per_step": sec * 1e3, "h2d_bytes_per_step": 3 * nc * 16,
+               "d2h_bytes_per_step": 3 * nc * 16,
+               "api": "ColumnEtdrkEngine (host state in, column all-gather, host state out)"}
+    if not args.no_e2e and comm is None and ccomm is None:
         st_host = PrognosticState.from_stack(ic, par.cfg)
         n_e2e = max(3, min(args.steps, 20))
         st_host = stepper.step(st_host, w.dt)  # warm
@@ -459,7 +555,7 @@ def main():
 
     # kernels per step: counted from the captured step graph (ETD2RK); the linear
     # configs launch one fused pole-sum kernel (lg) or kernel + tree combine (l)
-    per_step_launches = (eng.kernel_launches if etd else None) or \
+    per_step_launches = (eng.kernel_launches if etd and ccomm is None else None) or \
         ((9 if comm is None else 12) if etd else (1 if w.group == "lg" else 2))
     line = {
         "metric": "REXI pole-solves*SH-coeffs/s", "value": value, "unit": "pole-solve*coeff/s",
@@ -470,9 +566,11 @@ def main():
         "config": {"workload": w.name, "trunc": w.trunc, "grid": [par.cfg.nlat, par.cfg.nlon],
                    "n_poles": w.n_poles, "dt": w.dt,
                    "units_per_step": units_per_step,
-                   "parallelism": f"poles sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+                   "parallelism": ((f"zonal columns sharded over {world} GPU(s)" if ccomm
+                                    else f"poles sharded over {world} GPU(s)")
+                                   if multi else "1 GPU"),
                    "l2": "flushed (256 MB write) before every timed step",
-                   "cuda_graph": bool(etd and comm is None)},
+                   "cuda_graph": bool(etd and not multi)},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": per_step_launches * args.steps,
         "clocks": clocks, "kernel_breakdown_ms": breakdown,
@@ -480,7 +578,7 @@ def main():
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if comm is not None:
+    if multi:
         dist.destroy_process_group()
 
 

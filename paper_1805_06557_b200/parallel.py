@@ -315,6 +315,8 @@ class ColumnComm:
 
     def all_to_all(self, send, send_counts, recv, recv_counts):
         """Byte slabs ordered by peer (swx_sht_shard_counts order)."""
+        if self.world == 1:  # the self slab never travels
+            return
         self.dist.all_to_all_single(recv[: sum(recv_counts)], send[: sum(send_counts)],
                                     list(recv_counts), list(send_counts), group=self.group)
 
