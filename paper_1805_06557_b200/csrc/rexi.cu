@@ -63,7 +63,12 @@ template <int NP>
 __device__ __forceinline__ PhiDiv tree_pd(const double2 *__restrict__ A, const double2 *__restrict__ B,
                                           const double2 *__restrict__ C, int t0, int st, double2 bp,
                                           double2 bd) {
-  if constexpr (NP == 1) {
+  if constexpr (NP == 2) {  // pole pair: one FMA chain (see tree_pd_m)
+    PhiDiv o;
+    o.p = cfma(A[t0 + st], bp, cfma(B[t0 + st], bd, cfma(A[t0], bp, cmul(B[t0], bd))));
+    o.d = cfma(A[t0 + st], bd, cfma(C[t0 + st], bp, cfma(A[t0], bd, cmul(C[t0], bp))));
+    return o;
+  } else if constexpr (NP == 1) {
     const double2 fa = A[t0], fb = B[t0], fc = C[t0];
     PhiDiv o;
     o.p = cfma(fa, bp, cmul(fb, bd));  // (a phi + dt phibar div) / det, beta folded
@@ -80,7 +85,9 @@ __device__ __forceinline__ PhiDiv tree_pd(const double2 *__restrict__ A, const d
 
 template <int NP>
 __device__ __forceinline__ double2 tree_z(const double2 *__restrict__ D, int t0, int st, double2 bz) {
-  if constexpr (NP == 1) {
+  if constexpr (NP == 2) {
+    return cfma(D[t0 + st], bz, cmul(D[t0], bz));
+  } else if constexpr (NP == 1) {
     return cmul(D[t0], bz);  // vort / a, beta folded
   } else {
     const double2 x = tree_z<NP / 2>(D, t0, st, bz);
@@ -90,13 +97,25 @@ __device__ __forceinline__ double2 tree_z(const double2 *__restrict__ D, int t0,
 
 // the same trees for MPL modes of one degree at once: every factor load is
 // shared by the MPL modes (per-mode pairwise order unchanged)
-template <int NP, int MPL>
+// PR: the leaves are pole pairs (2k, 2k+1) whose two terms are summed as
+// one FMA chain (the pair's add folded into the FMAs); the tree above the
+// pairs is unchanged, so blocks of >= 2 aligned poles still combine in
+// tree_sum's order (rank-count independent)
+template <int NP, int MPL, bool PR = false>
 __device__ __forceinline__ void tree_pd_m(const double2 *__restrict__ A,
                                           const double2 *__restrict__ B,
                                           const double2 *__restrict__ C, int t0, int st,
                                           const double2 (&bp)[MPL], const double2 (&bd)[MPL],
                                           PhiDiv (&o)[MPL]) {
-  if constexpr (NP == 1) {
+  if constexpr (PR && NP == 2) {
+    const double2 fa = A[t0], fb = B[t0], fc = C[t0];
+    const double2 ga = A[t0 + st], gb = B[t0 + st], gc = C[t0 + st];
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) {
+      o[j].p = cfma(ga, bp[j], cfma(gb, bd[j], cfma(fa, bp[j], cmul(fb, bd[j]))));
+      o[j].d = cfma(ga, bd[j], cfma(gc, bp[j], cfma(fa, bd[j], cmul(fc, bp[j]))));
+    }
+  } else if constexpr (NP == 1) {
     const double2 fa = A[t0], fb = B[t0], fc = C[t0];
 #pragma unroll
     for (int j = 0; j < MPL; ++j) {
@@ -105,8 +124,8 @@ __device__ __forceinline__ void tree_pd_m(const double2 *__restrict__ A,
     }
   } else {
     PhiDiv y[MPL];
-    tree_pd_m<NP / 2, MPL>(A, B, C, t0, st, bp, bd, o);
-    tree_pd_m<NP / 2, MPL>(A, B, C, t0 + (NP / 2) * st, st, bp, bd, y);
+    tree_pd_m<NP / 2, MPL, PR>(A, B, C, t0, st, bp, bd, o);
+    tree_pd_m<NP / 2, MPL, PR>(A, B, C, t0 + (NP / 2) * st, st, bp, bd, y);
 #pragma unroll
     for (int j = 0; j < MPL; ++j) {
       o[j].p = cadd(o[j].p, y[j].p);
@@ -115,17 +134,21 @@ __device__ __forceinline__ void tree_pd_m(const double2 *__restrict__ A,
   }
 }
 
-template <int NP, int MPL>
+template <int NP, int MPL, bool PR = false>
 __device__ __forceinline__ void tree_z_m(const double2 *__restrict__ D, int t0, int st,
                                          const double2 (&bz)[MPL], double2 (&o)[MPL]) {
-  if constexpr (NP == 1) {
+  if constexpr (PR && NP == 2) {
+    const double2 fd = D[t0], gd = D[t0 + st];
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) o[j] = cfma(gd, bz[j], cmul(fd, bz[j]));
+  } else if constexpr (NP == 1) {
     const double2 fd = D[t0];
 #pragma unroll
     for (int j = 0; j < MPL; ++j) o[j] = cmul(fd, bz[j]);
   } else {
     double2 y[MPL];
-    tree_z_m<NP / 2, MPL>(D, t0, st, bz, o);
-    tree_z_m<NP / 2, MPL>(D, t0 + (NP / 2) * st, st, bz, y);
+    tree_z_m<NP / 2, MPL, PR>(D, t0, st, bz, o);
+    tree_z_m<NP / 2, MPL, PR>(D, t0 + (NP / 2) * st, st, bz, y);
 #pragma unroll
     for (int j = 0; j < MPL; ++j) o[j] = cadd(o[j], y[j]);
   }
@@ -318,7 +341,7 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
 // Static-geometry variant with MPL modes per lane group: LPM lanes own MPL
 // modes of the same degree (m = base + g, base + g + 128/LPM, ...), so each
 // factor load from shared memory feeds MPL modes.
-template <int NRHS, int NP, int LPM, int MPL>
+template <int NRHS, int NP, int LPM, int MPL, bool PR = false>
 __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
     const int4 *__restrict__ sched, int n_items, int realify, Axpy ep, int fac_ready,
@@ -373,8 +396,8 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
       }
       PhiDiv pd[MPL];
       double2 z[MPL];
-      tree_pd_m<PPL, MPL>(F, F + NP, F + 2 * NP, 0, LPM, bp, bd, pd);
-      tree_z_m<PPL, MPL>(F + 3 * NP, 0, LPM, bz, z);
+      tree_pd_m<PPL, MPL, PR>(F, F + NP, F + 2 * NP, 0, LPM, bp, bd, pd);
+      tree_z_m<PPL, MPL, PR>(F + 3 * NP, 0, LPM, bz, z);
 #pragma unroll
       for (int o = 1; o < LPM; o <<= 1)
 #pragma unroll
@@ -399,6 +422,210 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
     }
   }
 }
+}
+
+// K1 (persistent form): the lane-group mapping of rexi_lg_mm_kernel over
+// one-pass items (l, 32 modes) sorted largest first and dealt round-robin to
+// sm_count x occupancy persistent CTAs, so every SM gets the same number of
+// items (the one-shot grid of 645 two-pass CTAs runs 1.45 waves at T256);
+// item k+1's factor table streams into the second shared-memory buffer
+// (cp.async) while item k computes.  Same trees, same bits.
+__device__ __forceinline__ void lg_cp16(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int NRHS, int NP, int LPM, int MPL>
+__global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_pers_kernel(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
+    const int4 *__restrict__ sched, int n_items, int realify, Axpy ep, int fac_ready,
+    double2 *__restrict__ out) {
+  constexpr int PPL = NP / LPM;
+  constexpr int GROUPS = 128 / LPM;
+  constexpr int TAB = NRHS * 4 * NP;     // double2 per factor table
+  extern __shared__ double2 fac2[];      // [2][TAB]
+  pdl_trigger();
+  if (!fac_ready) pdl_wait();
+  auto stage = [&](int it, int buf) {
+    const double2 *src = fac_g + (size_t)sched[it].x * TAB;
+    double2 *dst = fac2 + buf * TAB;
+    for (int i = threadIdx.x; i < TAB; i += blockDim.x) lg_cp16(dst + i, src + i);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int it = blockIdx.x;
+  if (it < n_items) stage(it, 0);
+  pdl_wait();
+  const int q = threadIdx.x & (LPM - 1);
+  const int g = threadIdx.x / LPM;
+  for (int k = 0; it < n_items; it += gridDim.x, ++k) {
+    const int nxt = it + gridDim.x;
+    if (nxt < n_items) {
+      stage(nxt, (k + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double2 *fac = fac2 + (k & 1) * TAB;
+    const int4 w = sched[it];
+    const int l = w.x, m0 = w.y, m1 = w.z;
+    int m[MPL];
+    bool has[MPL];
+    size_t idx[MPL];
+#pragma unroll
+    for (int j = 0; j < MPL; ++j) {
+      m[j] = m0 + g + j * GROUPS;
+      has[j] = m[j] < m1;
+      idx[j] = has[j] ? (size_t)col_offset(trunc, m[j]) + (l - m[j]) : 0;
+    }
+#pragma unroll 1
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 *F = fac + (size_t)r * 4 * NP + q;
+      double2 bp[MPL], bz[MPL], bd[MPL], e[MPL][3];
+#pragma unroll
+      for (int j = 0; j < MPL; ++j) {
+        bp[j] = bz[j] = bd[j] = make_double2(0.0, 0.0);
+        if (has[j]) {
+          bp[j] = rhs[(size_t)(r * 3 + 0) * ncoef + idx[j]];
+          bz[j] = rhs[(size_t)(r * 3 + 1) * ncoef + idx[j]];
+          bd[j] = rhs[(size_t)(r * 3 + 2) * ncoef + idx[j]];
+        }
+        if (ep.base && has[j] && q == 0)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) e[j][c] = ep.base[(size_t)(r * 3 + c) * ncoef + idx[j]];
+      }
+      PhiDiv pd[MPL];
+      double2 z[MPL];
+      tree_pd_m<PPL, MPL, true>(F, F + NP, F + 2 * NP, 0, LPM, bp, bd, pd);
+      tree_z_m<PPL, MPL, true>(F + 3 * NP, 0, LPM, bz, z);
+#pragma unroll
+      for (int o = 1; o < LPM; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < MPL; ++j) {
+          pd[j].p = cadd(pd[j].p, shfl_xor2(pd[j].p, o));
+          pd[j].d = cadd(pd[j].d, shfl_xor2(pd[j].d, o));
+          z[j] = cadd(z[j], shfl_xor2(z[j], o));
+        }
+#pragma unroll
+      for (int j = 0; j < MPL; ++j)
+        if (has[j] && q == 0) {
+          if (realify && m[j] == 0) pd[j].p.y = z[j].y = pd[j].d.y = 0.0;
+          const size_t o = (size_t)r * 3 * ncoef + idx[j];
+          double2 v[3] = {pd[j].p, z[j], pd[j].d};
+          if (ep.base)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              v[c] = make_double2(e[j][c].x + v[c].x * ep.scale, e[j][c].y + v[c].y * ep.scale);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) out[o + (size_t)c * ncoef] = v[c];
+        }
+    }
+    __syncthreads();  // buffer k & 1 is restaged by item k + 2
+  }
+}
+
+// K1 (warp form): one warp = 32 modes of one degree l, one lane = one mode
+// walking all NP poles itself, so no lane-group butterfly and no shared
+// memory: the per-(pole, l) factors are warp-uniform loads (one L1 line
+// serves the whole warp).  Blocks of 32 poles are statically unrolled trees
+// with pair leaves; blocks combine through a binary counter -- the same
+// perfect pairwise tree (tree_sum's order) as rexi_lg_mm_kernel<..., true>,
+// hence identical bits.  1-warp CTAs, one per 32-mode item, all resident at
+// once at T256 (1161 warps): the load balances over the SMs without waves.
+// Factor layout: natural pole order (lg_geom lpm = 1).
+template <int NRHS, int NP>
+__global__ void __launch_bounds__(32) rexi_lg_warp_kernel(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
+    const int4 *__restrict__ sched, int realify, Axpy ep, int fac_ready,
+    double2 *__restrict__ out) {
+  constexpr int NB = NP / 32;  // 32-pole blocks
+  static_assert(NB >= 1 && NB <= (1 << kLgLevels), "pole count");
+  pdl_trigger();
+  const int4 w = sched[blockIdx.x];
+  const int l = w.x, m = w.y + (int)threadIdx.x;
+  const bool has = m < w.z;
+  const size_t idx = has ? (size_t)col_offset(trunc, m) + (l - m) : 0;
+  extern __shared__ double2 fsm[];  // [NRHS][4][NP]
+  {
+    // factor tables do not depend on the preceding kernel: stage them first
+    // (PDL overlap); all loads in flight before the first store
+    if (!fac_ready) pdl_wait();
+    const double4 *src = reinterpret_cast<const double4 *>(fac_g + (size_t)l * NRHS * 4 * NP);
+    double4 *dst = reinterpret_cast<double4 *>(fsm);
+    constexpr int N4 = NRHS * 2 * NP, PER = N4 / 32;
+    double4 t[PER < 16 ? PER : 16];
+#pragma unroll
+    for (int c0 = 0; c0 < PER; c0 += 16) {
+#pragma unroll
+      for (int c = 0; c < 16 && c0 + c < PER; ++c) t[c] = src[(c0 + c) * 32 + threadIdx.x];
+#pragma unroll
+      for (int c = 0; c < 16 && c0 + c < PER; ++c) dst[(c0 + c) * 32 + threadIdx.x] = t[c];
+    }
+    __syncwarp();
+  }
+  pdl_wait();
+#pragma unroll 1
+  for (int r = 0; r < NRHS; ++r) {
+    const double2 *F = fsm + (size_t)r * 4 * NP;
+    double2 bp[1] = {make_double2(0.0, 0.0)}, bz[1] = {bp[0]}, bd[1] = {bp[0]};
+    double2 e[3];
+    if (has) {
+      bp[0] = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
+      bz[0] = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
+      bd[0] = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
+      if (ep.base)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) e[c] = ep.base[(size_t)(r * 3 + c) * ncoef + idx];
+    }
+    // (phi', div) tree, then the vort tree (halves the live state)
+    PhiDiv stk[kLgLevels], v[1];
+#pragma unroll 1
+    for (int blk = 0; blk < NB; ++blk) {
+      const double2 *Fb = F + blk * 32;
+      tree_pd_m<32, 1, true>(Fb, Fb + NP, Fb + 2 * NP, 0, 1, bp, bd, v);
+      bool done = false;
+#pragma unroll
+      for (int lv = 0; lv < kLgLevels; ++lv)
+        if (!done) {
+          if ((blk >> lv) & 1) {
+            v[0].p = cadd(stk[lv].p, v[0].p);
+            v[0].d = cadd(stk[lv].d, v[0].d);
+          } else {
+            stk[lv] = v[0];
+            done = true;
+          }
+        }
+    }
+    double2 zs[kLgLevels], z[1];
+#pragma unroll 1
+    for (int blk = 0; blk < NB; ++blk) {
+      tree_z_m<32, 1, true>(F + 3 * NP + blk * 32, 0, 1, bz, z);
+      bool done = false;
+#pragma unroll
+      for (int lv = 0; lv < kLgLevels; ++lv)
+        if (!done) {
+          if ((blk >> lv) & 1) {
+            z[0] = cadd(zs[lv], z[0]);
+          } else {
+            zs[lv] = z[0];
+            done = true;
+          }
+        }
+    }
+    if (has) {
+      PhiDiv pd = v[0];
+      double2 zz = z[0];
+      if (realify && m == 0) pd.p.y = zz.y = pd.d.y = 0.0;
+      const size_t o = (size_t)r * 3 * ncoef + idx;
+      double2 val[3] = {pd.p, zz, pd.d};
+      if (ep.base)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          val[c] = make_double2(e[c].x + val[c].x * ep.scale, e[c].y + val[c].y * ep.scale);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[o + (size_t)c * ncoef] = val[c];
+    }
+  }
 }
 
 // =====================================================================
@@ -1072,14 +1299,23 @@ struct LgGeom {
   int np, lpm, ppl, leaf, log2_ppl, log2_lpm;
 };
 
+// pole counts served by rexi_lg_warp_kernel (SWX_LG_WARP=0: the lane-group
+// kernels, for A/B measurements)
+static bool lg_warp_form(int np) {
+  static const int env = getenv("SWX_LG_WARP") ? atoi(getenv("SWX_LG_WARP")) : 0;
+  return env && (np == 128 || np == 256 || np == 512);
+}
+
 static int lg_geom(int P, LgGeom &g) {
   g.np = next_pow2(P);
   // lanes per mode / leaf subtree (tuning overrides: SWX_LG_LPM, SWX_LG_LEAF)
   static const int env_lpm = getenv("SWX_LG_LPM") ? atoi(getenv("SWX_LG_LPM")) : 8;
   static const int env_leaf = getenv("SWX_LG_LEAF") ? atoi(getenv("SWX_LG_LEAF")) : 8;
   g.lpm = std::min(env_lpm, g.np);
+  if (lg_warp_form(g.np)) g.lpm = 1;  // rexi_lg_warp_kernel: natural pole order
   g.ppl = g.np / g.lpm;
   g.leaf = std::min(g.ppl, env_leaf);
+  if (g.lpm == 1 && lg_warp_form(g.np)) g.leaf = 32;  // 32-pole blocks, <= 16 of them
   if (g.ppl / g.leaf > (1 << kLgLevels))
     return fail(SWX_ERR_CONFIG, "lg tree deeper than the register stack");
   g.log2_ppl = g.log2_lpm = 0;
@@ -1130,25 +1366,67 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
   }
   // static geometries of the common pole counts (128 / 256 / 512 poles, 8 lanes per mode)
   static const int env_mpl = getenv("SWX_LG_MPL") ? atoi(getenv("SWX_LG_MPL")) : 2;
+  if (g.lpm == 1 && lg_warp_form(g.np)) {
+    int n_items = 0;
+    const int4 *items = lg_schedule(s, 32, &n_items);
+    if (!items) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
+    auto k = g.np == 128 ? rexi_lg_warp_kernel<NRHS, 128>
+             : g.np == 256 ? rexi_lg_warp_kernel<NRHS, 256>
+                           : rexi_lg_warp_kernel<NRHS, 512>;
+    const size_t fsm = (size_t)NRHS * 4 * g.np * sizeof(double2);
+    static bool attr[2][3] = {{false, false, false}, {false, false, false}};
+    const int ai = g.np == 128 ? 0 : g.np == 256 ? 1 : 2;
+    if (fsm > 48 * 1024 && !attr[NRHS - 1][ai]) {
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+      attr[NRHS - 1][ai] = true;
+    }
+    SWX_CUDA_TRY(launch_pdl(k, dim3(n_items), dim3(32), fsm, st, rhs, fac, s->trunc, s->ncoef,
+                            items, realify, ep, fac_ready, out));
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
+  // SWX_LG_PAIR=0: per-pole leaves (every term rounded before the tree)
+  static const int env_pair = getenv("SWX_LG_PAIR") ? atoi(getenv("SWX_LG_PAIR")) : 1;
   if (g.lpm == 8 && g.ppl == 32 && env_mpl == 2) {
-    auto k = rexi_lg_mm_kernel<NRHS, 256, 8, 2>;
-    static int per_sm[3] = {0, 0, 0};
-    if (!per_sm[NRHS]) {
+    auto k = env_pair ? rexi_lg_mm_kernel<NRHS, 256, 8, 2, true>
+                      : rexi_lg_mm_kernel<NRHS, 256, 8, 2, false>;
+    static int per_sm[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    if (!per_sm[env_pair][NRHS]) {
       if (smem > 48 * 1024)
         SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int b = 0;
       SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, 128, smem));
-      per_sm[NRHS] = std::max(b, 1);
+      per_sm[env_pair][NRHS] = std::max(b, 1);
     }
-    // one pass (32 modes) per item, items largest first, persistent CTAs
+    // SWX_LG_PERSIST=2: persistent CTAs with double-buffered factor staging
     static const int env_pers = getenv("SWX_LG_PERSIST") ? atoi(getenv("SWX_LG_PERSIST")) : 0;
+    if (env_pers == 2 && env_pair) {
+      auto kp = rexi_lg_pers_kernel<NRHS, 256, 8, 2>;
+      static int pp[3] = {0, 0, 0};
+      const size_t smem2 = 2 * smem;
+      if (!pp[NRHS]) {
+        if (smem2 > 48 * 1024)
+          SWX_CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        int b = 0;
+        SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kp, 128, smem2));
+        pp[NRHS] = std::max(b, 1);
+      }
+      int n_items = 0;
+      const int4 *items = lg_schedule(s, -32, &n_items);
+      if (!items) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
+      const int grid = std::min(n_items, sm_count() * pp[NRHS]);
+      SWX_CUDA_TRY(launch_pdl(kp, dim3(grid), dim3(128), smem2, st, rhs, fac, s->trunc, s->ncoef,
+                              items, n_items, realify, ep, fac_ready, out));
+      SWX_LAUNCH_CHECK();
+      return SWX_OK;
+    }
     int n_items = n_cta;
     const int4 *items = sched;
     int grid = n_cta;
     if (env_pers) {
       items = lg_schedule(s, -32, &n_items);
       if (!items) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
-      grid = std::min(n_items, sm_count() * per_sm[NRHS]);
+      grid = std::min(n_items, sm_count() * per_sm[env_pair][NRHS]);
     }
     SWX_CUDA_TRY(launch_pdl(k, dim3(grid), dim3(128), smem, st, rhs, fac, s->trunc, s->ncoef,
                             items, n_items, realify, ep, fac_ready, out));
