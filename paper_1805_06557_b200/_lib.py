@@ -14,7 +14,8 @@ import threading
 from .errors import ConfigurationError, DataError, SolverError, SwerexiError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libswx.so")
+# SWX_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("SWX_LIB") or os.path.join(HERE, "libswx.so")
 
 SWX_OK, SWX_ERR_CONFIG, SWX_ERR_SOLVER, SWX_ERR_DATA, SWX_ERR_CUDA = range(5)
 SWX_GROUP_LG, SWX_GROUP_L = 0, 1

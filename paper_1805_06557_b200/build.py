@@ -45,6 +45,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
            "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-Xptxas", "-warn-spills",
            *[os.path.join(CSRC, s) for s in SOURCES],
            *(["-DSWX_TRACE"] if trace else []),
+           *[f"-D{d}" for d in os.environ.get("SWX_DEFINES", "").split()],
            "-o", LIB + ".tmp",
            f"-L{cuda}/lib64", "-lcufft", "-lgomp", f"-Xlinker", f"-rpath={cuda}/lib64"]
     if verbose:

@@ -644,7 +644,10 @@ __global__ void __launch_bounds__(32) rexi_lg_warp_kernel(
 // transpose in tree order every 8 chain elements.
 // =====================================================================
 constexpr int kLWarps = 4;  // warps per CTA
-constexpr int kFlush = 8;   // chain elements per reduction flush
+#ifndef SWX_LSEG
+#define SWX_LSEG 4
+#endif
+constexpr int kFlush = 2 * SWX_LSEG;   // chain elements per reduction flush
 
 // Per chain element, forward Thomas step of chain c at k (l = m + k):
 //   den = diag_k - sub_k c'_{k-1};  c'_k = sup_k / den;
@@ -661,7 +664,8 @@ constexpr int kFlush = 8;   // chain elements per reduction flush
 // so the two chains share every coefficient and right-hand side of the
 // position, give two independent dependency chains (ILP), and together
 // produce (vort_l, div_l, phi'_l).
-constexpr int kLSeg = 4;  // positions per segment (x 2 chains = kFlush rows)
+constexpr int kLSeg = SWX_LSEG;  // positions per segment (x 2 chains = kFlush rows)
+static_assert(kLSeg == 4 || kLSeg == 8, "segment length");
 
 template <int NRHS>
 struct LPos {
@@ -727,24 +731,131 @@ __device__ __forceinline__ void l_fwd(const LPos<NRHS> &e, bool isz, double2 a, 
   }
 }
 
+// the same step from the cached pivot inverse inv = 1/den (bitwise equal:
+// l_fwd computes den, inv = crecip(den) and then exactly these operations);
+// the chain's c' is not needed for y
 template <int NRHS>
+__device__ __forceinline__ void l_fwd_c(const LPos<NRHS> &e, bool isz, double2 ia, double2 inv,
+                                        double2 (&y)[NRHS]) {
+  const double sub = (isz ? -1.0 : 1.0) * e.L;
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) {
+    double2 q;
+    if (isz) {
+      q = e.bz[r];
+    } else {
+      const double2 t = make_double2(e.h * ia.x, e.h * ia.y);
+      q = csub(e.bd[r], cmul(t, e.bp[r]));
+    }
+    q = make_double2(fma(-sub, y[r].x, q.x), fma(-sub, y[r].y, q.y));
+    y[r] = cmul(q, inv);
+  }
+}
+
+// mbarrier / bulk-copy helpers of the cached chain kernel
+__device__ __forceinline__ unsigned lc_smem(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void lc_bar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(lc_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void lc_bar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LC_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LC_WAIT_%=;\n}\n" ::"r"(lc_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void lc_bulk(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(lc_smem(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          lc_smem(dst)),
+      "l"(src), "r"(bytes), "r"(lc_smem(bar))
+      : "memory");
+}
+constexpr int kLRing = 2;               // cached pivots: segments in flight per warp
+constexpr int kLSegW = kLSeg * 64;      // double2 per segment block (positions x chains x lanes)
+
+// cache index of (global pole gp, packed slot s, chain c)
+__device__ __forceinline__ size_t linv_at(int gp, int ncoef, int s, int c) {
+  return ((size_t)(gp >> 5) * ncoef + s) * 64 + c * 32 + (gp & 31);
+}
+
+// fills the pivot cache: one thread per (pole, m, chain), the forward sweep
+// of l_fwd (poles >= P use alpha = 1 like the pole-sum kernel's idle lanes)
+__global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_pad, int trunc,
+                               int ncoef, const double *__restrict__ lconst,
+                               const double *__restrict__ chain, double2 *__restrict__ linv) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)P_pad * (trunc + 1) * 2;
+  if (t >= total) return;
+  const int lane = (int)(t & 31);
+  const long long w = t >> 5;  // (pole block, m, chain)
+  const int c = (int)(w & 1);
+  const int m = (int)((w >> 1) % (trunc + 1));
+  const int pb = (int)((w >> 1) / (trunc + 1));
+  const int gp = pb * 32 + lane;
+  const double2 a = gp < P ? alpha[gp] : make_double2(1.0, 0.0);
+  const double2 ia = crecip(a);
+  const double *gl = lconst + (trunc + 1);
+  const int off = col_offset(trunc, m);
+  double2 cp = make_double2(0.0, 0.0);
+  for (int k = 0; k < trunc + 1 - m; ++k) {
+    const int s = off + k;
+    const bool isz = ((k + c) & 1) == 0;
+    const double sg = isz ? -1.0 : 1.0;
+    const double sub = sg * chain[s], sup = sg * chain[ncoef + s];
+    double2 diag = make_double2(a.x, a.y + chain[2 * ncoef + s]);
+    if (!isz) {
+      diag.x = fma(gl[m + k], ia.x, diag.x);
+      diag.y = fma(gl[m + k], ia.y, diag.y);
+    }
+    const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
+    const double2 inv = crecip(den);
+    cp = cscale(sup, inv);
+    linv[linv_at(gp, ncoef, s, c)] = inv;
+  }
+}
+
+template <int NRHS, bool CACHED = false>
 __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
     const double2 *__restrict__ beta, int beta_stride, int pole0, int P,
     int n_blocks, int trunc, int ncoef, double dt, double phibar,
     const double *__restrict__ lconst, const double *__restrict__ chain,
-    double2 *__restrict__ scratch, double2 *__restrict__ part) {
+    double2 *__restrict__ scratch, double2 *__restrict__ part,
+    const double2 *__restrict__ linv) {
   // reduction buffer: [warp][row][r][comp][32] (dynamic, NRHS * 32 KB)
   extern __shared__ double2 red_raw[];
   auto red = reinterpret_cast<double2 (*)[kFlush][NRHS][2][32]>(red_raw);
   __shared__ LPos<NRHS> pos_s[kLWarps][kLSeg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // cached pivots: per-warp ring of kLRing segment blocks filled by bulk copies
+  double2 *ring = red_raw + (size_t)kLWarps * kFlush * NRHS * 2 * 32 + (size_t)warp * kLRing * kLSegW;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(red_raw + (size_t)kLWarps * kFlush * NRHS * 2 * 32 +
+                                                (size_t)kLWarps * kLRing * kLSegW) +
+                   warp * kLRing;
+  int seq = 0, cons = 0;  // segment blocks issued / consumed by this warp
+  if constexpr (CACHED) {
+    if (lane == 0)
+      for (int j = 0; j < kLRing; ++j) lc_bar_init(bars + j);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+  }
   const int gwarp = blockIdx.x * kLWarps + warp;
   const int total_warps = gridDim.x * kLWarps;
   const int n_items = (trunc + 1) * n_blocks;
   const double dtpb = dt * phibar;
   const int max_seg = (trunc + 1 + kLSeg - 1) / kLSeg;
-  constexpr int CKW = 2 * (1 + NRHS);  // checkpoint words per lane: (cp, y) x 2 chains
+  // checkpoint words per lane: (cp, y) x 2 chains; cached pivots: y only
+  constexpr int CKW = CACHED ? 2 * NRHS : 2 * (1 + NRHS);
+  constexpr int CY = CACHED ? 0 : 1;  // offset of y in a chain's checkpoint words
   double2 *slot = scratch + (size_t)gwarp * max_seg * 32 * CKW;
   LPos<NRHS> *sp = pos_s[warp];
 
@@ -767,6 +878,39 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     const int off = col_offset(trunc, m);
     const int nseg = (nl + kLSeg - 1) / kLSeg;
 
+    // cached pivots: segment blocks of this warp's 32 poles (contiguous in
+    // the cache: pole0 is a multiple of 32) in the order pass 1 (0..nseg-1)
+    // then pass 2 (nseg-1..0), kLRing blocks in flight
+    const double2 *lsrc = CACHED ? linv + ((size_t)((pole0 + pb * 32) >> 5) * ncoef + off) * 64
+                                 : nullptr;
+    auto issue = [&](int i) {  // flat index i of the 2 * nseg block loads
+      if constexpr (CACHED) {
+        if (i < 2 * nseg) {
+          const int sg = i < nseg ? i : 2 * nseg - 1 - i;
+          const int cnt = min(kLSeg, nl - sg * kLSeg);
+          if (lane == 0)
+            lc_bulk(ring + (seq % kLRing) * kLSegW, lsrc + (size_t)sg * kLSegW,
+                    (unsigned)(cnt * 64 * sizeof(double2)), bars + seq % kLRing);
+          ++seq;
+        }
+      }
+    };
+    auto acquire = [&]() -> const double2 * {  // next block in flat order
+      if constexpr (CACHED) {
+        lc_bar_wait(bars + cons % kLRing, (cons / kLRing) & 1);
+        return ring + (cons % kLRing) * kLSegW;
+      }
+      return nullptr;
+    };
+    auto release = [&](int i) {  // block i consumed: its slot takes block i + kLRing
+      if constexpr (CACHED) {
+        __syncwarp();
+        ++cons;
+        issue(i + kLRing);
+      }
+    };
+    if constexpr (CACHED)
+      for (int i = 0; i < kLRing; ++i) issue(i);
     // ---- pass 1: forward sweep of both chains, checkpoint every segment
     double2 cp[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     double2 y[2][NRHS];
@@ -780,9 +924,9 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       double2 *dst = slot + ((size_t)sgi * 32 + lane) * CKW;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        dst[c * (1 + NRHS)] = cp[c];
+        if constexpr (!CACHED) dst[c * (CY + NRHS)] = cp[c];
 #pragma unroll
-        for (int r = 0; r < NRHS; ++r) dst[c * (1 + NRHS) + 1 + r] = y[c][r];
+        for (int r = 0; r < NRHS; ++r) dst[c * (CY + NRHS) + CY + r] = y[c][r];
       }
       const int k0 = sgi * kLSeg;
       const int n = min(kLSeg, nl - k0);
@@ -790,14 +934,21 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       if (sgi + 1 < nseg)  // next segment's loads fly during this segment's sweep
         l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 + kLSeg,
                       min(kLSeg, nl - k0 - kLSeg), lane, nxt);
+      const double2 *iv = acquire();
 #pragma unroll
       for (int e = 0; e < kLSeg; ++e) {
         if (e < n) {
           const int k = k0 + e;
-          l_fwd<NRHS>(sp[e], (k & 1) == 0, a, ia, cp[0], y[0]);
-          l_fwd<NRHS>(sp[e], (k & 1) == 1, a, ia, cp[1], y[1]);
+          if constexpr (CACHED) {
+            l_fwd_c<NRHS>(sp[e], (k & 1) == 0, ia, iv[e * 64 + lane], y[0]);
+            l_fwd_c<NRHS>(sp[e], (k & 1) == 1, ia, iv[e * 64 + 32 + lane], y[1]);
+          } else {
+            l_fwd<NRHS>(sp[e], (k & 1) == 0, a, ia, cp[0], y[0]);
+            l_fwd<NRHS>(sp[e], (k & 1) == 1, a, ia, cp[1], y[1]);
+          }
         }
       }
+      release(sgi);
     }
     // ---- pass 2: segments backwards: recompute (c', y) in registers, back-substitute
     double2 xn[2][NRHS];
@@ -810,9 +961,9 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       const double2 *src = slot + ((size_t)sgi * 32 + lane) * CKW;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        ck_cp[c] = src[c * (1 + NRHS)];
+        if constexpr (!CACHED) ck_cp[c] = src[c * (CY + NRHS)];
 #pragma unroll
-        for (int r = 0; r < NRHS; ++r) ck_y[c][r] = src[c * (1 + NRHS) + 1 + r];
+        for (int r = 0; r < NRHS; ++r) ck_y[c][r] = src[c * (CY + NRHS) + CY + r];
       }
     };
     load_ck(nseg - 1);
@@ -823,7 +974,7 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       const int n = min(kLSeg, nl - k0);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        cp[c] = ck_cp[c];
+        if constexpr (!CACHED) cp[c] = ck_cp[c];
 #pragma unroll
         for (int r = 0; r < NRHS; ++r) y[c][r] = ck_y[c][r];
       }
@@ -832,6 +983,7 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
         load_ck(sgi - 1);
         l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 - kLSeg, kLSeg, lane, nxt);
       }
+      const double2 *iv = acquire();
       double2 cps[2][kLSeg], ys[2][NRHS][kLSeg];
 #pragma unroll
       for (int e = 0; e < kLSeg; ++e) {
@@ -839,13 +991,21 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
           const int k = k0 + e;
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            l_fwd<NRHS>(sp[e], ((k + c) & 1) == 0, a, ia, cp[c], y[c]);
+            if constexpr (CACHED) {
+              const bool isz = ((k + c) & 1) == 0;
+              const double2 inv = iv[e * 64 + c * 32 + lane];
+              l_fwd_c<NRHS>(sp[e], isz, ia, inv, y[c]);
+              cp[c] = cscale((isz ? -1.0 : 1.0) * sp[e].U, inv);
+            } else {
+              l_fwd<NRHS>(sp[e], ((k + c) & 1) == 0, a, ia, cp[c], y[c]);
+            }
             cps[c][e] = cp[c];
 #pragma unroll
             for (int r = 0; r < NRHS; ++r) ys[c][r][e] = y[c][r];
           }
         }
       }
+      release(2 * nseg - 1 - sgi);  // pivots of this segment are in cps now
       // back substitution; (position e, chain c) -> reduction row (n-1-e)*2 + c
 #pragma unroll
       for (int e = kLSeg - 1; e >= 0; --e) {
@@ -871,9 +1031,11 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
         }
       }
       __syncwarp();
-      // lane j reduces row ee = j>>2 over the 8 poles 8q..8q+7, q = j&3
+      // lane j reduces row ee = j / LPR over the PR poles PR*q .. PR*q+PR-1,
+      // q = j % LPR (kFlush rows, LPR lanes per row), then LPR-lane butterfly
+      constexpr int LPR = 32 / kFlush, PR = 32 / LPR;
       const int nrows = 2 * n;
-      const int ee = lane >> 2, q = lane & 3;
+      const int ee = lane / LPR, q = lane % LPR;
       const int eidx = ee < nrows ? ee : 0;
       const int epos = n - 1 - (eidx >> 1), ec = eidx & 1;
       const int kk = k0 + epos;
@@ -882,14 +1044,16 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       for (int r = 0; r < NRHS; ++r) {
 #pragma unroll
         for (int comp = 0; comp < 2; ++comp) {
-          double2 v[8];
+          double2 v[PR];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = red[warp][eidx][r][comp][(8 * q + i) ^ eidx];
-          const double2 s01 = cadd(v[0], v[1]), s23 = cadd(v[2], v[3]);
-          const double2 s45 = cadd(v[4], v[5]), s67 = cadd(v[6], v[7]);
-          double2 acc = cadd(cadd(s01, s23), cadd(s45, s67));
-          acc = cadd(acc, shfl_xor2(acc, 1));
-          acc = cadd(acc, shfl_xor2(acc, 2));
+          for (int i = 0; i < PR; ++i) v[i] = red[warp][eidx][r][comp][(PR * q + i) ^ eidx];
+#pragma unroll
+          for (int w = 1; w < PR; w <<= 1)  // pairwise tree over the lane's poles
+#pragma unroll
+            for (int i = 0; i < PR; i += 2 * w) v[i] = cadd(v[i], v[i + w]);
+          double2 acc = v[0];
+#pragma unroll
+          for (int o = 1; o < LPR; o <<= 1) acc = cadd(acc, shfl_xor2(acc, o));
           if (q == 0 && ee < nrows && (comp == 0 || !eisz)) {
             const int field = comp == 1 ? 0 : (eisz ? 1 : 2);
             part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + kk] = acc;
@@ -1137,6 +1301,7 @@ extern "C" int swx_solver_destroy(swx_solver s) {
   cudaFree(s->d_lconst);
   cudaFree(s->d_chain);
   cudaFree(s->d_alpha);
+  cudaFree(s->d_linv);
   for (auto &kv : s->lg_sched) cudaFree(kv.second.first);
   delete[] s->h_norm;
   delete[] s->h_alpha;
@@ -1221,6 +1386,29 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
                h_alphas[p].re, h_alphas[p].im);
       return fail(SWX_ERR_SOLVER, buf);
     }
+    // pivot cache (32 B per pole x coefficient), built when it fits in half
+    // of the free device memory; SWX_L_CACHE=0 keeps the recomputing kernel
+    cudaFree(s->d_linv);
+    s->d_linv = nullptr;
+    s->linv_bytes = 0;
+    const char *ev = getenv("SWX_L_CACHE");
+    if (!ev || atoi(ev) != 0) {
+      const int p_pad = ((n_poles + 31) / 32 + 1) * 32;  // + one block for idle lanes
+      const size_t bytes = (size_t)p_pad * s->ncoef * 2 * sizeof(double2);
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && bytes <= fr / 2 &&
+          cudaMalloc(&s->d_linv, bytes) == cudaSuccess) {
+        s->linv_bytes = bytes;
+        const long long threads = (long long)p_pad * n * 2;
+        l_cache_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+            s->d_alpha, n_poles, p_pad, s->trunc, s->ncoef, s->d_lconst, s->d_chain, s->d_linv);
+        SWX_LAUNCH_CHECK();
+        SWX_CUDA_TRY(cudaStreamSynchronize(st));
+      } else {
+        cudaGetLastError();  // a failed optional allocation is not an error
+        s->d_linv = nullptr;
+      }
+    }
   } else {
     SWX_CUDA_TRY(cudaStreamSynchronize(st));
   }
@@ -1230,17 +1418,23 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
 // ---- launch geometry helpers
 static constexpr int kLgMaxP = 512;  // poles per lg launch (smem = NRHS*64*P bytes)
 
-static size_t l_smem_bytes(int nrhs) {
-  return (size_t)kLWarps * kFlush * nrhs * 2 * 32 * sizeof(double2);
+static size_t l_smem_bytes(int nrhs, bool cached = false) {
+  return (size_t)kLWarps * kFlush * nrhs * 2 * 32 * sizeof(double2) +
+         (cached ? (size_t)kLWarps * kLRing * (kLSegW * sizeof(double2) + sizeof(uint64_t)) : 0);
 }
 
 static int l_grid_warps(swx_solver s, int n_items) {
-  if (!s->l_blocks_per_sm) {
+  static int per_sm[2] = {0, 0};  // resident CTAs of the recomputing / cached kernel
+  const int ci = s->d_linv ? 1 : 0;
+  if (!per_sm[ci]) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rexi_l_kernel<1>, kLWarps * 32,
-                                                  l_smem_bytes(1));
-    s->l_blocks_per_sm = std::max(1, b);
+    auto k = ci ? rexi_l_kernel<1, true> : rexi_l_kernel<1, false>;
+    const size_t sm = l_smem_bytes(1, ci);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kLWarps * 32, sm);
+    per_sm[ci] = std::max(1, b);
   }
+  s->l_blocks_per_sm = per_sm[ci];
   const int cap = sm_count() * s->l_blocks_per_sm * kLWarps;
   return std::min(cap, ((n_items + kLWarps - 1) / kLWarps) * kLWarps);
 }
@@ -1477,13 +1671,15 @@ static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
   double2 *scratch = (double2 *)ws;
   const size_t sbytes = l_scratch_bytes(s, NRHS, P);
   double2 *part = (double2 *)(ws + ((sbytes + 255) / 256) * 256);
-  const size_t smem = l_smem_bytes(NRHS);
+  // the cached kernel streams 32-pole blocks of the pivot cache: aligned blocks only
+  const bool cached = s->d_linv && pole0 % 32 == 0;
+  const size_t smem = l_smem_bytes(NRHS, cached);
+  auto k = cached ? rexi_l_kernel<NRHS, true> : rexi_l_kernel<NRHS, false>;
   if (smem > 48 * 1024)
-    SWX_CUDA_TRY(cudaFuncSetAttribute(rexi_l_kernel<NRHS>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  rexi_l_kernel<NRHS><<<warps / kLWarps, kLWarps * 32, smem, st>>>(
+    SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<warps / kLWarps, kLWarps * 32, smem, st>>>(
       rhs, s->d_alpha, betas, s->n_poles, pole0, P, nb, s->trunc, s->ncoef, s->dt,
-      s->phibar, s->d_lconst, s->d_chain, scratch, part);
+      s->phibar, s->d_lconst, s->d_chain, scratch, part, s->d_linv);
   SWX_LAUNCH_CHECK();
   const size_t stride = (size_t)NRHS * 3 * s->ncoef;
   tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, nb, s->ncoef,

@@ -91,6 +91,11 @@ struct swx_solver_s {
   std::map<std::tuple<int, int, int>, std::pair<int4 *, int>> lg_sched;
   // column shard of the lg pole sums (swx_solver_set_columns): [col_lo, col_hi)
   int col_lo = 0, col_hi = -1;
+  // l group: cached forward pivots 1/den per (pole, m, position, chain) of the
+  // warmed shift set (the analogue of the reference's per-(m, alpha) LU
+  // cache, solvers.py:168-194), layout [pole/32][slot][chain][pole%32]
+  double2 *d_linv = nullptr;
+  size_t linv_bytes = 0;
   int l_blocks_per_sm = 0;
 };
 
