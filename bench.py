@@ -208,6 +208,12 @@ def load_traffic():
     return {}
 
 
+def _l_cache_bytes(dr):
+    """Size of the warm-time pivot cache of an l solver (0: lg, or not built)."""
+    from paper_1805_06557_b200 import _lib
+    return int(_lib.load().swx_solver_cache_bytes(dr.solver._native(dr.alphas).h))
+
+
 def column_breakdown(torch, eng, ccomm, flush, reps=5):
     """Rank-local device times of the column-sharded step's pieces: the
     three tendency stages (each with its slab pack/unpack copies) and one
@@ -311,7 +317,11 @@ def main():
         ic = seeded_linear_state(w.trunc, 0)
         u = to_device(pack(ic))
         out = torch.empty_like(u)
-        dr = stepper._for_dt(w.dt)[2]
+        torch.cuda.synchronize()
+        t_warm = time.perf_counter()
+        dr = stepper._for_dt(w.dt)[2]   # warm: guards (+ the l pivot cache), untimed
+        torch.cuda.synchronize()
+        t_warm = time.perf_counter() - t_warm
         if comm is not None:
             dr.comm = comm
             dr.range = comm.pole_range(w.n_poles)
@@ -485,6 +495,35 @@ def main():
         roofline = {"kernel": dominant, "bound": "fp64", "achieved": None, "peak": peak64,
                     "unit": "TFLOP/s", "frac": None, "ms_per_launch": ms, "traffic": None}
 
+    # ---- cfg4: SH transform round trip of the seeded phi' field (SURVEY §8d:
+    # synthesis then analysis, 2 x (4 nlat ncoef + 2.5 nlon log2(nlon) nlat) flops)
+    sh_rt = None
+    if args.config == "cfg4":
+        from paper_1805_06557_b200.sphere import plan_for
+        plan = plan_for(par.cfg)
+        phi = u[0:1].contiguous()
+        grid = plan.synthesis_dev(phi)
+        back = plan.analysis_dev(grid)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tt = []
+        for _ in range(5):
+            flush.zero_()
+            e0.record()
+            plan.synthesis_dev(phi, grid)
+            plan.analysis_dev(grid, back)
+            e1.record()
+            e1.synchronize()
+            tt.append(e0.elapsed_time(e1))
+        import math
+        nlat_, nlon_ = par.cfg.nlat, par.cfg.nlon
+        fl = 2 * (4.0 * nlat_ * nc + 2.5 * nlon_ * math.log2(nlon_) * nlat_)
+        ms_rt = min(tt)
+        err = float((back - phi).abs().max() / phi.abs().max())
+        sh_rt = {"ms": ms_rt, "coeffs_per_s": nc / (ms_rt * 1e-3),
+                 "algorithmic_flops": fl, "tflops": fl / (ms_rt * 1e-3) / 1e12,
+                 "rel_linf_round_trip": err, "path": "on-the-fly Legendre recurrence (no table at T1279)"}
+
     # ---- end to end through the public API (host numpy in, host numpy out)
     e2e = None
     if not args.no_e2e and ccomm is not None:
@@ -570,8 +609,11 @@ def main():
                                     else f"poles sharded over {world} GPU(s)")
                                    if multi else "1 GPU"),
                    "l2": "flushed (256 MB write) before every timed step",
-                   "cuda_graph": bool(etd and not multi)},
+                   "cuda_graph": bool(etd and not multi),
+                   **({} if etd else {"warm_s": round(t_warm, 3),
+                                      "l_pivot_cache_bytes": _l_cache_bytes(dr)})},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        **({"sh_round_trip": sh_rt} if sh_rt else {}),
         "gpu_launches": per_step_launches * args.steps,
         "clocks": clocks, "kernel_breakdown_ms": breakdown,
         "wall_s_timed_region": wall,

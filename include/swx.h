@@ -227,6 +227,11 @@ int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx_shard *sh,
  * columns in d_out are left unspecified.  SWX_ERR_CONFIG for the Coriolis
  * group, whose ranks shard the poles instead (parallel.py:100-182).        */
 int swx_solver_set_columns(swx_solver s, int m_begin, int m_end);
+/* Bytes of the Coriolis group's warm-time pivot cache (1/den per pole, m,
+ * chain position and chain: the analogue of the reference's per-(m, alpha)
+ * LU cache, solvers.py:168-194); 0 when not built (lg group, SWX_L_CACHE=0,
+ * or more than half the free device memory).                               */
+size_t swx_solver_cache_bytes(swx_solver s);
 
 /* ---- host layout conversion (API edge) ------------------------------------
  * Dense (T+1)x(T+1) complex128 fields, C order (row l, column m) -- the

@@ -1889,3 +1889,5 @@ extern "C" int swx_solver_set_columns(swx_solver s, int m_begin, int m_end) {
   s->col_hi = m_end;
   return SWX_OK;
 }
+
+extern "C" size_t swx_solver_cache_bytes(swx_solver s) { return s ? s->linv_bytes : 0; }

@@ -1753,6 +1753,131 @@ __global__ void __launch_bounds__(kAT, 1) analysis_kernel(ShtView p, const doubl
 }
 
 // ---------------------------------------------------------------------
+// Plain analysis without the Legendre table (T > ~700), the transpose of the
+// synthesis walk: CTA = (column m, block of 256 latitude pairs), thread =
+// pair, walking the column's degrees with the reference recurrence
+// (sphere.py:86-101, bit-identical to the other walkers).  Per 16-degree
+// chunk a lane forms its 16 contributions P_l(x_i) A_par(i) (prepared rows:
+// quadrature weight, dlon and hemisphere fold applied, sphere.py:297-315)
+// and the warp sums them over its 32 pairs with a transposed butterfly
+// (16 values -> one per lane pair in 16 shuffle steps), the 8 warps combine
+// in shared memory in fixed order and the pair blocks through a partial
+// buffer reduced in fixed order by analysis_col_reduce -- deterministic,
+// FP64 FMA work only (no 8-column DMMA padding for one or two fields).
+// ---------------------------------------------------------------------
+constexpr int kACT = 256;  // threads per CTA
+#ifndef SWX_ACOL_PPT
+#define SWX_ACOL_PPT 4
+#endif
+constexpr int kAPP = SWX_ACOL_PPT;  // latitude pairs per thread (CTA = 1024 pairs)
+
+#ifndef SWX_ACOL_MINB
+#define SWX_ACOL_MINB 2
+#endif
+template <int NF>
+__global__ void __launch_bounds__(kACT, NF == 1 ? SWX_ACOL_MINB : 1) analysis_col_kernel(ShtView p, const double *A, int f0,
+                                                            double2 *part, double2 *out) {
+  __shared__ double2 red[kACT / 32][16][NF];
+  const int m = blockIdx.x, pb = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int T = p.trunc, kmax = T + 1 - m;
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  // pairs pb * 1024 + q * 256 + tid, q < kAPP: their contributions are summed
+  // in the thread before the butterfly
+  double x[kAPP], p0[kAPP], p1[kAPP];
+  double2 ae[kAPP][NF], ao[kAPP][NF];
+#pragma unroll
+  for (int q = 0; q < kAPP; ++q) {
+    const int i = pb * kACT * kAPP + q * kACT + threadIdx.x;
+    x[q] = p0[q] = p1[q] = 0.0;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) ae[q][f] = ao[q][f] = make_double2(0.0, 0.0);
+    if (i < p.nh) {
+      x[q] = p.d_x[i];
+      const double seed = p.d_seed[(size_t)m * p.nh + i];
+      p0[q] = seed;
+      p1[q] = sqrt(2.0 * m + 3.0) * x[q] * seed;  // sphere.py:96-97
+      const double *base = A + (size_t)m * 2 * p.nhp * kAS + (size_t)i * kAS;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        ae[q][f] = make_double2(base[2 * (f0 + f)], base[2 * (f0 + f) + 1]);
+        ao[q][f] = make_double2(base[(size_t)p.nhp * kAS + 2 * (f0 + f)],
+                                base[(size_t)p.nhp * kAS + 2 * (f0 + f) + 1]);
+      }
+    }
+  }
+  const int d = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                ((lane >> 1) & 1);  // degree slot a lane pair ends with
+  const size_t nc = p.ncoef;
+  const int off = col_offset(T, m);
+  for (int k0 = 0; k0 < kmax; k0 += 16) {
+    double2 v[16][NF];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int k = k0 + e;
+      const double2 c2 = k + 2 <= kmax ? __ldg(reinterpret_cast<const double2 *>(rc + k + 2))
+                                       : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kAPP; ++q) {
+        const double pv = k < kmax ? p0[q] : 0.0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const double2 a = (e & 1) ? ao[q][f] : ae[q][f];  // parity of l - m (k0 even)
+          v[e][f] = q == 0 ? make_double2(pv * a.x, pv * a.y)
+                           : make_double2(fma(pv, a.x, v[e][f].x), fma(pv, a.y, v[e][f].y));
+        }
+        const double pn = fma(x[q], p1[q], -c2.x * p0[q]) * c2.y;
+        p0[q] = p1[q];
+        p1[q] = pn;
+      }
+    }
+    // transposed butterfly over the warp's 32 lanes
+#pragma unroll
+    for (int w = 8, o = 16; w >= 1; w >>= 1, o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int e = 0; e < w; ++e)
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const double2 snd = up ? v[e][f] : v[e + w][f];
+          const double2 kp = up ? v[e + w][f] : v[e][f];
+          v[e][f] = cadd(kp, shfl_xor2(snd, o));
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) v[0][f] = cadd(v[0][f], shfl_xor2(v[0][f], 1));
+    __syncthreads();  // previous chunk's readers are done with red
+    if ((lane & 1) == 0)
+#pragma unroll
+      for (int f = 0; f < NF; ++f) red[warp][d][f] = v[0][f];
+    __syncthreads();
+    if (threadIdx.x < 16 * NF) {
+      const int e = threadIdx.x % 16, f = threadIdx.x / 16;
+      if (k0 + e < kmax) {
+        double2 acc = red[0][e][f];
+#pragma unroll
+        for (int q = 1; q < kACT / 32; ++q) acc = cadd(acc, red[q][e][f]);
+        if (out)  // one pair block: final value
+          out[(size_t)f * nc + off + k0 + e] = acc;
+        else
+          part[((size_t)pb * NF + f) * nc + off + k0 + e] = acc;
+      }
+    }
+  }
+}
+
+// out[f] = sum over pair blocks of part[pb][f] (ascending pb, fixed order)
+__global__ void analysis_col_reduce(const double2 *part, int npb, int nf, size_t nc,
+                                    double2 *out) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)nf * nc) return;
+  const size_t f = t / nc, s = t - f * nc;
+  double2 acc = part[(0 * nf + f) * nc + s];
+  for (int b = 1; b < npb; ++b) acc = cadd(acc, part[((size_t)b * nf + f) * nc + s]);
+  out[f * nc + s] = acc;
+}
+
+// ---------------------------------------------------------------------
 // Table path.  Pbar_l^m at the north node of every pair is precomputed at
 // plan time with the same recurrence (bit-identical to the walkers); the
 // transforms then stream it instead of re-running the recurrence, and
@@ -2969,6 +3094,32 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
     dim3 g((p->nhp + 127) / 128, p->nm);
     prep_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, nf, w.A);
     SWX_LAUNCH_CHECK();
+    // column walk (SWX_ANA_COL=0: the warp-specialised DMMA kernel); the
+    // pair-block partials live in the synthesis rows area of the workspace
+    static const int st_col = env_int("SWX_ANA_COL", 1);
+    const int npb = (p->nh + kACT * kAPP - 1) / (kACT * kAPP);
+    const size_t pbytes = (size_t)npb * 2 * p->ncoef * sizeof(double2);
+    const size_t c2r_bytes = 5 * (size_t)p->nlat * std::max(p->nfreq, p->nfreq_t) * sizeof(double2);
+    if (st_col && pbytes <= c2r_bytes) {
+      for (int fa = 0; fa < nf; fa += 2) {
+        const int nb = std::min(2, nf - fa);
+        dim3 ga(p->nm, npb);
+        double2 *dst = out + (size_t)(f0 + fa) * p->ncoef;
+        double2 *fin = npb == 1 ? dst : nullptr;
+        if (nb == 2)
+          analysis_col_kernel<2><<<ga, kACT, 0, s>>>(static_cast<const ShtView &>(*p), w.A, fa, w.c2r, fin);
+        else
+          analysis_col_kernel<1><<<ga, kACT, 0, s>>>(static_cast<const ShtView &>(*p), w.A, fa, w.c2r, fin);
+        SWX_LAUNCH_CHECK();
+        if (npb > 1) {
+          const size_t n = (size_t)nb * p->ncoef;
+          analysis_col_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w.c2r, npb, nb,
+                                                                         p->ncoef, dst);
+          SWX_LAUNCH_CHECK();
+        }
+      }
+      continue;
+    }
     if ((rc = launch_analysis<1>(p, w.A, nullptr, nullptr, 0, out + (size_t)f0 * p->ncoef, nf, s)))
       return rc;
   }
