@@ -523,6 +523,25 @@ def main():
         sh_rt = {"ms": ms_rt, "coeffs_per_s": nc / (ms_rt * 1e-3),
                  "algorithmic_flops": fl, "tflops": fl / (ms_rt * 1e-3) / 1e12,
                  "rel_linf_round_trip": err, "path": "on-the-fly Legendre recurrence (no table at T1279)"}
+        if multi:  # the same round trip column/latitude-sharded over the ranks
+            from paper_1805_06557_b200.parallel import ShardedTransforms
+            cc = ColumnComm()
+            xs = ShardedTransforms(plan, ColumnShard(par.cfg, rank, world))
+            tt = []
+            for _ in range(5):
+                flush.zero_()
+                dist.barrier()
+                e0.record()
+                xs.synthesis(cc, phi, grid)
+                xs.analysis(cc, grid, back)
+                e1.record()
+                e1.synchronize()
+                tt.append(e0.elapsed_time(e1))
+            tm = torch.tensor([min(tt)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            sh_rt["sharded"] = {"ms": float(tm.item()), "ranks": world,
+                                "decomposition": "columns (Legendre) x latitude pairs (FFT), "
+                                                 "one all-to-all per transform"}
 
     # ---- end to end through the public API (host numpy in, host numpy out)
     e2e = None

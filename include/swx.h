@@ -222,6 +222,25 @@ int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx_shard *sh,
                            const swx_c128 *d_state, const swx_c128 *d_sub, swx_c128 *d_out,
                            const void *d_recv, void *d_send, void *d_workspace,
                            size_t ws_bytes, void *stream);
+/* Column-sharded plain transforms (the cfg4 T1279 round trip): synthesis
+ * stage 0 synthesises the own columns of n_fields (<= 4) packed fields for
+ * every latitude and packs the Fourier rows of every peer's latitude pairs;
+ * stage 1 unpacks the rows received and runs the longitude transforms of
+ * the own pairs' rows into d_grid ((n_fields, nlat, nlon); only the own
+ * rows -- south [a, b), north [nlat-b, nlat-a) of pairs [a, b) -- are
+ * written).  Analysis stage 0 transforms the own rows of d_grid and packs
+ * the Fourier coefficients of every peer's columns; stage 1 unpacks, folds
+ * and contracts the own columns into their slots of d_coeffs (table-free
+ * plans, T > ~700).  Exchange byte counts: swx_sht_transform_shard_counts
+ * (which = 0 synthesis, 1 analysis).                                       */
+size_t swx_sht_transform_shard_counts(swx_sht p, const swx_shard *sh, int which, int n_fields,
+                                      size_t *h_send, size_t *h_recv);
+int swx_sht_synthesis_shard(swx_sht p, int stage, int n_fields, const swx_shard *sh,
+                            const swx_c128 *d_coeffs, double *d_grid, const void *d_recv,
+                            void *d_send, void *d_workspace, size_t ws_bytes, void *stream);
+int swx_sht_analysis_shard(swx_sht p, int stage, int n_fields, const swx_shard *sh,
+                           const double *d_grid, swx_c128 *d_coeffs, const void *d_recv,
+                           void *d_send, void *d_workspace, size_t ws_bytes, void *stream);
 /* Restrict the pole sums of an lg solver to columns [m_begin, m_end) (the
  * column shard of the caller's rank; m_end < 0: all).  Slots of other
  * columns in d_out are left unspecified.  SWX_ERR_CONFIG for the Coriolis

@@ -1463,9 +1463,9 @@ __global__ void __launch_bounds__(SqCfg<R, R>::NT, 2) grid_sq1_kernel(ShtView p,
 }
 
 // plain analysis prep: nf (<= 4) grids already FFT'd into Q (pitch nfreq)
-__global__ void prep_plain_kernel(ShtView p, const double2 *Q, int nf, double *A) {
+__global__ void prep_plain_kernel(ShtView p, const double2 *Q, int nf, double *A, int m0 = 0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int m = blockIdx.y;
+  const int m = blockIdx.y + m0;
   if (i >= p.nhp) return;
   double2 ev[4], od[4];
 #pragma unroll
@@ -1776,9 +1776,10 @@ constexpr int kAPP = SWX_ACOL_PPT;  // latitude pairs per thread (CTA = 1024 pai
 #endif
 template <int NF>
 __global__ void __launch_bounds__(kACT, NF == 1 ? SWX_ACOL_MINB : 1) analysis_col_kernel(ShtView p, const double *A, int f0,
-                                                            double2 *part, double2 *out) {
+                                                            double2 *part, double2 *out,
+                                                            int m0 = 0) {
   __shared__ double2 red[kACT / 32][16][NF];
-  const int m = blockIdx.x, pb = blockIdx.y;
+  const int m = blockIdx.x + m0, pb = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int T = p.trunc, kmax = T + 1 - m;
   const double4 *rc = p.d_rc + rc_offset(T, m);
@@ -1867,11 +1868,12 @@ __global__ void __launch_bounds__(kACT, NF == 1 ? SWX_ACOL_MINB : 1) analysis_co
 }
 
 // out[f] = sum over pair blocks of part[pb][f] (ascending pb, fixed order)
-__global__ void analysis_col_reduce(const double2 *part, int npb, int nf, size_t nc,
-                                    double2 *out) {
+__global__ void analysis_col_reduce(const double2 *part, int npb, int nf, size_t nc, size_t s0,
+                                    size_t s1, double2 *out) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (size_t)nf * nc) return;
-  const size_t f = t / nc, s = t - f * nc;
+  const size_t ns = s1 - s0;  // slots [s0, s1): the launch's columns
+  if (t >= (size_t)nf * ns) return;
+  const size_t f = t / ns, s = s0 + (t - f * ns);
   double2 acc = part[(0 * nf + f) * nc + s];
   for (int b = 1; b < npb; ++b) acc = cadd(acc, part[((size_t)b * nf + f) * nc + s]);
   out[f * nc + s] = acc;
@@ -3069,6 +3071,42 @@ extern "C" int swx_sht_synthesis(swx_sht p, int n_fields, const swx_c128 *d_coef
   return c2r_exec(p, p->nlon, n_fields, w.c2r, d_grid, s);
 }
 
+// the pair-block partials of analysis_col_kernel live in the synthesis rows
+// area of the workspace
+static bool analysis_col_fits(swx_sht p) {
+  const int npb = (p->nh + kACT * kAPP - 1) / (kACT * kAPP);
+  const size_t pbytes = (size_t)npb * 2 * p->ncoef * sizeof(double2);
+  const size_t c2r_bytes = 5 * (size_t)p->nlat * std::max(p->nfreq, p->nfreq_t) * sizeof(double2);
+  return pbytes <= c2r_bytes;
+}
+
+// column-walk analysis of nf (<= 4) prepared fields, columns [m0, m1)
+static int analysis_cols(swx_sht p, ShtWs &w, int nf, int m0, int m1, double2 *out, cudaStream_t s) {
+  const int npb = (p->nh + kACT * kAPP - 1) / (kACT * kAPP);
+  if (m1 <= m0) return SWX_OK;
+  for (int fa = 0; fa < nf; fa += 2) {
+    const int nb = std::min(2, nf - fa);
+    dim3 ga(m1 - m0, npb);
+    double2 *dst = out + (size_t)fa * p->ncoef;
+    double2 *fin = npb == 1 ? dst : nullptr;
+    if (nb == 2)
+      analysis_col_kernel<2><<<ga, kACT, 0, s>>>(static_cast<const ShtView &>(*p), w.A, fa, w.c2r,
+                                                 fin, m0);
+    else
+      analysis_col_kernel<1><<<ga, kACT, 0, s>>>(static_cast<const ShtView &>(*p), w.A, fa, w.c2r,
+                                                 fin, m0);
+    SWX_LAUNCH_CHECK();
+    if (npb > 1) {
+      const size_t s0 = col_offset(p->trunc, m0), s1 = col_offset(p->trunc, m1);
+      const size_t n = (size_t)nb * (s1 - s0);
+      analysis_col_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w.c2r, npb, nb, p->ncoef,
+                                                                     s0, s1, dst);
+      SWX_LAUNCH_CHECK();
+    }
+  }
+  return SWX_OK;
+}
+
 extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
                                 swx_c128 *d_coeffs, void *d_ws, size_t ws_bytes, void *stream) {
   int rc = check_ws(p, d_ws, ws_bytes);
@@ -3094,30 +3132,10 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
     dim3 g((p->nhp + 127) / 128, p->nm);
     prep_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, nf, w.A);
     SWX_LAUNCH_CHECK();
-    // column walk (SWX_ANA_COL=0: the warp-specialised DMMA kernel); the
-    // pair-block partials live in the synthesis rows area of the workspace
+    // column walk (SWX_ANA_COL=0: the warp-specialised DMMA kernel)
     static const int st_col = env_int("SWX_ANA_COL", 1);
-    const int npb = (p->nh + kACT * kAPP - 1) / (kACT * kAPP);
-    const size_t pbytes = (size_t)npb * 2 * p->ncoef * sizeof(double2);
-    const size_t c2r_bytes = 5 * (size_t)p->nlat * std::max(p->nfreq, p->nfreq_t) * sizeof(double2);
-    if (st_col && pbytes <= c2r_bytes) {
-      for (int fa = 0; fa < nf; fa += 2) {
-        const int nb = std::min(2, nf - fa);
-        dim3 ga(p->nm, npb);
-        double2 *dst = out + (size_t)(f0 + fa) * p->ncoef;
-        double2 *fin = npb == 1 ? dst : nullptr;
-        if (nb == 2)
-          analysis_col_kernel<2><<<ga, kACT, 0, s>>>(static_cast<const ShtView &>(*p), w.A, fa, w.c2r, fin);
-        else
-          analysis_col_kernel<1><<<ga, kACT, 0, s>>>(static_cast<const ShtView &>(*p), w.A, fa, w.c2r, fin);
-        SWX_LAUNCH_CHECK();
-        if (npb > 1) {
-          const size_t n = (size_t)nb * p->ncoef;
-          analysis_col_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w.c2r, npb, nb,
-                                                                         p->ncoef, dst);
-          SWX_LAUNCH_CHECK();
-        }
-      }
+    if (st_col && analysis_col_fits(p)) {
+      if ((rc = analysis_cols(p, w, nf, 0, p->nm, out + (size_t)f0 * p->ncoef, s))) return rc;
       continue;
     }
     if ((rc = launch_analysis<1>(p, w.A, nullptr, nullptr, 0, out + (size_t)f0 * p->ncoef, nf, s)))
@@ -3702,4 +3720,206 @@ extern "C" int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx
     default:
       return fail(SWX_ERR_CONFIG, "shard stage must be 0, 1 or 2");
   }
+}
+
+// ---------------------------------------------------------------------
+// Column-sharded plain transforms (the T1279 round trip of SURVEY §8d/§8f
+// f1): synthesis of the own columns for every latitude, an all-to-all of
+// the Fourier rows to the owners of the latitude pairs, the longitude
+// transforms of the own pairs' rows; analysis in reverse.  The grid holds
+// the own pairs' rows (south rows [a, b), north rows [nlat-b, nlat-a) of the
+// pair range [a, b)); coefficients the own columns' slots.
+// ---------------------------------------------------------------------
+namespace {
+
+// latitude row blocks of a pair range (clipped to the real pairs)
+static int pair_row_blocks(swx_sht p, int a, int b, int2 *blk) {
+  a = std::min(a, p->nh);
+  b = std::min(b, p->nh);
+  if (b <= a) return 0;
+  blk[0] = make_int2(a, b - a);                   // south rows js = i
+  blk[1] = make_int2(p->nlat - b, b - a);         // north rows jn = nlat - 1 - i
+  return 2;
+}
+
+// exchange blocks of the Fourier rows ([f][nlat][nfreq] at base `rows`):
+// latitudes of `lat_rank`, columns of `col_rank`
+static void row_blocks(swx_sht p, const swx_shard *sh, int nf, int lat_rank, int col_rank,
+                       std::vector<Blk> &out) {
+  out.clear();
+  const int m0 = sh->m_bounds[col_rank], nm = sh->m_bounds[col_rank + 1] - m0;
+  int2 rb[2];
+  const int nb = pair_row_blocks(p, sh->p_bounds[lat_rank], sh->p_bounds[lat_rank + 1], rb);
+  if (nm <= 0) return;
+  for (int f = 0; f < nf; ++f)
+    for (int q = 0; q < nb; ++q)
+      out.push_back({(((size_t)f * p->nlat + rb[q].x) * p->nfreq + m0) * sizeof(double2),
+                     (size_t)p->nfreq * sizeof(double2), (size_t)nm * sizeof(double2),
+                     (size_t)rb[q].y});
+}
+
+// which = 0: synthesis (own columns -> peers' rows); 1: analysis (own rows ->
+// peers' columns).  dir 0 packs the sends, 1 unpacks the receives.
+static int rows_move(swx_sht p, const swx_shard *sh, int which, int nf, int dir, char *base,
+                     char *slab, cudaStream_t s) {
+  std::vector<Blk> blks;
+  size_t o = 0;
+  for (int peer = 0; peer < sh->nranks; ++peer) {
+    if (peer == sh->rank) continue;
+    const int me = sh->rank;
+    // synthesis: send (lat = peer, col = me), receive (lat = me, col = peer)
+    // analysis : send (lat = me, col = peer), receive (lat = peer, col = me)
+    if (which == 0)
+      row_blocks(p, sh, nf, dir == 0 ? peer : me, dir == 0 ? me : peer, blks);
+    else
+      row_blocks(p, sh, nf, dir == 0 ? me : peer, dir == 0 ? peer : me, blks);
+    for (const Blk &b : blks) {
+      if (dir == 0)
+        SWX_CUDA_TRY(cudaMemcpy2DAsync(slab + o, b.width, base + b.off, b.pitch, b.width, b.rows,
+                                       cudaMemcpyDeviceToDevice, s));
+      else
+        SWX_CUDA_TRY(cudaMemcpy2DAsync(base + b.off, b.pitch, slab + o, b.width, b.width, b.rows,
+                                       cudaMemcpyDeviceToDevice, s));
+      o += b.width * b.rows;
+    }
+  }
+  return SWX_OK;
+}
+
+static int check_plain_shard(swx_sht p, const swx_shard *sh, int nf) {
+  if (!p) return fail(SWX_ERR_CONFIG, "null SHT plan");
+  if (!sh || sh->nranks < 1 || sh->nranks > SWX_MAX_RANKS || sh->rank < 0 ||
+      sh->rank >= sh->nranks)
+    return fail(SWX_ERR_CONFIG, "bad shard");
+  const int K = sh->nranks;
+  if (sh->m_bounds[0] != 0 || sh->m_bounds[K] != p->trunc + 1 || sh->p_bounds[0] != 0 ||
+      sh->p_bounds[K] != p->nt16)
+    return fail(SWX_ERR_CONFIG, "shard bounds do not cover the plan");
+  if (nf < 1 || nf > 4) return fail(SWX_ERR_CONFIG, "1..4 fields per sharded transform");
+  return SWX_OK;
+}
+
+// cuFFT over the own latitude rows of nf fields (two row blocks per field)
+static int rows_fft(swx_sht p, const swx_shard *sh, int nf, bool inverse, double2 *spec,
+                    double *grid, cudaStream_t s) {
+  int2 rb[2];
+  const int nb = pair_row_blocks(p, sh->p_bounds[sh->rank], sh->p_bounds[sh->rank + 1], rb);
+  for (int q = 0; q < nb; ++q) {
+    cufftHandle h;
+    int rc = get_plan(p, inverse ? CUFFT_Z2D : CUFFT_D2Z, p->nlon, rb[q].y, &h);
+    if (rc) return rc;
+    cufftSetStream(h, s);
+    for (int f = 0; f < nf; ++f) {
+      const size_t r0 = (size_t)f * p->nlat + rb[q].x;
+      cufftResult r = inverse
+                          ? cufftExecZ2D(h, (cufftDoubleComplex *)(spec + r0 * p->nfreq), grid + r0 * p->nlon)
+                          : cufftExecD2Z(h, grid + r0 * p->nlon, (cufftDoubleComplex *)(spec + r0 * p->nfreq));
+      if (r != CUFFT_SUCCESS) return fail(SWX_ERR_CUDA, "cufftExec (sharded rows) failed");
+    }
+  }
+  return SWX_OK;
+}
+
+}  // namespace
+
+extern "C" size_t swx_sht_transform_shard_counts(swx_sht p, const swx_shard *sh, int which, int nf,
+                                                 size_t *h_send, size_t *h_recv) {
+  if (check_plain_shard(p, sh, nf) || (which != 0 && which != 1) || !h_send || !h_recv) return 0;
+  std::vector<Blk> blks;
+  size_t ts = 0, tr = 0;
+  const int me = sh->rank;
+  for (int peer = 0; peer < sh->nranks; ++peer) {
+    h_send[peer] = h_recv[peer] = 0;
+    if (peer == me) continue;
+    row_blocks(p, sh, nf, which == 0 ? peer : me, which == 0 ? me : peer, blks);
+    h_send[peer] = blocks_bytes(blks);
+    row_blocks(p, sh, nf, which == 0 ? me : peer, which == 0 ? peer : me, blks);
+    h_recv[peer] = blocks_bytes(blks);
+    ts += h_send[peer];
+    tr += h_recv[peer];
+  }
+  return std::max<size_t>(std::max(ts, tr), 1);
+}
+
+extern "C" int swx_sht_synthesis_shard(swx_sht p, int stage, int n_fields, const swx_shard *sh,
+                                       const swx_c128 *d_coeffs, double *d_grid,
+                                       const void *d_recv, void *d_send, void *d_ws,
+                                       size_t ws_bytes, void *stream) {
+  int rc = check_ws(p, d_ws, ws_bytes);
+  if (rc) return rc;
+  if ((rc = check_plain_shard(p, sh, n_fields))) return rc;
+  const bool multi = sh->nranks > 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  ShtWs w = carve(p, d_ws);
+  const int r = sh->rank, m0 = sh->m_bounds[r], m1 = sh->m_bounds[r + 1];
+  if (stage == 0) {
+    if (!d_coeffs) return fail(SWX_ERR_CONFIG, "null coefficients");
+    if (multi && !d_send) return fail(SWX_ERR_CONFIG, "null send slab");
+    if ((rc = zero_pad(p, w.c2r, n_fields, p->nfreq, s))) return rc;
+    if (m1 > m0) {
+      SynthArgs a;
+      a.coef = (const double2 *)d_coeffs;
+      a.c2r = w.c2r;
+      a.lc = nullptr;
+      a.want_lc = 0;
+      a.nfreq = p->nfreq;
+      a.m0 = m0;
+      int nt;
+      dim3 g = synth_grid(p, n_fields, &nt);
+      g.x = m1 - m0;
+      if ((rc = launch_synth<1>(p, g, nt, a, s))) return rc;
+    }
+    return multi ? rows_move(p, sh, 0, n_fields, 0, (char *)w.c2r, (char *)d_send, s) : SWX_OK;
+  }
+  if (stage == 1) {
+    if (!d_grid) return fail(SWX_ERR_CONFIG, "null grid");
+    if (multi && !d_recv) return fail(SWX_ERR_CONFIG, "null receive slab");
+    if (multi && (rc = rows_move(p, sh, 0, n_fields, 1, (char *)w.c2r, (char *)d_recv, s)))
+      return rc;
+    return rows_fft(p, sh, n_fields, true, w.c2r, d_grid, s);
+  }
+  return fail(SWX_ERR_CONFIG, "sharded synthesis stage must be 0 or 1");
+}
+
+extern "C" int swx_sht_analysis_shard(swx_sht p, int stage, int n_fields, const swx_shard *sh,
+                                      const double *d_grid, swx_c128 *d_coeffs,
+                                      const void *d_recv, void *d_send, void *d_ws,
+                                      size_t ws_bytes, void *stream) {
+  int rc = check_ws(p, d_ws, ws_bytes);
+  if (rc) return rc;
+  if ((rc = check_plain_shard(p, sh, n_fields))) return rc;
+  if (p->use_tab || !analysis_col_fits(p))
+    return fail(SWX_ERR_CONFIG, "sharded analysis is the table-free path (T > ~700)");
+  const bool multi = sh->nranks > 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  ShtWs w = carve(p, d_ws);
+  const int r = sh->rank, m0 = sh->m_bounds[r], m1 = sh->m_bounds[r + 1];
+  if (stage == 0) {
+    if (!d_grid) return fail(SWX_ERR_CONFIG, "null grid");
+    if (multi && !d_send) return fail(SWX_ERR_CONFIG, "null send slab");
+    // own rows into the workspace grid (the caller's grid is never touched)
+    int2 rb[2];
+    const int nb = pair_row_blocks(p, sh->p_bounds[r], sh->p_bounds[r + 1], rb);
+    for (int f = 0; f < n_fields; ++f)
+      for (int q = 0; q < nb; ++q) {
+        const size_t r0 = (size_t)f * p->nlat + rb[q].x;
+        SWX_CUDA_TRY(cudaMemcpyAsync(w.grid + r0 * p->nlon, d_grid + r0 * p->nlon,
+                                     (size_t)rb[q].y * p->nlon * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+      }
+    if ((rc = rows_fft(p, sh, n_fields, false, w.Q, w.grid, s))) return rc;
+    return multi ? rows_move(p, sh, 1, n_fields, 0, (char *)w.Q, (char *)d_send, s) : SWX_OK;
+  }
+  if (stage == 1) {
+    if (!d_coeffs) return fail(SWX_ERR_CONFIG, "null coefficients");
+    if (multi && !d_recv) return fail(SWX_ERR_CONFIG, "null receive slab");
+    if (multi && (rc = rows_move(p, sh, 1, n_fields, 1, (char *)w.Q, (char *)d_recv, s)))
+      return rc;
+    if (m1 <= m0) return SWX_OK;
+    dim3 g((p->nhp + 127) / 128, m1 - m0);
+    prep_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, n_fields, w.A, m0);
+    SWX_LAUNCH_CHECK();
+    return analysis_cols(p, w, n_fields, m0, m1, (double2 *)d_coeffs, s);
+  }
+  return fail(SWX_ERR_CONFIG, "sharded analysis stage must be 0 or 1");
 }

@@ -495,3 +495,72 @@ class ColumnEtdrkEngine:
         """View of the own columns' slots of ``x`` (default: the state)."""
         a, b = self.shard.slots()
         return (self.u if x is None else x)[..., a:b]
+
+
+class ShardedTransforms:
+    """Plain synthesis / analysis of one rank's share (the cfg4 round trip
+    sharded like the tendency): columns for the Legendre sums, latitude pairs
+    for the longitude transforms, one all-to-all per transform
+    (swx_sht_synthesis_shard / swx_sht_analysis_shard)."""
+
+    def __init__(self, plan, shard: ColumnShard, n_fields: int = 1):
+        import ctypes
+
+        import torch
+
+        self.plan, self.shard, self.nf = plan, shard, int(n_fields)
+        lib = self._lib = _lib.lib()
+        dev = plan.device
+        self.workspace = torch.empty(plan.workspace.numel(), dtype=torch.uint8, device=dev)
+        K = shard.nranks
+        self.counts, size = [], 1
+        for which in (0, 1):
+            snd, rcv = (ctypes.c_size_t * K)(), (ctypes.c_size_t * K)()
+            n = lib.swx_sht_transform_shard_counts(plan._h, ctypes.byref(shard.c), which, self.nf,
+                                                   snd, rcv)
+            if n == 0:
+                _lib.check(_lib.SWX_ERR_CONFIG)
+            self.counts.append((tuple(snd), tuple(rcv)))
+            size = max(size, int(n))
+        self.send = torch.empty(size, dtype=torch.uint8, device=dev)
+        self.recv = torch.empty(size, dtype=torch.uint8, device=dev)
+        self._which = 0
+
+    def slabs(self, ex: int):
+        s, r = self.counts[ex]
+        return self.send, s, self.recv, r
+
+    def own_rows(self):
+        """Latitude rows this rank's grid holds (south block, north block)."""
+        nlat = self.plan.cfg.nlat
+        nh = (nlat + 1) // 2
+        a, b = (min(x, nh) for x in self.shard.p_bounds[self.shard.rank:self.shard.rank + 2])
+        return np.unique(np.r_[np.arange(a, b), np.arange(nlat - b, nlat - a)]).astype(int)
+
+    def synthesis_phases(self, coeffs, grid, stream=None):
+        import ctypes
+
+        fn, sh = self._lib.swx_sht_synthesis_shard, ctypes.byref(self.shard.c)
+        ws = (ptr(self.workspace), self.workspace.numel(), stream_ptr(stream))
+        _lib.check(fn(self.plan._h, 0, self.nf, sh, ptr(coeffs), 0, 0, ptr(self.send), *ws))
+        yield self, 0
+        _lib.check(fn(self.plan._h, 1, self.nf, sh, 0, ptr(grid), ptr(self.recv), 0, *ws))
+
+    def analysis_phases(self, grid, coeffs, stream=None):
+        import ctypes
+
+        fn, sh = self._lib.swx_sht_analysis_shard, ctypes.byref(self.shard.c)
+        ws = (ptr(self.workspace), self.workspace.numel(), stream_ptr(stream))
+        _lib.check(fn(self.plan._h, 0, self.nf, sh, ptr(grid), 0, 0, ptr(self.send), *ws))
+        yield self, 1
+        _lib.check(fn(self.plan._h, 1, self.nf, sh, 0, ptr(coeffs), ptr(self.recv), 0, *ws))
+
+    def synthesis(self, comm: ColumnComm, coeffs, grid, stream=None):
+        for t, ex in self.synthesis_phases(coeffs, grid, stream):
+            comm.all_to_all(*t.slabs(ex))
+        return grid
+
+    def analysis(self, comm: ColumnComm, grid, coeffs, stream=None):
+        for t, ex in self.analysis_phases(grid, coeffs, stream):
+            comm.all_to_all(*t.slabs(ex))
+        return coeffs
