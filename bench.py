@@ -197,6 +197,14 @@ def _tendency_nlon(trunc: int, nlon: int) -> int:
     return n
 
 
+def _hbm_peak() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 7700.0  # B200_PROFILING.md fallback
+
+
 def load_traffic():
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
@@ -494,6 +502,21 @@ def main():
         ms = breakdown[dominant]["ms_per_launch"]
         roofline = {"kernel": dominant, "bound": "fp64", "achieved": None, "peak": peak64,
                     "unit": "TFLOP/s", "frac": None, "ms_per_launch": ms, "traffic": None}
+    # the l chains with the warm-time pivot cache stream 64 B per pole-solve x
+    # coefficient (two 16 B pivots per chain position, read in both sweeps,
+    # SURVEY §8d "factor-caching design"): HBM-bound; the FP64 figure moves
+    # to "fp64" inside the line
+    if roofline and dominant == "rexi_l" and not etd and (_l_cache_bytes(dr) or 0) > 0:
+        ms = breakdown[dominant]["ms_per_launch"]
+        alg_bytes = 64.0 * units_per_step / world
+        hbm_peak = _hbm_peak()
+        ach_gbs = alg_bytes / (ms * 1e-3) / 1e9
+        fp64 = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac")}
+        roofline = {"kernel": dominant, "bound": "hbm", "achieved": ach_gbs, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": ach_gbs / hbm_peak,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+                    "algorithmic_bytes_per_launch": alg_bytes,
+                    "traffic": traffic.get("rexi_l_" + args.config), "fp64": fp64}
 
     # ---- cfg4: SH transform round trip of the seeded phi' field (SURVEY §8d:
     # synthesis then analysis, 2 x (4 nlat ncoef + 2.5 nlon log2(nlon) nlat) flops)
