@@ -184,6 +184,20 @@ int swx_sht_tendency_sub(swx_sht p, int atoms, const swx_c128 *d_state,
                          const swx_c128 *d_sub, swx_c128 *d_out, void *d_workspace,
                          size_t ws_bytes, void *stream);
 
+/* The three stages of swx_sht_tendency[_sub] separately, on a column range:
+ * stage 0 synthesises columns [m0, m1) of d_state into the workspace's grid
+ * stage rows, stage 1 runs the fused grid stage (every latitude pair; needs
+ * all columns synthesised), stage 2 the analysis of columns [m0, m1) into
+ * d_out (minus d_sub when non-null).  Column blocks of stages 0 and 2 are
+ * independent, so a caller can pipeline them with the per-column pole sums
+ * (the ETD2RK engine's analysis -> psi_k -> synthesis chain).  Fused-grid
+ * (table) plans only.                                                       */
+int swx_sht_tendency_part(swx_sht p, int stage, int atoms, int m0, int m1,
+                          const swx_c128 *d_state, const swx_c128 *d_sub, swx_c128 *d_out,
+                          void *d_workspace, size_t ws_bytes, void *stream);
+/* 1 when the plan has the separable (fused-grid, table) tendency stages.    */
+int swx_sht_has_stages(swx_sht p);
+
 /* ---- column-sharded N term over ranks -----------------
  * The reference evaluates the non-linear tendency on every worker (the
  * paper's replicated "no communication" non-linearities, parallel.py:185-214,

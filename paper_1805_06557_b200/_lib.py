@@ -68,6 +68,8 @@ SIGNATURES = {
     "swx_sht_tendency_shard": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
     "swx_solver_set_columns": (_I, [_P, _I, _I]),
     "swx_solver_cache_bytes": (_S, [_P]),
+    "swx_sht_tendency_part": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _S, _P]),
+    "swx_sht_has_stages": (_I, [_P]),
     "swx_sht_transform_shard_counts": (_S, [_P, _P, _I, _I, _P, _P]),
     "swx_sht_synthesis_shard": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _S, _P]),
     "swx_sht_analysis_shard": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _S, _P]),

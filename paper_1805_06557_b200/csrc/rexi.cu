@@ -779,7 +779,10 @@ __device__ __forceinline__ void lc_bulk(void *dst, const void *src, unsigned byt
       "l"(src), "r"(bytes), "r"(lc_smem(bar))
       : "memory");
 }
-constexpr int kLRing = 2;               // cached pivots: segments in flight per warp
+#ifndef SWX_LRING
+#define SWX_LRING 2
+#endif
+constexpr int kLRing = SWX_LRING;       // cached pivots: segments in flight per warp
 constexpr int kLSegW = kLSeg * 64;      // double2 per segment block (positions x chains x lanes)
 
 // cache index of (global pole gp, packed slot s, chain c)

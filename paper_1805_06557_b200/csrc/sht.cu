@@ -3923,3 +3923,62 @@ extern "C" int swx_sht_analysis_shard(swx_sht p, int stage, int n_fields, const 
   }
   return fail(SWX_ERR_CONFIG, "sharded analysis stage must be 0 or 1");
 }
+
+// ---------------------------------------------------------------------
+// Column-range stages of the single-rank tendency (the pipelined ETD2RK
+// engine): stage 0 synthesises columns [m0, m1) into the grid-stage rows,
+// stage 1 runs the fused grid stage of every latitude pair, stage 2 the
+// analysis of columns [m0, m1) (out = tendency - sub when sub is given).
+// Only the table / fused-grid path has separable stages.
+// ---------------------------------------------------------------------
+extern "C" int swx_sht_tendency_part(swx_sht p, int stage, int atoms, int m0, int m1,
+                                     const swx_c128 *d_state, const swx_c128 *d_sub,
+                                     swx_c128 *d_out, void *d_ws, size_t ws_bytes,
+                                     void *stream) {
+  int rc = check_ws(p, d_ws, ws_bytes);
+  if (rc) return rc;
+  if (!p->fused_grid || !p->use_tab)
+    return fail(SWX_ERR_CONFIG, "tendency stages need the fused grid stage (Legendre table)");
+  if (atoms <= 0 || (atoms & ~(SWX_TEND_LC | SWX_TEND_N)))
+    return fail(SWX_ERR_CONFIG, "atoms must be a non-empty subset of {lc, n}");
+  if (p->omega == 0.0) atoms &= ~SWX_TEND_LC;  // swe.py:200-201
+  if (atoms == 0) return fail(SWX_ERR_CONFIG, "tendency stages with no active atom");
+  if (m0 < 0 || m1 > p->trunc + 1 || m1 < m0) return fail(SWX_ERR_CONFIG, "bad column range");
+  cudaStream_t s = (cudaStream_t)stream;
+  ShtWs w = carve(p, d_ws);
+  switch (stage) {
+    case 0: {
+      if (!d_state) return fail(SWX_ERR_CONFIG, "null state");
+      if (m1 == m0) return SWX_OK;
+      SynthArgs a;
+      a.coef = (const double2 *)d_state;
+      a.c2r = w.c2r;
+      a.lc = w.lc;
+      a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
+      a.nfreq = p->nfreq_t;
+      a.zpack = 1;
+      a.m0 = m0;
+      int nt;
+      dim3 g = synth_grid(p, 1, &nt);
+      g.x = m1 - m0;
+      const size_t smem = synth_smem(5, 2, 1, nt);
+      auto k = synth_kernel<0, 1>;
+      if (smem > 48 * 1024)
+        SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
+      SWX_LAUNCH_CHECK();
+      return SWX_OK;
+    }
+    case 1:
+      return launch_grid(p, atoms, w, s);
+    case 2:
+      if (!d_out) return fail(SWX_ERR_CONFIG, "null output");
+      if (m1 == m0) return SWX_OK;
+      return launch_analysis_tab<0>(p, w.A, (double2 *)d_out, 3, s, (const double2 *)d_sub,
+                                    first_item(p->trunc, m0), first_item(p->trunc, m1));
+    default:
+      return fail(SWX_ERR_CONFIG, "tendency stage must be 0, 1 or 2");
+  }
+}
+
+extern "C" int swx_sht_has_stages(swx_sht p) { return p && p->fused_grid && p->use_tab ? 1 : 0; }

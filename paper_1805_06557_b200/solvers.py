@@ -131,6 +131,12 @@ class ShiftedLinearSolver:
         self._native(alphas)
         return self
 
+    def set_columns(self, alphas, m0: int, m1: int):
+        """Restrict the following lg pole sums of this shift set to columns
+        [m0, m1) (swx_solver_set_columns; the launch captures the schedule, so
+        a caller can alternate ranges between launches).  Private solvers only."""
+        _lib.check(self._lib.swx_solver_set_columns(self._native(alphas).h, int(m0), int(m1)))
+
     def workspace(self, nat: _Native, n_rhs: int, lo: int, hi: int, stream=None):
         """Scratch for one pole sum; one buffer per stream, so sums issued
         concurrently on different streams never share partials."""

@@ -231,6 +231,22 @@ class ShtPlan:
         _lib.check(self._lib.swx_sht_set_synth_event(
             self._h, event.cuda_event if event is not None else 0))
 
+    def fused_stages(self) -> bool:
+        """Whether the tendency has separable stages (fused grid / table path)."""
+        return bool(self._lib.swx_sht_has_stages(self._h))
+
+    def tendency_part(self, stage: int, atoms: int, m0: int, m1: int, state=None, out=None,
+                      sub=None, stream=None, workspace=None):
+        """One stage of the tendency on columns [m0, m1) (swx_sht_tendency_part);
+        ``workspace`` (default: the plan's) carries the stage results between
+        calls."""
+        ws = self.workspace if workspace is None else workspace
+        _lib.check(self._lib.swx_sht_tendency_part(
+            self._h, int(stage), int(atoms), int(m0), int(m1),
+            ptr(state) if state is not None else 0, ptr(sub) if sub is not None else 0,
+            ptr(out) if out is not None else 0, ptr(ws), ws.numel(), stream_ptr(stream)))
+        return out
+
     def tendency_dev(self, atoms: int, state, out=None, stream=None, sub=None):
         """out = tendency(state) (minus ``sub`` when given, fused on the device)."""
         import torch
@@ -353,3 +369,4 @@ def vortdiv_from_uv(u: GridField, v: GridField, cfg: SphereConfig):
     z, d = plan.vortdiv_dev(ug, vg)
     return (SpectralField(unpack(z.cpu().numpy(), cfg.trunc)),
             SpectralField(unpack(d.cpu().numpy(), cfg.trunc)))
+

@@ -540,3 +540,31 @@ def test_column_sharded_t1279_round_trip(K):
         got[:, a:z] = b[:, a:z]
     assert float((got - ref_back).abs().max() / ref_back.abs().max()) <= 1e-14
     assert rel_linf(got.cpu().numpy(), c.cpu().numpy()) <= 1e-10
+
+
+@pytest.mark.parametrize("trunc", [63, 256])
+def test_pipelined_etdrk_bitwise(trunc, monkeypatch):
+    """The column-block pipelined ETD2RK step (analysis -> psi_k -> synthesis
+    chains overlapped per column block, the next step's synthesis at the end
+    of each step) equals the plain step graph bitwise over 3 steps, both
+    device-resident and through step_host."""
+    import paper_1805_06557_b200.steppers as S
+    par = params(trunc)
+    ic = ost.seeded_balanced_state(osh.grid_for(trunc))
+    setup = RexiSetup(num_poles=128)
+    engines = {}
+    for blocks in (0, 2, 3):
+        monkeypatch.setattr(S, "_PIPE_BLOCKS", blocks)
+        st = S.EtdrkStepper(LG, LC_N, par, setup)
+        eng = st.engine(1800.0)
+        assert eng.pipe == (blocks > 1)
+        eng.load(ic)
+        for _ in range(3):
+            eng.step_dev()
+        engines[blocks] = (st, eng.u.cpu().numpy())
+    ref = engines[0][1]
+    assert np.array_equal(engines[2][1], ref) and np.array_equal(engines[3][1], ref)
+    s0 = PrognosticState.from_stack(ic, par.cfg)
+    a = engines[0][0].step(s0, 1800.0).stack()
+    b = engines[2][0].step(s0, 1800.0).stack()
+    assert np.array_equal(a, b)
