@@ -768,11 +768,13 @@ __device__ __forceinline__ void lc_bar_wait(uint64_t *bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void lc_bulk(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+__device__ __forceinline__ void lc_expect(uint64_t *bar, unsigned bytes) {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(lc_smem(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void lc_copy(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
           lc_smem(dst)),
@@ -788,6 +790,31 @@ constexpr int kLSegW = kLSeg * 64;      // double2 per segment block (positions 
 // cache index of (global pole gp, packed slot s, chain c)
 __device__ __forceinline__ size_t linv_at(int gp, int ncoef, int s, int c) {
   return ((size_t)(gp >> 5) * ncoef + s) * 64 + c * 32 + (gp & 31);
+}
+
+// per-position chain data of one solve, packed per column (slot order) so the
+// cached chain kernel can stream whole segments with bulk copies
+template <int NRHS>
+__global__ void l_pack_kernel(const double2 *__restrict__ rhs, const double *__restrict__ lconst,
+                              const double *__restrict__ chain, int trunc, int ncoef,
+                              LPos<NRHS> *__restrict__ pos) {
+  const int m = blockIdx.y, k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > trunc - m) return;
+  const int s = col_offset(trunc, m) + k, l = m + k;
+  LPos<NRHS> e;
+  e.L = chain[s];
+  e.U = chain[ncoef + s];
+  e.rot = chain[2 * ncoef + s];
+  e.g = lconst[(trunc + 1) + l];
+  e.h = lconst[2 * (trunc + 1) + l];
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) {
+    const double2 *b = rhs + (size_t)r * 3 * ncoef;
+    e.bp[r] = b[s];
+    e.bz[r] = b[ncoef + s];
+    e.bd[r] = b[2 * ncoef + s];
+  }
+  pos[s] = e;
 }
 
 // fills the pivot cache: one thread per (pole, m, chain), the forward sweep
@@ -826,23 +853,29 @@ __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_p
   }
 }
 
+#ifndef SWX_LC_MINB
+#define SWX_LC_MINB 3  // resident CTAs per SM the cached kernel's register budget targets
+#endif
 template <int NRHS, bool CACHED = false>
-__global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
+__global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
     const double2 *__restrict__ beta, int beta_stride, int pole0, int P,
     int n_blocks, int trunc, int ncoef, double dt, double phibar,
     const double *__restrict__ lconst, const double *__restrict__ chain,
     double2 *__restrict__ scratch, double2 *__restrict__ part,
-    const double2 *__restrict__ linv) {
+    const double2 *__restrict__ linv, const LPos<NRHS> *__restrict__ lpos) {
   // reduction buffer: [warp][row][r][comp][32] (dynamic, NRHS * 32 KB)
   extern __shared__ double2 red_raw[];
   auto red = reinterpret_cast<double2 (*)[kFlush][NRHS][2][32]>(red_raw);
   __shared__ LPos<NRHS> pos_s[kLWarps][kLSeg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // cached pivots: per-warp ring of kLRing segment blocks filled by bulk copies
-  double2 *ring = red_raw + (size_t)kLWarps * kFlush * NRHS * 2 * 32 + (size_t)warp * kLRing * kLSegW;
+  // cached pivots: per-warp ring of kLRing segment slots filled by bulk copies,
+  // each the segment's pivots (kLSegW double2) then its packed positions
+  constexpr int PW = (int)(sizeof(LPos<NRHS>) / sizeof(double2));
+  constexpr int SLOTW = kLSegW + kLSeg * PW;
+  double2 *ring = red_raw + (size_t)kLWarps * kFlush * NRHS * 2 * 32 + (size_t)warp * kLRing * SLOTW;
   uint64_t *bars = reinterpret_cast<uint64_t *>(red_raw + (size_t)kLWarps * kFlush * NRHS * 2 * 32 +
-                                                (size_t)kLWarps * kLRing * kLSegW) +
+                                                (size_t)kLWarps * kLRing * SLOTW) +
                    warp * kLRing;
   int seq = 0, cons = 0;  // segment blocks issued / consumed by this warp
   if constexpr (CACHED) {
@@ -886,14 +919,21 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     // then pass 2 (nseg-1..0), kLRing blocks in flight
     const double2 *lsrc = CACHED ? linv + ((size_t)((pole0 + pb * 32) >> 5) * ncoef + off) * 64
                                  : nullptr;
+    const LPos<NRHS> *psrc = CACHED ? lpos + off : nullptr;
     auto issue = [&](int i) {  // flat index i of the 2 * nseg block loads
       if constexpr (CACHED) {
         if (i < 2 * nseg) {
           const int sg = i < nseg ? i : 2 * nseg - 1 - i;
           const int cnt = min(kLSeg, nl - sg * kLSeg);
-          if (lane == 0)
-            lc_bulk(ring + (seq % kLRing) * kLSegW, lsrc + (size_t)sg * kLSegW,
-                    (unsigned)(cnt * 64 * sizeof(double2)), bars + seq % kLRing);
+          if (lane == 0) {
+            double2 *dst = ring + (seq % kLRing) * SLOTW;
+            uint64_t *bar = bars + seq % kLRing;
+            const unsigned bi = (unsigned)(cnt * 64 * sizeof(double2));
+            const unsigned bp = (unsigned)(cnt * sizeof(LPos<NRHS>));
+            lc_expect(bar, bi + bp);
+            lc_copy(dst, lsrc + (size_t)sg * kLSegW, bi, bar);
+            lc_copy(dst + kLSegW, psrc + (size_t)sg * kLSeg, bp, bar);
+          }
           ++seq;
         }
       }
@@ -901,7 +941,7 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
     auto acquire = [&]() -> const double2 * {  // next block in flat order
       if constexpr (CACHED) {
         lc_bar_wait(bars + cons % kLRing, (cons / kLRing) & 1);
-        return ring + (cons % kLRing) * kLSegW;
+        return ring + (cons % kLRing) * SLOTW;
       }
       return nullptr;
     };
@@ -922,7 +962,8 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) y[c][r] = make_double2(0.0, 0.0);
     LPos<NRHS> nxt;
-    l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, 0, min(kLSeg, nl), lane, nxt);
+    if constexpr (!CACHED)
+      l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, 0, min(kLSeg, nl), lane, nxt);
     for (int sgi = 0; sgi < nseg; ++sgi) {
       double2 *dst = slot + ((size_t)sgi * 32 + lane) * CKW;
 #pragma unroll
@@ -933,18 +974,21 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       }
       const int k0 = sgi * kLSeg;
       const int n = min(kLSeg, nl - k0);
-      l_publish<NRHS>(nxt, n, lane, sp);
-      if (sgi + 1 < nseg)  // next segment's loads fly during this segment's sweep
-        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 + kLSeg,
-                      min(kLSeg, nl - k0 - kLSeg), lane, nxt);
+      if constexpr (!CACHED) {
+        l_publish<NRHS>(nxt, n, lane, sp);
+        if (sgi + 1 < nseg)  // next segment's loads fly during this segment's sweep
+          l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 + kLSeg,
+                        min(kLSeg, nl - k0 - kLSeg), lane, nxt);
+      }
       const double2 *iv = acquire();
+      const LPos<NRHS> *sq = CACHED ? reinterpret_cast<const LPos<NRHS> *>(iv + kLSegW) : sp;
 #pragma unroll
       for (int e = 0; e < kLSeg; ++e) {
         if (e < n) {
           const int k = k0 + e;
           if constexpr (CACHED) {
-            l_fwd_c<NRHS>(sp[e], (k & 1) == 0, ia, iv[e * 64 + lane], y[0]);
-            l_fwd_c<NRHS>(sp[e], (k & 1) == 1, ia, iv[e * 64 + 32 + lane], y[1]);
+            l_fwd_c<NRHS>(sq[e], (k & 1) == 0, ia, iv[e * 64 + lane], y[0]);
+            l_fwd_c<NRHS>(sq[e], (k & 1) == 1, ia, iv[e * 64 + 32 + lane], y[1]);
           } else {
             l_fwd<NRHS>(sp[e], (k & 1) == 0, a, ia, cp[0], y[0]);
             l_fwd<NRHS>(sp[e], (k & 1) == 1, a, ia, cp[1], y[1]);
@@ -970,8 +1014,9 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
       }
     };
     load_ck(nseg - 1);
-    l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, (nseg - 1) * kLSeg,
-                  nl - (nseg - 1) * kLSeg, lane, nxt);
+    if constexpr (!CACHED)
+      l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, (nseg - 1) * kLSeg,
+                    nl - (nseg - 1) * kLSeg, lane, nxt);
     for (int sgi = nseg - 1; sgi >= 0; --sgi) {
       const int k0 = sgi * kLSeg;
       const int n = min(kLSeg, nl - k0);
@@ -981,12 +1026,15 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
 #pragma unroll
         for (int r = 0; r < NRHS; ++r) y[c][r] = ck_y[c][r];
       }
-      l_publish<NRHS>(nxt, n, lane, sp);
+      if constexpr (!CACHED) l_publish<NRHS>(nxt, n, lane, sp);
       if (sgi > 0) {  // previous segment's checkpoint and data fly during this one
         load_ck(sgi - 1);
-        l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 - kLSeg, kLSeg, lane, nxt);
+        if constexpr (!CACHED)
+          l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, k0 - kLSeg, kLSeg, lane, nxt);
       }
       const double2 *iv = acquire();
+      const LPos<NRHS> *sq = CACHED ? reinterpret_cast<const LPos<NRHS> *>(iv + kLSegW) : sp;
+      double2 bps[kLSeg][NRHS];  // phi' recovery data, read before the slot is released
       double2 cps[2][kLSeg], ys[2][NRHS][kLSeg];
 #pragma unroll
       for (int e = 0; e < kLSeg; ++e) {
@@ -997,8 +1045,8 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
             if constexpr (CACHED) {
               const bool isz = ((k + c) & 1) == 0;
               const double2 inv = iv[e * 64 + c * 32 + lane];
-              l_fwd_c<NRHS>(sp[e], isz, ia, inv, y[c]);
-              cp[c] = cscale((isz ? -1.0 : 1.0) * sp[e].U, inv);
+              l_fwd_c<NRHS>(sq[e], isz, ia, inv, y[c]);
+              cp[c] = cscale((isz ? -1.0 : 1.0) * sq[e].U, inv);
             } else {
               l_fwd<NRHS>(sp[e], ((k + c) & 1) == 0, a, ia, cp[c], y[c]);
             }
@@ -1006,9 +1054,11 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
 #pragma unroll
             for (int r = 0; r < NRHS; ++r) ys[c][r][e] = y[c][r];
           }
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) bps[e][r] = sq[e].bp[r];
         }
       }
-      release(2 * nseg - 1 - sgi);  // pivots of this segment are in cps now
+      release(2 * nseg - 1 - sgi);  // pivots and positions of this segment are in registers
       // back substitution; (position e, chain c) -> reduction row (n-1-e)*2 + c
 #pragma unroll
       for (int e = kLSeg - 1; e >= 0; --e) {
@@ -1025,7 +1075,7 @@ __global__ void __launch_bounds__(kLWarps * 32) rexi_l_kernel(
               xn[c][r] = x;
               red[warp][er][r][0][phys] = cmul(bet[r], x);
               if (!isz) {
-                const double2 b = sp[e].bp[r];
+                const double2 b = bps[e][r];
                 const double2 ph = cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), ia);
                 red[warp][er][r][1][phys] = cmul(bet[r], ph);
               }
@@ -1422,8 +1472,11 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
 static constexpr int kLgMaxP = 512;  // poles per lg launch (smem = NRHS*64*P bytes)
 
 static size_t l_smem_bytes(int nrhs, bool cached = false) {
+  const size_t pos = nrhs == 1 ? sizeof(LPos<1>) : sizeof(LPos<2>);
   return (size_t)kLWarps * kFlush * nrhs * 2 * 32 * sizeof(double2) +
-         (cached ? (size_t)kLWarps * kLRing * (kLSegW * sizeof(double2) + sizeof(uint64_t)) : 0);
+         (cached ? (size_t)kLWarps * kLRing * (kLSegW * sizeof(double2) + kLSeg * pos) +
+                       (size_t)kLWarps * kLRing * sizeof(uint64_t)
+                 : 0);
 }
 
 static int l_grid_warps(swx_solver s, int n_items) {
@@ -1463,7 +1516,8 @@ extern "C" size_t swx_rexi_workspace_bytes(swx_solver s, int n_rhs,
     return ((fac + 255) / 256) * 256 + (chunks > 1 ? chunks * state : 0);
   }
   const int nb = (P + 31) / 32;
-  return l_scratch_bytes(s, n_rhs, P) + (size_t)nb * state + 256;
+  const size_t pos = (size_t)s->ncoef * (n_rhs == 1 ? sizeof(LPos<1>) : sizeof(LPos<2>));
+  return l_scratch_bytes(s, n_rhs, P) + (size_t)nb * state + 256 + pos + 256;
 }
 
 // modes per CTA for a given lanes-per-mode; schedules built lazily
@@ -1678,11 +1732,20 @@ static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
   const bool cached = s->d_linv && pole0 % 32 == 0;
   const size_t smem = l_smem_bytes(NRHS, cached);
   auto k = cached ? rexi_l_kernel<NRHS, true> : rexi_l_kernel<NRHS, false>;
+  // packed per-position data (after the partials), streamed by the cached kernel
+  const size_t stride_parts = (size_t)NRHS * 3 * s->ncoef * nb;
+  LPos<NRHS> *lpos = reinterpret_cast<LPos<NRHS> *>(
+      (char *)part + ((stride_parts * sizeof(double2) + 255) / 256) * 256);
+  if (cached) {
+    dim3 gp((s->trunc + 1 + 127) / 128, s->trunc + 1);
+    l_pack_kernel<NRHS><<<gp, 128, 0, st>>>(rhs, s->d_lconst, s->d_chain, s->trunc, s->ncoef, lpos);
+    SWX_LAUNCH_CHECK();
+  }
   if (smem > 48 * 1024)
     SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<warps / kLWarps, kLWarps * 32, smem, st>>>(
       rhs, s->d_alpha, betas, s->n_poles, pole0, P, nb, s->trunc, s->ncoef, s->dt,
-      s->phibar, s->d_lconst, s->d_chain, scratch, part, s->d_linv);
+      s->phibar, s->d_lconst, s->d_chain, scratch, part, s->d_linv, lpos);
   SWX_LAUNCH_CHECK();
   const size_t stride = (size_t)NRHS * 3 * s->ncoef;
   tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, nb, s->ncoef,
