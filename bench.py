@@ -36,7 +36,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=48)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg4"), default="cfg2")
+    ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg3", "cfg4"), default="cfg2")
     ap.add_argument("--shard", choices=("auto", "poles", "cols"), default="auto",
                     help="N>1: shard REXI poles (+ all-reduce) or zonal columns (ETD2RK: "
                          "sharded N term, 4 all-to-alls per step); auto = cols for cfg2")
@@ -222,6 +222,78 @@ def _l_cache_bytes(dr):
     return int(_lib.load().swx_solver_cache_bytes(dr.solver._native(dr.alphas).h))
 
 
+def run_stiffness(args, rank, world):
+    """cfg3: config 2's ETD2RK setup over the 36-case stiffness sweep
+    (workloads.stiffness_cases), 24 device-resident steps per case (graph
+    replays, L2 flushed before each step, CUDA events around each step); the
+    line's value is the sweep's total pole-solve*coeff over its total time,
+    and every case must stay finite (the reference's blow-up check,
+    steppers.py:516-520).  Replicated on every rank (the sweep's cases are
+    independent; each rank runs the whole sweep) -- one GPU is the unit."""
+    import torch
+
+    from paper_1805_06557_b200.device import ncoef
+    from paper_1805_06557_b200.rexi import RexiSetup
+    from paper_1805_06557_b200.steppers import EtdrkStepper
+    from paper_1805_06557_b200.swe import LC_N, LG, ModelParams
+    from paper_1805_06557_b200.sphere import SphereConfig, plan_for
+    from paper_1805_06557_b200.workloads import seeded_balanced_state, stiffness_cases
+
+    cfg = SphereConfig.for_truncation(256)
+    nc = ncoef(256)
+    plan = plan_for(cfg)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    sampler = ClockSampler(0)
+    sampler.start()
+    rows, tot_units, tot_ms, stable = [], 0.0, 0.0, True
+    ic = seeded_balanced_state(cfg)  # config 2's initial state for every case
+    for case in stiffness_cases():
+        par = ModelParams(case.phibar, cfg)
+        eng = EtdrkStepper(LG, LC_N, par, RexiSetup(10.0, case.p1, case.n_poles)).engine(case.dt)
+        eng.load(ic)
+        for _ in range(max(1, args.warmup)):
+            eng.step_dev()
+        eng.load(ic)
+        torch.cuda.synchronize()
+        ms, blow = 0.0, None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for k in range(1, case.steps + 1):
+            flush.zero_()
+            e0.record()
+            eng.step_dev()
+            e1.record()
+            e1.synchronize()
+            ms += e0.elapsed_time(e1)
+            if blow is None:  # the reference's blow-up check (untimed)
+                phi = plan.synthesis_dev(eng.u[0:1].contiguous())
+                if not bool(torch.isfinite(phi).all()) or float(phi.abs().max()) > 1e6:
+                    blow = k
+        ok = blow is None
+        stable &= ok
+        units = 3.0 * case.n_poles * nc * case.steps
+        tot_units += units
+        tot_ms += ms
+        rows.append({"phibar_g": case.phibar_g, "dt": case.dt, "y": round(case.y, 2),
+                     "p1": case.p1, "n_poles": case.n_poles,
+                     "ms_per_step": round(ms / case.steps, 4), "stable": ok,
+                     "blow_up_step": blow})
+    clocks = sampler.stop()
+    line = {"metric": "REXI pole-solves*SH-coeffs/s", "value": tot_units / (tot_ms * 1e-3),
+            "unit": "pole-solve*coeff/s", "n_gpus": 1, "steps": 24, "warmup": args.warmup,
+            "ms_per_step": tot_ms / (24 * len(rows)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded, SURVEY §8d)",
+            "config": {"workload": "cfg3 stiffness sweep of cfg2 (T256, 36 cases x 24 steps)",
+                       "trunc": 256, "grid": [cfg.nlat, cfg.nlon],
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "cuda_graph": True},
+            "all_stable": stable, "cases": rows, "clocks": clocks,
+            "note": "unstable cases run all 24 steps (timed like the rest); their blow-up "
+                    "step matches the oracle's (tests/golden/cfg3_verdicts.json)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def column_breakdown(torch, eng, ccomm, flush, reps=5):
     """Rank-local device times of the column-sharded step's pieces: the
     three tendency stages (each with its slab pack/unpack copies) and one
@@ -283,6 +355,9 @@ def main():
                                                  seeded_linear_state)
 
     torch.cuda.set_device(local)
+    if args.config == "cfg3":
+        run_stiffness(args, rank, world)
+        return
     comm = ccomm = None
     etd = args.config == "cfg2"
     mode = args.shard if args.shard != "auto" else ("cols" if etd else "poles")

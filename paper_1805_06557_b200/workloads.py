@@ -54,6 +54,38 @@ CONFIGS = {
 }
 
 
+@dataclasses.dataclass(frozen=True)
+class StiffCase:
+    """One cfg3 case: config 2's setup at Phibar = phibar_g * g and dt."""
+    phibar_g: float
+    dt: float
+    y: float            # dt * sqrt(Phibar T (T+1)) / a: the fastest gravity-wave phase
+    p1: float
+    n_poles: int
+    steps: int = 24
+
+    @property
+    def phibar(self) -> float:
+        return self.phibar_g * G
+
+
+def stiffness_cases(trunc: int = 256, radius: float = 6.37122e6) -> list:
+    """cfg3: Phibar/g in {2000, ..., 18000} (benchmarks.py:240-249)
+    x dt in {300, 900, 1800, 3600} s; contour p0 = 10 and the smallest
+    power-of-two N with REXI error <= 1e-7 for y = dt sqrt(Phibar T(T+1))/a:
+    y <= 15.2 -> (p1 30, N 128); <= 22.7 -> (30, 256); <= 30.5 -> (40, 512);
+    <= 45.4 -> (60, 1024); else (80, 2048) (y <= 60.9 at the corner)."""
+    table = ((15.2, 30.0, 128), (22.7, 30.0, 256), (30.5, 40.0, 512), (45.4, 60.0, 1024),
+             (61.0, 80.0, 2048))
+    out = []
+    for pg in range(2000, 18001, 2000):
+        for dt in (300.0, 900.0, 1800.0, 3600.0):
+            y = dt * np.sqrt(pg * G * trunc * (trunc + 1)) / radius
+            p1, n = next((p, n) for lim, p, n in table if y <= lim)
+            out.append(StiffCase(float(pg), dt, float(y), p1, n))
+    return out
+
+
 def seeded_linear_state(trunc: int, seed: int = 0) -> np.ndarray:
     """cfg0/1/4 input (dense (3, n, n)): amplitudes 1e3, 1e-5, 1e-5 with
     (l+1)^-2 decay; m = 0 real."""

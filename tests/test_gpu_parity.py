@@ -568,3 +568,57 @@ def test_pipelined_etdrk_bitwise(trunc, monkeypatch):
     a = engines[0][0].step(s0, 1800.0).stack()
     b = engines[2][0].step(s0, 1800.0).stack()
     assert np.array_equal(a, b)
+
+
+def test_cfg3_stiffness_sweep_t256_matches_oracle_verdicts():
+    """cfg3: all 36 (Phibar, dt) cases of the stiffness sweep at T256
+    (contours per workloads.stiffness_cases, N up to 2048), 24 device-resident
+    ETD2RK steps each with the reference's blow-up check (synthesis of phi',
+    |phi'| > 1e6, steppers.py:516-520) after every step.  Cases the oracle
+    integrated (tests/golden/cfg3_verdicts.json) must blow up at the same step
+    (or stay stable); every other case must stay stable."""
+    import json
+    import os
+    from paper_1805_06557_b200.steppers import EtdrkStepper
+    from paper_1805_06557_b200.workloads import seeded_balanced_state, stiffness_cases
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cfg3_verdicts.json")) as fh:
+        verdicts = json.load(fh)
+    cfg = SphereConfig.for_truncation(256)
+    plan = plan_for(cfg)
+    ic = seeded_balanced_state(cfg)
+    cases = stiffness_cases()
+    assert len(cases) == 36 and max(c.y for c in cases) < 61.0
+    for case in cases:
+        par = ModelParams(case.phibar, cfg)
+        eng = EtdrkStepper(LG, LC_N, par, RexiSetup(10.0, case.p1, case.n_poles)).engine(case.dt)
+        eng.load(ic)
+        blow = None
+        for k in range(1, case.steps + 1):
+            eng.step_dev()
+            phi = plan.synthesis_dev(eng.u[0:1].contiguous())
+            if not bool(torch.isfinite(phi).all()) or float(phi.abs().max()) > 1e6:
+                blow = k
+                break
+        want = verdicts.get(f"{case.phibar_g:.0f},{case.dt:.0f}", {"blow_up_step": None})
+        assert blow == want["blow_up_step"], (case, blow, want)
+
+
+def test_cfg3_mid_case_24_steps_vs_oracle():
+    """A mid cfg3 case (Phibar = 10000 g, dt = 1800 s: p1 = 30, N = 256) for the
+    full 24 steps at T85 against the oracle trajectory (rel L2 <= 1e-8)."""
+    from paper_1805_06557_b200.workloads import stiffness_cases
+    case = next(c for c in stiffness_cases() if c.phibar_g == 10000 and c.dt == 1800.0)
+    trunc = 85
+    cfg = SphereConfig.for_truncation(trunc)
+    par = ModelParams(case.phibar, cfg)
+    grid = osh.Grid(trunc)
+    ic = ost.seeded_balanced_state(grid)
+    model = orx.Model(trunc, case.phibar)
+    sets = {k: ost.contour_coeffs(k, 10.0, case.p1, case.n_poles) for k in (0, 1, 2)}
+    ref = ic
+    for _ in range(case.steps):
+        ref = ost.etdrk2_step(model, grid, case.dt, sets, ref)
+    stepper = build_stepper("lg_rexi_lc_n_etdrk", par, RexiSetup(10.0, case.p1, case.n_poles))
+    res = integrate(stepper, PrognosticState.from_stack(ic, cfg), case.dt, case.steps * case.dt)
+    assert not res.diverged
+    assert rel_l2(pack(res.state.stack()), olay.pack(ref)) <= 1e-8
