@@ -1602,7 +1602,20 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
   int rc = lg_geom(P, g);
   if (rc) return rc;
   int n_cta = 0;
-  const int4 *sched = lg_schedule(s, kLgPasses * 4 * 32 / g.lpm, &n_cta);
+  // modes per CTA: kLgPasses passes amortise the factor staging, but small
+  // truncations (cfg0: 64 one-item degrees) need more, smaller items to fill
+  // the SMs -- halve the passes while there are fewer than 2 items per SM
+  int passes = kLgPasses;
+  {
+    const int lo = s->col_lo, hi = s->col_hi < 0 ? s->trunc + 1 : s->col_hi;
+    auto items_for = [&](int mpc) {
+      long n = 0;
+      for (int l = lo; l <= s->trunc; ++l) n += (std::min(l + 1, hi) - lo + mpc - 1) / mpc;
+      return n;
+    };
+    while (passes > 1 && items_for(passes * 4 * 32 / g.lpm) < 2L * sm_count()) passes /= 2;
+  }
+  const int4 *sched = lg_schedule(s, passes * 4 * 32 / g.lpm, &n_cta);
   if (!sched) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
   const size_t smem = (size_t)NRHS * 4 * g.np * sizeof(double2);
 #define SWX_LG_CASE(LV)                                                                        \
