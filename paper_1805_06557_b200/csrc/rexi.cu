@@ -265,7 +265,7 @@ __device__ __forceinline__ double2 axpy_out(const Axpy &ep, size_t i, double2 v)
   return make_double2(b.x + v.x * ep.scale, b.y + v.y * ep.scale);
 }
 
-constexpr int kLgPasses = 4;  // 16-mode passes per CTA (factor staging amortised 4x)
+constexpr int kLgPasses = 2;  // 16-mode passes per CTA (factor staging amortised 2x; 4: 28.7 -> 2: 26.7 us at cfg2)
 
 // SLPM > 0 (with SNB > 0): static geometry -- LPM lanes per mode, SNB leaf
 // blocks per lane -- so every pole's tree is fully unrolled (same pairwise
@@ -1605,8 +1605,9 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
   // modes per CTA: kLgPasses passes amortise the factor staging, but small
   // truncations (cfg0: 64 one-item degrees) need more, smaller items to fill
   // the SMs -- halve the passes while there are fewer than 2 items per SM
-  int passes = kLgPasses;
-  {
+  static const int env_passes = getenv("SWX_LG_PASSES") ? atoi(getenv("SWX_LG_PASSES")) : 0;
+  int passes = env_passes > 0 ? env_passes : kLgPasses;
+  if (env_passes <= 0) {
     const int lo = s->col_lo, hi = s->col_hi < 0 ? s->trunc + 1 : s->col_hi;
     auto items_for = [&](int mpc) {
       long n = 0;
