@@ -1867,6 +1867,130 @@ __global__ void __launch_bounds__(kACT, NF == 1 ? SWX_ACOL_MINB : 1) analysis_co
   }
 }
 
+// The tendency analysis in the same column-walk form (T > 341, no table):
+// per pair the fold of the products and Coriolis terms into the 7 series
+// (tend_row, 1/cos folded into the H series), per degree the contributions
+// P_l A_P[par] + H_l A_H[1 - par] to (vort, div, phi', ke) with
+// H_l = c.z P_{l-1} - c.w P_{l+1} (sphere.py:102-111), 8-degree chunks
+// reduced over the warp by the transposed butterfly, over the CTA in shared
+// memory, over pair blocks by analysis_col_tend_reduce (which also adds
+// l(l+1)/a^2 ke to div and subtracts `sub`).  One pair per thread.
+constexpr int kTCT = 256;
+#ifndef SWX_ACT_MINB
+#define SWX_ACT_MINB 2
+#endif
+
+__global__ void __launch_bounds__(kTCT, SWX_ACT_MINB) analysis_col_tend_kernel(ShtView p, const double2 *Q,
+                                                                   const double2 *lc, int atoms,
+                                                                   double2 *part) {
+  __shared__ double2 red[kTCT / 32][8][3];
+  const int m = blockIdx.x, pb = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = pb * kTCT + threadIdx.x;
+  const int T = p.trunc, kmax = T + 1 - m;
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  const double *llk = p.d_lconst + (T + 1) + m;  // l(l+1)/a^2 of degree m + k
+  double2 ev[7], od[7];
+  tend_row<true>(p, Q, lc, atoms, m, i, ev, od);  // zeros beyond the real pairs
+  double x = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
+  if (i < p.nh) {
+    x = p.d_x[i];
+    const double seed = p.d_seed[(size_t)m * p.nh + i];
+    p0 = seed;
+    p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
+  }
+  const int d = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  const size_t nc = p.ncoef;
+  const int off = col_offset(T, m);
+  for (int k0 = 0; k0 < kmax; k0 += 8) {
+    double2 v[8][3];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = k0 + e;
+      const bool live = k < kmax;
+      const double lk = live ? __ldg(llk + k) : 0.0;
+      // {(l+1) e_l, l e_{l+1}} of degree l (the H coefficients)
+      const double2 c = live ? __ldg(reinterpret_cast<const double2 *>(rc + k) + 1)
+                             : make_double2(0.0, 0.0);
+      const double2 c2 = k + 2 <= kmax ? __ldg(reinterpret_cast<const double2 *>(rc + k + 2))
+                                       : make_double2(0.0, 0.0);
+      const double pv = live ? p0 : 0.0;
+      const double hv = live ? fma(c.x, pm1, -c.y * p1) : 0.0;
+      const double2 *ap = (e & 1) ? od : ev;        // P series: parity of l - m
+      const double2 *ah = (e & 1) ? ev + 4 : od + 4;  // H series: the opposite parity
+      // (vort, div + l(l+1)/a^2 ke, phi'): the kinetic-energy series folded
+      // into div per degree, so three sums leave the thread
+      const double pk = pv * lk;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        double2 t = make_double2(pv * ap[s].x, pv * ap[s].y);
+        if (s == 1) t = make_double2(fma(pk, ap[3].x, t.x), fma(pk, ap[3].y, t.y));
+        v[e][s] = make_double2(fma(hv, ah[s].x, t.x), fma(hv, ah[s].y, t.y));
+      }
+      const double pn = fma(x, p1, -c2.x * p0) * c2.y;
+      pm1 = p0;
+      p0 = p1;
+      p1 = pn;
+    }
+    // transposed butterfly: 8 degrees x 3 sums -> one degree per lane quad
+#pragma unroll
+    for (int w = 4, o = 16; w >= 1; w >>= 1, o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int e = 0; e < w; ++e)
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const double2 snd = up ? v[e][f] : v[e + w][f];
+          const double2 kp = up ? v[e + w][f] : v[e][f];
+          v[e][f] = cadd(kp, shfl_xor2(snd, o));
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      v[0][f] = cadd(v[0][f], shfl_xor2(v[0][f], 2));
+      v[0][f] = cadd(v[0][f], shfl_xor2(v[0][f], 1));
+    }
+    __syncthreads();  // previous chunk's readers are done with red
+    if ((lane & 3) == 0)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) red[warp][d][f] = v[0][f];
+    __syncthreads();
+    if (threadIdx.x < 24) {
+      const int e = threadIdx.x & 7, f = threadIdx.x >> 3;
+      if (k0 + e < kmax) {
+        double2 acc = red[0][e][f];
+#pragma unroll
+        for (int q = 1; q < kTCT / 32; ++q) acc = cadd(acc, red[q][e][f]);
+        part[((size_t)pb * 3 + f) * nc + off + k0 + e] = acc;
+      }
+    }
+  }
+}
+
+// out = (phi' = sum s2, vort = sum s0, div = sum s1) - sub, pair blocks
+// summed in ascending order
+__global__ void analysis_col_tend_reduce(ShtView p, const double2 *part, int npb,
+                                         const double2 *sub, double2 *out) {
+  const size_t s = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nc = p.ncoef;
+  if (s >= nc) return;
+  double2 acc[3];
+#pragma unroll
+  for (int f = 0; f < 3; ++f) acc[f] = part[(size_t)f * nc + s];
+  for (int b = 1; b < npb; ++b)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) acc[f] = cadd(acc[f], part[((size_t)b * 3 + f) * nc + s]);
+  double2 v[3] = {acc[2], acc[0], acc[1]};
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    if (sub) {
+      const double2 b = sub[(size_t)f * nc + s];
+      v[f] = make_double2(v[f].x + b.x * -1.0, v[f].y + b.y * -1.0);
+    }
+    out[(size_t)f * nc + s] = v[f];
+  }
+}
+
 // out[f] = sum over pair blocks of part[pb][f] (ascending pb, fixed order)
 __global__ void analysis_col_reduce(const double2 *part, int npb, int nf, size_t nc, size_t s0,
                                     size_t s1, double2 *out) {
@@ -2633,7 +2757,9 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
       tot += 2LL * ((T + 3 - m) / 2) * p->nt16;
     }
     const double tab_bytes = 8.0 * (double)tot;
-    p->use_tab = tab_bytes <= 4.0e9;
+    // SWX_SHT_TABLE=0: the table-free (on-the-fly recurrence) paths at any T (tests)
+    const char *et = getenv("SWX_SHT_TABLE");
+    p->use_tab = tab_bytes <= 4.0e9 && !(et && atoi(et) == 0);
     if (p->use_tab) {
       std::vector<double> rc16(p->nt16, 0.0);
       for (int i = 0; i < nh; ++i) rc16[i] = rcos[i];
@@ -3376,6 +3502,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     return SWX_OK;
   }
   if ((rc = synth_state(p, state, w, (atoms & SWX_TEND_LC) ? 1 : 0, p->nfreq_t, s))) return rc;
+  if (p->synth_done) SWX_CUDA_TRY(cudaEventRecord(p->synth_done, s));
   mark(1);
   if (atoms & SWX_TEND_N) {
     if ((rc = c2r_exec(p, p->nlon_t, 4, w.c2r, w.grid, s))) return rc;
@@ -3400,7 +3527,22 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     sub = nullptr;
   } else {
     mark(5);  // prep is fused into the analysis kernel
-    if ((rc = launch_analysis<0>(p, w.A, w.Q, w.lc, atoms, out, 3, s))) return rc;
+    // column walk (SWX_ANA_COL=0: the warp-specialised DMMA kernel); the
+    // pair-block partials live in the (now free) synthesis rows area
+    static const int st_col = env_int("SWX_ANA_COL", 1);
+    const int npb = (p->nh + kTCT - 1) / kTCT;
+    const size_t c2r_bytes = 5 * (size_t)p->nlat * std::max(p->nfreq, p->nfreq_t) * sizeof(double2);
+    if (st_col && (size_t)npb * 3 * p->ncoef * sizeof(double2) <= c2r_bytes) {
+      analysis_col_tend_kernel<<<dim3(p->nm, npb), kTCT, 0, s>>>(static_cast<const ShtView &>(*p),
+                                                               w.Q, w.lc, atoms, w.c2r);
+      SWX_LAUNCH_CHECK();
+      analysis_col_tend_reduce<<<(unsigned)((p->ncoef + 255) / 256), 256, 0, s>>>(
+          static_cast<const ShtView &>(*p), w.c2r, npb, sub, out);
+      SWX_LAUNCH_CHECK();
+      sub = nullptr;  // applied by the reduce
+    } else if ((rc = launch_analysis<0>(p, w.A, w.Q, w.lc, atoms, out, 3, s))) {
+      return rc;
+    }
   }
   if (sub) {
     const size_t n = 3 * (size_t)p->ncoef;

@@ -622,3 +622,49 @@ def test_cfg3_mid_case_24_steps_vs_oracle():
     res = integrate(stepper, PrognosticState.from_stack(ic, cfg), case.dt, case.steps * case.dt)
     assert not res.diverged
     assert rel_l2(pack(res.state.stack()), olay.pack(ref)) <= 1e-8
+
+
+@pytest.mark.parametrize("trunc", [42, 85])
+def test_table_free_transforms_and_tendency_vs_oracle(trunc, monkeypatch):
+    """The on-the-fly (table-free) paths that serve T > ~340 -- column-walk
+    plain analysis, state synthesis + cuFFT grid stage + column-walk tendency
+    analysis (with the fused subtraction) -- forced at small T
+    (SWX_SHT_TABLE=0) against the oracle."""
+    from paper_1805_06557_b200.sphere import ShtPlan
+    monkeypatch.setenv("SWX_SHT_TABLE", "0")
+    cfg = SphereConfig.for_truncation(trunc)
+    plan = ShtPlan(cfg)
+    assert not plan.fused_stages()
+    g = osh.grid_for(trunc)
+    st = ost.seeded_balanced_state(g)
+    st[2] = ost.seeded_linear_state(trunc, 9)[2] * 1e-1
+    ref = olay.pack(g.tendency_lc_n(st))
+    dst = to_device(olay.pack(st))
+    out = plan.tendency_dev(3, dst).cpu().numpy()
+    assert rel_linf(out, ref) <= 1e-10
+    sub = to_device(pack(ost.seeded_linear_state(trunc, 6)))
+    got = plan.tendency_dev(3, dst, sub=sub).cpu().numpy()
+    assert rel_linf(got, ref - sub.cpu().numpy()) <= 1e-10
+    c = ost.seeded_linear_state(trunc, 5)[0:1] / 1e3
+    back = plan.analysis_dev(plan.synthesis_dev(to_device(olay.pack(c)))).cpu().numpy()
+    assert rel_linf(back, olay.pack(c)) <= 1e-10
+
+
+def test_etdrk_graph_capture_above_fused_range():
+    """T > 341 (cuFFT grid stage, no fused stages): the ETD2RK step graph
+    captures (psi0 waits on the synthesis event of the non-fused path too) and
+    equals the uncaptured engine bitwise over two steps."""
+    from paper_1805_06557_b200.steppers import EtdrkStepper
+    from paper_1805_06557_b200.workloads import seeded_balanced_state
+    trunc = 383
+    par = params(trunc)
+    ic = seeded_balanced_state(par.cfg)
+    outs = []
+    for graph in (True, False):
+        eng = EtdrkStepper(LG, LC_N, par, RexiSetup(num_poles=128), graph=graph).engine(900.0)
+        assert not eng.plan.fused_stages()
+        eng.load(ic)
+        for _ in range(2):
+            eng.step_dev()
+        outs.append(eng.u.cpu().numpy())
+    assert np.all(np.isfinite(outs[0])) and np.array_equal(outs[0], outs[1])
