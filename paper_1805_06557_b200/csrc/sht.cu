@@ -2759,7 +2759,15 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     const double tab_bytes = 8.0 * (double)tot;
     // SWX_SHT_TABLE=0: the table-free (on-the-fly recurrence) paths at any T (tests)
     const char *et = getenv("SWX_SHT_TABLE");
-    p->use_tab = tab_bytes <= 4.0e9 && !(et && atoi(et) == 0);
+    // the table is streamed by the table analysis (HBM-bound: 12.6 GB at T1279
+    // is ~2 ms, half the column walk's time for the 7-series tendency); its
+    // budget (SWX_SHT_TABLE_GB, default 24 GB) is also capped at a quarter of
+    // the free device memory
+    const char *eg = getenv("SWX_SHT_TABLE_GB");
+    double budget = (eg ? atof(eg) : 24.0) * 1e9;
+    size_t fr = 0, totm = 0;
+    if (cudaMemGetInfo(&fr, &totm) == cudaSuccess) budget = std::min(budget, 0.25 * (double)fr);
+    p->use_tab = tab_bytes <= budget && !(et && atoi(et) == 0);
     if (p->use_tab) {
       std::vector<double> rc16(p->nt16, 0.0);
       for (int i = 0; i < nh; ++i) rc16[i] = rcos[i];
@@ -3248,7 +3256,10 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
     SWX_CUDA_TRY(cudaMemcpyAsync(w.grid, d_grid + (size_t)f0 * p->nlat * p->nlon, gbytes,
                                  cudaMemcpyDeviceToDevice, s));
     if ((rc = r2c_exec(p, p->nlon, nf, w.grid, w.Q, s))) return rc;
-    if (p->use_tab) {
+    // plain fields: the column walk above T ~700 even when the table exists
+    // (one series: 0.56 ms at T1279 against >= 1.9 ms of table streaming)
+    static const int st_colp = env_int("SWX_ANA_COL", 1);
+    if (p->use_tab && !(st_colp && p->trunc > 700 && analysis_col_fits(p))) {
       dim3 g((p->nt16 + 127) / 128, p->nm);
       prep_tab_plain_kernel<<<g, 128, 0, s>>>(static_cast<const ShtView &>(*p), w.Q, nf, w.A);
       SWX_LAUNCH_CHECK();
@@ -4030,8 +4041,8 @@ extern "C" int swx_sht_analysis_shard(swx_sht p, int stage, int n_fields, const 
   int rc = check_ws(p, d_ws, ws_bytes);
   if (rc) return rc;
   if ((rc = check_plain_shard(p, sh, n_fields))) return rc;
-  if (p->use_tab || !analysis_col_fits(p))
-    return fail(SWX_ERR_CONFIG, "sharded analysis is the table-free path (T > ~700)");
+  if (!analysis_col_fits(p))
+    return fail(SWX_ERR_CONFIG, "sharded analysis: partial buffer exceeds the workspace");
   const bool multi = sh->nranks > 1;
   cudaStream_t s = (cudaStream_t)stream;
   ShtWs w = carve(p, d_ws);

@@ -668,3 +668,17 @@ def test_etdrk_graph_capture_above_fused_range():
             eng.step_dev()
         outs.append(eng.u.cpu().numpy())
     assert np.all(np.isfinite(outs[0])) and np.array_equal(outs[0], outs[1])
+
+
+def test_t1279_tendency_table_vs_column_walk(monkeypatch):
+    """At T1279 the tendency analysis streams the 12.6 GB Legendre table
+    (TMA + DMMA); the table-free column walk (validated against the oracle
+    at small T) gives the same tendency to rounding."""
+    from paper_1805_06557_b200.sphere import ShtPlan
+    from paper_1805_06557_b200.workloads import seeded_balanced_state
+    cfg = SphereConfig.for_truncation(1279)
+    st = to_device(pack(seeded_balanced_state(cfg)))
+    a = plan_for(cfg).tendency_dev(3, st)
+    monkeypatch.setenv("SWX_SHT_TABLE", "0")
+    b = ShtPlan(cfg).tendency_dev(3, st)
+    assert float((a - b).abs().max() / b.abs().max()) <= 1e-12
