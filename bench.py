@@ -36,7 +36,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=48)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg3", "cfg4"), default="cfg2")
+    ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg3", "cfg4", "etd1279"),
+                    default="cfg2")
     ap.add_argument("--shard", choices=("auto", "poles", "cols"), default="auto",
                     help="N>1: shard REXI poles (+ all-reduce) or zonal columns (ETD2RK: "
                          "sharded N term, 4 all-to-alls per step); auto = cols for cfg2")
@@ -114,9 +115,13 @@ def run_reference(args, rank, world):
     from paper_1805_06557_b200.workloads import CONFIGS
 
     w = CONFIGS[args.config]
+    if w.trunc > 341 and w.stepper == "lg_rexi_lc_n_etdrk":
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the CPU transforms need dense Legendre tables of ~25 GB each at T1279"}))
+        return
     model = orx.Model(w.trunc, w.phibar)
     nc = olay.ncoef(w.trunc)
-    if args.config == "cfg2":
+    if w.stepper == "lg_rexi_lc_n_etdrk":
         grid = osh.grid_for(w.trunc)
         st = ost.seeded_balanced_state(grid)
         sets = {k: ost.contour_coeffs(k, w.p0, w.p1, w.n_poles) for k in (0, 1, 2)}
@@ -359,7 +364,7 @@ def main():
         run_stiffness(args, rank, world)
         return
     comm = ccomm = None
-    etd = args.config == "cfg2"
+    etd = CONFIGS[args.config].stepper == "lg_rexi_lc_n_etdrk"
     mode = args.shard if args.shard != "auto" else ("cols" if etd else "poles")
     if mode == "cols" and not etd:
         raise SystemExit("--shard cols is the ETD2RK (cfg2) decomposition")
@@ -467,7 +472,9 @@ def main():
         plan = eng.plan
         reps = 5
         # with the fused grid stage, C2R+products+R2C+prep all land in "grid_fused"
-        stage_names = ["synth_state", "fft_c2r", "grid_products", "grid_fused", "prep", "analysis"]
+        stage_names = (["synth_state", "fft_c2r", "grid_products", "grid_fused", "prep", "analysis"]
+                       if plan.fused_stages() else
+                       ["synth_state", "fft_c2r", "grid_products", "fft_r2c", "prep", "analysis"])
         acc = np.zeros(7)
         for _ in range(reps):
             flush.zero_()
@@ -572,7 +579,11 @@ def main():
                     "peak_source": "measured on this GPU by bench.py (swx_fp64_fma_probe, "
                                    "DFMA); MEASURED_PEAKS.json has no FP64 entry",
                     "algorithmic_flops_per_launch": flops[dominant],
-                    "traffic": traffic.get(dominant)}
+                    # per-launch DRAM bytes from profiles/traffic.json: cfg2 keys are
+                    # plain kernel names, other configs carry a _<config> suffix
+                    "traffic": traffic.get(f"{dominant}_{args.config}",
+                                           traffic.get(dominant) if args.config == "cfg2"
+                                           else None)}
     elif dominant is not None:
         ms = breakdown[dominant]["ms_per_launch"]
         roofline = {"kernel": dominant, "bound": "fp64", "achieved": None, "peak": peak64,
@@ -684,7 +695,7 @@ def main():
 
     # ---- CPU baseline: the oracle on this host, bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not (etd and w.trunc > 341):
         from oracle import layout as olay
         from oracle import rexi as orx
         from oracle import sht as osh

@@ -51,6 +51,10 @@ CONFIGS = {
     "cfg2": Workload("cfg2 lg_rexi_lc_n_etdrk T256 N=256", 256, "lg", "lg_rexi_lc_n_etdrk",
                      1800.0, 256, steps=48),
     "cfg4": Workload("cfg4 l_rexi T1279 N=1024", 1279, "l", "l_rexi", 14400.0, 1024),
+    # not a BASELINE config: cfg2's ETD2RK at the north star's largest truncation
+    # (dt = 300 s keeps y = dt sqrt(Phibar T(T+1))/a = 18.9 inside the N = 256 contour)
+    "etd1279": Workload("lg_rexi_lc_n_etdrk T1279 N=256 (cfg2 setup at T1279)", 1279, "lg",
+                        "lg_rexi_lc_n_etdrk", 300.0, 256),
 }
 
 
