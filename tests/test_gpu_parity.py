@@ -682,3 +682,24 @@ def test_t1279_tendency_table_vs_column_walk(monkeypatch):
     monkeypatch.setenv("SWX_SHT_TABLE", "0")
     b = ShtPlan(cfg).tendency_dev(3, st)
     assert float((a - b).abs().max() / b.abs().max()) <= 1e-12
+
+
+def test_integration_md_binding_example(golden_small):
+    """The ctypes binding INTEGRATION.md shows a swerexi maintainer (section 2)
+    runs as written against the library and reproduces the reference's cfg0
+    lg REXI step."""
+    import os
+    import re
+    from paper_1805_06557_b200 import _lib as L
+    from paper_1805_06557_b200.rexi import RexiSetup
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# swerexi/gpu_solver\.py.*?)```", text, re.S).group(1)
+    code = code.replace('ctypes.CDLL("libswx.so")', f'ctypes.CDLL({L.LIB_PATH!r})')
+    ns = {"SolverError": RuntimeError}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    par = params(63)
+    coeffs = RexiSetup().coefficients("psi0", 3600.0)
+    solver = ns["GpuShiftedSolver"]("lg", 3600.0, par)
+    out = solver.rexi_sum(coeffs.alphas, coeffs.betas, unpack(golden_small["cfg0_in"], 63))
+    assert rel_linf(out, golden_small["cfg0_out"]) <= LIN_BAR
