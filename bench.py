@@ -38,9 +38,10 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg3", "cfg4", "etd1279"),
                     default="cfg2")
-    ap.add_argument("--shard", choices=("auto", "poles", "cols"), default="auto",
+    ap.add_argument("--shard", choices=("auto", "poles", "cols", "cols-p2p"), default="auto",
                     help="N>1: shard REXI poles (+ all-reduce) or zonal columns (ETD2RK: "
-                         "sharded N term, 4 all-to-alls per step); auto = cols for cfg2")
+                         "sharded N term, 4 all-to-alls per step; cols-p2p: direct copies "
+                         "into the peers' symmetric-memory workspaces); auto = cols for cfg2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -312,11 +313,11 @@ def column_breakdown(torch, eng, ccomm, flush, reps=5):
         ev[0].record()
         t.stage(0, eng.u, None, None)
         ev[1].record()
-        ccomm.all_to_all(*t.slabs(0))
+        ccomm.exchange(t, 0)
         ev[2].record()
         t.stage(1)
         ev[3].record()
-        ccomm.all_to_all(*t.slabs(1))
+        ccomm.exchange(t, 1)
         ev[4].record()
         t.stage(2, None, eng.nu[0], None)
         ev[5].record()
@@ -366,14 +367,17 @@ def main():
     comm = ccomm = None
     etd = CONFIGS[args.config].stepper == "lg_rexi_lc_n_etdrk"
     mode = args.shard if args.shard != "auto" else ("cols" if etd else "poles")
-    if mode == "cols" and not etd:
+    if mode.startswith("cols") and not etd:
         raise SystemExit("--shard cols is the ETD2RK (cfg2) decomposition")
     # SWX_FORCE_COMM=1 routes a 1-rank run through the multi-rank path (NCCL
     # process group, pole reduce or column exchanges), to exercise it on 1 GPU
     force = os.environ.get("SWX_FORCE_COMM") == "1"
     if world > 1 or force:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        if mode == "cols":
+        if mode == "cols-p2p":
+            from paper_1805_06557_b200.parallel import SymmetricColumnComm
+            ccomm = SymmetricColumnComm()
+        elif mode == "cols":
             ccomm = ColumnComm()
         else:
             comm = PoleComm(deterministic=os.environ.get("SWX_FAST_REDUCE") != "1")
@@ -386,7 +390,8 @@ def main():
     if ccomm is not None:
         stepper = EtdrkStepper(group, LC_N, par, w.setup)
         shard = ColumnShard(par.cfg, rank, world)
-        eng = ColumnEtdrkEngine(group, LC_N, par, w.dt, stepper.coeff_set(w.dt), shard)
+        eng = ColumnEtdrkEngine(group, LC_N, par, w.dt, stepper.coeff_set(w.dt), shard, ccomm)
+        eng.use_graph = os.environ.get("SWX_COL_GRAPH") == "1"
         ic = seeded_balanced_state(par.cfg)
         eng.load(ic)
 
@@ -733,7 +738,7 @@ def main():
         "config": {"workload": w.name, "trunc": w.trunc, "grid": [par.cfg.nlat, par.cfg.nlon],
                    "n_poles": w.n_poles, "dt": w.dt,
                    "units_per_step": units_per_step,
-                   "parallelism": ((f"zonal columns sharded over {world} GPU(s)" if ccomm
+                   "parallelism": ((f"zonal columns sharded over {world} GPU(s) ({mode})" if ccomm
                                     else f"poles sharded over {world} GPU(s)")
                                    if multi else "1 GPU"),
                    "l2": "flushed (256 MB write) before every timed step",

@@ -255,6 +255,14 @@ int swx_sht_synthesis_shard(swx_sht p, int stage, int n_fields, const swx_shard 
 int swx_sht_analysis_shard(swx_sht p, int stage, int n_fields, const swx_shard *sh,
                            const double *d_grid, swx_c128 *d_coeffs, const void *d_recv,
                            void *d_send, void *d_workspace, size_t ws_bytes, void *stream);
+/* Direct exchange over peer memory (alternative to pack -> all-to-all ->
+ * unpack; run the stages with null slabs): copies this rank's blocks of
+ * `exchange` from d_ws into every peer's workspace h_peer_ws[r] (device
+ * addresses valid on this device, e.g. a symmetric-memory rendezvous) at the
+ * same offsets.  Every rank's push must complete (barrier) before stage
+ * exchange + 1 runs anywhere.                                               */
+int swx_sht_shard_push(swx_sht p, const swx_shard *sh, int exchange, int atoms,
+                       const void *d_ws, const uint64_t *h_peer_ws, void *stream);
 /* Restrict the pole sums of an lg solver to columns [m_begin, m_end) (the
  * column shard of the caller's rank; m_end < 0: all).  Slots of other
  * columns in d_out are left unspecified.  SWX_ERR_CONFIG for the Coriolis

@@ -69,6 +69,7 @@ SIGNATURES = {
     "swx_shard_init": (_I, [_P, _I, _I, _I, _I]),
     "swx_sht_shard_counts": (_S, [_P, _P, _I, _I, _P, _P]),
     "swx_sht_tendency_shard": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
+    "swx_sht_shard_push": (_I, [_P, _P, _I, _I, _P, _P, _P]),
     "swx_solver_set_columns": (_I, [_P, _I, _I]),
     "swx_solver_cache_bytes": (_S, [_P]),
     "swx_sht_tendency_part": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _S, _P]),

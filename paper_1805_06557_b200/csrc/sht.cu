@@ -3832,7 +3832,6 @@ extern "C" int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx
   switch (stage) {
     case 0: {
       if (!d_state) return fail(SWX_ERR_CONFIG, "null state");
-      if (multi && !d_send) return fail(SWX_ERR_CONFIG, "null send slab");
       if (m1 > m0) {
         SynthArgs a;
         a.coef = (const double2 *)d_state;
@@ -3853,19 +3852,18 @@ extern "C" int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx
         SWX_LAUNCH_CHECK();
       }
       if (p->synth_done) SWX_CUDA_TRY(cudaEventRecord(p->synth_done, s));
-      return multi ? shard_move(p, w, sh, 0, atoms, 0, (char *)d_send, s) : SWX_OK;
+      // null slabs: the caller moves the blocks itself (swx_sht_shard_push)
+      return multi && d_send ? shard_move(p, w, sh, 0, atoms, 0, (char *)d_send, s) : SWX_OK;
     }
     case 1: {
-      if (multi && (!d_send || !d_recv)) return fail(SWX_ERR_CONFIG, "null exchange slab");
-      if (multi && (rc = shard_move(p, w, sh, 0, atoms, 1, (char *)d_recv, s))) return rc;
+      if (multi && d_recv && (rc = shard_move(p, w, sh, 0, atoms, 1, (char *)d_recv, s))) return rc;
       const int i0 = sh->p_bounds[r], i1 = sh->p_bounds[r + 1];
       if ((rc = launch_grid(p, atoms, w, s, i0, i1 - i0))) return rc;
-      return multi ? shard_move(p, w, sh, 1, atoms, 0, (char *)d_send, s) : SWX_OK;
+      return multi && d_send ? shard_move(p, w, sh, 1, atoms, 0, (char *)d_send, s) : SWX_OK;
     }
     case 2: {
       if (!d_out) return fail(SWX_ERR_CONFIG, "null output");
-      if (multi && !d_recv) return fail(SWX_ERR_CONFIG, "null receive slab");
-      if (multi && (rc = shard_move(p, w, sh, 1, atoms, 1, (char *)d_recv, s))) return rc;
+      if (multi && d_recv && (rc = shard_move(p, w, sh, 1, atoms, 1, (char *)d_recv, s))) return rc;
       if (m1 <= m0) return SWX_OK;
       return launch_analysis_tab<0>(p, w.A, (double2 *)d_out, 3, s, (const double2 *)d_sub,
                                     first_item(p->trunc, m0), first_item(p->trunc, m1));
@@ -4135,3 +4133,31 @@ extern "C" int swx_sht_tendency_part(swx_sht p, int stage, int atoms, int m0, in
 }
 
 extern "C" int swx_sht_has_stages(swx_sht p) { return p && p->fused_grid && p->use_tab ? 1 : 0; }
+
+// Direct exchange over peer memory: this rank's blocks of `exchange` go
+// straight from its workspace into every peer's workspace at the same
+// offsets (copy engines over NVLink / NVSwitch when h_peer_ws holds
+// peer-mapped addresses, e.g. a symmetric-memory rendezvous), replacing
+// pack -> all-to-all -> unpack.  The caller orders it: every rank's push of
+// exchange k completes (a barrier) before any rank runs stage k + 1.
+extern "C" int swx_sht_shard_push(swx_sht p, const swx_shard *sh, int exchange, int atoms,
+                                  const void *d_ws, const uint64_t *h_peer_ws, void *stream) {
+  int rc = check_shard(p, sh);
+  if (rc) return rc;
+  if ((exchange != 0 && exchange != 1) || !d_ws || !h_peer_ws)
+    return fail(SWX_ERR_CONFIG, "bad shard push");
+  if (p->omega == 0.0) atoms &= ~SWX_TEND_LC;
+  cudaStream_t s = (cudaStream_t)stream;
+  ShtWs w = carve(p, nullptr);
+  std::vector<Blk> blks;
+  for (int peer = 0; peer < sh->nranks; ++peer) {
+    if (peer == sh->rank) continue;
+    char *dst = reinterpret_cast<char *>((uintptr_t)h_peer_ws[peer]);
+    if (!dst) return fail(SWX_ERR_CONFIG, "null peer workspace");
+    shard_blocks(p, w, sh, exchange, atoms, sh->rank, peer, blks);
+    for (const Blk &b : blks)
+      SWX_CUDA_TRY(cudaMemcpy2DAsync(dst + b.off, b.pitch, (const char *)d_ws + b.off, b.pitch,
+                                     b.width, b.rows, cudaMemcpyDefault, s));
+  }
+  return SWX_OK;
+}

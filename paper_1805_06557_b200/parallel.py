@@ -313,6 +313,14 @@ class ColumnComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
+    def workspace(self, nbytes: int, device):
+        """The workspace a ShardedTendency of this communicator uses (None: its own)."""
+        return None
+
+    def exchange(self, tend, ex: int, stream=None):
+        """Exchange ``ex`` of a sharded stage pipeline (NCCL all-to-all of the slabs)."""
+        self.all_to_all(*tend.slabs(ex))
+
     def all_to_all(self, send, send_counts, recv, recv_counts):
         """Byte slabs ordered by peer (swx_sht_shard_counts order)."""
         if self.world == 1:  # the self slab never travels
@@ -351,7 +359,7 @@ class ShardedTendency:
     exchange ``ex`` for the caller's all-to-all.
     """
 
-    def __init__(self, plan, shard: ColumnShard, atoms: int):
+    def __init__(self, plan, shard: ColumnShard, atoms: int, workspace=None):
         import ctypes
 
         import torch
@@ -359,7 +367,10 @@ class ShardedTendency:
         self.plan, self.shard, self.atoms = plan, shard, int(atoms)
         lib = self._lib = _lib.lib()
         dev = plan.device
-        self.workspace = torch.empty(plan.workspace.numel(), dtype=torch.uint8, device=dev)
+        # ``workspace``: caller-provided (e.g. symmetric memory for direct pushes)
+        self.workspace = (torch.empty(plan.workspace.numel(), dtype=torch.uint8, device=dev)
+                          if workspace is None else workspace)
+        self.direct = False  # True: stages leave the exchanges to push()
         K = shard.nranks
         self.counts = []
         size = 1
@@ -380,11 +391,22 @@ class ShardedTendency:
     def stage(self, k: int, state=None, out=None, sub=None, stream=None):
         import ctypes
 
+        slabs = (0, 0) if self.direct else (ptr(self.recv), ptr(self.send))
         _lib.check(self._lib.swx_sht_tendency_shard(
             self.plan._h, int(k), self.atoms, ctypes.byref(self.shard.c),
             ptr(state) if state is not None else 0, ptr(sub) if sub is not None else 0,
-            ptr(out) if out is not None else 0, ptr(self.recv), ptr(self.send),
+            ptr(out) if out is not None else 0, *slabs,
             ptr(self.workspace), self.workspace.numel(), stream_ptr(stream)))
+
+    def push(self, ex: int, peer_ws, stream=None):
+        """Direct exchange: this rank's blocks of ``ex`` into every peer's
+        workspace (``peer_ws``: device addresses of the ranks' workspaces)."""
+        import ctypes
+
+        addrs = (ctypes.c_uint64 * self.shard.nranks)(*[int(a) for a in peer_ws])
+        _lib.check(self._lib.swx_sht_shard_push(
+            self.plan._h, ctypes.byref(self.shard.c), int(ex), self.atoms, ptr(self.workspace),
+            addrs, stream_ptr(stream)))
 
     def phases(self, state, out, sub=None, stream=None):
         """Generator: runs the stages, yielding (self, ex) where exchange
@@ -397,7 +419,7 @@ class ShardedTendency:
 
     def run(self, comm: ColumnComm, state, out, sub=None, stream=None):
         for t, ex in self.phases(state, out, sub, stream):
-            comm.all_to_all(*t.slabs(ex))
+            comm.exchange(t, ex, stream)
         return out
 
 
@@ -419,6 +441,41 @@ def virtual_exchange(ranks, ex: int):
             assert n == rcounts_s[r], (r, s, n, rcounts_s[r])
             if n:
                 recv_s[ro:ro + n].copy_(send_r[so:so + n])
+
+
+def virtual_push(ranks, ex: int):
+    """Direct-push exchange between co-resident shards of one device (the
+    peer-memory path's addressing, checked on one GPU)."""
+    addrs = [r.workspace.data_ptr() for r in ranks]
+    for r in ranks:
+        r.push(ex, addrs)
+
+
+class SymmetricColumnComm(ColumnComm):
+    """Column exchanges by direct copies into the peers' workspaces over
+    NVLink (torch symmetric memory: the workspaces are rendezvoused once and
+    every rank writes its blocks straight into the peers' copies, then a
+    device-side barrier), instead of pack -> NCCL all-to-all -> unpack.
+    Opt-in (``bench.py --shard cols-p2p``); the default column path is NCCL."""
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        import torch.distributed._symmetric_memory as symm
+
+        self.symm = symm
+        self.handles = {}
+
+    def workspace(self, nbytes: int, device):
+        """A symmetric workspace of ``nbytes`` (the same size on every rank)."""
+        t = self.symm.empty(nbytes, dtype=__import__("torch").uint8, device=device)
+        h = self.symm.rendezvous(t, self.dist.group.WORLD if self.group is None else self.group)
+        self.handles[t.data_ptr()] = h
+        return t
+
+    def exchange(self, tend, ex: int, stream=None):
+        h = self.handles[tend.workspace.data_ptr()]
+        tend.push(ex, list(h.buffer_ptrs), stream)
+        h.barrier()
 
 
 def run_lockstep(gens, exchange):
@@ -452,7 +509,8 @@ class ColumnEtdrkEngine:
     """
 
     def __init__(self, linear_group: TermGroup, remainder_group: TermGroup,
-                 params: ModelParams, dt: float, coeff_set: dict, shard: ColumnShard):
+                 params: ModelParams, dt: float, coeff_set: dict, shard: ColumnShard,
+                 comm: ColumnComm | None = None):
         import torch
 
         from .sphere import plan_for
@@ -466,7 +524,9 @@ class ColumnEtdrkEngine:
         self.shard = shard
         self.plan = plan_for(params.cfg)
         atoms = atoms_mask(remainder_group)
-        self.tend = ShardedTendency(self.plan, shard, atoms)
+        ws = comm.workspace(self.plan.workspace.numel(), self.plan.device) if comm else None
+        self.tend = ShardedTendency(self.plan, shard, atoms, workspace=ws)
+        self.tend.direct = ws is not None  # peer-memory pushes instead of slabs
         solver = ShiftedLinearSolver(linear_group, dt, params, columns=shard.columns)
         self.rexi = DeviceRexi(solver, coeff_set[0].alphas,
                                {k: coeff_set[k].betas for k in (0, 1, 2)})
@@ -484,8 +544,37 @@ class ColumnEtdrkEngine:
         self.rexi.apply((2,), self.d, self.u[None], stream, base=self.a[None], scale=dt)
 
     def step_dev(self, comm: ColumnComm, stream=None):
+        if getattr(self, "use_graph", False):
+            return self._step_graph(comm)
         for t, ex in self.phases(stream):
-            comm.all_to_all(*t.slabs(ex))
+            comm.exchange(t, ex, stream)
+        return self.u
+
+    def _step_graph(self, comm: ColumnComm):
+        """The step (kernels, slab copies and the exchanges) replayed as one
+        CUDA graph, captured after one eager warm-up step (opt-in:
+        ``use_graph = True`` / SWX_COL_GRAPH=1; NCCL collectives and the
+        symmetric-memory barrier are stream-capturable)."""
+        import torch
+
+        g = getattr(self, "_graph", None)
+        if g is None:
+            s = torch.cuda.Stream()
+            saved = self.u.clone()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                for t, ex in self.phases(s):
+                    comm.exchange(t, ex, s)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            self.u.copy_(saved)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for t, ex in self.phases(s):
+                    comm.exchange(t, ex, s)
+            self._graph = g
+        g.replay()
         return self.u
 
     def load(self, stack: np.ndarray):

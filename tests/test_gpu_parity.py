@@ -703,3 +703,32 @@ def test_integration_md_binding_example(golden_small):
     solver = ns["GpuShiftedSolver"]("lg", 3600.0, par)
     out = solver.rexi_sum(coeffs.alphas, coeffs.betas, unpack(golden_small["cfg0_in"], 63))
     assert rel_linf(out, golden_small["cfg0_out"]) <= LIN_BAR
+
+
+@pytest.mark.parametrize("K", [2, 3])
+def test_column_sharded_tendency_direct_push_bitwise(K):
+    """The peer-memory exchange (swx_sht_shard_push: each rank copies its
+    blocks straight into the peers' workspaces, no slabs, no all-to-all) with
+    co-resident virtual ranks: bitwise equal to the single-rank tendency."""
+    from paper_1805_06557_b200.parallel import (ColumnShard, ShardedTendency, run_lockstep,
+                                                virtual_push)
+    trunc = 256
+    cfg = SphereConfig.for_truncation(trunc)
+    plan = plan_for(cfg)
+    g = osh.grid_for(trunc)
+    st = ost.seeded_balanced_state(g)
+    st[2] = ost.seeded_linear_state(trunc, 9)[2] * 1e-1
+    st = to_device(olay.pack(st))
+    ref = plan.tendency_dev(3, st).cpu().numpy()
+    shards = [ColumnShard(cfg, r, K) for r in range(K)]
+    tends = [ShardedTendency(plan, sh, 3) for sh in shards]
+    for t in tends:
+        t.direct = True
+    outs = [torch.full_like(st, float("nan")) for _ in range(K)]
+    run_lockstep((t.phases(st, o) for t, o in zip(tends, outs)),
+                 lambda items: virtual_push([t for t, _ in items], items[0][1]))
+    full = np.full(ref.shape, np.nan, dtype=ref.dtype)
+    for sh, o in zip(shards, outs):
+        a, b = sh.slots()
+        full[:, a:b] = o[:, a:b].cpu().numpy()
+    assert np.array_equal(full, ref)
