@@ -38,10 +38,12 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("cfg0", "cfg1", "cfg2", "cfg3", "cfg4", "etd1279"),
                     default="cfg2")
-    ap.add_argument("--shard", choices=("auto", "poles", "cols", "cols-p2p"), default="auto",
+    ap.add_argument("--shard", choices=("auto", "poles", "cols", "cols-p2p", "cols-fused"),
+                    default="auto",
                     help="N>1: shard REXI poles (+ all-reduce) or zonal columns (ETD2RK: "
                          "sharded N term, 4 all-to-alls per step; cols-p2p: direct copies "
-                         "into the peers' symmetric-memory workspaces); auto = cols for cfg2")
+                         "into the peers' symmetric-memory workspaces; cols-fused: the stage "
+                         "kernels store into the peers' workspaces); auto = cols for cfg2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -374,7 +376,7 @@ def main():
     force = os.environ.get("SWX_FORCE_COMM") == "1"
     if world > 1 or force:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        if mode == "cols-p2p":
+        if mode in ("cols-p2p", "cols-fused"):
             from paper_1805_06557_b200.parallel import SymmetricColumnComm
             ccomm = SymmetricColumnComm()
         elif mode == "cols":
@@ -392,6 +394,8 @@ def main():
         shard = ColumnShard(par.cfg, rank, world)
         eng = ColumnEtdrkEngine(group, LC_N, par, w.dt, stepper.coeff_set(w.dt), shard, ccomm)
         eng.use_graph = os.environ.get("SWX_COL_GRAPH") == "1"
+        if mode == "cols-fused":
+            ccomm.fuse(eng.tend)
         ic = seeded_balanced_state(par.cfg)
         eng.load(ic)
 

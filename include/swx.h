@@ -263,6 +263,21 @@ int swx_sht_analysis_shard(swx_sht p, int stage, int n_fields, const swx_shard *
  * exchange + 1 runs anywhere.                                               */
 int swx_sht_shard_push(swx_sht p, const swx_shard *sh, int exchange, int atoms,
                        const void *d_ws, const uint64_t *h_peer_ws, void *stream);
+/* Fused exchange: the stages store straight into the owners' workspaces --
+ * the synthesis epilogue writes each latitude pair's Fourier rows into the
+ * pair owner's workspace, the grid stage each column's prepared rows into
+ * the column owner's -- so there is no copy step at all; only a barrier
+ * between the stages.  swx_sht_peer_map_create uploads the owners and the
+ * ranks' workspace addresses (h_peer_ws[r], valid on this device: peer-mapped
+ * symmetric memory, or co-resident workspaces); stages as in
+ * swx_sht_tendency_shard.                                                   */
+int swx_sht_peer_map_create(swx_sht p, const swx_shard *sh, const uint64_t *h_peer_ws,
+                            void **d_map);
+int swx_sht_peer_map_destroy(void *d_map);
+int swx_sht_tendency_shard_peer(swx_sht p, int stage, int atoms, const swx_shard *sh,
+                                const void *d_map, const swx_c128 *d_state,
+                                const swx_c128 *d_sub, swx_c128 *d_out, void *d_workspace,
+                                size_t ws_bytes, void *stream);
 /* Restrict the pole sums of an lg solver to columns [m_begin, m_end) (the
  * column shard of the caller's rank; m_end < 0: all).  Slots of other
  * columns in d_out are left unspecified.  SWX_ERR_CONFIG for the Coriolis

@@ -70,6 +70,9 @@ SIGNATURES = {
     "swx_sht_shard_counts": (_S, [_P, _P, _I, _I, _P, _P]),
     "swx_sht_tendency_shard": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
     "swx_sht_shard_push": (_I, [_P, _P, _I, _I, _P, _P, _P]),
+    "swx_sht_peer_map_create": (_I, [_P, _P, _P, ctypes.POINTER(_P)]),
+    "swx_sht_peer_map_destroy": (_I, [_P]),
+    "swx_sht_tendency_shard_peer": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _S, _P]),
     "swx_solver_set_columns": (_I, [_P, _I, _I]),
     "swx_solver_cache_bytes": (_S, [_P]),
     "swx_sht_tendency_part": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _S, _P]),

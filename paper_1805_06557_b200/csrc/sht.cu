@@ -43,8 +43,27 @@
 #include "swx_common.cuh"
 #include "fft_reg.cuh"
 
+// Peer-store map of the column-sharded tendency (swx_sht_peer_map_create):
+// the workspace base address of every rank (peer-mapped) and the owners of
+// latitude pairs (Fourier rows written by the synthesis) and of columns
+// (prepared rows written by the grid stage).
+struct PeerMap {
+  int n;
+  int pbnd[SWX_MAX_RANKS + 1];  // pair bounds
+  int mbnd[SWX_MAX_RANKS + 1];  // column bounds
+  unsigned long long base[SWX_MAX_RANKS];
+  long long off_c2r, off_lc, off_A;  // byte offsets of the regions in a workspace
+};
+
+__host__ __device__ inline int peer_owner(const int *bnd, int n, int x) {
+  int o = 0;
+  while (o + 1 < n && x >= bnd[o + 1]) ++o;
+  return o;
+}
+
 // POD view passed to kernels by value
 struct ShtView {
+  const PeerMap *pm = nullptr;  // peer stores of the sharded tendency (null: local)
   int trunc = 0, nlat = 0, nlon = 0, nh = 0, nm = 0, nfreq = 0, ncoef = 0;
   int nhp = 0;       // latitude pairs padded to the analysis chunk granularity
   int kc = 0;        // analysis latitude chunk (multiple of 16, <= 256)
@@ -158,6 +177,7 @@ constexpr int kSL = 128;  // l rows staged per chunk
 // from the even/odd partial sums: sp[q] = (vort, div, phi', psi, chi),
 // sh[q] = (dpsi/dlat, dchi/dlat) with q the parity of l - m
 // fr[hemi] = (f, df/dlat) of the pair's two latitudes
+template <bool PEER = false>
 __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a, int m, int i,
                                            int jn, int js, double rcos, const double2 (&sp)[2][5],
                                            const double2 (&sh)[2][2], const double2 (&fr)[2]) {
@@ -211,13 +231,21 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
       const double sc = p.fscale;  // nlon * dlon: fft(irfft(G) * nlon) * dlon
       const double2 l1 = make_double2(sc * (-f * gd.x - fp * v.x), sc * (-f * gd.y - fp * v.y));
       const double2 l2 = make_double2(sc * (f * gz.x - fp * u.x), sc * (f * gz.y - fp * u.y));
-      a.lc[(size_t)j * p.nm + m] = l1;
-      a.lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m] = l2;
+      double2 *lb = a.lc;
+      if (PEER)  // the pair's owner's workspace (peer store)
+        lb = reinterpret_cast<double2 *>(p.pm->base[peer_owner(p.pm->pbnd, p.pm->n, i)] +
+                                         p.pm->off_lc);
+      lb[(size_t)j * p.nm + m] = l1;
+      lb[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m] = l2;
     }
   }
   if (a.zpack) {
     const int T1 = p.trunc + 1;
-    double2 *z = a.c2r + (size_t)i * 8 * T1 + m;
+    double2 *zb = a.c2r;
+    if (PEER)
+      zb = reinterpret_cast<double2 *>(p.pm->base[peer_owner(p.pm->pbnd, p.pm->n, i)] +
+                                       p.pm->off_c2r);
+    double2 *z = zb + (size_t)i * 8 * T1 + m;
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const double2 n = X[0][f], s = X[1][f];
@@ -246,7 +274,7 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
 // d/dlat series -- so fewer loaded coefficients are live at once and the
 // kernel fits two 7-warp CTAs per SM (<= 128 registers); the recurrence is
 // recomputed (3 of 17 FP64 per degree).
-template <int MODE, int SPLIT>
+template <int MODE, int SPLIT, bool PEER = false>
 __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 : 512,
                                   MODE == 0 && SPLIT == 1   ? SWX_SYNTH_MINB
                                   : MODE == 0 && SPLIT == 4 ? 2
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
     trace_mark(1);
     const double2 fr[2] = {make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]),
                            make_double2(p.d_frow[js], p.d_frow[p.nlat + js])};
-    state_rows(p, a, m, i, jn, js, rcos, sp, sh, fr);
+    state_rows<PEER>(p, a, m, i, jn, js, rcos, sp, sh, fr);
     trace_mark(2);
   }
 }
@@ -1134,7 +1162,11 @@ __device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bo
     }
     double2 ev[7], od[7];
     tend_fold<true>(p, F, L1, L2, m, pk, ev, od);
-    double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+    double *Am = A;
+    if (p.pm)  // the column's owner's workspace (peer store)
+      Am = reinterpret_cast<double *>(p.pm->base[peer_owner(p.pm->mbnd, p.pm->n, m)] +
+                                      p.pm->off_A);
+    double *base = Am + (size_t)m * 4 * ps + (size_t)i * kAG;
     put_row_t(base + 0 * ps, ev, 4, i);
     put_row_t(base + 1 * ps, od, 4, i);
     put_row_t(base + 2 * ps, ev + 4, 3, i);
@@ -1146,7 +1178,11 @@ __device__ __forceinline__ void grid_fold(const ShtView &p, int i, int atoms, bo
 __device__ __forceinline__ void grid_zero_rows(const ShtView &p, int i, double *A) {
   const size_t ps = (size_t)p.nt16 * kAG;
   for (int m = threadIdx.x; m <= p.trunc; m += blockDim.x) {
-    double *base = A + (size_t)m * 4 * ps + (size_t)i * kAG;
+    double *Am = A;
+    if (p.pm)
+      Am = reinterpret_cast<double *>(p.pm->base[peer_owner(p.pm->mbnd, p.pm->n, m)] +
+                                      p.pm->off_A);
+    double *base = Am + (size_t)m * 4 * ps + (size_t)i * kAG;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -3845,7 +3881,7 @@ extern "C" int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx
         dim3 g = synth_grid(p, 1, &nt);
         g.x = m1 - m0;
         const size_t smem = synth_smem(5, 2, 1, nt);
-        auto k = synth_kernel<0, 1>;
+        auto k = p->pm ? synth_kernel<0, 1, true> : synth_kernel<0, 1, false>;
         if (smem > 48 * 1024)
           SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
@@ -4160,4 +4196,50 @@ extern "C" int swx_sht_shard_push(swx_sht p, const swx_shard *sh, int exchange, 
                                      b.width, b.rows, cudaMemcpyDefault, s));
   }
   return SWX_OK;
+}
+
+// ---- fused exchange: the sharded stages store straight into the owners'
+// workspaces (peer stores from the synthesis and grid-stage epilogues)
+extern "C" int swx_sht_peer_map_create(swx_sht p, const swx_shard *sh, const uint64_t *h_peer_ws,
+                                       void **d_map) {
+  int rc = check_shard(p, sh);
+  if (rc) return rc;
+  if (!h_peer_ws || !d_map) return fail(SWX_ERR_CONFIG, "null peer table");
+  PeerMap m{};
+  m.n = sh->nranks;
+  for (int r = 0; r <= sh->nranks; ++r) {
+    m.pbnd[r] = sh->p_bounds[r];
+    m.mbnd[r] = sh->m_bounds[r];
+  }
+  for (int r = 0; r < sh->nranks; ++r) {
+    if (!h_peer_ws[r]) return fail(SWX_ERR_CONFIG, "null peer workspace");
+    m.base[r] = h_peer_ws[r];
+  }
+  ShtWs w = carve(p, nullptr);
+  m.off_c2r = (long long)((char *)w.c2r - (char *)nullptr);
+  m.off_lc = (long long)((char *)w.lc - (char *)nullptr);
+  m.off_A = (long long)((char *)w.A - (char *)nullptr);
+  void *d = nullptr;
+  SWX_CUDA_TRY(cudaMalloc(&d, sizeof(PeerMap)));
+  SWX_CUDA_TRY(cudaMemcpy(d, &m, sizeof(PeerMap), cudaMemcpyHostToDevice));
+  *d_map = d;
+  return SWX_OK;
+}
+
+extern "C" int swx_sht_peer_map_destroy(void *d_map) {
+  cudaFree(d_map);
+  return SWX_OK;
+}
+
+extern "C" int swx_sht_tendency_shard_peer(swx_sht p, int stage, int atoms, const swx_shard *sh,
+                                           const void *d_map, const swx_c128 *d_state,
+                                           const swx_c128 *d_sub, swx_c128 *d_out, void *d_ws,
+                                           size_t ws_bytes, void *stream) {
+  if (!p || !d_map) return fail(SWX_ERR_CONFIG, "null plan or peer map");
+  // stages 0 and 1 store into the owners' workspaces; stage 2 reads its own
+  p->pm = stage < 2 ? static_cast<const PeerMap *>(d_map) : nullptr;
+  const int rc = swx_sht_tendency_shard(p, stage, atoms, sh, d_state, d_sub, d_out, nullptr,
+                                        nullptr, d_ws, ws_bytes, stream);
+  p->pm = nullptr;
+  return rc;
 }

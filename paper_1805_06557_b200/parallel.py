@@ -371,6 +371,7 @@ class ShardedTendency:
         self.workspace = (torch.empty(plan.workspace.numel(), dtype=torch.uint8, device=dev)
                           if workspace is None else workspace)
         self.direct = False  # True: stages leave the exchanges to push()
+        self.pmap = None     # device peer map: stages store into the owners' workspaces
         K = shard.nranks
         self.counts = []
         size = 1
@@ -391,12 +392,38 @@ class ShardedTendency:
     def stage(self, k: int, state=None, out=None, sub=None, stream=None):
         import ctypes
 
+        if self.pmap is not None:  # fused: peer stores from the stage epilogues
+            _lib.check(self._lib.swx_sht_tendency_shard_peer(
+                self.plan._h, int(k), self.atoms, ctypes.byref(self.shard.c), self.pmap,
+                ptr(state) if state is not None else 0, ptr(sub) if sub is not None else 0,
+                ptr(out) if out is not None else 0, ptr(self.workspace),
+                self.workspace.numel(), stream_ptr(stream)))
+            return
         slabs = (0, 0) if self.direct else (ptr(self.recv), ptr(self.send))
         _lib.check(self._lib.swx_sht_tendency_shard(
             self.plan._h, int(k), self.atoms, ctypes.byref(self.shard.c),
             ptr(state) if state is not None else 0, ptr(sub) if sub is not None else 0,
             ptr(out) if out is not None else 0, *slabs,
             ptr(self.workspace), self.workspace.numel(), stream_ptr(stream)))
+
+    def use_peer_stores(self, peer_ws):
+        """Fuse the exchanges into the stage epilogues: the kernels store into
+        the owners' workspaces (``peer_ws``: device addresses of every rank's
+        workspace, this rank's included)."""
+        import ctypes
+
+        addrs = (ctypes.c_uint64 * self.shard.nranks)(*[int(a) for a in peer_ws])
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.swx_sht_peer_map_create(self.plan._h, ctypes.byref(self.shard.c),
+                                                     addrs, ctypes.byref(h)))
+        self.pmap = h
+
+    def __del__(self):
+        if getattr(self, "pmap", None) is not None:
+            try:
+                self._lib.swx_sht_peer_map_destroy(self.pmap)
+            except Exception:
+                pass
 
     def push(self, ex: int, peer_ws, stream=None):
         """Direct exchange: this rank's blocks of ``ex`` into every peer's
@@ -474,8 +501,13 @@ class SymmetricColumnComm(ColumnComm):
 
     def exchange(self, tend, ex: int, stream=None):
         h = self.handles[tend.workspace.data_ptr()]
-        tend.push(ex, list(h.buffer_ptrs), stream)
-        h.barrier()
+        if tend.pmap is None:  # copy-engine pushes, then the barrier
+            tend.push(ex, list(h.buffer_ptrs), stream)
+        h.barrier()            # fused peer stores: the barrier alone
+
+    def fuse(self, tend):
+        """Switch a tendency on this communicator's workspace to peer stores."""
+        tend.use_peer_stores(list(self.handles[tend.workspace.data_ptr()].buffer_ptrs))
 
 
 def run_lockstep(gens, exchange):

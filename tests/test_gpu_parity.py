@@ -732,3 +732,33 @@ def test_column_sharded_tendency_direct_push_bitwise(K):
         a, b = sh.slots()
         full[:, a:b] = o[:, a:b].cpu().numpy()
     assert np.array_equal(full, ref)
+
+
+@pytest.mark.parametrize("trunc,K", [(63, 3), (85, 2), (256, 2), (256, 4)])
+def test_column_sharded_tendency_peer_stores_bitwise(trunc, K):
+    """Fused exchange: the synthesis and grid-stage epilogues store straight
+    into the owners' workspaces (virtual ranks' workspaces on one GPU stand in
+    for peer-mapped memory); no copies, only the stage ordering.  Bitwise
+    equal to the single-rank tendency (with and without the subtraction)."""
+    from paper_1805_06557_b200.parallel import ColumnShard, ShardedTendency, run_lockstep
+    cfg = SphereConfig.for_truncation(trunc)
+    plan = plan_for(cfg)
+    g = osh.grid_for(trunc)
+    st = ost.seeded_balanced_state(g)
+    st[2] = ost.seeded_linear_state(trunc, 9)[2] * 1e-1
+    st = to_device(olay.pack(st))
+    sub = to_device(pack(ost.seeded_linear_state(trunc, 6)))
+    for sb in (None, sub):
+        ref = plan.tendency_dev(3, st, sub=sb).cpu().numpy()
+        shards = [ColumnShard(cfg, r, K) for r in range(K)]
+        tends = [ShardedTendency(plan, sh, 3) for sh in shards]
+        addrs = [t.workspace.data_ptr() for t in tends]
+        for t in tends:
+            t.use_peer_stores(addrs)
+        outs = [torch.full_like(st, float("nan")) for _ in range(K)]
+        run_lockstep((t.phases(st, o, sb) for t, o in zip(tends, outs)), lambda items: None)
+        full = np.full(ref.shape, np.nan, dtype=ref.dtype)
+        for sh, o in zip(shards, outs):
+            a, b = sh.slots()
+            full[:, a:b] = o[:, a:b].cpu().numpy()
+        assert np.array_equal(full, ref), (trunc, K, sb is None)
