@@ -666,6 +666,12 @@ constexpr int kFlush = 2 * SWX_LSEG;   // chain elements per reduction flush
 // produce (vort_l, div_l, phi'_l).
 constexpr int kLSeg = SWX_LSEG;  // positions per segment (x 2 chains = kFlush rows)
 static_assert(kLSeg == 4 || kLSeg == 8, "segment length");
+#ifndef SWX_LFLUSH
+#define SWX_LFLUSH 2
+#endif
+constexpr int kFS = SWX_LFLUSH;          // segments per pole reduction (1 or 2)
+constexpr int kFRows = kFlush * kFS;     // reduction rows per flush
+static_assert((kFS == 1 || kFS == 2) && kFRows <= 32, "flush grouping");
 
 template <int NRHS>
 struct LPos {
@@ -866,15 +872,15 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
     const double2 *__restrict__ linv, const LPos<NRHS> *__restrict__ lpos) {
   // reduction buffer: [warp][row][r][comp][32] (dynamic, NRHS * 32 KB)
   extern __shared__ double2 red_raw[];
-  auto red = reinterpret_cast<double2 (*)[kFlush][NRHS][2][32]>(red_raw);
+  auto red = reinterpret_cast<double2 (*)[kFRows][NRHS][2][32]>(red_raw);
   __shared__ LPos<NRHS> pos_s[kLWarps][kLSeg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // cached pivots: per-warp ring of kLRing segment slots filled by bulk copies,
   // each the segment's pivots (kLSegW double2) then its packed positions
   constexpr int PW = (int)(sizeof(LPos<NRHS>) / sizeof(double2));
   constexpr int SLOTW = kLSegW + kLSeg * PW;
-  double2 *ring = red_raw + (size_t)kLWarps * kFlush * NRHS * 2 * 32 + (size_t)warp * kLRing * SLOTW;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(red_raw + (size_t)kLWarps * kFlush * NRHS * 2 * 32 +
+  double2 *ring = red_raw + (size_t)kLWarps * kFRows * NRHS * 2 * 32 + (size_t)warp * kLRing * SLOTW;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(red_raw + (size_t)kLWarps * kFRows * NRHS * 2 * 32 +
                                                 (size_t)kLWarps * kLRing * SLOTW) +
                    warp * kLRing;
   int seq = 0, cons = 0;  // segment blocks issued / consumed by this warp
@@ -1017,6 +1023,7 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
     if constexpr (!CACHED)
       l_fetch<NRHS>(chain, lconst, rhs, ncoef, trunc, m, (nseg - 1) * kLSeg,
                     nl - (nseg - 1) * kLSeg, lane, nxt);
+    int gcnt = 0, gk0a = 0, gna = 0, gk0b = 0, gnb = 0;  // segments waiting for the reduction
     for (int sgi = nseg - 1; sgi >= 0; --sgi) {
       const int k0 = sgi * kLSeg;
       const int n = min(kLSeg, nl - k0);
@@ -1067,7 +1074,7 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const bool isz = ((k + c) & 1) == 0;
-            const int er = (n - 1 - e) * 2 + c;
+            const int er = gcnt * kFlush + (n - 1 - e) * 2 + c;
             const int phys = lane ^ er;
 #pragma unroll
             for (int r = 0; r < NRHS; ++r) {
@@ -1083,16 +1090,29 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
           }
         }
       }
+      // group kFS segments per reduction (the last segment flushes)
+      if (gcnt == 0) {
+        gk0a = k0;
+        gna = n;
+      } else {
+        gk0b = k0;
+        gnb = n;
+      }
+      if (++gcnt < kFS && sgi > 0) continue;
       __syncwarp();
       // lane j reduces row ee = j / LPR over the PR poles PR*q .. PR*q+PR-1,
-      // q = j % LPR (kFlush rows, LPR lanes per row), then LPR-lane butterfly
-      constexpr int LPR = 32 / kFlush, PR = 32 / LPR;
-      const int nrows = 2 * n;
+      // q = j % LPR (kFRows rows, LPR lanes per row), then LPR-lane butterfly;
+      // row ee = slot * kFlush + (n_slot - 1 - pos) * 2 + chain
+      constexpr int LPR = 32 / kFRows, PR = 32 / LPR;
       const int ee = lane / LPR, q = lane % LPR;
-      const int eidx = ee < nrows ? ee : 0;
-      const int epos = n - 1 - (eidx >> 1), ec = eidx & 1;
-      const int kk = k0 + epos;
+      const int slot_e = ee / kFlush, within = ee % kFlush;
+      const int ns = slot_e == 0 ? gna : gnb, k0s = slot_e == 0 ? gk0a : gk0b;
+      const bool valid = slot_e < gcnt && within < 2 * ns;
+      const int eidx = valid ? ee : 0;
+      const int epos = ns - 1 - (within >> 1), ec = within & 1;
+      const int kk = k0s + epos;
       const bool eisz = ((kk + ec) & 1) == 0;
+      gcnt = 0;
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) {
 #pragma unroll
@@ -1107,7 +1127,7 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
           double2 acc = v[0];
 #pragma unroll
           for (int o = 1; o < LPR; o <<= 1) acc = cadd(acc, shfl_xor2(acc, o));
-          if (q == 0 && ee < nrows && (comp == 0 || !eisz)) {
+          if (q == 0 && valid && (comp == 0 || !eisz)) {
             const int field = comp == 1 ? 0 : (eisz ? 1 : 2);
             part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + kk] = acc;
           }
@@ -1473,7 +1493,7 @@ static constexpr int kLgMaxP = 512;  // poles per lg launch (smem = NRHS*64*P by
 
 static size_t l_smem_bytes(int nrhs, bool cached = false) {
   const size_t pos = nrhs == 1 ? sizeof(LPos<1>) : sizeof(LPos<2>);
-  return (size_t)kLWarps * kFlush * nrhs * 2 * 32 * sizeof(double2) +
+  return (size_t)kLWarps * kFRows * nrhs * 2 * 32 * sizeof(double2) +
          (cached ? (size_t)kLWarps * kLRing * (kLSegW * sizeof(double2) + kLSeg * pos) +
                        (size_t)kLWarps * kLRing * sizeof(uint64_t)
                  : 0);
