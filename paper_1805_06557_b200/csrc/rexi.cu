@@ -860,7 +860,7 @@ __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_p
 }
 
 #ifndef SWX_LC_MINB
-#define SWX_LC_MINB 3  // resident CTAs per SM the cached kernel's register budget targets
+#define SWX_LC_MINB 2  // resident CTAs per SM the cached kernel's register budget targets
 #endif
 template <int NRHS, bool CACHED = false>
 __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l_kernel(
