@@ -62,18 +62,21 @@ def rexi_step(group, model: orx.Model, dt, alphas, betas, stack, factors=None):
     return orx.rexi_sum(group, model, dt, alphas, betas, stack, factors)
 
 
-def etdrk2_step(model: orx.Model, grid: osh.Grid, dt: float, coeff_sets, stack):
-    """ETD2RK with lg by REXI and LC_N as the remainder (steppers.py:238-269).
+def etdrk2_step(model: orx.Model, grid: osh.Grid, dt: float, coeff_sets, stack,
+                group: str = "lg", remainder: str = "lc_n", factors=None):
+    """ETD2RK with ``group`` (lg | l) by REXI and ``remainder`` (lc_n | n) as the
+    non-linear part (steppers.py:238-269; tendency_group swe.py:254-279).
 
     ``coeff_sets[k] = (alphas, betas_k)`` for psi_k, k = 0, 1, 2.
     """
     def apply_psi(k, v):
         a, b = coeff_sets[k]
-        return orx.rexi_sum("lg", model, dt, a, b, v)
+        return orx.rexi_sum(group, model, dt, a, b, v, factors)
 
-    nu = grid.tendency_lc_n(stack)
+    rhs = grid.tendency_lc_n if remainder == "lc_n" else grid.tendency_n
+    nu = rhs(stack)
     a = apply_psi(0, stack) + apply_psi(1, nu) * dt
-    na = grid.tendency_lc_n(a)
+    na = rhs(a)
     return a + apply_psi(2, na - nu) * dt
 
 

@@ -762,3 +762,24 @@ def test_column_sharded_tendency_peer_stores_bitwise(trunc, K):
             a, b = sh.slots()
             full[:, a:b] = o[:, a:b].cpu().numpy()
         assert np.array_equal(full, ref), (trunc, K, sb is None)
+
+
+def test_l_rexi_n_etdrk_vs_oracle():
+    """The paper's ETD2RK with the full linear operator L = L_g + L_c by REXI
+    (Coriolis chain solves with the fused ETD2RK epilogues) and N alone as the
+    remainder (build_stepper("l_rexi_n_etdrk")), 3 steps at T42 vs the oracle."""
+    from oracle import stepping as ostep
+    trunc, dt, n = 42, 1200.0, 128
+    par = params(trunc)
+    grid = osh.Grid(trunc)
+    ic = ost.seeded_balanced_state(grid)
+    model = orx.Model(trunc, 1e4 * G)
+    sets = {k: ost.contour_coeffs(k, 10.0, 30.0, n) for k in (0, 1, 2)}
+    fac = orx.LFactors(model, dt)
+    ref = ic
+    for _ in range(3):
+        ref = ostep.etdrk2_step(model, grid, dt, sets, ref, group="l", remainder="n", factors=fac)
+    stepper = build_stepper("l_rexi_n_etdrk", par, RexiSetup(10.0, 30.0, n))
+    res = integrate(stepper, PrognosticState.from_stack(ic, par.cfg), dt, 3 * dt)
+    assert not res.diverged
+    assert rel_l2(pack(res.state.stack()), olay.pack(ref)) <= 1e-10
