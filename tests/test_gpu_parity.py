@@ -783,3 +783,17 @@ def test_l_rexi_n_etdrk_vs_oracle():
     res = integrate(stepper, PrognosticState.from_stack(ic, par.cfg), dt, 3 * dt)
     assert not res.diverged
     assert rel_l2(pack(res.state.stack()), olay.pack(ref)) <= 1e-10
+
+
+def test_twisted_l_chains_opt_in(golden_small, golden_medium, monkeypatch):
+    """The opt-in twisted chain solve (SWX_L_TWIST=1: both ends of every chain
+    eliminated by a warp pair, pivots cached in the twisted layout) against
+    the reference's T42 and cfg1 l steps."""
+    monkeypatch.setenv("SWX_L_TWIST", "1")
+    for trunc, dt, n, src, key in ((42, 3600.0, 128, golden_small, "T42_l128"),
+                                   (128, 7200.0, 256, golden_medium, "cfg1")):
+        par = params(trunc)
+        c = coeffs(n)
+        solver = ShiftedLinearSolver(L, dt, par)  # fresh: warms (and caches) twisted
+        out = solver.rexi_sum(c.alphas, c.betas, unpack(src[key + "_in"], trunc))
+        assert rel_linf(pack(out) if out.ndim == 3 else out, src[key + "_out"]) <= LIN_BAR, key
