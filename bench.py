@@ -553,12 +553,7 @@ def main():
     nlat = par.cfg.nlat
     leg = 4.0 * nlat * nc  # per complex series, no symmetry credit
     import math
-    nlon_t = nlat * 2  # placeholder if the plan is not available
-    try:
-        from paper_1805_06557_b200.sphere import plan_for as _pf
-        nlon_t = int(_tendency_nlon(par.cfg.trunc, par.cfg.nlon))
-    except Exception:
-        pass
+    nlon_t = int(_tendency_nlon(par.cfg.trunc, par.cfg.nlon))
     # fused grid stage: 4 inverse + 5 forward complex FFTs of length nlon_t per
     # latitude pair (5 N log2 N each) + 9 flops per grid point and hemisphere
     grid_flops = (nlat // 2) * (9 * 5.0 * nlon_t * math.log2(nlon_t) + 2 * 9.0 * nlon_t)

@@ -24,7 +24,7 @@ from paper_1805_06557_b200.errors import SolverError  # noqa: E402
 from paper_1805_06557_b200.rexi import RexiSetup, coeffs_for_contour, shifted_contour_from_points  # noqa: E402
 from paper_1805_06557_b200.solvers import ShiftedLinearSolver  # noqa: E402
 from paper_1805_06557_b200.sphere import SphereConfig, plan_for  # noqa: E402
-from paper_1805_06557_b200.steppers import (EtdrkStepper, RexiStepper, build_stepper,  # noqa: E402
+from paper_1805_06557_b200.steppers import (EtdrkStepper, build_stepper,  # noqa: E402
                                             integrate, rexi_step)
 from paper_1805_06557_b200.swe import L, LC_N, LG, ModelParams, PrognosticState  # noqa: E402
 
