@@ -797,3 +797,22 @@ def test_twisted_l_chains_opt_in(golden_small, golden_medium, monkeypatch):
         solver = ShiftedLinearSolver(L, dt, par)  # fresh: warms (and caches) twisted
         out = solver.rexi_sum(c.alphas, c.betas, unpack(src[key + "_in"], trunc))
         assert rel_linf(pack(out) if out.ndim == 3 else out, src[key + "_out"]) <= LIN_BAR, key
+
+
+@pytest.mark.parametrize("trunc", [170, 300, 341])
+def test_fused_stockham_grid_stage_vs_table_free(trunc, monkeypatch):
+    """Truncations whose tendency FFT length has no register-FFT split
+    (Stockham fused grid stage, nlon_t up to 1024) agree with the table-free
+    path (cuFFT grid stage + column-walk analysis) to rounding."""
+    from paper_1805_06557_b200.sphere import ShtPlan
+    from paper_1805_06557_b200.workloads import seeded_balanced_state
+    cfg = SphereConfig.for_truncation(trunc)
+    plan = plan_for(cfg)
+    assert plan.fused_stages()
+    st = seeded_balanced_state(cfg)
+    st[2] = ost.seeded_linear_state(trunc, 9)[2] * 1e-1
+    st = to_device(pack(st))
+    a = plan.tendency_dev(3, st)
+    monkeypatch.setenv("SWX_SHT_TABLE", "0")
+    b = ShtPlan(cfg).tendency_dev(3, st)
+    assert float((a - b).abs().max() / b.abs().max()) <= 1e-12
