@@ -2795,7 +2795,7 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     const double tab_bytes = 8.0 * (double)tot;
     // SWX_SHT_TABLE=0: the table-free (on-the-fly recurrence) paths at any T (tests)
     const char *et = getenv("SWX_SHT_TABLE");
-    // the table is streamed by the table analysis (HBM-bound: 12.6 GB at T1279
+    // the table is streamed by the table analysis (HBM-bound: 6.3 GB at T1279
     // is ~2 ms, half the column walk's time for the 7-series tendency); its
     // budget (SWX_SHT_TABLE_GB, default 24 GB) is also capped at a quarter of
     // the free device memory

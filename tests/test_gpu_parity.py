@@ -671,7 +671,7 @@ def test_etdrk_graph_capture_above_fused_range():
 
 
 def test_t1279_tendency_table_vs_column_walk(monkeypatch):
-    """At T1279 the tendency analysis streams the 12.6 GB Legendre table
+    """At T1279 the tendency analysis streams the 6.3 GB parity-split Legendre table
     (TMA + DMMA); the table-free column walk (validated against the oracle
     at small T) gives the same tendency to rounding."""
     from paper_1805_06557_b200.sphere import ShtPlan
