@@ -3317,6 +3317,8 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
   return SWX_OK;
 }
 
+static int launch_synth_tab(swx_sht p, const SynthArgs &a, ShtWs &w, cudaStream_t s);
+
 static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, int nfreq,
                        cudaStream_t s) {
   int rc = zero_pad(p, w.c2r, 4, nfreq, s);
@@ -3327,6 +3329,11 @@ static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, i
   a.lc = w.lc;
   a.want_lc = want_lc;
   a.nfreq = nfreq;
+  // table synthesis (DMMA over the streamed Legendre table) above truncation
+  // SWX_SYNTH_TAB_BIG (default -1: off; at T1279 the launch is 1.91 -> 1.63 ms
+  // but the ETD2RK step 8.89 -> 9.00 ms: it competes with the overlapped psi0)
+  static const int tab_big = env_int("SWX_SYNTH_TAB_BIG", -1);
+  if (p->use_tab && tab_big >= 0 && p->trunc > tab_big) return launch_synth_tab(p, a, w, s);
   int nt;
   dim3 g = synth_grid(p, 1, &nt);
   return launch_synth<0>(p, g, nt, a, s);
