@@ -423,9 +423,27 @@ def main():
             dr.comm = comm
             dr.range = comm.pole_range(w.n_poles)
 
-        def step():
+        def step_eager():
             dr.apply((0,), u[None], out[None])
             return out
+
+        step = step_eager
+        if comm is None and os.environ.get("SWX_LIN_GRAPH", "1") == "1":
+            # single rank: the step's launches (pole sum, + packing and the tree
+            # combine for the l chains) replayed as one CUDA graph
+            gs = torch.cuda.Stream()
+            gs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(gs):
+                step_eager()  # warm-up: workspaces, schedules
+            torch.cuda.current_stream().wait_stream(gs)
+            torch.cuda.synchronize()
+            lin_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(lin_graph, stream=gs):
+                step_eager()
+
+            def step():
+                lin_graph.replay()
+                return out
         units_per_step = w.n_poles * nc
 
     for _ in range(args.warmup):
@@ -759,7 +777,7 @@ def main():
                                     else f"poles sharded over {world} GPU(s)")
                                    if multi else "1 GPU"),
                    "l2": "flushed (256 MB write) before every timed step",
-                   "cuda_graph": bool(etd and not multi),
+                   "cuda_graph": bool(not multi and (etd or os.environ.get("SWX_LIN_GRAPH", "1") == "1")),
                    **({} if etd else {"warm_s": round(t_warm, 3),
                                       "l_pivot_cache_bytes": _l_cache_bytes(dr)})},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
