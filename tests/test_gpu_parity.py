@@ -816,3 +816,25 @@ def test_fused_stockham_grid_stage_vs_table_free(trunc, monkeypatch):
     monkeypatch.setenv("SWX_SHT_TABLE", "0")
     b = ShtPlan(cfg).tendency_dev(3, st)
     assert float((a - b).abs().max() / b.abs().max()) <= 1e-12
+
+
+def test_cfg4_pole_blocks_combine_bitwise():
+    """cfg4 at full size (T1279, N = 1024, pivot-cached chains): the per-rank
+    partials of K = 2 and 8 contiguous pole blocks, combined by the fixed tree,
+    equal the one-launch sum bitwise (the multi-GPU decomposition's
+    determinism at the size it is meant for)."""
+    trunc = 1279
+    par = params(trunc)
+    c = coeffs(1024)
+    sl = ShiftedLinearSolver(L, 14400.0, par)
+    rhs = to_device(olay.pack(ost.seeded_linear_state(trunc, 0)))[None]
+    bet = to_device(c.betas.reshape(1, -1))
+    full = sl.rexi_sum_dev(c.alphas, bet, rhs).cpu().numpy()
+    lib = _lib.load()
+    for k in (2, 8):
+        parts = torch.stack([sl.rexi_sum_dev(c.alphas, bet, rhs,
+                                             pole_range=(r * 1024 // k, (r + 1) * 1024 // k),
+                                             realify=False) for r in range(k)]).contiguous()
+        out = torch.empty_like(rhs)
+        _lib.check(lib.swx_tree_combine(trunc, 1, k, ptr(parts), 1, ptr(out), stream_ptr()))
+        assert np.array_equal(out.cpu().numpy(), full), k
