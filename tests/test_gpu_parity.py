@@ -838,3 +838,32 @@ def test_cfg4_pole_blocks_combine_bitwise():
         out = torch.empty_like(rhs)
         _lib.check(lib.swx_tree_combine(trunc, 1, k, ptr(parts), 1, ptr(out), stream_ptr()))
         assert np.array_equal(out.cpu().numpy(), full), k
+
+
+def test_l_group_without_rotation_equals_lg():
+    """With Omega = 0 the Coriolis chains decouple: the l pole sum equals the
+    lg one (test_solvers.py:86-98 analogue, 1e-13)."""
+    par = params(42, omega=0.0)
+    c = coeffs(128)
+    st = ost.seeded_linear_state(42, 3)
+    a = ShiftedLinearSolver(L, 1800.0, par).rexi_sum(c.alphas, c.betas, st)
+    b = ShiftedLinearSolver(LG, 1800.0, par).rexi_sum(c.alphas, c.betas, st)
+    assert rel_linf(pack(a), pack(b)) <= 1e-13
+
+
+def test_gravity_eigenmode_rexi_step():
+    """REXI on a gravity eigenmode of one (l, m) returns e^{i omega dt} times
+    the mode (test_steppers.py:208-213 analogue, 1e-10): L_g on (phi', div)
+    is [[0, -Phibar], [kappa_l, 0]] (swe.py:169-185)."""
+    trunc, l, m, dt = 42, 9, 3, 900.0
+    par = params(trunc)
+    phibar = par.mean_geopotential
+    kap = l * (l + 1) / par.cfg.radius_a ** 2
+    omega = np.sqrt(phibar * kap)
+    st = np.zeros((3, trunc + 1, trunc + 1), dtype=np.complex128)
+    st[0, l, m] = phibar       # eigenvector (phi', div) = (Phibar, -i omega) for lambda = i omega
+    st[2, l, m] = -1j * omega
+    c = RexiSetup().coefficients("psi0", dt)
+    out = ShiftedLinearSolver(LG, dt, par).rexi_sum(c.alphas, c.betas, st)
+    want = st * np.exp(1j * omega * dt)
+    assert np.max(np.abs(out - want)) <= 1e-10 * np.max(np.abs(want))
