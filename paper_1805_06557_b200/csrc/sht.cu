@@ -2167,15 +2167,19 @@ __global__ void prep_tab_vortdiv_kernel(ShtView p, const double2 *Q, double *A) 
 // of each parity plane cover the own rows of both parities and the P_{l-1},
 // P_{l+1} neighbours that form H = dP/dlat (sphere.py:102-111).  CTAs are
 // persistent and the ring runs across item boundaries.
-constexpr int kTL = 32;                 // degrees per item
+#ifndef SWX_TAB_TL
+#define SWX_TAB_TL 32
+#endif
+constexpr int kTL = SWX_TAB_TL;         // degrees per item (32 or 64)
+constexpr int kTCW = kTL / 8;           // consumer warps (parity x 8-degree rows)
 constexpr int kTK = 16;                 // latitude pairs per stage
 constexpr int kTS = 4;                  // ring depth
 constexpr int kPR = 20;                 // smem pitch of a staged table row (doubles) = TMA box width
-constexpr int kTBoxRows = 17;           // rows per parity plane per stage
-constexpr int kP1 = 352;                // plane-1 box offset (doubles, 128 B aligned)
-constexpr int kSB = 704;                // prepared-row blocks offset (doubles, 128 B aligned)
+constexpr int kTBoxRows = kTL / 2 + 1;  // rows per parity plane per stage
+constexpr int kP1 = (kTBoxRows * kPR + 15) / 16 * 16;          // plane-1 box offset (doubles, 128 B aligned)
+constexpr int kSB = (kP1 + kTBoxRows * kPR + 15) / 16 * 16;    // prepared-row blocks offset
 constexpr int kStage = kSB + 4 * kTK * kAG;  // doubles per stage (multiple of 16)
-constexpr int kTabThreads = 5 * 32;
+constexpr int kTabThreads = (kTCW + 1) * 32;
 constexpr size_t tab_smem(int kts) {
   return (size_t)kts * kStage * sizeof(double) + 2 * kts * sizeof(uint64_t);
 }
@@ -2241,14 +2245,14 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
   if (threadIdx.x == 0) {
     for (int q = 0; q < kTS; ++q) {
       mbar_init(full + q, 1);
-      mbar_init(empty + q, 4);
+      mbar_init(empty + q, kTCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   pdl_wait();  // the prepared rows come from the preceding kernel
 
-  if (wid == 4) {
+  if (wid == kTCW) {
     // ---------------- producer warp (one lane) ----------------
     // per stage: one 2D box (kPR pairs x 17 rows) from each parity plane --
     // plane 0 rows r0..r0+16, plane 1 rows r0-1..r0+15 (rows outside the
