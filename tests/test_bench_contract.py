@@ -52,3 +52,26 @@ def test_reference_arm_under_torchrun_rank0_only():
     lines = _json_lines(r.stdout)
     assert len(lines) == 1  # rank 1 exits without output
     _check_reference_line(lines[0], 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_our_arm_contract_keys_cfg0():
+    """Our arm's line: the contract keys with values from this run (cfg0 keeps it short)."""
+    r = subprocess.run([sys.executable, "bench.py", "--config", "cfg0", "--steps", "3",
+                        "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["metric"] == "REXI pole-solves*SH-coeffs/s" and d["value"] > 0
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
+    rf = d["roofline"]
+    assert rf["bound"] in ("fp64", "hbm", "tensor") and 0 < rf["frac"] <= 1.2
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+    e2e = d["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert e2e["value"] < d["value"]  # host copies and layout conversion inside
+    assert d["gpu_launches"] >= 1
+    assert "sm_mhz" in d["clocks"]
