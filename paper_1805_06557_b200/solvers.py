@@ -17,6 +17,7 @@ tests and small cases (one fused launch per pole with a one-hot weight).
 from __future__ import annotations
 
 import collections
+import weakref
 import ctypes
 import dataclasses
 import functools
@@ -109,6 +110,7 @@ class ShiftedLinearSolver:
         self._code = _lib.SWX_GROUP_L if group.atoms == L.atoms else _lib.SWX_GROUP_LG
         self._lib = _lib.lib()
         self._sets: collections.OrderedDict = collections.OrderedDict()
+        self._held: dict = {}  # key -> weakref of every live handle (pinned ones outlive the LRU)
         self._ws = {}
         self.columns = None if columns is None else (int(columns[0]), int(columns[1]))
 
@@ -120,8 +122,12 @@ class ShiftedLinearSolver:
         if hit is not None:
             self._sets.move_to_end(key)
             return hit
-        nat = _Native(self._lib, self._code, self.params.cfg, self.dt,
-                      self.params.mean_geopotential, a, stream_ptr(), self.columns)
+        ref = self._held.get(key)
+        nat = ref() if ref is not None else None
+        if nat is None:  # not held by an engine either: build (and guard) it
+            nat = _Native(self._lib, self._code, self.params.cfg, self.dt,
+                          self.params.mean_geopotential, a, stream_ptr(), self.columns)
+            self._held[key] = weakref.ref(nat)
         self._sets[key] = nat
         while len(self._sets) > self._MAX_SETS:
             self._sets.popitem(last=False)
@@ -130,6 +136,13 @@ class ShiftedLinearSolver:
     def warm(self, alphas):
         self._native(alphas)
         return self
+
+    def pin(self, alphas) -> _Native:
+        """The shift set's native handle, for holders whose CUDA graphs capture
+        its device memory (DeviceRexi): while the returned object is referenced
+        the set survives LRU eviction, and later lookups of the same shifts get
+        this handle back instead of a new one."""
+        return self._native(alphas)
 
     def set_columns(self, alphas, m0: int, m1: int):
         """Restrict the following lg pole sums of this shift set to columns

@@ -48,6 +48,17 @@ def rel_linf(x, ref):
     return out
 
 
+def rel_to_scale(x, ref, scale):
+    """Per-field max |x - ref| over the max of ``scale`` (the entrywise sum of
+    |beta_n x_n| of a pole sum), max over fields: the rounding floor of a sum
+    whose terms cancel is relative to its terms, not to the sum."""
+    x, ref, scale = (np.asarray(a) for a in (x, ref, scale))
+    x = x.reshape(x.shape[0], -1)
+    ref = ref.reshape(x.shape)
+    scale = scale.reshape(x.shape)
+    return float(max(np.max(np.abs(a - b)) / np.max(s) for a, b, s in zip(x, ref, scale)))
+
+
 def rel_l2(x, ref):
     x = np.asarray(x).reshape(-1)
     ref = np.asarray(ref).reshape(-1)

@@ -4,7 +4,7 @@
 import numpy as np
 import pytest
 
-from conftest import rel_l2, rel_linf
+from conftest import rel_l2, rel_linf, rel_to_scale
 from oracle import layout, rexi as orx, sht as osh, stepping as ost
 
 G = 9.80616
@@ -129,3 +129,61 @@ def test_cfg1_l_rexi(golden_medium):
     st = layout.unpack(golden_medium["cfg1_in"], 128)
     out = orx.rexi_sum("l", model(128), 7200.0, a, b, st)
     assert rel_linf(layout.pack(out), golden_medium["cfg1_out"]) < 1e-12
+
+
+# ---------------------------------------------------------------- T1279 / T383
+# fixtures from tests/golden/make_golden_large.py (the reference run on the
+# pieces of the large problems it can hold)
+
+def _load(name):
+    import os
+
+    from conftest import GOLDEN
+    return np.load(os.path.join(GOLDEN, name))
+
+
+@pytest.mark.parametrize("m", [640, 1279])
+def test_oracle_cfg4_columns_all_poles(m):
+    """The oracle's band LU + tree over all 1024 cfg4 poles on column m
+    equals the reference's (solvers.py:168-212, steppers.py:157-172)."""
+    gold = _load("l1279.npz")
+    trunc = 1279
+    fac = orx.LFactors(model(trunc), 14400.0)
+    st = ost.seeded_linear_state(trunc, 0)
+    a, b = gold["alphas"], gold["betas"]
+    col = np.ascontiguousarray(st[:, m:, m].T).reshape(-1)
+    terms = []
+    for k in range(a.size):
+        lu, piv = fac.factor(m, a[k])
+        x, info = orx.lapack.zgbtrs(lu, orx.KL, orx.KU, col, piv)
+        assert info == 0
+        fac.cache.clear()
+        terms.append(b[k] * x.reshape(-1, 3).T)
+    for i, k in enumerate(gold["poles"]):  # single solves: no cancellation
+        assert rel_linf(terms[k], gold[f"poles_m{m}"][i]) <= 1e-12
+    got = orx.tree_sum(np.stack(terms))
+    assert rel_to_scale(got, gold[f"sum_m{m}"], gold[f"abs_m{m}"]) <= 1e-13
+
+
+def test_oracle_t1279_legendre_chunks():
+    """Oracle tables on the T1279 latitude chunks reproduce the reference's
+    chunked synthesis rows and analysis columns (sphere.py:72-112, 297-347)."""
+    gold = _load("sht1279.npz")
+    trunc, nlon = 1279, 3840
+    x = gold["x"]
+    xo, wo = osh.gauss_nodes(1920)
+    assert np.array_equal(xo, x) and np.array_equal(wo, gold["w"])
+    spec = ost.seeded_linear_state(trunc, 0)[0]
+    for j0, j1 in gold["chunks"]:
+        P, _ = osh.legendre_tables(trunc, x[j0:j1])
+        P = P[:, : trunc + 1, :]
+        g = np.einsum("jlm,lm->jm", P, spec)
+        half = np.zeros((j1 - j0, nlon // 2 + 1), dtype=np.complex128)
+        half[:, : trunc + 1] = g
+        rows = np.fft.irfft(half, n=nlon, axis=1) * nlon
+        assert rel_linf(rows.ravel(), gold[f"synth_{j0}"].ravel()) <= 1e-12
+        four = np.fft.fft(gold[f"grid_{j0}"], axis=1) * (2 * np.pi / nlon)
+        fw = four[:, : trunc + 1] * gold["w"][j0:j1, None]
+        for m in gold["cols"]:
+            c = np.einsum("jl,j->l", P[:, m:, m], fw[:, m])
+            assert rel_linf(c, gold[f"ana_{j0}_m{m}"]) <= 1e-12
