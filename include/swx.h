@@ -132,6 +132,12 @@ int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,
 int swx_tree_combine(int trunc, int n_states, int n_parts,
                      const swx_c128 *d_parts, int realify, swx_c128 *d_out,
                      void *stream);
+/* d_out[i] = tree_sum(d_parts[p * n_values + i], p < n_parts) for i < n_values,
+ * no realify: the per-slice combine of the tree-order reduce-scatter
+ * (PoleComm, parallel.py:161-169) -- every rank combines its 1/K slice of
+ * all ranks' block partials, then the slices are all-gathered.            */
+int swx_tree_combine_flat(size_t n_values, int n_parts, const swx_c128 *d_parts,
+                          swx_c128 *d_out, void *stream);
 /* d_out = d_x + s * d_y over n_states packed states (PrognosticState
  * __add__/__mul__, swe.py:135-157).  d_out may alias d_x.                    */
 int swx_state_axpy(int trunc, int n_states, const swx_c128 *d_x, double s,

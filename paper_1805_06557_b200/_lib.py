@@ -47,6 +47,7 @@ SIGNATURES = {
     "swx_rexi_sum_prepared_axpy": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P, _D, _P, _P, _S, _P]),
     "swx_apply": (_I, [_P, C128, _P, _P, _P]),
     "swx_tree_combine": (_I, [_I, _I, _I, _P, _I, _P, _P]),
+    "swx_tree_combine_flat": (_I, [_S, _I, _P, _P, _P]),
     "swx_state_axpy": (_I, [_I, _I, _P, _D, _P, _P, _P]),
     "swx_sht_create": (_I, [ctypes.POINTER(_P), _I, _I, _I, _D, _D, _P, _P, _P]),
     "swx_sht_destroy": (_I, [_P]),

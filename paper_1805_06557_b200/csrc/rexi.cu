@@ -2394,6 +2394,16 @@ extern "C" int swx_tree_combine(int trunc, int n_states, int n_parts,
   return SWX_OK;
 }
 
+extern "C" int swx_tree_combine_flat(size_t n_values, int n_parts, const swx_c128 *d_parts,
+                                     swx_c128 *d_out, void *stream) {
+  if (n_parts < 1 || n_parts > (1 << 20)) return fail(SWX_ERR_CONFIG, "bad tree_combine_flat arguments");
+  if (n_values == 0) return SWX_OK;
+  tree_combine_kernel<<<(unsigned)((n_values + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const double2 *)d_parts, n_values, n_parts, 1, 0, 0, Axpy{nullptr, 0.0}, (double2 *)d_out);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
 extern "C" int swx_state_axpy(int trunc, int n_states, const swx_c128 *d_x,
                               double s, const swx_c128 *d_y, swx_c128 *d_out,
                               void *stream) {

@@ -92,52 +92,194 @@ class TimingBreakdown:
         return json.dumps(d, sort_keys=True)
 
 
-class PoleComm:
-    """Rank-level pole sharding over an initialised torch.distributed group."""
+def pole_nodes(n_poles: int, world: int) -> tuple[int, tuple]:
+    """Aligned subtrees of ``tree_sum`` (steppers.py:157-172) dealt to ranks.
 
-    def __init__(self, group=None, deterministic: bool = True):
+    Level h of the reference's pairwise tree (odd tails carried) holds the
+    tree sums of the aligned pole blocks [j 2^h, (j+1) 2^h) clipped to N,
+    and the rest of the reduction is ``tree_sum`` over those nodes.  Ranks
+    get contiguous runs of nodes (``distribute_terms`` over the node count)
+    at the coarsest level whose pole counts are balanced within 12.5 %; a
+    rank sums each of its nodes separately, so the combine over all nodes
+    reproduces the serial tree bit for bit for EVERY N and K.  For
+    power-of-two N and K this is one node per rank, the reference's own
+    contiguous blocks (parallel.py:47-58).  Returns (node size, per-rank
+    tuples of (lo, hi) pole ranges).
+    """
+    if n_poles < 1 or world < 1:
+        raise ConfigurationError("need at least one pole and one rank")
+    if world > n_poles:
+        raise ConfigurationError("more ranks than REXI poles")
+    h = max((n_poles // world).bit_length() - 1, 0)
+    while True:
+        size = 1 << h
+        n_nodes = -(-n_poles // size)
+        assign = distribute_terms(n_nodes, world).assignments
+        ranges = tuple(tuple((j * size, min((j + 1) * size, n_poles)) for j in a) for a in assign)
+        load = max(sum(b - a for a, b in r) for r in ranges)
+        if h == 0 or load <= 1.125 * n_poles / world:
+            return size, ranges
+        h -= 1
+
+
+class _Collectives:
+    """torch.distributed calls on device tensors.  NCCL takes them as they
+    are; with the gloo backend (CPU collectives: the multi-process tests
+    that run every rank on one GPU) the tensors are staged through host
+    memory -- the device kernels around the exchange are the same."""
+
+    def _init_group(self, group):
         import torch.distributed as dist
 
         if not dist.is_initialized():
-            raise ConfigurationError("PoleComm needs an initialised torch.distributed group")
+            raise ConfigurationError(
+                f"{type(self).__name__} needs an initialised torch.distributed group")
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.staged = dist.get_backend(group) == "gloo"
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        """all_to_all_single on flat tensors (element splits)."""
+        if self.staged and inp.is_cuda:
+            o = out.new_empty(out.shape, device="cpu")
+            self.dist.all_to_all_single(o, inp.cpu(), list(out_splits), list(in_splits),
+                                        group=self.group)
+            out.copy_(o)
+        else:
+            self.dist.all_to_all_single(out, inp, list(out_splits), list(in_splits),
+                                        group=self.group)
+
+    def _ag(self, out, inp):
+        """all_gather_into_tensor on flat tensors."""
+        if self.staged and inp.is_cuda:
+            o = out.new_empty(out.shape, device="cpu")
+            self.dist.all_gather_into_tensor(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+        else:
+            self.dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def _ar(self, t):
+        if self.staged and t.is_cuda:
+            c = t.cpu()
+            self.dist.all_reduce(c, group=self.group)
+            t.copy_(c)
+        else:
+            self.dist.all_reduce(t, group=self.group)
+
+
+def torch_view_real(t):
+    """Flat float64 view of a complex128 tensor (collectives move reals)."""
+    import torch
+
+    return torch.view_as_real(t).reshape(-1) if t.is_complex() else t.reshape(-1)
+
+
+class PoleComm(_Collectives):
+    """Rank-level pole sharding over an initialised torch.distributed group.
+
+    Each rank sums its aligned tree nodes (``pole_nodes``) un-realified; the
+    deterministic reduce is a tree-order reduce-scatter: one all-to-all
+    hands rank s the s-th 1/K slice of every node partial, rank s combines
+    its slice over all nodes in tree order on the device
+    (``swx_tree_combine_flat``), one all-gather assembles the slices, and
+    the m = 0 column is realified.  Each rank moves 2 (K-1)/K of a state
+    (per node it owns) instead of the K-1 states of an all-gather of the
+    partials, and the result is bitwise the serial ``tree_sum`` for every
+    K.  ``deterministic=False`` is the reference's fast path: the
+    ``distribute_terms`` blocks and one all-reduce (~1e-13 of the tree).
+    """
+
+    def __init__(self, group=None, deterministic: bool = True):
+        self._init_group(group)
         self.deterministic = deterministic
 
-    def pole_range(self, n_poles: int) -> tuple[int, int]:
-        chunk = distribute_terms(n_poles, self.world).assignments[self.rank]
-        if not chunk:
-            raise ConfigurationError("more ranks than REXI poles")
-        return chunk[0], chunk[-1] + 1
+    def nodes(self, n_poles: int, deterministic: bool | None = None) -> tuple:
+        """This rank's pole ranges: aligned tree nodes (deterministic) or its
+        distribute_terms block."""
+        det = self.deterministic if deterministic is None else deterministic
+        if not det:
+            chunk = distribute_terms(n_poles, self.world).assignments[self.rank]
+            if not chunk:
+                raise ConfigurationError("more ranks than REXI poles")
+            return ((chunk[0], chunk[-1] + 1),)
+        return pole_nodes(n_poles, self.world)[1][self.rank]
 
-    def gather_parts(self, partial):
-        """All-gather of the per-rank partial sums -> (K, *partial.shape)."""
+    def pole_range(self, n_poles: int, deterministic: bool | None = None) -> tuple[int, int]:
+        """Contiguous pole span of this rank (the union of its nodes)."""
+        nd = self.nodes(n_poles, deterministic)
+        return nd[0][0], nd[-1][1]
+
+    # -- the exchange (device-agnostic: tensors of any device) ---------------
+    def scatter_slices(self, parts, n_poles: int):
+        """Reduce-scatter exchange: ``parts`` (M_r, ...) complex node partials
+        of this rank -> (M, S) complex: the rank's slice (S values) of every
+        node partial of every rank, in node (= tree) order."""
         import torch
 
-        flat = partial.contiguous().reshape(-1)
-        parts = torch.empty((self.world * flat.numel(),), dtype=partial.dtype,
-                            device=partial.device)
-        self.dist.all_gather_into_tensor(parts, flat, group=self.group)
-        return parts.view((self.world,) + tuple(partial.shape))
+        counts = [len(r) for r in pole_nodes(n_poles, self.world)[1]]
+        m_r = parts.shape[0]
+        if m_r != counts[self.rank]:
+            raise ConfigurationError("node partials do not match the pole partition")
+        E = parts[0].numel()
+        K = self.world
+        S = -(-E // K)
+        flat = parts.reshape(m_r, E)
+        if E != K * S:
+            pad = torch.zeros((m_r, K * S), dtype=parts.dtype, device=parts.device)
+            pad[:, :E] = flat
+            flat = pad
+        send = flat.view(m_r, K, S).transpose(0, 1).contiguous()  # (K dest, M_r, S)
+        recv = torch.empty((sum(counts), S), dtype=parts.dtype, device=parts.device)
+        self._a2a(torch_view_real(recv), torch_view_real(send),
+                  [2 * c * S for c in counts], [2 * m_r * S] * K)
+        return recv
 
-    def reduce_realify(self, partial, trunc: int, stream=None):
-        """In-place: partial <- realify(reduce over ranks of partial)."""
+    def gather_slices(self, mine, out):
+        """All-gather of the combined slices into ``out`` (E complex values)."""
         import torch
 
-        n_states = partial.numel() // (3 * ncoef(trunc))
+        E = out.numel()
+        S = mine.numel()
+        full = torch.empty(self.world * S, dtype=mine.dtype, device=mine.device)
+        self._ag(torch_view_real(full), torch_view_real(mine))
+        out.view(-1).copy_(full[:E])
+        return out
+
+    # -- device reduce ---------------------------------------------------------
+    def reduce_nodes_realify(self, parts, out, trunc: int, n_poles: int, stream=None,
+                             deterministic: bool | None = None):
+        """out <- realify(tree-order reduce over ranks of the node partials
+        ``parts`` (M_r, n_states, 3, ncoef)); ``out`` may alias parts[0]."""
+        import torch
+
+        det = self.deterministic if deterministic is None else deterministic
+        n_states = out.numel() // (3 * ncoef(trunc))
         lib = _lib.load()
         with torch.cuda.stream(stream) if stream is not None else _null():
-            if self.deterministic:
-                parts = self.gather_parts(partial)
-                _lib.check(lib.swx_tree_combine(trunc, n_states, self.world, ptr(parts), 1,
-                                                ptr(partial), stream_ptr(stream)))
+            if det:
+                recv = self.scatter_slices(parts, n_poles)
+                mine = torch.empty(recv.shape[1], dtype=recv.dtype, device=recv.device)
+                _lib.check(lib.swx_tree_combine_flat(recv.shape[1], recv.shape[0], ptr(recv),
+                                                     ptr(mine), stream_ptr(stream)))
+                self.gather_slices(mine, out)
             else:
-                self.dist.all_reduce(partial, group=self.group)
-                _lib.check(lib.swx_tree_combine(trunc, n_states, 1, ptr(partial), 1,
-                                                ptr(partial), stream_ptr(stream)))
-        return partial
+                if parts.shape[0] != 1:
+                    raise ConfigurationError("the fast reduce takes one block per rank")
+                if out.data_ptr() != parts.data_ptr():
+                    out.copy_(parts[0])
+                self._ar(torch_view_real(out))
+            _lib.check(lib.swx_tree_combine(trunc, n_states, 1, ptr(out), 1, ptr(out),
+                                            stream_ptr(stream)))
+        return out
+
+    def reduce_realify(self, partial, trunc: int, n_poles: int, stream=None,
+                       deterministic: bool | None = None):
+        """In-place: partial <- realify(reduce over ranks of partial), one
+        node per rank."""
+        return self.reduce_nodes_realify(partial[None], partial, trunc, n_poles, stream,
+                                         deterministic)
 
 
 class _null:
@@ -182,13 +324,17 @@ def parallel_rexi_apply(group: TermGroup, state, dt: float, coeffs: RexiCoeffici
 
     t0 = time.perf_counter()
     if comm is not None:
-        lo, hi = comm.pole_range(coeffs.num_terms)
-        out = solver.rexi_sum_dev(coeffs.alphas, betas, rhs, pole_range=(lo, hi), realify=False)
+        nodes = comm.nodes(coeffs.num_terms, deterministic)
+        parts = torch.empty((len(nodes),) + tuple(rhs.shape), dtype=rhs.dtype, device=rhs.device)
+        for j, (lo, hi) in enumerate(nodes):
+            solver.rexi_sum_dev(coeffs.alphas, betas, rhs, parts[j], pole_range=(lo, hi),
+                                realify=False)
         torch.cuda.synchronize()
         t_solves = time.perf_counter() - t0
         t0 = time.perf_counter()
-        comm.deterministic = deterministic
-        comm.reduce_realify(out, cfg.trunc)
+        out = parts[0]
+        comm.reduce_nodes_realify(parts, out, cfg.trunc, coeffs.num_terms,
+                                  deterministic=deterministic)
     elif deterministic:
         out = solver.rexi_sum_dev(coeffs.alphas, betas, rhs, realify=True)
         torch.cuda.synchronize()
@@ -300,18 +446,11 @@ class ColumnShard:
         return column_slots(self.cfg.trunc, self.m_bounds[r], self.m_bounds[r + 1])
 
 
-class ColumnComm:
+class ColumnComm(_Collectives):
     """torch.distributed plumbing of the column shards (NCCL on GPUs)."""
 
     def __init__(self, group=None):
-        import torch.distributed as dist
-
-        if not dist.is_initialized():
-            raise ConfigurationError("ColumnComm needs an initialised torch.distributed group")
-        self.dist = dist
-        self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
+        self._init_group(group)
 
     def workspace(self, nbytes: int, device):
         """The workspace a ShardedTendency of this communicator uses (None: its own)."""
@@ -325,8 +464,7 @@ class ColumnComm:
         """Byte slabs ordered by peer (swx_sht_shard_counts order)."""
         if self.world == 1:  # the self slab never travels
             return
-        self.dist.all_to_all_single(recv[: sum(recv_counts)], send[: sum(send_counts)],
-                                    list(recv_counts), list(send_counts), group=self.group)
+        self._a2a(recv[: sum(recv_counts)], send[: sum(send_counts)], recv_counts, send_counts)
 
     def gather_columns(self, state, shard: ColumnShard):
         """Full packed state(s) on every rank from the ranks' own columns.
@@ -341,7 +479,7 @@ class ColumnComm:
         mine[..., : b - a] = state[..., a:b]
         flat = torch.view_as_real(mine).reshape(-1) if mine.is_complex() else mine.reshape(-1)
         allp = torch.empty((self.world * flat.numel(),), dtype=flat.dtype, device=state.device)
-        self.dist.all_gather_into_tensor(allp, flat, group=self.group)
+        self._ag(allp, flat)
         if mine.is_complex():
             allp = torch.view_as_complex(allp.view(-1, 2))
         allp = allp.view((self.world,) + tuple(mine.shape))

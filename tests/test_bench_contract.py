@@ -38,6 +38,10 @@ def test_reference_arm_one_process():
     lines = _json_lines(r.stdout)
     assert len(lines) == 1
     _check_reference_line(lines[0], 1)
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1805_06557_b200.workloads import CONFIGS
+    assert lines[0]["config"] == json.loads(json.dumps(bench.bench_config(CONFIGS["cfg0"])))
 
 
 @pytest.mark.timeout(900)
@@ -75,3 +79,8 @@ def test_our_arm_contract_keys_cfg0():
     assert e2e["value"] < d["value"]  # host copies and layout conversion inside
     assert d["gpu_launches"] >= 1
     assert "sm_mhz" in d["clocks"]
+    # both arms describe the workload with the identical config dict
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "cfg0",
+                        "--steps", "1", "--warmup", "1"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600)
+    assert _json_lines(r.stdout)[0]["config"] == d["config"]

@@ -867,3 +867,39 @@ def test_gravity_eigenmode_rexi_step():
     out = ShiftedLinearSolver(LG, dt, par).rexi_sum(c.alphas, c.betas, st)
     want = st * np.exp(1j * omega * dt)
     assert np.max(np.abs(out - want)) <= 1e-10 * np.max(np.abs(want))
+
+
+def test_captured_graph_survives_shift_set_eviction(golden_medium):
+    """A captured ETD2RK graph keeps its shift set alive when more than
+    _MAX_SETS other sets pass through the shared get_solver instance."""
+    from paper_1805_06557_b200.solvers import ShiftedLinearSolver, get_solver
+
+    par = params(42)
+    st = PrognosticState.from_stack(unpack(golden_medium["T42etd_ic"], 42), par.cfg)
+    stepper = build_stepper("lg_rexi_lc_n_etdrk", par, RexiSetup(num_poles=128))
+    s1 = pack(stepper.step(st, 1800.0).stack())  # captures the step graph
+    sol = get_solver("lg", 1800.0, par)
+    for k in range(ShiftedLinearSolver._MAX_SETS + 2):
+        sol.warm(coeffs(16 + 4 * k).alphas)
+        torch.zeros(1 << 22, dtype=torch.complex128, device="cuda")  # churn the allocator
+    again = pack(stepper.step(st, 1800.0).stack())
+    assert np.array_equal(again, s1)
+    assert rel_linf(again, golden_medium["T42etd_step1"]) <= 1e-10
+
+
+def test_instrumented_etdrk_step_fills_breakdown(golden_medium):
+    """instrument(collector): the reference's instrumented ETD2RK path
+    (steppers.py:416-443) -- psi_k through parallel_rexi_apply, timed
+    tendencies -- fills every category and gives the same step."""
+    from paper_1805_06557_b200.steppers import TimingCollector
+
+    par = params(42)
+    st = PrognosticState.from_stack(unpack(golden_medium["T42etd_ic"], 42), par.cfg)
+    stepper = build_stepper("lg_rexi_lc_n_etdrk", par, RexiSetup(num_poles=128))
+    col = TimingCollector()
+    stepper.instrument(col, workers=2)
+    s1 = pack(stepper.step(st, 1800.0).stack())
+    assert rel_linf(s1, golden_medium["T42etd_step1"]) <= 1e-10
+    for name in ("overall", "nonlinearities", "rexi_total", "broadcast", "term_solves", "reduce"):
+        assert getattr(col, name) > 0.0, name
+    assert col.nonlinearities < col.overall

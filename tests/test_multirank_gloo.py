@@ -1,6 +1,10 @@
-"""World-size-2 gloo run of the pole-sharded reduce (CPU): each rank sums its
-contiguous pole block (oracle partial), PoleComm all-gathers the partials and
-the fixed tree over blocks reproduces the serial tree_sum bitwise."""
+"""Multi-rank gloo runs on CPU (world size 2 and 3).
+
+Pole shards: each rank sums its aligned tree nodes (oracle partials), the
+real PoleComm exchange (all-to-all of 1/K slices, all-gather of the combined
+slices) moves them, and the tree over nodes -- here the oracle's tree_sum
+standing in for swx_tree_combine_flat -- reproduces the serial tree_sum
+bitwise, for power-of-two and other pole / rank counts."""
 
 import os
 import socket
@@ -26,37 +30,69 @@ def _worker(rank, world, port, result_path):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from oracle import rexi as orx
     from oracle import stepping as ost
-    from paper_1805_06557_b200.parallel import PoleComm
+    from paper_1805_06557_b200.parallel import PoleComm, pole_nodes
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         comm = PoleComm()
-        for group, n in (("lg", 128), ("l", 16)):
+        for group, n in (("lg", 128), ("l", 16), ("lg", 96), ("l", 12)):
             a, b = ost.contour_coeffs(0, 10.0, 30.0, n)
             st = ost.seeded_linear_state(21, seed=4)
             model = orx.Model(21, 1e4 * 9.80616)
-            lo, hi = comm.pole_range(n)
-            assert (lo, hi) == ((0, n // 2) if rank == 0 else (n // 2, n))
-            part = orx.rexi_partial(group, model, 480.0, a, b, st, lo, hi)
-            t = torch.from_numpy(np.ascontiguousarray(part))
-            parts = comm.gather_parts(t).numpy()
-            combined, _ = orx.realify(orx.tree_sum(parts))
-            serial = orx.rexi_sum(group, model, 480.0, a, b, st, chunk=n // 2)
+            nodes = comm.nodes(n)
+            assert nodes == pole_nodes(n, world)[1][rank]
+            if world == 2 and n in (128, 16):  # power of two: the reference's blocks
+                assert nodes == (((0, n // 2),) if rank == 0 else ((n // 2, n),))
+            parts = np.stack([orx.rexi_partial(group, model, 480.0, a, b, st, lo, hi)
+                              for lo, hi in nodes])
+            recv = comm.scatter_slices(torch.from_numpy(parts), n).numpy()
+            mine = torch.from_numpy(np.ascontiguousarray(orx.tree_sum(recv)))
+            out = torch.empty(parts[0].shape, dtype=torch.complex128)
+            comm.gather_slices(mine, out)
+            combined, _ = orx.realify(out.numpy())
+            if group == "l":  # one-shot tree over all n poles (the reference's order)
+                sols = np.stack([orx.LFactors(model, 480.0).solve(x, st) for x in a])
+                serial, _ = orx.realify(orx.tree_sum(b[:, None, None, None] * sols))
+            else:
+                serial = orx.rexi_sum(group, model, 480.0, a, b, st)
             if rank == 0:
-                np.save(result_path + f"_{group}.npy", np.stack([combined, serial]))
+                np.save(result_path + f"_{group}{n}.npy", np.stack([combined, serial]))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_tree_reduce_bitwise(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_pole_tree_reduce_scatter_bitwise(tmp_path, world):
     port = _free_port()
     path = str(tmp_path / "res")
-    mp.spawn(_worker, args=(2, port, path), nprocs=2, join=True)
-    for group in ("lg", "l"):
-        combined, serial = np.load(path + f"_{group}.npy")
-        assert np.array_equal(combined, serial), group
+    mp.spawn(_worker, args=(world, port, path), nprocs=world, join=True)
+    for tag in ("lg128", "l16", "lg96", "l12"):
+        combined, serial = np.load(path + f"_{tag}.npy")
+        assert np.array_equal(combined, serial), tag
+
+
+def test_pole_nodes_partition():
+    """Aligned nodes cover the poles in order; power-of-two N and K give the
+    reference's distribute_terms blocks; loads balanced within 12.5 %."""
+    from paper_1805_06557_b200.parallel import distribute_terms, pole_nodes
+
+    for n in (12, 16, 96, 100, 128, 256, 1000, 1024, 2048):
+        for k in range(1, 9):
+            if k > n:
+                continue
+            size, ranges = pole_nodes(n, k)
+            flat = [r for rr in ranges for r in rr]
+            assert flat[0][0] == 0 and flat[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(flat, flat[1:]))
+            assert all(lo % size == 0 and (hi - lo == size or hi == n) for lo, hi in flat)
+            assert all(len(r) >= 1 for r in ranges)
+            if n & (n - 1) == 0 and k & (k - 1) == 0:
+                blocks = distribute_terms(n, k).assignments
+                assert [((b[0], b[-1] + 1),) for b in blocks] == list(ranges)
+            if size > 1:
+                assert max(sum(h - l for l, h in r) for r in ranges) <= 1.125 * n / k
 
 
 # ------------------------------------------------------------------ column shards
