@@ -547,9 +547,10 @@ def main():
         fused = comm is None  # single rank: the ETD2RK axpys live in the sum epilogues
 
         def local_sum(ks, rhs, out, base=None):
-            b, prep = dr.betas_for(ks)
-            dr.solver.rexi_sum_prepared_dev(dr.alphas, b, prep, rhs, out, dr.range,
-                                            comm is None, None, base, w.dt)
+            b, preps = dr.betas_for(ks)
+            for prep, nd in zip(preps, dr.nodes):  # this rank's tree nodes
+                dr.solver.rexi_sum_prepared_dev(dr.alphas, b, prep, rhs, out, nd,
+                                                comm is None, None, base, w.dt)
         # the step runs three single-RHS prepared sums: psi0(u) (side stream,
         # concurrent with N(u)), psi1(N(u)) and psi2(N(a) - N(u)), the last two
         # with the fused update out = base + dt * sum; warm caches first

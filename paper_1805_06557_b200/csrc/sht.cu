@@ -83,6 +83,8 @@ struct ShtView {
   int2 *d_segs = nullptr;
   int *d_segoff = nullptr;    // [m] index of the first segment of column m
   double *d_ckpt = nullptr;
+  double *d_sck = nullptr;    // [m][quarter c][2][nh]: P at the state synthesis' segment starts
+  double4 *d_wc = nullptr;    // [m][k] (rc layout): {inv_lap_k, c_{k+1}.z inv_lap_{k+1}, c_{k-1}.w inv_lap_{k-1}, 0}
   int n_acta = 0;             // persistent analysis CTAs
   int2 *d_arange = nullptr;   // [cta] contiguous range of work items
   // table path (T small enough): Pbar at the north node of each pair,
@@ -1581,6 +1583,208 @@ __global__ void ckpt_kernel(ShtView p) {
   }
 }
 
+// ---------------------------------------------------------------------
+// State synthesis on the FP64 tensor cores (the default for one block of
+// latitude pairs, T <= 341).  The contraction G[pair][series] = sum_l
+// P_l(pair) C_l[series] is a product with K = degrees; its K dimension is
+// laid out as 4 quarters of the column: at step j, k-slot c of the m8n8k4
+// DMMA is degree s_c + j of quarter c (s_c even, so every k-slot of a step
+// has the parity of j and the even / odd sums of sphere.py's hemisphere
+// fold stay separate accumulators).  Lane (r, c) of a warp runs the
+// reference recurrence (sphere.py:98-100) of latitude pairs r and r + 8 in
+// quarter c, started from plan-time values at s_c (sck_kernel) -- that is
+// the lane's A-fragment element, no table and no redundant walk -- and the
+// 8 complex series of the column (vort, div, phi', psi, chi, and the dP/dlat
+// series of psi, chi summed by parts) are the B fragments, staged once per
+// CTA.  Each coefficient load feeds 16 pairs (two row tiles), against one
+// pair per broadcast load in synth_kernel (shared-memory bound at ~1/4 of
+// the FP64 rate).  CTA = (column, half of the latitude pairs), longest
+// columns first.
+// ---------------------------------------------------------------------
+__host__ __device__ inline int syn_seg_start(int kmax, int c) {
+  return c >= 4 ? kmax + 1 : ((c * (kmax + 1)) / 4) & ~1;
+}
+
+// plan time: P_{s_c} and P_{s_c + 1} of every column, quarter and pair
+__global__ void sck_kernel(ShtView p) {
+  const int m = blockIdx.x;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= p.nh) return;
+  const int T = p.trunc, kmax = T + 1 - m;
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  const double x = p.d_x[i];
+  const double seed = p.d_seed[(size_t)m * p.nh + i];
+  double p0 = seed, p1 = kmax >= 1 ? sqrt(2.0 * m + 3.0) * x * seed : 0.0;
+  double *ck = p.d_sck + (size_t)m * 8 * p.nh;
+  int c = 0;
+  for (int k = 0; k <= kmax && c < 4; ++k) {
+    while (c < 4 && syn_seg_start(kmax, c) == k) {
+      ck[(size_t)(c * 2) * p.nh + i] = p0;
+      ck[(size_t)(c * 2 + 1) * p.nh + i] = p1;
+      ++c;
+    }
+    double p2 = 0.0;
+    if (k + 2 <= kmax) {
+      const double4 c2 = rc[k + 2];
+      p2 = fma(x, p1, -c2.x * p0) * c2.y;  // identical to the walkers
+    }
+    p0 = p1;
+    p1 = p2;
+  }
+}
+
+// CTA = (column, one half of the latitude pairs), longest columns first.
+template <bool PEER = false>
+__global__ void __launch_bounds__(256, 2) synth_mma_kernel(ShtView p, SynthArgs a, int m_first,
+                                                           int wpb, int lmax) {
+  extern __shared__ __align__(16) double smem_syn[];
+  const int m = m_first + (blockIdx.x >> 1), blk = blockIdx.x & 1;
+  const int T = p.trunc, nc = p.ncoef, nh = p.nh, kmax = T + 1 - m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane & 3, r = lane >> 2;
+  const int SS = lmax * 16 + 8;  // doubles per staged quarter (odd multiple of 8: conflict-free B)
+  const int RS = lmax + 2;
+  double *Cs = smem_syn;                                          // [4][SS]
+  double2 *Rc = reinterpret_cast<double2 *>(smem_syn + 4 * SS);  // [4][RS]
+  pdl_trigger();
+  trace_mark(0);
+  int L = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) L = max(L, syn_seg_start(kmax, q + 1) - syn_seg_start(kmax, q));
+  L = (L + 1) & ~1;
+  // plan data first (PDL prologue): the lane's pairs, quarter start values,
+  // recurrence constants and the epilogue's per-pair data
+  const int pbase = (blk * wpb + warp) * 16;
+  const int iA = pbase + r, iB = pbase + 8 + r, ie = pbase + lane;
+  const bool wact = pbase < nh;
+  const bool eact = wact && lane < 16 && ie < nh;  // epilogue thread of pair ie
+  double xA = 0.0, xB = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  const double *ck = p.d_sck + ((size_t)m * 8 + c * 2) * nh;
+  if (iA < nh) {
+    xA = p.d_x[iA];
+    a0 = ck[iA];
+    a1 = ck[nh + iA];
+  }
+  if (iB < nh) {
+    xB = p.d_x[iB];
+    b0 = ck[iB];
+    b1 = ck[nh + iB];
+  }
+  int jn = 0, js = 0;
+  double rcos = 0.0;
+  double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  if (eact) {
+    jn = p.d_jn[ie];
+    js = p.d_js[ie];
+    rcos = p.d_rcos[ie];
+    fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
+    fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
+  }
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  for (int t = threadIdx.x; t < 4 * RS; t += blockDim.x) {
+    const int q = t / RS, u = t - q * RS;
+    const int sq = syn_seg_start(kmax, q), n = syn_seg_start(kmax, q + 1) - sq;
+    const int k = sq + u;
+    double4 cc = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (u < n + 2 && k <= kmax) cc = rc[k];
+    Rc[t] = make_double2(cc.x, cc.y);
+  }
+  pdl_wait();  // the coefficients come from the preceding kernel
+  trace_mark(1);
+  const int off = col_offset(T, m);
+  const double4 *wcm = p.d_wc + rc_offset(T, m);
+  for (int t = threadIdx.x; t < 4 * L; t += blockDim.x) {
+    const int q = t / L, u = t - q * L;
+    const int sq = syn_seg_start(kmax, q), eq = syn_seg_start(kmax, q + 1);
+    const int k = sq + u, sl = off + k;
+    const bool on = k < eq;  // degree in the quarter (k <= kmax)
+    const bool in = on && k < kmax;
+    const bool up = on && k + 1 < kmax, dn = on && k >= 1;
+    const double4 cw = on ? wcm[k] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const double2 zero = make_double2(0.0, 0.0);
+    const double2 z = in ? a.coef[nc + sl] : zero, d = in ? a.coef[2 * nc + sl] : zero;
+    const double2 ph = in ? a.coef[sl] : zero;
+    const double2 zp = up ? a.coef[nc + sl + 1] : zero, dp = up ? a.coef[2 * nc + sl + 1] : zero;
+    const double2 zm = dn ? a.coef[nc + sl - 1] : zero, dm = dn ? a.coef[2 * nc + sl - 1] : zero;
+    // dP/dlat series of psi, chi summed by parts (see synth_kernel)
+    double2 wz = make_double2(cw.y * zp.x, cw.y * zp.y), wd = make_double2(cw.y * dp.x, cw.y * dp.y);
+    wz = make_double2(wz.x - cw.z * zm.x, wz.y - cw.z * zm.y);
+    wd = make_double2(wd.x - cw.z * dm.x, wd.y - cw.z * dm.y);
+    double2 *row = reinterpret_cast<double2 *>(Cs + (size_t)q * SS + (size_t)u * 16);
+    row[0] = z;
+    row[1] = d;
+    row[2] = ph;
+    row[3] = make_double2(z.x * cw.x, z.y * cw.x);  // psi = inv_lap(vort)
+    row[4] = make_double2(d.x * cw.x, d.y * cw.x);  // chi = inv_lap(div)
+    row[5] = wz;
+    row[6] = wd;
+    row[7] = zero;
+  }
+  __syncthreads();
+  trace_mark(2);
+  // D[parity][row tile][col tile][2]
+  double D[2][2][2][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) D[q][u][v][0] = D[q][u][v][1] = 0.0;
+  if (wact) {
+    const double *cq = Cs + (size_t)c * SS + r;  // B[k = c][n = r]
+    const double2 *rq = Rc + c * RS;
+#pragma unroll 1
+    for (int j = 0; j < L; j += 2) {
+      double t0 = cq[j * 16], t1 = cq[j * 16 + 8];
+      dmma(D[0][0][0][0], D[0][0][0][1], a0, t0);
+      dmma(D[0][0][1][0], D[0][0][1][1], a0, t1);
+      dmma(D[0][1][0][0], D[0][1][0][1], b0, t0);
+      dmma(D[0][1][1][0], D[0][1][1][1], b0, t1);
+      t0 = cq[j * 16 + 16];
+      t1 = cq[j * 16 + 24];
+      dmma(D[1][0][0][0], D[1][0][0][1], a1, t0);
+      dmma(D[1][0][1][0], D[1][0][1][1], a1, t1);
+      dmma(D[1][1][0][0], D[1][1][0][1], b1, t0);
+      dmma(D[1][1][1][0], D[1][1][1][1], b1, t1);
+      const double2 r2 = rq[j + 2], r3 = rq[j + 3];
+      const double a2 = fma(xA, a1, -r2.x * a0) * r2.y;  // sphere.py:98-100
+      const double b2 = fma(xB, b1, -r2.x * b0) * r2.y;
+      const double a3 = fma(xA, a2, -r3.x * a1) * r3.y;
+      const double b3 = fma(xB, b2, -r3.x * b1) * r3.y;
+      a0 = a2;
+      a1 = a3;
+      b0 = b2;
+      b1 = b3;
+    }
+  }
+  __syncthreads();  // staging area free: per-warp gather of the pairs' sums
+  trace_mark(3);
+  double2 *E = reinterpret_cast<double2 *>(smem_syn) + (size_t)warp * 256;  // [16 pairs][2][8]
+  if (wact) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+          E[(u * 8 + r) * 16 + q * 8 + v * 4 + c] = make_double2(D[q][u][v][0], D[q][u][v][1]);
+  }
+  __syncwarp();
+  if (!eact) return;
+  const double2 *e = E + lane * 16;
+  double2 sp[2][5], sh[2][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) sp[q][k] = e[q * 8 + k];
+    // the dP/dlat series of parity-q degrees belong to H parity 1 - q
+    sh[1 - q][0] = make_double2(e[q * 8 + 5].x * rcos, e[q * 8 + 5].y * rcos);
+    sh[1 - q][1] = make_double2(e[q * 8 + 6].x * rcos, e[q * 8 + 6].y * rcos);
+  }
+  state_rows<PEER>(p, a, m, ie, jn, js, rcos, sp, sh, fr);
+  if (lane == 0 && warp == 0) trace_mark(4);
+}
+
 // Persistent, warp-specialised analysis.  One CTA per SM walks a contiguous,
 // cost-balanced range of (m, segment) work items (sorted by m, so the
 // prepared rows of a column are built once per CTA and column).  Per item,
@@ -2690,6 +2894,20 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     lc[l] = l ? -(radius * radius) / ll1 : 0.0;  // sphere.py:362-363
     lc[T + 1 + l] = ll1 / (radius * radius);       // -laplacian eigenvalue
   }
+  // per-degree constants of the state synthesis' staged series (the products
+  // synth_kernel forms at staging time, once at plan time)
+  std::vector<double4> wc(nrc);
+  for (int m = 0; m <= T; ++m) {
+    const int kmax = T + 1 - m;
+    for (int k = 0; k <= kmax; ++k) {
+      const double4 *r = rc.data() + rc_offset(T, m);
+      double4 c = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (k < kmax) c.x = lc[m + k];
+      if (k + 1 < kmax) c.y = r[k + 1].z * lc[m + k + 1];
+      if (k >= 1 && k - 1 < kmax) c.z = r[k - 1].w * lc[m + k - 1];
+      wc[rc_offset(T, m) + k] = c;
+    }
+  }
   std::vector<double> frow(2 * nlat);
   for (int j = 0; j < nlat; ++j) {
     const double s = h_sinlat[j];
@@ -2710,6 +2928,7 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
   up((void **)&p->d_ws, ws.data(), sizeof(double) * nh);
   up((void **)&p->d_seed, seed.data(), sizeof(double) * seed.size());
   up((void **)&p->d_rc, rc.data(), sizeof(double4) * rc.size());
+  up((void **)&p->d_wc, wc.data(), sizeof(double4) * wc.size());
   up((void **)&p->d_lconst, lc.data(), sizeof(double) * lc.size());
   up((void **)&p->d_frow, frow.data(), sizeof(double) * frow.size());
   if (e != cudaSuccess) {
@@ -2752,8 +2971,12 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
   up((void **)&p->d_segoff, segoff.data(), sizeof(int) * segoff.size());
   up((void **)&p->d_segs, segs.data(), sizeof(int2) * segs.size());
   if (e == cudaSuccess) e = cudaMalloc(&p->d_ckpt, sizeof(double) * 3 * (size_t)nh * segs.size());
+  if (e == cudaSuccess && nh <= 256)
+    e = cudaMalloc(&p->d_sck, sizeof(double) * 8 * (size_t)nh * (T + 1));
   if (e == cudaSuccess) {
     ckpt_kernel<<<dim3(T + 1, (nh + 127) / 128), 128>>>(static_cast<const ShtView &>(*p));
+    if (p->d_sck)
+      sck_kernel<<<dim3(T + 1, (nh + 127) / 128), 128>>>(static_cast<const ShtView &>(*p));
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
@@ -2903,6 +3126,8 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_segs);
   cudaFree(p->d_segoff);
   cudaFree(p->d_ckpt);
+  cudaFree(p->d_sck);
+  cudaFree(p->d_wc);
   cudaFree(p->d_arange);
   cudaFree(p->d_ptoff);
   cudaFree(p->d_ptab);
@@ -3323,6 +3548,37 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
 
 static int launch_synth_tab(swx_sht p, const SynthArgs &a, ShtWs &w, cudaStream_t s);
 
+// state synthesis of columns [m0, m1) (MODE 0): the DMMA kernel for one
+// block of latitude pairs (T <= 341), the recurrence kernel otherwise
+static int launch_state_synth(swx_sht p, const SynthArgs &a0, int m0, int m1, bool peer,
+                              cudaStream_t s) {
+  int nt;
+  dim3 g = synth_grid(p, 1, &nt);
+  if (p->d_sck) {
+    const int wpb = (((p->nh + 15) / 16) + 1) / 2;  // warps per CTA: half the pairs
+    const int lmax = ((p->trunc + 2) / 4 + 2 + 1) & ~1;  // longest quarter, even
+    const size_t stage = (size_t)(4 * (lmax * 16 + 8) + 8 * (lmax + 2)) * sizeof(double);
+    const size_t smem = std::max(stage, (size_t)wpb * 256 * sizeof(double2));
+    auto k = peer ? synth_mma_kernel<true> : synth_mma_kernel<false>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SWX_CUDA_TRY(launch_pdl(k, dim3(2 * (m1 - m0)), dim3(32 * wpb), smem, s,
+                            static_cast<const ShtView &>(*p), a0, m0, wpb, lmax));
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
+  SynthArgs a = a0;
+  a.m0 = m0;
+  g.x = m1 - m0;
+  const size_t smem = synth_smem(5, 2, 1, nt);
+  auto k = peer ? synth_kernel<0, 1, true> : synth_kernel<0, 1, false>;
+  if (smem > 48 * 1024)
+    SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
 static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, int nfreq,
                        cudaStream_t s) {
   int rc = zero_pad(p, w.c2r, 4, nfreq, s);
@@ -3338,9 +3594,7 @@ static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, i
   // but the ETD2RK step 8.89 -> 9.00 ms: it competes with the overlapped psi0)
   static const int tab_big = env_int("SWX_SYNTH_TAB_BIG", -1);
   if (p->use_tab && tab_big >= 0 && p->trunc > tab_big) return launch_synth_tab(p, a, w, s);
-  int nt;
-  dim3 g = synth_grid(p, 1, &nt);
-  return launch_synth<0>(p, g, nt, a, s);
+  return launch_state_synth(p, a, 0, p->trunc + 1, false, s);
 }
 
 extern "C" int swx_sht_uv(swx_sht p, const swx_c128 *d_vort, const swx_c128 *d_div,
@@ -3543,10 +3797,8 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     static const int st_tab = env_int("SWX_SYNTH_TAB", 0);
     if (st_tab) {
       if ((rc = launch_synth_tab(p, a, w, s))) return rc;
-    } else {
-      int nt;
-      dim3 g = synth_grid(p, 1, &nt);
-      if ((rc = launch_synth<0>(p, g, nt, a, s))) return rc;
+    } else if ((rc = launch_state_synth(p, a, 0, p->trunc + 1, false, s))) {
+      return rc;
     }
     if (p->synth_done) SWX_CUDA_TRY(cudaEventRecord(p->synth_done, s));
     mark(1);
@@ -3887,16 +4139,7 @@ extern "C" int swx_sht_tendency_shard(swx_sht p, int stage, int atoms, const swx
         a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
         a.nfreq = p->nfreq_t;
         a.zpack = 1;
-        a.m0 = m0;
-        int nt;
-        dim3 g = synth_grid(p, 1, &nt);
-        g.x = m1 - m0;
-        const size_t smem = synth_smem(5, 2, 1, nt);
-        auto k = p->pm ? synth_kernel<0, 1, true> : synth_kernel<0, 1, false>;
-        if (smem > 48 * 1024)
-          SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
-        SWX_LAUNCH_CHECK();
+        if ((rc = launch_state_synth(p, a, m0, m1, p->pm != nullptr, s))) return rc;
       }
       if (p->synth_done) SWX_CUDA_TRY(cudaEventRecord(p->synth_done, s));
       // null slabs: the caller moves the blocks itself (swx_sht_shard_push)
@@ -4155,17 +4398,7 @@ extern "C" int swx_sht_tendency_part(swx_sht p, int stage, int atoms, int m0, in
       a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
       a.nfreq = p->nfreq_t;
       a.zpack = 1;
-      a.m0 = m0;
-      int nt;
-      dim3 g = synth_grid(p, 1, &nt);
-      g.x = m1 - m0;
-      const size_t smem = synth_smem(5, 2, 1, nt);
-      auto k = synth_kernel<0, 1>;
-      if (smem > 48 * 1024)
-        SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
-      SWX_LAUNCH_CHECK();
-      return SWX_OK;
+      return launch_state_synth(p, a, m0, m1, false, s);
     }
     case 1:
       return launch_grid(p, atoms, w, s);
