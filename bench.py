@@ -459,6 +459,16 @@ def main():
     torch.cuda.synchronize()
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    if os.environ.get("SWX_TRACE_OUT"):  # per-CTA phase marks of one step (trace build only)
+        tlib = _lib.load()
+        flush.zero_()
+        torch.cuda.synchronize()
+        tlib.swx_trace(1, None, 0)
+        step()
+        torch.cuda.synchronize()
+        tbuf = np.zeros((4096, 8), dtype=np.uint64)
+        tlib.swx_trace(0, tbuf.ctypes.data, 4096)
+        np.save(os.environ["SWX_TRACE_OUT"], tbuf)
     sampler = ClockSampler(local)
     sampler.start()
     t_soak = time.perf_counter()

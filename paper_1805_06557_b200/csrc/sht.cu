@@ -1785,6 +1785,500 @@ __global__ void __launch_bounds__(256, 2) synth_mma_kernel(ShtView p, SynthArgs 
   if (lane == 0 && warp == 0) trace_mark(4);
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void *ptr) {
+  return (unsigned)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SWX_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra SWX_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double *dst, const double *src, unsigned bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_2d(double *dst, const CUtensorMap *map, int c0, int c1,
+                                       uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Persistent form of synth_mma_kernel: gridDim.x CTAs (two per SM) walk the
+// (column, pair block) items in a static snake order over the longest-first
+// item list (CTA b: items b, 2G-1-b, 2G+b, ...), which balances the column
+// lengths per CTA.  A column's raw inputs (the three coefficient runs, the
+// dP/dlat weights and the recurrence constants: 5 contiguous runs) arrive by
+// bulk copy into a staging buffer while the previous item's DMMA loop runs;
+// the derived B rows are built from shared memory.  Identical arithmetic to
+// synth_mma_kernel, so the results are bitwise equal.
+__device__ __forceinline__ void bulk_g2s_v(void *dst, const void *src, unsigned bytes,
+                                           uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kEP = 17;  // per-pair stride (double2) of the epilogue gather: conflict-free
+// row stride (double2) of the staged recurrence constants: = 2 mod 4, so the
+// four quarters' broadcast loads fall in distinct bank groups
+__host__ __device__ inline int syn_rs(int lmax) { return (lmax + 2) % 4 ? lmax + 2 : lmax + 4; }
+
+template <bool PEER = false>
+__global__ void __launch_bounds__(256, 2) synth_mma_pers_kernel(ShtView p, SynthArgs a,
+                                                                int m_first, int nitems, int wpb,
+                                                                int lmax) {
+  extern __shared__ __align__(128) double smem_syn[];
+  const int T = p.trunc, nc = p.ncoef, nh = p.nh, T1 = T + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane & 3, r = lane >> 2;
+  const int SS = lmax * 16 + 8;  // doubles per staged quarter (odd multiple of 8: conflict-free B)
+  const int RS = syn_rs(lmax);
+  const int TR = (T1 + 2) & ~1;  // raw run capacity (double2), keeps 32-byte alignment
+  double *Cs = smem_syn;                                            // [4][SS]
+  double2 *Rc = reinterpret_cast<double2 *>(smem_syn + 4 * SS);    // [4][RS]
+  double2 *Rw = Rc + 4 * RS;                                        // [3][TR] phi', vort, div
+  double4 *Rwc = reinterpret_cast<double4 *>(Rw + 3 * TR);         // [TR] dP/dlat weights
+  double4 *Rrc = Rwc + TR;                                          // [TR] recurrence constants
+  double2 *E = reinterpret_cast<double2 *>(Rrc + TR) + (size_t)warp * 16 * kEP;  // [16 pairs][kEP]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<double2 *>(Rrc + TR) +
+                                               (size_t)wpb * 16 * kEP);
+  const int G = gridDim.x, b = blockIdx.x;
+  auto item_of = [&](int k) { return (k & 1) ? 2 * G * ((k >> 1) + 1) - 1 - b : 2 * G * (k >> 1) + b; };
+  auto issue = [&](int idx) {  // raw inputs of item idx (one elected thread)
+    const int m = m_first + (idx >> 1), kmax = T1 - m;
+    const int off = col_offset(T, m), ro = rc_offset(T, m);
+    const unsigned cb = (unsigned)kmax * 16u, wb = (unsigned)(kmax + 1) * 32u;
+    mbar_expect_tx(bar, 3 * cb + 2 * wb);
+    bulk_g2s_v(Rw, a.coef + off, cb, bar);
+    bulk_g2s_v(Rw + TR, a.coef + nc + off, cb, bar);
+    bulk_g2s_v(Rw + 2 * TR, a.coef + 2 * nc + off, cb, bar);
+    bulk_g2s_v(Rwc, p.d_wc + ro, wb, bar);
+    bulk_g2s_v(Rrc, p.d_rc + ro, wb, bar);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  trace_mark(0);
+  int idx = item_of(0);
+  pdl_wait();  // the coefficients come from the preceding kernel
+  trace_mark(1);
+  if (threadIdx.x == 0 && idx < nitems) issue(idx);
+  for (int k = 0; idx < nitems; ++k) {
+    const int m = m_first + (idx >> 1), blk = idx & 1, kmax = T1 - m;
+    int L = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) L = max(L, syn_seg_start(kmax, q + 1) - syn_seg_start(kmax, q));
+    L = (L + 1) & ~1;
+    // plan data of the item (in flight while the raw inputs land)
+    const int pbase = (blk * wpb + warp) * 16;
+    const int iA = pbase + r, iB = pbase + 8 + r, ie = pbase + lane;
+    const bool wact = pbase < nh;
+    const bool eact = wact && lane < 16 && ie < nh;  // epilogue thread of pair ie
+    double xA = 0.0, xB = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    const double *ck = p.d_sck + ((size_t)m * 8 + c * 2) * nh;
+    if (iA < nh) {
+      xA = p.d_x[iA];
+      a0 = ck[iA];
+      a1 = ck[nh + iA];
+    }
+    if (iB < nh) {
+      xB = p.d_x[iB];
+      b0 = ck[iB];
+      b1 = ck[nh + iB];
+    }
+    int jn = 0, js = 0;
+    double rcos = 0.0;
+    double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    if (eact) {
+      jn = p.d_jn[ie];
+      js = p.d_js[ie];
+      rcos = p.d_rcos[ie];
+      fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
+      fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
+    }
+    mbar_wait(bar, k & 1);
+    for (int t = threadIdx.x; t < 4 * RS; t += blockDim.x) {
+      const int q = t / RS, u = t - q * RS;
+      const int sq = syn_seg_start(kmax, q), n = syn_seg_start(kmax, q + 1) - sq;
+      const int kk = sq + u;
+      double4 cc = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (u < n + 2 && kk <= kmax) cc = Rrc[kk];
+      Rc[t] = make_double2(cc.x, cc.y);
+    }
+    for (int t = threadIdx.x; t < 4 * L; t += blockDim.x) {
+      const int q = t / L, u = t - q * L;
+      const int sq = syn_seg_start(kmax, q), eq = syn_seg_start(kmax, q + 1);
+      const int kk = sq + u;
+      const bool on = kk < eq;  // degree in the quarter (kk <= kmax)
+      const bool in = on && kk < kmax;
+      const bool up = on && kk + 1 < kmax, dn = on && kk >= 1;
+      const double4 cw = on ? Rwc[kk] : make_double4(0.0, 0.0, 0.0, 0.0);
+      const double2 zero = make_double2(0.0, 0.0);
+      const double2 z = in ? Rw[TR + kk] : zero, d = in ? Rw[2 * TR + kk] : zero;
+      const double2 ph = in ? Rw[kk] : zero;
+      const double2 zp = up ? Rw[TR + kk + 1] : zero, dp = up ? Rw[2 * TR + kk + 1] : zero;
+      const double2 zm = dn ? Rw[TR + kk - 1] : zero, dm = dn ? Rw[2 * TR + kk - 1] : zero;
+      double2 wz = make_double2(cw.y * zp.x, cw.y * zp.y), wd = make_double2(cw.y * dp.x, cw.y * dp.y);
+      wz = make_double2(wz.x - cw.z * zm.x, wz.y - cw.z * zm.y);
+      wd = make_double2(wd.x - cw.z * dm.x, wd.y - cw.z * dm.y);
+      double2 *row = reinterpret_cast<double2 *>(Cs + (size_t)q * SS + (size_t)u * 16);
+      row[0] = z;
+      row[1] = d;
+      row[2] = ph;
+      row[3] = make_double2(z.x * cw.x, z.y * cw.x);  // psi = inv_lap(vort)
+      row[4] = make_double2(d.x * cw.x, d.y * cw.x);  // chi = inv_lap(div)
+      row[5] = wz;
+      row[6] = wd;
+      row[7] = zero;
+    }
+    __syncthreads();  // rows staged; the raw buffer is free for the next item
+    if (k < 2) trace_mark(2 + 2 * k);
+    const int nidx = item_of(k + 1);
+    if (threadIdx.x == 0 && nidx < nitems) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(nidx);
+    }
+    double D[2][2][2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) D[q][u][v][0] = D[q][u][v][1] = 0.0;
+    if (wact) {
+      const double *cq = Cs + (size_t)c * SS + r;  // B[k = c][n = r]
+      const double2 *rq = Rc + c * RS;
+#pragma unroll 1
+      for (int j = 0; j < L; j += 2) {
+        double t0 = cq[j * 16], t1 = cq[j * 16 + 8];
+        dmma(D[0][0][0][0], D[0][0][0][1], a0, t0);
+        dmma(D[0][0][1][0], D[0][0][1][1], a0, t1);
+        dmma(D[0][1][0][0], D[0][1][0][1], b0, t0);
+        dmma(D[0][1][1][0], D[0][1][1][1], b0, t1);
+        t0 = cq[j * 16 + 16];
+        t1 = cq[j * 16 + 24];
+        dmma(D[1][0][0][0], D[1][0][0][1], a1, t0);
+        dmma(D[1][0][1][0], D[1][0][1][1], a1, t1);
+        dmma(D[1][1][0][0], D[1][1][0][1], b1, t0);
+        dmma(D[1][1][1][0], D[1][1][1][1], b1, t1);
+        const double2 r2 = rq[j + 2], r3 = rq[j + 3];
+        const double a2 = fma(xA, a1, -r2.x * a0) * r2.y;  // sphere.py:98-100
+        const double b2 = fma(xB, b1, -r2.x * b0) * r2.y;
+        const double a3 = fma(xA, a2, -r3.x * a1) * r3.y;
+        const double b3 = fma(xB, b2, -r3.x * b1) * r3.y;
+        a0 = a2;
+        a1 = a3;
+        b0 = b2;
+        b1 = b3;
+      }
+      // per-warp gather of the pairs' sums, then one epilogue thread per pair
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            E[(u * 8 + r) * kEP + q * 8 + v * 4 + c] = make_double2(D[q][u][v][0], D[q][u][v][1]);
+      __syncwarp();
+      if (eact) {
+        const double2 *e = E + lane * kEP;
+        double2 sp[2][5], sh[2][2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+#pragma unroll
+          for (int s = 0; s < 5; ++s) sp[q][s] = e[q * 8 + s];
+          sh[1 - q][0] = make_double2(e[q * 8 + 5].x * rcos, e[q * 8 + 5].y * rcos);
+          sh[1 - q][1] = make_double2(e[q * 8 + 6].x * rcos, e[q * 8 + 6].y * rcos);
+        }
+        state_rows<PEER>(p, a, m, ie, jn, js, rcos, sp, sh, fr);
+      }
+      __syncwarp();
+    }
+    __syncthreads();  // every warp is done with the staged rows
+    if (k < 2) trace_mark(3 + 2 * k);
+    idx = nidx;
+  }
+  trace_mark(6);
+}
+
+// Warp-specialised persistent state synthesis (one CTA per SM, nh <= 224).
+// Consumer warp w owns latitude pairs [16w, 16w + 16) for every column, so
+// its pair data is loaded once; the CTA walks whole columns in the snake
+// order over the longest-first column list (CTA b: columns b, 2G-1-b, 2G+b,
+// ...).  Two producer warps stage column k+1 (bulk copies of the three
+// coefficient runs, the dP/dlat weights, the recurrence constants and the
+// quarter start values into a private raw buffer / the column's half of a
+// double buffer, then the derived B rows) while the consumers run column k's
+// DMMA loop; full/empty mbarriers per buffer.  The arithmetic per column and
+// pair is the synth_mma_kernel's, so the results are bitwise equal.
+constexpr int kSynPW = 2;  // producer warps
+
+template <bool PEER = false>
+__global__ void __launch_bounds__(480, 1) synth_ws_kernel(ShtView p, SynthArgs a, int m_first,
+                                                          int ncol, int nwc, int lmax) {
+  extern __shared__ __align__(128) double smem_syn[];
+  const int T = p.trunc, nc = p.ncoef, nh = p.nh, T1 = T + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // quarter stride = 4 mod 16 doubles: the B-fragment loads (two half-warps of
+  // 64-bit accesses) hit 16 distinct bank pairs
+  const int SS = lmax * 16 + 4, RS = syn_rs(lmax);
+  const int TR = (T1 + 2) & ~1;
+  const int SK = (8 * nh + 15) & ~15;  // doubles per staged quarter-start block (128-byte multiple)
+  double *Cs0 = smem_syn;                                             // [2][4][SS]
+  double2 *Rc0 = reinterpret_cast<double2 *>(Cs0 + 2 * 4 * SS);     // [2][4][RS]
+  double *Sk0 = reinterpret_cast<double *>(Rc0 + 2 * 4 * RS);        // [2][SK]
+  double2 *Rw = reinterpret_cast<double2 *>(Sk0 + 2 * SK);           // [3][TR]
+  double4 *Rwc = reinterpret_cast<double4 *>(Rw + 3 * TR);            // [TR]
+  double4 *Rrc = Rwc + TR;                                            // [TR]
+  double2 *E0 = reinterpret_cast<double2 *>(Rrc + TR);                // [nwc][16][kEP]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(E0 + (size_t)nwc * 16 * kEP);
+  uint64_t *full = bars, *empty = bars + 2, *rawbar = bars + 4;
+  const int G = gridDim.x, b = blockIdx.x;
+  auto col_of = [&](int k) { return (k & 1) ? 2 * G * ((k >> 1) + 1) - 1 - b : 2 * G * (k >> 1) + b; };
+  if (threadIdx.x == 0) {
+    mbar_init(full + 0, 32 * kSynPW);
+    mbar_init(full + 1, 32 * kSynPW);
+    mbar_init(empty + 0, nwc);
+    mbar_init(empty + 1, nwc);
+    mbar_init(rawbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  trace_mark(0);
+  const int pt = threadIdx.x - 32 * nwc;  // producer thread 0 .. 32 kSynPW - 1 (< 0: consumer)
+  // raw inputs of the k-th column (one elected producer thread)
+  auto issue = [&](int k) {
+    const int m = m_first + col_of(k), kmax = T1 - m;
+    const int off = col_offset(T, m), ro = rc_offset(T, m);
+    const unsigned cb = (unsigned)kmax * 16u, wb = (unsigned)(kmax + 1) * 32u;
+    const unsigned sb = (unsigned)(8 * nh) * 8u;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(rawbar, 3 * cb + 2 * wb + sb);
+    bulk_g2s_v(Rw, a.coef + off, cb, rawbar);
+    bulk_g2s_v(Rw + TR, a.coef + nc + off, cb, rawbar);
+    bulk_g2s_v(Rw + 2 * TR, a.coef + 2 * nc + off, cb, rawbar);
+    bulk_g2s_v(Rwc, p.d_wc + ro, wb, rawbar);
+    bulk_g2s_v(Rrc, p.d_rc + ro, wb, rawbar);
+    bulk_g2s_v(Sk0 + (size_t)(k & 1) * SK, p.d_sck + (size_t)m * 8 * nh, sb, rawbar);
+  };
+  // derived B rows and recurrence constants of the k-th column from the raw
+  // buffer, by threads t0, t0 + nt, ...
+  auto derive = [&](int k, int t0, int nt) {
+    const int buf = k & 1;
+    const int m = m_first + col_of(k), kmax = T1 - m;
+    double *Cs = Cs0 + (size_t)buf * 4 * SS;
+    double2 *Rc = Rc0 + (size_t)buf * 4 * RS;
+    int L = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) L = max(L, syn_seg_start(kmax, q + 1) - syn_seg_start(kmax, q));
+    L = (L + 1) & ~1;
+    for (int t = t0; t < 4 * RS; t += nt) {
+      const int q = t / RS, u = t - q * RS;
+      const int sq = syn_seg_start(kmax, q), n = syn_seg_start(kmax, q + 1) - sq;
+      const int kk = sq + u;
+      double4 cc = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (u < n + 2 && kk <= kmax) cc = Rrc[kk];
+      Rc[t] = make_double2(cc.x, cc.y);
+    }
+    for (int t = t0; t < 4 * L; t += nt) {
+      const int q = t / L, u = t - q * L;
+      const int sq = syn_seg_start(kmax, q), eq = syn_seg_start(kmax, q + 1);
+      const int kk = sq + u;
+      const bool on = kk < eq;  // degree in the quarter (kk <= kmax)
+      const bool in = on && kk < kmax;
+      const bool up = on && kk + 1 < kmax, dn = on && kk >= 1;
+      const double4 cw = on ? Rwc[kk] : make_double4(0.0, 0.0, 0.0, 0.0);
+      const double2 zero = make_double2(0.0, 0.0);
+      const double2 z = in ? Rw[TR + kk] : zero, d = in ? Rw[2 * TR + kk] : zero;
+      const double2 ph = in ? Rw[kk] : zero;
+      const double2 zp = up ? Rw[TR + kk + 1] : zero, dp = up ? Rw[2 * TR + kk + 1] : zero;
+      const double2 zm = dn ? Rw[TR + kk - 1] : zero, dm = dn ? Rw[2 * TR + kk - 1] : zero;
+      // dP/dlat series of psi, chi summed by parts (see synth_kernel)
+      double2 wz = make_double2(cw.y * zp.x, cw.y * zp.y), wd = make_double2(cw.y * dp.x, cw.y * dp.y);
+      wz = make_double2(wz.x - cw.z * zm.x, wz.y - cw.z * zm.y);
+      wd = make_double2(wd.x - cw.z * dm.x, wd.y - cw.z * dm.y);
+      double2 *row = reinterpret_cast<double2 *>(Cs + (size_t)q * SS + (size_t)u * 16);
+      row[0] = z;
+      row[1] = d;
+      row[2] = ph;
+      row[3] = make_double2(z.x * cw.x, z.y * cw.x);  // psi = inv_lap(vort)
+      row[4] = make_double2(d.x * cw.x, d.y * cw.x);  // chi = inv_lap(div)
+      row[5] = wz;
+      row[6] = wd;
+      row[7] = zero;
+    }
+  };
+  // the first column: every warp stages it (the consumers would idle)
+  if (pt == 0) {
+    pdl_wait();  // the coefficients come from the preceding kernel
+    issue(0);
+  }
+  mbar_wait(rawbar, 0);
+  derive(0, threadIdx.x, blockDim.x);
+  __syncthreads();
+  if (warp >= nwc) {
+    // ---------------- producers ----------------
+    mbar_arrive(full + 0);
+    for (int k = 1; col_of(k) < ncol; ++k) {
+      const int buf = k & 1;
+      if (k >= 2) mbar_wait(empty + buf, ((k >> 1) - 1) & 1);
+      if (pt == 0) issue(k);
+      mbar_wait(rawbar, k & 1);
+      derive(k, pt, 32 * kSynPW);
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kSynPW) : "memory");  // raw buffer consumed
+      mbar_arrive(full + buf);
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int c = lane & 3, r = lane >> 2;
+  const int pbase = warp * 16;
+  const int iA = pbase + r, iB = pbase + 8 + r, ie = pbase + lane;
+  const bool eact = lane < 16 && ie < nh;  // epilogue thread of pair ie
+  const bool bact = pbase + 8 < nh;         // the second row tile holds pairs
+  const double xA = iA < nh ? p.d_x[iA] : 0.0, xB = iB < nh ? p.d_x[iB] : 0.0;
+  int jn = 0, js = 0;
+  double rcos = 0.0;
+  double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  if (eact) {
+    jn = p.d_jn[ie];
+    js = p.d_js[ie];
+    rcos = p.d_rcos[ie];
+    fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
+    fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
+  }
+  double2 *E = E0 + (size_t)warp * 16 * kEP;
+  for (int k = 0;; ++k) {
+    const int idx = col_of(k);
+    if (idx >= ncol) break;
+    const int buf = k & 1;
+    const int m = m_first + idx, kmax = T1 - m;
+    int L = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) L = max(L, syn_seg_start(kmax, q + 1) - syn_seg_start(kmax, q));
+    L = (L + 1) & ~1;
+    mbar_wait(full + buf, (k >> 1) & 1);
+    if (k < 2) trace_mark(1 + 3 * k);
+    const double *ck = Sk0 + (size_t)buf * SK + (size_t)(c * 2) * nh;
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    if (iA < nh) {
+      a0 = ck[iA];
+      a1 = ck[nh + iA];
+    }
+    if (iB < nh) {
+      b0 = ck[iB];
+      b1 = ck[nh + iB];
+    }
+    double D[2][2][2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) D[q][u][v][0] = D[q][u][v][1] = 0.0;
+    const double *cq = Cs0 + (size_t)buf * 4 * SS + (size_t)c * SS + r;  // B[k = c][n = r]
+    const double2 *rq = Rc0 + (size_t)buf * 4 * RS + c * RS;
+    if (bact) {
+#pragma unroll 1
+      for (int j = 0; j < L; j += 2) {
+        double t0 = cq[j * 16], t1 = cq[j * 16 + 8];
+        dmma(D[0][0][0][0], D[0][0][0][1], a0, t0);
+        dmma(D[0][0][1][0], D[0][0][1][1], a0, t1);
+        dmma(D[0][1][0][0], D[0][1][0][1], b0, t0);
+        dmma(D[0][1][1][0], D[0][1][1][1], b0, t1);
+        t0 = cq[j * 16 + 16];
+        t1 = cq[j * 16 + 24];
+        dmma(D[1][0][0][0], D[1][0][0][1], a1, t0);
+        dmma(D[1][0][1][0], D[1][0][1][1], a1, t1);
+        dmma(D[1][1][0][0], D[1][1][0][1], b1, t0);
+        dmma(D[1][1][1][0], D[1][1][1][1], b1, t1);
+        const double2 r2 = rq[j + 2], r3 = rq[j + 3];
+        const double a2 = fma(xA, a1, -r2.x * a0) * r2.y;  // sphere.py:98-100
+        const double b2 = fma(xB, b1, -r2.x * b0) * r2.y;
+        const double a3 = fma(xA, a2, -r3.x * a1) * r3.y;
+        const double b3 = fma(xB, b2, -r3.x * b1) * r3.y;
+        a0 = a2;
+        a1 = a3;
+        b0 = b2;
+        b1 = b3;
+      }
+    } else {  // the warp's second row tile holds no pair: half the MMAs
+#pragma unroll 1
+      for (int j = 0; j < L; j += 2) {
+        double t0 = cq[j * 16], t1 = cq[j * 16 + 8];
+        dmma(D[0][0][0][0], D[0][0][0][1], a0, t0);
+        dmma(D[0][0][1][0], D[0][0][1][1], a0, t1);
+        t0 = cq[j * 16 + 16];
+        t1 = cq[j * 16 + 24];
+        dmma(D[1][0][0][0], D[1][0][0][1], a1, t0);
+        dmma(D[1][0][1][0], D[1][0][1][1], a1, t1);
+        const double2 r2 = rq[j + 2], r3 = rq[j + 3];
+        const double a2 = fma(xA, a1, -r2.x * a0) * r2.y;  // sphere.py:98-100
+        const double a3 = fma(xA, a2, -r3.x * a1) * r3.y;
+        a0 = a2;
+        a1 = a3;
+      }
+    }
+    __syncwarp();
+    if (k < 2) trace_mark(2 + 3 * k);
+    if (lane == 0) mbar_arrive(empty + buf);  // staged column consumed by this warp
+    // per-warp gather of the pairs' sums, then one epilogue thread per pair
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+          E[(u * 8 + r) * kEP + q * 8 + v * 4 + c] = make_double2(D[q][u][v][0], D[q][u][v][1]);
+    __syncwarp();
+    if (eact) {
+      const double2 *e = E + lane * kEP;
+      double2 sp[2][5], sh[2][2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) sp[q][s] = e[q * 8 + s];
+        sh[1 - q][0] = make_double2(e[q * 8 + 5].x * rcos, e[q * 8 + 5].y * rcos);
+        sh[1 - q][1] = make_double2(e[q * 8 + 6].x * rcos, e[q * 8 + 6].y * rcos);
+      }
+      state_rows<PEER>(p, a, m, ie, jn, js, rcos, sp, sh, fr);
+    }
+    __syncwarp();
+    if (k < 1) trace_mark(3);
+  }
+  trace_mark(6);
+}
+
 // Persistent, warp-specialised analysis.  One CTA per SM walks a contiguous,
 // cost-balanced range of (m, segment) work items (sorted by m, so the
 // prepared rows of a column are built once per CTA and column).  Per item,
@@ -2390,48 +2884,6 @@ constexpr size_t tab_smem(int kts) {
 static_assert(kP1 >= kTBoxRows * kPR && kSB >= kP1 + kTBoxRows * kPR, "stage layout");
 static_assert((kStage * 8) % 128 == 0 && (kP1 * 8) % 128 == 0 && (kSB * 8) % 128 == 0, "TMA alignment");
 
-__device__ __forceinline__ unsigned smem_u32(const void *ptr) {
-  return (unsigned)__cvta_generic_to_shared(ptr);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "SWX_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra SWX_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(double *dst, const double *src, unsigned bytes,
-                                         uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_2d(double *dst, const CUtensorMap *map, int c0, int c1,
-                                       uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
 template <int MODE, int kTS = 4>
 __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
                                                                    const __grid_constant__ CUtensorMap tmap,
@@ -2446,6 +2898,7 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
   constexpr int NPART = MODE == 0 ? 2 : 1;
   const size_t ps = (size_t)nt * kAG;
   pdl_trigger();
+  if (MODE == 0) trace_mark(0, 1024);
   if (threadIdx.x == 0) {
     for (int q = 0; q < kTS; ++q) {
       mbar_init(full + q, 1);
@@ -2455,6 +2908,7 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
   }
   __syncthreads();
   pdl_wait();  // the prepared rows come from the preceding kernel
+  if (MODE == 0) trace_mark(1, 1024);
 
   if (wid == kTCW) {
     // ---------------- producer warp (one lane) ----------------
@@ -2569,6 +3023,7 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
       if (valid && lc4 < nf) out[(size_t)lc4 * p.ncoef + slotc] = make_double2(cp0, cp1);
     }
   }
+  if (MODE == 0) trace_mark(6, 1024);
 }
 
 // ---------------------------------------------------------------------
@@ -3554,6 +4009,49 @@ static int launch_state_synth(swx_sht p, const SynthArgs &a0, int m0, int m1, bo
                               cudaStream_t s) {
   int nt;
   dim3 g = synth_grid(p, 1, &nt);
+  static const int wsk = env_int("SWX_SYNTH_WS", 1);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    SWX_CUDA_TRY(cudaGetDevice(&dev));
+    SWX_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int nwc = (p->nh + 15) / 16;  // consumer warps: 16 latitude pairs each
+  if (p->d_sck && wsk && nwc + kSynPW <= 15) {
+    const int lmax = ((p->trunc + 2) / 4 + 2 + 1) & ~1;  // longest quarter, even
+    const int T1 = p->trunc + 1, TR = (T1 + 2) & ~1;
+    const int SS = lmax * 16 + 4, RS = syn_rs(lmax), SK = (8 * p->nh + 15) & ~15;
+    const size_t smem = sizeof(double) * (2 * 4 * (size_t)SS + 2 * (size_t)SK) +
+                        sizeof(double2) * (2 * 4 * (size_t)RS + 3 * (size_t)TR) +
+                        sizeof(double4) * 2 * (size_t)TR + sizeof(double2) * 16 * kEP * (size_t)nwc +
+                        5 * sizeof(uint64_t);
+    const int ncol = m1 - m0;
+    const int G = std::min(ncol, nsm);
+    auto k = peer ? synth_ws_kernel<true> : synth_ws_kernel<false>;
+    SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SWX_CUDA_TRY(launch_pdl(k, dim3(G), dim3(32 * (nwc + kSynPW)), smem, s,
+                            static_cast<const ShtView &>(*p), a0, m0, ncol, nwc, lmax));
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
+  static const int pers = env_int("SWX_SYNTH_PERS", 1);
+  if (p->d_sck && pers) {
+    const int wpb = (((p->nh + 15) / 16) + 1) / 2;  // warps per CTA: half the pairs
+    const int lmax = ((p->trunc + 2) / 4 + 2 + 1) & ~1;  // longest quarter, even
+    const int T1 = p->trunc + 1, TR = (T1 + 2) & ~1;
+    const size_t smem = sizeof(double) * (4 * (size_t)(lmax * 16 + 8)) +
+                        sizeof(double2) * (4 * (size_t)syn_rs(lmax) + 3 * (size_t)TR) +
+                        sizeof(double4) * 2 * (size_t)TR + sizeof(double2) * 16 * kEP * (size_t)wpb + 16;
+    const int nitems = 2 * (m1 - m0);
+    const int G = std::min(nitems, 2 * nsm);
+    auto k = peer ? synth_mma_pers_kernel<true> : synth_mma_pers_kernel<false>;
+    if (smem > 48 * 1024)
+      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SWX_CUDA_TRY(launch_pdl(k, dim3(G), dim3(32 * wpb), smem, s,
+                            static_cast<const ShtView &>(*p), a0, m0, nitems, wpb, lmax));
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
   if (p->d_sck) {
     const int wpb = (((p->nh + 15) / 16) + 1) / 2;  // warps per CTA: half the pairs
     const int lmax = ((p->trunc + 2) / 4 + 2 + 1) & ~1;  // longest quarter, even

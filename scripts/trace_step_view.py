@@ -1,0 +1,22 @@
+"""Timeline of one traced ETD2RK step (bench.py with SWX_TRACE_OUT, trace build):
+the last synthesis (slots 0..), table analysis (1024..) and grid stage (2048..)
+launches of the step; us from the synthesis' first CTA entry."""
+import sys
+import numpy as np
+
+b = np.load(sys.argv[1]).astype(np.int64)
+def rows(lo, hi):
+    r = b[lo:hi]
+    return r[(r[:, 1:] > 0).any(axis=1)]
+s, a, g = rows(0, 1024), rows(1024, 2048), rows(2048, 4096)
+t0 = s[:, 1].min()
+def show(name, r):
+    print(name, "CTAs", len(r))
+    for k in range(7):
+        v = r[:, 1 + k]
+        v = v[v > 0]
+        if len(v):
+            print(f"   mark {k}", np.percentile((v - t0) / 1e3, [0, 50, 90, 100]).round(2))
+show("synth", s)
+show("grid", g)
+show("analysis", a)
