@@ -464,10 +464,12 @@ def main():
         flush.zero_()
         torch.cuda.synchronize()
         tlib.swx_trace(1, None, 0)
+        tlib.swx_trace_rexi(1, None, 0)
         step()
         torch.cuda.synchronize()
-        tbuf = np.zeros((4096, 8), dtype=np.uint64)
-        tlib.swx_trace(0, tbuf.ctypes.data, 4096)
+        tbuf = np.zeros((2, 4096, 8), dtype=np.uint64)
+        tlib.swx_trace(0, tbuf[0].ctypes.data, 4096)
+        tlib.swx_trace_rexi(0, tbuf[1].ctypes.data, 4096)
         np.save(os.environ["SWX_TRACE_OUT"], tbuf)
     sampler = ClockSampler(local)
     sampler.start()

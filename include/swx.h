@@ -332,6 +332,8 @@ int swx_fp64_fma_probe(double *d_sink, int n_blocks, int iters, void *stream);
  * square fused grid stage): enable 1/0 (-1: unchanged); when h_out is
  * non-null, copies n_ctas records of 8 u64 {smid, globaltimer marks (ns)}.  */
 int swx_trace(int enable, unsigned long long *h_out, int n_ctas);
+/* the same for the REXI pole-sum kernels (rexi.cu's trace buffer) */
+int swx_trace_rexi(int enable, unsigned long long *h_out, int n_ctas);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,7 @@ SIGNATURES = {
     "swx_e2e_destroy": (_I, [_P]),
     "swx_e2e_step": (_I, [_P, _P, _P, _P, _P, _P]),
     "swx_trace": (_I, [_I, _P, _I]),
+    "swx_trace_rexi": (_I, [_I, _P, _I]),
     "swx_shard_init": (_I, [_P, _I, _I, _I, _I]),
     "swx_sht_shard_counts": (_S, [_P, _P, _I, _I, _P, _P]),
     "swx_sht_tendency_shard": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _S, _P]),

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
   constexpr int GROUPS = 128 / LPM;      // lane groups per CTA
   extern __shared__ double2 fac[];       // [NRHS][4][NP], interleaved (t*LPM + q)
   pdl_trigger();
+  trace_mark(0);
   // prepared factor tables do not depend on the preceding kernel: stage them
   // before waiting for it (PDL overlap)
   if (!fac_ready) pdl_wait();
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
   }
   __syncthreads();
   pdl_wait();
+  if (it == blockIdx.x) trace_mark(1);
   const int q = threadIdx.x & (LPM - 1);
   const int g = threadIdx.x / LPM;
   for (int base = m0; base < m1; base += GROUPS * MPL) {
@@ -421,7 +423,8 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
         }
     }
   }
-}
+  }
+  trace_mark(6);
 }
 
 // K1 (persistent form): the lane-group mapping of rexi_lg_mm_kernel over
@@ -2428,3 +2431,22 @@ extern "C" int swx_solver_set_columns(swx_solver s, int m_begin, int m_end) {
 }
 
 extern "C" size_t swx_solver_cache_bytes(swx_solver s) { return s ? s->linv_bytes : 0; }
+
+// per-CTA phase marks of this translation unit's kernels (trace build; see
+// swx_trace in sht.cu)
+extern "C" int swx_trace_rexi(int enable, unsigned long long *h_out, int n_ctas) {
+  if (enable >= 0) {
+    SWX_CUDA_TRY(cudaMemcpyToSymbol(swx::g_trace_on, &enable, sizeof(int)));
+    if (enable) {
+      static unsigned long long z[swx::kTraceCtas * swx::kTraceSlots];
+      SWX_CUDA_TRY(cudaMemcpyToSymbol(swx::g_trace, z, sizeof(z)));
+    }
+  }
+  if (h_out && n_ctas > 0) {
+    const int n = std::min(n_ctas, swx::kTraceCtas);
+    SWX_CUDA_TRY(cudaDeviceSynchronize());
+    SWX_CUDA_TRY(cudaMemcpyFromSymbol(h_out, swx::g_trace,
+                                      sizeof(unsigned long long) * swx::kTraceSlots * n));
+  }
+  return SWX_OK;
+}

@@ -111,6 +111,9 @@ struct ShtView {
   int2 *d_slist = nullptr;     // (m, 16-pair block), LPT order per CTA
   int n_titems = 0;            // analysis warp items (m, l0, par)
   int4 *d_titems = nullptr;
+  // on-the-fly tendency analysis (T <= kAckTMax): P_k, P_{k+1} of every
+  // column, pair and segment start k = g * ack_steps(m), [m][g][nt16][2]
+  double *d_ack = nullptr;
 };
 
 struct swx_sht_s : ShtView {
@@ -2884,6 +2887,260 @@ constexpr size_t tab_smem(int kts) {
 static_assert(kP1 >= kTBoxRows * kPR && kSB >= kP1 + kTBoxRows * kPR, "stage layout");
 static_assert((kStage * 8) % 128 == 0 && (kP1 * 8) % 128 == 0 && (kSB * 8) % 128 == 0, "TMA alignment");
 
+
+// ---------------------------------------------------------------------
+// Tendency analysis with the Legendre functions generated in the DMMA
+// A fragments (no P table traffic).  Column m's degrees k = l - m = 0..kmax
+// (kmax = T+1-m: P_{T+1} feeds the dP/dlat part) are cut into 16 segments
+// of S = ack_steps(m) (even) degrees.  D[M = segment][N = column] +=
+// A[M = segment][K = 4 pairs] * B[K = pair][N = column]: lane (r, c) of a
+// warp runs the recurrence (sphere.py:98-100, bit-identical to the table)
+// of segment r for pair c of the current 4-pair block from the plan-time
+// segment-start values, so the 8 rows of every MMA are 8 different degrees
+// of the same parity and the B fragment (the prepared rows of that parity)
+// is shared.  Per degree k the kernel forms
+//   F[k] = sum_i P_k(i) R0_i[par k]   (vort, div, phi', KE columns)
+//   G[k] = sum_i P_k(i) R1_i[par k]   (the 1/cos-folded d/dlat rows)
+// and the dP/dlat series by parts, sum_i (cz P_{k-1} - cw P_{k+1}) R1_i =
+// cz G[k-1] - cw G[k+1] (the table kernel's h per pair, summed first).
+// CTA = column, 8 warps = 2 segment windows x 4 pair quarters; the quarter
+// partials are added in fixed order ((q0 + q2) + (q1 + q3)).
+// ---------------------------------------------------------------------
+constexpr int kAckWin = 3;              // segment windows (8 segments each) per column
+constexpr int kAckSeg = 8 * kAckWin;    // segments per column
+constexpr int kAckSMax = 12;            // steps per segment (accumulators per lane: 4 * kAckSMax)
+constexpr int kAckTMax = kAckSeg * kAckSMax - 2;  // largest truncation (T + 2 <= kAckSeg S)
+constexpr int kAckThreads = kAckWin * 4 * 32;     // windows x 4 pair quarters
+__host__ __device__ inline int ack_steps(int trunc, int m) {
+  return 2 * ((trunc + 2 - m + 2 * kAckSeg - 1) / (2 * kAckSeg));
+}
+// pair pitch (double2) of a segment's start values: = 4 mod 8, so the four
+// segments a half-warp reads fall in distinct bank groups
+__host__ __device__ inline int ack_pitch(int nt16) { return nt16 + 4; }
+
+// plan time: segment-start values of every column and padded pair
+__global__ void ack_kernel(ShtView p) {
+  const int m = blockIdx.x;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= p.nt16) return;
+  const int T = p.trunc, kmax = T + 1 - m, S = ack_steps(T, m);
+  const int ckp = ack_pitch(p.nt16);
+  double *ck = p.d_ack + (size_t)m * kAckSeg * ckp * 2;
+  if (i >= p.nh) {
+    for (int g = 0; g < kAckSeg; ++g) ck[((size_t)g * ckp + i) * 2] = ck[((size_t)g * ckp + i) * 2 + 1] = 0.0;
+    return;
+  }
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  const double x = p.d_x[i];
+  const double seed = p.d_seed[(size_t)m * p.nh + i];
+  double p0 = seed, p1 = kmax >= 1 ? sqrt(2.0 * m + 3.0) * x * seed : 0.0;
+  int g = 0;
+  for (int k = 0; k <= kmax; ++k) {
+    if (k == g * S && g < kAckSeg) {
+      ck[((size_t)g * ckp + i) * 2] = p0;
+      ck[((size_t)g * ckp + i) * 2 + 1] = p1;
+      ++g;
+    }
+    double p2 = 0.0;
+    if (k + 2 <= kmax) {
+      const double4 c2 = rc[k + 2];
+      p2 = fma(x, p1, -c2.x * p0) * c2.y;  // identical to the walkers
+    }
+    p0 = p1;
+    p1 = p2;
+  }
+  for (; g < kAckSeg; ++g) ck[((size_t)g * ckp + i) * 2] = ck[((size_t)g * ckp + i) * 2 + 1] = 0.0;
+}
+
+constexpr int kAckRed = kAckWin * 2 * kAckSMax * 2 * 64;  // reduction buffer (doubles)
+
+__global__ void __launch_bounds__(kAckThreads, 1) analysis_otf_kernel(ShtView p, const double *A,
+                                                              double2 *out, const double2 *sub,
+                                                              int m_first, int ncol) {
+  extern __shared__ __align__(128) double osm[];
+  const int nt = p.nt16, ckp = ack_pitch(nt);
+  const size_t ps = (size_t)nt * kAG;
+  double *red = osm;                                            // [win][2][S][part][64]
+  double *rows = red + kAckRed;                                 // [4][nt][kAG]: the column's prepared rows
+  double2 *cks = reinterpret_cast<double2 *>(rows + 4 * ps);    // [16][ckp]: segment starts
+  double2 *rcS = cks + (size_t)kAckSeg * ckp;                   // [16 S + 2]
+  double *xs = reinterpret_cast<double *>(rcS + kAckSeg * kAckSMax + 2);  // [nt]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(xs + nt);
+  const int T = p.trunc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int win = warp % kAckWin, qtr = warp / kAckWin;
+  const int r = lane >> 2, c = lane & 3;
+  const int G = gridDim.x;
+  auto col_of = [&](int it) {  // columns b, 2G-1-b, 2G+b, ... of the longest-first list
+    return (it & 1) ? 2 * G * ((it >> 1) + 1) - 1 - (int)blockIdx.x : 2 * G * (it >> 1) + (int)blockIdx.x;
+  };
+  const unsigned rb = (unsigned)(4 * ps * sizeof(double)), cb = (unsigned)(kAckSeg * ckp * sizeof(double2));
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) xs[i] = i < p.nh ? p.d_x[i] : 0.0;
+  __syncthreads();
+  pdl_trigger();
+  trace_mark(0, 1024);
+  for (int it = 0;; ++it) {
+  const int idx = col_of(it);
+  if (idx >= ncol) break;
+  const int m = m_first + idx;
+  const int kmax = T + 1 - m, S = ack_steps(T, m);
+  if (it > 0) __syncthreads();  // the previous column's shared-memory reads are done
+  if (threadIdx.x == 0) {
+    // the segment starts are plan data; the prepared rows come from the
+    // preceding kernel (first column: wait for it)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(bar, rb + cb);
+    bulk_g2s_v(cks, p.d_ack + (size_t)m * kAckSeg * ckp * 2, cb, bar);
+    if (it == 0) pdl_wait();
+    bulk_g2s_v(rows, A + (size_t)m * 4 * ps, rb, bar);
+  }
+  // recurrence constants of the column
+  const double4 *rc = p.d_rc + rc_offset(T, m);
+  for (int k = threadIdx.x; k < kAckSeg * S + 2; k += blockDim.x) {
+    const double4 v = k <= kmax ? rc[k] : make_double4(0.0, 0.0, 0.0, 0.0);
+    rcS[k] = make_double2(v.x, v.y);
+  }
+  const int g = win * 8 + r;  // this lane's segment
+  const int k0 = g * S;
+  const double2 *ck = cks + (size_t)g * ckp;
+  const int nb = nt / 4, nbq = (nb + 3) / 4;
+  const int b0 = qtr * nbq, b1 = min(nb, b0 + nbq);
+  __syncthreads();  // rcS staged
+  mbar_wait(bar, it & 1);
+  if (it == 0) trace_mark(1, 1024);
+  double DF[kAckSMax][2], DG[kAckSMax][2];
+#pragma unroll
+  for (int j = 0; j < kAckSMax; ++j) DF[j][0] = DF[j][1] = DG[j][0] = DG[j][1] = 0.0;
+  // software pipeline: the next block's operands are loaded under this block's MMAs
+#define OTF_LOAD(b)                                                        \
+  {                                                                        \
+    const int i = 4 * (b) + c;                                             \
+    nx = xs[i];                                                            \
+    const double2 q = ck[i];                                               \
+    nP0 = q.x;                                                             \
+    nP1 = q.y;                                                             \
+    const int col = r ^ ((i & 2) ? 4 : 0); /* rotated rows (bit 1 set) */  \
+    const double *row = rows + (size_t)i * kAG + col;                      \
+    nbf0 = row[0 * ps];                                                    \
+    nbf1 = row[1 * ps];                                                    \
+    nbg0 = row[2 * ps];                                                    \
+    nbg1 = row[3 * ps];                                                    \
+  }
+  // the pair blocks of this warp, SS = S steps per segment (compile time:
+  // no predicated-off MMAs on short columns)
+#define OTF_BLOCKS(SS)                                                                         \
+  {                                                                                            \
+    double nx = 0.0, nP0 = 0.0, nP1 = 0.0, nbf0 = 0.0, nbf1 = 0.0, nbg0 = 0.0, nbg1 = 0.0;     \
+    if (b0 < b1) OTF_LOAD(b0)                                                                  \
+    for (int b = b0; b < b1; ++b) {                                                            \
+      const double x = nx;                                                                     \
+      double P0 = nP0, P1 = nP1;                                                               \
+      const double bf[2] = {nbf0, nbf1}, bg[2] = {nbg0, nbg1};                                 \
+      if (b + 1 < b1) OTF_LOAD(b + 1)                                                          \
+      _Pragma("unroll") for (int j = 0; j < (SS); ++j) {                                       \
+        dmma(DF[j][0], DF[j][1], P0, bf[j & 1]);                                               \
+        dmma(DG[j][0], DG[j][1], P0, bg[j & 1]);                                               \
+        const double2 c2 = rcS[k0 + j + 2];                                                    \
+        const double P2 = fma(x, P1, -c2.x * P0) * c2.y;                                       \
+        P0 = P1;                                                                               \
+        P1 = P2;                                                                               \
+      }                                                                                        \
+    }                                                                                          \
+  }
+  switch (S) {
+    case 2: OTF_BLOCKS(2) break;
+    case 4: OTF_BLOCKS(4) break;
+    case 6: OTF_BLOCKS(6) break;
+    case 8: OTF_BLOCKS(8) break;
+    case 10: OTF_BLOCKS(10) break;
+    default: OTF_BLOCKS(12) break;
+  }
+#undef OTF_BLOCKS
+#undef OTF_LOAD
+  if (it < 2) trace_mark(2 + 2 * it, 1024);
+  // fixed-order reduction over the pair quarters: ((q0 + q2) + (q1 + q3))
+  double *rw = red + (size_t)win * 2 * kAckSMax * 128;  // [2][S][part][64] per window
+#define OTF_PUT(slot)                                                        \
+  _Pragma("unroll") for (int j = 0; j < kAckSMax; ++j) if (j < S) {        \
+    double *d = rw + ((size_t)(slot) * kAckSMax + j) * 128 + lane * 2;      \
+    d[0] = DF[j][0];                                                         \
+    d[1] = DF[j][1];                                                         \
+    d[64] = DG[j][0];                                                        \
+    d[65] = DG[j][1];                                                        \
+  }
+#define OTF_ADD(slot)                                                        \
+  _Pragma("unroll") for (int j = 0; j < kAckSMax; ++j) if (j < S) {        \
+    const double *d = rw + ((size_t)(slot) * kAckSMax + j) * 128 + lane * 2; \
+    DF[j][0] += d[0];                                                        \
+    DF[j][1] += d[1];                                                        \
+    DG[j][0] += d[64];                                                       \
+    DG[j][1] += d[65];                                                       \
+  }
+  if (qtr >= 2) { OTF_PUT(qtr - 2) }
+  __syncthreads();
+  if (qtr < 2) { OTF_ADD(qtr) }
+  __syncthreads();
+  if (qtr == 1) { OTF_PUT(0) }
+  __syncthreads();
+  if (qtr == 0) { OTF_ADD(0) }
+#undef OTF_PUT
+#undef OTF_ADD
+  __syncthreads();  // reduction buffer free: the finals go to fin[k][16]
+  double *fin = red;
+  if (qtr == 0) {
+#pragma unroll
+    for (int j = 0; j < kAckSMax; ++j) {
+      if (j >= S) continue;
+      const int k = k0 + j;
+      if (k <= kmax) {
+        double *f = fin + (size_t)k * 16;
+        f[2 * c] = DF[j][0];
+        f[2 * c + 1] = DF[j][1];
+        f[8 + 2 * c] = DG[j][0];
+        f[8 + 2 * c + 1] = DG[j][1];
+      }
+    }
+  }
+  __syncthreads();
+  if (it < 2) trace_mark(3 + 2 * it, 1024);
+  // epilogue: one degree per thread (swe.py:188-251 via the prepared rows)
+  const int off = col_offset(T, m);
+  const size_t nc = p.ncoef;
+  for (int k = threadIdx.x; k < kmax; k += blockDim.x) {
+    const int l = m + k;
+    const double4 c4 = rc[k];
+    const double cz = k > 0 ? c4.z : 0.0, cw = c4.w;  // l = m has no P_{l-1}
+    const double *f = fin + (size_t)k * 16;
+    const double *gm = k > 0 ? fin + (size_t)(k - 1) * 16 + 8 : nullptr;
+    const double *gp = fin + (size_t)(k + 1) * 16 + 8;
+    double h[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) h[q] = fma(cz, gm ? gm[q] : 0.0, -cw * gp[q]);
+    const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
+    double2 vo = make_double2(f[0] + h[0], f[1] + h[1]);
+    double2 di = make_double2(f[2] + h[2], f[3] + h[3]);
+    double2 ph = make_double2(f[4] + h[4], f[5] + h[5]);
+    di.x += llk * f[6];
+    di.y += llk * f[7];
+    const size_t o = (size_t)off + k;
+    if (sub) {  // fused difference N(a) - N(u) of the ETD2RK step
+      const double2 b0v = sub[nc + o], b1v = sub[2 * nc + o], b2v = sub[o];
+      vo = make_double2(vo.x + b0v.x * -1.0, vo.y + b0v.y * -1.0);
+      di = make_double2(di.x + b1v.x * -1.0, di.y + b1v.y * -1.0);
+      ph = make_double2(ph.x + b2v.x * -1.0, ph.y + b2v.y * -1.0);
+    }
+    out[nc + o] = vo;
+    out[2 * nc + o] = di;
+    out[o] = ph;
+  }
+  }
+  trace_mark(6, 1024);
+}
+
 template <int MODE, int kTS = 4>
 __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
                                                                    const __grid_constant__ CUtensorMap tmap,
@@ -3554,6 +3811,20 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
       p->fused_grid = e == cudaSuccess;
     }
   }
+  // segment starts of the on-the-fly tendency analysis
+  if (p->fused_grid && T <= kAckTMax) {
+    e = cudaMalloc(&p->d_ack, sizeof(double) * (size_t)(T + 1) * kAckSeg * ack_pitch(p->nt16) * 2);
+    if (e == cudaSuccess) e = cudaMemset(p->d_ack, 0, sizeof(double) * (size_t)(T + 1) * kAckSeg * ack_pitch(p->nt16) * 2);
+    if (e == cudaSuccess) {
+      ack_kernel<<<dim3(T + 1, (p->nt16 + 127) / 128), 128>>>(static_cast<const ShtView &>(*p));
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    if (e != cudaSuccess) {
+      swx_sht_destroy(p);
+      return fail(SWX_ERR_CUDA, std::string("sht analysis checkpoints: ") + cudaGetErrorString(e));
+    }
+  }
   cufftHandle h;
   int rcd = get_plan(p, CUFFT_Z2D, p->nlon_t, 4 * nlat, &h);
   if (!rcd) rcd = get_plan(p, CUFFT_D2Z, p->nlon_t, 5 * nlat, &h);
@@ -3582,6 +3853,7 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_segoff);
   cudaFree(p->d_ckpt);
   cudaFree(p->d_sck);
+  cudaFree(p->d_ack);
   cudaFree(p->d_wc);
   cudaFree(p->d_arange);
   cudaFree(p->d_ptoff);
@@ -3696,9 +3968,49 @@ static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int n
   return SWX_OK;
 }
 
+// column of table-analysis item `it` (items are m-major)
+static int item_col(int trunc, int it) {
+  int n = 0;
+  for (int c = 0; c <= trunc; ++c) {
+    if (n >= it) return c;
+    n += (trunc + 1 - c + kTL - 1) / kTL;
+  }
+  return trunc + 1;
+}
+
 template <int MODE>
 static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
                                const double2 *sub = nullptr, int it0 = 0, int it1 = -1) {
+  // SWX_ANA_OTF: 0 (default) stream the P table, 1 generate P in the MMA fragments,
+  // 2 generate it for the differenced tendency only (N(a) - N(u) of
+  // the ETD2RK step: nothing runs beside it), stream it otherwise (the first
+  // tendency shares the SMs with the psi0 pole sum, which is FP64-bound: the
+  // HBM-bound table stream pairs better with it)
+  static const int otf = env_int("SWX_ANA_OTF", 0);
+  if (MODE == 0 && p->d_ack && (otf == 1 || (otf == 2 && sub))) {
+    const int m0 = item_col(p->trunc, it0);
+    const int m1 = it1 < 0 ? p->trunc + 1 : item_col(p->trunc, it1);
+    if (m1 <= m0) return SWX_OK;
+    const size_t nt = p->nt16;
+    const size_t smem = sizeof(double) * (kAckRed + 4 * nt * kAG + nt) +
+                        sizeof(double2) * ((size_t)kAckSeg * ack_pitch(p->nt16) + kAckSeg * kAckSMax + 2) + 16;
+    static size_t attr = 0;  // the largest dynamic shared memory set so far
+    if (smem > attr) {
+      SWX_CUDA_TRY(cudaFuncSetAttribute(analysis_otf_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      SWX_CUDA_TRY(cudaGetDevice(&dev));
+      SWX_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    SWX_CUDA_TRY(launch_pdl(analysis_otf_kernel, dim3(std::min(m1 - m0, nsm)), dim3(kAckThreads), smem, s,
+                            static_cast<const ShtView &>(*p), A, out, sub, m0, m1 - m0));
+    SWX_LAUNCH_CHECK();
+    return SWX_OK;
+  }
   static const int stages = env_int("SWX_TAB_STAGES", 4);  // tuning: ring depth 4 or 8
   return stages == 8 ? launch_analysis_tab_k<MODE, 8>(p, A, out, nf, s, sub, it0, it1)
                      : launch_analysis_tab_k<MODE, 4>(p, A, out, nf, s, sub, it0, it1);
