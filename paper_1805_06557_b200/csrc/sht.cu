@@ -167,6 +167,11 @@ struct SynthArgs {
   int m0 = 0;
 };
 
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 // mbarrier / bulk-copy (TMA) helpers
 __device__ __forceinline__ unsigned smem_u32(const void *ptr) {
   return (unsigned)__cvta_generic_to_shared(ptr);
@@ -199,6 +204,21 @@ __device__ __forceinline__ void bulk_g2s(double *dst, const double *src, unsigne
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// the same with an L2 eviction-priority policy (createpolicy) on the loaded lines
+__device__ __forceinline__ void tma_2d_hint(double *dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 
 __device__ __forceinline__ void tma_2d(double *dst, const CUtensorMap *map, int c0, int c1,
@@ -3176,6 +3196,9 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
     // column read neighbouring finite rows or zeros; they only feed masked or
     // discarded outputs) -- and the 4 (2) prepared-row blocks of the stage
     if (lane != 0) return;
+    // the P table is read by both tendencies of an ETD2RK step: keep its
+    // lines ahead of the streamed data in the L2 replacement order
+    const uint64_t pol = l2_evict_last_policy();
     const unsigned bytes =
         (unsigned)((2 * kTBoxRows * kPR + NPART * 2 * kTK * kAG) * sizeof(double));
     int q = 0;  // sequence number of the stage being filled
@@ -3193,8 +3216,8 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
         mbar_expect_tx(full + slot, bytes);
         double *sb = tsm + (size_t)slot * kStage;
         const int k0 = st * kTK;
-        tma_2d(sb, &tmap, k0, row0, full + slot);
-        tma_2d(sb + kP1, &tmap, k0, row1, full + slot);
+        tma_2d_hint(sb, &tmap, k0, row0, full + slot, pol);
+        tma_2d_hint(sb + kP1, &tmap, k0, row1, full + slot, pol);
 #pragma unroll
         for (int b = 0; b < NPART * 2; ++b)  // part * 2 + parity
           bulk_g2s(sb + kSB + b * kTK * kAG, Ab + (size_t)b * ps + (size_t)k0 * kAG,
@@ -3931,10 +3954,6 @@ static int launch_analysis(swx_sht p, const double *A, const double2 *Q, const d
 
 // state-synthesis geometry (tuning overrides SWX_SYNTH_NT / SWX_SYNTH_SPLIT):
 // pairs per CTA half and whether long columns are split over two halves
-static int env_int(const char *name, int dflt) {
-  const char *e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
 
 template <int MODE, int KTS>
 static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
@@ -3969,6 +3988,7 @@ static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int n
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
+
 
 // column of table-analysis item `it` (items are m-major)
 static int item_col(int trunc, int it) {
