@@ -305,17 +305,6 @@ int swx_host_pack(int trunc, int n_fields, const swx_c128 *const *h_dense,
                   swx_c128 *h_packed);
 int swx_host_unpack(int trunc, int n_fields, const swx_c128 *h_packed,
                     swx_c128 *const *h_dense);
-/* One end-to-end step at the API edge with host/device overlap (the
- * EtdrkStepper.step path): field f is packed into the handle's pinned
- * staging while field f-1's H2D copy runs, the caller's instantiated step
- * graph (cudaGraphExec_t updating d_state in place) is launched on `stream`,
- * and field f is unpacked into h_dense_out[f] while field f+1's D2H copy
- * runs.  Synchronises `stream`'s D2H copies before returning.               */
-typedef struct swx_e2e_s *swx_e2e;
-int swx_e2e_create(swx_e2e *out, int trunc, int n_fields);
-int swx_e2e_destroy(swx_e2e e);
-int swx_e2e_step(swx_e2e e, const swx_c128 *const *h_dense_in, swx_c128 *d_state,
-                 void *graph_exec, swx_c128 *const *h_dense_out, void *stream);
 
 /* ---- measurement helpers (bench.py) ---------------------------------------
  * swx_sht_tendency with per-stage device times (ms) written to h_stage_ms[7]:

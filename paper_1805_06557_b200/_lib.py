@@ -63,9 +63,6 @@ SIGNATURES = {
     "swx_fp64_fma_probe": (_I, [_P, _I, _I, _P]),
     "swx_host_pack": (_I, [_I, _I, _P, _P]),
     "swx_host_unpack": (_I, [_I, _I, _P, _P]),
-    "swx_e2e_create": (_I, [ctypes.POINTER(_P), _I, _I]),
-    "swx_e2e_destroy": (_I, [_P]),
-    "swx_e2e_step": (_I, [_P, _P, _P, _P, _P, _P]),
     "swx_trace": (_I, [_I, _P, _I]),
     "swx_trace_rexi": (_I, [_I, _P, _I]),
     "swx_shard_init": (_I, [_P, _I, _I, _I, _I]),

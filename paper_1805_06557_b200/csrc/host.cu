@@ -70,71 +70,3 @@ extern "C" int swx_host_unpack(int trunc, int n_fields, const swx_c128 *h_packed
   convert<false>(trunc, n_fields, nullptr, h_dense, h_packed, nullptr);
   return SWX_OK;
 }
-
-// ---------------------------------------------------------------------------
-// End-to-end step at the API edge with host/device overlap: pack field f into
-// pinned memory while field f-1's H2D copy is in flight, replay the caller's
-// step graph, then unpack field f while field f+1's D2H copy is in flight.
-// ---------------------------------------------------------------------------
-#include <cuda_runtime.h>
-
-struct swx_e2e_s {
-  int trunc = 0, n_fields = 3;
-  long nc = 0;
-  swx_c128 *pin_in = nullptr, *pin_out = nullptr;
-  cudaEvent_t ev[8] = {};
-};
-
-extern "C" int swx_e2e_create(swx_e2e *out, int trunc, int n_fields) {
-  if (!out || trunc < 0 || n_fields < 1 || n_fields > 8) return SWX_ERR_CONFIG;
-  auto *e = new swx_e2e_s();
-  e->trunc = trunc;
-  e->n_fields = n_fields;
-  e->nc = (long)(trunc + 1) * (trunc + 2) / 2;
-  const size_t bytes = sizeof(swx_c128) * e->nc * n_fields;
-  bool ok = cudaHostAlloc(&e->pin_in, bytes, cudaHostAllocDefault) == cudaSuccess &&
-            cudaHostAlloc(&e->pin_out, bytes, cudaHostAllocDefault) == cudaSuccess;
-  for (int f = 0; ok && f < n_fields; ++f)
-    ok = cudaEventCreateWithFlags(&e->ev[f], cudaEventDisableTiming) == cudaSuccess;
-  if (!ok) {
-    swx_e2e_destroy(e);
-    return SWX_ERR_CUDA;
-  }
-  *out = e;
-  return SWX_OK;
-}
-
-extern "C" int swx_e2e_destroy(swx_e2e e) {
-  if (!e) return SWX_OK;
-  cudaFreeHost(e->pin_in);
-  cudaFreeHost(e->pin_out);
-  for (int f = 0; f < e->n_fields; ++f)
-    if (e->ev[f]) cudaEventDestroy(e->ev[f]);
-  delete e;
-  return SWX_OK;
-}
-
-extern "C" int swx_e2e_step(swx_e2e e, const swx_c128 *const *h_dense_in, swx_c128 *d_state,
-                            void *graph_exec, swx_c128 *const *h_dense_out, void *stream) {
-  if (!e || !h_dense_in || !d_state || !graph_exec || !h_dense_out) return SWX_ERR_CONFIG;
-  cudaStream_t s = (cudaStream_t)stream;
-  const size_t fb = sizeof(swx_c128) * e->nc;
-  for (int f = 0; f < e->n_fields; ++f) {
-    convert<true>(e->trunc, 1, h_dense_in + f, nullptr, nullptr, e->pin_in + f * e->nc);
-    if (cudaMemcpyAsync(d_state + f * e->nc, e->pin_in + f * e->nc, fb, cudaMemcpyHostToDevice,
-                        s) != cudaSuccess)
-      return SWX_ERR_CUDA;
-  }
-  if (cudaGraphLaunch((cudaGraphExec_t)graph_exec, s) != cudaSuccess) return SWX_ERR_CUDA;
-  for (int f = 0; f < e->n_fields; ++f) {
-    if (cudaMemcpyAsync(e->pin_out + f * e->nc, d_state + f * e->nc, fb, cudaMemcpyDeviceToHost,
-                        s) != cudaSuccess ||
-        cudaEventRecord(e->ev[f], s) != cudaSuccess)
-      return SWX_ERR_CUDA;
-  }
-  for (int f = 0; f < e->n_fields; ++f) {
-    if (cudaEventSynchronize(e->ev[f]) != cudaSuccess) return SWX_ERR_CUDA;
-    convert<false>(e->trunc, 1, nullptr, h_dense_out + f, e->pin_out + f * e->nc, nullptr);
-  }
-  return SWX_OK;
-}

@@ -427,209 +427,6 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
   trace_mark(6);
 }
 
-// K1 (persistent form): the lane-group mapping of rexi_lg_mm_kernel over
-// one-pass items (l, 32 modes) sorted largest first and dealt round-robin to
-// sm_count x occupancy persistent CTAs, so every SM gets the same number of
-// items (the one-shot grid of 645 two-pass CTAs runs 1.45 waves at T256);
-// item k+1's factor table streams into the second shared-memory buffer
-// (cp.async) while item k computes.  Same trees, same bits.
-__device__ __forceinline__ void lg_cp16(void *dst, const void *src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-}
-
-template <int NRHS, int NP, int LPM, int MPL>
-__global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_pers_kernel(
-    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
-    const int4 *__restrict__ sched, int n_items, int realify, Axpy ep, int fac_ready,
-    double2 *__restrict__ out) {
-  constexpr int PPL = NP / LPM;
-  constexpr int GROUPS = 128 / LPM;
-  constexpr int TAB = NRHS * 4 * NP;     // double2 per factor table
-  extern __shared__ double2 fac2[];      // [2][TAB]
-  pdl_trigger();
-  if (!fac_ready) pdl_wait();
-  auto stage = [&](int it, int buf) {
-    const double2 *src = fac_g + (size_t)sched[it].x * TAB;
-    double2 *dst = fac2 + buf * TAB;
-    for (int i = threadIdx.x; i < TAB; i += blockDim.x) lg_cp16(dst + i, src + i);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  int it = blockIdx.x;
-  if (it < n_items) stage(it, 0);
-  pdl_wait();
-  const int q = threadIdx.x & (LPM - 1);
-  const int g = threadIdx.x / LPM;
-  for (int k = 0; it < n_items; it += gridDim.x, ++k) {
-    const int nxt = it + gridDim.x;
-    if (nxt < n_items) {
-      stage(nxt, (k + 1) & 1);
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    }
-    __syncthreads();
-    const double2 *fac = fac2 + (k & 1) * TAB;
-    const int4 w = sched[it];
-    const int l = w.x, m0 = w.y, m1 = w.z;
-    int m[MPL];
-    bool has[MPL];
-    size_t idx[MPL];
-#pragma unroll
-    for (int j = 0; j < MPL; ++j) {
-      m[j] = m0 + g + j * GROUPS;
-      has[j] = m[j] < m1;
-      idx[j] = has[j] ? (size_t)col_offset(trunc, m[j]) + (l - m[j]) : 0;
-    }
-#pragma unroll 1
-    for (int r = 0; r < NRHS; ++r) {
-      const double2 *F = fac + (size_t)r * 4 * NP + q;
-      double2 bp[MPL], bz[MPL], bd[MPL], e[MPL][3];
-#pragma unroll
-      for (int j = 0; j < MPL; ++j) {
-        bp[j] = bz[j] = bd[j] = make_double2(0.0, 0.0);
-        if (has[j]) {
-          bp[j] = rhs[(size_t)(r * 3 + 0) * ncoef + idx[j]];
-          bz[j] = rhs[(size_t)(r * 3 + 1) * ncoef + idx[j]];
-          bd[j] = rhs[(size_t)(r * 3 + 2) * ncoef + idx[j]];
-        }
-        if (ep.base && has[j] && q == 0)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) e[j][c] = ep.base[(size_t)(r * 3 + c) * ncoef + idx[j]];
-      }
-      PhiDiv pd[MPL];
-      double2 z[MPL];
-      tree_pd_m<PPL, MPL, true>(F, F + NP, F + 2 * NP, 0, LPM, bp, bd, pd);
-      tree_z_m<PPL, MPL, true>(F + 3 * NP, 0, LPM, bz, z);
-#pragma unroll
-      for (int o = 1; o < LPM; o <<= 1)
-#pragma unroll
-        for (int j = 0; j < MPL; ++j) {
-          pd[j].p = cadd(pd[j].p, shfl_xor2(pd[j].p, o));
-          pd[j].d = cadd(pd[j].d, shfl_xor2(pd[j].d, o));
-          z[j] = cadd(z[j], shfl_xor2(z[j], o));
-        }
-#pragma unroll
-      for (int j = 0; j < MPL; ++j)
-        if (has[j] && q == 0) {
-          if (realify && m[j] == 0) pd[j].p.y = z[j].y = pd[j].d.y = 0.0;
-          const size_t o = (size_t)r * 3 * ncoef + idx[j];
-          double2 v[3] = {pd[j].p, z[j], pd[j].d};
-          if (ep.base)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              v[c] = make_double2(e[j][c].x + v[c].x * ep.scale, e[j][c].y + v[c].y * ep.scale);
-#pragma unroll
-          for (int c = 0; c < 3; ++c) out[o + (size_t)c * ncoef] = v[c];
-        }
-    }
-    __syncthreads();  // buffer k & 1 is restaged by item k + 2
-  }
-}
-
-// K1 (warp form): one warp = 32 modes of one degree l, one lane = one mode
-// walking all NP poles itself, so no lane-group butterfly and no shared
-// memory: the per-(pole, l) factors are warp-uniform loads (one L1 line
-// serves the whole warp).  Blocks of 32 poles are statically unrolled trees
-// with pair leaves; blocks combine through a binary counter -- the same
-// perfect pairwise tree (tree_sum's order) as rexi_lg_mm_kernel<..., true>,
-// hence identical bits.  1-warp CTAs, one per 32-mode item, all resident at
-// once at T256 (1161 warps): the load balances over the SMs without waves.
-// Factor layout: natural pole order (lg_geom lpm = 1).
-template <int NRHS, int NP>
-__global__ void __launch_bounds__(32) rexi_lg_warp_kernel(
-    const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
-    const int4 *__restrict__ sched, int realify, Axpy ep, int fac_ready,
-    double2 *__restrict__ out) {
-  constexpr int NB = NP / 32;  // 32-pole blocks
-  static_assert(NB >= 1 && NB <= (1 << kLgLevels), "pole count");
-  pdl_trigger();
-  const int4 w = sched[blockIdx.x];
-  const int l = w.x, m = w.y + (int)threadIdx.x;
-  const bool has = m < w.z;
-  const size_t idx = has ? (size_t)col_offset(trunc, m) + (l - m) : 0;
-  extern __shared__ double2 fsm[];  // [NRHS][4][NP]
-  {
-    // factor tables do not depend on the preceding kernel: stage them first
-    // (PDL overlap); all loads in flight before the first store
-    if (!fac_ready) pdl_wait();
-    const double4 *src = reinterpret_cast<const double4 *>(fac_g + (size_t)l * NRHS * 4 * NP);
-    double4 *dst = reinterpret_cast<double4 *>(fsm);
-    constexpr int N4 = NRHS * 2 * NP, PER = N4 / 32;
-    double4 t[PER < 16 ? PER : 16];
-#pragma unroll
-    for (int c0 = 0; c0 < PER; c0 += 16) {
-#pragma unroll
-      for (int c = 0; c < 16 && c0 + c < PER; ++c) t[c] = src[(c0 + c) * 32 + threadIdx.x];
-#pragma unroll
-      for (int c = 0; c < 16 && c0 + c < PER; ++c) dst[(c0 + c) * 32 + threadIdx.x] = t[c];
-    }
-    __syncwarp();
-  }
-  pdl_wait();
-#pragma unroll 1
-  for (int r = 0; r < NRHS; ++r) {
-    const double2 *F = fsm + (size_t)r * 4 * NP;
-    double2 bp[1] = {make_double2(0.0, 0.0)}, bz[1] = {bp[0]}, bd[1] = {bp[0]};
-    double2 e[3];
-    if (has) {
-      bp[0] = rhs[(size_t)(r * 3 + 0) * ncoef + idx];
-      bz[0] = rhs[(size_t)(r * 3 + 1) * ncoef + idx];
-      bd[0] = rhs[(size_t)(r * 3 + 2) * ncoef + idx];
-      if (ep.base)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) e[c] = ep.base[(size_t)(r * 3 + c) * ncoef + idx];
-    }
-    // (phi', div) tree, then the vort tree (halves the live state)
-    PhiDiv stk[kLgLevels], v[1];
-#pragma unroll 1
-    for (int blk = 0; blk < NB; ++blk) {
-      const double2 *Fb = F + blk * 32;
-      tree_pd_m<32, 1, true>(Fb, Fb + NP, Fb + 2 * NP, 0, 1, bp, bd, v);
-      bool done = false;
-#pragma unroll
-      for (int lv = 0; lv < kLgLevels; ++lv)
-        if (!done) {
-          if ((blk >> lv) & 1) {
-            v[0].p = cadd(stk[lv].p, v[0].p);
-            v[0].d = cadd(stk[lv].d, v[0].d);
-          } else {
-            stk[lv] = v[0];
-            done = true;
-          }
-        }
-    }
-    double2 zs[kLgLevels], z[1];
-#pragma unroll 1
-    for (int blk = 0; blk < NB; ++blk) {
-      tree_z_m<32, 1, true>(F + 3 * NP + blk * 32, 0, 1, bz, z);
-      bool done = false;
-#pragma unroll
-      for (int lv = 0; lv < kLgLevels; ++lv)
-        if (!done) {
-          if ((blk >> lv) & 1) {
-            z[0] = cadd(zs[lv], z[0]);
-          } else {
-            zs[lv] = z[0];
-            done = true;
-          }
-        }
-    }
-    if (has) {
-      PhiDiv pd = v[0];
-      double2 zz = z[0];
-      if (realify && m == 0) pd.p.y = zz.y = pd.d.y = 0.0;
-      const size_t o = (size_t)r * 3 * ncoef + idx;
-      double2 val[3] = {pd.p, zz, pd.d};
-      if (ep.base)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          val[c] = make_double2(e[c].x + val[c].x * ep.scale, e[c].y + val[c].y * ep.scale);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) out[o + (size_t)c * ncoef] = val[c];
-    }
-  }
-}
 
 // =====================================================================
 // K2: Coriolis-group chains.  With phi' eliminated (phi_l = (bphi_l +
@@ -828,12 +625,9 @@ __global__ void l_pack_kernel(const double2 *__restrict__ rhs, const double *__r
 
 // fills the pivot cache: one thread per (pole, m, chain), the forward sweep
 // of l_fwd (poles >= P use alpha = 1 like the pole-sum kernel's idle lanes)
-__host__ __device__ inline int l_tw_top_segs(int nseg) { return nseg >= 2 ? (nseg + 1) / 2 : nseg; }
-
 __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_pad, int trunc,
                                int ncoef, const double *__restrict__ lconst,
-                               const double *__restrict__ chain, double2 *__restrict__ linv,
-                               int twisted) {
+                               const double *__restrict__ chain, double2 *__restrict__ linv) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)P_pad * (trunc + 1) * 2;
   if (t >= total) return;
@@ -848,14 +642,8 @@ __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_p
   const double *gl = lconst + (trunc + 1);
   const int off = col_offset(trunc, m);
   const int nl = trunc + 1 - m;
-  // twisted layout (rexi_l_tw_kernel): top-down pivots below mid, bottom-up above
-  int mid = nl;
-  if (twisted) {
-    const int nseg = (nl + kLSeg - 1) / kLSeg, nsT = l_tw_top_segs(nseg);
-    if (nsT < nseg) mid = nsT * kLSeg;
-  }
   double2 cp = make_double2(0.0, 0.0);
-  for (int k = 0; k < mid; ++k) {
+  for (int k = 0; k < nl; ++k) {
     const int s = off + k;
     const bool isz = ((k + c) & 1) == 0;
     const double sg = isz ? -1.0 : 1.0;
@@ -868,22 +656,6 @@ __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_p
     const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
     const double2 inv = crecip(den);
     cp = cscale(sup, inv);
-    linv[linv_at(gp, ncoef, s, c)] = inv;
-  }
-  double2 ap = make_double2(0.0, 0.0);  // a''_{k+1}
-  for (int k = nl - 1; k >= mid; --k) {
-    const int s = off + k;
-    const bool isz = ((k + c) & 1) == 0;
-    const double sg = isz ? -1.0 : 1.0;
-    const double sub = sg * chain[s], sup = sg * chain[ncoef + s];
-    double2 diag = make_double2(a.x, a.y + chain[2 * ncoef + s]);
-    if (!isz) {
-      diag.x = fma(gl[m + k], ia.x, diag.x);
-      diag.y = fma(gl[m + k], ia.y, diag.y);
-    }
-    const double2 den = make_double2(fma(-sup, ap.x, diag.x), fma(-sup, ap.y, diag.y));
-    const double2 inv = crecip(den);
-    ap = cscale(sub, inv);
     linv[linv_at(gp, ncoef, s, c)] = inv;
   }
 }
@@ -1167,338 +939,7 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
   }
 }
 
-// ---------------------------------------------------------------------------
-// Twisted ("burn at both ends") chain solve over the pivot cache.  A warp
-// pair shares an item (m, 32-pole block): the top warp eliminates positions
-// [0, mid) downwards (pivots 1/den+ in the cache), the bottom warp positions
-// [mid, n) upwards (pivots 1/den- stored at those positions), the two meet
-// in a 2x2 interface solve for x_mid, then substitute outwards.  Each warp
-// walks half the chain, so the serial depth per item halves; items are
-// dealt to warp pairs longest first to the least-loaded pair (host LPT).
-//   top:    x_k + c'_k x_{k+1} = y_k,   c'_k = sup_k/den+_k
-//   bottom: x_k + a''_k x_{k-1} = z_k,  a''_k = sub_k/den-_k,
-//           den-_k = diag_k - sup_k a''_{k+1},  z_k = (r_k - sup_k z_{k+1})/den-_k
-//   x_mid = (z_mid - a''_mid y_{mid-1}) / (1 - a''_mid c'_{mid-1})
-// ---------------------------------------------------------------------------
-// upward (bottom) step: z = (q - sup z_prev) inv-
-template <int NRHS>
-__device__ __forceinline__ void l_bwd_c(const LPos<NRHS> &e, bool isz, double2 ia, double2 inv,
-                                        double2 (&z)[NRHS]) {
-  const double sup = (isz ? -1.0 : 1.0) * e.U;
-#pragma unroll
-  for (int r = 0; r < NRHS; ++r) {
-    double2 q;
-    if (isz) {
-      q = e.bz[r];
-    } else {
-      const double2 t = make_double2(e.h * ia.x, e.h * ia.y);
-      q = csub(e.bd[r], cmul(t, e.bp[r]));
-    }
-    q = make_double2(fma(-sup, z[r].x, q.x), fma(-sup, z[r].y, q.y));
-    z[r] = cmul(q, inv);
-  }
-}
 
-__device__ __forceinline__ double2 cdiv_l(double2 a, double2 b) { return cmul(a, crecip(b)); }
-
-template <int NRHS>
-__global__ void __launch_bounds__(kLWarps * 32, SWX_LC_MINB) rexi_l_tw_kernel(
-    const double2 *__restrict__ alpha, const double2 *__restrict__ beta, int beta_stride,
-    int pole0, int P, int n_blocks, int trunc, int ncoef, double dt, double phibar,
-    double2 *__restrict__ scratch, double2 *__restrict__ part, const double2 *__restrict__ linv,
-    const LPos<NRHS> *__restrict__ lpos, const int2 *__restrict__ slots,
-    const int *__restrict__ items) {
-  extern __shared__ double2 red_raw[];
-  auto red = reinterpret_cast<double2 (*)[kFRows][NRHS][2][32]>(red_raw);
-  __shared__ double2 xch[kLWarps / 2][2][2][NRHS + 1][32];  // [pair][top|bottom][chain][y|z.., c'|a'']
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pr = warp >> 1;
-  const bool bot = (warp & 1) != 0;
-  constexpr int PW = (int)(sizeof(LPos<NRHS>) / sizeof(double2));
-  constexpr int SLOTW = kLSegW + kLSeg * PW;
-  double2 *ring = red_raw + (size_t)kLWarps * kFRows * NRHS * 2 * 32 + (size_t)warp * kLRing * SLOTW;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(red_raw + (size_t)kLWarps * kFRows * NRHS * 2 * 32 +
-                                                (size_t)kLWarps * kLRing * SLOTW) +
-                   warp * kLRing;
-  int seq = 0, cons = 0;
-  if (lane == 0)
-    for (int j = 0; j < kLRing; ++j) lc_bar_init(bars + j);
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  __syncwarp();
-  const int gwarp = blockIdx.x * kLWarps + warp;
-  const double dtpb = dt * phibar;
-  const int max_seg = (trunc + 1 + kLSeg - 1) / kLSeg;
-  constexpr int CKW = 2 * NRHS;
-  double2 *slot = scratch + (size_t)gwarp * max_seg * 32 * CKW;
-  const int2 rng = slots[blockIdx.x * (kLWarps / 2) + pr];
-  for (int it = rng.x; it < rng.y; ++it) {
-    const int item = items[it];
-    const int m = item / n_blocks;
-    const int pb = item - m * n_blocks;
-    const int pl = pb * 32 + lane;
-    const bool active = pl < P;
-    double2 a = make_double2(1.0, 0.0);
-    double2 bet[NRHS];
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) bet[r] = make_double2(0.0, 0.0);
-    if (active) {
-      a = alpha[pole0 + pl];
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) bet[r] = beta[r * beta_stride + pole0 + pl];
-    }
-    const double2 ia = crecip(a);
-    const int nl = trunc + 1 - m;
-    const int off = col_offset(trunc, m);
-    const int nseg = (nl + kLSeg - 1) / kLSeg;
-    const int nsT = l_tw_top_segs(nseg);
-    const bool split = nsT < nseg;
-    if (bot && !split) continue;  // short chain: the top warp solves it alone
-    const int mid = split ? nsT * kLSeg : nl;
-    const int nsw = bot ? nseg - nsT : nsT;  // this warp's segments
-    // this warp's segment in flat order f (pass 1 then pass 2)
-    auto seg_of = [&](int f) {
-      if (!bot) return f < nsw ? f : 2 * nsw - 1 - f;
-      return f < nsw ? nseg - 1 - f : nsT + (f - nsw);
-    };
-    const double2 *lsrc = linv + ((size_t)((pole0 + pb * 32) >> 5) * ncoef + off) * 64;
-    const LPos<NRHS> *psrc = lpos + off;
-    auto issue = [&](int f) {
-      if (f < 2 * nsw) {
-        const int sg = seg_of(f);
-        const int cnt = min(kLSeg, nl - sg * kLSeg);
-        if (lane == 0) {
-          double2 *dst = ring + (seq % kLRing) * SLOTW;
-          uint64_t *bar = bars + seq % kLRing;
-          const unsigned bi = (unsigned)(cnt * 64 * sizeof(double2));
-          const unsigned bp = (unsigned)(cnt * sizeof(LPos<NRHS>));
-          lc_expect(bar, bi + bp);
-          lc_copy(dst, lsrc + (size_t)sg * kLSegW, bi, bar);
-          lc_copy(dst + kLSegW, psrc + (size_t)sg * kLSeg, bp, bar);
-        }
-        ++seq;
-      }
-    };
-    auto acquire = [&]() -> const double2 * {
-      lc_bar_wait(bars + cons % kLRing, (cons / kLRing) & 1);
-      return ring + (cons % kLRing) * SLOTW;
-    };
-    auto release = [&](int f) {
-      __syncwarp();
-      ++cons;
-      issue(f + kLRing);
-    };
-    for (int i = 0; i < kLRing; ++i) issue(i);
-    // ---- pass 1: eliminate towards the interface, checkpoint every segment
-    double2 y[2][NRHS], edge[2];  // edge: c'_{mid-1} (top) or a''_mid (bottom)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      edge[c] = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) y[c][r] = make_double2(0.0, 0.0);
-    }
-    for (int f = 0; f < nsw; ++f) {
-      const int sg = seg_of(f);
-      double2 *dst = slot + ((size_t)f * 32 + lane) * CKW;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) dst[c * NRHS + r] = y[c][r];
-      const int k0 = sg * kLSeg;
-      const int n = min(kLSeg, nl - k0);
-      const double2 *iv = acquire();
-      const LPos<NRHS> *sq = reinterpret_cast<const LPos<NRHS> *>(iv + kLSegW);
-      if (!bot) {
-#pragma unroll
-        for (int e = 0; e < kLSeg; ++e) {
-          if (e < n) {
-            const int k = k0 + e;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const bool isz = ((k + c) & 1) == 0;
-              const double2 inv = iv[e * 64 + c * 32 + lane];
-              l_fwd_c<NRHS>(sq[e], isz, ia, inv, y[c]);
-              if (k == mid - 1) edge[c] = cscale((isz ? -1.0 : 1.0) * sq[e].U, inv);
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = kLSeg - 1; e >= 0; --e) {
-          if (e < n) {
-            const int k = k0 + e;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const bool isz = ((k + c) & 1) == 0;
-              const double2 inv = iv[e * 64 + c * 32 + lane];
-              l_bwd_c<NRHS>(sq[e], isz, ia, inv, y[c]);
-              if (k == mid) edge[c] = cscale((isz ? -1.0 : 1.0) * sq[e].L, inv);
-            }
-          }
-        }
-      }
-      release(f);
-    }
-    // ---- interface: x_mid from both ends (shared through the pair's slots)
-    double2 xs[2][NRHS];  // top: x_mid (to substitute downwards); bottom: x_{mid-1}
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) xs[c][r] = make_double2(0.0, 0.0);
-    if (split) {
-      const int me = bot ? 1 : 0;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) xch[pr][me][c][r][lane] = y[c][r];
-        xch[pr][me][c][NRHS][lane] = edge[c];
-      }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pr) : "memory");
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const double2 cpt = xch[pr][0][c][NRHS][lane], app = xch[pr][1][c][NRHS][lane];
-        const double2 den = csub(make_double2(1.0, 0.0), cmul(app, cpt));
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) {
-          const double2 yt = xch[pr][0][c][r][lane], zb = xch[pr][1][c][r][lane];
-          const double2 xm = cdiv_l(csub(zb, cmul(app, yt)), den);
-          xs[c][r] = bot ? csub(yt, cmul(cpt, xm)) : xm;
-        }
-      }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pr) : "memory");  // slots reusable
-    }
-    // ---- pass 2: recompute each segment from its checkpoint, substitute outwards
-    double2 ck[2][NRHS];
-    auto load_ck = [&](int f) {
-      const double2 *src = slot + ((size_t)f * 32 + lane) * CKW;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) ck[c][r] = src[c * NRHS + r];
-    };
-    load_ck(nsw - 1);
-    int gcnt = 0, gk0a = 0, gna = 0, gk0b = 0, gnb = 0;
-    for (int f2 = 0; f2 < nsw; ++f2) {
-      const int f = nsw + f2;     // flat index of this block
-      const int jck = nsw - 1 - f2;  // pass-1 checkpoint of this segment
-      const int sg = seg_of(f);
-      const int k0 = sg * kLSeg;
-      const int n = min(kLSeg, nl - k0);
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) y[c][r] = ck[c][r];
-      if (jck > 0) load_ck(jck - 1);
-      const double2 *iv = acquire();
-      const LPos<NRHS> *sq = reinterpret_cast<const LPos<NRHS> *>(iv + kLSegW);
-      double2 bps[kLSeg][NRHS], cps[2][kLSeg], ys[2][NRHS][kLSeg];
-      if (!bot) {
-#pragma unroll
-        for (int e = 0; e < kLSeg; ++e) {
-          if (e < n) {
-            const int k = k0 + e;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const bool isz = ((k + c) & 1) == 0;
-              const double2 inv = iv[e * 64 + c * 32 + lane];
-              l_fwd_c<NRHS>(sq[e], isz, ia, inv, y[c]);
-              cps[c][e] = cscale((isz ? -1.0 : 1.0) * sq[e].U, inv);
-#pragma unroll
-              for (int r = 0; r < NRHS; ++r) ys[c][r][e] = y[c][r];
-            }
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r) bps[e][r] = sq[e].bp[r];
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = kLSeg - 1; e >= 0; --e) {
-          if (e < n) {
-            const int k = k0 + e;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const bool isz = ((k + c) & 1) == 0;
-              const double2 inv = iv[e * 64 + c * 32 + lane];
-              l_bwd_c<NRHS>(sq[e], isz, ia, inv, y[c]);
-              cps[c][e] = cscale((isz ? -1.0 : 1.0) * sq[e].L, inv);  // a''_k
-#pragma unroll
-              for (int r = 0; r < NRHS; ++r) ys[c][r][e] = y[c][r];
-            }
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r) bps[e][r] = sq[e].bp[r];
-          }
-        }
-      }
-      release(f);
-      // substitution (top: downwards, bottom: upwards); row = slot*kFlush + step*2 + chain
-#pragma unroll
-      for (int st = 0; st < kLSeg; ++st) {
-        const int e = bot ? st : kLSeg - 1 - st;
-        if (e < n) {
-          const int k = k0 + e;
-          const int stp = bot ? e : n - 1 - e;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const bool isz = ((k + c) & 1) == 0;
-            const int er = gcnt * kFlush + stp * 2 + c;
-            const int phys = lane ^ er;
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r) {
-              const double2 x = csub(ys[c][r][e], cmul(cps[c][e], xs[c][r]));
-              xs[c][r] = x;
-              red[warp][er][r][0][phys] = cmul(bet[r], x);
-              if (!isz) {
-                const double2 b = bps[e][r];
-                const double2 ph = cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), ia);
-                red[warp][er][r][1][phys] = cmul(bet[r], ph);
-              }
-            }
-          }
-        }
-      }
-      if (gcnt == 0) {
-        gk0a = k0;
-        gna = n;
-      } else {
-        gk0b = k0;
-        gnb = n;
-      }
-      if (++gcnt < kFS && f2 + 1 < nsw) continue;
-      __syncwarp();
-      constexpr int LPR = 32 / kFRows, PR = 32 / LPR;
-      const int ee = lane / LPR, q = lane % LPR;
-      const int slot_e = ee / kFlush, within = ee % kFlush;
-      const int ns = slot_e == 0 ? gna : gnb, k0s = slot_e == 0 ? gk0a : gk0b;
-      const bool valid = slot_e < gcnt && within < 2 * ns;
-      const int eidx = valid ? ee : 0;
-      const int stpw = within >> 1, ec = within & 1;
-      const int epos = bot ? stpw : ns - 1 - stpw;
-      const int kk = k0s + epos;
-      const bool eisz = ((kk + ec) & 1) == 0;
-      gcnt = 0;
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) {
-#pragma unroll
-        for (int comp = 0; comp < 2; ++comp) {
-          double2 v[PR];
-#pragma unroll
-          for (int i = 0; i < PR; ++i) v[i] = red[warp][eidx][r][comp][(PR * q + i) ^ eidx];
-#pragma unroll
-          for (int w = 1; w < PR; w <<= 1)
-#pragma unroll
-            for (int i = 0; i < PR; i += 2 * w) v[i] = cadd(v[i], v[i + w]);
-          double2 acc = v[0];
-#pragma unroll
-          for (int o = 1; o < LPR; o <<= 1) acc = cadd(acc, shfl_xor2(acc, o));
-          if (q == 0 && valid && (comp == 0 || !eisz)) {
-            const int field = comp == 1 ? 0 : (eisz ? 1 : 2);
-            part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + kk] = acc;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
 
 // warm-up guard for the l group: forward sweep only, min |pivot|^2 per
 // (pole, m, chain); flags the first offending (pole, m) (solvers.py:176-184)
@@ -1737,10 +1178,6 @@ extern "C" int swx_solver_destroy(swx_solver s) {
   cudaFree(s->d_chain);
   cudaFree(s->d_alpha);
   cudaFree(s->d_linv);
-  for (auto &kv : s->tw_sched) {
-    cudaFree(kv.second.first);
-    cudaFree(kv.second.second);
-  }
   for (auto &kv : s->lg_sched) cudaFree(kv.second.first);
   delete[] s->h_norm;
   delete[] s->h_alpha;
@@ -1831,10 +1268,6 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
     s->d_linv = nullptr;
     s->linv_bytes = 0;
     const char *ev = getenv("SWX_L_CACHE");
-    // SWX_L_TWIST=1: twisted layout + rexi_l_tw_kernel (correct; measured no
-    // faster at cfg1 (0.091 vs 0.092 ms) and slower at cfg4 (22.1 vs 14.2 ms))
-    const char *et = getenv("SWX_L_TWIST");
-    s->linv_tw = et && atoi(et) != 0;
     if (!ev || atoi(ev) != 0) {
       const int p_pad = ((n_poles + 31) / 32 + 1) * 32;  // + one block for idle lanes
       const size_t bytes = (size_t)p_pad * s->ncoef * 2 * sizeof(double2);
@@ -1844,8 +1277,7 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
         s->linv_bytes = bytes;
         const long long threads = (long long)p_pad * n * 2;
         l_cache_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-            s->d_alpha, n_poles, p_pad, s->trunc, s->ncoef, s->d_lconst, s->d_chain, s->d_linv,
-            s->linv_tw);
+            s->d_alpha, n_poles, p_pad, s->trunc, s->ncoef, s->d_lconst, s->d_chain, s->d_linv);
         SWX_LAUNCH_CHECK();
         SWX_CUDA_TRY(cudaStreamSynchronize(st));
       } else {
@@ -1886,25 +1318,10 @@ static int l_grid_warps(swx_solver s, int n_items) {
   return std::min(cap, ((n_items + kLWarps - 1) / kLWarps) * kLWarps);
 }
 
-// twisted kernel: persistent CTAs (resident per SM x SMs), two warp pairs each
-static int tw_ctas(int nrhs) {
-  static int per_sm[3] = {0, 0, 0};
-  if (!per_sm[nrhs]) {
-    int b = 0;
-    const size_t sm = l_smem_bytes(nrhs, true);
-    const void *k = nrhs == 1 ? (const void *)rexi_l_tw_kernel<1> : (const void *)rexi_l_tw_kernel<2>;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kLWarps * 32, sm);
-    per_sm[nrhs] = std::max(1, b);
-  }
-  return sm_count() * per_sm[nrhs];
-}
-
 static size_t l_scratch_bytes(swx_solver s, int n_rhs, int P) {
   const int nb = (P + 31) / 32;
   const int n_items = (s->trunc + 1) * nb;
   int warps = l_grid_warps(s, n_items);
-  if (s->d_linv && s->linv_tw) warps = std::max(warps, tw_ctas(n_rhs) * kLWarps);
   const int max_seg = (s->trunc + 1 + kLSeg - 1) / kLSeg;
   return (size_t)warps * max_seg * 32 * 2 * (1 + n_rhs) * sizeof(double2);
 }
@@ -1956,23 +1373,14 @@ struct LgGeom {
   int np, lpm, ppl, leaf, log2_ppl, log2_lpm;
 };
 
-// pole counts served by rexi_lg_warp_kernel (SWX_LG_WARP=0: the lane-group
-// kernels, for A/B measurements)
-static bool lg_warp_form(int np) {
-  static const int env = getenv("SWX_LG_WARP") ? atoi(getenv("SWX_LG_WARP")) : 0;
-  return env && (np == 128 || np == 256 || np == 512);
-}
-
 static int lg_geom(int P, LgGeom &g) {
   g.np = next_pow2(P);
   // lanes per mode / leaf subtree (tuning overrides: SWX_LG_LPM, SWX_LG_LEAF)
   static const int env_lpm = getenv("SWX_LG_LPM") ? atoi(getenv("SWX_LG_LPM")) : 8;
   static const int env_leaf = getenv("SWX_LG_LEAF") ? atoi(getenv("SWX_LG_LEAF")) : 8;
   g.lpm = std::min(env_lpm, g.np);
-  if (lg_warp_form(g.np)) g.lpm = 1;  // rexi_lg_warp_kernel: natural pole order
   g.ppl = g.np / g.lpm;
   g.leaf = std::min(g.ppl, env_leaf);
-  if (g.lpm == 1 && lg_warp_form(g.np)) g.leaf = 32;  // 32-pole blocks, <= 16 of them
   if (g.ppl / g.leaf > (1 << kLgLevels))
     return fail(SWX_ERR_CONFIG, "lg tree deeper than the register stack");
   g.log2_ppl = g.log2_lpm = 0;
@@ -2037,70 +1445,19 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
   }
   // static geometries of the common pole counts (128 / 256 / 512 poles, 8 lanes per mode)
   static const int env_mpl = getenv("SWX_LG_MPL") ? atoi(getenv("SWX_LG_MPL")) : 2;
-  if (g.lpm == 1 && lg_warp_form(g.np)) {
-    int n_items = 0;
-    const int4 *items = lg_schedule(s, 32, &n_items);
-    if (!items) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
-    auto k = g.np == 128 ? rexi_lg_warp_kernel<NRHS, 128>
-             : g.np == 256 ? rexi_lg_warp_kernel<NRHS, 256>
-                           : rexi_lg_warp_kernel<NRHS, 512>;
-    const size_t fsm = (size_t)NRHS * 4 * g.np * sizeof(double2);
-    static bool attr[2][3] = {{false, false, false}, {false, false, false}};
-    const int ai = g.np == 128 ? 0 : g.np == 256 ? 1 : 2;
-    if (fsm > 48 * 1024 && !attr[NRHS - 1][ai]) {
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-      attr[NRHS - 1][ai] = true;
-    }
-    SWX_CUDA_TRY(launch_pdl(k, dim3(n_items), dim3(32), fsm, st, rhs, fac, s->trunc, s->ncoef,
-                            items, realify, ep, fac_ready, out));
-    SWX_LAUNCH_CHECK();
-    return SWX_OK;
-  }
   // SWX_LG_PAIR=0: per-pole leaves (every term rounded before the tree)
   static const int env_pair = getenv("SWX_LG_PAIR") ? atoi(getenv("SWX_LG_PAIR")) : 1;
   if (g.lpm == 8 && g.ppl == 32 && env_mpl == 2) {
     auto k = env_pair ? rexi_lg_mm_kernel<NRHS, 256, 8, 2, true>
                       : rexi_lg_mm_kernel<NRHS, 256, 8, 2, false>;
-    static int per_sm[2][3] = {{0, 0, 0}, {0, 0, 0}};
-    if (!per_sm[env_pair][NRHS]) {
+    static bool attr[2][3] = {{false, false, false}, {false, false, false}};
+    if (!attr[env_pair][NRHS]) {
       if (smem > 48 * 1024)
         SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int b = 0;
-      SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, 128, smem));
-      per_sm[env_pair][NRHS] = std::max(b, 1);
+      attr[env_pair][NRHS] = true;
     }
-    // SWX_LG_PERSIST=2: persistent CTAs with double-buffered factor staging
-    static const int env_pers = getenv("SWX_LG_PERSIST") ? atoi(getenv("SWX_LG_PERSIST")) : 0;
-    if (env_pers == 2 && env_pair) {
-      auto kp = rexi_lg_pers_kernel<NRHS, 256, 8, 2>;
-      static int pp[3] = {0, 0, 0};
-      const size_t smem2 = 2 * smem;
-      if (!pp[NRHS]) {
-        if (smem2 > 48 * 1024)
-          SWX_CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        int b = 0;
-        SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kp, 128, smem2));
-        pp[NRHS] = std::max(b, 1);
-      }
-      int n_items = 0;
-      const int4 *items = lg_schedule(s, -32, &n_items);
-      if (!items) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
-      const int grid = std::min(n_items, sm_count() * pp[NRHS]);
-      SWX_CUDA_TRY(launch_pdl(kp, dim3(grid), dim3(128), smem2, st, rhs, fac, s->trunc, s->ncoef,
-                              items, n_items, realify, ep, fac_ready, out));
-      SWX_LAUNCH_CHECK();
-      return SWX_OK;
-    }
-    int n_items = n_cta;
-    const int4 *items = sched;
-    int grid = n_cta;
-    if (env_pers) {
-      items = lg_schedule(s, -32, &n_items);
-      if (!items) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
-      grid = std::min(n_items, sm_count() * per_sm[env_pair][NRHS]);
-    }
-    SWX_CUDA_TRY(launch_pdl(k, dim3(grid), dim3(128), smem, st, rhs, fac, s->trunc, s->ncoef,
-                            items, n_items, realify, ep, fac_ready, out));
+    SWX_CUDA_TRY(launch_pdl(k, dim3(n_cta), dim3(128), smem, st, rhs, fac, s->trunc, s->ncoef,
+                            sched, n_cta, realify, ep, fac_ready, out));
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
@@ -2151,7 +1508,7 @@ static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
   // the cached kernel streams 32-pole blocks of the pivot cache: aligned blocks only
   const bool cached = s->d_linv && pole0 % 32 == 0;
   const size_t smem = l_smem_bytes(NRHS, cached);
-  auto k = cached && !s->linv_tw ? rexi_l_kernel<NRHS, true> : rexi_l_kernel<NRHS, false>;
+  auto k = cached ? rexi_l_kernel<NRHS, true> : rexi_l_kernel<NRHS, false>;
   // packed per-position data (after the partials), streamed by the cached kernel
   const size_t stride_parts = (size_t)NRHS * 3 * s->ncoef * nb;
   LPos<NRHS> *lpos = reinterpret_cast<LPos<NRHS> *>(
@@ -2161,49 +1518,7 @@ static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
     l_pack_kernel<NRHS><<<gp, 128, 0, st>>>(rhs, s->d_lconst, s->d_chain, s->trunc, s->ncoef, lpos);
     SWX_LAUNCH_CHECK();
   }
-  if (cached && s->linv_tw) {
-    // twisted solve: warp pairs over LPT-balanced item lists (built once per geometry)
-    const int ctas = tw_ctas(NRHS), pairs = ctas * (kLWarps / 2);
-    auto &sc = s->tw_sched[std::make_pair(nb, pairs)];
-    if (!sc.first) {
-      std::vector<std::pair<int, int>> cost;  // (segments on the longer side, item)
-      for (int it = 0; it < n_items; ++it) {
-        const int m = it / nb, nl = s->trunc + 1 - m, nseg = (nl + kLSeg - 1) / kLSeg;
-        cost.push_back({l_tw_top_segs(nseg), it});
-      }
-      std::stable_sort(cost.begin(), cost.end(),
-                       [](const std::pair<int, int> &x, const std::pair<int, int> &y) {
-                         return x.first > y.first;
-                       });
-      std::vector<std::vector<int>> lists(pairs);
-      std::vector<long long> load(pairs, 0);
-      for (auto &c : cost) {
-        const int j = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        lists[j].push_back(c.second);
-        load[j] += c.first + 1;  // + the interface
-      }
-      std::vector<int2> rg(pairs);
-      std::vector<int> flat;
-      for (int j = 0; j < pairs; ++j) {
-        rg[j] = make_int2((int)flat.size(), (int)(flat.size() + lists[j].size()));
-        flat.insert(flat.end(), lists[j].begin(), lists[j].end());
-      }
-      int2 *d_rg = nullptr;
-      int *d_it = nullptr;
-      SWX_CUDA_TRY(cudaMalloc(&d_rg, sizeof(int2) * rg.size()));
-      SWX_CUDA_TRY(cudaMalloc(&d_it, sizeof(int) * std::max<size_t>(flat.size(), 1)));
-      SWX_CUDA_TRY(cudaMemcpy(d_rg, rg.data(), sizeof(int2) * rg.size(), cudaMemcpyHostToDevice));
-      SWX_CUDA_TRY(cudaMemcpy(d_it, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
-      sc = std::make_pair(d_rg, d_it);
-    }
-    auto kt = rexi_l_tw_kernel<NRHS>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kt<<<ctas, kLWarps * 32, smem, st>>>(s->d_alpha, betas, s->n_poles, pole0, P, nb, s->trunc,
-                                         s->ncoef, s->dt, s->phibar, scratch, part, s->d_linv,
-                                         lpos, sc.first, sc.second);
-    SWX_LAUNCH_CHECK();
-  } else {
+  {
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<warps / kLWarps, kLWarps * 32, smem, st>>>(

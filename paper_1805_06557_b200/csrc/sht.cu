@@ -99,28 +99,14 @@ struct ShtView {
   long long *d_ptoff = nullptr;
   double *d_ptab = nullptr;
   double *d_rcos16 = nullptr;  // 1/cos per padded pair (0 on padding)
-  int n_pitems = 0;            // state-synthesis items (m, first pair, pairs)
-  int4 *d_pitems = nullptr;
-  int n_sitems = 0;            // state-synthesis items (m, kb, ke, seg), longest first
-  int4 *d_sitems = nullptr;
-  int *d_scnt = nullptr;       // [m] arrival counters of split columns
-  double2 *d_spart = nullptr;  // [m][2][nh][14] partial sums of split columns
-  int tab_rows = 0;            // rows of the P table (both planes of every column)
-  int n_sblk = 0;              // table synthesis: CTAs and their item ranges
-  int2 *d_sblk = nullptr;      // [cta] [begin, end) into d_slist
-  int2 *d_slist = nullptr;     // (m, 16-pair block), LPT order per CTA
   int n_titems = 0;            // analysis warp items (m, l0, par)
   int4 *d_titems = nullptr;
-  // on-the-fly tendency analysis (T <= kAckTMax): P_k, P_{k+1} of every
-  // column, pair and segment start k = g * ack_steps(m), [m][g][nt16][2]
-  double *d_ack = nullptr;
 };
 
 struct swx_sht_s : ShtView {
   std::map<long long, cufftHandle> plans;
   cudaEvent_t synth_done = nullptr;  // recorded after each tendency's synthesis (optional)
   CUtensorMap ptab_map;    // 2D view [rows][nt16] of the P table, box kTBox x 17
-  CUtensorMap ptab_map16;  // the same view, box kPR x 16 (table synthesis)
 };
 
 namespace swx {
@@ -149,21 +135,8 @@ struct SynthArgs {
   // (X_s = X_n on the equator node), i.e. the packed row z = north + i south
   // at bin m and at bin N - m.
   int zpack = 0;
-  // cross-CTA column split (state synthesis): CTA b runs items[b] =
-  // (m, kb, ke, seg); seg >= 0 marks one of the two segments of a long
-  // column, whose partial sums meet in `part` and are combined in fixed
-  // order (segment 0 + segment 1) by whichever CTA arrives second (`cnt`)
-  const int4 *items = nullptr;
-  int *cnt = nullptr;
-  double2 *part = nullptr;
-  // nyb > 0: 1D grid, block b = column b / nyb, pair block b % nyb (all pair
-  // blocks of the long columns dispatch first)
-  int nyb = 0;
-  // pitems: CTA b runs column pitems[b].x for pairs [y, y + z) -- the long
-  // columns split over two SMs by latitude pairs, one CTA per SM
-  const int4 *pitems = nullptr;
   // first column of the launch (column-sharded tendency: CTA x runs column
-  // m0 + x of the default and nyb dispatches)
+  // m0 + x)
   int m0 = 0;
 };
 
@@ -341,51 +314,27 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
 // half starts mid-column (a multiple of kSeg) from the plan-time recurrence
 // checkpoint, halving the per-thread walk of the long columns; the halves'
 // partial sums are added in a fixed order (first + second).
-// SPLIT = 3 (state synthesis): two thread groups per latitude pair share the
-// staged column and each run the recurrence; group 0 sums (vort, div, phi'),
-// group 1 (psi, chi) and the two d/dlat series -- twice the warps on the long
-// columns' critical path, half the accumulators per thread; group 1 hands
-// its sums to group 0 through shared memory.
-// SPLIT = 4 (state synthesis): every staged chunk is walked twice from the
-// same recurrence state -- (vort, div, phi') first, then (psi, chi) and the
-// d/dlat series -- so fewer loaded coefficients are live at once and the
-// kernel fits two 7-warp CTAs per SM (<= 128 registers); the recurrence is
-// recomputed (3 of 17 FP64 per degree).
 template <int MODE, int SPLIT, bool PEER = false>
-__global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 : 512,
-                                  MODE == 0 && SPLIT == 1   ? SWX_SYNTH_MINB
-                                  : MODE == 0 && SPLIT == 4 ? 2
-                                                            : 1) synth_kernel(ShtView p,
-                                                                              SynthArgs a) {
-  constexpr bool GRP = SPLIT == 3;
-  constexpr bool TWO = SPLIT == 4;
-  constexpr int NSPL = GRP ? 2 : (TWO ? 1 : SPLIT);  // thread sets per CTA
+__global__ void __launch_bounds__(MODE == 0 && SPLIT == 1 ? 256 : 512,
+                                  MODE == 0 && SPLIT == 1 ? SWX_SYNTH_MINB : 1) synth_kernel(ShtView p,
+                                                                                         SynthArgs a) {
+  constexpr int NSPL = SPLIT;  // thread sets per CTA
   constexpr int NS = MODE == 0 ? 5 : 1;  // P series (vort, div, phi, psi, chi)
   constexpr int NH = MODE == 0 ? 2 : 0;  // H series (psi, chi)
   constexpr int NACC = 4 * (NS + NH);
-  extern __shared__ __align__(16) double smem_syn[];
+  extern __shared__ __align__(128) double smem_syn[];
   const int NT = blockDim.x / NSPL;
   const int grp = threadIdx.x / NT, tt0 = threadIdx.x - grp * NT;
-  const int half = GRP ? 0 : grp;  // staging set (groups share one)
+  const int half = grp;  // staging set
   // staged series: NS P-series; MODE 0 adds the two d/dlat series summed by
   // parts (w_k = c_{k+1}.z v_{k+1} - c_{k-1}.w v_{k-1}, v = psi, chi), so
   // sum_k H_k v_k = rcos sum_k P_k w_k and no per-pair H arithmetic is needed
   constexpr int NC = NS + NH;
   double2 *cs = reinterpret_cast<double2 *>(smem_syn) + (size_t)half * NC * kSL;  // [NC][kSL]
-  constexpr int NSTG = GRP ? 1 : NSPL;  // staging sets
-  double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)NSTG * NC * kSL * 2) +
+  double4 *rcs = reinterpret_cast<double4 *>(smem_syn + (size_t)NSPL * NC * kSL * 2) +
                  (size_t)half * (kSL + 2);
-  int4 itm = make_int4((a.nyb > 0 ? blockIdx.x / a.nyb : blockIdx.x) + a.m0, 0, 0, -1);
-  if (MODE == 0 && (SPLIT == 1 || SPLIT == 4) && a.items) itm = a.items[blockIdx.x];
-  int pstart = (a.nyb > 0 ? blockIdx.x % a.nyb : blockIdx.y) * NT, pcount = NT;
-  if (MODE == 0 && SPLIT == 1 && a.pitems) {
-    const int4 pi = a.pitems[blockIdx.x];
-    itm = make_int4(pi.x, 0, 0, -1);
-    pstart = pi.y;
-    pcount = pi.z;
-  }
-  const int m = itm.x;
-  const int i = pstart + tt0;
+  const int m = blockIdx.x + a.m0;
+  const int i = blockIdx.y * NT + tt0;
   const int field = MODE == 1 ? blockIdx.z : 0;
   pdl_trigger();
   if (MODE == 0) trace_mark(0);
@@ -393,18 +342,14 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
   const int off = col_offset(T, m);
   const int kmax = T + 1 - m;
   const double4 *rc = p.d_rc + rc_offset(T, m);
-  const bool has = i < p.nh && tt0 < pcount;
+  const bool has = i < p.nh;
   // warps without pairs skip the walk (they still stage and synchronise)
   const bool warp_busy = __any_sync(0xffffffffu, has);
   // this half's degree range [kb, ke) of the column
   int split = kmax;
   if (SPLIT == 2 && kmax > 96) split = ((kmax / 2 + kSeg - 1) / kSeg) * kSeg;
-  int kb = half == 0 ? 0 : split;
-  int ke = half == 0 ? split : kmax;
-  if (itm.w >= 0) {  // one segment of a split column
-    kb = itm.y;
-    ke = itm.z;
-  }
+  const int kb = half == 0 ? 0 : split;
+  const int ke = half == 0 ? split : kmax;
   double x = 0.0, rcos = 0.0, pm1 = 0.0, p0 = 0.0, p1 = 0.0;
   if (has) {
     x = p.d_x[i];
@@ -440,7 +385,7 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
   // column's last segment runs one degree further (P-series coefficients 0)
   const int kw = (NH > 0 && ke == kmax) ? kmax + 1 : ke;
   const int nchunk_w = SPLIT == 2 ? nchunk : max(nchunk, (kw - kb + kSL - 1) / kSL);
-  const int tst = GRP ? (int)threadIdx.x : tt0, nst = GRP ? (int)blockDim.x : NT;  // stagers
+  const int tst = tt0, nst = NT;  // stagers
   for (int ch = 0; ch < nchunk_w; ++ch) {
     const int k0 = kb + ch * kSL;  // chunk start (even)
     const int n = max(0, min(kSL, kw - k0));
@@ -492,50 +437,32 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
     __syncthreads();
     // two degrees per iteration (static parity q = 0, 1: l - m = k0 + tt)
     // entering: pm1 = P_{k-1}, p0 = P_k, p1 = P_{k+1}
-    const double c0 = p0, c1 = p1;  // chunk-entry recurrence state (TWO)
-#pragma unroll 1
-    for (int pass = 0; pass < (TWO ? 2 : 1) && warp_busy; ++pass) {
-    if (TWO && pass == 1) {
-      p0 = c0;
-      p1 = c1;
-    }
-    for (int t = 0; t < n; t += 2) {
-      const double2 r2 = rcA[t + 2];
-      const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
-      const double2 r3 = rcA[t + 3];
-      const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
-      if ((!GRP || grp == 0) && (!TWO || pass == 0)) {
+    if (warp_busy) {
+      for (int t = 0; t < n; t += 2) {
+        const double2 r2 = rcA[t + 2];
+        const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
+        const double2 r3 = rcA[t + 3];
+        const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
 #pragma unroll
-        for (int s2 = 0; s2 < ((GRP || TWO) ? 3 : NS); ++s2) {
+        for (int s2 = 0; s2 < NS; ++s2) {
           const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
           sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
           sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
           sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
           sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
         }
-      }
-      if ((GRP && grp == 1) || (TWO && pass == 1)) {
 #pragma unroll
-        for (int s2 = 3; s2 < NS; ++s2) {
-          const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
-          sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
-          sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
-          sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
-          sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
+        for (int s2 = 0; s2 < NH; ++s2) {  // H parity 1 - q
+          const double2 w0 = cs[(NS + s2) * kSL + t], w1 = cs[(NS + s2) * kSL + t + 1];
+          sh[1][s2].x = fma(p0, w0.x, sh[1][s2].x);
+          sh[1][s2].y = fma(p0, w0.y, sh[1][s2].y);
+          sh[0][s2].x = fma(p1, w1.x, sh[0][s2].x);
+          sh[0][s2].y = fma(p1, w1.y, sh[0][s2].y);
         }
+        pm1 = p1;
+        p0 = p2;
+        p1 = p3;
       }
-#pragma unroll
-      for (int s2 = 0; s2 < (((GRP && grp == 0) || (TWO && pass == 0)) ? 0 : NH); ++s2) {  // H parity 1 - q
-        const double2 w0 = cs[(NS + s2) * kSL + t], w1 = cs[(NS + s2) * kSL + t + 1];
-        sh[1][s2].x = fma(p0, w0.x, sh[1][s2].x);
-        sh[1][s2].y = fma(p0, w0.y, sh[1][s2].y);
-        sh[0][s2].x = fma(p1, w1.x, sh[0][s2].x);
-        sh[0][s2].y = fma(p1, w1.y, sh[0][s2].y);
-      }
-      pm1 = p1;
-      p0 = p2;
-      p1 = p3;
-    }
     }
   }
   if (SPLIT == 2) {
@@ -573,71 +500,6 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
       }
     }
   }
-  if constexpr (GRP) {
-    // group 1 hands (psi, chi) and the d/dlat sums to group 0
-    __syncthreads();
-    double2 *red = reinterpret_cast<double2 *>(smem_syn);  // [NT][8] (staging reused)
-    if (grp == 1) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        red[(size_t)tt0 * 8 + q * 4 + 0] = sp[q][3];
-        red[(size_t)tt0 * 8 + q * 4 + 1] = sp[q][4];
-        red[(size_t)tt0 * 8 + q * 4 + 2] = sh[q][0];
-        red[(size_t)tt0 * 8 + q * 4 + 3] = sh[q][1];
-      }
-    }
-    __syncthreads();
-    if (grp == 1) return;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      sp[q][3] = red[(size_t)tt0 * 8 + q * 4 + 0];
-      sp[q][4] = red[(size_t)tt0 * 8 + q * 4 + 1];
-      sh[q][0] = red[(size_t)tt0 * 8 + q * 4 + 2];
-      sh[q][1] = red[(size_t)tt0 * 8 + q * 4 + 3];
-    }
-  }
-  if constexpr (MODE == 0 && (SPLIT == 1 || SPLIT == 4)) {
-    if (itm.w >= 0) {
-      constexpr int NP = 2 * (NS + NH);  // partial sums per pair (complex)
-      if (has) {
-        double2 *mine = a.part + (((size_t)m * 2 + itm.w) * p.nh + i) * NP;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-#pragma unroll
-          for (int s2 = 0; s2 < NS; ++s2) mine[q * NS + s2] = sp[q][s2];
-#pragma unroll
-          for (int s2 = 0; s2 < NH; ++s2) mine[2 * NS + q * NH + s2] = sh[q][s2];
-        }
-      }
-      __threadfence();
-      __syncthreads();
-      __shared__ int s_last;
-      if (threadIdx.x == 0) {
-        s_last = atomicAdd(a.cnt + m, 1) == 1;
-        if (s_last) a.cnt[m] = 0;  // ready for the next launch
-      }
-      __syncthreads();
-      if (!s_last) return;
-      __threadfence();
-      if (has) {
-        const double2 *oth = a.part + (((size_t)m * 2 + (1 - itm.w)) * p.nh + i) * NP;
-        const bool first = itm.w == 0;  // fixed order: segment 0 + segment 1
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-#pragma unroll
-          for (int s2 = 0; s2 < NS; ++s2) {
-            const double2 o = __ldcg(oth + q * NS + s2);
-            sp[q][s2] = first ? cadd(sp[q][s2], o) : cadd(o, sp[q][s2]);
-          }
-#pragma unroll
-          for (int s2 = 0; s2 < NH; ++s2) {
-            const double2 o = __ldcg(oth + 2 * NS + q * NH + s2);
-            sh[q][s2] = first ? cadd(sh[q][s2], o) : cadd(o, sh[q][s2]);
-          }
-        }
-      }
-    }
-  }
   if (!has) return;
   const int jn = p.d_jn[i], js = p.d_js[i];
   const int nf = a.nfreq;
@@ -662,331 +524,6 @@ __global__ void __launch_bounds__(MODE == 0 && (SPLIT == 1 || SPLIT == 4) ? 256 
     state_rows<PEER>(p, a, m, i, jn, js, rcos, sp, sh, fr);
     trace_mark(2);
   }
-}
-
-// State synthesis with the whole column staged once (T small enough):
-// CTA = (m, block of latitude pairs), one thread per pair walking l = m..T+1.
-// The dP/dlat series are summed by parts,
-//   sum_k H_k v_k = rcos sum_j P_j (c_{j+1}.z v_{j+1} - c_{j-1}.w v_{j-1}),
-// (H_k = (c_k.z P_{k-1} - c_k.w P_{k+1}) rcos, sphere.py:102-111), so the
-// psi/chi derivative series become two more P series with per-column
-// coefficients w_j staged with the others: 7 complex series of P and the
-// recurrence per degree, no per-pair H arithmetic.  P_j of parity q feeds the
-// H parity 1 - q.
-constexpr int kSCS = 7;  // staged series: vort, div, phi', psi, chi, w_psi, w_chi
-
-__host__ __device__ inline int synth_col_kp(int trunc, int m) {
-  return ((trunc + 3 - m) + 1) & ~1;  // degrees j = 0..kmax (kmax = T+1-m), padded even
-}
-
-// paired = 1: CTA j runs columns j and T - j (equal work per CTA)
-__global__ void __launch_bounds__(256) synth_col_kernel(ShtView p, SynthArgs a, int paired) {
-  extern __shared__ __align__(16) double2 scs[];
-  const int ncol = paired && blockIdx.x != p.trunc - blockIdx.x ? 2 : 1;
-  for (int cc = 0; cc < ncol; ++cc) {
-  const int m = cc == 0 ? blockIdx.x : p.trunc - blockIdx.x;
-  if (cc > 0) __syncthreads();  // staging area reuse
-  const int T = p.trunc, nc = p.ncoef;
-  const int kmax = T + 1 - m;
-  const int KP = synth_col_kp(T, m);           // staged degrees (>= kmax + 1, even)
-  const int KS = synth_col_kp(T, 0) + 2;       // series stride (all columns)
-  double2 *cs = scs;                            // [kSCS][KS]
-  double2 *rcA = scs + kSCS * KS;               // [KS] {e_{l-1}, 1/e_l}
-  double2 *rzw = rcA + KS;                      // [KS] {(l+1)e_l, l e_{l+1}}
-  const int i = blockIdx.y * blockDim.x + threadIdx.x;
-  const bool has = i < p.nh;
-  // per-pair values first: their latency overlaps the staging
-  double x = 0.0, rcos = 0.0, seed = 0.0;
-  int jn = 0, js = 0;
-  double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  if (has) {
-    x = p.d_x[i];
-    rcos = p.d_rcos[i];
-    seed = p.d_seed[(size_t)m * p.nh + i];
-    jn = p.d_jn[i];
-    js = p.d_js[i];
-    if (a.want_lc) {
-      fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
-      fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
-    }
-  }
-  const int off = col_offset(T, m);
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  for (int t = threadIdx.x; t < KP + 2; t += blockDim.x) {
-    double4 c = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (t <= kmax) c = rc[t];
-    rcA[t] = make_double2(c.x, c.y);
-    rzw[t] = make_double2(c.z, c.w);
-    if (t < KP) {
-      const bool in = t < kmax;
-      const int s = off + t;
-      const double il = in ? p.d_lconst[m + t] : 0.0;
-      const double2 z = in ? a.coef[nc + s] : make_double2(0.0, 0.0);
-      const double2 d = in ? a.coef[2 * nc + s] : make_double2(0.0, 0.0);
-      cs[0 * KS + t] = z;
-      cs[1 * KS + t] = d;
-      cs[2 * KS + t] = in ? a.coef[s] : make_double2(0.0, 0.0);
-      cs[3 * KS + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
-      cs[4 * KS + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
-    }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < KP; t += blockDim.x) {
-#pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) {
-      const double2 *v = cs + (3 + s2) * KS;
-      const double2 up = t + 1 < KP ? v[t + 1] : make_double2(0.0, 0.0);
-      const double2 dn = t > 0 ? v[t - 1] : make_double2(0.0, 0.0);
-      const double cz = t + 1 < KP + 2 ? rzw[t + 1].x : 0.0;
-      const double cw = t > 0 ? rzw[t - 1].y : 0.0;
-      cs[(5 + s2) * KS + t] = make_double2(cz * up.x - cw * dn.x, cz * up.y - cw * dn.y);
-    }
-  }
-  __syncthreads();
-  if (has) {
-  double p0 = seed, p1 = sqrt(2.0 * m + 3.0) * x * seed;  // sphere.py:96-97
-  double2 sp[2][5], sw[2][2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-#pragma unroll
-    for (int s2 = 0; s2 < 5; ++s2) sp[q][s2] = make_double2(0.0, 0.0);
-    sw[q][0] = sw[q][1] = make_double2(0.0, 0.0);
-  }
-  for (int t = 0; t < KP; t += 2) {
-    const double2 r2 = rcA[t + 2], r3 = rcA[t + 3];
-    const double p2 = fma(x, p1, -r2.x * p0) * r2.y;  // sphere.py:98-100
-    const double p3 = fma(x, p2, -r3.x * p1) * r3.y;
-#pragma unroll
-    for (int s2 = 0; s2 < 5; ++s2) {
-      const double2 v0 = cs[s2 * KS + t], v1 = cs[s2 * KS + t + 1];
-      sp[0][s2].x = fma(p0, v0.x, sp[0][s2].x);
-      sp[0][s2].y = fma(p0, v0.y, sp[0][s2].y);
-      sp[1][s2].x = fma(p1, v1.x, sp[1][s2].x);
-      sp[1][s2].y = fma(p1, v1.y, sp[1][s2].y);
-    }
-#pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) {
-      const double2 w0 = cs[(5 + s2) * KS + t], w1 = cs[(5 + s2) * KS + t + 1];
-      sw[1][s2].x = fma(p0, w0.x, sw[1][s2].x);
-      sw[1][s2].y = fma(p0, w0.y, sw[1][s2].y);
-      sw[0][s2].x = fma(p1, w1.x, sw[0][s2].x);
-      sw[0][s2].y = fma(p1, w1.y, sw[0][s2].y);
-    }
-    p0 = p2;
-    p1 = p3;
-  }
-  double2 sh[2][2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) sh[q][s2] = make_double2(sw[q][s2].x * rcos, sw[q][s2].y * rcos);
-  state_rows(p, a, m, i, jn, js, rcos, sp, sh, fr);
-  }
-  }
-}
-
-static size_t synth_col_smem(int trunc) {
-  const int KS = synth_col_kp(trunc, 0) + 2;
-  return (size_t)(kSCS + 2) * KS * sizeof(double2);
-}
-
-// State synthesis, PPT latitude pairs per thread.  The column sums are bound
-// by shared-memory broadcast loads (every coefficient load returns 512 B to
-// a warp for 2 FMAs per pair), so each loaded coefficient now feeds PPT
-// pairs: CTA = column m, thread t owns pairs t, t + NT, ...; same staging,
-// recurrence, d/dlat series summed by parts and epilogue as synth_kernel<0>.
-template <int PPT>
-__global__ void __launch_bounds__(256) synth_pp_kernel(ShtView p, SynthArgs a) {
-  constexpr int NS = 5, NH = 2, NC = NS + NH;
-  extern __shared__ __align__(16) double smem_syn[];
-  const int NT = blockDim.x;
-  double2 *cs = reinterpret_cast<double2 *>(smem_syn);  // [NC][kSL]
-  double2 *rcA = reinterpret_cast<double2 *>(smem_syn + (size_t)NC * kSL * 2);  // [kSL + 4]
-  // item: (m, kb, ke, seg) -- a whole column (seg < 0) or one of the two
-  // checkpoint-aligned segments of a long column (a.items)
-  const int4 itm = a.items ? a.items[blockIdx.x] : make_int4(blockIdx.x, 0, 0, -1);
-  const int m = itm.x;
-  pdl_trigger();
-  trace_mark(0);
-  const int T = p.trunc, nc = p.ncoef;
-  const int off = col_offset(T, m);
-  const int kmax = T + 1 - m;
-  const int kb = itm.w >= 0 ? itm.y : 0, ke = itm.w >= 0 ? itm.z : kmax;
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  double x[PPT], p0[PPT], p1[PPT];
-  double2 sp[PPT][2][NS], sh[PPT][2][NH];
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int i = threadIdx.x + j * NT;
-    x[j] = p0[j] = p1[j] = 0.0;
-    if (i < p.nh) {
-      x[j] = p.d_x[i];
-      if (kb == 0) {
-        const double seed = p.d_seed[(size_t)m * p.nh + i];
-        p0[j] = seed;
-        p1[j] = sqrt(2.0 * m + 3.0) * x[j] * seed;  // sphere.py:96-97
-      } else {  // plan-time recurrence checkpoint at degree kb (multiple of kSeg)
-        const double *ck = p.d_ckpt + ((size_t)p.d_segoff[m] + kb / kSeg) * 3 * p.nh;
-        p0[j] = ck[p.nh + i];
-        p1[j] = ck[2 * p.nh + i];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-#pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2) sp[j][q][s2] = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int s2 = 0; s2 < NH; ++s2) sh[j][q][s2] = make_double2(0.0, 0.0);
-    }
-  }
-  pdl_wait();  // the coefficients come from the preceding kernel
-  const int kw = ke == kmax ? kmax + 1 : ke;  // the w-series pair P_{T+1} with w_kmax
-  const int nchunk = (kw - kb + kSL - 1) / kSL;
-  for (int ch = 0; ch < nchunk; ++ch) {
-    const int k0 = kb + ch * kSL;
-    const int n = min(kSL, kw - k0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < kSL + 4; t += NT) {
-      const int k = k0 + t;
-      const double4 c = k <= kmax ? rc[k] : make_double4(0.0, 0.0, 0.0, 0.0);
-      rcA[t] = make_double2(c.x, c.y);
-    }
-    for (int t = threadIdx.x; t < ((n + 1) & ~1); t += NT) {
-      const int s = off + k0 + t;
-      const int k = k0 + t;
-      const bool in = t < n && k < kmax;
-      const double il = in ? p.d_lconst[m + k] : 0.0;
-      const double2 z = in ? a.coef[nc + s] : make_double2(0.0, 0.0);
-      const double2 d = in ? a.coef[2 * nc + s] : make_double2(0.0, 0.0);
-      cs[0 * kSL + t] = z;
-      cs[1 * kSL + t] = d;
-      cs[2 * kSL + t] = in ? a.coef[s] : make_double2(0.0, 0.0);
-      cs[3 * kSL + t] = make_double2(z.x * il, z.y * il);  // psi = inv_lap(vort)
-      cs[4 * kSL + t] = make_double2(d.x * il, d.y * il);  // chi = inv_lap(div)
-      double2 wz = make_double2(0.0, 0.0), wd = wz;
-      if (t < n && k <= kmax) {
-        if (k + 1 < kmax) {
-          const double cz = rc[k + 1].z * p.d_lconst[m + k + 1];
-          const double2 zp = a.coef[nc + s + 1], dp = a.coef[2 * nc + s + 1];
-          wz = make_double2(cz * zp.x, cz * zp.y);
-          wd = make_double2(cz * dp.x, cz * dp.y);
-        }
-        if (k >= 1 && k - 1 < kmax) {
-          const double cw = rc[k - 1].w * p.d_lconst[m + k - 1];
-          const double2 zm = a.coef[nc + s - 1], dm = a.coef[2 * nc + s - 1];
-          wz = make_double2(wz.x - cw * zm.x, wz.y - cw * zm.y);
-          wd = make_double2(wd.x - cw * dm.x, wd.y - cw * dm.y);
-        }
-      }
-      cs[5 * kSL + t] = wz;
-      cs[6 * kSL + t] = wd;
-    }
-    __syncthreads();
-    for (int t = 0; t < n; t += 2) {
-      const double2 r2 = rcA[t + 2], r3 = rcA[t + 3];
-      double q0[PPT], q1[PPT];
-#pragma unroll
-      for (int j = 0; j < PPT; ++j) {
-        const double p2 = fma(x[j], p1[j], -r2.x * p0[j]) * r2.y;  // sphere.py:98-100
-        const double p3 = fma(x[j], p2, -r3.x * p1[j]) * r3.y;
-        q0[j] = p0[j];
-        q1[j] = p1[j];
-        p0[j] = p2;
-        p1[j] = p3;
-      }
-#pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2) {
-        const double2 v0 = cs[s2 * kSL + t], v1 = cs[s2 * kSL + t + 1];
-#pragma unroll
-        for (int j = 0; j < PPT; ++j) {
-          sp[j][0][s2].x = fma(q0[j], v0.x, sp[j][0][s2].x);
-          sp[j][0][s2].y = fma(q0[j], v0.y, sp[j][0][s2].y);
-          sp[j][1][s2].x = fma(q1[j], v1.x, sp[j][1][s2].x);
-          sp[j][1][s2].y = fma(q1[j], v1.y, sp[j][1][s2].y);
-        }
-      }
-#pragma unroll
-      for (int s2 = 0; s2 < NH; ++s2) {  // P of parity q feeds the H parity 1 - q
-        const double2 w0 = cs[(NS + s2) * kSL + t], w1 = cs[(NS + s2) * kSL + t + 1];
-#pragma unroll
-        for (int j = 0; j < PPT; ++j) {
-          sh[j][1][s2].x = fma(q0[j], w0.x, sh[j][1][s2].x);
-          sh[j][1][s2].y = fma(q0[j], w0.y, sh[j][1][s2].y);
-          sh[j][0][s2].x = fma(q1[j], w1.x, sh[j][0][s2].x);
-          sh[j][0][s2].y = fma(q1[j], w1.y, sh[j][0][s2].y);
-        }
-      }
-    }
-  }
-  if (itm.w >= 0) {
-    // split column: partial sums meet in a.part; the second CTA to arrive
-    // adds them in fixed order (segment 0 + segment 1) and writes the rows
-    constexpr int NP = 2 * (NS + NH);
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const int i = threadIdx.x + j * NT;
-      if (i >= p.nh) continue;
-      double2 *mine = a.part + (((size_t)m * 2 + itm.w) * p.nh + i) * NP;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-#pragma unroll
-        for (int s2 = 0; s2 < NS; ++s2) mine[q * NS + s2] = sp[j][q][s2];
-#pragma unroll
-        for (int s2 = 0; s2 < NH; ++s2) mine[2 * NS + q * NH + s2] = sh[j][q][s2];
-      }
-    }
-    __threadfence();
-    __syncthreads();
-    __shared__ int s_last;
-    if (threadIdx.x == 0) {
-      s_last = atomicAdd(a.cnt + m, 1) == 1;
-      if (s_last) a.cnt[m] = 0;  // ready for the next launch
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const bool first = itm.w == 0;
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const int i = threadIdx.x + j * NT;
-      if (i >= p.nh) continue;
-      const double2 *oth = a.part + (((size_t)m * 2 + (1 - itm.w)) * p.nh + i) * NP;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-#pragma unroll
-        for (int s2 = 0; s2 < NS; ++s2) {
-          const double2 o = __ldcg(oth + q * NS + s2);
-          sp[j][q][s2] = first ? cadd(sp[j][q][s2], o) : cadd(o, sp[j][q][s2]);
-        }
-#pragma unroll
-        for (int s2 = 0; s2 < NH; ++s2) {
-          const double2 o = __ldcg(oth + 2 * NS + q * NH + s2);
-          sh[j][q][s2] = first ? cadd(sh[j][q][s2], o) : cadd(o, sh[j][q][s2]);
-        }
-      }
-    }
-  }
-  trace_mark(1);
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int i = threadIdx.x + j * NT;
-    if (i >= p.nh) continue;
-    const double rcos = p.d_rcos[i];
-    const int jn = p.d_jn[i], js = p.d_js[i];
-    double2 shr[2][2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int s2 = 0; s2 < NH; ++s2)
-        shr[q][s2] = make_double2(sh[j][q][s2].x * rcos, sh[j][q][s2].y * rcos);
-    double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-    if (a.want_lc) {
-      fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
-      fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
-    }
-    state_rows(p, a, m, i, jn, js, rcos, sp[j], shr, fr);
-  }
-  trace_mark(2);
 }
 
 // zero the C2R rows above m = T (cuFFT may overwrite its input)
@@ -1621,7 +1158,6 @@ __global__ void prep_plain_kernel(ShtView p, const double2 *Q, int nf, double *A
 // ---------------------------------------------------------------------
 constexpr int kAT = 256;
 constexpr int kAL = 16;
-constexpr int kRS = 20;  // tile row stride (doubles): conflict-free A fragments
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -1671,10 +1207,12 @@ __global__ void ckpt_kernel(ShtView p) {
 // the lane's A-fragment element, no table and no redundant walk -- and the
 // 8 complex series of the column (vort, div, phi', psi, chi, and the dP/dlat
 // series of psi, chi summed by parts) are the B fragments, staged once per
-// CTA.  Each coefficient load feeds 16 pairs (two row tiles), against one
+// column.  Each coefficient load feeds 16 pairs (two row tiles), against one
 // pair per broadcast load in synth_kernel (shared-memory bound at ~1/4 of
-// the FP64 rate).  CTA = (column, half of the latitude pairs), longest
-// columns first.
+// the FP64 rate).  Two kernels: synth_ws_kernel (one CTA per SM, whole
+// columns, producer warps staging the next column; nh <= 208) and
+// synth_mma_pers_kernel (two CTAs per SM over (column, half of the pairs)
+// items; nh <= 256).
 // ---------------------------------------------------------------------
 __host__ __device__ inline int syn_seg_start(int kmax, int c) {
   return c >= 4 ? kmax + 1 : ((c * (kmax + 1)) / 4) & ~1;
@@ -1708,166 +1246,15 @@ __global__ void sck_kernel(ShtView p) {
   }
 }
 
-// CTA = (column, one half of the latitude pairs), longest columns first.
-template <bool PEER = false>
-__global__ void __launch_bounds__(256, 2) synth_mma_kernel(ShtView p, SynthArgs a, int m_first,
-                                                           int wpb, int lmax) {
-  extern __shared__ __align__(16) double smem_syn[];
-  const int m = m_first + (blockIdx.x >> 1), blk = blockIdx.x & 1;
-  const int T = p.trunc, nc = p.ncoef, nh = p.nh, kmax = T + 1 - m;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = lane & 3, r = lane >> 2;
-  const int SS = lmax * 16 + 8;  // doubles per staged quarter (odd multiple of 8: conflict-free B)
-  const int RS = lmax + 2;
-  double *Cs = smem_syn;                                          // [4][SS]
-  double2 *Rc = reinterpret_cast<double2 *>(smem_syn + 4 * SS);  // [4][RS]
-  pdl_trigger();
-  trace_mark(0);
-  int L = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) L = max(L, syn_seg_start(kmax, q + 1) - syn_seg_start(kmax, q));
-  L = (L + 1) & ~1;
-  // plan data first (PDL prologue): the lane's pairs, quarter start values,
-  // recurrence constants and the epilogue's per-pair data
-  const int pbase = (blk * wpb + warp) * 16;
-  const int iA = pbase + r, iB = pbase + 8 + r, ie = pbase + lane;
-  const bool wact = pbase < nh;
-  const bool eact = wact && lane < 16 && ie < nh;  // epilogue thread of pair ie
-  double xA = 0.0, xB = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-  const double *ck = p.d_sck + ((size_t)m * 8 + c * 2) * nh;
-  if (iA < nh) {
-    xA = p.d_x[iA];
-    a0 = ck[iA];
-    a1 = ck[nh + iA];
-  }
-  if (iB < nh) {
-    xB = p.d_x[iB];
-    b0 = ck[iB];
-    b1 = ck[nh + iB];
-  }
-  int jn = 0, js = 0;
-  double rcos = 0.0;
-  double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  if (eact) {
-    jn = p.d_jn[ie];
-    js = p.d_js[ie];
-    rcos = p.d_rcos[ie];
-    fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
-    fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
-  }
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  for (int t = threadIdx.x; t < 4 * RS; t += blockDim.x) {
-    const int q = t / RS, u = t - q * RS;
-    const int sq = syn_seg_start(kmax, q), n = syn_seg_start(kmax, q + 1) - sq;
-    const int k = sq + u;
-    double4 cc = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (u < n + 2 && k <= kmax) cc = rc[k];
-    Rc[t] = make_double2(cc.x, cc.y);
-  }
-  pdl_wait();  // the coefficients come from the preceding kernel
-  trace_mark(1);
-  const int off = col_offset(T, m);
-  const double4 *wcm = p.d_wc + rc_offset(T, m);
-  for (int t = threadIdx.x; t < 4 * L; t += blockDim.x) {
-    const int q = t / L, u = t - q * L;
-    const int sq = syn_seg_start(kmax, q), eq = syn_seg_start(kmax, q + 1);
-    const int k = sq + u, sl = off + k;
-    const bool on = k < eq;  // degree in the quarter (k <= kmax)
-    const bool in = on && k < kmax;
-    const bool up = on && k + 1 < kmax, dn = on && k >= 1;
-    const double4 cw = on ? wcm[k] : make_double4(0.0, 0.0, 0.0, 0.0);
-    const double2 zero = make_double2(0.0, 0.0);
-    const double2 z = in ? a.coef[nc + sl] : zero, d = in ? a.coef[2 * nc + sl] : zero;
-    const double2 ph = in ? a.coef[sl] : zero;
-    const double2 zp = up ? a.coef[nc + sl + 1] : zero, dp = up ? a.coef[2 * nc + sl + 1] : zero;
-    const double2 zm = dn ? a.coef[nc + sl - 1] : zero, dm = dn ? a.coef[2 * nc + sl - 1] : zero;
-    // dP/dlat series of psi, chi summed by parts (see synth_kernel)
-    double2 wz = make_double2(cw.y * zp.x, cw.y * zp.y), wd = make_double2(cw.y * dp.x, cw.y * dp.y);
-    wz = make_double2(wz.x - cw.z * zm.x, wz.y - cw.z * zm.y);
-    wd = make_double2(wd.x - cw.z * dm.x, wd.y - cw.z * dm.y);
-    double2 *row = reinterpret_cast<double2 *>(Cs + (size_t)q * SS + (size_t)u * 16);
-    row[0] = z;
-    row[1] = d;
-    row[2] = ph;
-    row[3] = make_double2(z.x * cw.x, z.y * cw.x);  // psi = inv_lap(vort)
-    row[4] = make_double2(d.x * cw.x, d.y * cw.x);  // chi = inv_lap(div)
-    row[5] = wz;
-    row[6] = wd;
-    row[7] = zero;
-  }
-  __syncthreads();
-  trace_mark(2);
-  // D[parity][row tile][col tile][2]
-  double D[2][2][2][2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) D[q][u][v][0] = D[q][u][v][1] = 0.0;
-  if (wact) {
-    const double *cq = Cs + (size_t)c * SS + r;  // B[k = c][n = r]
-    const double2 *rq = Rc + c * RS;
-#pragma unroll 1
-    for (int j = 0; j < L; j += 2) {
-      double t0 = cq[j * 16], t1 = cq[j * 16 + 8];
-      dmma(D[0][0][0][0], D[0][0][0][1], a0, t0);
-      dmma(D[0][0][1][0], D[0][0][1][1], a0, t1);
-      dmma(D[0][1][0][0], D[0][1][0][1], b0, t0);
-      dmma(D[0][1][1][0], D[0][1][1][1], b0, t1);
-      t0 = cq[j * 16 + 16];
-      t1 = cq[j * 16 + 24];
-      dmma(D[1][0][0][0], D[1][0][0][1], a1, t0);
-      dmma(D[1][0][1][0], D[1][0][1][1], a1, t1);
-      dmma(D[1][1][0][0], D[1][1][0][1], b1, t0);
-      dmma(D[1][1][1][0], D[1][1][1][1], b1, t1);
-      const double2 r2 = rq[j + 2], r3 = rq[j + 3];
-      const double a2 = fma(xA, a1, -r2.x * a0) * r2.y;  // sphere.py:98-100
-      const double b2 = fma(xB, b1, -r2.x * b0) * r2.y;
-      const double a3 = fma(xA, a2, -r3.x * a1) * r3.y;
-      const double b3 = fma(xB, b2, -r3.x * b1) * r3.y;
-      a0 = a2;
-      a1 = a3;
-      b0 = b2;
-      b1 = b3;
-    }
-  }
-  __syncthreads();  // staging area free: per-warp gather of the pairs' sums
-  trace_mark(3);
-  double2 *E = reinterpret_cast<double2 *>(smem_syn) + (size_t)warp * 256;  // [16 pairs][2][8]
-  if (wact) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int v = 0; v < 2; ++v)
-          E[(u * 8 + r) * 16 + q * 8 + v * 4 + c] = make_double2(D[q][u][v][0], D[q][u][v][1]);
-  }
-  __syncwarp();
-  if (!eact) return;
-  const double2 *e = E + lane * 16;
-  double2 sp[2][5], sh[2][2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-#pragma unroll
-    for (int k = 0; k < 5; ++k) sp[q][k] = e[q * 8 + k];
-    // the dP/dlat series of parity-q degrees belong to H parity 1 - q
-    sh[1 - q][0] = make_double2(e[q * 8 + 5].x * rcos, e[q * 8 + 5].y * rcos);
-    sh[1 - q][1] = make_double2(e[q * 8 + 6].x * rcos, e[q * 8 + 6].y * rcos);
-  }
-  state_rows<PEER>(p, a, m, ie, jn, js, rcos, sp, sh, fr);
-  if (lane == 0 && warp == 0) trace_mark(4);
-}
 
-// Persistent form of synth_mma_kernel: gridDim.x CTAs (two per SM) walk the
-// (column, pair block) items in a static snake order over the longest-first
-// item list (CTA b: items b, 2G-1-b, 2G+b, ...), which balances the column
-// lengths per CTA.  A column's raw inputs (the three coefficient runs, the
-// dP/dlat weights and the recurrence constants: 5 contiguous runs) arrive by
-// bulk copy into a staging buffer while the previous item's DMMA loop runs;
-// the derived B rows are built from shared memory.  Identical arithmetic to
-// synth_mma_kernel, so the results are bitwise equal.
+// Persistent DMMA state synthesis over (column, half of the pairs) items:
+// gridDim.x CTAs (two per SM) walk the items in a static snake order over
+// the longest-first item list (CTA b: items b, 2G-1-b, 2G+b, ...), which
+// balances the column lengths per CTA.  A column's raw inputs (the three
+// coefficient runs, the dP/dlat weights and the recurrence constants: 5
+// contiguous runs) arrive by bulk copy into a staging buffer while the
+// previous item's DMMA loop runs; the derived B rows are built from shared
+// memory.  Same arithmetic per (column, pair) as synth_ws_kernel.
 
 constexpr int kEP = 17;  // per-pair stride (double2) of the epilogue gather: conflict-free
 // row stride (double2) of the staged recurrence constants: = 2 mod 4, so the
@@ -2064,7 +1451,7 @@ __global__ void __launch_bounds__(256, 2) synth_mma_pers_kernel(ShtView p, Synth
 // quarter start values into a private raw buffer / the column's half of a
 // double buffer, then the derived B rows) while the consumers run column k's
 // DMMA loop; full/empty mbarriers per buffer.  The arithmetic per column and
-// pair is the synth_mma_kernel's, so the results are bitwise equal.
+// pair is synth_mma_pers_kernel's, so the results are bitwise equal.
 constexpr int kSynPW = 2;  // producer warps
 
 template <bool PEER = false>
@@ -2896,7 +2283,7 @@ __global__ void prep_tab_vortdiv_kernel(ShtView p, const double2 *Q, double *A) 
 constexpr int kTL = SWX_TAB_TL;         // degrees per item (32 or 64)
 constexpr int kTCW = kTL / 8;           // consumer warps (parity x 8-degree rows)
 constexpr int kTK = 16;                 // latitude pairs per stage
-constexpr int kTS = 4;                  // ring depth
+
 constexpr int kPR = 20;                 // smem pitch of a staged table row (doubles) = TMA box width
 constexpr int kTBoxRows = kTL / 2 + 1;  // rows per parity plane per stage
 constexpr int kP1 = (kTBoxRows * kPR + 15) / 16 * 16;          // plane-1 box offset (doubles, 128 B aligned)
@@ -2910,258 +2297,6 @@ static_assert(kP1 >= kTBoxRows * kPR && kSB >= kP1 + kTBoxRows * kPR, "stage lay
 static_assert((kStage * 8) % 128 == 0 && (kP1 * 8) % 128 == 0 && (kSB * 8) % 128 == 0, "TMA alignment");
 
 
-// ---------------------------------------------------------------------
-// Tendency analysis with the Legendre functions generated in the DMMA
-// A fragments (no P table traffic).  Column m's degrees k = l - m = 0..kmax
-// (kmax = T+1-m: P_{T+1} feeds the dP/dlat part) are cut into 16 segments
-// of S = ack_steps(m) (even) degrees.  D[M = segment][N = column] +=
-// A[M = segment][K = 4 pairs] * B[K = pair][N = column]: lane (r, c) of a
-// warp runs the recurrence (sphere.py:98-100, bit-identical to the table)
-// of segment r for pair c of the current 4-pair block from the plan-time
-// segment-start values, so the 8 rows of every MMA are 8 different degrees
-// of the same parity and the B fragment (the prepared rows of that parity)
-// is shared.  Per degree k the kernel forms
-//   F[k] = sum_i P_k(i) R0_i[par k]   (vort, div, phi', KE columns)
-//   G[k] = sum_i P_k(i) R1_i[par k]   (the 1/cos-folded d/dlat rows)
-// and the dP/dlat series by parts, sum_i (cz P_{k-1} - cw P_{k+1}) R1_i =
-// cz G[k-1] - cw G[k+1] (the table kernel's h per pair, summed first).
-// CTA = column, 8 warps = 2 segment windows x 4 pair quarters; the quarter
-// partials are added in fixed order ((q0 + q2) + (q1 + q3)).
-// ---------------------------------------------------------------------
-constexpr int kAckWin = 3;              // segment windows (8 segments each) per column
-constexpr int kAckSeg = 8 * kAckWin;    // segments per column
-constexpr int kAckSMax = 12;            // steps per segment (accumulators per lane: 4 * kAckSMax)
-constexpr int kAckTMax = kAckSeg * kAckSMax - 2;  // largest truncation (T + 2 <= kAckSeg S)
-constexpr int kAckThreads = kAckWin * 4 * 32;     // windows x 4 pair quarters
-__host__ __device__ inline int ack_steps(int trunc, int m) {
-  return 2 * ((trunc + 2 - m + 2 * kAckSeg - 1) / (2 * kAckSeg));
-}
-// pair pitch (double2) of a segment's start values: = 4 mod 8, so the four
-// segments a half-warp reads fall in distinct bank groups
-__host__ __device__ inline int ack_pitch(int nt16) { return nt16 + 4; }
-
-// plan time: segment-start values of every column and padded pair
-__global__ void ack_kernel(ShtView p) {
-  const int m = blockIdx.x;
-  const int i = blockIdx.y * blockDim.x + threadIdx.x;
-  if (i >= p.nt16) return;
-  const int T = p.trunc, kmax = T + 1 - m, S = ack_steps(T, m);
-  const int ckp = ack_pitch(p.nt16);
-  double *ck = p.d_ack + (size_t)m * kAckSeg * ckp * 2;
-  if (i >= p.nh) {
-    for (int g = 0; g < kAckSeg; ++g) ck[((size_t)g * ckp + i) * 2] = ck[((size_t)g * ckp + i) * 2 + 1] = 0.0;
-    return;
-  }
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  const double x = p.d_x[i];
-  const double seed = p.d_seed[(size_t)m * p.nh + i];
-  double p0 = seed, p1 = kmax >= 1 ? sqrt(2.0 * m + 3.0) * x * seed : 0.0;
-  int g = 0;
-  for (int k = 0; k <= kmax; ++k) {
-    if (k == g * S && g < kAckSeg) {
-      ck[((size_t)g * ckp + i) * 2] = p0;
-      ck[((size_t)g * ckp + i) * 2 + 1] = p1;
-      ++g;
-    }
-    double p2 = 0.0;
-    if (k + 2 <= kmax) {
-      const double4 c2 = rc[k + 2];
-      p2 = fma(x, p1, -c2.x * p0) * c2.y;  // identical to the walkers
-    }
-    p0 = p1;
-    p1 = p2;
-  }
-  for (; g < kAckSeg; ++g) ck[((size_t)g * ckp + i) * 2] = ck[((size_t)g * ckp + i) * 2 + 1] = 0.0;
-}
-
-constexpr int kAckRed = kAckWin * 2 * kAckSMax * 2 * 64;  // reduction buffer (doubles)
-
-__global__ void __launch_bounds__(kAckThreads, 1) analysis_otf_kernel(ShtView p, const double *A,
-                                                              double2 *out, const double2 *sub,
-                                                              int m_first, int ncol) {
-  extern __shared__ __align__(128) double osm[];
-  const int nt = p.nt16, ckp = ack_pitch(nt);
-  const size_t ps = (size_t)nt * kAG;
-  double *red = osm;                                            // [win][2][S][part][64]
-  double *rows = red + kAckRed;                                 // [4][nt][kAG]: the column's prepared rows
-  double2 *cks = reinterpret_cast<double2 *>(rows + 4 * ps);    // [16][ckp]: segment starts
-  double2 *rcS = cks + (size_t)kAckSeg * ckp;                   // [16 S + 2]
-  double *xs = reinterpret_cast<double *>(rcS + kAckSeg * kAckSMax + 2);  // [nt]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(xs + nt);
-  const int T = p.trunc;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int win = warp % kAckWin, qtr = warp / kAckWin;
-  const int r = lane >> 2, c = lane & 3;
-  const int G = gridDim.x;
-  auto col_of = [&](int it) {  // columns b, 2G-1-b, 2G+b, ... of the longest-first list
-    return (it & 1) ? 2 * G * ((it >> 1) + 1) - 1 - (int)blockIdx.x : 2 * G * (it >> 1) + (int)blockIdx.x;
-  };
-  const unsigned rb = (unsigned)(4 * ps * sizeof(double)), cb = (unsigned)(kAckSeg * ckp * sizeof(double2));
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) xs[i] = i < p.nh ? p.d_x[i] : 0.0;
-  __syncthreads();
-  pdl_trigger();
-  trace_mark(0, 1024);
-  for (int it = 0;; ++it) {
-  const int idx = col_of(it);
-  if (idx >= ncol) break;
-  const int m = m_first + idx;
-  const int kmax = T + 1 - m, S = ack_steps(T, m);
-  if (it > 0) __syncthreads();  // the previous column's shared-memory reads are done
-  if (threadIdx.x == 0) {
-    // the segment starts are plan data; the prepared rows come from the
-    // preceding kernel (first column: wait for it)
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_expect_tx(bar, rb + cb);
-    bulk_g2s_v(cks, p.d_ack + (size_t)m * kAckSeg * ckp * 2, cb, bar);
-    if (it == 0) pdl_wait();
-    bulk_g2s_v(rows, A + (size_t)m * 4 * ps, rb, bar);
-  }
-  // recurrence constants of the column
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  for (int k = threadIdx.x; k < kAckSeg * S + 2; k += blockDim.x) {
-    const double4 v = k <= kmax ? rc[k] : make_double4(0.0, 0.0, 0.0, 0.0);
-    rcS[k] = make_double2(v.x, v.y);
-  }
-  const int g = win * 8 + r;  // this lane's segment
-  const int k0 = g * S;
-  const double2 *ck = cks + (size_t)g * ckp;
-  const int nb = nt / 4, nbq = (nb + 3) / 4;
-  const int b0 = qtr * nbq, b1 = min(nb, b0 + nbq);
-  __syncthreads();  // rcS staged
-  mbar_wait(bar, it & 1);
-  if (it == 0) trace_mark(1, 1024);
-  double DF[kAckSMax][2], DG[kAckSMax][2];
-#pragma unroll
-  for (int j = 0; j < kAckSMax; ++j) DF[j][0] = DF[j][1] = DG[j][0] = DG[j][1] = 0.0;
-  // software pipeline: the next block's operands are loaded under this block's MMAs
-#define OTF_LOAD(b)                                                        \
-  {                                                                        \
-    const int i = 4 * (b) + c;                                             \
-    nx = xs[i];                                                            \
-    const double2 q = ck[i];                                               \
-    nP0 = q.x;                                                             \
-    nP1 = q.y;                                                             \
-    const int col = r ^ ((i & 2) ? 4 : 0); /* rotated rows (bit 1 set) */  \
-    const double *row = rows + (size_t)i * kAG + col;                      \
-    nbf0 = row[0 * ps];                                                    \
-    nbf1 = row[1 * ps];                                                    \
-    nbg0 = row[2 * ps];                                                    \
-    nbg1 = row[3 * ps];                                                    \
-  }
-  // the pair blocks of this warp, SS = S steps per segment (compile time:
-  // no predicated-off MMAs on short columns)
-#define OTF_BLOCKS(SS)                                                                         \
-  {                                                                                            \
-    double nx = 0.0, nP0 = 0.0, nP1 = 0.0, nbf0 = 0.0, nbf1 = 0.0, nbg0 = 0.0, nbg1 = 0.0;     \
-    if (b0 < b1) OTF_LOAD(b0)                                                                  \
-    for (int b = b0; b < b1; ++b) {                                                            \
-      const double x = nx;                                                                     \
-      double P0 = nP0, P1 = nP1;                                                               \
-      const double bf[2] = {nbf0, nbf1}, bg[2] = {nbg0, nbg1};                                 \
-      if (b + 1 < b1) OTF_LOAD(b + 1)                                                          \
-      _Pragma("unroll") for (int j = 0; j < (SS); ++j) {                                       \
-        dmma(DF[j][0], DF[j][1], P0, bf[j & 1]);                                               \
-        dmma(DG[j][0], DG[j][1], P0, bg[j & 1]);                                               \
-        const double2 c2 = rcS[k0 + j + 2];                                                    \
-        const double P2 = fma(x, P1, -c2.x * P0) * c2.y;                                       \
-        P0 = P1;                                                                               \
-        P1 = P2;                                                                               \
-      }                                                                                        \
-    }                                                                                          \
-  }
-  switch (S) {
-    case 2: OTF_BLOCKS(2) break;
-    case 4: OTF_BLOCKS(4) break;
-    case 6: OTF_BLOCKS(6) break;
-    case 8: OTF_BLOCKS(8) break;
-    case 10: OTF_BLOCKS(10) break;
-    default: OTF_BLOCKS(12) break;
-  }
-#undef OTF_BLOCKS
-#undef OTF_LOAD
-  if (it < 2) trace_mark(2 + 2 * it, 1024);
-  // fixed-order reduction over the pair quarters: ((q0 + q2) + (q1 + q3))
-  double *rw = red + (size_t)win * 2 * kAckSMax * 128;  // [2][S][part][64] per window
-#define OTF_PUT(slot)                                                        \
-  _Pragma("unroll") for (int j = 0; j < kAckSMax; ++j) if (j < S) {        \
-    double *d = rw + ((size_t)(slot) * kAckSMax + j) * 128 + lane * 2;      \
-    d[0] = DF[j][0];                                                         \
-    d[1] = DF[j][1];                                                         \
-    d[64] = DG[j][0];                                                        \
-    d[65] = DG[j][1];                                                        \
-  }
-#define OTF_ADD(slot)                                                        \
-  _Pragma("unroll") for (int j = 0; j < kAckSMax; ++j) if (j < S) {        \
-    const double *d = rw + ((size_t)(slot) * kAckSMax + j) * 128 + lane * 2; \
-    DF[j][0] += d[0];                                                        \
-    DF[j][1] += d[1];                                                        \
-    DG[j][0] += d[64];                                                       \
-    DG[j][1] += d[65];                                                       \
-  }
-  if (qtr >= 2) { OTF_PUT(qtr - 2) }
-  __syncthreads();
-  if (qtr < 2) { OTF_ADD(qtr) }
-  __syncthreads();
-  if (qtr == 1) { OTF_PUT(0) }
-  __syncthreads();
-  if (qtr == 0) { OTF_ADD(0) }
-#undef OTF_PUT
-#undef OTF_ADD
-  __syncthreads();  // reduction buffer free: the finals go to fin[k][16]
-  double *fin = red;
-  if (qtr == 0) {
-#pragma unroll
-    for (int j = 0; j < kAckSMax; ++j) {
-      if (j >= S) continue;
-      const int k = k0 + j;
-      if (k <= kmax) {
-        double *f = fin + (size_t)k * 16;
-        f[2 * c] = DF[j][0];
-        f[2 * c + 1] = DF[j][1];
-        f[8 + 2 * c] = DG[j][0];
-        f[8 + 2 * c + 1] = DG[j][1];
-      }
-    }
-  }
-  __syncthreads();
-  if (it < 2) trace_mark(3 + 2 * it, 1024);
-  // epilogue: one degree per thread (swe.py:188-251 via the prepared rows)
-  const int off = col_offset(T, m);
-  const size_t nc = p.ncoef;
-  for (int k = threadIdx.x; k < kmax; k += blockDim.x) {
-    const int l = m + k;
-    const double4 c4 = rc[k];
-    const double cz = k > 0 ? c4.z : 0.0, cw = c4.w;  // l = m has no P_{l-1}
-    const double *f = fin + (size_t)k * 16;
-    const double *gm = k > 0 ? fin + (size_t)(k - 1) * 16 + 8 : nullptr;
-    const double *gp = fin + (size_t)(k + 1) * 16 + 8;
-    double h[6];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) h[q] = fma(cz, gm ? gm[q] : 0.0, -cw * gp[q]);
-    const double llk = p.d_lconst[(T + 1) + l];  // l(l+1)/a^2
-    double2 vo = make_double2(f[0] + h[0], f[1] + h[1]);
-    double2 di = make_double2(f[2] + h[2], f[3] + h[3]);
-    double2 ph = make_double2(f[4] + h[4], f[5] + h[5]);
-    di.x += llk * f[6];
-    di.y += llk * f[7];
-    const size_t o = (size_t)off + k;
-    if (sub) {  // fused difference N(a) - N(u) of the ETD2RK step
-      const double2 b0v = sub[nc + o], b1v = sub[2 * nc + o], b2v = sub[o];
-      vo = make_double2(vo.x + b0v.x * -1.0, vo.y + b0v.y * -1.0);
-      di = make_double2(di.x + b1v.x * -1.0, di.y + b1v.y * -1.0);
-      ph = make_double2(ph.x + b2v.x * -1.0, ph.y + b2v.y * -1.0);
-    }
-    out[nc + o] = vo;
-    out[2 * nc + o] = di;
-    out[o] = ph;
-  }
-  }
-  trace_mark(6, 1024);
-}
 
 template <int MODE, int kTS = 4>
 __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
@@ -3308,224 +2443,6 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
   if (MODE == 0) trace_mark(6, 1024);
 }
 
-// ---------------------------------------------------------------------
-// Table synthesis of the state (T small enough for the P table).  The
-// recurrence is replaced by the plan-time table and the column sums become
-// DMMA GEMMs: for column m and parity plane q,
-//   out[pair][c] = sum_r Pq[r][pair] * Cq[r][c],   c = 16 coefficient columns
-// with Cq rows (degree l = m + 2r + q) = {vort, div, phi', psi, chi, w_psi,
-// w_chi, 0} (re, im): the psi/chi series and, summed by parts, their d/dlat
-// series (w_j = c_{j+1}.z v_{j+1} - c_{j-1}.w v_{j-1}, rc as in sphere.py:
-// 102-111), so all 7 series are P-series.  Plane q's w columns feed the
-// H parity 1 - q.  synth_coef_kernel builds C (row layout of the table,
-// columns rotated by (r & 3) * 4 for conflict-free B fragments);
-// synth_tab_kernel streams table tiles (2D TMA) and C rows (bulk copies)
-// through an mbarrier ring, 4 consumer warps = (parity, 8-pair tile), and
-// writes the packed grid-stage rows and Coriolis terms (state_rows).
-// ---------------------------------------------------------------------
-constexpr int kSK = 16;                       // table rows per plane per stage
-constexpr int kSTS = 4;                       // ring depth
-constexpr int kSTab = 2 * kSK * kPR;          // table doubles per stage
-constexpr int kSStage = kSTab + 2 * kSK * 16; // + coefficient rows
-constexpr size_t kSTabSmem = (size_t)kSTS * kSStage * sizeof(double) +
-                             (size_t)2 * 2 * 16 * 16 * sizeof(double) +
-                             (2 * kSTS + 4) * sizeof(uint64_t);
-static_assert((kSStage * 8) % 128 == 0 && (kSTab * 8) % 128 == 0, "TMA alignment");
-
-__global__ void synth_coef_kernel(ShtView p, const double2 *state, double *Cs) {
-  const int m = blockIdx.x;
-  const int k = blockIdx.y * blockDim.x + threadIdx.x;
-  const int T = p.trunc, nc = p.ncoef;
-  const int half = (T + 3 - m) >> 1;
-  if (k >= 2 * half) return;
-  pdl_trigger();
-  pdl_wait();  // the state comes from the preceding kernel
-  const int kmax = T + 1 - m;  // degrees k = 0..kmax (kmax: l = T + 1)
-  const int off = col_offset(T, m);
-  const double4 *rc = p.d_rc + rc_offset(T, m);
-  auto coef = [&](int kk, int f) -> double2 {  // f: 0 vort, 1 div, 2 phi
-    if (kk < 0 || kk >= kmax) return make_double2(0.0, 0.0);
-    return state[(size_t)(f == 2 ? 0 : f + 1) * nc + off + kk];
-  };
-  auto inv_lap = [&](int kk) { return kk >= 0 && kk < kmax ? p.d_lconst[m + kk] : 0.0; };
-  double c[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) c[j] = 0.0;
-  if (k <= kmax) {
-    const double2 z = coef(k, 0), d = coef(k, 1), ph = coef(k, 2);
-    const double il = inv_lap(k);
-    c[0] = z.x;
-    c[1] = z.y;
-    c[2] = d.x;
-    c[3] = d.y;
-    c[4] = ph.x;
-    c[5] = ph.y;
-    c[6] = z.x * il;
-    c[7] = z.y * il;
-    c[8] = d.x * il;
-    c[9] = d.y * il;
-    // w_k = c_{k+1}.z v_{k+1} - c_{k-1}.w v_{k-1}, v = psi, chi
-    const double czp = k + 1 <= kmax ? rc[k + 1].z : 0.0;
-    const double cwm = k >= 1 ? rc[k - 1].w : 0.0;
-    const double ilp = inv_lap(k + 1), ilm = inv_lap(k - 1);
-    const double2 zp = coef(k + 1, 0), zm = coef(k - 1, 0), dp = coef(k + 1, 1), dm = coef(k - 1, 1);
-    c[10] = czp * (zp.x * ilp) - cwm * (zm.x * ilm);
-    c[11] = czp * (zp.y * ilp) - cwm * (zm.y * ilm);
-    c[12] = czp * (dp.x * ilp) - cwm * (dm.x * ilm);
-    c[13] = czp * (dp.y * ilp) - cwm * (dm.y * ilm);
-  }
-  const int q = k & 1, r = k >> 1;
-  const size_t row = (size_t)(p.d_ptoff[m] / p.nt16) + (size_t)q * half + r;
-  double *o = Cs + row * 16;
-  const int rot = (r & 3) << 2;
-#pragma unroll
-  for (int j = 0; j < 16; j += 2)
-    *reinterpret_cast<double2 *>(o + (j ^ rot)) = make_double2(c[j], c[j + 1]);
-}
-
-constexpr int kSynThreads = 6 * 32;  // 4 consumer warps, TMA producer, epilogue warp
-
-__global__ void __launch_bounds__(kSynThreads) synth_tab_kernel(ShtView p,
-                                                                const __grid_constant__ CUtensorMap tmap,
-                                                                const double *Cs, SynthArgs a) {
-  extern __shared__ __align__(128) double ssm[];
-  double *Out = ssm + (size_t)kSTS * kSStage;  // [2 buffers][2 planes][16 pairs][16]
-  uint64_t *full = reinterpret_cast<uint64_t *>(Out + 2 * 2 * 16 * 16);
-  uint64_t *empty = full + kSTS;
-  uint64_t *ofull = empty + kSTS;   // [2] item sums ready (128 consumer threads)
-  uint64_t *oempty = ofull + 2;     // [2] item rows written (epilogue warp)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int T = p.trunc;
-  pdl_trigger();
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kSTS; ++q) {
-      mbar_init(full + q, 1);
-      mbar_init(empty + q, 4);
-    }
-    for (int b2 = 0; b2 < 2; ++b2) {
-      mbar_init(ofull + b2, 128);  // every consumer thread releases its own writes
-      mbar_init(oempty + b2, 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  pdl_wait();  // coefficient rows come from synth_coef_kernel
-  const int2 rng = p.d_sblk[blockIdx.x];
-  if (wid == 4) {
-    // ---------------- producer (one lane) ----------------
-    if (lane != 0) return;
-    const unsigned bytes = (unsigned)((kSTab + 2 * kSK * 16) * sizeof(double));
-    int qn = 0;
-    for (int it = rng.x; it < rng.y; ++it) {
-      const int2 itm = p.d_slist[it];
-      const int m = itm.x, pb = itm.y;
-      const int half = (T + 3 - m) >> 1;
-      const int nst = (half + kSK - 1) / kSK;
-      const int row0 = (int)(p.d_ptoff[m] / p.nt16);
-      for (int st = 0; st < nst; ++st, ++qn) {
-        const int slot = qn % kSTS, pass = qn / kSTS;
-        if (pass > 0) mbar_wait(empty + slot, (pass - 1) & 1);
-        mbar_expect_tx(full + slot, bytes);
-        double *sb = ssm + (size_t)slot * kSStage;
-        const int r0 = st * kSK;
-        tma_2d(sb, &tmap, pb * 16, row0 + r0, full + slot);
-        tma_2d(sb + kSK * kPR, &tmap, pb * 16, row0 + half + r0, full + slot);
-        bulk_g2s(sb + kSTab, Cs + (size_t)(row0 + r0) * 16, kSK * 16 * sizeof(double), full + slot);
-        bulk_g2s(sb + kSTab + kSK * 16, Cs + (size_t)(row0 + half + r0) * 16,
-                 kSK * 16 * sizeof(double), full + slot);
-      }
-    }
-    return;
-  }
-  if (wid == 5) {
-    // ---------------- epilogue warp: Fourier rows of the finished items ----
-    int n = 0;
-    for (int it = rng.x; it < rng.y; ++it, ++n) {
-      const int2 itm = p.d_slist[it];
-      const int m = itm.x, pb = itm.y;
-      const int ip = pb * 16 + lane;
-      const bool ep = lane < 16 && ip < p.nh;
-      double rcos = 0.0;
-      int jn = 0, js = 0;
-      double2 fr[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-      if (ep) {
-        rcos = p.d_rcos[ip];
-        jn = p.d_jn[ip];
-        js = p.d_js[ip];
-        if (a.want_lc) {
-          fr[0] = make_double2(p.d_frow[jn], p.d_frow[p.nlat + jn]);
-          fr[1] = make_double2(p.d_frow[js], p.d_frow[p.nlat + js]);
-        }
-      }
-      const int buf = n & 1;
-      mbar_wait(ofull + buf, (n >> 1) & 1);
-      const double *ob = Out + (size_t)buf * 2 * 16 * 16;
-      double2 sp[2][5], sh[2][2];
-      if (ep) {
-#pragma unroll
-        for (int qq = 0; qq < 2; ++qq) {
-          const double *o = ob + ((size_t)qq * 16 + lane) * 16;
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) sp[qq][s2] = make_double2(o[2 * s2], o[2 * s2 + 1]);
-#pragma unroll
-          for (int s2 = 0; s2 < 2; ++s2)  // plane qq's w columns: H parity 1 - qq
-            sh[1 - qq][s2] = make_double2(o[10 + 2 * s2] * rcos, o[11 + 2 * s2] * rcos);
-        }
-      }
-      if (ep) state_rows(p, a, m, ip, jn, js, rcos, sp, sh, fr);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(oempty + buf);  // buffer reads long complete
-    }
-    return;
-  }
-  // ---------------- consumers ----------------
-  const int lr = lane >> 2, lc4 = lane & 3;
-  const int q = wid & 1, t = wid >> 1;  // parity plane, 8-pair tile
-  int qn = 0, n = 0;
-  for (int it = rng.x; it < rng.y; ++it, ++n) {
-    const int2 itm = p.d_slist[it];
-    const int m = itm.x;
-    const int half = (T + 3 - m) >> 1;
-    const int nst = (half + kSK - 1) / kSK;
-    double acc[4][2][2];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int nn = 0; nn < 2; ++nn) acc[u][nn][0] = acc[u][nn][1] = 0.0;
-    for (int st = 0; st < nst; ++st, ++qn) {
-      const int slot = qn % kSTS;
-      mbar_wait(full + slot, (qn / kSTS) & 1);
-      const double *sb = ssm + (size_t)slot * kSStage;
-      const double *sT = sb + q * kSK * kPR;
-      const double *sC = sb + kSTab + q * kSK * 16;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = 4 * u + lc4;  // row within the stage
-        const bool valid = st * kSK + rr < half;
-        const double av = sT[rr * kPR + t * 8 + lr];
-#pragma unroll
-        for (int nn = 0; nn < 2; ++nn) {
-          const double bv = valid ? sC[rr * 16 + ((nn * 8 + lr) ^ (lc4 << 2))] : 0.0;
-          dmma(acc[u][nn][0], acc[u][nn][1], av, bv);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + slot);
-    }
-    // hand the item's sums to the epilogue warp (double-buffered)
-    const int buf = n & 1;
-    if (n >= 2) mbar_wait(oempty + buf, ((n >> 1) - 1) & 1);
-    double *ob = Out + (size_t)buf * 2 * 16 * 16;
-    // C fragment: pair t*8 + lr, columns nn*8 + 2*lc4 + {0, 1}
-#pragma unroll
-    for (int nn = 0; nn < 2; ++nn) {
-      double *o = ob + ((size_t)q * 16 + t * 8 + lr) * 16 + nn * 8 + 2 * lc4;
-      o[0] = (acc[0][nn][0] + acc[1][nn][0]) + (acc[2][nn][0] + acc[3][nn][0]);
-      o[1] = (acc[0][nn][1] + acc[1][nn][1]) + (acc[2][nn][1] + acc[3][nn][1]);
-    }
-    mbar_arrive(ofull + buf);
-  }
-}
 
 // FFT size of the tendency path: smallest 7-smooth n >= 3T+1 (the user
 // grid's nlon when that is already 7-smooth and alias-free)
@@ -3717,32 +2634,6 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
-  // state-synthesis items: columns longer than 128 degrees split in two at a
-  // checkpoint (multiple of kSeg), the rest whole; longest first (LPT order)
-  if (e == cudaSuccess) {
-    std::vector<int4> it;
-    int nsplit = 0;
-    for (int m = 0; m <= T; ++m) {
-      const int kmax = T + 1 - m;
-      if (kmax > 2 * kSeg) {
-        int sp = (int)std::lround(kmax / (2.0 * kSeg)) * kSeg;
-        sp = std::max(kSeg, std::min(sp, kmax - 1));
-        it.push_back(make_int4(m, 0, sp, 0));
-        it.push_back(make_int4(m, sp, kmax, 1));
-        ++nsplit;
-      } else {
-        it.push_back(make_int4(m, 0, kmax, -1));
-      }
-    }
-    std::stable_sort(it.begin(), it.end(),
-                     [](const int4 &a, const int4 &b) { return a.z - a.y > b.z - b.y; });
-    p->n_sitems = (int)it.size();
-    up((void **)&p->d_sitems, it.data(), sizeof(int4) * it.size());
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_scnt, sizeof(int) * (T + 1));
-    if (e == cudaSuccess) e = cudaMemset(p->d_scnt, 0, sizeof(int) * (T + 1));
-    if (e == cudaSuccess && nsplit)
-      e = cudaMalloc(&p->d_spart, sizeof(double2) * (size_t)(T + 1) * 2 * nh * 14);
-  }
   if (e != cudaSuccess) {
     swx_sht_destroy(p);
     return fail(SWX_ERR_CUDA, std::string("sht checkpoints: ") + cudaGetErrorString(e));
@@ -3794,14 +2685,7 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
               &p->ptab_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, p->d_ptab, dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-          const cuuint32_t box16[2] = {(cuuint32_t)kPR, (cuuint32_t)kSK};
-          if (cr == CUDA_SUCCESS)
-            cr = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(
-                &p->ptab_map16, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, p->d_ptab, dims, strides, box16,
-                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
           if (cr != CUDA_SUCCESS) e = cudaErrorInvalidValue;
-          p->tab_rows = (int)(tot / p->nt16);
         }
       }
       if (e == cudaSuccess) {
@@ -3836,20 +2720,6 @@ extern "C" int swx_sht_create(swx_sht *out, int trunc, int nlat, int nlon,
       p->fused_grid = e == cudaSuccess;
     }
   }
-  // segment starts of the on-the-fly tendency analysis
-  if (p->fused_grid && T <= kAckTMax) {
-    e = cudaMalloc(&p->d_ack, sizeof(double) * (size_t)(T + 1) * kAckSeg * ack_pitch(p->nt16) * 2);
-    if (e == cudaSuccess) e = cudaMemset(p->d_ack, 0, sizeof(double) * (size_t)(T + 1) * kAckSeg * ack_pitch(p->nt16) * 2);
-    if (e == cudaSuccess) {
-      ack_kernel<<<dim3(T + 1, (p->nt16 + 127) / 128), 128>>>(static_cast<const ShtView &>(*p));
-      e = cudaGetLastError();
-      if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    }
-    if (e != cudaSuccess) {
-      swx_sht_destroy(p);
-      return fail(SWX_ERR_CUDA, std::string("sht analysis checkpoints: ") + cudaGetErrorString(e));
-    }
-  }
   cufftHandle h;
   int rcd = get_plan(p, CUFFT_Z2D, p->nlon_t, 4 * nlat, &h);
   if (!rcd) rcd = get_plan(p, CUFFT_D2Z, p->nlon_t, 5 * nlat, &h);
@@ -3878,19 +2748,12 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_segoff);
   cudaFree(p->d_ckpt);
   cudaFree(p->d_sck);
-  cudaFree(p->d_ack);
   cudaFree(p->d_wc);
   cudaFree(p->d_arange);
   cudaFree(p->d_ptoff);
   cudaFree(p->d_ptab);
   cudaFree(p->d_rcos16);
   cudaFree(p->d_titems);
-  cudaFree(p->d_sitems);
-  cudaFree(p->d_pitems);
-  cudaFree(p->d_sblk);
-  cudaFree(p->d_slist);
-  cudaFree(p->d_scnt);
-  cudaFree(p->d_spart);
   cudaFree(p->d_tw);
   delete p;
   return SWX_OK;
@@ -3904,7 +2767,7 @@ extern "C" int swx_sht_destroy(swx_sht p) {
 //   A    : nm * 4 * nhp * kAS double
 struct ShtWs {
   double2 *c2r, *Q, *lc;
-  double *grid, *A, *Cs;
+  double *grid, *A;
   size_t bytes;
 };
 static size_t al(size_t b) { return (b + 255) / 256 * 256; }
@@ -3921,9 +2784,6 @@ static ShtWs carve(swx_sht p, void *base) {
   w.A = (double *)(c + o);
   o += al(std::max((size_t)p->nm * 4 * p->nhp * kAS, (size_t)p->nm * 4 * p->nt16 * kAG) *
           sizeof(double));
-  // table-synthesis coefficient rows (+ one stage of slack for the last column)
-  w.Cs = (double *)(c + o);
-  o += al(p->use_tab ? (size_t)(p->tab_rows + 2 * kSK) * 16 * sizeof(double) : 0);
   w.bytes = o;
   return w;
 }
@@ -3990,49 +2850,9 @@ static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int n
 }
 
 
-// column of table-analysis item `it` (items are m-major)
-static int item_col(int trunc, int it) {
-  int n = 0;
-  for (int c = 0; c <= trunc; ++c) {
-    if (n >= it) return c;
-    n += (trunc + 1 - c + kTL - 1) / kTL;
-  }
-  return trunc + 1;
-}
-
 template <int MODE>
 static int launch_analysis_tab(swx_sht p, const double *A, double2 *out, int nf, cudaStream_t s,
                                const double2 *sub = nullptr, int it0 = 0, int it1 = -1) {
-  // SWX_ANA_OTF: 0 (default) stream the P table, 1 generate P in the MMA fragments,
-  // 2 generate it for the differenced tendency only (N(a) - N(u) of
-  // the ETD2RK step: nothing runs beside it), stream it otherwise (the first
-  // tendency shares the SMs with the psi0 pole sum, which is FP64-bound: the
-  // HBM-bound table stream pairs better with it)
-  static const int otf = env_int("SWX_ANA_OTF", 0);
-  if (MODE == 0 && p->d_ack && (otf == 1 || (otf == 2 && sub))) {
-    const int m0 = item_col(p->trunc, it0);
-    const int m1 = it1 < 0 ? p->trunc + 1 : item_col(p->trunc, it1);
-    if (m1 <= m0) return SWX_OK;
-    const size_t nt = p->nt16;
-    const size_t smem = sizeof(double) * (kAckRed + 4 * nt * kAG + nt) +
-                        sizeof(double2) * ((size_t)kAckSeg * ack_pitch(p->nt16) + kAckSeg * kAckSMax + 2) + 16;
-    static size_t attr = 0;  // the largest dynamic shared memory set so far
-    if (smem > attr) {
-      SWX_CUDA_TRY(cudaFuncSetAttribute(analysis_otf_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      SWX_CUDA_TRY(cudaGetDevice(&dev));
-      SWX_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    }
-    SWX_CUDA_TRY(launch_pdl(analysis_otf_kernel, dim3(std::min(m1 - m0, nsm)), dim3(kAckThreads), smem, s,
-                            static_cast<const ShtView &>(*p), A, out, sub, m0, m1 - m0));
-    SWX_LAUNCH_CHECK();
-    return SWX_OK;
-  }
   static const int stages = env_int("SWX_TAB_STAGES", 4);  // tuning: ring depth 4 or 8
   return stages == 8 ? launch_analysis_tab_k<MODE, 8>(p, A, out, nf, s, sub, it0, it1)
                      : launch_analysis_tab_k<MODE, 4>(p, A, out, nf, s, sub, it0, it1);
@@ -4082,86 +2902,6 @@ static size_t synth_smem(int ns, int nh, int split, int nt) {
 template <int MODE>
 static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStream_t s) {
   const int ns = MODE == 0 ? 5 : 1, nh = MODE == 0 ? 2 : 0;
-  static const int st_nt = env_int("SWX_SYNTH_NT", 0), st_split = env_int("SWX_SYNTH_SPLIT", 0);
-  static const int st_grp = env_int("SWX_SYNTH_GRP", 0);
-  static const int st_two = env_int("SWX_SYNTH_TWO", 0);
-  if (MODE == 0 && st_two && nt <= 256) {
-    // two passes per staged chunk (SPLIT = 4), optionally with split items
-    const size_t smem = synth_smem(ns, nh, 1, nt);
-    auto k = synth_kernel<MODE, 4>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    static const int st_items2 = env_int("SWX_SYNTH_ITEMS", 0);
-    SynthArgs ai = a;
-    if (st_items2 && p->d_sitems && p->d_spart && g.y == 1) {
-      ai.items = p->d_sitems;
-      ai.cnt = p->d_scnt;
-      ai.part = p->d_spart;
-      g.x = p->n_sitems;
-    }
-    SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), ai));
-    return SWX_OK;
-  }
-  static const int st_ppt = env_int("SWX_SYNTH_PPT", 0);
-  if (MODE == 0 && (st_ppt == 2 || st_ppt == 3) && p->nh <= 256 * st_ppt && p->d_ckpt) {
-    // PPT latitude pairs per thread: one CTA per column, NT = pairs / PPT
-    const int ntp = std::max(32, ((p->nh + st_ppt - 1) / st_ppt + 31) / 32 * 32);
-    dim3 gp(p->nm, 1, 1);
-    const size_t smem = ((size_t)(ns + nh) * kSL * 2 + (kSL + 4) * 2) * sizeof(double);
-    auto k = st_ppt == 2 ? synth_pp_kernel<2> : synth_pp_kernel<3>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    static const int st_items = env_int("SWX_SYNTH_ITEMS", 1);
-    SynthArgs ai = a;
-    if (st_items && p->d_sitems && p->d_spart) {
-      ai.items = p->d_sitems;
-      ai.cnt = p->d_scnt;
-      ai.part = p->d_spart;
-      gp.x = p->n_sitems;
-    }
-    SWX_CUDA_TRY(launch_pdl(k, gp, dim3(ntp), smem, s, static_cast<const ShtView &>(*p), ai));
-    return SWX_OK;
-  }
-  if (MODE == 0 && st_grp && nt <= 256) {
-    // two series groups per latitude pair (SPLIT = 3)
-    const size_t smem = std::max(synth_smem(ns, nh, 1, nt), (size_t)nt * 8 * sizeof(double2));
-    auto k = synth_kernel<MODE, 3>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SWX_CUDA_TRY(launch_pdl(k, g, dim3(2 * nt), smem, s, static_cast<const ShtView &>(*p), a));
-    return SWX_OK;
-  }
-  static const int st_col = env_int("SWX_SYNTH_COL", 0);
-  if (MODE == 0 && st_col && synth_col_smem(p->trunc) <= 64 * 1024) {
-    const int ntc = st_nt > 0 ? st_nt : nt;
-    g.y = (p->nh + ntc - 1) / ntc;
-    const size_t smem = synth_col_smem(p->trunc);
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(synth_col_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int paired = st_col == 2 ? 1 : 0;
-    if (paired) g.x = p->trunc / 2 + 1;
-    synth_col_kernel<<<g, ntc, smem, s>>>(static_cast<const ShtView &>(*p), a, paired);
-    SWX_LAUNCH_CHECK();
-    return SWX_OK;
-  }
-  if (MODE == 0 && p->d_ckpt && st_nt > 0) {
-    nt = st_nt;
-    g.y = (p->nh + nt - 1) / nt;
-    SynthArgs am = a;
-    am.nyb = g.y;  // column-major dispatch: long columns' blocks first
-    g.x *= g.y;
-    g.y = 1;
-    const int sp = st_split && 2 * nt <= 512 ? 2 : 1;
-    if (sp == 1 && nt > 256) return fail(SWX_ERR_CONFIG, "SWX_SYNTH_NT > 256");
-    const size_t smem = synth_smem(ns, nh, sp, nt);
-    auto k = sp == 2 ? synth_kernel<MODE, 2> : synth_kernel<MODE, 1>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SWX_CUDA_TRY(launch_pdl(k, g, dim3(sp * nt), smem, s, static_cast<const ShtView &>(*p), am));
-    SWX_LAUNCH_CHECK();
-    return SWX_OK;
-  }
   // split long columns over two half-blocks (plain synthesis only: for the
   // 7-series state variant the 448-thread CTAs fit one per SM and lose more
   // to waves than they gain on the critical path)
@@ -4174,60 +2914,9 @@ static int launch_synth(swx_sht p, dim3 g, int nt, const SynthArgs &a, cudaStrea
   } else {
     const size_t smem = synth_smem(ns, nh, 1, nt);
     auto k = synth_kernel<MODE, 1>;
-    // cross-CTA split of the long columns: balanced, but at one 7-warp CTA per
-    // SM (142 registers) the extra items run as a second wave -- off by default
-    static const int st_items = env_int("SWX_SYNTH_ITEMS", 0);
-    // SWX_SYNTH_PSPLIT=n: columns m < n split by latitude pairs over two CTAs
-    // (measured: no gain; with 128-thread CTAs every column must be split)
-    static const int st_psplit = env_int("SWX_SYNTH_PSPLIT", 0);
-    SynthArgs ai = a;
-    if (MODE == 0 && st_psplit > 0 && g.y == 1 && p->nh >= 64 && !st_items) {
-      if (!p->d_pitems) {
-        std::vector<int4> it;
-        const int h0 = ((p->nh + 1) / 2 + 31) / 32 * 32;  // first half, whole warps
-        for (int m = 0; m <= p->trunc; ++m) {
-          if (m < st_psplit) {
-            it.push_back(make_int4(m, 0, h0, 0));
-            it.push_back(make_int4(m, h0, p->nh - h0, 0));
-          } else {
-            it.push_back(make_int4(m, 0, p->nh, 0));
-          }
-        }
-        int4 *d = nullptr;
-        SWX_CUDA_TRY(cudaMalloc(&d, sizeof(int4) * it.size()));
-        SWX_CUDA_TRY(cudaMemcpy(d, it.data(), sizeof(int4) * it.size(), cudaMemcpyHostToDevice));
-        p->d_pitems = d;
-        p->n_pitems = (int)it.size();
-      }
-      ai.pitems = p->d_pitems;
-      g.x = p->n_pitems;
-      // SWX_SYNTH_PBIG=1: one CTA per SM (the split halves get whole SMs);
-      // otherwise 128-thread CTAs (the first half's width) co-reside
-      static const int st_big = env_int("SWX_SYNTH_PBIG", 0);
-      const int h0 = ((p->nh + 1) / 2 + 31) / 32 * 32;
-      if (!st_big && st_psplit <= p->trunc)
-        return fail(SWX_ERR_CONFIG, "SWX_SYNTH_PSPLIT without PBIG must split every column");
-      const int bt = st_big ? nt : std::max(h0, p->nh - h0);
-      const size_t sm2 = synth_smem(ns, nh, 1, bt);
-      const size_t big = st_big ? std::max(sm2, (size_t)120 * 1024) : sm2;
-      static bool attr = false;
-      if (!attr && big > 48 * 1024) {
-        SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big));
-        attr = true;
-      }
-      SWX_CUDA_TRY(launch_pdl(k, g, dim3(bt), big, s, static_cast<const ShtView &>(*p), ai));
-      SWX_LAUNCH_CHECK();
-      return SWX_OK;
-    }
-    if (MODE == 0 && st_items && p->d_sitems && p->d_spart && g.y == 1) {
-      ai.items = p->d_sitems;
-      ai.cnt = p->d_scnt;
-      ai.part = p->d_spart;
-      g.x = p->n_sitems;
-    }
     if (smem > 48 * 1024)
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), ai));
+    SWX_CUDA_TRY(launch_pdl(k, g, dim3(nt), smem, s, static_cast<const ShtView &>(*p), a));
   }
   SWX_LAUNCH_CHECK();
   return SWX_OK;
@@ -4335,7 +3024,6 @@ extern "C" int swx_sht_analysis(swx_sht p, int n_fields, const double *d_grid,
   return SWX_OK;
 }
 
-static int launch_synth_tab(swx_sht p, const SynthArgs &a, ShtWs &w, cudaStream_t s);
 
 // state synthesis of columns [m0, m1) (MODE 0): the DMMA kernel for one
 // block of latitude pairs (T <= 341), the recurrence kernel otherwise
@@ -4343,6 +3031,7 @@ static int launch_state_synth(swx_sht p, const SynthArgs &a0, int m0, int m1, bo
                               cudaStream_t s) {
   int nt;
   dim3 g = synth_grid(p, 1, &nt);
+  // SWX_SYNTH_WS=0: the two-CTAs-per-SM persistent form at any nh <= 256
   static const int wsk = env_int("SWX_SYNTH_WS", 1);
   static int nsm = 0;
   if (!nsm) {
@@ -4368,8 +3057,7 @@ static int launch_state_synth(swx_sht p, const SynthArgs &a0, int m0, int m1, bo
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
-  static const int pers = env_int("SWX_SYNTH_PERS", 1);
-  if (p->d_sck && pers) {
+  if (p->d_sck) {
     const int wpb = (((p->nh + 15) / 16) + 1) / 2;  // warps per CTA: half the pairs
     const int lmax = ((p->trunc + 2) / 4 + 2 + 1) & ~1;  // longest quarter, even
     const int T1 = p->trunc + 1, TR = (T1 + 2) & ~1;
@@ -4383,19 +3071,6 @@ static int launch_state_synth(swx_sht p, const SynthArgs &a0, int m0, int m1, bo
       SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SWX_CUDA_TRY(launch_pdl(k, dim3(G), dim3(32 * wpb), smem, s,
                             static_cast<const ShtView &>(*p), a0, m0, nitems, wpb, lmax));
-    SWX_LAUNCH_CHECK();
-    return SWX_OK;
-  }
-  if (p->d_sck) {
-    const int wpb = (((p->nh + 15) / 16) + 1) / 2;  // warps per CTA: half the pairs
-    const int lmax = ((p->trunc + 2) / 4 + 2 + 1) & ~1;  // longest quarter, even
-    const size_t stage = (size_t)(4 * (lmax * 16 + 8) + 8 * (lmax + 2)) * sizeof(double);
-    const size_t smem = std::max(stage, (size_t)wpb * 256 * sizeof(double2));
-    auto k = peer ? synth_mma_kernel<true> : synth_mma_kernel<false>;
-    if (smem > 48 * 1024)
-      SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SWX_CUDA_TRY(launch_pdl(k, dim3(2 * (m1 - m0)), dim3(32 * wpb), smem, s,
-                            static_cast<const ShtView &>(*p), a0, m0, wpb, lmax));
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
@@ -4421,11 +3096,6 @@ static int synth_state(swx_sht p, const double2 *state, ShtWs &w, int want_lc, i
   a.lc = w.lc;
   a.want_lc = want_lc;
   a.nfreq = nfreq;
-  // table synthesis (DMMA over the streamed Legendre table) above truncation
-  // SWX_SYNTH_TAB_BIG (default -1: off; at T1279 the launch is 1.91 -> 1.63 ms
-  // but the ETD2RK step 8.89 -> 9.00 ms: it competes with the overlapped psi0)
-  static const int tab_big = env_int("SWX_SYNTH_TAB_BIG", -1);
-  if (p->use_tab && tab_big >= 0 && p->trunc > tab_big) return launch_synth_tab(p, a, w, s);
   return launch_state_synth(p, a, 0, p->trunc + 1, false, s);
 }
 
@@ -4479,57 +3149,6 @@ extern "C" int swx_sht_vortdiv(swx_sht p, const double *d_u, const double *d_v,
 // table synthesis of the state: coefficient rows, then the streamed DMMA sums.
 // Items (m, 16-pair block) are assigned to persistent CTAs longest-first to
 // the least-loaded CTA (cost = stages + 1), once per plan.
-static int launch_synth_tab(swx_sht p, const SynthArgs &a, ShtWs &w, cudaStream_t s) {
-  const int T = p->trunc;
-  if (!p->d_sblk) {
-    SWX_CUDA_TRY(cudaFuncSetAttribute(synth_tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kSTabSmem));
-    int b = 0;
-    SWX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, synth_tab_kernel, kSynThreads,
-                                                               kSTabSmem));
-    int dev = 0, nsm = 0;
-    SWX_CUDA_TRY(cudaGetDevice(&dev));
-    SWX_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    std::vector<std::pair<int, int2>> items;  // (cost, (m, pb))
-    const int npb = p->nt16 / 16;
-    for (int m = 0; m <= T; ++m) {
-      const int half = (T + 3 - m) / 2;
-      const int cost = (half + kSK - 1) / kSK + 1;
-      for (int pb = 0; pb < npb; ++pb) items.push_back({cost, make_int2(m, pb)});
-    }
-    std::stable_sort(items.begin(), items.end(),
-                     [](const std::pair<int, int2> &x, const std::pair<int, int2> &y) {
-                       return x.first > y.first;
-                     });
-    const int nc = std::max(1, std::min((int)items.size(), nsm * std::max(b, 1)));
-    std::vector<std::vector<int2>> lists(nc);
-    std::vector<long long> load(nc, 0);
-    for (auto &it : items) {  // LPT: least-loaded CTA first
-      int k = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-      lists[k].push_back(it.second);
-      load[k] += it.first;
-    }
-    std::vector<int2> blk(nc), flat;
-    for (int k = 0; k < nc; ++k) {
-      blk[k] = make_int2((int)flat.size(), (int)(flat.size() + lists[k].size()));
-      flat.insert(flat.end(), lists[k].begin(), lists[k].end());
-    }
-    int2 *d_blk = nullptr, *d_list = nullptr;
-    SWX_CUDA_TRY(cudaMalloc(&d_blk, sizeof(int2) * blk.size()));
-    SWX_CUDA_TRY(cudaMalloc(&d_list, sizeof(int2) * flat.size()));
-    SWX_CUDA_TRY(cudaMemcpy(d_blk, blk.data(), sizeof(int2) * blk.size(), cudaMemcpyHostToDevice));
-    SWX_CUDA_TRY(cudaMemcpy(d_list, flat.data(), sizeof(int2) * flat.size(), cudaMemcpyHostToDevice));
-    p->d_sblk = d_blk;
-    p->d_slist = d_list;
-    p->n_sblk = nc;
-  }
-  SWX_CUDA_TRY(launch_pdl(synth_coef_kernel, dim3(T + 1, (T + 3 + 127) / 128), dim3(128), 0, s,
-                          static_cast<const ShtView &>(*p), a.coef, w.Cs));
-  SWX_CUDA_TRY(launch_pdl(synth_tab_kernel, dim3(p->n_sblk), dim3(kSynThreads), kSTabSmem, s,
-                          static_cast<const ShtView &>(*p), p->ptab_map16, (const double *)w.Cs,
-                          a));
-  return SWX_OK;
-}
 
 template <int R>
 static int launch_grid_sq1(swx_sht p, int atoms, ShtWs &w, cudaStream_t s, int i0, int npairs) {
@@ -4624,14 +3243,7 @@ static int tendency_impl(swx_sht p, int atoms, const double2 *state, double2 *ou
     a.want_lc = (atoms & SWX_TEND_LC) ? 1 : 0;
     a.nfreq = p->nfreq_t;
     a.zpack = 1;  // packed north/south rows for the fused grid stage
-    // table synthesis (DMMA): correct but slower than the recurrence kernel at
-    // T256 (2 CTAs/SM at 144 registers) -- opt-in
-    static const int st_tab = env_int("SWX_SYNTH_TAB", 0);
-    if (st_tab) {
-      if ((rc = launch_synth_tab(p, a, w, s))) return rc;
-    } else if ((rc = launch_state_synth(p, a, 0, p->trunc + 1, false, s))) {
-      return rc;
-    }
+    if ((rc = launch_state_synth(p, a, 0, p->trunc + 1, false, s))) return rc;
     if (p->synth_done) SWX_CUDA_TRY(cudaEventRecord(p->synth_done, s));
     mark(1);
     mark(2);

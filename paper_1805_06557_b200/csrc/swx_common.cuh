@@ -96,9 +96,6 @@ struct swx_solver_s {
   // cache, solvers.py:168-194), layout [pole/32][slot][chain][pole%32]
   double2 *d_linv = nullptr;
   size_t linv_bytes = 0;
-  int linv_tw = 0;  // cache in the twisted layout (rexi_l_tw_kernel)
-  // twisted-kernel schedules (LPT item lists per warp pair), keyed by (P, pairs)
-  std::map<std::pair<int, int>, std::pair<int2 *, int *>> tw_sched;
   int l_blocks_per_sm = 0;
 };
 

@@ -33,7 +33,3 @@ print("step_dev us", tm(lambda: eng.step_dev()))
 print("step (e2e) us", tm(lambda: st.step(s0, 1800.0)))
 print("np.take one field us", tm(lambda: np.take(np.ascontiguousarray(fields[0]).reshape(-1), flat_index(T), out=stage.np_in[0])))
 print("host cpus", torch.get_num_threads())
-import paper_1805_06557_b200.steppers as S
-for flag in (False, True, False, True):
-    S._E2E_GRAPH = flag
-    print("e2e graph=%s us" % flag, tm(lambda: st.step(s0, 1800.0), k=50))

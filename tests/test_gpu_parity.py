@@ -542,34 +542,6 @@ def test_column_sharded_t1279_round_trip(K):
     assert rel_linf(got.cpu().numpy(), c.cpu().numpy()) <= 1e-10
 
 
-@pytest.mark.parametrize("trunc", [63, 256])
-def test_pipelined_etdrk_bitwise(trunc, monkeypatch):
-    """The column-block pipelined ETD2RK step (analysis -> psi_k -> synthesis
-    chains overlapped per column block, the next step's synthesis at the end
-    of each step) equals the plain step graph bitwise over 3 steps, both
-    device-resident and through step_host."""
-    import paper_1805_06557_b200.steppers as S
-    par = params(trunc)
-    ic = ost.seeded_balanced_state(osh.grid_for(trunc))
-    setup = RexiSetup(num_poles=128)
-    engines = {}
-    for blocks in (0, 2, 3):
-        monkeypatch.setattr(S, "_PIPE_BLOCKS", blocks)
-        st = S.EtdrkStepper(LG, LC_N, par, setup)
-        eng = st.engine(1800.0)
-        assert eng.pipe == (blocks > 1)
-        eng.load(ic)
-        for _ in range(3):
-            eng.step_dev()
-        engines[blocks] = (st, eng.u.cpu().numpy())
-    ref = engines[0][1]
-    assert np.array_equal(engines[2][1], ref) and np.array_equal(engines[3][1], ref)
-    s0 = PrognosticState.from_stack(ic, par.cfg)
-    a = engines[0][0].step(s0, 1800.0).stack()
-    b = engines[2][0].step(s0, 1800.0).stack()
-    assert np.array_equal(a, b)
-
-
 def test_cfg3_stiffness_sweep_t256_matches_oracle_verdicts():
     """cfg3: all 36 (Phibar, dt) cases of the stiffness sweep at T256
     (contours per workloads.stiffness_cases, N up to 2048), 24 device-resident
@@ -783,20 +755,6 @@ def test_l_rexi_n_etdrk_vs_oracle():
     res = integrate(stepper, PrognosticState.from_stack(ic, par.cfg), dt, 3 * dt)
     assert not res.diverged
     assert rel_l2(pack(res.state.stack()), olay.pack(ref)) <= 1e-10
-
-
-def test_twisted_l_chains_opt_in(golden_small, golden_medium, monkeypatch):
-    """The opt-in twisted chain solve (SWX_L_TWIST=1: both ends of every chain
-    eliminated by a warp pair, pivots cached in the twisted layout) against
-    the reference's T42 and cfg1 l steps."""
-    monkeypatch.setenv("SWX_L_TWIST", "1")
-    for trunc, dt, n, src, key in ((42, 3600.0, 128, golden_small, "T42_l128"),
-                                   (128, 7200.0, 256, golden_medium, "cfg1")):
-        par = params(trunc)
-        c = coeffs(n)
-        solver = ShiftedLinearSolver(L, dt, par)  # fresh: warms (and caches) twisted
-        out = solver.rexi_sum(c.alphas, c.betas, unpack(src[key + "_in"], trunc))
-        assert rel_linf(pack(out) if out.ndim == 3 else out, src[key + "_out"]) <= LIN_BAR, key
 
 
 @pytest.mark.parametrize("trunc", [170, 300, 341])
