@@ -122,6 +122,21 @@ int swx_rexi_sum_prepared_axpy(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
                                double scale, swx_c128 *d_out, void *d_workspace,
                                size_t workspace_bytes, void *stream);
 
+/* The prepared sum (d_base may be null: plain sum) started from a table
+ * analysis' column counters instead of stream order: d_ready is the address
+ * returned by swx_sht_set_done_signal for the SH plan whose signalled
+ * tendency immediately precedes this call on the stream.  The pole-sum items
+ * (degree l, 32 modes) wait for their columns (generation x item count;
+ * the counters only grow), so the sum overlaps the tail of the analysis.
+ * One stream per SH plan.  Same arithmetic as
+ * swx_rexi_sum_prepared(_axpy) (bitwise).  Replaces the stream-ordered
+ * `etdrk2_generic` pole sums of steppers.py:259-269 on the device step.     */
+int swx_rexi_sum_prepared_ready(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                                const swx_c128 *d_betas, const void *d_prep, int pole_begin,
+                                int pole_end, int realify, const swx_c128 *d_base,
+                                double scale, swx_c128 *d_out, void *d_workspace,
+                                size_t workspace_bytes, int *d_ready, void *stream);
+
 /* Forward operator (dt L + alpha) x -- apply_stacked, solvers.py:252-256.   */
 int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,
               swx_c128 *d_out, void *stream);
@@ -183,6 +198,13 @@ int swx_sht_tendency(swx_sht p, int atoms, const swx_c128 *d_state,
  * so independent work on another stream can overlap the lighter grid and
  * analysis stages instead of the FP64-bound synthesis.                      */
 int swx_sht_set_synth_event(swx_sht p, void *event);
+/* Column hand-off to a following lg pole sum: while on, the tendency's table
+ * analysis bumps a generation counter (d_counters[T+1]) before it lets
+ * dependent kernels launch and counts each completed item in per-column
+ * counters d_counters[m]; *d_counters receives their address (pass it to
+ * swx_rexi_sum_prepared_ready).  Needs the table analysis (the fused-stage
+ * plans).  No reference counterpart (device scheduling).                    */
+int swx_sht_set_done_signal(swx_sht p, int on, int **d_counters);
 /* d_out = tendency(d_state) - d_sub, the difference N(a) - N(u) of the
  * ETD2RK stage (steppers.py:262-266) fused into the analysis epilogue;
  * bitwise equal to swx_sht_tendency followed by swx_state_axpy(-1).        */

@@ -45,6 +45,7 @@ SIGNATURES = {
     "swx_rexi_prepare": (_I, [_P, _I, _P, _I, _I, _P, _S, _P]),
     "swx_rexi_sum_prepared": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _S, _P]),
     "swx_rexi_sum_prepared_axpy": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P, _D, _P, _P, _S, _P]),
+    "swx_rexi_sum_prepared_ready": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P, _D, _P, _P, _S, _P, _P]),
     "swx_apply": (_I, [_P, C128, _P, _P, _P]),
     "swx_tree_combine": (_I, [_I, _I, _I, _P, _I, _P, _P]),
     "swx_tree_combine_flat": (_I, [_S, _I, _P, _P, _P]),
@@ -59,6 +60,7 @@ SIGNATURES = {
     "swx_sht_tendency": (_I, [_P, _I, _P, _P, _P, _S, _P]),
     "swx_sht_tendency_sub": (_I, [_P, _I, _P, _P, _P, _P, _S, _P]),
     "swx_sht_set_synth_event": (_I, [_P, _P]),
+    "swx_sht_set_done_signal": (_I, [_P, _I, ctypes.POINTER(_P)]),
     "swx_sht_tendency_profile": (_I, [_P, _I, _P, _P, _P, _S, _P, _P]),
     "swx_fp64_fma_probe": (_I, [_P, _I, _I, _P]),
     "swx_host_pack": (_I, [_I, _I, _P, _P]),

@@ -334,6 +334,15 @@ __global__ void __launch_bounds__(128) rexi_lg_kernel(
   }
 }
 
+// degrees per table-analysis item (sht.cu kTL): a column of length T+1-m is
+// complete after ceil((T+1-m)/kAnaItemDeg) items
+constexpr int kAnaItemDeg = 32;
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 #ifndef SWX_LG_MINB
 #define SWX_LG_MINB 3  // resident CTAs per SM the two-mode kernel's register budget targets
 #endif
@@ -345,10 +354,18 @@ template <int NRHS, int NP, int LPM, int MPL, bool PR = false>
 __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ fac_g, int trunc, int ncoef,
     const int4 *__restrict__ sched, int n_items, int realify, Axpy ep, int fac_ready,
-    double2 *__restrict__ out) {
+    int *__restrict__ ready, double2 *__restrict__ out) {
   constexpr int PPL = NP / LPM;          // poles per lane
   constexpr int GROUPS = 128 / LPM;      // lane groups per CTA
   extern __shared__ double2 fac[];       // [NRHS][4][NP], interleaved (t*LPM + q)
+  // column hand-off: this launch consumes the analysis generation current at
+  // launch (the producer bumps it before it lets dependents launch); read it
+  // before letting the next kernel launch, so a later analysis cannot bump it
+  __shared__ int s_gen;
+  if (ready) {
+    if (threadIdx.x == 0) s_gen = ld_acquire(ready + trunc + 1);
+    __syncthreads();
+  }
   pdl_trigger();
   trace_mark(0);
   // prepared factor tables do not depend on the preceding kernel: stage them
@@ -364,8 +381,27 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
     double4 *dst = reinterpret_cast<double4 *>(fac);
     for (int i = threadIdx.x; i < NRHS * 2 * NP; i += blockDim.x) dst[i] = src[i];
   }
-  __syncthreads();
-  pdl_wait();
+  if (ready) {
+    // column hand-off from the table analysis (swx_sht_set_done_signal): the
+    // item's columns are complete when all their analysis items have counted
+    // in; ordered after the analysis' stores by its fence + this acquire
+    // one thread per column of the item (<= 128 modes per item), in parallel
+    const int m = m0 + (int)threadIdx.x;
+    if (m < min(m1, l + 1)) {
+      // the counters only grow: generation g of the column is complete at
+      // g x (its item count)
+      const int need = s_gen * ((trunc + 1 - m + kAnaItemDeg - 1) / kAnaItemDeg);
+      // bounded wait (~4 s): a missing count must not hang the device
+      for (long long spin = 0; ld_acquire(ready + m) < need; ++spin) {
+        if (spin > (1LL << 25)) __trap();
+        __nanosleep(128);
+      }
+    }
+    __syncthreads();
+  } else {
+    __syncthreads();
+    pdl_wait();
+  }
   if (it == blockIdx.x) trace_mark(1);
   const int q = threadIdx.x & (LPM - 1);
   const int g = threadIdx.x / LPM;
@@ -1350,11 +1386,19 @@ static const int4 *lg_schedule(swx_solver s, int mpc_in, int *n_cta) {
   const int lo = s->col_lo, hi = s->col_hi < 0 ? s->trunc + 1 : s->col_hi;
   auto &e = s->lg_sched[std::make_tuple(mpc_in, lo, hi)];
   if (!e.first) {
-    const int mpc = mpc_in < 0 ? -mpc_in : mpc_in;
+    // bit 16 of mpc_in: column-block-major order (the analysis hand-off)
+    const bool mmajor = mpc_in > 0 && (mpc_in >> 16) != 0;
+    const int mpc = mpc_in < 0 ? -mpc_in : (mpc_in & 0xffff);
     std::vector<int4> sched;
-    for (int l = s->trunc; l >= lo; --l)
-      for (int m0 = lo; m0 <= l && m0 < hi; m0 += mpc)
-        sched.push_back(make_int4(l, m0, std::min(std::min(l + 1, hi), m0 + mpc), 0));
+    if (mmajor) {
+      for (int m0 = lo; m0 < hi; m0 += mpc)
+        for (int l = s->trunc; l >= m0; --l)
+          sched.push_back(make_int4(l, m0, std::min(std::min(l + 1, hi), m0 + mpc), 0));
+    } else {
+      for (int l = s->trunc; l >= lo; --l)
+        for (int m0 = lo; m0 <= l && m0 < hi; m0 += mpc)
+          sched.push_back(make_int4(l, m0, std::min(std::min(l + 1, hi), m0 + mpc), 0));
+    }
     if (sched.empty()) sched.push_back(make_int4(0, 0, 0, 0));  // empty shard: one idle CTA
     if (mpc_in < 0)
       std::stable_sort(sched.begin(), sched.end(),
@@ -1411,7 +1455,7 @@ static int build_lg_factors(swx_solver s, const double2 *betas, int pole0, int P
 template <int NRHS>
 static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, int realify,
                   double2 *out, cudaStream_t st, Axpy ep = Axpy{nullptr, 0.0},
-                  int fac_ready = 0) {
+                  int fac_ready = 0, int *ready = nullptr) {
   LgGeom g;
   int rc = lg_geom(P, g);
   if (rc) return rc;
@@ -1430,7 +1474,11 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
     };
     while (passes > 1 && items_for(passes * 4 * 32 / g.lpm) < 2L * sm_count()) passes /= 2;
   }
-  const int4 *sched = lg_schedule(s, passes * 4 * 32 / g.lpm, &n_cta);
+  // the column hand-off needs the static two-mode kernel and a whole-column
+  // schedule in column order (the analysis completes columns roughly in m)
+  const bool hand = ready && g.lpm == 8 && g.ppl == 32 && s->col_lo == 0 && s->col_hi < 0;
+  if (!hand) ready = nullptr;  // not served: stream order (wait for the whole analysis)
+  const int4 *sched = lg_schedule(s, (hand ? 1 << 16 : 0) + passes * 4 * 32 / g.lpm, &n_cta);
   if (!sched) return fail(SWX_ERR_CUDA, "lg schedule allocation failed");
   const size_t smem = (size_t)NRHS * 4 * g.np * sizeof(double2);
 #define SWX_LG_CASE(LV)                                                                        \
@@ -1457,7 +1505,7 @@ static int run_lg(swx_solver s, const double2 *rhs, const double2 *fac, int P, i
       attr[env_pair][NRHS] = true;
     }
     SWX_CUDA_TRY(launch_pdl(k, dim3(n_cta), dim3(128), smem, st, rhs, fac, s->trunc, s->ncoef,
-                            sched, n_cta, realify, ep, fac_ready, out));
+                            sched, n_cta, realify, ep, fac_ready, ready, out));
     SWX_LAUNCH_CHECK();
     return SWX_OK;
   }
@@ -1632,11 +1680,13 @@ extern "C" int swx_rexi_prepare(swx_solver s, int n_rhs, const swx_c128 *d_betas
 static int rexi_sum_prepared_impl(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
                                   const swx_c128 *d_betas, const void *d_prep, int pole_begin,
                                   int pole_end, int realify, Axpy ep, swx_c128 *d_out,
-                                  void *d_workspace, size_t workspace_bytes, void *stream) {
+                                  void *d_workspace, size_t workspace_bytes, void *stream,
+                                  int *ready = nullptr) {
   const bool cor = s && s->group == SWX_GROUP_L && s->omega > 0.0;
-  if (!s || cor || !d_prep)  // nothing prepared for the chain solver
+  if (!s || cor || !d_prep) {  // nothing prepared for the chain solver: stream order
     return rexi_sum_impl(s, n_rhs, d_rhs, d_betas, pole_begin, pole_end, realify, ep, d_out,
                          d_workspace, workspace_bytes, stream);
+  }
   if (n_rhs < 1 || n_rhs > 2) return fail(SWX_ERR_CONFIG, "n_rhs must be 1 or 2");
   if (pole_begin < 0 || pole_end > s->n_poles || pole_end <= pole_begin)
     return fail(SWX_ERR_CONFIG, "bad pole range");
@@ -1647,8 +1697,8 @@ static int rexi_sum_prepared_impl(swx_solver s, int n_rhs, const swx_c128 *d_rhs
   const int chunks = (P + kLgMaxP - 1) / kLgMaxP;
   const size_t t = swx_rexi_prepared_bytes(s, n_rhs, pole_begin, pole_end) / chunks;
   if (chunks == 1)
-    return n_rhs == 1 ? run_lg<1>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep, 1)
-                      : run_lg<2>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep, 1);
+    return n_rhs == 1 ? run_lg<1>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep, 1, ready)
+                      : run_lg<2>(s, rhs, (const double2 *)d_prep, P, realify, out, st, ep, 1, ready);
   const size_t stride = (size_t)n_rhs * 3 * s->ncoef;
   if (!d_workspace || workspace_bytes < chunks * stride * sizeof(double2))
     return fail(SWX_ERR_CONFIG, "workspace too small");
@@ -1685,6 +1735,18 @@ extern "C" int swx_rexi_sum_prepared_axpy(swx_solver s, int n_rhs, const swx_c12
   return rexi_sum_prepared_impl(s, n_rhs, d_rhs, d_betas, d_prep, pole_begin, pole_end, realify,
                                 Axpy{(const double2 *)d_base, scale}, d_out, d_workspace,
                                 workspace_bytes, stream);
+}
+
+extern "C" int swx_rexi_sum_prepared_ready(swx_solver s, int n_rhs, const swx_c128 *d_rhs,
+                                           const swx_c128 *d_betas, const void *d_prep,
+                                           int pole_begin, int pole_end, int realify,
+                                           const swx_c128 *d_base, double scale,
+                                           swx_c128 *d_out, void *d_workspace,
+                                           size_t workspace_bytes, int *d_ready, void *stream) {
+  if (!d_ready) return fail(SWX_ERR_CONFIG, "null column counters");
+  return rexi_sum_prepared_impl(s, n_rhs, d_rhs, d_betas, d_prep, pole_begin, pole_end, realify,
+                                Axpy{(const double2 *)d_base, scale}, d_out, d_workspace,
+                                workspace_bytes, stream, d_ready);
 }
 
 extern "C" int swx_apply(swx_solver s, swx_c128 alpha, const swx_c128 *d_x,

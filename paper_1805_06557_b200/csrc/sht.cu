@@ -105,6 +105,10 @@ struct ShtView {
 
 struct swx_sht_s : ShtView {
   std::map<long long, cufftHandle> plans;
+  // column hand-off to a following lg pole sum (swx_sht_set_done_signal):
+  // [T+1] per-column item counters + [1] CTA counter of the consumer
+  int *d_done = nullptr;
+  int done_signal = 0;
   cudaEvent_t synth_done = nullptr;  // recorded after each tendency's synthesis (optional)
   CUtensorMap ptab_map;    // 2D view [rows][nt16] of the P table, box kTBox x 17
 };
@@ -2302,7 +2306,8 @@ template <int MODE, int kTS = 4>
 __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
                                                                    const __grid_constant__ CUtensorMap tmap,
                                                                    const double *A, double2 *out,
-                                                                   int nf, const double2 *sub) {
+                                                                   int nf, const double2 *sub,
+                                                                   int *done) {
   extern __shared__ __align__(128) double tsm[];
   uint64_t *full = reinterpret_cast<uint64_t *>(tsm + (size_t)kTS * kStage);
   uint64_t *empty = full + kTS;
@@ -2311,6 +2316,15 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
   const int nst = nt / kTK;  // stages per item
   constexpr int NPART = MODE == 0 ? 2 : 1;
   const size_t ps = (size_t)nt * kAG;
+  if (done && blockIdx.x == 0) {
+    // column hand-off: bump the generation before any dependent can launch
+    // (the consumer reads it at launch and waits for generation x items)
+    if (threadIdx.x == 0) {
+      const int g = atomicAdd(done + T + 1, 1);
+      if (g < 0) done[T + 1] = 0;  // (uses the result: the add has completed)
+    }
+    __syncthreads();
+  }
   pdl_trigger();
   if (MODE == 0) trace_mark(0, 1024);
   if (threadIdx.x == 0) {
@@ -2439,6 +2453,12 @@ __global__ void __launch_bounds__(kTabThreads) analysis_tab_kernel(ShtView p,
     } else {
       if (valid && lc4 < nf) out[(size_t)lc4 * p.ncoef + slotc] = make_double2(cp0, cp1);
     }
+    if (done) {  // count the item in for column m (the lg hand-off): fence, then signal
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(kTCW * 32) : "memory");
+      if (threadIdx.x == 0) atomicAdd(done + m, 1);
+    }
+    if (MODE == 0 && it == (int)blockIdx.x) trace_mark(2, 1024);
   }
   if (MODE == 0) trace_mark(6, 1024);
 }
@@ -2748,6 +2768,7 @@ extern "C" int swx_sht_destroy(swx_sht p) {
   cudaFree(p->d_segoff);
   cudaFree(p->d_ckpt);
   cudaFree(p->d_sck);
+  cudaFree(p->d_done);
   cudaFree(p->d_wc);
   cudaFree(p->d_arange);
   cudaFree(p->d_ptoff);
@@ -2843,8 +2864,9 @@ static int launch_analysis_tab_k(swx_sht p, const double *A, double2 *out, int n
   const int slots = nsm * per_sm;
   const int per_cta = (v.n_titems + slots - 1) / slots;
   const int blocks = std::max(1, (v.n_titems + per_cta - 1) / per_cta);
+  int *done = MODE == 0 && p->done_signal ? p->d_done : nullptr;
   SWX_CUDA_TRY(launch_pdl(k, dim3(blocks), dim3(kTabThreads), smem, s, v, p->ptab_map, A, out, nf,
-                          sub));
+                          sub, done));
   SWX_LAUNCH_CHECK();
   return SWX_OK;
 }
@@ -3398,6 +3420,18 @@ extern "C" int swx_trace(int enable, unsigned long long *h_out, int n_ctas) {
 // after the synthesis of every subsequent tendency of this plan, so a caller
 // can start independent work on another stream once the synthesis -- the
 // FP64-heaviest stage -- has finished (the ETD2RK engine starts psi0(u) there).
+extern "C" int swx_sht_set_done_signal(swx_sht p, int on, int **d_counters) {
+  if (!p) return fail(SWX_ERR_CONFIG, "null SHT plan");
+  if (on && !p->use_tab) return fail(SWX_ERR_CONFIG, "the column hand-off needs the table analysis");
+  if (on && !p->d_done) {
+    SWX_CUDA_TRY(cudaMalloc(&p->d_done, sizeof(int) * (p->trunc + 2)));
+    SWX_CUDA_TRY(cudaMemset(p->d_done, 0, sizeof(int) * (p->trunc + 2)));
+  }
+  p->done_signal = on ? 1 : 0;
+  if (d_counters) *d_counters = p->d_done;
+  return SWX_OK;
+}
+
 extern "C" int swx_sht_set_synth_event(swx_sht p, void *event) {
   if (!p) return fail(SWX_ERR_CONFIG, "null plan");
   p->synth_done = (cudaEvent_t)event;

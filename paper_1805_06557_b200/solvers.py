@@ -199,11 +199,22 @@ class ShiftedLinearSolver:
         return buf
 
     def rexi_sum_prepared_dev(self, alphas, betas_dev, prep, rhs_dev, out_dev, pole_range=None,
-                              realify: bool = True, stream=None, base=None, scale: float = 0.0):
-        """Prepared pole sum; with ``base``: out = base + scale * sum (fused)."""
+                              realify: bool = True, stream=None, base=None, scale: float = 0.0,
+                              ready: int = 0):
+        """Prepared pole sum; with ``base``: out = base + scale * sum (fused).
+        ``ready``: device address of an SH plan's column counters
+        (SHTPlan.set_done_signal) -- the sum starts on columns as the preceding
+        table analysis completes them instead of after the whole analysis."""
         nat = self._native(alphas)
         n_rhs = rhs_dev.shape[0]
         lo, hi = pole_range if pole_range is not None else (0, nat.alphas.size)
+        if ready:
+            ws, nbytes = self.workspace(nat, n_rhs, lo, hi, stream)
+            _lib.check(self._lib.swx_rexi_sum_prepared_ready(
+                nat.h, n_rhs, ptr(rhs_dev), ptr(betas_dev), ptr(prep) if prep is not None else 0,
+                lo, hi, 1 if realify else 0, ptr(base) if base is not None else 0, float(scale),
+                ptr(out_dev), ptr(ws) if nbytes else 0, nbytes, int(ready), stream_ptr(stream)))
+            return out_dev
         if prep is None and base is None:
             return self.rexi_sum_dev(alphas, betas_dev, rhs_dev, out_dev, pole_range, realify,
                                      stream)

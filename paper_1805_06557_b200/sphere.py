@@ -231,6 +231,20 @@ class ShtPlan:
         _lib.check(self._lib.swx_sht_set_synth_event(
             self._h, event.cuda_event if event is not None else 0))
 
+    def set_done_signal(self, on: bool) -> int:
+        """While on, the following tendency calls count each completed table-
+        analysis item in per-column device counters (and bump a generation
+        counter per call), whose address is returned (0 if the plan has no
+        table analysis): an lg pole sum given that address (``ready=``) right
+        after a signalled tendency on the same stream starts on columns as they
+        complete.  The counters only grow, so a signalled call without a
+        waiting pole sum is harmless; one stream per plan."""
+        if on and not self.fused_stages():
+            return 0
+        out = ctypes.c_void_p()
+        _lib.check(self._lib.swx_sht_set_done_signal(self._h, 1 if on else 0, ctypes.byref(out)))
+        return int(out.value or 0)
+
     def fused_stages(self) -> bool:
         """Whether the tendency has separable stages (fused grid / table path)."""
         return bool(self._lib.swx_sht_has_stages(self._h))

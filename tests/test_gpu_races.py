@@ -7,6 +7,9 @@ this GPU pool: profiles/r02/sanitizer_unavailable.txt).
   cache streamed through a bulk-copy ring) is run many times on the same
   input; a shared-memory or cross-CTA race shows up as a bitwise difference
   between runs.
+* Hand-off: the pole sum that starts on columns as the table analysis
+  completes them (generation-counted, no stream-order wait) is checked across
+  back-to-back steps against steps with a full synchronisation in between.
 * Canaries: outputs are written into the middle of larger buffers whose
   guard regions hold a NaN bit pattern; a write outside the output slice
   (a bad index or a tail CTA) changes a guard word.
@@ -48,9 +51,11 @@ def guards_intact(buf, n: int) -> bool:
     return bool(np.all(lo == pat) and np.all(hi == pat))
 
 
-@pytest.mark.parametrize("trunc", [63, 256])
+@pytest.mark.parametrize("trunc", [63, 85, 256])
 def test_etdrk_step_graph_repeat_bitwise(trunc):
-    """30 replays of the captured ETD2RK step from the same state: identical bits."""
+    """30 replays of the captured ETD2RK step from the same state: identical bits
+    (the step includes the analysis -> pole-sum column hand-off, whose early
+    starts are most likely at small T where the kernels co-reside)."""
     g = 9.80616
     cfg = SphereConfig.for_truncation(trunc)
     par = ModelParams(1e4 * g, cfg)
@@ -112,3 +117,25 @@ def test_pole_sum_repeat_bitwise_and_guards(group, trunc, n_poles):
         assert torch.equal(cur, ref)
     torch.cuda.synchronize()
     assert guards_intact(buf, n)
+
+
+@pytest.mark.parametrize("trunc", [42, 85])
+def test_handoff_steps_equal_synchronised_steps(trunc):
+    """Ten back-to-back captured ETD2RK steps (each pole sum may start while
+    the preceding analysis still runs, and the next step's kernels launch
+    early) equal ten steps with a device synchronisation after each: bitwise."""
+    g = 9.80616
+    cfg = SphereConfig.for_truncation(trunc)
+    par = ModelParams(1e4 * g, cfg)
+    st = EtdrkStepper(LG, LC_N, par, RexiSetup(num_poles=256))
+    eng = st.engine(900.0)
+    u0 = to_device(pack(seeded_balanced_state(cfg)))
+    eng.u.copy_(u0)
+    for _ in range(10):
+        eng.step_dev()
+    back_to_back = eng.u.clone()
+    eng.u.copy_(u0)
+    for _ in range(10):
+        eng.step_dev()
+        torch.cuda.synchronize()
+    assert torch.equal(back_to_back, eng.u)
