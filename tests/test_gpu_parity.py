@@ -391,6 +391,37 @@ def test_split_and_explicit_steppers_golden(golden_split, sid):
     assert rel_l2(pack(st.stack()), golden_split[f"T21split_{sid}"]) <= 1e-10
 
 
+@pytest.mark.parametrize("sid", ["lg_rexi_lc_n_erk_ver0", "lg_irk_lc_n_erk_ver1",
+                                 "lg_rexi_lc_n_erk_ver1"])
+def test_split_steppers_device_resident_match_host_path(sid):
+    """The device-resident Strang split (one upload, three device sub-steps,
+    one download) equals the host-composed path (taken when instrumented)
+    to rounding, at T85."""
+    import time
+
+    from paper_1805_06557_b200.steppers import TimingCollector
+
+    par = params(85)
+    st0 = PrognosticState.from_stack(ost.seeded_balanced_state(osh.grid_for(85)), par.cfg)
+    dev = build_stepper(sid, par, RexiSetup(num_poles=128))
+    host = build_stepper(sid, par, RexiSetup(num_poles=128)).instrument(TimingCollector())
+    a = dev.step(st0, 600.0)
+    b = host.step(st0, 600.0)
+    assert rel_l2(pack(a.stack()), pack(b.stack())) <= 1e-12
+    for _ in range(3):  # warm both paths (plans, solvers, staging)
+        dev.step(st0, 600.0)
+        host.step(st0, 600.0)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        dev.step(st0, 600.0)
+    t1 = time.perf_counter()
+    for _ in range(5):
+        host.step(st0, 600.0)
+    t2 = time.perf_counter()
+    print(f"{sid}: device-resident {(t1 - t0) / 5 * 1e3:.2f} ms, host-composed "
+          f"{(t2 - t1) / 5 * 1e3:.2f} ms per step")
+
+
 # ---------------------------------------------------------------- f4: IC, error, winds
 
 @pytest.mark.parametrize("trunc", [21, 42])
