@@ -975,6 +975,365 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
   }
 }
 
+// =====================================================================
+// K2p: the same chains for short columns (T <= 32 * kLPartQ - 1), one lane
+// GROUP per system instead of one thread: the warp-per-system partition of the
+// tridiagonal solve.  A group of W lanes (W = 1..32, a power of two) owns one
+// (pole, m, chain); lane j holds the q consecutive rows j*q .. j*q+q-1 in
+// registers (q even, so a row's vorticity/divergence type is the same in every
+// lane and every branch on it is warp-uniform).
+//   1. downward sweep in the lane: rows become  x_i + c_i x_{i+1} + A_i x_L = D_i
+//      (x_L = the previous lane's last unknown; the Thomas step of l_fwd plus
+//      the fill column A);
+//   2. upward sweep: rows i < q-1 become  x_i + A_i x_L + C_i x_R = D_i  with
+//      x_R = the lane's own last unknown;
+//   3. the last rows of the W lanes, with the next lane's first row substituted,
+//      form a W x W tridiagonal system in the X_j = x_{j,q-1}: parallel cyclic
+//      reduction over the group with width-W shuffles, log2 W steps;
+//   4. x_i = D_i - A_i X_{j-1} - C_i X_j, then the beta weights and phi'.
+// No pivot cache, no second pass, no scratch: every (pole, m, chain) is W
+// threads of parallel work instead of one serial thread, which is what a
+// T128 x 256-pole sum lacks (1032 warps of serial chains on 148 SMs).
+// A CTA is 256 threads: min(32 W, 256) threads per column slot, 8 / W columns
+// per CTA when W < 8; it covers one 32-pole block in 32 W / 256 passes.  The
+// beta-weighted solutions go through a shared-memory stage ([pole][i*W + j],
+// conflict-free for writers and readers) and are summed over the poles as the
+// perfect binary tree of tree_sum, so `part` holds the same aligned 32-pole
+// subtrees as rexi_l_kernel's.
+// =====================================================================
+#ifndef SWX_LPART_Q
+#define SWX_LPART_Q 8
+#endif
+#ifndef SWX_LPART_MINB
+#define SWX_LPART_MINB 2
+#endif
+constexpr int kLPartQ = SWX_LPART_Q;  // rows per lane at most (even)
+static_assert(kLPartQ % 2 == 0 && kLPartQ >= 2, "rows per lane");
+
+template <int N>
+__device__ __forceinline__ double2 tree_ld(const double2 *p, int stride) {
+  if constexpr (N == 1) {
+    return p[0];
+  } else {
+    return cadd(tree_ld<N / 2>(p, stride), tree_ld<N / 2>(p + (size_t)(N / 2) * stride, stride));
+  }
+}
+__device__ __forceinline__ double2 tree_ld_n(const double2 *p, int stride, int n) {
+  switch (n) {
+    case 32: return tree_ld<32>(p, stride);
+    case 16: return tree_ld<16>(p, stride);
+    case 8: return tree_ld<8>(p, stride);
+    case 4: return tree_ld<4>(p, stride);
+    case 2: return tree_ld<2>(p, stride);
+    default: return p[0];
+  }
+}
+// value of lane (own - s) / (own + s) inside the W-lane group, 0 outside it
+__device__ __forceinline__ double2 grp_up(double2 v, int s, int W, int j) {
+  const double x = __shfl_up_sync(0xffffffffu, v.x, s, W);
+  const double y = __shfl_up_sync(0xffffffffu, v.y, s, W);
+  return j >= s ? make_double2(x, y) : make_double2(0.0, 0.0);
+}
+__device__ __forceinline__ double2 grp_down(double2 v, int s, int W, int j) {
+  const double x = __shfl_down_sync(0xffffffffu, v.x, s, W);
+  const double y = __shfl_down_sync(0xffffffffu, v.y, s, W);
+  return j + s < W ? make_double2(x, y) : make_double2(0.0, 0.0);
+}
+// a - b*c
+__device__ __forceinline__ double2 cnfma(double2 b, double2 c, double2 a) {
+  return make_double2(fma(-b.x, c.x, fma(b.y, c.y, a.x)), fma(-b.x, c.y, fma(-b.y, c.x, a.y)));
+}
+
+// 1/z with the reciprocal of |z|^2 from the hardware approximation and two
+// Newton steps (no special cases: the pivots here are finite and far from the
+// denormal range; relative error of a few ulp)
+__device__ __forceinline__ double2 crecip_nr(double2 z) {
+  const double n = fma(z.x, z.x, z.y * z.y);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(n));
+  r = fma(r, fma(-n, r, 1.0), r);
+  r = fma(r, fma(-n, r, 1.0), r);
+  return make_double2(z.x * r, -z.y * r);
+}
+// -(a*b)
+__device__ __forceinline__ double2 cnmul(double2 a, double2 b) {
+  return make_double2(fma(a.y, b.y, -__dmul_rn(a.x, b.x)), fma(-a.x, b.y, -__dmul_rn(a.y, b.x)));
+}
+
+// shared-memory geometry of one CTA.  Per column slot, lane j of a system owns
+//   doubles  [j*SD .. ): sub[q] sup[q] rot[q] g[q/2] h[q/2]      SD = 4q + 1
+//   double2  [j*SC .. ): per rhs b1[q] bp[q/2]                   SC = (nrhs*3q/2) | 1
+// and, per pole of the pass, the same SC-strided block of outputs (x[q], phi'[q/2]
+// per rhs).  The odd strides make the per-lane accesses conflict-free with
+// compile-time offsets inside the lane's block.
+#ifndef SWX_LPART_THREADS
+#define SWX_LPART_THREADS 256
+#endif
+constexpr int kLPartT = SWX_LPART_THREADS;  // threads per CTA
+__host__ __device__ inline int lpart_sd(int q) { return 4 * q + 1; }
+__host__ __device__ inline int lpart_sc(int nrhs, int q) { return (nrhs * 3 * q / 2) | 1; }
+
+template <int NRHS, int QV>
+__device__ __forceinline__ void lpart_body(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
+    const double2 *__restrict__ beta, int beta_stride, int pole0, int P, int trunc, int ncoef,
+    double dtpb, const double *__restrict__ lconst, const double *__restrict__ chain,
+    const int4 it, const int pb, double2 *__restrict__ part, double2 *lp_raw) {
+  constexpr int SD = 4 * QV + 1, SC = (NRHS * 3 * QV / 2) | 1, HQ = QV / 2, E = 3 * QV / 2;
+  const int W = it.z;
+  const int tps = min(32 * W, kLPartT);    // threads per column slot
+  const int nslots = kLPartT / tps;
+  const int ppp = tps / W;                 // poles per pass
+  const int passes = 32 / ppp;
+  const int tid = threadIdx.x;
+  const int slot = tid / tps, ts = tid - slot * tps;
+  const int g = ts / W, j = ts - g * W;
+  const bool has_col = slot < it.y;
+  const int col = it.x + (has_col ? slot : 0);
+  const int m = col >> 1, c = col & 1;
+  const int nl = trunc + 1 - m, off = col_offset(trunc, m);
+  const int nout = W * SC;  // outputs of one pole (with the pad entries)
+  // smem: [slot] doubles | [slot] complex row data | [slot][pole] stage | [slot][pass] partials
+  double *rd_all = reinterpret_cast<double *>(lp_raw);
+  const int dcount = (nslots * W * SD + 1) & ~1;
+  double2 *cd_all = reinterpret_cast<double2 *>(rd_all + dcount);
+  double2 *stage_all = cd_all + (size_t)nslots * W * SC;
+  double *rd = rd_all + (size_t)slot * W * SD;
+  double2 *cd = cd_all + (size_t)slot * W * SC;
+  double2 *stage = stage_all + (size_t)slot * ppp * nout;
+  double2 *pacc = stage_all + (size_t)nslots * ppp * nout + (size_t)slot * passes * nout;
+
+  // ---- stage the column's rows into the owning lanes' blocks
+  for (int idx = ts; idx < W * QV; idx += tps) {
+    const int jj = idx / QV, i = idx - jj * QV;
+    const int k = idx;  // row jj*q + i
+    const bool isz = ((i + c) & 1) == 0;
+    double sub = 0.0, sup = 0.0, rot = 0.0, gk = 0.0, hk = 0.0;
+    double2 b1[NRHS], bp[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) b1[r] = bp[r] = make_double2(0.0, 0.0);
+    if (k < nl) {
+      const int s = off + k, l = m + k;
+      const double sg = isz ? -1.0 : 1.0;
+      sub = sg * chain[s];
+      sup = sg * chain[ncoef + s];
+      rot = chain[2 * ncoef + s];
+      if (!isz) {
+        gk = lconst[(trunc + 1) + l];
+        hk = lconst[2 * (trunc + 1) + l];
+      }
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        const double2 *b = rhs + (size_t)r * 3 * ncoef;
+        b1[r] = isz ? b[ncoef + s] : b[2 * ncoef + s];
+        if (!isz) bp[r] = b[s];
+      }
+    }
+    double *d = rd + jj * SD;
+    d[i] = sub;
+    d[QV + i] = sup;
+    d[2 * QV + i] = rot;
+    double2 *cc = cd + jj * SC;
+    if (!isz) {
+      d[3 * QV + (i >> 1)] = gk;
+      d[3 * QV + HQ + (i >> 1)] = hk;
+    }
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      cc[r * E + i] = b1[r];
+      if (!isz) cc[r * E + QV + (i >> 1)] = bp[r];
+    }
+  }
+  __syncthreads();
+  const double *d = rd + j * SD;
+  const double2 *cc = cd + j * SC;
+
+  for (int pass = 0; pass < passes; ++pass) {
+    const int pl = pb * 32 + pass * ppp + g;  // pole within [0, P)
+    double2 a = make_double2(1.0, 0.0);
+    double2 bet[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) bet[r] = make_double2(0.0, 0.0);
+    if (pl < P) {
+      a = alpha[pole0 + pl];
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) bet[r] = beta[r * beta_stride + pole0 + pl];
+    }
+    const double2 ia = crecip_nr(a);
+    double2 bia[NRHS];  // beta / alpha: the weight of phi' (solvers.py:139-141)
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) bia[r] = cmul(bet[r], ia);
+    // ---- 1. downward sweep: x_i + C_i x_{i+1} + A_i x_L = D_i
+    double2 A[QV], C[QV], D[NRHS][QV];
+#pragma unroll
+    for (int i = 0; i < QV; ++i) {
+      const bool isz = ((i + c) & 1) == 0;
+      const double sub = d[i], sup = d[QV + i];
+      double2 den = make_double2(a.x, a.y + d[2 * QV + i]);
+      double2 t = make_double2(0.0, 0.0);  // h / alpha
+      if (!isz) {
+        const double gk = d[3 * QV + (i >> 1)], hk = d[3 * QV + HQ + (i >> 1)];
+        den.x = fma(gk, ia.x, den.x);
+        den.y = fma(gk, ia.y, den.y);
+        t = make_double2(hk * ia.x, hk * ia.y);
+      }
+      if (i > 0) {
+        den.x = fma(-sub, C[i - 1].x, den.x);
+        den.y = fma(-sub, C[i - 1].y, den.y);
+      }
+      const double2 inv = crecip_nr(den);
+      C[i] = cscale(sup, inv);
+      if (i == 0) {
+        A[0] = cscale(sub, inv);
+      } else {
+        A[i] = cmul(cscale(-sub, A[i - 1]), inv);
+      }
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        double2 qv = cc[r * E + i];
+        if (!isz) qv = cnfma(t, cc[r * E + QV + (i >> 1)], qv);
+        if (i > 0) {
+          qv.x = fma(-sub, D[r][i - 1].x, qv.x);
+          qv.y = fma(-sub, D[r][i - 1].y, qv.y);
+        }
+        D[r][i] = cmul(qv, inv);
+      }
+    }
+    // ---- 2. upward sweep, running: the first row as x_0 + fA x_L + fC x_R = fD
+    // (x_R = the lane's last unknown); the stored rows keep the downward form
+    double2 fA = A[QV - 2], fC = C[QV - 2], fD[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) fD[r] = D[r][QV - 2];
+#pragma unroll
+    for (int i = QV - 3; i >= 0; --i) {
+      fA = cnfma(C[i], fA, A[i]);
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) fD[r] = cnfma(C[i], fD[r], D[r][i]);
+      fC = cnmul(C[i], fC);
+    }
+    // ---- 3. reduced system over the group: ra X_{j-1} + rb X_j + rc X_{j+1} = rd.
+    // Neighbour values from outside the group only ever multiply exact zeros
+    // (ra = 0 in lanes j < s, rc = 0 in lanes j >= W - s), so the clamped
+    // shuffles need no masking.
+    double2 ra, rb, rc, rv[NRHS];
+    {
+      const double2 cL = C[QV - 1];
+      const double2 nA = make_double2(__shfl_down_sync(0xffffffffu, fA.x, 1, W),
+                                      __shfl_down_sync(0xffffffffu, fA.y, 1, W));
+      const double2 nC = make_double2(__shfl_down_sync(0xffffffffu, fC.x, 1, W),
+                                      __shfl_down_sync(0xffffffffu, fC.y, 1, W));
+      ra = A[QV - 1];
+      rb = cnfma(cL, nA, make_double2(1.0, 0.0));
+      rc = cnmul(cL, nC);
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        const double2 nD = make_double2(__shfl_down_sync(0xffffffffu, fD[r].x, 1, W),
+                                        __shfl_down_sync(0xffffffffu, fD[r].y, 1, W));
+        rv[r] = cnfma(cL, nD, D[r][QV - 1]);
+      }
+    }
+    for (int s = 1; s < W; s <<= 1) {
+      const double2 inv = crecip_nr(rb);
+      const double2 an = cmul(ra, inv), cn = cmul(rc, inv);
+      const double2 an_m = make_double2(__shfl_up_sync(0xffffffffu, an.x, s, W),
+                                        __shfl_up_sync(0xffffffffu, an.y, s, W));
+      const double2 cn_m = make_double2(__shfl_up_sync(0xffffffffu, cn.x, s, W),
+                                        __shfl_up_sync(0xffffffffu, cn.y, s, W));
+      const double2 an_p = make_double2(__shfl_down_sync(0xffffffffu, an.x, s, W),
+                                        __shfl_down_sync(0xffffffffu, an.y, s, W));
+      const double2 cn_p = make_double2(__shfl_down_sync(0xffffffffu, cn.x, s, W),
+                                        __shfl_down_sync(0xffffffffu, cn.y, s, W));
+      ra = cnmul(an, an_m);
+      rc = cnmul(cn, cn_p);
+      rb = cnfma(cn, an_p, cnfma(an, cn_m, make_double2(1.0, 0.0)));
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        const double2 dn = cmul(rv[r], inv);
+        const double2 dn_m = make_double2(__shfl_up_sync(0xffffffffu, dn.x, s, W),
+                                          __shfl_up_sync(0xffffffffu, dn.y, s, W));
+        const double2 dn_p = make_double2(__shfl_down_sync(0xffffffffu, dn.x, s, W),
+                                          __shfl_down_sync(0xffffffffu, dn.y, s, W));
+        rv[r] = cnfma(cn, dn_p, cnfma(an, dn_m, dn));
+      }
+    }
+    const double2 invb = crecip_nr(rb);
+    // ---- 4. back substitution x_i = D_i - C_i x_{i+1} - A_i X_{j-1}, beta
+    // weights, phi' (solvers.py:134-141) -> the pole's stage block
+    double2 *st = stage + (size_t)g * nout + j * SC;
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 X = cmul(rv[r], invb);
+      const double2 XL = make_double2(__shfl_up_sync(0xffffffffu, X.x, 1, W),
+                                      __shfl_up_sync(0xffffffffu, X.y, 1, W));
+      double2 x = X;
+#pragma unroll
+      for (int i = QV - 1; i >= 0; --i) {
+        const bool isz = ((i + c) & 1) == 0;
+        if (i < QV - 1) x = cnfma(C[i], x, cnfma(A[i], XL, D[r][i]));
+        st[r * E + i] = cmul(bet[r], x);
+        if (!isz) {
+          const double2 b = cc[r * E + QV + (i >> 1)];
+          st[r * E + QV + (i >> 1)] =
+              cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), bia[r]);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- pole tree of the pass; single pass: straight to `part`
+    auto store = [&](int o, double2 v) {
+      const int jj = o / SC, e = o - jj * SC;
+      if (e >= NRHS * E) return;  // pad entry
+      const int r = e / E, e2 = e - r * E;
+      int i, field;
+      if (e2 < QV) {
+        i = e2;
+        field = ((i + c) & 1) == 0 ? 1 : 2;
+      } else {
+        i = 2 * (e2 - QV) + (c == 0 ? 1 : 0);
+        field = 0;
+      }
+      const int k = jj * QV + i;
+      if (k < nl) part[((size_t)(pb * NRHS + r) * 3 + field) * ncoef + off + k] = v;
+    };
+    for (int o = ts; o < nout; o += tps) {
+      const double2 v = tree_ld_n(stage + o, nout, ppp);
+      if (passes > 1) {
+        pacc[(size_t)pass * nout + o] = v;
+      } else if (has_col) {
+        store(o, v);
+      }
+    }
+    __syncthreads();
+    if (passes > 1 && pass == passes - 1 && has_col)
+      for (int o = ts; o < nout; o += tps) store(o, tree_ld_n(pacc + o, nout, passes));
+  }
+}
+
+template <int NRHS>
+__global__ void __launch_bounds__(kLPartT, SWX_LPART_MINB) rexi_l_part_kernel(
+    const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
+    const double2 *__restrict__ beta, int beta_stride, int pole0, int P, int trunc, int ncoef,
+    double dt, double phibar, const double *__restrict__ lconst,
+    const double *__restrict__ chain, const int4 *__restrict__ items,
+    double2 *__restrict__ part) {
+  extern __shared__ double2 lp_raw[];
+  const int4 it = items[blockIdx.x];  // first column (2m + chain), columns, W, q
+  const double dtpb = dt * phibar;
+#define SWX_LPART_CASE(QQ)                                                                   \
+  case QQ:                                                                                   \
+    if constexpr (QQ <= kLPartQ)                                                             \
+      lpart_body<NRHS, QQ>(rhs, alpha, beta, beta_stride, pole0, P, trunc, ncoef, dtpb,      \
+                           lconst, chain, it, blockIdx.y, part, lp_raw);                     \
+    break;
+  switch (it.w) {
+    SWX_LPART_CASE(2)
+    SWX_LPART_CASE(4)
+    SWX_LPART_CASE(6)
+    SWX_LPART_CASE(8)
+    default: break;
+  }
+#undef SWX_LPART_CASE
+}
 
 
 // warm-up guard for the l group: forward sweep only, min |pivot|^2 per
@@ -1214,12 +1573,15 @@ extern "C" int swx_solver_destroy(swx_solver s) {
   cudaFree(s->d_chain);
   cudaFree(s->d_alpha);
   cudaFree(s->d_linv);
+  cudaFree(s->d_lpart);
   for (auto &kv : s->lg_sched) cudaFree(kv.second.first);
   delete[] s->h_norm;
   delete[] s->h_alpha;
   delete s;
   return SWX_OK;
 }
+
+static bool l_use_part(swx_solver s);
 
 extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
                                int n_poles, int *err_pole, int *err_index,
@@ -1304,7 +1666,7 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
     s->d_linv = nullptr;
     s->linv_bytes = 0;
     const char *ev = getenv("SWX_L_CACHE");
-    if (!ev || atoi(ev) != 0) {
+    if ((!ev || atoi(ev) != 0) && !l_use_part(s)) {  // the partition kernel needs no cache
       const int p_pad = ((n_poles + 31) / 32 + 1) * 32;  // + one block for idle lanes
       const size_t bytes = (size_t)p_pad * s->ncoef * 2 * sizeof(double2);
       size_t fr = 0, tot = 0;
@@ -1543,10 +1905,109 @@ static int launch_lg(swx_solver s, const double2 *rhs, const double2 *betas,
   return run_lg<NRHS>(s, rhs, fac_ws, P, realify, out, st, ep);
 }
 
+// ---- partition kernel (short columns): geometry, schedule, launch
+// the partition kernel serves every column when all of them fit 32 lanes x
+// kLPartQ rows (SWX_L_PART=0: the thread-per-chain kernels for every T)
+static bool l_use_part(swx_solver s) {
+  static int on = -1;
+  if (on < 0) {
+    const char *ev = getenv("SWX_L_PART");
+    on = (!ev || atoi(ev) != 0) ? 1 : 0;
+  }
+  return on && s->trunc + 1 <= 32 * kLPartQ;
+}
+
+static size_t lpart_smem_bytes(int nrhs, int W, int q) {
+  const int tps = std::min(32 * W, kLPartT), nslots = kLPartT / tps, ppp = tps / W;
+  const int passes = 32 / ppp, nout = W * lpart_sc(nrhs, q);
+  const int dcount = (nslots * W * lpart_sd(q) + 1) & ~1;
+  return (size_t)dcount * sizeof(double) + (size_t)nslots * nout * sizeof(double2) +
+         (size_t)nslots * ppp * nout * sizeof(double2) +
+         (passes > 1 ? (size_t)nslots * passes * nout * sizeof(double2) : 0);
+}
+
+// lanes per system and rows per lane of a column of nl rows: the cheapest
+// (W, q) with q even, W q >= nl under an instruction-count model (rows: the two
+// sweeps, the back substitution and the epilogue; PCR: log2 W steps per lane)
+static void lpart_geometry(int nl, int &W, int &q) {
+  double best = 1e300;
+  W = 32;
+  q = kLPartQ;
+  for (int w = 1, lg = 0; w <= 32; w <<= 1, ++lg) {
+    int qq = (nl + w - 1) / w;
+    qq += qq & 1;
+    qq = std::max(qq, 2);
+    if (qq > kLPartQ) continue;
+    const double cost = (double)w * (qq * 68.0 + lg * 75.0 + 30.0);
+    if (cost < best) {
+      best = cost;
+      W = w;
+      q = qq;
+    }
+  }
+}
+
+static int lpart_schedule(swx_solver s) {
+  if (s->d_lpart) return SWX_OK;
+  std::vector<int4> items;
+  const int ncols = 2 * (s->trunc + 1);
+  int max_rows = 0;
+  for (int col = 0; col < ncols;) {
+    int W, q;
+    lpart_geometry(s->trunc + 1 - (col >> 1), W, q);
+    const int per_cta = std::max(1, kLPartT / (32 * W));
+    int n = 1;
+    while (n < per_cta && col + n < ncols) {  // same lane count in every slot of the CTA
+      int W2, q2;
+      lpart_geometry(s->trunc + 1 - ((col + n) >> 1), W2, q2);
+      if (W2 != W) break;
+      ++n;
+    }
+    items.push_back(make_int4(col, n, W, q));  // q of the first (longest) column
+    max_rows = std::max(max_rows, W * q);
+    col += n;
+  }
+  SWX_CUDA_TRY(cudaMalloc(&s->d_lpart, sizeof(int4) * items.size()));
+  SWX_CUDA_TRY(cudaMemcpy(s->d_lpart, items.data(), sizeof(int4) * items.size(),
+                          cudaMemcpyHostToDevice));
+  s->lpart_ctas = (int)items.size();
+  s->lpart_max_rows = max_rows;
+  s->h_lpart.assign(items.begin(), items.end());
+  return SWX_OK;
+}
+
+template <int NRHS>
+static int launch_l_part(swx_solver s, const double2 *rhs, const double2 *betas, int pole0,
+                         int P, int realify, double2 *out, double2 *part, cudaStream_t st,
+                         Axpy ep) {
+  int rc = lpart_schedule(s);
+  if (rc) return rc;
+  const int nb = (P + 31) / 32;
+  size_t smem = 0;
+  for (const int4 &it : s->h_lpart) smem = std::max(smem, lpart_smem_bytes(NRHS, it.z, it.w));
+  auto k = rexi_l_part_kernel<NRHS>;
+  if (smem > 48 * 1024)
+    SWX_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(s->lpart_ctas, nb), kLPartT, smem, st>>>(rhs, s->d_alpha, betas, s->n_poles, pole0, P,
+                                                s->trunc, s->ncoef, s->dt, s->phibar,
+                                                s->d_lconst, s->d_chain, s->d_lpart, part);
+  SWX_LAUNCH_CHECK();
+  const size_t stride = (size_t)NRHS * 3 * s->ncoef;
+  tree_combine_kernel<<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(part, stride, nb, s->ncoef,
+                                                                        s->trunc, realify, ep, out);
+  SWX_LAUNCH_CHECK();
+  return SWX_OK;
+}
+
 template <int NRHS>
 static int launch_l(swx_solver s, const double2 *rhs, const double2 *betas,
                     int pole0, int P, int realify, double2 *out, char *ws,
                     cudaStream_t st, Axpy ep = Axpy{nullptr, 0.0}) {
+  if (l_use_part(s)) {
+    const size_t sb = l_scratch_bytes(s, NRHS, P);
+    return launch_l_part<NRHS>(s, rhs, betas, pole0, P, realify, out,
+                               (double2 *)(ws + ((sb + 255) / 256) * 256), st, ep);
+  }
   const int nb = (P + 31) / 32;
   const int n_items = (s->trunc + 1) * nb;
   const int warps = l_grid_warps(s, n_items);

@@ -8,6 +8,7 @@
 #include <tuple>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "../../include/swx.h"
 
@@ -97,6 +98,12 @@ struct swx_solver_s {
   double2 *d_linv = nullptr;
   size_t linv_bytes = 0;
   int l_blocks_per_sm = 0;
+  // l group, short columns: CTA items (first column 2m+chain, columns, W, q) of
+  // the partition kernel (rexi_l_part_kernel), built at the first launch
+  int4 *d_lpart = nullptr;
+  int lpart_ctas = 0;
+  int lpart_max_rows = 0;  // largest W*q of an item
+  std::vector<int4> h_lpart;
 };
 
 // ---- per-CTA phase tracer (measurement helper, swx_trace_*) ---------------
