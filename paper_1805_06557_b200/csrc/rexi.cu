@@ -509,6 +509,35 @@ constexpr int kFS = SWX_LFLUSH;          // segments per pole reduction (1 or 2)
 constexpr int kFRows = kFlush * kFS;     // reduction rows per flush
 static_assert((kFS == 1 || kFS == 2) && kFRows <= 32, "flush grouping");
 
+// 1/z with the reciprocal of |z|^2 from the hardware approximation and two
+// Newton steps (no special cases: the pivots here are finite and far from the
+// denormal range; relative error of a few ulp)
+__device__ __forceinline__ double2 crecip_nr(double2 z) {
+  const double n = fma(z.x, z.x, z.y * z.y);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(n));
+  r = fma(r, fma(-n, r, 1.0), r);
+  r = fma(r, fma(-n, r, 1.0), r);
+  return make_double2(z.x * r, -z.y * r);
+}
+// -(a*b)
+__device__ __forceinline__ double2 cnmul(double2 a, double2 b) {
+  return make_double2(fma(a.y, b.y, -__dmul_rn(a.x, b.x)), fma(-a.x, b.y, -__dmul_rn(a.y, b.x)));
+}
+
+#ifndef SWX_L_FASTRCP
+#define SWX_L_FASTRCP 1  // cfg4 without the pivot cache: 16.9 -> 14.5 ms
+#endif
+// pivot reciprocal of the thread-per-chain kernels (and of the cache and the
+// guard, which must produce the same bits)
+__device__ __forceinline__ double2 lrecip(double2 z) {
+#if SWX_L_FASTRCP
+  return crecip_nr(z);
+#else
+  return crecip(z);
+#endif
+}
+
 template <int NRHS>
 struct LPos {
   double L, U, rot, g, h;  // couplings, rotation, dt^2 phibar kappa, dt kappa
@@ -557,7 +586,7 @@ __device__ __forceinline__ void l_fwd(const LPos<NRHS> &e, bool isz, double2 a, 
     diag.y = fma(e.g, ia.y, diag.y);
   }
   const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
-  const double2 inv = crecip(den);
+  const double2 inv = lrecip(den);
   cp = cscale(sup, inv);
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) {
@@ -574,7 +603,7 @@ __device__ __forceinline__ void l_fwd(const LPos<NRHS> &e, bool isz, double2 a, 
 }
 
 // the same step from the cached pivot inverse inv = 1/den (bitwise equal:
-// l_fwd computes den, inv = crecip(den) and then exactly these operations);
+// l_fwd computes den, inv = lrecip(den) and then exactly these operations);
 // the chain's c' is not needed for y
 template <int NRHS>
 __device__ __forceinline__ void l_fwd_c(const LPos<NRHS> &e, bool isz, double2 ia, double2 inv,
@@ -674,7 +703,7 @@ __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_p
   const int pb = (int)((w >> 1) / (trunc + 1));
   const int gp = pb * 32 + lane;
   const double2 a = gp < P ? alpha[gp] : make_double2(1.0, 0.0);
-  const double2 ia = crecip(a);
+  const double2 ia = lrecip(a);
   const double *gl = lconst + (trunc + 1);
   const int off = col_offset(trunc, m);
   const int nl = trunc + 1 - m;
@@ -690,7 +719,7 @@ __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_p
       diag.y = fma(gl[m + k], ia.y, diag.y);
     }
     const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
-    const double2 inv = crecip(den);
+    const double2 inv = lrecip(den);
     cp = cscale(sup, inv);
     linv[linv_at(gp, ncoef, s, c)] = inv;
   }
@@ -699,8 +728,11 @@ __global__ void l_cache_kernel(const double2 *__restrict__ alpha, int P, int P_p
 #ifndef SWX_LC_MINB
 #define SWX_LC_MINB 2  // resident CTAs per SM the cached kernel's register budget targets
 #endif
+#ifndef SWX_LU_MINB
+#define SWX_LU_MINB 1  // the same for the recomputing kernel
+#endif
 template <int NRHS, bool CACHED = false>
-__global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l_kernel(
+__global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : SWX_LU_MINB) rexi_l_kernel(
     const double2 *__restrict__ rhs, const double2 *__restrict__ alpha,
     const double2 *__restrict__ beta, int beta_stride, int pole0, int P,
     int n_blocks, int trunc, int ncoef, double dt, double phibar,
@@ -752,7 +784,7 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : 1) rexi_l
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) bet[r] = beta[r * beta_stride + pole0 + pl];
     }
-    const double2 ia = crecip(a);
+    const double2 ia = lrecip(a);
     const int nl = trunc + 1 - m;
     const int off = col_offset(trunc, m);
     const int nseg = (nl + kLSeg - 1) / kLSeg;
@@ -1042,22 +1074,6 @@ __device__ __forceinline__ double2 grp_down(double2 v, int s, int W, int j) {
 // a - b*c
 __device__ __forceinline__ double2 cnfma(double2 b, double2 c, double2 a) {
   return make_double2(fma(-b.x, c.x, fma(b.y, c.y, a.x)), fma(-b.x, c.y, fma(-b.y, c.x, a.y)));
-}
-
-// 1/z with the reciprocal of |z|^2 from the hardware approximation and two
-// Newton steps (no special cases: the pivots here are finite and far from the
-// denormal range; relative error of a few ulp)
-__device__ __forceinline__ double2 crecip_nr(double2 z) {
-  const double n = fma(z.x, z.x, z.y * z.y);
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(n));
-  r = fma(r, fma(-n, r, 1.0), r);
-  r = fma(r, fma(-n, r, 1.0), r);
-  return make_double2(z.x * r, -z.y * r);
-}
-// -(a*b)
-__device__ __forceinline__ double2 cnmul(double2 a, double2 b) {
-  return make_double2(fma(a.y, b.y, -__dmul_rn(a.x, b.x)), fma(-a.x, b.y, -__dmul_rn(a.y, b.x)));
 }
 
 // shared-memory geometry of one CTA.  Per column slot, lane j of a system owns
@@ -1351,7 +1367,7 @@ __global__ void l_guard_kernel(const double2 *__restrict__ alpha, int P,
   const int rem = t - n * (trunc + 1) * 2;
   const int m = rem >> 1, c = rem & 1;
   const double2 a = alpha[n];
-  const double2 ia = crecip(a);
+  const double2 ia = lrecip(a);
   const double *gl = lconst + (trunc + 1);
   const int off = col_offset(trunc, m);
   double2 cp = make_double2(0.0, 0.0);
@@ -1369,7 +1385,7 @@ __global__ void l_guard_kernel(const double2 *__restrict__ alpha, int P,
     const double2 den = make_double2(fma(-sub, cp.x, diag.x), fma(-sub, cp.y, diag.y));
     const double d2 = fma(den.x, den.x, den.y * den.y);
     dmin2 = fmin(dmin2, d2);
-    cp = cscale(sup, crecip(den));
+    cp = cscale(sup, lrecip(den));
   }
   const double nrm = norm_m[m] + sqrt(fma(a.x, a.x, a.y * a.y));
   if (!(dmin2 > 0.0) || nrm * nrm > 1e26 * dmin2) {

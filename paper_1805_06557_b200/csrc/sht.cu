@@ -1021,6 +1021,10 @@ __global__ void __launch_bounds__(SqCfg<R, R>::NT, 2) grid_sq1_kernel(ShtView p,
   double2 *F = gsm;  // [5][FS]
   const int i = blockIdx.x + i0;  // latitude pair (padded to nt16)
   if (i >= p.nh) {
+    // padding pair: no global write before the wait (the analysis two kernels
+    // back in the PDL chain may still be reading these rows)
+    pdl_trigger();
+    pdl_wait();
     grid_zero_rows(p, i, A);
     return;
   }
