@@ -892,3 +892,44 @@ def test_instrumented_etdrk_step_fills_breakdown(golden_medium):
     for name in ("overall", "nonlinearities", "rexi_total", "broadcast", "term_solves", "reduce"):
         assert getattr(col, name) > 0.0, name
     assert col.nonlinearities < col.overall
+
+
+# ------------------------------------------------ partition form of the l chains
+
+@pytest.mark.parametrize("trunc,n_poles", [(1, 3), (2, 8), (7, 5), (8, 33), (16, 40), (33, 31),
+                                           (64, 64), (65, 17), (129, 40), (200, 12), (255, 40)])
+def test_l_partition_kernel_edge_truncations_vs_oracle(trunc, n_poles):
+    """The warp-per-system partition solve (rexi_l_part_kernel, every T <= 255):
+    every lanes-per-system class (columns of 1..256 rows: W = 1..32, q = 2..8),
+    padded last lanes, pole counts that are not multiples of the 32-pole block
+    or of the poles per pass, against the oracle's band LU (solvers.py:196-212)."""
+    st = ost.seeded_linear_state(trunc, 5)
+    a, b = ost.contour_coeffs(0, 10.0, 30.0, n_poles)
+    model = orx.Model(trunc, 1e4 * G)
+    ref = olay.pack(orx.rexi_sum("l", model, 1800.0, a, b, st))
+    sl = ShiftedLinearSolver(L, 1800.0, params(trunc))
+    out = sl.rexi_sum_dev(a, to_device(np.asarray(b).reshape(1, -1)), to_device(pack(st))[None])
+    assert rel_linf(out[0].cpu().numpy(), ref) <= LIN_BAR
+
+
+def test_l_partition_kernel_two_rhs_and_pole_subranges_t255():
+    """T255 (the largest truncation the partition kernel serves: 32 lanes x 8
+    rows): two fused right-hand sides against the oracle, and unaligned pole
+    sub-ranges summing to the full result."""
+    trunc, n = 255, 48
+    par = params(trunc)
+    sl = ShiftedLinearSolver(L, 900.0, par)
+    c0, c1 = coeffs(n, 0), coeffs(n, 1)
+    u, v = ost.seeded_linear_state(trunc, 1), ost.seeded_linear_state(trunc, 2)
+    rhs = to_device(np.stack([pack(u), pack(v)]))
+    bet = to_device(np.stack([c0.betas, c1.betas]))
+    out = sl.rexi_sum_dev(c0.alphas, bet, rhs).cpu().numpy()
+    model = orx.Model(trunc, 1e4 * G)
+    for r, (st, c) in enumerate(((u, c0), (v, c1))):
+        ref = olay.pack(orx.rexi_sum("l", model, 900.0, c.alphas, c.betas, st))
+        assert rel_linf(out[r], ref) <= LIN_BAR
+    parts = [sl.rexi_sum_dev(c0.alphas, bet, rhs, pole_range=pr, realify=False).cpu().numpy()
+             for pr in ((0, 7), (7, 39), (39, 48))]
+    tot = parts[0] + parts[1] + parts[2]
+    unreal = sl.rexi_sum_dev(c0.alphas, bet, rhs, realify=False).cpu().numpy()
+    assert rel_linf(tot[0], unreal[0]) <= 1e-12 and rel_linf(tot[1], unreal[1]) <= 1e-12
