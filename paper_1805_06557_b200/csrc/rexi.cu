@@ -1117,7 +1117,7 @@ __device__ __forceinline__ void lpart_body(
   double *rd = rd_all + (size_t)slot * W * SD;
   double2 *cd = cd_all + (size_t)slot * W * SC;
   double2 *stage = stage_all + (size_t)slot * ppp * nout;
-  double2 *pacc = stage_all + (size_t)nslots * ppp * nout + (size_t)slot * passes * nout;
+  double2 *pacc = stage_all + (size_t)nslots * ppp * nout + (size_t)slot * (passes / 2) * nout;
 
   // ---- stage the column's rows into the owning lanes' blocks
   for (int idx = ts; idx < W * QV; idx += tps) {
@@ -1165,7 +1165,12 @@ __device__ __forceinline__ void lpart_body(
   const double2 *cc = cd + j * SC;
 
   for (int pass = 0; pass < passes; ++pass) {
-    const int pl = pb * 32 + pass * ppp + g;  // pole within [0, P)
+    // two consecutive passes of a thread take adjacent poles (a leaf pair of the
+    // pole tree): the second adds into the first's stage entries, thread-private,
+    // so only every second pass ends in the CTA-wide pole tree
+    const bool pairs = passes > 1;
+    const int rnd = pairs ? pass >> 1 : pass, sub = pairs ? pass & 1 : 0;
+    const int pl = pb * 32 + (pairs ? rnd * 2 * ppp + 2 * g + sub : g);  // pole within [0, P)
     double2 a = make_double2(1.0, 0.0);
     double2 bet[NRHS];
 #pragma unroll
@@ -1286,14 +1291,18 @@ __device__ __forceinline__ void lpart_body(
       for (int i = QV - 1; i >= 0; --i) {
         const bool isz = ((i + c) & 1) == 0;
         if (i < QV - 1) x = cnfma(C[i], x, cnfma(A[i], XL, D[r][i]));
-        st[r * E + i] = cmul(bet[r], x);
+        double2 v = cmul(bet[r], x);
+        if (sub) v = cadd(st[r * E + i], v);
+        st[r * E + i] = v;
         if (!isz) {
           const double2 b = cc[r * E + QV + (i >> 1)];
-          st[r * E + QV + (i >> 1)] =
-              cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), bia[r]);
+          v = cmul(make_double2(fma(dtpb, x.x, b.x), fma(dtpb, x.y, b.y)), bia[r]);
+          if (sub) v = cadd(st[r * E + QV + (i >> 1)], v);
+          st[r * E + QV + (i >> 1)] = v;
         }
       }
     }
+    if (pairs && !sub) continue;
     __syncthreads();
     // ---- pole tree of the pass; single pass: straight to `part`
     auto store = [&](int o, double2 v) {
@@ -1313,15 +1322,16 @@ __device__ __forceinline__ void lpart_body(
     };
     for (int o = ts; o < nout; o += tps) {
       const double2 v = tree_ld_n(stage + o, nout, ppp);
-      if (passes > 1) {
-        pacc[(size_t)pass * nout + o] = v;
+      if (passes > 2) {
+        pacc[(size_t)rnd * nout + o] = v;
       } else if (has_col) {
         store(o, v);
       }
     }
+    if (pass == passes - 1 && passes <= 2) break;
     __syncthreads();
-    if (passes > 1 && pass == passes - 1 && has_col)
-      for (int o = ts; o < nout; o += tps) store(o, tree_ld_n(pacc + o, nout, passes));
+    if (passes > 2 && pass == passes - 1 && has_col)
+      for (int o = ts; o < nout; o += tps) store(o, tree_ld_n(pacc + o, nout, passes / 2));
   }
 }
 
@@ -1939,7 +1949,7 @@ static size_t lpart_smem_bytes(int nrhs, int W, int q) {
   const int dcount = (nslots * W * lpart_sd(q) + 1) & ~1;
   return (size_t)dcount * sizeof(double) + (size_t)nslots * nout * sizeof(double2) +
          (size_t)nslots * ppp * nout * sizeof(double2) +
-         (passes > 1 ? (size_t)nslots * passes * nout * sizeof(double2) : 0);
+         (passes > 2 ? (size_t)nslots * (passes / 2) * nout * sizeof(double2) : 0);
 }
 
 // lanes per system and rows per lane of a column of nl rows: the cheapest
