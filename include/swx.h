@@ -313,7 +313,8 @@ int swx_sht_tendency_shard_peer(swx_sht p, int stage, int atoms, const swx_shard
 int swx_solver_set_columns(swx_solver s, int m_begin, int m_end);
 /* Bytes of the Coriolis group's warm-time pivot cache (1/den per pole, m,
  * chain position and chain: the analogue of the reference's per-(m, alpha)
- * LU cache, solvers.py:168-194); 0 when not built (lg group, SWX_L_CACHE=0,
+ * LU cache, solvers.py:168-194); 0 when not built (lg group, truncations
+ * up to T255 - served by the cache-free partition kernel -, SWX_L_CACHE=0,
  * or more than half the free device memory).                               */
 size_t swx_solver_cache_bytes(swx_solver s);
 

@@ -41,6 +41,37 @@ static int next_pow2(int x) {
   return p;
 }
 
+// mbarrier / bulk-copy helpers (factor-table staging of the lg sums, pivot ring of
+// the cached chain kernel)
+__device__ __forceinline__ unsigned lc_smem(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void lc_bar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(lc_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void lc_bar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LC_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LC_WAIT_%=;\n}\n" ::"r"(lc_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void lc_expect(uint64_t *bar, unsigned bytes) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(lc_smem(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void lc_copy(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          lc_smem(dst)),
+      "l"(src), "r"(bytes), "r"(lc_smem(bar))
+      : "memory");
+}
+
 // =====================================================================
 // K1: gravity-group pole sum.  One CTA per (degree l, block of m); the
 // per-(pole, l) factors (beta folded in) are hoisted into shared memory:
@@ -362,10 +393,16 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
   // launch (the producer bumps it before it lets dependents launch); read it
   // before letting the next kernel launch, so a later analysis cannot bump it
   __shared__ int s_gen;
-  if (ready) {
-    if (threadIdx.x == 0) s_gen = ld_acquire(ready + trunc + 1);
-    __syncthreads();
+  __shared__ uint64_t fac_bar;  // completion of the item's factor-table bulk copy
+  // the first item's schedule entry (plan data): its load flies during the set-up
+  int4 w = sched[min((int)blockIdx.x, n_items - 1)];
+  if (threadIdx.x == 0) {
+    lc_bar_init(&fac_bar);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (ready) s_gen = ld_acquire(ready + trunc + 1);
   }
+  __syncthreads();
+  unsigned fac_phase = 0;
   pdl_trigger();
   trace_mark(0);
   // prepared factor tables do not depend on the preceding kernel: stage them
@@ -373,14 +410,19 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
   if (!fac_ready) pdl_wait();
   // persistent CTAs over (l, mode block) items, largest first
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-  if (it != blockIdx.x) __syncthreads();  // previous item's factor reads done
-  const int4 w = sched[it];
-  const int l = w.x, m0 = w.y, m1 = w.z;
-  {
-    const double4 *src = reinterpret_cast<const double4 *>(fac_g + (size_t)l * NRHS * 4 * NP);
-    double4 *dst = reinterpret_cast<double4 *>(fac);
-    for (int i = threadIdx.x; i < NRHS * 2 * NP; i += blockDim.x) dst[i] = src[i];
+  if (it != blockIdx.x) {
+    __syncthreads();  // previous item's factor reads done
+    w = sched[it];
   }
+  const int l = w.x, m0 = w.y, m1 = w.z;
+  // the degree's factor table (contiguous) by one bulk copy: it lands while the
+  // CTA waits for its columns and fetches its right-hand sides
+  if (threadIdx.x == 0) {
+    constexpr unsigned kBytes = NRHS * 4 * NP * sizeof(double2);
+    lc_expect(&fac_bar, kBytes);
+    lc_copy(fac, fac_g + (size_t)l * NRHS * 4 * NP, kBytes, &fac_bar);
+  }
+  bool fac_pending = true;
   if (ready) {
     // column hand-off from the table analysis (swx_sht_set_done_signal): the
     // item's columns are complete when all their analysis items have counted
@@ -434,6 +476,11 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
       }
       PhiDiv pd[MPL];
       double2 z[MPL];
+      if (fac_pending) {  // first use of the table in this item
+        lc_bar_wait(&fac_bar, fac_phase);
+        fac_phase ^= 1u;
+        fac_pending = false;
+      }
       tree_pd_m<PPL, MPL, PR>(F, F + NP, F + 2 * NP, 0, LPM, bp, bd, pd);
       tree_z_m<PPL, MPL, PR>(F + 3 * NP, 0, LPM, bz, z);
 #pragma unroll
@@ -458,6 +505,10 @@ __global__ void __launch_bounds__(128, SWX_LG_MINB) rexi_lg_mm_kernel(
           for (int c = 0; c < 3; ++c) out[o + (size_t)c * ncoef] = v[c];
         }
     }
+  }
+  if (fac_pending) {  // an item without modes: never leave a copy in flight
+    lc_bar_wait(&fac_bar, fac_phase);
+    fac_phase ^= 1u;
   }
   }
   trace_mark(6);
@@ -623,35 +674,6 @@ __device__ __forceinline__ void l_fwd_c(const LPos<NRHS> &e, bool isz, double2 i
   }
 }
 
-// mbarrier / bulk-copy helpers of the cached chain kernel
-__device__ __forceinline__ unsigned lc_smem(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void lc_bar_init(uint64_t *bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(lc_smem(bar)) : "memory");
-}
-__device__ __forceinline__ void lc_bar_wait(uint64_t *bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "LC_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra LC_WAIT_%=;\n}\n" ::"r"(lc_smem(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void lc_expect(uint64_t *bar, unsigned bytes) {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(lc_smem(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void lc_copy(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          lc_smem(dst)),
-      "l"(src), "r"(bytes), "r"(lc_smem(bar))
-      : "memory");
-}
 #ifndef SWX_LRING
 #define SWX_LRING 2
 #endif
