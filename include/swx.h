@@ -317,6 +317,13 @@ int swx_solver_set_columns(swx_solver s, int m_begin, int m_end);
  * up to T255 - served by the cache-free partition kernel -, SWX_L_CACHE=0,
  * or more than half the free device memory).                               */
 size_t swx_solver_cache_bytes(swx_solver s);
+/* Geometry of the Coriolis group's partition kernel (truncations up to T255)
+ * for a column of n_rows = T + 1 - m chain rows: lanes per (pole, m, chain)
+ * system (a power of two <= 32) and rows per lane (even, <= 8), lanes x rows
+ * >= n_rows.  Host only (no device needed); SWX_ERR_CONFIG outside 1..256.
+ * The per-m work split the reference leaves to LAPACK's band LU
+ * (solvers.py:196-212).                                                     */
+int swx_l_partition_geometry(int n_rows, int *lanes, int *rows_per_lane);
 
 /* ---- host layout conversion (API edge) ------------------------------------
  * Dense (T+1)x(T+1) complex128 fields, C order (row l, column m) -- the

@@ -63,6 +63,7 @@ SIGNATURES = {
     "swx_sht_set_done_signal": (_I, [_P, _I, ctypes.POINTER(_P)]),
     "swx_sht_tendency_profile": (_I, [_P, _I, _P, _P, _P, _S, _P, _P]),
     "swx_fp64_fma_probe": (_I, [_P, _I, _I, _P]),
+    "swx_l_partition_geometry": (_I, [_I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "swx_host_pack": (_I, [_I, _I, _P, _P]),
     "swx_host_unpack": (_I, [_I, _I, _P, _P]),
     "swx_trace": (_I, [_I, _P, _I]),

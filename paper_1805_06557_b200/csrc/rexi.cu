@@ -1630,6 +1630,7 @@ extern "C" int swx_solver_destroy(swx_solver s) {
 }
 
 static bool l_use_part(swx_solver s);
+static int lpart_schedule(swx_solver s);
 
 extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
                                int n_poles, int *err_pole, int *err_index,
@@ -1707,6 +1708,12 @@ extern "C" int swx_solver_warm(swx_solver s, const swx_c128 *h_alphas,
       snprintf(buf, sizeof buf, "numerically singular band matrix for (m=%d, alpha=(%.17g%+.17gj))", m,
                h_alphas[p].re, h_alphas[p].im);
       return fail(SWX_ERR_SOLVER, buf);
+    }
+    // the partition kernel's item table: built here, not at the first launch
+    // (which may sit inside a stream capture)
+    if (l_use_part(s)) {
+      const int rc = lpart_schedule(s);
+      if (rc) return rc;
     }
     // pivot cache (32 B per pole x coefficient), built when it fits in half
     // of the free device memory; SWX_L_CACHE=0 keeps the recomputing kernel
@@ -1993,6 +2000,12 @@ static void lpart_geometry(int nl, int &W, int &q) {
       q = qq;
     }
   }
+}
+
+extern "C" int swx_l_partition_geometry(int n_rows, int *lanes, int *rows_per_lane) {
+  if (n_rows < 1 || n_rows > 32 * kLPartQ || !lanes || !rows_per_lane) return SWX_ERR_CONFIG;
+  lpart_geometry(n_rows, *lanes, *rows_per_lane);
+  return SWX_OK;
 }
 
 static int lpart_schedule(swx_solver s) {

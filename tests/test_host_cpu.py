@@ -212,3 +212,27 @@ def test_column_shard_bounds_c_matches_host_mirror(trunc):
         assert max(abs(n - ideal) for n in sizes) <= trunc + 1
     with pytest.raises(ConfigurationError):
         ColumnShard(cfg, 2, 2)
+
+
+def test_l_partition_geometry_covers_every_column():
+    """swx_l_partition_geometry (host code in the library): for every column
+    length of T <= 255 the lanes x rows tile covers the column with lanes a
+    power of two <= 32 and rows per lane even and <= 8; lanes never grow as the
+    column shrinks (the schedule groups columns of equal lane count) and the
+    padding stays below one row per lane plus the evenness slack."""
+    import ctypes
+
+    lib = _lib.load()
+    prev = 32
+    for n in range(256, 0, -1):
+        w, q = ctypes.c_int(0), ctypes.c_int(0)
+        assert lib.swx_l_partition_geometry(n, ctypes.byref(w), ctypes.byref(q)) == 0
+        w, q = w.value, q.value
+        assert w in (1, 2, 4, 8, 16, 32) and q in (2, 4, 6, 8)
+        assert w * q >= n
+        assert w * (q - 2) < n or q == 2          # no removable row pair
+        assert w <= prev
+        prev = w
+    w, q = ctypes.c_int(0), ctypes.c_int(0)
+    assert lib.swx_l_partition_geometry(257, ctypes.byref(w), ctypes.byref(q)) != 0
+    assert lib.swx_l_partition_geometry(0, ctypes.byref(w), ctypes.byref(q)) != 0
