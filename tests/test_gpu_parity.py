@@ -484,14 +484,20 @@ def test_column_sharded_tendency_bitwise(trunc, ks):
     g = osh.grid_for(trunc)
     st = ost.seeded_balanced_state(g)
     st[2] = ost.seeded_linear_state(trunc, 9)[2] * 1e-1
+    oracle = olay.pack(g.tendency_lc_n(st))  # swe.py:188-279 restated on the CPU
     st = to_device(olay.pack(st))
-    sub = to_device(pack(ost.seeded_linear_state(trunc, 6)))
+    sub_h = pack(ost.seeded_linear_state(trunc, 6))
+    sub = to_device(sub_h)
     plan = plan_for(SphereConfig.for_truncation(trunc))
     ref = plan.tendency_dev(3, st).cpu().numpy()
     ref_sub = plan.tendency_dev(3, st, sub=sub).cpu().numpy()
     for K in ks:
-        assert np.array_equal(_virtual_tendency(trunc, K, st), ref), K
-        assert np.array_equal(_virtual_tendency(trunc, K, st, sub), ref_sub), K
+        got = _virtual_tendency(trunc, K, st)
+        assert np.array_equal(got, ref), K
+        assert rel_linf(got, oracle) <= 1e-10, K            # the shards against the oracle itself
+        got = _virtual_tendency(trunc, K, st, sub)
+        assert np.array_equal(got, ref_sub), K
+        assert rel_linf(got, oracle - sub_h) <= 1e-10, K
 
 
 def test_column_sharded_etdrk_bitwise():
@@ -516,9 +522,19 @@ def test_column_sharded_etdrk_bitwise():
         run_lockstep((e.phases() for e in engines),
                      lambda items: virtual_exchange([t for t, _ in items], items[0][1]))
     want = ref.u.cpu().numpy()
+    # the same two steps by the CPU oracle (steppers.py:238-269 restated)
+    grid = osh.grid_for(trunc)
+    osets = {k: (np.asarray(sets[k].alphas), np.asarray(sets[k].betas)) for k in (0, 1, 2)}
+    model = orx.Model(trunc, 1e4 * G)
+    oref = ic
+    for _ in range(2):
+        oref = ost.etdrk2_step(model, grid, dt, osets, oref)
+    oref = olay.pack(oref)
     for e in engines:
         a, b = e.shard.slots()
-        assert np.array_equal(e.own().cpu().numpy(), want[:, a:b]), e.shard.rank
+        own = e.own().cpu().numpy()
+        assert np.array_equal(own, want[:, a:b]), e.shard.rank
+        assert rel_l2(own, oref[:, a:b]) <= 1e-9, e.shard.rank
 
 
 def test_lg_column_restricted_sum_bitwise():
