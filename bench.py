@@ -159,11 +159,14 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": val, "unit": "pole-solve*coeff/s", "cores": cores,
                          "kind": "port",
                          "sample": f"{len(times)} full steps of {w.name} (numpy/scipy oracle, "
-                                   f"{cores} host threads for BLAS)"},
+                                   f"{cores} host threads for BLAS)" + PORT_NOTE},
         "e2e": {"value": val, "unit": "pole-solve*coeff/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+PORT_NOTE = ("; kind 'port': the oracle restatement of swerexi, measured 1.1-1.2x slower than swerexi itself on 8 cores of the build container (VERDICT r1), so ratios against it are that much generous")
 
 
 def bench_config(w) -> dict:
@@ -795,7 +798,7 @@ def main():
             sec = (time.perf_counter() - t0) * w.n_poles / n_s
             sample = f"{n_s} of {w.n_poles} poles of {w.name}, scaled"
         cpu = {"value": units_per_step / sec, "unit": "pole-solve*coeff/s",
-               "cores": len(os.sched_getaffinity(0)), "kind": "port", "sample": sample}
+               "cores": len(os.sched_getaffinity(0)), "kind": "port", "sample": sample + PORT_NOTE}
 
     # kernels per step: counted from the captured step graph (ETD2RK); the linear
     # configs launch one fused pole-sum kernel (lg) or kernel + tree combine (l)
