@@ -1082,17 +1082,6 @@ __device__ __forceinline__ double2 tree_ld_n(const double2 *p, int stride, int n
     default: return p[0];
   }
 }
-// value of lane (own - s) / (own + s) inside the W-lane group, 0 outside it
-__device__ __forceinline__ double2 grp_up(double2 v, int s, int W, int j) {
-  const double x = __shfl_up_sync(0xffffffffu, v.x, s, W);
-  const double y = __shfl_up_sync(0xffffffffu, v.y, s, W);
-  return j >= s ? make_double2(x, y) : make_double2(0.0, 0.0);
-}
-__device__ __forceinline__ double2 grp_down(double2 v, int s, int W, int j) {
-  const double x = __shfl_down_sync(0xffffffffu, v.x, s, W);
-  const double y = __shfl_down_sync(0xffffffffu, v.y, s, W);
-  return j + s < W ? make_double2(x, y) : make_double2(0.0, 0.0);
-}
 // a - b*c
 __device__ __forceinline__ double2 cnfma(double2 b, double2 c, double2 a) {
   return make_double2(fma(-b.x, c.x, fma(b.y, c.y, a.x)), fma(-b.x, c.y, fma(-b.y, c.x, a.y)));
@@ -2012,7 +2001,6 @@ static int lpart_schedule(swx_solver s) {
   if (s->d_lpart) return SWX_OK;
   std::vector<int4> items;
   const int ncols = 2 * (s->trunc + 1);
-  int max_rows = 0;
   for (int col = 0; col < ncols;) {
     int W, q;
     lpart_geometry(s->trunc + 1 - (col >> 1), W, q);
@@ -2025,14 +2013,12 @@ static int lpart_schedule(swx_solver s) {
       ++n;
     }
     items.push_back(make_int4(col, n, W, q));  // q of the first (longest) column
-    max_rows = std::max(max_rows, W * q);
     col += n;
   }
   SWX_CUDA_TRY(cudaMalloc(&s->d_lpart, sizeof(int4) * items.size()));
   SWX_CUDA_TRY(cudaMemcpy(s->d_lpart, items.data(), sizeof(int4) * items.size(),
                           cudaMemcpyHostToDevice));
   s->lpart_ctas = (int)items.size();
-  s->lpart_max_rows = max_rows;
   s->h_lpart.assign(items.begin(), items.end());
   return SWX_OK;
 }

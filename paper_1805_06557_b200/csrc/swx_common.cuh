@@ -99,10 +99,9 @@ struct swx_solver_s {
   size_t linv_bytes = 0;
   int l_blocks_per_sm = 0;
   // l group, short columns: CTA items (first column 2m+chain, columns, W, q) of
-  // the partition kernel (rexi_l_part_kernel), built at the first launch
+  // the partition kernel (rexi_l_part_kernel), built by swx_solver_warm
   int4 *d_lpart = nullptr;
   int lpart_ctas = 0;
-  int lpart_max_rows = 0;  // largest W*q of an item
   std::vector<int4> h_lpart;
 };
 
