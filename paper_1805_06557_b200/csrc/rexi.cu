@@ -1036,24 +1036,28 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : SWX_LU_MI
 // (pole, m, chain); lane j holds the q consecutive rows j*q .. j*q+q-1 in
 // registers (q even, so a row's vorticity/divergence type is the same in every
 // lane and every branch on it is warp-uniform).
-//   1. downward sweep in the lane: rows become  x_i + c_i x_{i+1} + A_i x_L = D_i
+//   1. downward sweep in the lane: rows become  x_i + C_i x_{i+1} + A_i x_L = D_i
 //      (x_L = the previous lane's last unknown; the Thomas step of l_fwd plus
-//      the fill column A);
-//   2. upward sweep: rows i < q-1 become  x_i + A_i x_L + C_i x_R = D_i  with
-//      x_R = the lane's own last unknown;
+//      the fill column A), kept in registers;
+//   2. upward sweep, carried as one running row: the lane's first row becomes
+//      x_0 + fA x_L + fC x_R = fD  with x_R = the lane's own last unknown;
 //   3. the last rows of the W lanes, with the next lane's first row substituted,
 //      form a W x W tridiagonal system in the X_j = x_{j,q-1}: parallel cyclic
-//      reduction over the group with width-W shuffles, log2 W steps;
-//   4. x_i = D_i - A_i X_{j-1} - C_i X_j, then the beta weights and phi'.
+//      reduction over the group with width-W shuffles, log2 W steps, rows
+//      normalised every step (reciprocals by rcp.approx + two Newton steps);
+//   4. back substitution from the stored rows, x_i = D_i - C_i x_{i+1} -
+//      A_i X_{j-1}, then the beta weights and phi'.
 // No pivot cache, no second pass, no scratch: every (pole, m, chain) is W
 // threads of parallel work instead of one serial thread, which is what a
 // T128 x 256-pole sum lacks (1032 warps of serial chains on 148 SMs).
 // A CTA is 256 threads: min(32 W, 256) threads per column slot, 8 / W columns
-// per CTA when W < 8; it covers one 32-pole block in 32 W / 256 passes.  The
-// beta-weighted solutions go through a shared-memory stage ([pole][i*W + j],
-// conflict-free for writers and readers) and are summed over the poles as the
-// perfect binary tree of tree_sum, so `part` holds the same aligned 32-pole
-// subtrees as rexi_l_kernel's.
+// per CTA when W < 8; it covers one 32-pole block in 32 W / 256 passes, two
+// consecutive passes of a thread taking a leaf pair of the pole tree.  Row data
+// and the beta-weighted solutions live in odd-strided per-lane blocks of shared
+// memory (conflict-free, compile-time offsets: q is a template parameter of
+// the body); the solutions are summed over the poles as the perfect binary
+// tree of tree_sum, so `part` holds the same aligned 32-pole subtrees as
+// rexi_l_kernel's.
 // =====================================================================
 #ifndef SWX_LPART_Q
 #define SWX_LPART_Q 8
