@@ -560,6 +560,13 @@ __global__ void products_kernel(double *g, size_t npts) {
 constexpr int kAS = 12;  // row stride (doubles) of prepared rows: conflict-free B fragments
 constexpr int kAG = 8;   // row stride of the prepared rows of the table path (global)
 
+// two complex values as one 256-bit store (sm_100: STG.256; dst 32-byte aligned)
+__device__ __forceinline__ void st256(double *dst, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(a.x), "d"(a.y), "d"(b.x),
+               "d"(b.y)
+               : "memory");
+}
+
 // one prepared row (4 complex = 64 B, 16-byte aligned): 4 vector stores
 __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
   double2 *d2 = reinterpret_cast<double2 *>(dst);
@@ -571,10 +578,15 @@ __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
 // stored rotated by two complex slots (column c -> c ^ 4 in doubles), which
 // makes the analysis' B-fragment reads from shared memory conflict-free
 __device__ __forceinline__ void put_row_t(double *dst, const double2 *v, int nv, int i) {
-  double2 *d2 = reinterpret_cast<double2 *>(dst);
-  const int rot = (i & 2) ? 2 : 0;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) d2[(c + rot) & 3] = c < nv ? v[c] : make_double2(0.0, 0.0);
+  // the 64-byte row as two full 32-byte sectors (two 256-bit stores) instead of
+  // four 16-byte partial-sector writes: the rows of a thread lie 53 KB apart, so
+  // every store is its own L2 transaction
+  const double2 zero = make_double2(0.0, 0.0);
+  const double2 v0 = v[0], v1 = nv > 1 ? v[1] : zero, v2 = nv > 2 ? v[2] : zero,
+                v3 = nv > 3 ? v[3] : zero;
+  const bool rot = (i & 2) != 0;  // rows of pairs with bit 1 set: halves swapped
+  st256(dst, rot ? v2 : v0, rot ? v3 : v1);
+  st256(dst + 4, rot ? v0 : v2, rot ? v1 : v3);
 }
 
 // fold one latitude pair of the tendency inputs into even/odd parts of the
