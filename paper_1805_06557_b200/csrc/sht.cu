@@ -134,8 +134,9 @@ struct SynthArgs {
   int nfreq;
   // zpack: the fused grid stage's input format instead of C2R rows: per
   // latitude pair i, field f (u, v, vort, phi'), bins m = 0..T:
-  //   c2r[((i * 4 + f) * 2 + 0) * (T+1) + m] = X_n(m) + i X_s(m)
-  //   c2r[((i * 4 + f) * 2 + 1) * (T+1) + m] = conj(X_n(m)) + i conj(X_s(m))
+  //   c2r[(i * 4 + f) * 2 (T+1) + 2 m + 0] = X_n(m) + i X_s(m)
+  //   c2r[(i * 4 + f) * 2 (T+1) + 2 m + 1] = conj(X_n(m)) + i conj(X_s(m))
+  // (the two values of a column adjacent: one 256-bit store per field)
   // (X_s = X_n on the equator node), i.e. the packed row z = north + i south
   // at bin m and at bin N - m.
   int zpack = 0;
@@ -216,10 +217,17 @@ __device__ __forceinline__ void bulk_g2s_v(void *dst, const void *src, unsigned 
       : "memory");
 }
 
+// two complex values as one 256-bit store (sm_100: STG.256; dst 32-byte aligned)
+__device__ __forceinline__ void st256(double *dst, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(a.x), "d"(a.y), "d"(b.x),
+               "d"(b.y)
+               : "memory");
+}
+
 // bin k of the packed complex row z = north + i south of field f (zero above T)
 __device__ __forceinline__ double2 zrow_bin(const double2 *zf, int k, int T, int N) {
   const bool lo = k <= T, hi = !lo && N - k <= T;
-  const double2 v = zf[(hi ? (T + 1) : 0) + (lo ? k : (hi ? N - k : 0))];
+  const double2 v = zf[2 * (lo ? k : (hi ? N - k : 0)) + (hi ? 1 : 0)];
   return (lo || hi) ? v : make_double2(0.0, 0.0);
 }
 
@@ -299,12 +307,13 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
     if (PEER)
       zb = reinterpret_cast<double2 *>(p.pm->base[peer_owner(p.pm->pbnd, p.pm->n, i)] +
                                        p.pm->off_c2r);
-    double2 *z = zb + (size_t)i * 8 * T1 + m;
+    double2 *z = zb + (size_t)i * 8 * T1 + 2 * m;
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const double2 n = X[0][f], s = X[1][f];
-      z[(f * 2 + 0) * T1] = make_double2(n.x - s.y, n.y + s.x);   // X_n + i X_s
-      z[(f * 2 + 1) * T1] = make_double2(n.x + s.y, -n.y + s.x);  // conj(X_n) + i conj(X_s)
+      // X_n + i X_s and conj(X_n) + i conj(X_s), one full 32-byte sector
+      st256(reinterpret_cast<double *>(z + (size_t)f * 2 * T1), make_double2(n.x - s.y, n.y + s.x),
+            make_double2(n.x + s.y, -n.y + s.x));
     }
   }
 }
@@ -559,13 +568,6 @@ __global__ void products_kernel(double *g, size_t npts) {
 // ---------------------------------------------------------------------
 constexpr int kAS = 12;  // row stride (doubles) of prepared rows: conflict-free B fragments
 constexpr int kAG = 8;   // row stride of the prepared rows of the table path (global)
-
-// two complex values as one 256-bit store (sm_100: STG.256; dst 32-byte aligned)
-__device__ __forceinline__ void st256(double *dst, double2 a, double2 b) {
-  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(a.x), "d"(a.y), "d"(b.x),
-               "d"(b.y)
-               : "memory");
-}
 
 // one prepared row (4 complex = 64 B, 16-byte aligned): 4 vector stores
 __device__ __forceinline__ void put_row(double *dst, const double2 *v, int nv) {
@@ -3514,9 +3516,9 @@ static void shard_blocks(swx_sht p, const ShtWs &w, const swx_shard *sh, int ex,
     const int a = std::min(sh->p_bounds[to], p->nh), b = std::min(sh->p_bounds[to + 1], p->nh);
     if (nm <= 0 || b <= a) return;
     if (atoms & SWX_TEND_N)
-      out.push_back({(size_t)((const char *)(w.c2r + (size_t)a * 8 * T1 + m0) - base),
-                     (size_t)T1 * sizeof(double2), (size_t)nm * sizeof(double2),
-                     (size_t)(b - a) * 8});
+      out.push_back({(size_t)((const char *)(w.c2r + (size_t)a * 8 * T1 + 2 * m0) - base),
+                     (size_t)2 * T1 * sizeof(double2), (size_t)2 * nm * sizeof(double2),
+                     (size_t)(b - a) * 4});
     if (atoms & SWX_TEND_LC)
       for (int term = 0; term < 2; ++term) {
         const double2 *lt = w.lc + (size_t)term * p->nlat * p->nm;
