@@ -297,8 +297,8 @@ __device__ __forceinline__ void state_rows(const ShtView &p, const SynthArgs &a,
       if (PEER)  // the pair's owner's workspace (peer store)
         lb = reinterpret_cast<double2 *>(p.pm->base[peer_owner(p.pm->pbnd, p.pm->n, i)] +
                                          p.pm->off_lc);
-      lb[(size_t)j * p.nm + m] = l1;
-      lb[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m] = l2;
+      // the two terms of (latitude j, column m) adjacent: one 256-bit store
+      st256(reinterpret_cast<double *>(lb + 2 * ((size_t)j * p.nm + m)), l1, l2);
     }
   }
   if (a.zpack) {
@@ -676,8 +676,8 @@ __device__ __forceinline__ void tend_row(const ShtView &p, const double2 *Q, con
     }
     L1[hemi] = L2[hemi] = make_double2(0.0, 0.0);
     if (atoms & SWX_TEND_LC) {
-      L1[hemi] = lc[(size_t)j * p.nm + m];
-      L2[hemi] = lc[(size_t)p.nlat * p.nm + (size_t)j * p.nm + m];
+      L1[hemi] = lc[2 * ((size_t)j * p.nm + m)];
+      L2[hemi] = lc[2 * ((size_t)j * p.nm + m) + 1];
     }
   }
   tend_fold<HCOS>(p, F, L1, L2, m, pair_k(p, i), ev, od);
@@ -871,7 +871,7 @@ __global__ void __launch_bounds__(kGridT) grid_tend_kernel(ShtView p, const doub
   grid_fold(
       p, i, atoms, nl, A, pk, [&](int f, int k) { return f < 4 ? R4[(size_t)f * N + k] : R1[k]; },
       [&](int term, int hemi, int m) {
-        return lc[(size_t)term * p.nlat * p.nm + (size_t)(hemi ? js0 : jn0) * p.nm + m];
+        return lc[2 * ((size_t)(hemi ? js0 : jn0) * p.nm + m) + term];
       });
 }
 
@@ -927,7 +927,7 @@ __global__ void __launch_bounds__(SqCfg<R1, R2>::NT, 2) grid_sq_kernel(ShtView p
     for (int t = threadIdx.x; t < 4 * (T + 1); t += blockDim.x) {
       const int q = t / (T + 1), m = t - q * (T + 1);  // q = term * 2 + hemi
       const int j = (q & 1) ? js : jn;
-      cp16(LCs + q * C::LCM + m, lc + (size_t)(q >> 1) * p.nlat * p.nm + (size_t)j * p.nm + m);
+      cp16(LCs + q * C::LCM + m, lc + 2 * ((size_t)j * p.nm + m) + (q >> 1));
     }
   cp_commit();
   if (nl) {
@@ -1057,7 +1057,7 @@ __global__ void __launch_bounds__(SqCfg<R, R>::NT, 2) grid_sq1_kernel(ShtView p,
     for (int t = threadIdx.x; t < 4 * (T + 1); t += blockDim.x) {
       const int q = t / (T + 1), m = t - q * (T + 1);  // q = term * 2 + hemi
       const int j = (q & 1) ? js : jn;
-      cp16(LCs + q * C::LCM + m, lc + (size_t)(q >> 1) * p.nlat * p.nm + (size_t)j * p.nm + m);
+      cp16(LCs + q * C::LCM + m, lc + 2 * ((size_t)j * p.nm + m) + (q >> 1));
     }
   cp_commit();
   if (nl) {
@@ -3519,16 +3519,15 @@ static void shard_blocks(swx_sht p, const ShtWs &w, const swx_shard *sh, int ex,
       out.push_back({(size_t)((const char *)(w.c2r + (size_t)a * 8 * T1 + 2 * m0) - base),
                      (size_t)2 * T1 * sizeof(double2), (size_t)2 * nm * sizeof(double2),
                      (size_t)(b - a) * 4});
-    if (atoms & SWX_TEND_LC)
-      for (int term = 0; term < 2; ++term) {
-        const double2 *lt = w.lc + (size_t)term * p->nlat * p->nm;
-        // south rows js = i, north rows jn = nlat - 1 - i (both contiguous)
-        const int j0[2] = {a, p->nlat - b};
-        for (int h = 0; h < 2; ++h)
-          out.push_back({(size_t)((const char *)(lt + (size_t)j0[h] * p->nm + m0) - base),
-                         (size_t)p->nm * sizeof(double2), (size_t)nm * sizeof(double2),
-                         (size_t)(b - a)});
-      }
+    if (atoms & SWX_TEND_LC) {
+      // both terms of a (latitude, column) are adjacent; south rows js = i, north
+      // rows jn = nlat - 1 - i (both contiguous)
+      const int j0[2] = {a, p->nlat - b};
+      for (int h = 0; h < 2; ++h)
+        out.push_back({(size_t)((const char *)(w.lc + 2 * ((size_t)j0[h] * p->nm + m0)) - base),
+                       (size_t)2 * p->nm * sizeof(double2), (size_t)2 * nm * sizeof(double2),
+                       (size_t)(b - a)});
+    }
   } else {  // prepared rows: columns of `to`, pairs of `from`
     const int m0 = sh->m_bounds[to], nm = sh->m_bounds[to + 1] - m0;
     const int a = sh->p_bounds[from], b = sh->p_bounds[from + 1];
