@@ -1066,6 +1066,7 @@ __global__ void __launch_bounds__(kLWarps * 32, CACHED ? SWX_LC_MINB : SWX_LU_MI
 #define SWX_LPART_MINB 2
 #endif
 constexpr int kLPartQ = SWX_LPART_Q;  // rows per lane at most (even)
+constexpr double kLPartTol2 = 5.6e-37;  // (2^-60)^2 with a margin: decoupling threshold of the PCR
 static_assert(kLPartQ % 2 == 0 && kLPartQ >= 2, "rows per lane");
 
 template <int N>
@@ -1268,7 +1269,20 @@ __device__ __forceinline__ void lpart_body(
         rv[r] = cnfma(cL, nD, D[r][QV - 1]);
       }
     }
+    const unsigned gmask = W == 32 ? 0xffffffffu : ((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1));
     for (int s = 1; s < W; s <<= 1) {
+      // a system whose couplings have all fallen below 2^-60 of the diagonal has
+      // decoupled (the dropped terms are far below one ulp of its solution): its
+      // couplings become exact zeros, after which further steps leave it bitwise
+      // unchanged, so the decision is per system -- independent of which systems
+      // share the warp -- and the warp leaves when all of its systems are done.
+      // Away from the resonant poles |C| ~ 0.02 per row, so one step usually
+      // suffices instead of log2 W.
+      const bool sig = ra.x * ra.x + ra.y * ra.y + rc.x * rc.x + rc.y * rc.y >
+                       kLPartTol2 * (rb.x * rb.x + rb.y * rb.y);
+      const unsigned bal = __ballot_sync(0xffffffffu, sig);
+      if (bal == 0) break;
+      if ((bal & gmask) == 0) ra = rc = make_double2(0.0, 0.0);
       const double2 inv = crecip_nr(rb);
       const double2 an = cmul(ra, inv), cn = cmul(rc, inv);
       const double2 an_m = make_double2(__shfl_up_sync(0xffffffffu, an.x, s, W),
